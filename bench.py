@@ -1,0 +1,341 @@
+"""Benchmark of the butterfly apply hot path on B200 (BASELINE.json metric:
+complex samples/s = N * nRHS / t_apply, plus % of HBM roofline).
+
+Default workload: BASELINE config 2 — FIO geometry N=2^20, r=16, leaf 16
+(L=16), complex128, 1 RHS — the single-GPU config the north star's ">= 60% of
+HBM roofline at N >= 2^20" target is quoted on. Factors are a seeded
+synthetic chain at the reference's exact shapes (full CPU construction of
+config 2 takes ~10-19 h in the reference).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config cfg2|cfg1|cfg0] [--dtype c128|c64] [--rhs k]
+
+--impl reference times the reference algorithm's CPU path (the NumPy oracle
+port in oracle/, the reference itself being pure Python that cannot travel
+to the GPU box) on the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (kernel, n, r, leaf, default rhs)
+    "cfg0": ("fio", 1 << 10, 12, 8, 1),
+    "cfg1": ("dftp", 1 << 16, 8, 16, 64),
+    "cfg2": ("fio", 1 << 20, 16, 16, 1),
+}
+METRIC = "BF apply complex-samples/s (N*nRHS/s)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
+    ap.add_argument("--rhs", type=int, default=0, help="right-hand sides (default: the config's)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def algorithmic(f, k, esz):
+    """Compulsory bytes/flops of one apply:
+    bytes = esz*(nnz - nnz_M) + esz/2*nnz_M + 2*esz*N*k ; flops = 8k(nnz - nnz_M) + 2k nnz_M."""
+    rep = f.nnz_report()
+    nnz, nm = rep.total, rep.middle
+    return esz * (nnz - nm) + esz // 2 * nm + 2 * esz * f.n * k, 8 * k * (nnz - nm) + 2 * k * nm
+
+
+def launch_bytes(f, k, esz):
+    """Algorithmic bytes of each launch of the forward chain, in launch order:
+    factor bytes + input vector + output vector (M is fused into the last H* launch)."""
+    p, r = f.partition, f.rank
+    nb, n0, _ = f.u_outer.blocks.shape
+    out = [("V*", esz * nb * n0 * r + esz * k * (nb * n0 + nb * r))]
+    for tf in reversed(f.h_chain):
+        rows, cols = tf.shape
+        extra = (esz // 2) * f.middle.nnz if tf.level == p.half else 0
+        out.append((f"H{tf.level}*", esz * tf.nnz + esz * k * (rows + cols) + extra))
+    for tf in f.g_chain:
+        rows, cols = tf.shape
+        out.append((f"G{tf.level}", esz * tf.nnz + esz * k * (rows + cols)))
+    out.append(("U", esz * nb * n0 * r + esz * k * (nb * n0 + nb * r)))
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc, self.path = index, None, None
+
+    def start(self):
+        try:
+            self.path = f"/tmp/bf_clocks_{os.getpid()}.csv"
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6 and parts[0].isdigit():
+                rows.append(parts)
+        if not rows:
+            return None
+        sm = [int(r[0]) for r in rows]
+        busy = [s for s in sm if s > 600] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(int(r[1]) for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def rhs_input(n, k, seed=0):
+    """g = complex_normal with SeedSequence(seed, spawn_key=(4, 0)) as the reference bench (bench.py:208-213)."""
+    rng = np.random.default_rng(np.random.SeedSequence(seed, spawn_key=(4, 0)))
+    g = rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k))
+    return g
+
+
+def oracle_chain(fh):
+    from oracle import chain as ochain
+    return ochain.Chain(fh.n, fh.partition.levels, fh.rank, fh.u_outer.blocks,
+                        [(t.level, t.blocks) for t in fh.g_chain], fh.middle.weights,
+                        [(t.level, t.blocks) for t in fh.h_chain], fh.v_outer.blocks)
+
+
+def time_cpu(fh, g, budget_s=20.0, max_steps=5):
+    """The reference algorithm on host cores: oracle port of ButterflyFactors.apply (median of runs)."""
+    from oracle import chain as ochain
+    oc = oracle_chain(fh)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_steps and (not times or time.perf_counter() - t_start < budget_s):
+        t0 = time.perf_counter()
+        ochain.apply(oc, g)
+        times.append(time.perf_counter() - t0)
+    return statistics.median(times), len(times)
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (NumPy oracle port) on host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    kern, n, r, leaf, k0 = CONFIGS[args.config]
+    k = args.rhs or k0
+    from paper_1502_01379_b200.partition import make_partition
+    from paper_1502_01379_b200.synthetic import synthetic_chain
+    p = make_partition(n, leaf)
+    fh = synthetic_chain(p, r, seed=20240801)
+    g = rhs_input(n, k)
+    from oracle import chain as ochain
+    oc = oracle_chain(fh)
+    for _ in range(min(args.warmup, 1)):
+        ochain.apply(oc, g)
+    times = []
+    budget = 150.0
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ochain.apply(oc, g)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > budget:
+            break
+    t = statistics.median(times)
+    val = n * k / t
+    cores = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    sample = f"{len(times)} full applies of {args.config} (N={n}, r={r}, k={k}), median"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "samples/s", "n_gpus": args.gpus,
+        "steps": len(times), "warmup": min(args.warmup, 1), "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"{args.config} FIO N={n} r={r} leaf={leaf} k={k} c128 (oracle port)",
+                   "n": n, "rank": r, "rhs": k},
+        "cpu_baseline": {"value": val, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
+        os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1502_01379_b200 as bf
+    from paper_1502_01379_b200 import _lib
+    from paper_1502_01379_b200.synthetic import synthetic_chain, to_host
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    kern, n, r, leaf, k0 = CONFIGS[args.config]
+    k = args.rhs or k0
+    esz = 16 if args.dtype == "c128" else 8
+    p = bf.make_partition(n, leaf)
+    f = synthetic_chain(p, r, seed=20240801 + rank, device="cuda")
+    plan = f.plan(args.dtype)
+    lib = _lib.load()
+    tdt = torch.complex128 if args.dtype == "c128" else torch.complex64
+    g_host = rhs_input(n, k)
+    g = torch.from_numpy(g_host).to("cuda").to(tdt)
+    out = torch.empty_like(g)
+    wsb = plan.workspace_bytes(k)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    steps, warm = args.steps, max(args.warmup, 3)
+
+    def apply_once(timer=None):
+        if timer is None:
+            _lib.check(lib.bf_apply(plan._h, ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(out.data_ptr()), k, 0,
+                                    ctypes.c_void_p(ws.data_ptr()), wsb, sp))
+        else:
+            _lib.check(lib.bf_apply_timed(plan._h, ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(out.data_ptr()), k,
+                                          0, ctypes.c_void_p(ws.data_ptr()), wsb, sp, timer))
+
+    for _ in range(warm):
+        apply_once()
+    torch.cuda.synchronize()
+
+    nlaunch = 2 + 2 * len(f.g_chain)
+    timer = ctypes.c_void_p()
+    _lib.check(lib.bf_timer_create(ctypes.byref(timer), steps, nlaunch))
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        apply_once(timer)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / steps
+    launch_ms = (ctypes.c_float * (steps * nlaunch))()
+    ns, nl = ctypes.c_uint32(), ctypes.c_uint32()
+    _lib.check(lib.bf_timer_read(timer, launch_ms, ctypes.byref(ns), ctypes.byref(nl)))
+    lib.bf_timer_destroy(timer)
+    per_launch = np.array(launch_ms[:]).reshape(steps, nl.value).mean(axis=0)
+    lb = launch_bytes(f, k, esz)
+    alg_bytes, alg_flops = algorithmic(f, k, esz)
+    peaks = {}
+    pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk_path):
+        peaks = json.load(open(pk_path))
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    # dominant kernel: the transfer-level launches (2*(L-h) of the 2+2(L-h) launches)
+    tr = [(name, b, t) for (name, b), t in zip(lb, per_launch) if name[0] in "GH"]
+    tr_bytes = sum(b for _, b, _ in tr) / len(tr)
+    tr_ms = sum(t for _, _, t in tr) / len(tr)
+    share = sum(t for _, _, t in tr) / max(per_launch.sum(), 1e-9)
+
+    # end to end through the public API with pinned host buffers
+    g_pin = torch.empty((n, k), dtype=tdt, pin_memory=True)
+    g_pin.copy_(torch.from_numpy(g_host).to(tdt))
+    o_pin = torch.empty((n, k), dtype=tdt, pin_memory=True)
+    g_np, o_np = g_pin.numpy(), o_pin.numpy()
+    for _ in range(2):
+        plan.apply(g_np, out=o_np)
+    e2e_steps = max(3, min(steps, 10))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        plan.apply(g_np, out=o_np)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
+        fh = to_host(f)
+        cpu_k = min(k, 16)
+        t_cpu, nrun = time_cpu(fh, g_host[:, :cpu_k].astype(np.complex128))
+        cpu = {"value": n * cpu_k / t_cpu, "unit": "samples/s", "cores": int(os.environ["OPENBLAS_NUM_THREADS"]),
+               "kind": "port",
+               "sample": f"oracle port of ButterflyFactors.apply on the identical factors, k={cpu_k}, "
+                         f"median of {nrun} applies ({t_cpu:.2f} s each); the path is effectively single-core"}
+        del fh
+
+    if rank == 0:
+        total = n * k * world
+        rec = {
+            "metric": METRIC, "value": total / (ms_step / 1e3), "unit": "samples/s", "n_gpus": world,
+            "steps": steps, "warmup": warm, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": f"{args.config} {kern.upper()} N={n} r={r} leaf={leaf} (L={p.levels}) k={k} "
+                                   f"{args.dtype}, synthetic seeded factors",
+                       "n": n, "rank": r, "levels": p.levels, "rhs": k, "parallelism": f"replicas{world}",
+                       "l2": "inputs larger than L2: each step streams "
+                             f"{alg_bytes / 1e9:.2f} GB of factors (L2 126 MB)"},
+            "roofline": {"bound": "hbm", "achieved": tr_bytes / (tr_ms / 1e3) / 1e9, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": tr_bytes / (tr_ms / 1e3) / 1e9 / hbm_peak, "traffic": None,
+                         "kernel": "level_kernel (transfer levels G/H)", "kernel_share_of_step": share,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+            "chain_roofline": {"algorithmic_bytes": alg_bytes, "algorithmic_flops": alg_flops,
+                               "achieved_gbs": alg_bytes / (ms_step / 1e3) / 1e9,
+                               "frac": alg_bytes / (ms_step / 1e3) / 1e9 / hbm_peak},
+            "per_launch_ms": {name: round(float(t), 5) for (name, _), t in zip(lb, per_launch)},
+            "e2e": {"value": total / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": n * k * esz,
+                    "d2h_bytes_per_step": n * k * esz, "ms_per_step": e2e_s * 1e3},
+            "gpu_launches": nlaunch * steps,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(rec))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,169 @@
+"""Generate tests/golden/*.npz by running the REFERENCE implementation itself.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden.py
+
+The fixtures pin both the CPU oracle (tests/test_oracle_golden.py) and the
+CUDA path (tests/test_apply_gpu.py, tests/test_construct_gpu.py) to the
+reference's own outputs on seeded inputs. Nothing at test time reads
+/root/reference; only this script does.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
+
+
+def _ref():
+    sys.path.insert(0, REF)
+    import butterfly  # noqa: F401  (the reference package)
+    return butterfly
+
+
+class DftPlus:
+    """Config-1 entry oracle exp(+2 pi i jk/n) handed to the reference factorize."""
+
+    def __init__(self, n):
+        self.n, self.shape = n, (n, n)
+
+    def block(self, rows, cols):
+        j = np.asarray(rows, dtype=np.int64)[:, None]
+        k = np.asarray(cols, dtype=np.int64)[None, :]
+        return np.exp(2j * np.pi * (((j * k) % self.n).astype(np.float64) / self.n))
+
+
+def _chain_arrays(f, prefix=""):
+    d = {prefix + "n": f.n, prefix + "levels": f.partition.levels, prefix + "rank": f.rank,
+         prefix + "u_leaf": f.u_outer.blocks, prefix + "v_leaf": f.v_outer.blocks,
+         prefix + "weights": f.middle.weights,
+         prefix + "g_lvls": np.array([tf.level for tf in f.g_chain]),
+         prefix + "h_lvls": np.array([tf.level for tf in f.h_chain])}
+    for tf in f.g_chain:
+        d[f"{prefix}g_{tf.level}"] = tf.blocks
+    for tf in f.h_chain:
+        d[f"{prefix}h_{tf.level}"] = tf.blocks
+    return d
+
+
+def gen_apply(bf, name, oracle, n, leaf, r, seed, k):
+    p = bf.make_partition(n, leaf)
+    f = bf.factorize(oracle, p, r, seed=seed)
+    rng = np.random.default_rng(np.random.SeedSequence(seed, spawn_key=(4, 0)))
+    g = bf.lowrank.complex_normal(rng, (n, k))
+    d = _chain_arrays(f)
+    d.update(g=g, fwd=f.apply(g), adj=f.apply_adjoint(g), fwd1=f.apply(g[:, 0]))
+    # eps_a as the reference bench computes it (bench.py:90-97, 208-211)
+    eps_rng = np.random.SeedSequence(seed, spawn_key=(4, 0))
+    d["eps_a"] = bf.bench.estimate_eps_a(f, bf.bench.RowSampledReference(oracle), 256, eps_rng)
+    np.savez_compressed(os.path.join(OUT, name), **d)
+    print(name, "levels", p.levels, "nnz", f.nnz_report().total, "eps_a", d["eps_a"])
+
+
+def gen_construct(bf, name, oracle, n, leaf, r, seed, blocks):
+    """Full factorize output plus per-block stage traces of the middle level."""
+    from butterfly.construct import _sample_block  # reference internals, traced below
+    p = bf.make_partition(n, leaf)
+    f = bf.factorize(oracle, p, r, seed=seed)
+    rng = np.random.default_rng(np.random.SeedSequence(seed, spawn_key=(4, 0)))
+    g = bf.lowrank.complex_normal(rng, (n, 2))
+    d = {"n": n, "levels": p.levels, "rank": r, "seed": seed, "g": g,
+         "fwd": f.apply(g), "adj": f.apply_adjoint(g), "weights": f.middle.weights}
+    if n <= 128:   # small enough to keep every factor and the middle-level triple
+        d.update(_chain_arrays(f))
+        u_h, mid, v_h = bf.middle_factorization_sampling(oracle, p, r, seed=seed)
+        d.update(u_h=u_h.blocks, v_h=v_h.blocks, w_h=mid.weights)
+    for (i, j) in blocks:
+        apx = _sample_block(oracle, p, r, bf.lowrank.DEFAULT_PARAMS, seed, i, j)
+        d[f"blk_{i}_{j}_u0"], d[f"blk_{i}_{j}_s0"], d[f"blk_{i}_{j}_v0"] = apx.u0, apx.sigma0, apx.v0
+    np.savez_compressed(os.path.join(OUT, name), **d)
+    print(name, "levels", p.levels)
+
+
+def gen_pivots(bf):
+    rng = np.random.default_rng(20240801)
+    d = {}
+    cases = []
+    a = rng.standard_normal((12, 40)) + 1j * rng.standard_normal((12, 40))
+    cases.append(("gauss", a, 8, 0.0))
+    b = np.repeat(a[:, :5], 4, axis=1)               # exact duplicate columns: tie rule
+    cases.append(("dups", b, 5, 0.0))
+    c = np.outer(a[:, 0], a[0, :]) + 1e-13 * a       # rank-1 plus noise: early stop with rel_tol
+    cases.append(("rank1", c, 6, 1e-11))
+    z = np.zeros((6, 9), dtype=complex)
+    cases.append(("zero", z, 3, 0.0))
+    ker = bf.FioKernel(4096)
+    e = ker.block(np.arange(0, 4096, 97)[:48], np.arange(1024, 2048))
+    cases.append(("fio", e, 16, 0.0))
+    for tag, mat, k, tol in cases:
+        d[f"{tag}_a"] = mat
+        d[f"{tag}_k"] = k
+        d[f"{tag}_tol"] = tol
+        d[f"{tag}_piv"] = np.array(bf.lowrank.select_pivot_columns(mat, k, tol), dtype=np.int64)
+    np.savez_compressed(os.path.join(OUT, "pivots.npz"), **d)
+    print("pivots.npz")
+
+
+def gen_entries(bf):
+    rng = np.random.default_rng(7)
+    d = {}
+    for n in (1024, 1 << 16, 1 << 20, 1 << 24):
+        rows = np.sort(rng.choice(n, size=64, replace=False))
+        cols = np.sort(rng.choice(n, size=64, replace=False))
+        d[f"fio_{n}_rows"], d[f"fio_{n}_cols"] = rows, cols
+        d[f"fio_{n}"] = bf.FioKernel(n).block(rows, cols)
+    d["fio_hand"] = np.array([bf.fio_entry(4, 0, 2), bf.fio_entry(4, 0, 0)])
+    n = 1 << 16
+    rows = np.sort(rng.choice(n, size=64, replace=False))
+    cols = np.sort(rng.choice(n, size=64, replace=False))
+    d["dftp_rows"], d["dftp_cols"], d["dftp"] = rows, cols, DftPlus(n).block(rows, cols)
+    np.savez_compressed(os.path.join(OUT, "entries.npz"), **d)
+    print("entries.npz")
+
+
+def gen_geometry(bf):
+    from butterfly.construct import _level_geometry
+    d = {}
+    for n, leaf in ((1024, 8), (1 << 16, 16), (1 << 20, 16), (256, 0.25), (64, 1), (1024, 1), (128, 0.25)):
+        p = bf.make_partition(n, leaf)
+        tag = f"{n}_{leaf}"
+        d[f"levels_{tag}"] = p.levels
+        ranges = []
+        for lvl in range(p.levels + 1):
+            for i in range(min(2 ** lvl, 4096)):
+                rg = p.node_range(lvl, i)
+                ranges.append((lvl, i, rg.start, rg.stop))
+        d[f"ranges_{tag}"] = np.array(ranges, dtype=np.int64)
+        shapes, leaf_shape = _level_geometry(p, 4)
+        d[f"shapes_{tag}"] = np.array([(lvl, int(sp), *(list(s) + [0] * (5 - len(s))))
+                                      for lvl, sp, s in shapes], dtype=np.int64)
+        d[f"leaf_{tag}"] = np.array(leaf_shape, dtype=np.int64)
+    np.savez_compressed(os.path.join(OUT, "geometry.npz"), **d)
+    print("geometry.npz")
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    bf = _ref()
+    gen_geometry(bf)
+    gen_entries(bf)
+    gen_pivots(bf)
+    gen_apply(bf, "apply_fio_n256_r8_leaf025.npz", bf.FioKernel(256), 256, 0.25, 8, 1, 3)
+    gen_apply(bf, "apply_cfg0_fio_n1024_r12_leaf8.npz", bf.FioKernel(1024), 1024, 8, 12, 0, 1)
+    gen_apply(bf, "apply_dftp_n1024_r8_leaf16.npz", DftPlus(1024), 1024, 16, 8, 0, 4)
+    gen_construct(bf, "construct_fio_n128_r4_leaf025.npz", bf.FioKernel(128), 128, 0.25, 4, 9,
+                  [(0, 0), (3, 5), (7, 7)])
+    gen_construct(bf, "construct_fio_n1024_r12_leaf8.npz", bf.FioKernel(1024), 1024, 8, 12, 0,
+                  [(0, 0), (2, 5), (7, 3)])
+    gen_construct(bf, "construct_fio_n1024_r8_leaf1.npz", bf.FioKernel(1024), 1024, 1, 8, 3,
+                  [(0, 0), (17, 30)])
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,169 @@
+// apply.cu — the butterfly apply chain on B200: level launches, the middle
+// factor, and the chain driver behind bf_apply / bf_apply_factor.
+//
+// Reference: ButterflyFactors._chain (pkg/src/butterfly/factors.py:217-237)
+//   forward:  V^L*  -> H^{L-1}* .. H^{h}*  -> M -> G^{h} .. G^{L-1} -> U^L
+//   adjoint:  U^L*  -> G^{L-1}* .. G^{h}*  -> M* -> H^{h} .. H^{L-1} -> V^L
+// with M (or M*) fused into the epilogue of the last adjoint-direction level.
+#include <algorithm>
+
+#include "level_kernel.cuh"
+#include "plan.h"
+
+namespace bfly {
+
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kConsumerWarps = 8;
+constexpr uint32_t kStageBytes = 36 * 1024;
+
+template <typename E>
+__global__ void middle_kernel(const E* __restrict__ in, E* __restrict__ out,
+                              const typename Cx<E>::R* __restrict__ W, uint32_t m, uint32_t r, uint32_t k,
+                              int adjoint) {
+  // forward (factors.py:180-184): out[i, j, rho] = W[i, j, rho] * in[j, i, rho]
+  // adjoint (factors.py:186-190): out[j, i, rho] = W[i, j, rho] * in[i, j, rho]
+  const uint64_t total = static_cast<uint64_t>(m) * m * r * k;
+  for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t kk = x % k, row = x / k;
+    const uint64_t rho = row % r, ij = row / r;
+    const uint64_t i = ij / m, j = ij % m;       // output block (i, j)
+    const uint64_t src = (j * m + i) * r + rho;  // input slot (j, i)
+    const auto w = adjoint ? W[src] : W[row];
+    const E v = in[src * k + kk];
+    out[x] = Cx<E>::make(w * v.x, w * v.y);
+  }
+}
+
+template <typename E>
+int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint64_t P, uint64_t units,
+                 const void* in, void* out, uint32_t k, int adjoint, int remap, cudaStream_t st) {
+  LevelArgs a{};
+  a.fac = fac;
+  a.in = in;
+  a.out = out;
+  a.mid_w = pl.weights;
+  a.R = R;
+  a.C = C;
+  a.nt = nt;
+  a.P = P;
+  a.units = units;
+  a.k = k;
+  a.adjoint = adjoint;
+  a.remap = remap;
+  a.m = pl.m;
+  a.r = pl.rank;
+  const uint64_t esz = sizeof(E);
+  const uint64_t fac_unit = static_cast<uint64_t>(nt) * R * C;
+  const uint64_t vec_col = adjoint ? static_cast<uint64_t>(nt) * R : C;  // vector elems per unit per rhs
+  // right-hand sides per tile: all of them unless one unit no longer fits a stage
+  uint32_t kt = k;
+  while (kt > 1 && (fac_unit + vec_col * kt) * esz > kStageBytes) kt = (kt + 1) / 2;
+  if (esz == 8 && kt > 1 && (kt & 1)) ++kt;
+  kt = std::min(kt, k);
+  uint64_t U = 1;
+  while (U * 2 <= units && (U * 2) * (fac_unit + vec_col * kt) * esz <= kStageBytes) U *= 2;
+  a.kt = kt;
+  a.ktiles = (k + kt - 1) / kt;
+  a.U = static_cast<uint32_t>(U);
+  a.ntiles = (units / U) * a.ktiles;
+  uint64_t stage = U * (fac_unit + vec_col * kt);
+  if (stage & 1) ++stage;
+  a.stage_elems = static_cast<uint32_t>(stage);
+  // lanes per output: fill the consumer threads, keep >= 4 terms per lane
+  const uint64_t n_out = adjoint ? U * C * kt : U * nt * R * kt;
+  const uint32_t terms = adjoint ? nt * R : C;
+  uint32_t S = 1;
+  while (S < 8 && n_out * S * 2 <= static_cast<uint64_t>(kConsumerWarps) * 32 && terms % (S * 2) == 0 &&
+         terms / (S * 2) >= 4)
+    S *= 2;
+  a.S = S;
+  const bool aligned = (reinterpret_cast<uintptr_t>(fac) % 16 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
+  a.bulk = aligned && (esz == 16 || ((R * C) % 2 == 0 && k % 2 == 0 && kt % 2 == 0 && R % 2 == 0 && C % 2 == 0));
+  const size_t smem = 128 + static_cast<size_t>(kStages) * a.stage_elems * esz;
+  auto kern = level_kernel<E, kStages, kConsumerWarps>;
+  BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const uint64_t grid = std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(pl.sms));
+  kern<<<static_cast<unsigned>(grid), (kConsumerWarps + 1) * 32, smem, st>>>(a);
+  BF_CUDA(cudaGetLastError());
+  return 0;
+}
+
+template <typename E>
+int launch_middle(const Plan& pl, const void* in, void* out, uint32_t k, int adjoint, cudaStream_t st) {
+  const uint64_t total = static_cast<uint64_t>(pl.m) * pl.m * pl.rank * k;
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, pl.sms * 8ull));
+  middle_kernel<E><<<grid, 256, 0, st>>>(static_cast<const E*>(in), static_cast<E*>(out),
+                                         static_cast<const typename Cx<E>::R*>(pl.weights), pl.m, pl.rank, k,
+                                         adjoint);
+  BF_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// One factor op, dispatched by kind. `lvl_idx` indexes the plan's level table.
+template <typename E>
+int factor_op(const Plan& pl, int which, int lvl_idx, int adjoint, const void* in, void* out, uint32_t k, int remap,
+              cudaStream_t st) {
+  if (which == BF_FACTOR_V || which == BF_FACTOR_U) {
+    const void* fac = which == BF_FACTOR_V ? pl.v_leaf : pl.u_leaf;
+    return launch_level<E>(pl, fac, pl.leaf_n0, pl.rank, 1, 1, pl.leaf_nb, in, out, k, adjoint, 0, st);
+  }
+  if (which == BF_FACTOR_M) return launch_middle<E>(pl, in, out, k, adjoint, st);
+  const LevelGeo& lg = pl.lev[lvl_idx];
+  const void* fac = which == BF_FACTOR_G ? pl.g_lev[lvl_idx] : pl.h_lev[lvl_idx];
+  return launch_level<E>(pl, fac, pl.rank, 2 * pl.rank, lg.splits ? 2 : 1, lg.P, lg.G * lg.P, in, out, k, adjoint,
+                         remap, st);
+}
+
+template <typename E>
+int timed_op(LaunchRecorder* rec, const Plan& pl, int which, int lvl_idx, int adjoint, const void* in, void* out,
+             uint32_t k, int remap, cudaStream_t st) {
+  int rc = rec ? rec->before(st) : 0;
+  if (!rc) rc = factor_op<E>(pl, which, lvl_idx, adjoint, in, out, k, remap, st);
+  if (!rc && rec) rc = rec->after(st);
+  return rc;
+}
+
+template <typename E>
+int chain(const Plan& pl, const void* in, void* out, uint32_t k, int adjoint, void* ws, cudaStream_t st,
+          LaunchRecorder* rec) {
+  const uint64_t dk = pl.dim_max * k;
+  E* bufs[2] = {static_cast<E*>(ws), static_cast<E*>(ws) + dk};
+  int cur = 0;
+  const int nl = static_cast<int>(pl.nlev);
+  const int lead = adjoint ? BF_FACTOR_U : BF_FACTOR_V;
+  const int down = adjoint ? BF_FACTOR_G : BF_FACTOR_H;
+  const int up = adjoint ? BF_FACTOR_H : BF_FACTOR_G;
+  const int trail = adjoint ? BF_FACTOR_V : BF_FACTOR_U;
+  int rc = timed_op<E>(rec, pl, lead, 0, 1, in, bufs[cur], k, 0, st);
+  if (rc) return rc;
+  for (int i = nl - 1; i >= 0; --i) {  // levels L-1 .. h, adjoint direction
+    rc = timed_op<E>(rec, pl, down, i, 1, bufs[cur], bufs[cur ^ 1], k, i == 0 ? (adjoint ? 2 : 1) : 0, st);
+    if (rc) return rc;
+    cur ^= 1;
+  }
+  for (int i = 0; i < nl; ++i) {  // levels h .. L-1, forward direction
+    rc = timed_op<E>(rec, pl, up, i, 0, bufs[cur], bufs[cur ^ 1], k, 0, st);
+    if (rc) return rc;
+    cur ^= 1;
+  }
+  return timed_op<E>(rec, pl, trail, 0, 0, bufs[cur], out, k, 0, st);
+}
+
+}  // namespace
+
+int plan_apply(const Plan& pl, const void* in, void* out, uint32_t k, int adjoint, void* ws, cudaStream_t st,
+               LaunchRecorder* rec) {
+  return pl.dtype == BF_C128 ? chain<double2>(pl, in, out, k, adjoint, ws, st, rec)
+                             : chain<float2>(pl, in, out, k, adjoint, ws, st, rec);
+}
+
+int plan_apply_factor(const Plan& pl, int which, int lvl_idx, int adjoint, const void* in, void* out, uint32_t k,
+                      cudaStream_t st) {
+  return pl.dtype == BF_C128 ? factor_op<double2>(pl, which, lvl_idx, adjoint, in, out, k, 0, st)
+                             : factor_op<float2>(pl, which, lvl_idx, adjoint, in, out, k, 0, st);
+}
+
+}  // namespace bfly

@@ -1,0 +1,368 @@
+// capi.cu — the extern "C" boundary declared in include/bfly.h.
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "common.cuh"
+#include "plan.h"
+
+namespace bfly {
+
+namespace {
+thread_local std::string g_last_error;
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
+
+// Copy `count` complex128 values (host or device) into plan storage of the plan dtype.
+int upload_complex(const Plan& pl, const void* src, void* dst, uint64_t count, void* tmp, uint64_t tmp_elems,
+                   cudaStream_t st) {
+  if (!count) return 0;
+  if (!src) return fail(BF_EINVAL, "null factor pointer");
+  if (pl.dtype == BF_C128) {
+    BF_CUDA(cudaMemcpyAsync(dst, src, count * 16, cudaMemcpyDefault, st));
+    return 0;
+  }
+  for (uint64_t off = 0; off < count; off += tmp_elems) {
+    const uint64_t c = count - off < tmp_elems ? count - off : tmp_elems;
+    BF_CUDA(cudaMemcpyAsync(tmp, static_cast<const double2*>(src) + off, c * 16, cudaMemcpyDefault, st));
+    int rc = convert_c128_to_c64(tmp, static_cast<float2*>(dst) + off, c, st);
+    if (rc) return rc;
+  }
+  return 0;
+}
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ") in " + what;
+  return e == cudaErrorMemoryAllocation ? BF_ENOMEM : BF_ECUDA;
+}
+
+}  // namespace bfly
+
+using namespace bfly;
+
+extern "C" {
+
+int bf_version(void) { return 1; }
+
+int bf_last_error(char* buf, size_t len) {
+  if (!buf || !len) return BF_EINVAL;
+  std::snprintf(buf, len, "%s", g_last_error.c_str());
+  return BF_OK;
+}
+
+int bf_plan_create(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, uint32_t max_rhs, int dtype,
+                   int device) {
+  if (!out) return fail(BF_EINVAL, "null plan output pointer");
+  *out = nullptr;
+  // DyadicPartition.__post_init__ (partition.py:25-34)
+  if (n < 4 || !is_pow2(n)) return fail(BF_EINVAL, "matrix dimension must be a power of two >= 4");
+  if (levels < 2 || levels % 2) return fail(BF_EINVAL, "tree depth must be even and >= 2");
+  if (levels / 2 >= 63 || (1ull << (levels / 2)) > n)
+    return fail(BF_EINVAL, "depth puts more nodes than n on the middle level");
+  if (levels > 40) return fail(BF_EINVAL, "tree depth too large");
+  if (rank < 1) return fail(BF_EINVAL, "rank must be positive");
+  if (dtype != BF_C128 && dtype != BF_C64) return fail(BF_EINVAL, "dtype must be BF_C128 or BF_C64");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return fail(BF_EINVAL, "no such CUDA device");
+  bf_plan* h = new (std::nothrow) bf_plan();
+  if (!h) return fail(BF_ENOMEM, "host allocation failed");
+  Plan& p = h->p;
+  p.device = device;
+  p.dtype = dtype;
+  p.n = n;
+  p.levels = levels;
+  p.half = levels / 2;
+  p.rank = rank;
+  p.max_rhs = max_rhs ? max_rhs : 1;
+  p.m = 1u << p.half;
+  p.side = n / p.m;
+  // construct.py:_level_geometry (216-227)
+  uint64_t nodes = p.m, rows = p.side;
+  for (uint32_t lvl = p.half; lvl < levels; ++lvl) {
+    LevelGeo g;
+    g.level = lvl;
+    g.P = 1ull << (levels - lvl - 1);
+    g.G = nodes;
+    g.splits = rows >= 2;
+    g.nblocks = g.G * (g.splits ? 2 : 1) * g.P;
+    if (g.splits) {
+      nodes *= 2;
+      rows /= 2;
+    }
+    p.lev.push_back(g);
+  }
+  p.nlev = static_cast<uint32_t>(p.lev.size());
+  p.leaf_nb = nodes;
+  p.leaf_n0 = static_cast<uint32_t>(rows);
+  const uint64_t full = (1ull << levels) * rank;
+  p.dim_max = full > n ? full : n;
+  {
+    DeviceGuard dg(device);
+    cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, device);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
+  *out = h;
+  return BF_OK;
+}
+
+void bf_plan_destroy(bf_plan* plan) {
+  if (!plan) return;
+  if (plan->p.base) {
+    DeviceGuard dg(plan->p.device);
+    cudaFree(plan->p.base);
+  }
+  delete plan;
+}
+
+int bf_plan_geometry(const bf_plan* plan, uint32_t* nlev, int8_t* splits, uint64_t* dims, uint64_t* leaf) {
+  if (!plan) return fail(BF_EINVAL, "null plan");
+  const Plan& p = plan->p;
+  if (nlev) *nlev = p.nlev;
+  for (uint32_t i = 0; i < p.nlev; ++i) {
+    const LevelGeo& g = p.lev[i];
+    if (splits) splits[i] = g.splits ? 1 : 0;
+    if (dims) {
+      uint64_t* d = dims + 5ull * i;
+      if (g.splits) {
+        d[0] = g.G; d[1] = 2; d[2] = g.P; d[3] = p.rank; d[4] = 2ull * p.rank;
+      } else {
+        d[0] = g.G; d[1] = g.P; d[2] = p.rank; d[3] = 2ull * p.rank; d[4] = 0;
+      }
+    }
+  }
+  if (leaf) {
+    leaf[0] = p.leaf_nb;
+    leaf[1] = p.leaf_n0;
+    leaf[2] = p.rank;
+  }
+  return BF_OK;
+}
+
+int bf_plan_upload(bf_plan* plan, const void* u_leaf, const void* const* g_levels, const double* weights,
+                   const void* const* h_levels, const void* v_leaf) {
+  if (!plan) return fail(BF_EINVAL, "null plan");
+  if (!g_levels || !h_levels) return fail(BF_EINVAL, "null level pointer array");
+  Plan& p = plan->p;
+  DeviceGuard dg(p.device);
+  const uint64_t es = p.elem(), rs = p.real();
+  const uint64_t leaf_elems = p.leaf_nb * p.leaf_n0 * p.rank;
+  const uint64_t w_elems = static_cast<uint64_t>(p.m) * p.m * p.rank;
+  uint64_t bytes = 2 * align_up(leaf_elems * es, 256) + align_up(w_elems * rs, 256);
+  for (const LevelGeo& g : p.lev) bytes += 2 * align_up(g.nblocks * p.rank * 2ull * p.rank * es, 256);
+  if (!p.base) {
+    cudaError_t e = cudaMalloc(&p.base, bytes);
+    if (e != cudaSuccess) {
+      p.base = nullptr;
+      return cuda_fail(e, "cudaMalloc(factor storage)");
+    }
+    p.base_bytes = bytes;
+  }
+  char* cur = static_cast<char*>(p.base);
+  auto carve = [&](uint64_t b) {
+    void* r = cur;
+    cur += align_up(b, 256);
+    return r;
+  };
+  p.u_leaf = carve(leaf_elems * es);
+  p.v_leaf = carve(leaf_elems * es);
+  p.weights = carve(w_elems * rs);
+  p.g_lev.assign(p.nlev, nullptr);
+  p.h_lev.assign(p.nlev, nullptr);
+  for (uint32_t i = 0; i < p.nlev; ++i) p.g_lev[i] = carve(p.lev[i].nblocks * p.rank * 2ull * p.rank * es);
+  for (uint32_t i = 0; i < p.nlev; ++i) p.h_lev[i] = carve(p.lev[i].nblocks * p.rank * 2ull * p.rank * es);
+
+  cudaStream_t st = nullptr;
+  void* tmp = nullptr;
+  const uint64_t tmp_elems = 1ull << 25;  // 512 MiB of complex128 staging for the C64 conversion
+  if (p.dtype == BF_C64) BF_CUDA(cudaMalloc(&tmp, tmp_elems * 16));
+  int rc = upload_complex(p, u_leaf, p.u_leaf, leaf_elems, tmp, tmp_elems, st);
+  if (!rc) rc = upload_complex(p, v_leaf, p.v_leaf, leaf_elems, tmp, tmp_elems, st);
+  for (uint32_t i = 0; !rc && i < p.nlev; ++i) {
+    const uint64_t c = p.lev[i].nblocks * p.rank * 2ull * p.rank;
+    rc = upload_complex(p, g_levels[i], p.g_lev[i], c, tmp, tmp_elems, st);
+    if (!rc) rc = upload_complex(p, h_levels[i], p.h_lev[i], c, tmp, tmp_elems, st);
+  }
+  if (!rc) {
+    if (!weights) {
+      rc = fail(BF_EINVAL, "null middle weights");
+    } else if (p.dtype == BF_C128) {
+      cudaError_t e = cudaMemcpyAsync(p.weights, weights, w_elems * 8, cudaMemcpyDefault, st);
+      if (e != cudaSuccess) rc = cuda_fail(e, "upload weights");
+    } else {
+      cudaError_t e = cudaMemcpyAsync(tmp, weights, w_elems * 8, cudaMemcpyDefault, st);
+      rc = e != cudaSuccess ? cuda_fail(e, "upload weights") : convert_f64_to_f32(tmp, p.weights, w_elems, st);
+    }
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (tmp) cudaFree(tmp);
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "bf_plan_upload");
+  p.uploaded = true;
+  return BF_OK;
+}
+
+uint64_t bf_apply_workspace_bytes(const bf_plan* plan, uint32_t k) {
+  if (!plan) return 0;
+  return 2ull * plan->p.dim_max * (k ? k : 1) * plan->p.elem();
+}
+
+int bf_apply(const bf_plan* plan, const void* in, void* out, uint32_t k, int adjoint, void* workspace,
+             uint64_t workspace_bytes, void* stream) {
+  if (!plan) return fail(BF_EINVAL, "null plan");
+  const Plan& p = plan->p;
+  if (!p.uploaded) return fail(BF_ESTATE, "plan has no factors (call bf_plan_upload)");
+  if (k < 1) return fail(BF_EINVAL, "need at least one right-hand side");
+  if (!in || !out) return fail(BF_EINVAL, "null input/output pointer");
+  if (!workspace || workspace_bytes < bf_apply_workspace_bytes(plan, k))
+    return fail(BF_EINVAL, "workspace too small (see bf_apply_workspace_bytes)");
+  DeviceGuard dg(p.device);
+  return plan_apply(p, in, out, k, adjoint ? 1 : 0, workspace, static_cast<cudaStream_t>(stream));
+}
+
+int bf_timer_create(bf_timer** out, uint32_t max_steps, uint32_t max_launches) {
+  if (!out || !max_steps || !max_launches) return fail(BF_EINVAL, "bad timer arguments");
+  *out = nullptr;
+  bf_timer* t = new (std::nothrow) bf_timer();
+  if (!t) return fail(BF_ENOMEM, "host allocation failed");
+  t->max_steps = max_steps;
+  t->max_launches = max_launches;
+  t->ev.assign(2ull * max_steps * max_launches, nullptr);
+  for (auto& e : t->ev) {
+    cudaError_t err = cudaEventCreate(&e);
+    if (err != cudaSuccess) {
+      e = nullptr;
+      bf_timer_destroy(t);
+      return cuda_fail(err, "cudaEventCreate");
+    }
+  }
+  *out = t;
+  return BF_OK;
+}
+
+void bf_timer_destroy(bf_timer* timer) {
+  if (!timer) return;
+  for (auto e : timer->ev)
+    if (e) cudaEventDestroy(e);
+  delete timer;
+}
+
+int bf_apply_timed(const bf_plan* plan, const void* in, void* out, uint32_t k, int adjoint, void* workspace,
+                   uint64_t workspace_bytes, void* stream, bf_timer* timer) {
+  if (!timer) return fail(BF_EINVAL, "null timer");
+  if (timer->steps >= timer->max_steps) return fail(BF_EINVAL, "timer is full");
+  if (!plan) return fail(BF_EINVAL, "null plan");
+  const Plan& p = plan->p;
+  if (!p.uploaded) return fail(BF_ESTATE, "plan has no factors (call bf_plan_upload)");
+  if (k < 1 || !in || !out) return fail(BF_EINVAL, "bad k or null pointer");
+  if (!workspace || workspace_bytes < bf_apply_workspace_bytes(plan, k))
+    return fail(BF_EINVAL, "workspace too small (see bf_apply_workspace_bytes)");
+  DeviceGuard dg(p.device);
+  LaunchRecorder rec;
+  rec.ev = timer->ev.data() + 2ull * timer->steps * timer->max_launches;
+  rec.cap = timer->max_launches;
+  int rc = plan_apply(p, in, out, k, adjoint ? 1 : 0, workspace, static_cast<cudaStream_t>(stream), &rec);
+  if (rc) return rc;
+  if (timer->steps == 0) timer->launches = rec.used;
+  if (rec.used != timer->launches) return fail(BF_EINVAL, "launch count changed between timed steps");
+  ++timer->steps;
+  return BF_OK;
+}
+
+int bf_timer_read(bf_timer* timer, float* launch_ms, uint32_t* steps, uint32_t* launches) {
+  if (!timer) return fail(BF_EINVAL, "null timer");
+  if (steps) *steps = timer->steps;
+  if (launches) *launches = timer->launches;
+  if (!launch_ms) return BF_OK;
+  for (uint32_t s = 0; s < timer->steps; ++s)
+    for (uint32_t i = 0; i < timer->launches; ++i) {
+      cudaEvent_t* e = timer->ev.data() + 2ull * (static_cast<uint64_t>(s) * timer->max_launches + i);
+      BF_CUDA(cudaEventSynchronize(e[1]));
+      float ms = 0;
+      BF_CUDA(cudaEventElapsedTime(&ms, e[0], e[1]));
+      launch_ms[static_cast<uint64_t>(s) * timer->launches + i] = ms;
+    }
+  return BF_OK;
+}
+
+int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint32_t k, int adjoint, void* stream) {
+  if (!plan) return fail(BF_EINVAL, "null plan");
+  const Plan& p = plan->p;
+  if (!p.uploaded) return fail(BF_ESTATE, "plan has no factors (call bf_plan_upload)");
+  if (k < 1) return fail(BF_EINVAL, "need at least one right-hand side");
+  if (!in_host || !out_host) return fail(BF_EINVAL, "null input/output pointer");
+  DeviceGuard dg(p.device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t io = p.n * k * p.elem();
+  const uint64_t wsb = bf_apply_workspace_bytes(plan, k);
+  void *din = nullptr, *dout = nullptr, *ws = nullptr;
+  BF_CUDA(cudaMallocAsync(&din, io, st));
+  BF_CUDA(cudaMallocAsync(&dout, io, st));
+  BF_CUDA(cudaMallocAsync(&ws, wsb, st));
+  int rc = 0;
+  cudaError_t e = cudaMemcpyAsync(din, in_host, io, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) rc = cuda_fail(e, "H2D input");
+  if (!rc) rc = plan_apply(p, din, dout, k, adjoint ? 1 : 0, ws, st);
+  if (!rc) {
+    e = cudaMemcpyAsync(out_host, dout, io, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "D2H output");
+  }
+  cudaFreeAsync(din, st);
+  cudaFreeAsync(dout, st);
+  cudaFreeAsync(ws, st);
+  e = cudaStreamSynchronize(st);
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "bf_apply_host");
+  return BF_OK;
+}
+
+int bf_apply_factor(const bf_plan* plan, int which, uint32_t level, int adjoint, const void* in, void* out,
+                    uint32_t k, void* stream) {
+  if (!plan) return fail(BF_EINVAL, "null plan");
+  const Plan& p = plan->p;
+  if (!p.uploaded) return fail(BF_ESTATE, "plan has no factors (call bf_plan_upload)");
+  if (which < BF_FACTOR_V || which > BF_FACTOR_U) return fail(BF_EINVAL, "unknown factor selector");
+  if (k < 1 || !in || !out) return fail(BF_EINVAL, "bad k or null pointer");
+  int idx = 0;
+  if (which == BF_FACTOR_G || which == BF_FACTOR_H) {
+    if (level < p.half || level >= p.levels) return fail(BF_EINVAL, "transfer level outside [half, levels)");
+    idx = static_cast<int>(level - p.half);
+  }
+  DeviceGuard dg(p.device);
+  return plan_apply_factor(p, which, idx, adjoint ? 1 : 0, in, out, k, static_cast<cudaStream_t>(stream));
+}
+
+int bf_entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr, const int64_t* cols, uint32_t nc,
+               void* out, void* stream) {
+  if (n < 1) return fail(BF_EINVAL, "n must be positive");
+  if ((nr && !rows) || (nc && !cols) || (static_cast<uint64_t>(nr) * nc && !out))
+    return fail(BF_EINVAL, "null pointer");
+  return entries(kernel_id, n, rows, nr, cols, nc, out, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

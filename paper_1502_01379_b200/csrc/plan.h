@@ -1,0 +1,77 @@
+// plan.h — device-resident factor chain (the C++ side of bf_plan).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/bfly.h"
+
+namespace bfly {
+
+// One transfer level ascending from half (construct.py:_level_geometry, 216-227).
+struct LevelGeo {
+  uint32_t level;
+  bool splits;
+  uint64_t G, P;       // nodes, pairs
+  uint64_t nblocks;    // G * (splits ? 2 : 1) * P
+};
+
+struct Plan {
+  int device = 0, dtype = BF_C128, sms = 148;
+  uint64_t n = 0;
+  uint32_t levels = 0, half = 0, rank = 0, max_rhs = 1;
+  uint32_t m = 0;            // middle nodes per side, 2^half
+  uint64_t side = 0;         // n / m
+  uint32_t nlev = 0;         // transfer levels per side
+  std::vector<LevelGeo> lev;
+  uint64_t leaf_nb = 0;      // leaf blocks
+  uint32_t leaf_n0 = 0;      // rows per leaf block
+  uint64_t dim_max = 0;      // largest intermediate vector length (2^L r)
+  // device storage: one allocation, carved per factor
+  void* base = nullptr;
+  uint64_t base_bytes = 0;
+  void* u_leaf = nullptr;
+  void* v_leaf = nullptr;
+  void* weights = nullptr;   // f64 (C128) or f32 (C64)
+  std::vector<void*> g_lev, h_lev;
+  bool uploaded = false;
+
+  size_t elem() const { return dtype == BF_C128 ? 16 : 8; }
+  size_t real() const { return dtype == BF_C128 ? 8 : 4; }
+};
+
+// Optional per-launch event recorder (bf_timer): ev[2i], ev[2i+1] bracket launch i.
+struct LaunchRecorder {
+  cudaEvent_t* ev = nullptr;
+  uint32_t cap = 0, used = 0;
+  int before(cudaStream_t st) {
+    if (!ev || used >= cap) return 0;
+    return cudaEventRecord(ev[2 * used], st) == cudaSuccess ? 0 : BF_ECUDA;
+  }
+  int after(cudaStream_t st) {
+    if (!ev || used >= cap) return 0;
+    return cudaEventRecord(ev[2 * used++ + 1], st) == cudaSuccess ? 0 : BF_ECUDA;
+  }
+};
+
+int plan_apply(const Plan& pl, const void* in, void* out, uint32_t k, int adjoint, void* ws, cudaStream_t st,
+               LaunchRecorder* rec = nullptr);
+int plan_apply_factor(const Plan& pl, int which, int lvl_idx, int adjoint, const void* in, void* out, uint32_t k,
+                      cudaStream_t st);
+int entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr, const int64_t* cols, uint32_t nc, void* out,
+            cudaStream_t st);
+int convert_c128_to_c64(const void* src, void* dst, uint64_t count, cudaStream_t st);
+int convert_f64_to_f32(const void* src, void* dst, uint64_t count, cudaStream_t st);
+
+}  // namespace bfly
+
+struct bf_plan {
+  bfly::Plan p;
+};
+
+struct bf_timer {
+  uint32_t max_steps = 0, max_launches = 0, steps = 0, launches = 0;
+  std::vector<cudaEvent_t> ev;  // [step][launch][2]
+};

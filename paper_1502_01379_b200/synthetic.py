@@ -1,0 +1,68 @@
+"""Seeded synthetic factor chains at exact ``_level_geometry`` shapes.
+
+Benchmark inputs for configs whose CPU construction is infeasible (BASELINE
+config 2 takes ~10-19 h in the reference, config 4a does not fit host RAM):
+blocks are complex Gaussians scaled by 1/sqrt(2*cols) (so every level
+roughly preserves the vector norm), middle weights U(0.5, 1.5) as in the
+reference's ``conftest.random_exact_chain`` (pkg/tests/conftest.py:20-39),
+drawn in the order V^L, H levels ascending, M, G levels ascending, U^L.
+``random_exact_chain`` itself is not used: it requires leaf rows <= r and
+fails at leaf 16.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .factors import BlockDiagonalFactor, ButterflyFactors, MiddleFactor, TransferFactor
+from .partition import DyadicPartition, level_geometry
+
+
+def synthetic_chain(p: DyadicPartition, r: int, seed: int = 20240801, device=None) -> ButterflyFactors:
+    """Host (NumPy, ``device=None``) or device (torch CUDA tensors) synthetic chain."""
+    shapes, leaf_shape = level_geometry(p, r)
+    if device is None:
+        rng = np.random.default_rng(seed)
+
+        def draw(shape):
+            scale = 1.0 / np.sqrt(2.0 * shape[-1])
+            out = np.empty(shape, dtype=np.complex128)
+            out.real = rng.standard_normal(shape) * scale
+            out.imag = rng.standard_normal(shape) * scale
+            return out
+
+        def weights():
+            return rng.uniform(0.5, 1.5, size=(p.mid_nodes, p.mid_nodes, r))
+    else:
+        import torch
+        gen = torch.Generator(device=device)
+        gen.manual_seed(seed)
+
+        def draw(shape):
+            scale = 1.0 / np.sqrt(2.0 * shape[-1])
+            t = torch.randn(tuple(shape) + (2,), dtype=torch.float64, device=device, generator=gen)
+            t.mul_(scale)
+            return torch.view_as_complex(t)
+
+        def weights():
+            w = torch.rand((p.mid_nodes, p.mid_nodes, r), dtype=torch.float64, device=device, generator=gen)
+            return w.add_(0.5)
+
+    v = draw(leaf_shape)
+    h = tuple(TransferFactor(lvl, draw(shape)) for lvl, _, shape in shapes)
+    w = weights()
+    g = tuple(TransferFactor(lvl, draw(shape)) for lvl, _, shape in shapes)
+    u = draw(leaf_shape)
+    return ButterflyFactors(p, r, BlockDiagonalFactor(u), g, MiddleFactor(w), h, BlockDiagonalFactor(v))
+
+
+def to_host(f: ButterflyFactors) -> ButterflyFactors:
+    """NumPy copy of a (possibly device-resident) chain."""
+    def h(a):
+        return a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+
+    return ButterflyFactors(f.partition, f.rank, BlockDiagonalFactor(h(f.u_outer.blocks)),
+                            tuple(TransferFactor(t.level, h(t.blocks)) for t in f.g_chain),
+                            MiddleFactor(h(f.middle.weights)),
+                            tuple(TransferFactor(t.level, h(t.blocks)) for t in f.h_chain),
+                            BlockDiagonalFactor(h(f.v_outer.blocks)))

@@ -1,0 +1,184 @@
+"""GPU parity of the apply chain (libbfly.so via the C ABI) against the CPU
+oracle and the reference's own golden outputs.
+
+Tolerances (BASELINE.json north_star): relative 2-norm <= 1e-11 for complex128,
+<= 1e-5 for the opt-in complex64 mode. Algebraic KATs follow
+pkg/tests/test_factors.py:16-51.
+"""
+
+import numpy as np
+import pytest
+
+import paper_1502_01379_b200 as bf
+from conftest import chain_from_golden, complex_gaussian, golden
+from oracle import chain as ochain
+from paper_1502_01379_b200.synthetic import synthetic_chain, to_host
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL128, TOL64 = 1e-11, 1e-5
+GOLDEN_APPLY = ["apply_fio_n256_r8_leaf025.npz", "apply_cfg0_fio_n1024_r12_leaf8.npz",
+                "apply_dftp_n1024_r8_leaf16.npz"]
+
+
+def rel(a, b):
+    a = a.cpu().numpy() if hasattr(a, "cpu") else a
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def product(c):
+    return bf.from_arrays(c.n, c.levels, c.rank, c.u_leaf, c.g_levels, c.weights, c.h_levels, c.v_leaf)
+
+
+def oracle_of(f):
+    h = to_host(f)
+    return ochain.Chain(h.n, h.partition.levels, h.rank, h.u_outer.blocks,
+                        [(t.level, t.blocks) for t in h.g_chain], h.middle.weights,
+                        [(t.level, t.blocks) for t in h.h_chain], h.v_outer.blocks)
+
+
+@pytest.fixture(scope="module", params=GOLDEN_APPLY)
+def case(request):
+    d = golden(request.param)
+    return d, product(chain_from_golden(d))
+
+
+def test_golden_forward_adjoint_c128(case):
+    d, f = case
+    g = torch.from_numpy(d["g"]).cuda()
+    assert rel(f.plan().apply(g), d["fwd"]) <= TOL128
+    assert rel(f.plan().apply(g, adjoint=True), d["adj"]) <= TOL128
+    one = f.apply(d["g"][:, 0])                       # host path, 1-D in -> 1-D out
+    assert one.ndim == 1 and one.dtype == np.complex128 and rel(one, d["fwd1"]) <= TOL128
+
+
+def test_golden_c64_mode(case):
+    d, f = case
+    pl = f.plan("c64")
+    g = torch.from_numpy(d["g"]).cuda()
+    out = pl.apply(g)
+    assert out.dtype == torch.complex64
+    assert rel(out.to(torch.complex128), d["fwd"]) <= TOL64
+    assert rel(pl.apply(g, adjoint=True).to(torch.complex128), d["adj"]) <= TOL64
+
+
+def test_host_and_device_paths_bitwise_equal(case):
+    d, f = case
+    dev = f.plan().apply(torch.from_numpy(d["g"]).cuda()).cpu().numpy()
+    host = f.apply(d["g"])
+    assert np.array_equal(dev, host)
+    again = f.apply(d["g"])
+    assert np.array_equal(host, again)                # run-to-run deterministic
+
+
+def test_zero_bad_length_and_upcast(case):
+    d, f = case
+    n = f.n
+    assert np.array_equal(f.apply(np.zeros(n, dtype=complex)), np.zeros(n, dtype=complex))
+    with pytest.raises(ValueError):
+        f.apply(np.zeros(n // 2))
+    with pytest.raises(ValueError):
+        f.apply_adjoint(np.zeros(n // 2))
+    real_in = np.arange(n, dtype=np.float32)          # any numeric dtype is upcast (factors.py:222)
+    assert f.apply(real_in).dtype == np.complex128
+    assert rel(f.apply(real_in), f.apply(real_in.astype(complex))) == 0.0
+
+
+def test_algebraic_kats(case, rng):
+    d, f = case
+    n = f.n
+    x, y = complex_gaussian(rng, n), complex_gaussian(rng, n)
+    a, b = 0.3 - 1.1j, -2.0 + 0.4j
+    lhs = f.apply(a * x + b * y)
+    rhs = a * f.apply(x) + b * f.apply(y)
+    assert np.linalg.norm(lhs - rhs) <= 1e-13 * np.linalg.norm(rhs)
+    ip1 = np.vdot(y, f.apply(x))
+    ip2 = np.vdot(f.apply_adjoint(y), x)
+    assert abs(ip1 - ip2) <= 1e-12 * abs(ip1)
+    block = complex_gaussian(rng, (n, 5))
+    out = f.apply(block)
+    for k in range(5):
+        col = f.apply(block[:, k])
+        assert np.linalg.norm(out[:, k] - col) <= 1e-13 * np.linalg.norm(col)
+
+
+def test_per_factor_parity(case):
+    """bf_apply_factor vs the oracle's per-factor maps (factors.py:49-56, 120-142, 180-190)."""
+    d, f = case
+    c = chain_from_golden(d)
+    pl = f.plan()
+    rng = np.random.default_rng(3)
+    k = 3
+    nb, n0, r = c.u_leaf.shape
+    for which, arr in (("V", c.v_leaf), ("U", c.u_leaf)):
+        x = complex_gaussian(rng, (nb * n0, k))
+        assert rel(pl.apply_factor(which, 0, True, torch.from_numpy(x).cuda()), ochain.leaf_adjoint(arr, x)) <= 1e-14
+        x = complex_gaussian(rng, (nb * r, k))
+        assert rel(pl.apply_factor(which, 0, False, torch.from_numpy(x).cuda()), ochain.leaf_forward(arr, x)) <= 1e-14
+    dim = c.weights.size
+    x = complex_gaussian(rng, (dim, k))
+    assert rel(pl.apply_factor("M", 0, False, torch.from_numpy(x).cuda()), ochain.middle_forward(c.weights, x)) == 0
+    assert rel(pl.apply_factor("M", 0, True, torch.from_numpy(x).cuda()), ochain.middle_adjoint(c.weights, x)) == 0
+    for which, levels in (("G", c.g_levels), ("H", c.h_levels)):
+        for lvl, b in levels:
+            tf = bf.TransferFactor(lvl, b)
+            rows, cols = tf.shape
+            x = complex_gaussian(rng, (cols, k))
+            got = pl.apply_factor(which, lvl, False, torch.from_numpy(x).cuda())
+            assert rel(got, ochain.transfer_forward(b, x)) <= 1e-14, (which, lvl)
+            x = complex_gaussian(rng, (rows, k))
+            got = pl.apply_factor(which, lvl, True, torch.from_numpy(x).cuda())
+            assert rel(got, ochain.transfer_adjoint(b, x)) <= 1e-14, (which, lvl)
+
+
+@pytest.mark.parametrize("n,leaf,r,k", [
+    (1 << 16, 16, 8, 64),     # config 1 geometry (L=12), 64 RHS
+    (1 << 12, 0.25, 5, 7),    # merge-only levels, odd rank and odd k
+    (1 << 14, 4, 25, 16),     # rank 25 (the 2D configs' rank), 16 RHS
+    (1 << 10, 16, 12, 300),   # many RHS: k split across tiles
+])
+def test_synthetic_geometries(n, leaf, r, k):
+    p = bf.make_partition(n, leaf)
+    f = synthetic_chain(p, r, seed=n + r)
+    oc = oracle_of(f)
+    g = complex_gaussian(np.random.default_rng(k), (n, k))
+    gd = torch.from_numpy(g).cuda()
+    assert rel(f.plan().apply(gd), ochain.apply(oc, g)) <= TOL128
+    assert rel(f.plan().apply(gd, adjoint=True), ochain.apply(oc, g, adjoint=True)) <= TOL128
+    assert rel(f.plan("c64").apply(gd).to(torch.complex128), ochain.apply(oc, g)) <= TOL64
+
+
+def test_config2_geometry_k1():
+    """BASELINE config 2 (FIO geometry N=2^20, r=16, leaf 16 -> L=16), synthetic factors, 1 RHS."""
+    p = bf.make_partition(1 << 20, 16)
+    f = synthetic_chain(p, 16, seed=2, device="cuda")
+    g = complex_gaussian(np.random.default_rng(0), (p.n,))
+    got = f.plan().apply(torch.from_numpy(g).cuda()).cpu().numpy()
+    want = ochain.apply(oracle_of(f), g)
+    assert rel(got, want) <= TOL128
+    got64 = f.plan("c64").apply(torch.from_numpy(g).cuda()).to(torch.complex128).cpu().numpy()
+    assert rel(got64, want) <= TOL64
+
+
+def test_entries_match_reference_golden():
+    from paper_1502_01379_b200 import _lib
+    import ctypes
+    d = golden("entries.npz")
+    lib = _lib.load()
+    for n in (1024, 1 << 16, 1 << 20, 1 << 24):
+        rows = torch.from_numpy(d[f"fio_{n}_rows"].astype(np.int64)).cuda()
+        cols = torch.from_numpy(d[f"fio_{n}_cols"].astype(np.int64)).cuda()
+        out = torch.empty((rows.numel(), cols.numel()), dtype=torch.complex128, device="cuda")
+        _lib.check(lib.bf_entries(_lib.BF_KERNEL_FIO, n, ctypes.c_void_p(rows.data_ptr()), rows.numel(),
+                                  ctypes.c_void_p(cols.data_ptr()), cols.numel(), ctypes.c_void_p(out.data_ptr()),
+                                  None))
+        torch.cuda.synchronize()
+        assert np.max(np.abs(out.cpu().numpy() - d[f"fio_{n}"])) <= 1e-15
+    rows = torch.from_numpy(d["dftp_rows"].astype(np.int64)).cuda()
+    cols = torch.from_numpy(d["dftp_cols"].astype(np.int64)).cuda()
+    out = torch.empty((rows.numel(), cols.numel()), dtype=torch.complex128, device="cuda")
+    _lib.check(lib.bf_entries(_lib.BF_KERNEL_DFTP, 1 << 16, ctypes.c_void_p(rows.data_ptr()), rows.numel(),
+                              ctypes.c_void_p(cols.data_ptr()), cols.numel(), ctypes.c_void_p(out.data_ptr()), None))
+    torch.cuda.synchronize()
+    assert np.max(np.abs(out.cpu().numpy() - d["dftp"])) <= 1e-15
