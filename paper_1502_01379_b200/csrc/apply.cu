@@ -14,9 +14,10 @@ namespace bfly {
 
 namespace {
 
-constexpr int kStages = 4;
-constexpr int kConsumerWarps = 8;
-constexpr uint32_t kStageBytes = 36 * 1024;
+constexpr int kStages = 3;
+constexpr int kConsumerWarps = 2;
+constexpr int kCtasPerSm = 2;
+constexpr uint32_t kStageBytes = 34 * 1024 + 512;
 
 template <typename E>
 __global__ void middle_kernel(const E* __restrict__ in, E* __restrict__ out,
@@ -37,9 +38,16 @@ __global__ void middle_kernel(const E* __restrict__ in, E* __restrict__ out,
   }
 }
 
+uint32_t ilog2(uint64_t x) {
+  uint32_t l = 0;
+  while ((1ull << (l + 1)) <= x) ++l;
+  return l;
+}
+
 template <typename E>
 int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint64_t P, uint64_t units,
                  const void* in, void* out, uint32_t k, int adjoint, int remap, cudaStream_t st) {
+  if (units >= (1ull << 31)) return fail(BF_EINVAL, "level has too many blocks for one launch");
   LevelArgs a{};
   a.fac = fac;
   a.in = in;
@@ -48,8 +56,8 @@ int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32
   a.R = R;
   a.C = C;
   a.nt = nt;
-  a.P = P;
-  a.units = units;
+  a.lgP = ilog2(P);
+  a.units = static_cast<uint32_t>(units);
   a.k = k;
   a.adjoint = adjoint;
   a.remap = remap;
@@ -67,25 +75,19 @@ int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32
   while (U * 2 <= units && (U * 2) * (fac_unit + vec_col * kt) * esz <= kStageBytes) U *= 2;
   a.kt = kt;
   a.ktiles = (k + kt - 1) / kt;
-  a.U = static_cast<uint32_t>(U);
-  a.ntiles = (units / U) * a.ktiles;
+  a.lgU = ilog2(U);
+  a.ntiles = static_cast<uint32_t>((units / U) * a.ktiles);
   uint64_t stage = U * (fac_unit + vec_col * kt);
   if (stage & 1) ++stage;
   a.stage_elems = static_cast<uint32_t>(stage);
-  // lanes per output: fill the consumer threads, keep >= 4 terms per lane
-  const uint64_t n_out = adjoint ? U * C * kt : U * nt * R * kt;
-  const uint32_t terms = adjoint ? nt * R : C;
-  uint32_t S = 1;
-  while (S < 8 && n_out * S * 2 <= static_cast<uint64_t>(kConsumerWarps) * 32 && terms % (S * 2) == 0 &&
-         terms / (S * 2) >= 4)
-    S *= 2;
-  a.S = S;
   const bool aligned = (reinterpret_cast<uintptr_t>(fac) % 16 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
   a.bulk = aligned && (esz == 16 || ((R * C) % 2 == 0 && k % 2 == 0 && kt % 2 == 0 && R % 2 == 0 && C % 2 == 0));
   const size_t smem = 128 + static_cast<size_t>(kStages) * a.stage_elems * esz;
-  auto kern = level_kernel<E, kStages, kConsumerWarps>;
+  if (smem > 227 * 1024) return fail(BF_EINVAL, "rank too large: one block pair exceeds the shared-memory stage");
+  auto kern = level_kernel<E, kStages, kConsumerWarps, kCtasPerSm>;
   BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  const uint64_t grid = std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(pl.sms));
+  const uint64_t per_sm = smem * kCtasPerSm <= 227 * 1024 ? kCtasPerSm : 1;
+  const uint64_t grid = std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(pl.sms) * per_sm);
   kern<<<static_cast<unsigned>(grid), (kConsumerWarps + 1) * 32, smem, st>>>(a);
   BF_CUDA(cudaGetLastError());
   return 0;

@@ -174,11 +174,17 @@ def test_entries_match_reference_golden():
                                   ctypes.c_void_p(cols.data_ptr()), cols.numel(), ctypes.c_void_p(out.data_ptr()),
                                   None))
         torch.cuda.synchronize()
-        assert np.max(np.abs(out.cpu().numpy() - d[f"fio_{n}"])) <= 1e-15
+        got, want = out.cpu().numpy(), d[f"fio_{n}"]
+        # exp(i a) with a = fl(2 pi Phi): the phase follows the reference's rounding sequence
+        # exactly (no FMA); CUDA's sin (<= 1 ulp, not correctly rounded) can move c(x) by an
+        # ulp, which moves Phi by at most an ulp. Bound: 2 ulp of the largest |a|.
+        amax = 2 * np.pi * n * 1.5
+        assert np.max(np.abs(got - want)) <= 2 * np.spacing(amax) + 4e-16
+        assert np.mean(got == want) >= 0.5   # measured: ~70% bit-identical
     rows = torch.from_numpy(d["dftp_rows"].astype(np.int64)).cuda()
     cols = torch.from_numpy(d["dftp_cols"].astype(np.int64)).cuda()
     out = torch.empty((rows.numel(), cols.numel()), dtype=torch.complex128, device="cuda")
     _lib.check(lib.bf_entries(_lib.BF_KERNEL_DFTP, 1 << 16, ctypes.c_void_p(rows.data_ptr()), rows.numel(),
                               ctypes.c_void_p(cols.data_ptr()), cols.numel(), ctypes.c_void_p(out.data_ptr()), None))
     torch.cuda.synchronize()
-    assert np.max(np.abs(out.cpu().numpy() - d["dftp"])) <= 1e-15
+    assert np.max(np.abs(out.cpu().numpy() - d["dftp"])) <= 4e-16   # exact phase; sin/cos ulps only
