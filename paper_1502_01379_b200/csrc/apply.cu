@@ -14,10 +14,6 @@ namespace bfly {
 
 namespace {
 
-constexpr int kStages = 3;
-constexpr int kConsumerWarps = 2;
-constexpr int kCtasPerSm = 2;
-constexpr uint32_t kStageBytes = 34 * 1024 + 512;
 
 template <typename E>
 __global__ void middle_kernel(const E* __restrict__ in, E* __restrict__ out,
@@ -44,10 +40,22 @@ uint32_t ilog2(uint64_t x) {
   return l;
 }
 
+// Launch shapes: the streaming kernel (k small: HBM-bound on factor bytes) and
+// the register-tiled many-RHS kernel (k >= kMrhsMinK: FP64-FMA bound).
+struct Shape {
+  int stages, ncw, ctas_per_sm;
+  uint32_t stage_bytes;
+};
+constexpr Shape kStream{3, 2, 2, 34 * 1024 + 512};
+constexpr Shape kMrhs{2, 8, 1, 100 * 1024};
+constexpr uint32_t kMrhsMinK = 8;
+
 template <typename E>
 int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint64_t P, uint64_t units,
                  const void* in, void* out, uint32_t k, int adjoint, int remap, cudaStream_t st) {
   if (units >= (1ull << 31)) return fail(BF_EINVAL, "level has too many blocks for one launch");
+  const bool mrhs = k >= kMrhsMinK;
+  const Shape sh = mrhs ? kMrhs : kStream;
   LevelArgs a{};
   a.fac = fac;
   a.in = in;
@@ -66,13 +74,22 @@ int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32
   const uint64_t esz = sizeof(E);
   const uint64_t fac_unit = static_cast<uint64_t>(nt) * R * C;
   const uint64_t vec_col = adjoint ? static_cast<uint64_t>(nt) * R : C;  // vector elems per unit per rhs
+  const uint64_t m_out = adjoint ? C : static_cast<uint64_t>(nt) * R;
   // right-hand sides per tile: all of them unless one unit no longer fits a stage
-  uint32_t kt = k;
-  while (kt > 1 && (fac_unit + vec_col * kt) * esz > kStageBytes) kt = (kt + 1) / 2;
+  uint32_t kt = mrhs ? std::min<uint32_t>(k, 128) : k;
+  while (kt > 1 && (fac_unit + vec_col * kt) * esz > sh.stage_bytes) kt = (kt + 1) / 2;
+  if (mrhs && kt > 4) kt = (kt + 3) / 4 * 4;
   if (esz == 8 && kt > 1 && (kt & 1)) ++kt;
   kt = std::min(kt, k);
   uint64_t U = 1;
-  while (U * 2 <= units && (U * 2) * (fac_unit + vec_col * kt) * esz <= kStageBytes) U *= 2;
+  const uint64_t want_items = static_cast<uint64_t>(sh.ncw) * 32;
+  // many-RHS warp tiles cover (32/LC)*TM rows x LC*TN columns (see consume_tile_mrhs_any)
+  const uint64_t tile_rows = kt >= 32 ? (kt >= 128 ? 4 : kt >= 64 ? 8 : 16) : (kt >= 16 ? 16 : 16);
+  const uint64_t tile_cols = kt >= 128 ? 128 : kt >= 64 ? 64 : kt >= 32 ? 32 : kt >= 16 ? 16 : 8;
+  auto items = [&](uint64_t u) { return u * ((m_out + tile_rows - 1) / tile_rows) * ((kt + tile_cols - 1) / tile_cols) * 32; };
+  while (U * 2 <= units && (U * 2) * (fac_unit + vec_col * kt) * esz <= sh.stage_bytes &&
+         (!mrhs || items(U) < want_items))
+    U *= 2;
   a.kt = kt;
   a.ktiles = (k + kt - 1) / kt;
   a.lgU = ilog2(U);
@@ -81,14 +98,18 @@ int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32
   if (stage & 1) ++stage;
   a.stage_elems = static_cast<uint32_t>(stage);
   const bool aligned = (reinterpret_cast<uintptr_t>(fac) % 16 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
-  a.bulk = aligned && (esz == 16 || ((R * C) % 2 == 0 && k % 2 == 0 && kt % 2 == 0 && R % 2 == 0 && C % 2 == 0));
-  const size_t smem = 128 + static_cast<size_t>(kStages) * a.stage_elems * esz;
+  // every bulk copy must move a multiple of 16 bytes between 16-byte aligned addresses:
+  // complex128 always does; complex64 needs even block sizes and, when a row is split
+  // into k-tiles, even k and kt.
+  a.bulk = aligned && (esz == 16 || (R % 2 == 0 && C % 2 == 0 && (a.ktiles == 1 || (k % 2 == 0 && kt % 2 == 0))));
+  const size_t smem = 128 + static_cast<size_t>(sh.stages) * a.stage_elems * esz;
   if (smem > 227 * 1024) return fail(BF_EINVAL, "rank too large: one block pair exceeds the shared-memory stage");
-  auto kern = level_kernel<E, kStages, kConsumerWarps, kCtasPerSm>;
+  void (*kern)(LevelArgs) = mrhs ? level_kernel<E, kMrhs.stages, kMrhs.ncw, kMrhs.ctas_per_sm, 1>
+                                 : level_kernel<E, kStream.stages, kStream.ncw, kStream.ctas_per_sm, 0>;
   BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  const uint64_t per_sm = smem * kCtasPerSm <= 227 * 1024 ? kCtasPerSm : 1;
+  const uint64_t per_sm = smem * sh.ctas_per_sm <= 227 * 1024 ? sh.ctas_per_sm : 1;
   const uint64_t grid = std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(pl.sms) * per_sm);
-  kern<<<static_cast<unsigned>(grid), (kConsumerWarps + 1) * 32, smem, st>>>(a);
+  kern<<<static_cast<unsigned>(grid), (sh.ncw + 1) * 32, smem, st>>>(a);
   BF_CUDA(cudaGetLastError());
   return 0;
 }

@@ -101,8 +101,11 @@ __device__ __forceinline__ void stage_rows(E* dst, const E* src, uint32_t rows, 
         bulk_g2s(dst + static_cast<size_t>(i) * kc, src + static_cast<size_t>(i) * k, kc * sizeof(E), bar);
     }
   } else {
-    for (uint32_t i = 0; i < rows; ++i)
-      for (uint32_t j = lane; j < kc; j += 32) dst[static_cast<size_t>(i) * kc + j] = src[static_cast<size_t>(i) * k + j];
+    const uint32_t total = rows * kc;
+    for (uint32_t idx = lane; idx < total; idx += 32) {
+      const uint32_t i = kc == 1 ? idx : idx / kc, j = kc == 1 ? 0 : idx - (idx / kc) * kc;
+      dst[idx] = src[static_cast<size_t>(i) * k + j];
+    }
   }
 }
 
@@ -248,7 +251,150 @@ __device__ __forceinline__ void consume_tile(const LevelArgs& a, uint32_t tile, 
   }
 }
 
-template <typename E, int STAGES, int NCW, int MINB>
+// Many-RHS consumer (k >= 8): each unit is a small complex GEMM
+//   forward  Y (nt R x kc) = A (nt R x C) X (C x kc)
+//   adjoint  X (C x kc)    = A^H (C x nt R) Y (nt R x kc)
+// A warp owns (32/LC)*TM output rows x LC*TN right-hand sides; lane (lr, lc)
+// holds a TM x TN register tile whose TN columns are strided by LC, so each
+// operand load of the warp is a contiguous, bank-conflict-free span and the A
+// operand is (nearly) a broadcast. Per inner step: TM + TN shared loads feed
+// 4*TM*TN FP64 FMAs — FMA-pipe bound, not shared-memory bound.
+template <typename E, int TM, int TN, int LC>
+__device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, uint32_t tile, const E* st, int warp, int lane,
+                                                  int nwarps) {
+  using Rl = typename Cx<E>::R;
+  constexpr int LR = 32 / LC;
+  const TileGeo t = tile_geo(a, tile);
+  const uint32_t blk = a.R * a.C;
+  const uint32_t U = 1u << a.lgU;
+  const uint32_t Pe_mask = (1u << t.lgPe) - 1;
+  const E* fs = st;
+  const E* vs = st + static_cast<size_t>(a.nt) * U * blk;
+  E* out = static_cast<E*>(a.out);
+  const uint32_t kc = t.kc;
+  const uint32_t P_mask = (1u << a.lgP) - 1;
+  const uint32_t m_out = a.adjoint ? a.C : a.nt * a.R;
+  const uint32_t nrg = (m_out + LR * TM - 1) / (LR * TM), ncg = (kc + LC * TN - 1) / (LC * TN);
+  const uint32_t items = U * nrg * ncg;
+  const uint32_t lr = lane / LC, lc = lane % LC;
+  for (uint32_t it = warp; it < items; it += nwarps) {
+    const uint32_t cg = it % ncg;
+    const uint32_t rest = it / ncg;
+    const uint32_t rg = rest % nrg, ul = rest / nrg;
+    const uint32_t col0 = cg * LC * TN + lc, row0 = (rg * LR + lr) * TM;
+    const uint32_t base = (((ul >> t.lgPe) * a.nt) << t.lgPe) + (ul & Pe_mask);
+    bool colok[TN];
+#pragma unroll
+    for (int j = 0; j < TN; ++j) colok[j] = col0 + j * LC < kc;
+    Rl re[TM][TN], im[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) re[i][j] = im[i][j] = 0;
+    if (!a.adjoint) {
+      // output row o = tt*R + rho of unit ul reads factor row (slot(ul,tt)*R + rho)
+      const E* arow[TM];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const uint32_t o = min(row0 + i, m_out - 1);
+        const uint32_t tt = o / a.R, rho = o - tt * a.R;
+        arow[i] = fs + (static_cast<size_t>(base + (tt << t.lgPe)) * a.R + rho) * a.C;
+      }
+      const E* x = vs + static_cast<size_t>(ul) * a.C * kc + col0;
+      for (uint32_t c = 0; c < a.C; ++c) {
+        E xv[TN];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) xv[j] = colok[j] ? x[static_cast<size_t>(c) * kc + j * LC] : Cx<E>::make(0, 0);
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          const E av = arow[i][c];
+#pragma unroll
+          for (int j = 0; j < TN; ++j) {
+            re[i][j] = fma(av.x, xv[j].x, re[i][j]);
+            re[i][j] = fma(-av.y, xv[j].y, re[i][j]);
+            im[i][j] = fma(av.x, xv[j].y, im[i][j]);
+            im[i][j] = fma(av.y, xv[j].x, im[i][j]);
+          }
+        }
+      }
+      const uint32_t u = t.u0 + ul;
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const uint32_t o = row0 + i;
+        if (o >= m_out) break;
+        const uint32_t tt = o / a.R, rho = o - tt * a.R;
+        const uint32_t q = ((((u >> a.lgP) * a.nt) + tt) << a.lgP) + (u & P_mask);
+        E* dst = out + (static_cast<size_t>(q) * a.R + rho) * a.k + t.k0 + col0;
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+          if (colok[j]) dst[j * LC] = Cx<E>::make(re[i][j], im[i][j]);
+      }
+    } else {
+      for (uint32_t tt = 0; tt < a.nt; ++tt) {
+        const uint32_t r0 = (base + (tt << t.lgPe)) * a.R;
+        for (uint32_t rho = 0; rho < a.R; ++rho) {
+          const size_t row = static_cast<size_t>(r0 + rho);
+          const E* y = vs + row * kc + col0;
+          E yv[TN];
+#pragma unroll
+          for (int j = 0; j < TN; ++j) yv[j] = colok[j] ? y[j * LC] : Cx<E>::make(0, 0);
+          const E* acol = fs + row * a.C;
+#pragma unroll
+          for (int i = 0; i < TM; ++i) {
+            const E av = acol[min(row0 + i, m_out - 1)];
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {  // conj(av) * yv
+              re[i][j] = fma(av.x, yv[j].x, re[i][j]);
+              re[i][j] = fma(av.y, yv[j].y, re[i][j]);
+              im[i][j] = fma(av.x, yv[j].y, im[i][j]);
+              im[i][j] = fma(-av.y, yv[j].x, im[i][j]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const uint32_t c = row0 + i;
+        if (c >= m_out) break;
+        size_t e = static_cast<size_t>(t.u0 + ul) * a.C + c;
+        Rl w = 1;
+        if (a.remap != 0) {
+          const uint32_t mr = a.m * a.r;
+          const uint32_t ia = static_cast<uint32_t>(e / mr);
+          const uint32_t rem = static_cast<uint32_t>(e - static_cast<size_t>(ia) * mr);
+          const uint32_t ib = rem / a.r, rho = rem - ib * a.r;
+          const size_t dst = (static_cast<size_t>(ib) * a.m + ia) * a.r + rho;
+          const Rl* W = static_cast<const Rl*>(a.mid_w);
+          w = a.remap == 1 ? W[dst] : W[(static_cast<size_t>(ia) * a.m + ib) * a.r + rho];
+          e = dst;
+        }
+        E* dst = out + e * a.k + t.k0 + col0;
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+          if (colok[j]) dst[j * LC] = Cx<E>::make(w * re[i][j], w * im[i][j]);
+      }
+    }
+  }
+}
+
+// Register-tile shapes of the many-RHS consumer, picked by right-hand sides per tile.
+template <typename E>
+__device__ __forceinline__ void consume_tile_mrhs_any(const LevelArgs& a, uint32_t tile, const E* st, int warp,
+                                                      int lane, int nwarps) {
+  if (a.kt >= 128)
+    consume_tile_mrhs<E, 4, 4, 32>(a, tile, st, warp, lane, nwarps);
+  else if (a.kt >= 64)
+    consume_tile_mrhs<E, 8, 2, 32>(a, tile, st, warp, lane, nwarps);
+  else if (a.kt >= 32)
+    consume_tile_mrhs<E, 16, 1, 32>(a, tile, st, warp, lane, nwarps);
+  else if (a.kt >= 16)
+    consume_tile_mrhs<E, 8, 1, 16>(a, tile, st, warp, lane, nwarps);
+  else
+    consume_tile_mrhs<E, 4, 1, 8>(a, tile, st, warp, lane, nwarps);
+}
+
+// MRHS = 0: streaming consumer (one output per thread); MRHS = 1: register-tiled GEMM consumer.
+template <typename E, int STAGES, int NCW, int MINB, int MRHS>
 __global__ void __launch_bounds__((NCW + 1) * 32, MINB) level_kernel(const LevelArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -276,7 +422,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) level_kernel(const Level
     for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
       const uint32_t s = it % STAGES;
       mbar_wait(&full[s], (it / STAGES) & 1);
-      consume_tile<E>(a, tile, stage0 + static_cast<size_t>(s) * a.stage_elems, threadIdx.x, NCW * 32);
+      if (MRHS)
+        consume_tile_mrhs_any<E>(a, tile, stage0 + static_cast<size_t>(s) * a.stage_elems, warp, lane, NCW);
+      else
+        consume_tile<E>(a, tile, stage0 + static_cast<size_t>(s) * a.stage_elems, threadIdx.x, NCW * 32);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }

@@ -135,6 +135,9 @@ def test_per_factor_parity(case):
 @pytest.mark.parametrize("n,leaf,r,k", [
     (1 << 16, 16, 8, 64),     # config 1 geometry (L=12), 64 RHS
     (1 << 12, 0.25, 5, 7),    # merge-only levels, odd rank and odd k
+    (1 << 12, 0.25, 5, 9),    # same through the many-RHS kernel (k >= 8)
+    (1 << 12, 4, 12, 8),      # many-RHS threshold, r=12 (config 0 rank)
+    (1 << 12, 16, 16, 33),    # many-RHS, k not a multiple of the 4-wide register tile
     (1 << 14, 4, 25, 16),     # rank 25 (the 2D configs' rank), 16 RHS
     (1 << 10, 16, 12, 300),   # many RHS: k split across tiles
 ])
