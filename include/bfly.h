@@ -53,6 +53,7 @@ extern "C" {
 /* entry-oracle kernels for bf_entries (kernels.py:23-42; config-1 DFT) */
 #define BF_KERNEL_FIO 0  /* exp(2 pi i (x xi + c(x)|xi|)), x=i/N, xi=j-N/2 (kernels.py:27-38) */
 #define BF_KERNEL_DFTP 1 /* exp(+2 pi i (j k mod N)/N) — BASELINE config 1                   */
+#define BF_KERNEL_DENSE 2 /* explicit n x n complex128 matrix on the device (DenseOracle)    */
 
 typedef struct bf_plan bf_plan;
 
@@ -121,6 +122,46 @@ int bf_timer_read(bf_timer* timer, float* launch_ms, uint32_t* steps, uint32_t* 
  * (kernels.py:34-38) via BlockView (oracles.py:66-68). */
 int bf_entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr,
                const int64_t* cols, uint32_t nc, void* out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Sampling construction (construct.py:43-68, lowrank.py:219-258, construct.py:127-163).
+ *
+ * bf_middle_blocks: randomized sampling SVD of `nblocks` middle-level blocks
+ * of DyadicPartition(n, levels) with rank r and OversamplingParams (q, iters)
+ * — one CTA per block. block_ij: device int32 (nblocks, 2) block coordinates
+ * (i, j); draws: device int32 (nblocks, 2*(iters+1), min(r*q, side)) — the
+ * rng.choice draws of block_rng(seed, 0, i, j) in consumption order (row,
+ * col, row, col, ...; lowrank.py:237-251), made on the host with the
+ * reference's generator; unused (may be NULL) when r*q >= side (dense
+ * branch). dense: device n x n complex128 for BF_KERNEL_DENSE, else NULL.
+ * Outputs (device): u_out, v_out (nblocks, side, r) complex128 = u0*sigma0,
+ * v0*sigma0; w_out (nblocks, r) f64 = floored_inverse(sigma0) — exactly what
+ * construct.py:63-65 scatters into U^h, V^h and M. Requires r*(q+1) <= 64.
+ */
+uint64_t bf_middle_workspace_bytes(uint64_t n, uint32_t levels, uint32_t rank, uint32_t nblocks);
+int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t rank, uint32_t q_over,
+                     uint32_t iters, const void* dense, uint32_t nblocks, const int32_t* block_ij,
+                     const int32_t* draws, void* u_out, void* v_out, double* w_out,
+                     void* workspace, uint64_t ws_bytes, void* stream);
+
+/* One level of _recurse (construct.py:127-163): cur (nb, rows, groups, r)
+ * complex128 -> transfer blocks (nb, 2, groups/2, r, 2r) when rows >= 2 (SVD
+ * of each (rows/2 x 2r) stack; keep = min(r, rows/2)) or (nb, groups/2, r, 2r)
+ * when rows == 1, and the next cur (2nb, rows/2, groups/2, r) or
+ * (nb, 1, groups/2, r). With workspace == NULL, *ws_bytes receives the
+ * scratch size. Requires 2r <= 64. */
+int bf_recurse_level(uint32_t rank, uint64_t nb, uint64_t rows, uint64_t groups, const void* cur,
+                     void* blocks, void* next, void* workspace, uint64_t* ws_bytes, void* stream);
+
+/* Greedy pivoted column selection (select_pivot_columns, lowrank.py:102-129)
+ * on a batch of device matrices a (batch, m, n) complex128 row-major with
+ * m <= 64: up to k picks each, in pick order, into pivots (batch, k) and pick
+ * counts into counts (batch); rel_tol as the reference's. pairwise = 1 sums
+ * the initial column norms in numpy's pairwise order (the reference matrix is
+ * F-ordered), 0 sequentially (C-ordered). Workspace >= 16*batch*m*n bytes. */
+int bf_select_pivots(const void* a, uint32_t batch, uint32_t m, uint32_t n, uint32_t k, double rel_tol,
+                     int pairwise, int32_t* pivots, int32_t* counts, void* workspace,
+                     uint64_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

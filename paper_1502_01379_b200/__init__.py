@@ -8,6 +8,9 @@ through the C ABI of include/bfly.h.
 from ._lib import OracleError
 from .factors import (BlockDiagonalFactor, ButterflyFactors, DevicePlan, MiddleFactor, NnzReport,
                       TransferFactor, factors_equal, from_arrays)
+from .construct import (DEFAULT_PARAMS, OversamplingParams, factorize, middle_factorization_sampling,
+                        recursive_factor_u, recursive_factor_v)
+from .kernels import DenseOracle, DftPlusKernel, FioKernel, fio_entry
 from .partition import BlockId, DyadicPartition, block_cols, block_rows, level_geometry, make_partition
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -1,0 +1,282 @@
+"""Sampling construction of the factor chain on the B200 — the reference's
+``construct.py`` entry point ``factorize`` (same signature, modes, errors),
+with every numeric stage in libbfly.so:
+
+* middle level: ``bf_middle_blocks`` — one CTA per block runs the randomized
+  sampling SVD (lowrank.py:219-258) on entries evaluated on the device;
+* recursion: ``bf_recurse_level`` — batched SVD of the (rows/2 x 2r) stacks
+  (construct.py:127-163).
+
+The host keeps only geometry and the random draws: each block's
+``rng.choice`` draws come from the reference's own generator
+``SeedSequence(seed, spawn_key=(0, i, j))`` (construct.py:31-33), which makes
+them identical to the reference's and independent of the schedule — so
+"sampling" and "streaming" produce bitwise-identical factors, as in the
+reference (pkg/tests/test_construct.py:197-202).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from concurrent.futures import ProcessPoolExecutor
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .factors import BlockDiagonalFactor, ButterflyFactors, MiddleFactor, TransferFactor
+from .kernels import is_entry_oracle, is_operator_oracle
+from .partition import DyadicPartition, level_geometry
+
+SAMPLING_DOMAIN = 0  # construct.py:26
+
+
+@dataclass(frozen=True)
+class OversamplingParams:
+    """p extra probe columns, q sample multiplier, iters skeleton sweeps (lowrank.py:33-48)."""
+
+    p: int = 5
+    q: int = 3
+    iters: int = 3
+
+    def __post_init__(self):
+        if self.p < 0 or self.q < 1 or self.iters < 1:
+            raise ValueError(f"invalid oversampling parameters {self}")
+
+
+DEFAULT_PARAMS = OversamplingParams()
+
+
+def block_rng(seed, *key) -> np.random.Generator:
+    """Independent generator for one construction sub-task (construct.py:31-33)."""
+    return np.random.default_rng(np.random.SeedSequence(seed, spawn_key=key))
+
+
+def _draws_for(args):
+    seed, side, rqs, iters, blocks = args
+    out = np.empty((len(blocks), 2 * (iters + 1), rqs), dtype=np.int32)
+    for b, (i, j) in enumerate(blocks):
+        rng = block_rng(seed, SAMPLING_DOMAIN, int(i), int(j))
+        for s in range(2 * (iters + 1)):  # row, col, row, col, ... (lowrank.py:237-251)
+            out[b, s] = rng.choice(side, size=rqs, replace=False)
+    return out
+
+
+def draw_tables(seed, side: int, r: int, params: OversamplingParams, blocks) -> np.ndarray:
+    """The reference's per-block rng.choice draws, in consumption order."""
+    rqs = min(r * params.q, side)
+    blocks = list(blocks)
+    if len(blocks) < 2048:
+        return _draws_for((seed, side, rqs, params.iters, blocks))
+    workers = min(16, os.cpu_count() or 1)
+    chunks = [blocks[k::workers] for k in range(workers)]
+    with ProcessPoolExecutor(workers) as ex:
+        parts = list(ex.map(_draws_for, [(seed, side, rqs, params.iters, c) for c in chunks]))
+    out = np.empty((len(blocks), 2 * (params.iters + 1), rqs), dtype=np.int32)
+    for k, part in enumerate(parts):
+        out[k::workers] = part
+    return out
+
+
+class _DeviceOracle:
+    """What the device needs to evaluate an entry oracle: a kernel id (+ matrix)."""
+
+    def __init__(self, oracle, n):
+        torch = _lib.require_cuda()
+        self.dense = None
+        kid = getattr(oracle, "kernel_id", None)
+        name = type(oracle).__name__
+        if kid in (_lib.BF_KERNEL_FIO, _lib.BF_KERNEL_DFTP):
+            self.kernel_id = kid
+        elif name == "FioKernel" and getattr(oracle, "n", None) == n:   # the reference's own class
+            self.kernel_id = _lib.BF_KERNEL_FIO
+        else:
+            # explicit matrix (DenseOracle) or any other entry oracle, materialised once
+            mat = getattr(oracle, "matrix", None)
+            if mat is None:
+                idx = np.arange(n)
+                mat = oracle.block(idx, idx)
+            self.dense = torch.as_tensor(np.ascontiguousarray(mat, dtype=np.complex128)).cuda()
+            self.kernel_id = _lib.BF_KERNEL_DENSE
+
+
+class MiddleSampler:
+    """Batched middle-level blocks on the device (construct.py:43-68)."""
+
+    def __init__(self, oracle, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0):
+        self.torch = _lib.require_cuda()
+        self.lib = _lib.load()
+        self.p, self.r, self.params, self.seed = p, r, params, seed
+        self.m, self.side = p.mid_nodes, p.mid_side
+        if self.side < r:
+            raise ValueError(f"middle blocks are {self.side} wide, below rank {r}")
+        self.dev = _DeviceOracle(oracle, p.n)
+        self.dense_branch = r * params.q >= self.side
+
+    def blocks(self, ij):
+        """(u0*sigma0, v0*sigma0, floored_inverse(sigma0)) for blocks ij, on the device."""
+        torch = self.torch
+        ij = np.asarray(ij, dtype=np.int32).reshape(-1, 2)
+        nb = ij.shape[0]
+        side, r = self.side, self.r
+        u = torch.empty((nb, side, r), dtype=torch.complex128, device="cuda")
+        v = torch.empty_like(u)
+        w = torch.empty((nb, r), dtype=torch.float64, device="cuda")
+        ij_d = torch.from_numpy(np.ascontiguousarray(ij)).cuda()
+        if self.dense_branch:
+            draws_d = None
+        else:
+            draws_d = torch.from_numpy(draw_tables(self.seed, side, r, self.params, ij.tolist())).cuda()
+        wsb = int(self.lib.bf_middle_workspace_bytes(self.p.n, self.p.levels, r, nb))
+        ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+        dense = ctypes.c_void_p(self.dev.dense.data_ptr()) if self.dev.dense is not None else None
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        rc = self.lib.bf_middle_blocks(self.dev.kernel_id, self.p.n, self.p.levels, r, self.params.q,
+                                       self.params.iters, dense, nb, ctypes.c_void_p(ij_d.data_ptr()),
+                                       ctypes.c_void_p(draws_d.data_ptr()) if draws_d is not None else None,
+                                       ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(v.data_ptr()),
+                                       ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(ws.data_ptr()), wsb, stream)
+        if rc != _lib.BF_OK:
+            msg = _lib.last_error()
+            if rc == _lib.BF_EINVAL:
+                raise ValueError(msg)
+            raise _lib.OracleError(f"entry oracle failed on middle blocks {ij[:1].tolist()}...: {msg}")
+        return u, v, w
+
+    def batch_rows(self) -> int:
+        """Block-rows per launch: enough CTAs to fill the GPU, bounded workspace."""
+        per_block = max(1, int(self.lib.bf_middle_workspace_bytes(self.p.n, self.p.levels, self.r, 1)))
+        by_mem = max(1, (4 << 30) // (per_block * self.m))
+        return max(1, min(self.m, max(1, 592 // self.m), by_mem))
+
+
+def recurse(cur, p: DyadicPartition, r: int):
+    """_recurse (construct.py:127-163) on a device stack (nodes, rows, groups, r)."""
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    pieces = []
+    cur = cur.contiguous()
+    for lvl in range(p.half, p.levels):
+        nb, rows, groups, _ = cur.shape
+        pairs = groups // 2
+        if rows >= 2:
+            blocks = torch.empty((nb, 2, pairs, r, 2 * r), dtype=torch.complex128, device="cuda")
+            nxt = torch.empty((2 * nb, rows // 2, pairs, r), dtype=torch.complex128, device="cuda")
+        else:
+            blocks = torch.empty((nb, pairs, r, 2 * r), dtype=torch.complex128, device="cuda")
+            nxt = torch.empty((nb, 1, pairs, r), dtype=torch.complex128, device="cuda")
+        need = ctypes.c_uint64(0)
+        _lib.check(lib.bf_recurse_level(r, nb, rows, groups, None, None, None, None, ctypes.byref(need), stream))
+        ws = torch.empty(max(int(need.value), 16), dtype=torch.uint8, device="cuda")
+        _lib.check(lib.bf_recurse_level(r, nb, rows, groups, ctypes.c_void_p(cur.data_ptr()),
+                                        ctypes.c_void_p(blocks.data_ptr()), ctypes.c_void_p(nxt.data_ptr()),
+                                        ctypes.c_void_p(ws.data_ptr()), ctypes.byref(need), stream),
+                   "bf_recurse_level")
+        pieces.append((lvl, blocks))
+        cur = nxt
+    return cur[:, :, 0, :].contiguous(), pieces
+
+
+def recursive_factor_u(u_h: BlockDiagonalFactor, p: DyadicPartition, r: int):
+    """Expand the middle left factor into leaf factor + transfer chain (construct.py:171-176)."""
+    torch = _lib.require_cuda()
+    blocks = u_h.blocks if hasattr(u_h.blocks, "data_ptr") else torch.as_tensor(np.asarray(u_h.blocks)).cuda()
+    cur = blocks.to(torch.complex128).reshape(p.mid_nodes, p.mid_side, p.mid_nodes, r)
+    leaf, pieces = recurse(cur, p, r)
+    return BlockDiagonalFactor(leaf), tuple(TransferFactor(lvl, b) for lvl, b in pieces)
+
+
+def recursive_factor_v(v_h: BlockDiagonalFactor, p: DyadicPartition, r: int):
+    """Same expansion for the right factor (construct.py:179-181)."""
+    return recursive_factor_u(v_h, p, r)
+
+
+def middle_factorization_sampling(entry, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0):
+    """U^h, M, V^h of the sampling construction (construct.py:53-68), device tensors."""
+    torch = _lib.require_cuda()
+    ms = MiddleSampler(entry, p, r, params, seed)
+    m, side = ms.m, ms.side
+    u = torch.zeros((m, side, m, r), dtype=torch.complex128, device="cuda")
+    v = torch.zeros_like(u)
+    w = torch.zeros((m, m, r), dtype=torch.float64, device="cuda")
+    step = ms.batch_rows()
+    for i0 in range(0, m, step):
+        rows = range(i0, min(m, i0 + step))
+        uu, vv, ww = ms.blocks([(i, j) for i in rows for j in range(m)])
+        k = len(rows)
+        u[i0:i0 + k] = uu.reshape(k, m, side, r).permute(0, 2, 1, 3)      # u[i, :, j, :]
+        v[:, :, i0:i0 + k, :] = vv.reshape(k, m, side, r).permute(1, 2, 0, 3)  # v[j, :, i, :]
+        w[i0:i0 + k] = ww.reshape(k, m, r)
+    return (BlockDiagonalFactor(u.reshape(m, side, m * r)), MiddleFactor(w),
+            BlockDiagonalFactor(v.reshape(m, side, m * r)))
+
+
+def _place(chain, leaf, k, leaf_k, pieces):
+    for lvl, blocks in pieces:
+        nb = blocks.shape[0]
+        chain[lvl][k * nb:(k + 1) * nb] = blocks
+    nb = leaf_k.shape[0]
+    leaf[k * nb:(k + 1) * nb] = leaf_k
+
+
+def factorize(oracle, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0,
+              mode="sampling") -> ButterflyFactors:
+    """Build the full sparse chain for the operator behind ``oracle`` (construct.py:184-213).
+
+    mode="sampling"   entry oracle; every middle block sampled once (V^h held on the device);
+    mode="streaming"  entry oracle; one middle block row/column at a time, O(n log n) memory,
+                      each block sampled twice — bitwise identical to "sampling";
+    mode="matvec"     operator-oracle construction: not part of this hot path.
+    """
+    if params is None:
+        params = DEFAULT_PARAMS
+    if r < 1:
+        raise ValueError(f"rank must be positive, got {r}")
+    if mode in ("sampling", "streaming") and not is_entry_oracle(oracle):
+        raise ValueError(f"mode={mode!r} needs an entry oracle")
+    if mode == "matvec":
+        if not is_operator_oracle(oracle):
+            raise ValueError("mode='matvec' needs an operator oracle")
+        raise NotImplementedError("mode='matvec' (probe construction) is outside the B200 hot path; "
+                                  "see DESIGN.md 'Out of scope'")
+    if mode not in ("sampling", "streaming"):
+        raise ValueError(f"unknown mode {mode!r}")
+    torch = _lib.require_cuda()
+    ms = MiddleSampler(oracle, p, r, params, seed)
+    m, side = ms.m, ms.side
+    shapes, leaf_shape = level_geometry(p, r)
+    weights = torch.zeros((m, m, r), dtype=torch.float64, device="cuda")
+    sides = []
+    v_full = None
+    if mode == "sampling":
+        v_full = torch.zeros((m, side, m, r), dtype=torch.complex128, device="cuda")
+    for axis in ("u", "v"):
+        chain = {lvl: torch.zeros(shape, dtype=torch.complex128, device="cuda") for lvl, _, shape in shapes}
+        leaf = torch.zeros(leaf_shape, dtype=torch.complex128, device="cuda")
+        if axis == "v" and mode == "sampling":
+            for k in range(m):
+                leaf_k, pieces = recurse(v_full[k:k + 1], p, r)
+                _place(chain, leaf, k, leaf_k, pieces)
+        else:
+            step = ms.batch_rows()
+            for k0 in range(0, m, step):
+                ks = range(k0, min(m, k0 + step))
+                ij = [((k, o) if axis == "u" else (o, k)) for k in ks for o in range(m)]
+                uu, vv, ww = ms.blocks(ij)
+                for idx, k in enumerate(ks):
+                    sl = slice(idx * m, (idx + 1) * m)
+                    if axis == "u":
+                        slab = uu[sl].permute(1, 0, 2).reshape(1, side, m, r)      # slab[0, :, j, :]
+                        weights[k] = ww[sl]
+                        if v_full is not None:
+                            v_full[:, :, k, :] = vv[sl]                            # v[j, :, i=k, :]
+                    else:
+                        slab = vv[sl].permute(1, 0, 2).reshape(1, side, m, r)      # slab[0, :, i, :]
+                    leaf_k, pieces = recurse(slab, p, r)
+                    _place(chain, leaf, k, leaf_k, pieces)
+        sides.append((BlockDiagonalFactor(leaf), tuple(TransferFactor(lvl, chain[lvl]) for lvl, _, _ in shapes)))
+    del v_full
+    (u_outer, g_chain), (v_outer, h_chain) = sides
+    return ButterflyFactors(p, r, u_outer, g_chain, MiddleFactor(weights), h_chain, v_outer)

@@ -360,7 +360,7 @@ int bf_apply_factor(const bf_plan* plan, int which, uint32_t level, int adjoint,
 int bf_entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr, const int64_t* cols, uint32_t nc,
                void* out, void* stream) {
   if (n < 1) return fail(BF_EINVAL, "n must be positive");
-  if ((nr && !rows) || (nc && !cols) || (static_cast<uint64_t>(nr) * nc && !out))
+  if ((nr && !rows) || (nc && !cols) || (static_cast<uint64_t>(nr) * nc != 0 && !out))
     return fail(BF_EINVAL, "null pointer");
   return entries(kernel_id, n, rows, nr, cols, nc, out, static_cast<cudaStream_t>(stream));
 }

@@ -1,0 +1,880 @@
+// construct.cu — the sampling construction on B200: batched randomized
+// sampling SVD of middle-level blocks (lowrank.py:219-258 via
+// construct.py:43-68) and the recursive block SVDs (construct.py:127-163).
+//
+// One CTA owns one middle block (or one recursion problem). The random draws
+// of every block are made on the host with the reference's own generator
+// (SeedSequence(seed, spawn_key=(0, i, j)), construct.py:31-33) and uploaded
+// as tables: the draws never depend on pivot results, so
+// the device consumes exactly the index sets the reference would.
+//
+// Stage kernels, per sweep s of `iters`:
+//   k_union      rows = union1d(draw, skeleton)             (lowrank.py:280-281)
+//   k_fill_wide  K(rows, :) or K(:, cols)^H  ->  (|set| x side)
+//   k_pivot_wide greedy pivoted Gram-Schmidt, r picks       (lowrank.py:102-129)
+// then the bases (k_fill_tall, k_pivot_tall, k_fill_sel, k_cgs2 — lowrank.py:
+// 132-154), the floored least-squares middle matrix and its SVD (k_mid,
+// lowrank.py:90-94, 257, 284-293) and the scaled factors (k_assemble).
+#include <algorithm>
+#include <vector>
+
+#include "entry_eval.cuh"
+#include "linalg.cuh"
+#include "plan.h"
+
+namespace bfly {
+
+constexpr int kMaxSet = 64;  // |rows|, |cols| <= r*q + r (r <= 16 at q = 3)
+
+struct BlockState {
+  int64_t r0, c0;
+  int32_t nrows, ncols, nskr, nskc, tc, tr, t, pad;
+  int32_t rows[kMaxSet], cols[kMaxSet];
+  int32_t skr[kMaxSet], skc[kMaxSet];
+  int32_t pivc[kMaxSet], pivr[kMaxSet];
+};
+
+struct MidArgs {
+  EntrySrc src;
+  int64_t side;
+  int r, rqs, iters, nblocks;
+  BlockState* st;
+  const int32_t* draws;   // (nblocks, 2*(iters+1), rqs)
+  double2* wide;          // (nblocks, S, side)
+  double2* tall;          // (nblocks, S, side)  column-major side x S
+  double2* qc;            // (nblocks, S, side)
+  double2* qr;            // (nblocks, S, side)
+  double2* qbuf;          // (nblocks, side)
+  double2* scr;           // (nblocks, 6, S, S) small-matrix scratch
+  double* sig;            // (nblocks, S)
+  double2* u_out;         // (nblocks, side, r)  u0 * sigma0
+  double2* v_out;         // (nblocks, side, r)  v0 * sigma0
+  double* w_out;          // (nblocks, r)        floored_inverse(sigma0)
+};
+
+enum { kRows = 0, kCols = 1 };
+
+__global__ void k_init(MidArgs a, const int32_t* ij) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.nblocks) return;
+  BlockState& s = a.st[b];
+  s.r0 = static_cast<int64_t>(ij[2 * b]) * a.side;
+  s.c0 = static_cast<int64_t>(ij[2 * b + 1]) * a.side;
+  s.nrows = s.ncols = s.nskr = s.nskc = s.tc = s.tr = s.t = 0;
+}
+
+// set = sorted unique(draw[slot] U skeleton)  (np.union1d)
+__global__ void k_union(MidArgs a, int slot, int which) {
+  BlockState& s = a.st[blockIdx.x];
+  __shared__ int32_t vals[2 * kMaxSet];
+  const int32_t* d = a.draws + (static_cast<int64_t>(blockIdx.x) * 2 * (a.iters + 1) + slot) * a.rqs;
+  const int nsk = which == kRows ? s.nskr : s.nskc;
+  const int32_t* sk = which == kRows ? s.skr : s.skc;
+  const int tot = a.rqs + nsk;
+  for (int i = threadIdx.x; i < tot; i += blockDim.x) vals[i] = i < a.rqs ? d[i] : sk[i - a.rqs];
+  __syncthreads();
+  int32_t* out = which == kRows ? s.rows : s.cols;
+  for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+    const int32_t v = vals[i];
+    bool dup = false;
+    int rank = 0;
+    for (int k = 0; k < tot; ++k) {
+      const int32_t w = vals[k];
+      if (w == v && k < i) dup = true;
+      // distinct values smaller than v: count each value once (its first occurrence)
+      if (w < v) {
+        bool first = true;
+        for (int q = 0; q < k; ++q) first &= vals[q] != w;
+        rank += first;
+      }
+    }
+    if (!dup) out[rank] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int cnt = 0;
+    for (int i = 0; i < tot; ++i) {
+      bool first = true;
+      for (int q = 0; q < i; ++q) first &= vals[q] != vals[i];
+      cnt += first;
+    }
+    if (which == kRows)
+      s.nrows = cnt;
+    else
+      s.ncols = cnt;
+  }
+}
+
+// rows mode: W[a][c] = K(r0 + rows[a], c0 + c)            (entry(rows, all))
+// cols mode: W[a][c] = conj(K(r0 + c, c0 + cols[a]))      (entry(all, cols)^H)
+__global__ void k_fill_wide(MidArgs a, int which) {
+  const BlockState& s = a.st[blockIdx.x];
+  const int nr = which == kRows ? s.nrows : s.ncols;
+  double2* W = a.wide + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  const int64_t total = nr * a.side;
+  for (int64_t x = blockIdx.y * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<int64_t>(gridDim.y) * blockDim.x) {
+    const int ai = static_cast<int>(x / a.side);
+    const int64_t c = x - ai * a.side;
+    W[x] = which == kRows ? entry_eval(a.src, s.r0 + s.rows[ai], s.c0 + c)
+                          : cconj(entry_eval(a.src, s.r0 + c, s.c0 + s.cols[ai]));
+  }
+}
+
+// Greedy column pivoting (select_pivot_columns, lowrank.py:102-129) on W
+// (nr x ncols, row-major, nr <= kMaxSet), k picks, CTA-cooperative. Initial
+// norms sum over rows in the reference's order: sequential when the
+// reference's matrix is C-ordered, numpy pairwise when it is F-ordered.
+// Residual norms are downdated, never recomputed; ties within 2*PIVOT_TIE
+// go to the lowest index. Returns the pick count; picks in pick order.
+// Shared: norms (ncols doubles), q (kMaxSet), red (32 doubles), redi (32 ints).
+__device__ int pivot_rows_core(double2* W, int nr, int ncols, int k, double rel_tol, bool pairwise, double* norms,
+                               double2* q, double* red, int* redi, int* picks) {
+  for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+    auto get = [&](int i) { return abs2(W[static_cast<int64_t>(i) * ncols + c]); };
+    norms[c] = pairwise ? pairwise_sum(get, 0, nr) : sequential_sum(get, nr);
+  }
+  __syncthreads();
+  k = min(k, min(nr, ncols));
+  double lm0 = 0.0;
+  for (int c = threadIdx.x; c < ncols; c += blockDim.x) lm0 = fmax(lm0, norms[c]);
+  const double floor_v = rel_tol * rel_tol * block_max(lm0, red);
+  int npick = 0;
+  for (int it = 0; it < k; ++it) {
+    double lm = 0.0;
+    for (int c = threadIdx.x; c < ncols; c += blockDim.x) lm = fmax(lm, norms[c]);
+    const double best = block_max(lm, red);
+    if (best <= floor_v || best <= 0.0) break;
+    const double thr = __dmul_rn(best, 1.0 - 2.0 * kPivotTie);
+    int li = INT_MAX;
+    for (int c = threadIdx.x; c < ncols; c += blockDim.x)
+      if (norms[c] >= thr) li = min(li, c);
+    const int j = block_min_int(li, redi);
+    const double sq = sqrt(norms[j]);
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+      const double2 w = W[static_cast<int64_t>(i) * ncols + j];
+      q[i] = make_double2(__ddiv_rn(w.x, sq), __ddiv_rn(w.y, sq));
+    }
+    if (threadIdx.x == 0) picks[npick] = j;
+    ++npick;
+    __syncthreads();
+    for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+      double2 pr = make_double2(0, 0);
+      for (int i = 0; i < nr; ++i) {
+        const double2 g = cmulc(q[i], W[static_cast<int64_t>(i) * ncols + c]);
+        pr.x += g.x;
+        pr.y += g.y;
+      }
+      for (int i = 0; i < nr; ++i) {
+        double2& w = W[static_cast<int64_t>(i) * ncols + c];
+        const double2 d = cmul(q[i], pr);
+        w.x -= d.x;
+        w.y -= d.y;
+      }
+      norms[c] = fmax(__dsub_rn(norms[c], abs2(pr)), 0.0);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) norms[j] = 0.0;
+    __syncthreads();
+  }
+  return npick;
+}
+
+// Sweep pivots: rows mode picks columns of K(rows, :) -> column skeleton;
+// cols mode picks columns of K(:, cols)^H -> row skeleton (lowrank.py:237-243).
+__global__ void k_pivot_wide(MidArgs a, int which) {
+  extern __shared__ double smem_d[];
+  double* norms = smem_d;                                       // side
+  double2* q = reinterpret_cast<double2*>(norms + a.side);      // kMaxSet
+  double* red = reinterpret_cast<double*>(q + kMaxSet);         // 32
+  int* redi = reinterpret_cast<int*>(red + 32);                 // 32
+  int* picks = redi + 32;                                       // kMaxSet
+  BlockState& s = a.st[blockIdx.x];
+  const int nr = which == kRows ? s.nrows : s.ncols;
+  double2* W = a.wide + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  const int npick = pivot_rows_core(W, nr, static_cast<int>(a.side), a.r, 0.0, which == kCols, norms, q, red, redi,
+                                    picks);
+  // skeleton = sorted(picks)
+  if (threadIdx.x == 0) {
+    int32_t* sk = which == kRows ? s.skc : s.skr;
+    for (int i = 0; i < npick; ++i) {
+      int rank = 0;
+      for (int m = 0; m < npick; ++m) rank += picks[m] < picks[i];
+      sk[rank] = picks[i];
+    }
+    if (which == kRows)
+      s.nskc = npick;
+    else
+      s.nskr = npick;
+  }
+}
+
+// Standalone batched pivot selection (bf_select_pivots): matrices (batch, m, n)
+// complex128 row-major, m <= kMaxSet, copied to scratch then pivoted in place.
+__global__ void k_select_pivots(const double2* A, double2* scratch, int m, int n, int k, double rel_tol, int pairwise,
+                                int32_t* pivots, int32_t* counts) {
+  extern __shared__ double smem_d[];
+  double* norms = smem_d;
+  double2* q = reinterpret_cast<double2*>(norms + n + (n & 1));
+  double* red = reinterpret_cast<double*>(q + kMaxSet);
+  int* redi = reinterpret_cast<int*>(red + 32);
+  int* picks = redi + 32;
+  const int64_t off = static_cast<int64_t>(blockIdx.x) * m * n;
+  for (int64_t x = threadIdx.x; x < static_cast<int64_t>(m) * n; x += blockDim.x) scratch[off + x] = A[off + x];
+  __syncthreads();
+  const int np = pivot_rows_core(scratch + off, m, n, k, rel_tol, pairwise != 0, norms, q, red, redi, picks);
+  for (int i = threadIdx.x; i < np; i += blockDim.x) pivots[static_cast<int64_t>(blockIdx.x) * k + i] = picks[i];
+  if (threadIdx.x == 0) counts[blockIdx.x] = np;
+}
+
+// Tall column-major fill: column p of T (side rows) is
+//   cols mode: K(r0 + :, c0 + cols[sel(p)])           (entry(all, cols))
+//   rows mode: conj(K(r0 + rows[sel(p)], c0 + :))     (entry(rows, all)^H)
+// with sel = identity (ncols/nrows columns) or the basis pivots (tc/tr columns).
+__global__ void k_fill_tall(MidArgs a, int which, int use_piv, double2* dst_base) {
+  const BlockState& s = a.st[blockIdx.x];
+  const int ncol = use_piv ? (which == kCols ? s.tc : s.tr) : (which == kCols ? s.ncols : s.nrows);
+  double2* T = dst_base + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  const int64_t total = ncol * a.side;
+  for (int64_t x = blockIdx.y * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<int64_t>(gridDim.y) * blockDim.x) {
+    const int p = static_cast<int>(x / a.side);
+    const int64_t i = x - p * a.side;
+    const int sel = use_piv ? (which == kCols ? s.pivc[p] : s.pivr[p]) : p;
+    T[x] = which == kCols ? entry_eval(a.src, s.r0 + i, s.c0 + s.cols[sel])
+                          : cconj(entry_eval(a.src, s.r0 + s.rows[sel], s.c0 + i));
+  }
+}
+
+// Greedy pivoting on the tall T (side x nc, column-major), up to kmax picks,
+// rel_tol = BASIS_TRIM; pick order kept (orthonormal_columns, lowrank.py:132-154).
+__global__ void k_pivot_tall(MidArgs a, int which) {
+  __shared__ double norms[kMaxSet];
+  __shared__ int picks[kMaxSet];
+  __shared__ int s_j, s_stop;
+  __shared__ double s_sq;
+  BlockState& s = a.st[blockIdx.x];
+  const int nc = which == kCols ? s.ncols : s.nrows;
+  const int side = static_cast<int>(a.side);
+  double2* T = a.tall + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  double2* q = a.qbuf + static_cast<int64_t>(blockIdx.x) * a.side;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+    const double2* col = T + static_cast<int64_t>(c) * side;
+    auto get = [&](int i) { return abs2(col[i]); };
+    norms[c] = which == kCols ? sequential_sum(get, side) : pairwise_sum(get, 0, side);
+  }
+  __syncthreads();
+  const int width = max(a.r, min(s.nrows, s.ncols) - a.r);
+  const int kmax = min(min(width, side), min(side, nc));
+  double mx0 = 0.0;
+  for (int c = 0; c < nc; ++c) mx0 = fmax(mx0, norms[c]);
+  const double floor_v = kBasisTrim * kBasisTrim * mx0;
+  int npick = 0;
+  for (int it = 0; it < kmax; ++it) {
+    if (threadIdx.x == 0) {
+      double best = 0.0;
+      for (int c = 0; c < nc; ++c) best = fmax(best, norms[c]);
+      s_stop = (best <= floor_v || best <= 0.0);
+      if (!s_stop) {
+        const double thr = __dmul_rn(best, 1.0 - 2.0 * kPivotTie);
+        int j = 0;
+        while (norms[j] < thr) ++j;
+        s_j = j;
+        s_sq = sqrt(norms[j]);
+        picks[npick] = j;
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;
+    const int j = s_j;
+    const double sq = s_sq;
+    const double2* cj = T + static_cast<int64_t>(j) * side;
+    for (int i = threadIdx.x; i < side; i += blockDim.x)
+      q[i] = make_double2(__ddiv_rn(cj[i].x, sq), __ddiv_rn(cj[i].y, sq));
+    ++npick;
+    __syncthreads();
+    for (int c = warp; c < nc; c += nw) {
+      double2* col = T + static_cast<int64_t>(c) * side;
+      double2 pr = make_double2(0, 0);
+      for (int i = lane; i < side; i += 32) {
+        const double2 g = cmulc(q[i], col[i]);
+        pr.x += g.x;
+        pr.y += g.y;
+      }
+      pr = warp_sum2(pr);
+      for (int i = lane; i < side; i += 32) {
+        const double2 d = cmul(q[i], pr);
+        col[i].x -= d.x;
+        col[i].y -= d.y;
+      }
+      if (lane == 0) norms[c] = fmax(__dsub_rn(norms[c], abs2(pr)), 0.0);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) norms[j] = 0.0;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int32_t* piv = which == kCols ? s.pivc : s.pivr;
+    for (int i = 0; i < npick; ++i) piv[i] = picks[i];
+    if (which == kCols)
+      s.tc = npick;
+    else
+      s.tr = npick;
+  }
+}
+
+// Classical Gram-Schmidt, two passes: an orthonormal basis of the selected
+// columns (the reference uses np.linalg.qr; only span(Q) reaches the factors,
+// see DESIGN.md "Construction parity").
+__global__ void k_cgs2(MidArgs a, int which) {
+  __shared__ double2 coef[kMaxSet];
+  __shared__ double red[32];
+  const BlockState& s = a.st[blockIdx.x];
+  const int t = which == kCols ? s.tc : s.tr;
+  const int side = static_cast<int>(a.side);
+  double2* Q = (which == kCols ? a.qc : a.qr) + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int p = 0; p < t; ++p) {
+    double2* x = Q + static_cast<int64_t>(p) * side;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int l = warp; l < p; l += nw) {
+        const double2* ql = Q + static_cast<int64_t>(l) * side;
+        double2 acc = make_double2(0, 0);
+        for (int i = lane; i < side; i += 32) {
+          const double2 g = cmulc(ql[i], x[i]);
+          acc.x += g.x;
+          acc.y += g.y;
+        }
+        acc = warp_sum2(acc);
+        if (lane == 0) coef[l] = acc;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < side; i += blockDim.x) {
+        double2 v = x[i];
+        for (int l = 0; l < p; ++l) {
+          const double2 d = cmul(Q[static_cast<int64_t>(l) * side + i], coef[l]);
+          v.x -= d.x;
+          v.y -= d.y;
+        }
+        x[i] = v;
+      }
+      __syncthreads();
+    }
+    double part = 0;
+    for (int i = threadIdx.x; i < side; i += blockDim.x) part += x[i].x * x[i].x + x[i].y * x[i].y;
+    const double nrm = sqrt(block_sum(part, red));
+    const double inv = nrm > 0 ? 1.0 / nrm : 0.0;
+    for (int i = threadIdx.x; i < side; i += blockDim.x) x[i] = make_double2(x[i].x * inv, x[i].y * inv);
+    __syncthreads();
+  }
+}
+
+// pinv_floored (lowrank.py:90-94) of M (m x n, shared) into P (n x m, global, row-major).
+__device__ void pinv_small(const double2* M, int m, int n, int ld, double2* P, double2* U, double2* V, double* sig,
+                           double2* W, double2* Vt, int* flag, int* perm, double* ssc) {
+  svd_small(M, m, n, ld, U, kMaxSet, V, kMaxSet, sig, W, Vt, flag, perm, ssc);
+  const int sn = min(m, n);
+  double smax = 0;
+  for (int k = 0; k < sn; ++k) smax = fmax(smax, sig[k]);
+  // P = V diag(finv) U^H  : P[c][a] = sum_k V[c][k] finv_k conj(U[a][k])
+  for (int x = threadIdx.x; x < n * m; x += blockDim.x) {
+    const int c = x / m, aa = x % m;
+    double2 acc = make_double2(0, 0);
+    for (int k = 0; k < sn; ++k) {
+      const double fi = floored_inv(sig[k], smax);
+      if (fi == 0.0) continue;
+      const double2 g = cmul(V[c * kMaxSet + k], cconj(U[aa * kMaxSet + k]));
+      acc.x += fi * g.x;
+      acc.y += fi * g.y;
+    }
+    P[c * kMaxSet + aa] = acc;
+  }
+  __syncthreads();
+}
+
+// mid = pinv(qc[rows, :tc]) @ K(rows, cols) @ pinv(qr[cols, :tr]^H); SVD(mid)
+// (lowrank.py:257, 284-293). Results: U_M (tc x s) in scr[4], V_M (tr x s) in
+// scr[5], sigma in sig, kept rank t = min(r, s) in state.
+__global__ void k_mid(MidArgs a) {
+  extern __shared__ double2 sm2[];
+  double2* Mb = sm2;                       // 64 x 64
+  double2* W = Mb + kMaxSet * kMaxSet;     // 64 x 64
+  double2* Vt = W + kMaxSet * kMaxSet;     // 64 x 64
+  __shared__ int flag, perm[kMaxSet];
+  __shared__ double ssc[kMaxSet], sg[kMaxSet];
+  BlockState& s = a.st[blockIdx.x];
+  const int side = static_cast<int>(a.side);
+  const int nrw = s.nrows, ncl = s.ncols, tc = s.tc, tr = s.tr;
+  double2* scr = a.scr + static_cast<int64_t>(blockIdx.x) * 6 * kMaxSet * kMaxSet;
+  double2* sU = scr;                          // svd scratch U
+  double2* sV = scr + 1 * kMaxSet * kMaxSet;  // svd scratch V
+  double2* P1 = scr + 2 * kMaxSet * kMaxSet;  // tc x nrows, later T1 = P1 Er (tc x ncols)
+  double2* P2 = scr + 3 * kMaxSet * kMaxSet;  // ncols x tr
+  double2* UM = scr + 4 * kMaxSet * kMaxSet;
+  double2* VM = scr + 5 * kMaxSet * kMaxSet;
+  const double2* QC = a.qc + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  const double2* QR = a.qr + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  if (tc == 0 || tr == 0) {
+    if (threadIdx.x == 0) s.t = 0;
+    return;
+  }
+  // P1 = pinv(qc[rows, :])
+  for (int x = threadIdx.x; x < nrw * tc; x += blockDim.x) {
+    const int i = x / tc, l = x % tc;
+    Mb[i * kMaxSet + l] = QC[static_cast<int64_t>(l) * side + s.rows[i]];
+  }
+  __syncthreads();
+  pinv_small(Mb, nrw, tc, kMaxSet, P1, sU, sV, sg, W, Vt, &flag, perm, ssc);
+  // P2 = pinv(qr[cols, :]^H)   (tr x ncols) -> (ncols x tr)
+  for (int x = threadIdx.x; x < tr * ncl; x += blockDim.x) {
+    const int l = x / ncl, c = x % ncl;
+    Mb[l * kMaxSet + c] = cconj(QR[static_cast<int64_t>(l) * side + s.cols[c]]);
+  }
+  __syncthreads();
+  pinv_small(Mb, tr, ncl, kMaxSet, P2, sU, sV, sg, W, Vt, &flag, perm, ssc);
+  // Er = K(rows, cols) into Mb ; T1 = P1 @ Er (tc x ncols) into W
+  for (int x = threadIdx.x; x < nrw * ncl; x += blockDim.x) {
+    const int i = x / ncl, c = x % ncl;
+    Mb[i * kMaxSet + c] = entry_eval(a.src, s.r0 + s.rows[i], s.c0 + s.cols[c]);
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < tc * ncl; x += blockDim.x) {
+    const int l = x / ncl, c = x % ncl;
+    double2 acc = make_double2(0, 0);
+    for (int i = 0; i < nrw; ++i) {
+      const double2 g = cmul(P1[l * kMaxSet + i], Mb[i * kMaxSet + c]);
+      acc.x += g.x;
+      acc.y += g.y;
+    }
+    W[l * kMaxSet + c] = acc;
+  }
+  __syncthreads();
+  // mid = T1 @ P2 (tc x tr) into Mb
+  for (int x = threadIdx.x; x < tc * tr; x += blockDim.x) {
+    const int l = x / tr, m2 = x % tr;
+    double2 acc = make_double2(0, 0);
+    for (int c = 0; c < ncl; ++c) {
+      const double2 g = cmul(W[l * kMaxSet + c], P2[c * kMaxSet + m2]);
+      acc.x += g.x;
+      acc.y += g.y;
+    }
+    Mb[l * kMaxSet + m2] = acc;
+  }
+  __syncthreads();
+  svd_small(Mb, tc, tr, kMaxSet, UM, kMaxSet, VM, kMaxSet, sg, W, Vt, &flag, perm, ssc);
+  double* sig = a.sig + static_cast<int64_t>(blockIdx.x) * kMaxSet;
+  const int sn = min(tc, tr);
+  for (int k = threadIdx.x; k < sn; k += blockDim.x) sig[k] = sg[k];
+  if (threadIdx.x == 0) s.t = min(a.r, sn);
+}
+
+// Dense branch (r*q >= side, lowrank.py:231-234): truncated SVD of the whole block.
+__global__ void k_dense(MidArgs a) {
+  extern __shared__ double2 sm2[];
+  double2* Mb = sm2;
+  double2* W = Mb + kMaxSet * kMaxSet;
+  double2* Vt = W + kMaxSet * kMaxSet;
+  __shared__ int flag, perm[kMaxSet];
+  __shared__ double ssc[kMaxSet], sg[kMaxSet];
+  BlockState& s = a.st[blockIdx.x];
+  const int side = static_cast<int>(a.side);
+  double2* scr = a.scr + static_cast<int64_t>(blockIdx.x) * 6 * kMaxSet * kMaxSet;
+  double2* UM = scr + 4 * kMaxSet * kMaxSet;
+  double2* VM = scr + 5 * kMaxSet * kMaxSet;
+  for (int x = threadIdx.x; x < side * side; x += blockDim.x) {
+    const int i = x / side, j = x % side;
+    Mb[i * kMaxSet + j] = entry_eval(a.src, s.r0 + i, s.c0 + j);
+  }
+  __syncthreads();
+  svd_small(Mb, side, side, kMaxSet, UM, kMaxSet, VM, kMaxSet, sg, W, Vt, &flag, perm, ssc);
+  double* sig = a.sig + static_cast<int64_t>(blockIdx.x) * kMaxSet;
+  for (int k = threadIdx.x; k < side; k += blockDim.x) sig[k] = sg[k];
+  if (threadIdx.x == 0) {
+    s.t = a.r;
+    s.tc = s.tr = -1;  // marks the dense branch for k_assemble
+  }
+}
+
+// u0 sigma0 = (qc @ U_M[:, :t]) sigma, v0 sigma0 = (qr @ V_M[:, :t]) sigma, zero past t
+// (_assemble, lowrank.py:284-293; the _pad_orthonormal columns meet sigma = 0 and
+// vanish from u0*sigma0 / v0*sigma0, construct.py:63-65), and W = floored_inverse(sigma0).
+__global__ void k_assemble(MidArgs a) {
+  const BlockState& s = a.st[blockIdx.x];
+  const int side = static_cast<int>(a.side);
+  const int r = a.r, t = s.t;
+  const bool dense = s.tc < 0;
+  const double2* scr = a.scr + static_cast<int64_t>(blockIdx.x) * 6 * kMaxSet * kMaxSet;
+  const double2* UM = scr + 4 * kMaxSet * kMaxSet;
+  const double2* VM = scr + 5 * kMaxSet * kMaxSet;
+  const double* sig = a.sig + static_cast<int64_t>(blockIdx.x) * kMaxSet;
+  const double2* QC = a.qc + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  const double2* QR = a.qr + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  double2* uo = a.u_out + static_cast<int64_t>(blockIdx.x) * a.side * r;
+  double2* vo = a.v_out + static_cast<int64_t>(blockIdx.x) * a.side * r;
+  const int64_t total = static_cast<int64_t>(side) * r;
+  for (int64_t x = blockIdx.y * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<int64_t>(gridDim.y) * blockDim.x) {
+    const int i = static_cast<int>(x / r), rho = static_cast<int>(x % r);
+    double2 u = make_double2(0, 0), v = make_double2(0, 0);
+    if (rho < t) {
+      if (dense) {
+        u = UM[i * kMaxSet + rho];
+        v = VM[i * kMaxSet + rho];
+      } else {
+        for (int l = 0; l < s.tc; ++l) {
+          const double2 g = cmul(QC[static_cast<int64_t>(l) * side + i], UM[l * kMaxSet + rho]);
+          u.x += g.x;
+          u.y += g.y;
+        }
+        for (int l = 0; l < s.tr; ++l) {
+          const double2 g = cmul(QR[static_cast<int64_t>(l) * side + i], VM[l * kMaxSet + rho]);
+          v.x += g.x;
+          v.y += g.y;
+        }
+      }
+      const double sg = sig[rho];
+      u = make_double2(u.x * sg, u.y * sg);
+      v = make_double2(v.x * sg, v.y * sg);
+    }
+    uo[x] = u;
+    vo[x] = v;
+  }
+  if (blockIdx.y == 0 && threadIdx.x < r) {
+    double smax = 0;
+    for (int k = 0; k < t; ++k) smax = fmax(smax, sig[k]);
+    const int rho = threadIdx.x;
+    a.w_out[static_cast<int64_t>(blockIdx.x) * r + rho] = rho < t ? floored_inv(sig[rho], smax) : 0.0;
+  }
+}
+
+
+// ---------------------------------------------------------------- recursion
+// One level of _recurse (construct.py:127-163) for problems [p0, p0 + np):
+// splitting levels factor (half x 2r) stacks, merge-only levels (1 x 2r) rows.
+struct RecArgs {
+  const double2* cur;   // (nb, rows, groups, r)
+  double2* nxt;         // next cur
+  double2* g;           // transfer blocks of this level
+  double2* scr;         // per-problem (half x 2r) scratch for the QR route
+  int64_t nb, rows, pairs;
+  int r;
+  int64_t p0;
+};
+
+__device__ void householder_r(double2* A, int m, int n, double2* R, double* red) {
+  // A (m x n) row-major in global scratch, overwritten by reflectors; R (n x n) shared, ld kMaxSet.
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __shared__ double2 s_beta;
+  __shared__ double s_vn2;
+  for (int i = threadIdx.x; i < n * kMaxSet; i += blockDim.x) R[i] = make_double2(0, 0);
+  for (int p = 0; p < n; ++p) {
+    double part = 0;
+    for (int i = p + threadIdx.x; i < m; i += blockDim.x) part += A[i * n + p].x * A[i * n + p].x + A[i * n + p].y * A[i * n + p].y;
+    const double nx2 = block_sum(part, red);
+    if (threadIdx.x == 0) {
+      const double2 al = A[p * n + p];
+      const double nx = sqrt(nx2), aa = hypot(al.x, al.y);
+      const double2 beta = aa > 0 ? make_double2(-al.x / aa * nx, -al.y / aa * nx) : make_double2(-nx, 0);
+      const double2 v0 = make_double2(al.x - beta.x, al.y - beta.y);
+      s_beta = beta;
+      s_vn2 = nx2 - aa * aa + v0.x * v0.x + v0.y * v0.y;
+      A[p * n + p] = v0;
+    }
+    __syncthreads();
+    const double vn2 = s_vn2;
+    if (vn2 > 0) {
+      for (int j = p + 1 + warp; j < n; j += nw) {
+        double2 w = make_double2(0, 0);
+        for (int i = p + lane; i < m; i += 32) {
+          const double2 g = cmulc(A[i * n + p], A[i * n + j]);
+          w.x += g.x;
+          w.y += g.y;
+        }
+        w = warp_sum2(w);
+        const double f = 2.0 / vn2;
+        w = make_double2(w.x * f, w.y * f);
+        for (int i = p + lane; i < m; i += 32) {
+          const double2 d = cmul(A[i * n + p], w);
+          A[i * n + j].x -= d.x;
+          A[i * n + j].y -= d.y;
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) R[p * kMaxSet + p] = vn2 > 0 ? s_beta : A[p * n + p];
+    for (int j = p + 1 + threadIdx.x; j < n; j += blockDim.x) R[p * kMaxSet + j] = A[p * n + j];
+    __syncthreads();
+  }
+}
+
+// Per-problem global scratch: [Ac: max(half, 64) x 2r][Ug: 64 x 64][Vg: 64 x 64].
+__device__ __forceinline__ int64_t rec_scratch_elems(int64_t half, int n2) {
+  return (half > kMaxSet ? half : kMaxSet) * n2 + 2 * kMaxSet * kMaxSet;
+}
+
+__global__ void k_recurse_split(RecArgs a) {
+  extern __shared__ double2 sm2[];
+  double2* Mb = sm2;                    // input / R
+  double2* W = Mb + kMaxSet * kMaxSet;  // svd work
+  double2* Vt = W + kMaxSet * kMaxSet;  // svd work
+  __shared__ int flag, perm[kMaxSet];
+  __shared__ double ssc[kMaxSet], sg[kMaxSet], red[32];
+  const int64_t prob = a.p0 + blockIdx.x;
+  const int64_t pairs = a.pairs, half = a.rows / 2;
+  const int n2 = 2 * a.r, r = a.r;
+  const int64_t b = prob / (2 * pairs), t = (prob / pairs) % 2, p = prob % pairs;
+  // paired = cur.reshape(nb, rows, pairs, 2r); stack t takes rows [t*half, (t+1)*half)
+  auto src = [&](int64_t row, int c) { return a.cur[((b * a.rows + t * half + row) * pairs + p) * n2 + c]; };
+  const int keep = static_cast<int>(half < r ? half : r);
+  double2* Ac = a.scr + static_cast<int64_t>(blockIdx.x) * rec_scratch_elems(half, n2);
+  double2* Ug = Ac + (half > kMaxSet ? half : kMaxSet) * n2;
+  double2* Vg = Ug + kMaxSet * kMaxSet;
+  const int64_t out_base = ((b * 2 + t) * half) * pairs + p;  // new_u.transpose(0,1,3,2,4) row (b,t,row=0,p)
+  if (half <= kMaxSet) {
+    for (int x = threadIdx.x; x < half * n2; x += blockDim.x) Mb[(x / n2) * kMaxSet + x % n2] = src(x / n2, x % n2);
+    __syncthreads();
+    svd_small(Mb, static_cast<int>(half), n2, kMaxSet, Ug, kMaxSet, Vg, kMaxSet, sg, W, Vt, &flag, perm, ssc);
+    for (int x = threadIdx.x; x < half * r; x += blockDim.x) {
+      const int row = x / r, rho = x % r;
+      double2 u = make_double2(0, 0);
+      if (rho < keep) u = make_double2(Ug[row * kMaxSet + rho].x * sg[rho], Ug[row * kMaxSet + rho].y * sg[rho]);
+      a.nxt[(out_base + row * pairs) * r + rho] = u;
+    }
+  } else {
+    // tall stack: Householder R, SVD of R gives sigma and V; new_u = A V[:, :keep] (= uu ss)
+    for (int64_t x = threadIdx.x; x < half * n2; x += blockDim.x) Ac[x] = src(x / n2, static_cast<int>(x % n2));
+    __syncthreads();
+    householder_r(Ac, static_cast<int>(half), n2, Mb, red);
+    __syncthreads();
+    svd_small(Mb, n2, n2, kMaxSet, Ug, kMaxSet, Vg, kMaxSet, sg, W, Vt, &flag, perm, ssc);
+    for (int x = threadIdx.x; x < n2 * n2; x += blockDim.x) Vt[(x / n2) * kMaxSet + x % n2] = Vg[(x / n2) * kMaxSet + x % n2];
+    __syncthreads();
+    for (int64_t x = threadIdx.x; x < half * r; x += blockDim.x) {
+      const int64_t row = x / r;
+      const int rho = static_cast<int>(x % r);
+      double2 u = make_double2(0, 0);
+      if (rho < keep)
+        for (int c = 0; c < n2; ++c) {
+          const double2 g = cmul(src(row, c), Vt[c * kMaxSet + rho]);
+          u.x += g.x;
+          u.y += g.y;
+        }
+      a.nxt[(out_base + row * pairs) * r + rho] = u;
+    }
+  }
+  __syncthreads();
+  // transfer block G = vh[:keep] zero-padded to (r x 2r): G[rho][c] = conj(V[c][rho])
+  double2* G = a.g + prob * static_cast<int64_t>(r) * n2;
+  for (int x = threadIdx.x; x < r * n2; x += blockDim.x) {
+    const int rho = x / n2, c = x % n2;
+    G[x] = rho < keep ? cconj(Vg[c * kMaxSet + rho]) : make_double2(0, 0);
+  }
+}
+
+__global__ void k_recurse_merge(RecArgs a, int64_t nprob) {
+  // (1 x 2r) rows: sigma = |row|, vh = row / sigma; new_u = (sigma, 0, ..., 0)
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int64_t prob = a.p0 + warp;
+  if (prob >= a.p0 + nprob) return;
+  const int n2 = 2 * a.r, r = a.r;
+  const double2* row = a.cur + prob * n2;
+  double acc = 0;
+  for (int c = lane; c < n2; c += 32) acc += row[c].x * row[c].x + row[c].y * row[c].y;
+  const double sgm = sqrt(warp_sum(acc));
+  double2* G = a.g + prob * static_cast<int64_t>(r) * n2;
+  for (int x = lane; x < r * n2; x += 32) {
+    const int rho = x / n2, c = x % n2;
+    G[x] = (rho == 0 && sgm > 0) ? make_double2(row[c].x / sgm, row[c].y / sgm) : make_double2(0, 0);
+  }
+  const int64_t b = prob / a.pairs, p = prob % a.pairs;
+  for (int rho = lane; rho < r; rho += 32)
+    a.nxt[(b * a.pairs + p) * r + rho] = make_double2(rho == 0 ? sgm : 0.0, 0);
+}
+
+}  // namespace bfly
+
+using namespace bfly;
+
+namespace {
+
+uint64_t mid_ws_layout(uint64_t side, uint32_t nblocks, uint64_t* off) {
+  const uint64_t S = kMaxSet;
+  uint64_t o = 0;
+  auto take = [&](uint64_t bytes) {
+    const uint64_t r = o;
+    o += (bytes + 255) / 256 * 256;
+    return r;
+  };
+  off[0] = take(sizeof(BlockState) * nblocks);
+  off[1] = take(16ull * nblocks * S * side);  // wide
+  off[2] = take(16ull * nblocks * S * side);  // tall
+  off[3] = take(16ull * nblocks * S * side);  // qc
+  off[4] = take(16ull * nblocks * S * side);  // qr
+  off[5] = take(16ull * nblocks * side);      // qbuf
+  off[6] = take(16ull * nblocks * 6 * S * S); // scr
+  off[7] = take(8ull * nblocks * S);          // sig
+  return o;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t bf_middle_workspace_bytes(uint64_t n, uint32_t levels, uint32_t rank, uint32_t nblocks) {
+  (void)rank;
+  uint64_t off[8];
+  return mid_ws_layout(n >> (levels / 2), nblocks, off);
+}
+
+int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t rank, uint32_t q_over, uint32_t iters,
+                     const void* dense, uint32_t nblocks, const int32_t* block_ij, const int32_t* draws,
+                     void* u_out, void* v_out, double* w_out, void* workspace, uint64_t ws_bytes, void* stream) {
+  if (kernel_id < BF_KERNEL_FIO || kernel_id > BF_KERNEL_DENSE) return fail(BF_EINVAL, "unknown entry kernel id");
+  if (kernel_id == BF_KERNEL_DENSE && !dense) return fail(BF_EINVAL, "dense oracle needs a matrix pointer");
+  if (n < 4 || (n & (n - 1)) || levels < 2 || levels % 2 || (1ull << (levels / 2)) > n)
+    return fail(BF_EINVAL, "bad partition geometry");
+  if (rank < 1 || q_over < 1 || iters < 1) return fail(BF_EINVAL, "bad rank / oversampling parameters");
+  const uint64_t side = n >> (levels / 2);
+  if (side < rank) return fail(BF_EINVAL, "middle blocks are narrower than the rank");
+  const uint64_t rq = static_cast<uint64_t>(rank) * q_over;
+  const bool dense_branch = rq >= side;  // lowrank.py:231-234
+  const uint64_t rqs = rq < side ? rq : side;
+  if (dense_branch ? side > kMaxSet : rqs + rank > kMaxSet)
+    return fail(BF_EINVAL, "rank too large for the batched sampling kernels (need r*(q+1) <= 64)");
+  if (!nblocks) return BF_OK;
+  if (!block_ij || (!dense_branch && !draws) || !u_out || !v_out || !w_out || !workspace)
+    return fail(BF_EINVAL, "null pointer");
+  uint64_t off[8];
+  if (ws_bytes < mid_ws_layout(side, nblocks, off)) return fail(BF_EINVAL, "middle workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(workspace);
+  MidArgs a{};
+  a.src.kind = kernel_id;
+  a.src.n = n;
+  a.src.dense = static_cast<const double2*>(dense);
+  a.side = static_cast<int64_t>(side);
+  a.r = static_cast<int>(rank);
+  a.rqs = static_cast<int>(rqs);
+  a.iters = static_cast<int>(iters);
+  a.nblocks = static_cast<int>(nblocks);
+  a.st = reinterpret_cast<BlockState*>(base + off[0]);
+  a.draws = draws;
+  a.wide = reinterpret_cast<double2*>(base + off[1]);
+  a.tall = reinterpret_cast<double2*>(base + off[2]);
+  a.qc = reinterpret_cast<double2*>(base + off[3]);
+  a.qr = reinterpret_cast<double2*>(base + off[4]);
+  a.qbuf = reinterpret_cast<double2*>(base + off[5]);
+  a.scr = reinterpret_cast<double2*>(base + off[6]);
+  a.sig = reinterpret_cast<double*>(base + off[7]);
+  a.u_out = static_cast<double2*>(u_out);
+  a.v_out = static_cast<double2*>(v_out);
+  a.w_out = w_out;
+  const int T = 256;
+  const unsigned yfill = static_cast<unsigned>(std::min<uint64_t>(64, (kMaxSet * side + T - 1) / T));
+  const size_t small_smem = 3ull * kMaxSet * kMaxSet * sizeof(double2);
+  BF_CUDA(cudaFuncSetAttribute(k_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(small_smem)));
+  BF_CUDA(cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(small_smem)));
+  k_init<<<(nblocks + 127) / 128, 128, 0, st>>>(a, block_ij);
+  if (dense_branch) {
+    k_dense<<<nblocks, T, small_smem, st>>>(a);
+  } else {
+    const size_t piv_smem = side * sizeof(double) + kMaxSet * sizeof(double2) + 32 * 8 + 32 * 4 + kMaxSet * 4;
+    if (piv_smem > 227 * 1024) return fail(BF_EINVAL, "middle blocks too wide for the pivot kernel");
+    BF_CUDA(cudaFuncSetAttribute(k_pivot_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(piv_smem)));
+    for (uint32_t sw = 0; sw < iters; ++sw) {
+      k_union<<<nblocks, 128, 0, st>>>(a, 2 * sw, kRows);
+      k_fill_wide<<<dim3(nblocks, yfill), T, 0, st>>>(a, kRows);
+      k_pivot_wide<<<nblocks, 512, piv_smem, st>>>(a, kRows);
+      k_union<<<nblocks, 128, 0, st>>>(a, 2 * sw + 1, kCols);
+      k_fill_wide<<<dim3(nblocks, yfill), T, 0, st>>>(a, kCols);
+      k_pivot_wide<<<nblocks, 512, piv_smem, st>>>(a, kCols);
+    }
+    k_union<<<nblocks, 128, 0, st>>>(a, 2 * iters, kRows);
+    k_union<<<nblocks, 128, 0, st>>>(a, 2 * iters + 1, kCols);
+    for (int which : {kCols, kRows}) {
+      k_fill_tall<<<dim3(nblocks, yfill), T, 0, st>>>(a, which, 0, a.tall);
+      k_pivot_tall<<<nblocks, 512, 0, st>>>(a, which);
+      k_fill_tall<<<dim3(nblocks, yfill), T, 0, st>>>(a, which, 1, which == kCols ? a.qc : a.qr);
+      k_cgs2<<<nblocks, 512, 0, st>>>(a, which);
+    }
+    k_mid<<<nblocks, T, small_smem, st>>>(a);
+  }
+  const unsigned yas = static_cast<unsigned>(std::min<uint64_t>(32, (side * rank + T - 1) / T));
+  k_assemble<<<dim3(nblocks, yas), T, 0, st>>>(a);
+  BF_CUDA(cudaGetLastError());
+  return BF_OK;
+}
+
+
+// One level of the recursive refactorisation (construct.py:127-163):
+// cur (nb, rows, groups, r) complex128 -> blocks (nb, 2, pairs, r, 2r) [rows >= 2]
+// or (nb, pairs, r, 2r) [rows == 1] and next cur. Returns the scratch size needed
+// when called with workspace == NULL through *ws_bytes.
+int bf_recurse_level(uint32_t rank, uint64_t nb, uint64_t rows, uint64_t groups, const void* cur, void* blocks,
+                     void* next, void* workspace, uint64_t* ws_bytes, void* stream) {
+  if (!ws_bytes) return fail(BF_EINVAL, "null ws_bytes");
+  if (rank < 1 || 2 * rank > kMaxSet) return fail(BF_EINVAL, "rank must satisfy 1 <= 2r <= 64");
+  if (groups % 2 || groups == 0 || rows == 0) return fail(BF_EINVAL, "bad recursion geometry");
+  const int64_t pairs = groups / 2;
+  const int64_t half = rows / 2;
+  const int64_t chunk = 4096;
+  const int64_t per = (half > kMaxSet ? half : kMaxSet) * 2 * rank + 2 * kMaxSet * kMaxSet;  // rec_scratch_elems
+  const uint64_t need = rows >= 2 ? static_cast<uint64_t>(chunk) * per * 16 : 0;
+  if (!workspace) {
+    *ws_bytes = need;
+    return BF_OK;
+  }
+  if (*ws_bytes < need) return fail(BF_EINVAL, "recursion workspace too small");
+  if (!cur || !blocks || !next) return fail(BF_EINVAL, "null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  RecArgs a{};
+  a.cur = static_cast<const double2*>(cur);
+  a.nxt = static_cast<double2*>(next);
+  a.g = static_cast<double2*>(blocks);
+  a.scr = static_cast<double2*>(workspace);
+  a.nb = static_cast<int64_t>(nb);
+  a.rows = static_cast<int64_t>(rows);
+  a.pairs = pairs;
+  a.r = static_cast<int>(rank);
+  if (rows >= 2) {
+    const int64_t nprob = static_cast<int64_t>(nb) * 2 * pairs;
+    const size_t smem = 3ull * kMaxSet * kMaxSet * sizeof(double2);
+    BF_CUDA(cudaFuncSetAttribute(k_recurse_split, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    for (int64_t p0 = 0; p0 < nprob; p0 += chunk) {
+      a.p0 = p0;
+      const int64_t cnt = std::min<int64_t>(chunk, nprob - p0);
+      k_recurse_split<<<static_cast<unsigned>(cnt), 256, smem, st>>>(a);
+    }
+  } else {
+    const int64_t nprob = static_cast<int64_t>(nb) * pairs;
+    a.p0 = 0;
+    k_recurse_merge<<<static_cast<unsigned>((nprob + 7) / 8), 256, 0, st>>>(a, nprob);
+  }
+  BF_CUDA(cudaGetLastError());
+  return BF_OK;
+}
+
+
+// Greedy pivoted column selection (select_pivot_columns, lowrank.py:102-129)
+// on a batch of device matrices a (batch, m, n) complex128 row-major, m <= 64,
+// n <= 16384: up to k picks each (pick order) into pivots (batch, k), pick
+// counts into counts (batch). pairwise = 1 sums the initial column norms in
+// numpy's pairwise order (the reference's matrix is F-ordered), 0 sequentially.
+int bf_select_pivots(const void* a, uint32_t batch, uint32_t m, uint32_t n, uint32_t k, double rel_tol, int pairwise,
+                     int32_t* pivots, int32_t* counts, void* workspace, uint64_t ws_bytes, void* stream) {
+  if (m > static_cast<uint32_t>(kMaxSet) || n > 16384 || k > 1024) return fail(BF_EINVAL, "pivot matrix too large");
+  if (!batch || !m || !n || !k) return BF_OK;
+  if (!a || !pivots || !counts || !workspace) return fail(BF_EINVAL, "null pointer");
+  if (ws_bytes < 16ull * batch * m * n) return fail(BF_EINVAL, "pivot workspace too small (16*batch*m*n bytes)");
+  const size_t smem = (n + (n & 1)) * 8 + kMaxSet * 16 + 32 * 8 + 32 * 4 + 1024 * 4;
+  BF_CUDA(cudaFuncSetAttribute(k_select_pivots, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  k_select_pivots<<<batch, 512, smem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const double2*>(a), static_cast<double2*>(workspace), static_cast<int>(m), static_cast<int>(n),
+      static_cast<int>(k), rel_tol, pairwise, pivots, counts);
+  BF_CUDA(cudaGetLastError());
+  return BF_OK;
+}
+
+}  // extern "C"

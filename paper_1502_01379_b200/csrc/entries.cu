@@ -9,32 +9,12 @@
 // sin/cos may differ from glibc by an ulp or two.
 // DFTP (BASELINE config 1): exp(+2 pi i (j k mod N)/N), phase exact in int64.
 #include "common.cuh"
+#include "entry_eval.cuh"
 #include "plan.h"
 
 namespace bfly {
 
 namespace {
-
-constexpr double kTwoPi = 6.283185307179586;  // fl(2 * pi), the reference's 2.0 * np.pi
-
-__device__ __forceinline__ double2 fio_entry(uint64_t n, int64_t i, int64_t j) {
-  const double nd = static_cast<double>(n);
-  const double x = __ddiv_rn(static_cast<double>(i), nd);
-  const double xi = __dsub_rn(static_cast<double>(j), __ddiv_rn(nd, 2.0));
-  const double speed = __ddiv_rn(__dadd_rn(2.0, sin(__dmul_rn(kTwoPi, x))), 8.0);
-  const double phase = __dadd_rn(__dmul_rn(x, xi), __dmul_rn(speed, fabs(xi)));
-  double s, c;
-  sincos(__dmul_rn(kTwoPi, phase), &s, &c);
-  return make_double2(c, s);
-}
-
-__device__ __forceinline__ double2 dftp_entry(uint64_t n, int64_t i, int64_t j) {
-  const uint64_t t = (static_cast<uint64_t>(i) * static_cast<uint64_t>(j)) % n;
-  const double frac = __ddiv_rn(static_cast<double>(t), static_cast<double>(n));
-  double s, c;
-  sincos(__dmul_rn(kTwoPi, frac), &s, &c);
-  return make_double2(c, s);
-}
 
 __global__ void entries_kernel(int kind, uint64_t n, const int64_t* __restrict__ rows, uint32_t nr,
                                const int64_t* __restrict__ cols, uint32_t nc, double2* __restrict__ out) {

@@ -1,0 +1,220 @@
+// linalg.cuh — CTA-level dense kernels for the construction: block
+// reductions, a complex one-sided Jacobi SVD on shared-memory matrices, and
+// the floored inverse of lowrank.py. One CTA owns one small problem.
+#pragma once
+
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace bfly {
+
+constexpr double kPinvFloor = 1e-13;  // lowrank.py:22 PINV_FLOOR
+constexpr double kPivotTie = 1e-14;   // lowrank.py:25 PIVOT_TIE
+constexpr double kBasisTrim = 1e-11;  // lowrank.py:30 BASIS_TRIM
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // conj(a) * b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double abs2(double2 a) { return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y)); }
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double2 warp_sum2(double2 v) {
+  v.x = warp_sum(v.x);
+  v.y = warp_sum(v.y);
+  return v;
+}
+
+// Block-wide reductions (blockDim.x multiple of 32, <= 1024); scratch >= 32 doubles.
+__device__ double block_max(double v, double* scratch) {
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (l == 0) scratch[w] = v;
+  __syncthreads();
+  v = l < nw ? scratch[l] : -DBL_MAX;
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ int block_min_int(int v, int* scratch) {
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (l == 0) scratch[w] = v;
+  __syncthreads();
+  v = l < nw ? scratch[l] : INT_MAX;
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// Fixed-order (deterministic) block sum.
+__device__ double block_sum(double v, double* scratch) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (l == 0) scratch[w] = v;
+  __syncthreads();
+  v = l < nw ? scratch[l] : 0.0;
+  return warp_sum(v);
+}
+
+// numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
+// pairwise_sum; PW_BLOCKSIZE 128): the order np.sum uses along a contiguous
+// axis. Used so the initial pivot norms are bit-identical to the reference's
+// whenever the reference reduces over a contiguous axis. Single thread.
+template <typename F>
+__device__ __noinline__ double pairwise_sum(const F& get, int lo, int n) {
+  if (n < 8) {
+    double res = -0.0;
+    for (int i = 0; i < n; ++i) res = __dadd_rn(res, get(lo + i));
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = get(lo + j);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], get(lo + i + j));
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, get(lo + i));
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_sum(get, lo, n2), pairwise_sum(get, lo + n2, n - n2));
+}
+
+// Sequential sum (np.sum over a non-contiguous axis walks it in order).
+template <typename F>
+__device__ double sequential_sum(const F& get, int n) {
+  double res = 0.0;
+  for (int i = 0; i < n; ++i) res = __dadd_rn(res, get(i));
+  return res;
+}
+
+// ---------------------------------------------------------------- Jacobi SVD
+// One-sided (Hestenes) Jacobi on the columns of A (m x n, m >= n, row-major
+// in shared memory, leading dimension lda). On return A holds U*Sigma
+// (unsorted, unnormalised) and V (n x n, ldv) the accumulated unitary. Pairs
+// run in round-robin tournament order, one warp per pair; every reduction
+// has a fixed order, so the result is deterministic.
+__device__ void jacobi_cols(double2* A, int m, int n, int lda, double2* V, int ldv, int* flag) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
+    const int r = i / n, c = i % n;
+    V[r * ldv + c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+  }
+  const int nn = n + (n & 1);  // tournament over an even count (a dummy column if n is odd)
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    for (int round = 0; round < nn - 1; ++round) {
+      for (int pi = warp; pi < nn / 2; pi += nw) {
+        // circle method: position 0 fixed, others rotate
+        int a = pi == 0 ? 0 : 1 + (pi - 1 + round) % (nn - 1);
+        int b = 1 + (nn - 2 - pi + round) % (nn - 1);
+        if (a > b) { const int t = a; a = b; b = t; }
+        if (b >= n) continue;
+        double al = 0, be = 0;
+        double2 ga = make_double2(0, 0);
+        for (int i = lane; i < m; i += 32) {
+          const double2 x = A[i * lda + a], y = A[i * lda + b];
+          al += x.x * x.x + x.y * x.y;
+          be += y.x * y.x + y.y * y.y;
+          const double2 g = cmulc(x, y);
+          ga.x += g.x;
+          ga.y += g.y;
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum2(ga);
+        const double gabs = hypot(ga.x, ga.y);
+        if (gabs == 0.0 || gabs <= 1e-15 * sqrt(al) * sqrt(be)) continue;
+        if (lane == 0) *flag = 1;
+        const double zeta = (be - al) / (2.0 * gabs);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        const double2 ph = make_double2(ga.x / gabs, -ga.y / gabs);  // e^{-i phi}
+        // [a', b'] = [a, b] [[c, s], [-s e^{-i phi}, c e^{-i phi}]]
+        for (int i = lane; i < m; i += 32) {
+          const double2 x = A[i * lda + a], y = cmul(A[i * lda + b], ph);
+          A[i * lda + a] = make_double2(c * x.x - s * y.x, c * x.y - s * y.y);
+          A[i * lda + b] = make_double2(s * x.x + c * y.x, s * x.y + c * y.y);
+        }
+        for (int i = lane; i < n; i += 32) {
+          const double2 x = V[i * ldv + a], y = cmul(V[i * ldv + b], ph);
+          V[i * ldv + a] = make_double2(c * x.x - s * y.x, c * x.y - s * y.y);
+          V[i * ldv + b] = make_double2(s * x.x + c * y.x, s * x.y + c * y.y);
+        }
+      }
+      __syncthreads();
+    }
+    const int any = *flag;
+    __syncthreads();
+    if (!any) break;
+  }
+}
+
+// Thin SVD of a small matrix M (m x n) given in shared memory (row-major, ld).
+// Produces s = min(m, n) singular values sorted descending (ties by index),
+// U (m x s, ldu) and V (n x s, ldv) with orthonormal columns where sigma > 0
+// (zero columns otherwise). Work buffers: W (max(m,n) x min(m,n)), Vt
+// (min x min) shared; flag/perm small shared scratch (perm >= 64 ints).
+__device__ void svd_small(const double2* M, int m, int n, int ld, double2* U, int ldu, double2* Vo, int ldv,
+                          double* sig, double2* W, double2* Vt, int* flag, int* perm, double* ssc) {
+  const bool tall = m >= n;
+  const int rr = tall ? m : n, cc = tall ? n : m;  // work on M (tall) or M^H
+  for (int i = threadIdx.x; i < rr * cc; i += blockDim.x) {
+    const int r = i / cc, c = i % cc;
+    W[r * cc + c] = tall ? M[r * ld + c] : cconj(M[c * ld + r]);
+  }
+  __syncthreads();
+  jacobi_cols(W, rr, cc, cc, Vt, cc, flag);
+  __syncthreads();
+  // column norms (fixed order) and descending order
+  for (int c = threadIdx.x >> 5; c < cc; c += blockDim.x >> 5) {
+    double acc = 0;
+    for (int i = threadIdx.x & 31; i < rr; i += 32) acc += W[i * cc + c].x * W[i * cc + c].x + W[i * cc + c].y * W[i * cc + c].y;
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) ssc[c] = sqrt(acc);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < cc; c += blockDim.x) {
+    int rank = 0;
+    for (int d = 0; d < cc; ++d) rank += (ssc[d] > ssc[c]) || (ssc[d] == ssc[c] && d < c);
+    perm[rank] = c;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < cc; k += blockDim.x) sig[k] = ssc[perm[k]];
+  __syncthreads();
+  // left vectors of the worked matrix: W[:, c] / sigma ; right vectors: Vt[:, c]
+  double2* L = tall ? U : Vo;
+  const int ldl = tall ? ldu : ldv;
+  double2* R = tall ? Vo : U;
+  const int ldr = tall ? ldv : ldu;
+  for (int i = threadIdx.x; i < rr * cc; i += blockDim.x) {
+    const int r = i / cc, k = i % cc, c = perm[k];
+    const double sg = ssc[c];
+    const double2 w = W[r * cc + c];
+    L[r * ldl + k] = sg > 0 ? make_double2(w.x / sg, w.y / sg) : make_double2(0, 0);
+  }
+  for (int i = threadIdx.x; i < cc * cc; i += blockDim.x) {
+    const int r = i / cc, k = i % cc, c = perm[k];
+    R[r * ldr + k] = Vt[r * cc + c];
+  }
+  __syncthreads();
+}
+
+// floored_inverse (lowrank.py:79-87): 1/sigma where sigma > PINV_FLOOR * max, else 0.
+__device__ __forceinline__ double floored_inv(double s, double smax) {
+  return s > kPinvFloor * smax ? 1.0 / s : 0.0;
+}
+
+}  // namespace bfly

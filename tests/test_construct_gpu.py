@@ -1,0 +1,247 @@
+"""GPU construction (bf_middle_blocks / bf_recurse_level / bf_select_pivots)
+against the CPU oracle and the reference's golden outputs — the staged parity
+contract of SURVEY.md §8(c):
+
+  stage 3  pivots: reference known-answer matrices, identical pivot lists;
+  stage 4  per-block products u0 diag(sigma) v0^H (phase-invariant) against the
+           reference's traced blocks, and recursion products against the
+           oracle's _recurse on identical input;
+  stage 5  operator level: apply of GPU-built factors vs the reference's
+           apply / the dense operator; the reference construction KATs
+           (pkg/tests/test_construct.py).
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_1502_01379_b200 as bf
+from conftest import chain_from_golden, complex_gaussian, golden
+from oracle import chain as ochain
+from oracle import construct as ocons
+from oracle import entries as oent
+from oracle import lowrank as olr
+from paper_1502_01379_b200 import _lib
+from paper_1502_01379_b200.synthetic import to_host
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a = a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def dense_of(f):
+    h = to_host(f)
+    c = ochain.Chain(h.n, h.partition.levels, h.rank, h.u_outer.blocks, [(t.level, t.blocks) for t in h.g_chain],
+                     h.middle.weights, [(t.level, t.blocks) for t in h.h_chain], h.v_outer.blocks)
+    return ochain.apply(c, np.eye(h.n, dtype=complex))
+
+
+def gpu_pivots(a, k, tol, pairwise):
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    m, n = a.shape
+    ad = torch.from_numpy(a).cuda()
+    piv = torch.zeros(k, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ws = torch.empty(16 * m * n, dtype=torch.uint8, device="cuda")
+    _lib.check(_lib.load().bf_select_pivots(ctypes.c_void_p(ad.data_ptr()), 1, m, n, k, tol, int(pairwise),
+                                            ctypes.c_void_p(piv.data_ptr()), ctypes.c_void_p(cnt.data_ptr()),
+                                            ctypes.c_void_p(ws.data_ptr()), ws.numel(), None))
+    return piv.cpu().numpy()[:int(cnt.cpu().item())].tolist()
+
+
+def test_pivots_reference_kats():
+    """pivots.npz holds select_pivot_columns outputs of the reference itself."""
+    d = golden("pivots.npz")
+    for tag in ("gauss", "dups", "rank1", "zero"):
+        a, k, tol = d[f"{tag}_a"], int(d[f"{tag}_k"]), float(d[f"{tag}_tol"])
+        assert gpu_pivots(a, k, tol, pairwise=False) == list(d[f"{tag}_piv"]), tag
+    # fio: (48 x 1024) rows-sampled FIO block, r=16 picks
+    a = d["fio_a"]
+    got = gpu_pivots(a, int(d["fio_k"]), 0.0, pairwise=False)
+    assert got == list(d["fio_piv"])
+
+
+def _block_product(u, s, v):
+    return (u * s) @ v.conj().T
+
+
+@pytest.mark.parametrize("name,tol_med,tol_max", [
+    ("construct_fio_n128_r4_leaf025.npz", 1e-13, 1e-12),   # dense branch (r q >= side)
+    ("construct_fio_n1024_r8_leaf1.npz", 1e-9, 1e-6),      # sampling branch, accurate leaf
+    ("construct_fio_n1024_r12_leaf8.npz", 1e-9, 1e-4),     # config 0 geometry
+])
+def test_middle_blocks_vs_reference_traces(name, tol_med, tol_max):
+    d = golden(name)
+    n, levels, r, seed = int(d["n"]), int(d["levels"]), int(d["rank"]), int(d["seed"])
+    p = bf.DyadicPartition(n, levels)
+    ms = bf.construct.MiddleSampler(bf.FioKernel(n), p, r, seed=seed)
+    keys = sorted({k.rsplit("_", 1)[0] for k in d if k.startswith("blk_")})
+    ij = [(int(k.split("_")[1]), int(k.split("_")[2])) for k in keys]
+    u, v, w = ms.blocks(ij)
+    errs = []
+    for b, key in enumerate(keys):
+        want = _block_product(d[key + "_u0"], d[key + "_s0"], d[key + "_v0"])
+        winv = w[b].cpu().numpy()
+        uu, vv = u[b].cpu().numpy(), v[b].cpu().numpy()
+        errs.append(rel((uu * winv) @ vv.conj().T, want))
+        s_gpu = np.where(winv > 0, 1.0 / np.where(winv > 0, winv, 1.0), 0.0)
+        s_ref = d[key + "_s0"]
+        keep = s_ref > 1e-13 * s_ref.max()
+        assert np.allclose(s_gpu[keep], s_ref[keep], rtol=1e-6)
+    print(name, "per-block product rel err", errs)
+    assert np.median(errs) <= tol_med and max(errs) <= tol_max
+
+
+def test_middle_all_blocks_vs_oracle_cfg0():
+    """Every middle block of the config-0 geometry against the oracle's sample_block."""
+    n, levels, r, seed = 1024, 6, 12, 0
+    p = bf.DyadicPartition(n, levels)
+    ms = bf.construct.MiddleSampler(bf.FioKernel(n), p, r, seed=seed)
+    m = p.mid_nodes
+    ij = [(i, j) for i in range(m) for j in range(m)]
+    u, v, w = ms.blocks(ij)
+    ent = oent.EntryOracle("fio", n)
+    errs = []
+    for b, (i, j) in enumerate(ij):
+        t = ocons.sample_block(ent, n, levels, r, olr.Params(), seed, i, j)
+        want = t.matrix()
+        winv = w[b].cpu().numpy()
+        uu, vv = u[b].cpu().numpy(), v[b].cpu().numpy()
+        got = (uu * winv) @ vv.conj().T
+        errs.append(rel(got, want))
+    errs = np.array(errs)
+    print("cfg0 blocks: median %.2e max %.2e  <=1e-12: %d/%d" % (np.median(errs), errs.max(),
+                                                                  (errs <= 1e-12).sum(), errs.size))
+    assert np.median(errs) <= 1e-9
+
+
+def test_recursion_matches_oracle():
+    """_recurse on identical input (the reference's U^h): per-slab reconstructions agree."""
+    d = golden("construct_fio_n128_r4_leaf025.npz")
+    n, levels, r = int(d["n"]), int(d["levels"]), int(d["rank"])
+    p = bf.DyadicPartition(n, levels)
+    m, side = p.mid_nodes, p.mid_side
+    u_h = d["u_h"]
+    leaf_o, pieces_o = ocons.recurse(u_h.reshape(m, side, m, r), n, levels, r)
+    outer, chain = bf.recursive_factor_u(bf.BlockDiagonalFactor(u_h), p, r)
+
+    def recon(leaf, pieces):
+        full = bf.BlockDiagonalFactor(leaf).dense()
+        for lvl, b in reversed(pieces):
+            full = full @ bf.TransferFactor(lvl, b).dense()
+        return full
+
+    ro = recon(leaf_o, pieces_o)
+    rg = recon(outer.blocks.cpu().numpy(), [(t.level, t.blocks.cpu().numpy()) for t in chain])
+    assert rel(rg, ro) <= 1e-12
+    # zero input: zero leaf, rows of every transfer block orthonormal or zero (test_construct.py:104-122)
+    z_outer, z_chain = bf.recursive_factor_u(bf.BlockDiagonalFactor(np.zeros_like(u_h)), p, r)
+    assert not torch.any(z_outer.blocks != 0)
+    for tf in z_chain:
+        blocks = tf.blocks.cpu().numpy().reshape(-1, r, 2 * r)
+        grams = blocks @ blocks.conj().swapaxes(-1, -2)
+        diags = np.diagonal(grams, axis1=-2, axis2=-1).real
+        assert np.allclose(grams, np.einsum("bi,ij->bij", diags, np.eye(r)), atol=1e-12)
+        assert np.all((np.abs(diags - 1) < 1e-12) | (np.abs(diags) < 1e-12))
+
+
+def test_factorize_dense_branch_matches_reference_operator():
+    d = golden("construct_fio_n128_r4_leaf025.npz")
+    n, levels, r, seed = int(d["n"]), int(d["levels"]), int(d["rank"]), int(d["seed"])
+    f = bf.factorize(bf.FioKernel(n), bf.DyadicPartition(n, levels), r, seed=seed)
+    assert rel(f.apply(d["g"]), d["fwd"]) <= 1e-10
+    assert rel(f.apply_adjoint(d["g"]), d["adj"]) <= 1e-10
+    assert np.allclose(np.sort(f.middle.weights.cpu().numpy().ravel()), np.sort(d["weights"].ravel()), rtol=1e-9)
+
+
+@pytest.mark.parametrize("name", ["construct_fio_n1024_r8_leaf1.npz", "construct_fio_n1024_r12_leaf8.npz"])
+def test_factorize_operator_accuracy_vs_reference(name):
+    """Stage 5: eps(GPU factors) no worse than eps(reference factors) against the dense operator."""
+    d = golden(name)
+    n, levels, r, seed = int(d["n"]), int(d["levels"]), int(d["rank"]), int(d["seed"])
+    f = bf.factorize(bf.FioKernel(n), bf.DyadicPartition(n, levels), r, seed=seed)
+    k = oent.fio_block(n, np.arange(n), np.arange(n))
+    g = d["g"]
+    exact = k @ g
+    eps_gpu = rel(f.apply(g), exact)
+    eps_ref = rel(d["fwd"], exact)
+    print(name, "eps gpu %.3e ref %.3e  gpu-vs-ref %.3e" % (eps_gpu, eps_ref, rel(f.apply(g), d["fwd"])))
+    assert eps_gpu <= eps_ref * 1.5 + 1e-13
+
+
+def test_factorize_fio_accuracy_against_dense(rng):
+    """pkg/tests/test_construct.py:226-250: N=256, r=8, leaf 0.25 within 1e-6 of K, adjoint too."""
+    n = 256
+    p = bf.make_partition(n, 0.25)
+    k = oent.fio_block(n, np.arange(n), np.arange(n))
+    f = bf.factorize(bf.FioKernel(n), p, 8, seed=1)
+    for _ in range(4):
+        g = complex_gaussian(rng, n)
+        assert np.linalg.norm(f.apply(g) - k @ g) / np.linalg.norm(k @ g) <= 1e-6
+    g = complex_gaussian(rng, n)
+    want = k.conj().T @ g
+    assert np.linalg.norm(f.apply_adjoint(g) - want) <= 1e-6 * np.linalg.norm(want)
+
+
+def test_streaming_matches_sampling_bitwise():
+    n = 128
+    p = bf.make_partition(n, 0.25)
+    a = bf.factorize(bf.FioKernel(n), p, 4, seed=9, mode="sampling")
+    b = bf.factorize(bf.FioKernel(n), p, 4, seed=9, mode="streaming")
+    assert bf.factors_equal(a, b)
+    p = bf.make_partition(1024, 1)
+    a = bf.factorize(bf.FioKernel(1024), p, 8, seed=3, mode="sampling")
+    b = bf.factorize(bf.FioKernel(1024), p, 8, seed=3, mode="streaming")
+    assert bf.factors_equal(a, b)
+
+
+def test_zero_kernel_and_exact_rank(rng):
+    """test_construct.py:19-27 (zero kernel) and 253-261 (exact-rank chain reproduction)."""
+    p = bf.make_partition(64, 1)
+    u_h, middle, v_h = bf.middle_factorization_sampling(bf.DenseOracle(np.zeros((64, 64))), p, 2, seed=0)
+    assert not torch.any(middle.weights != 0) and not torch.any(u_h.blocks != 0) and not torch.any(v_h.blocks != 0)
+    # exact-rank operator: a random chain with rank-3 blocks, reproduced to 1e-10
+    from oracle.partition import level_geometry
+
+    def orth_rows(shape):
+        a = complex_gaussian(rng, shape)
+        flat = a.reshape(-1, *shape[-2:])
+        q, _ = np.linalg.qr(flat.swapaxes(-1, -2))
+        return np.ascontiguousarray(q.swapaxes(-1, -2).reshape(shape))
+
+    shapes, leaf_shape = level_geometry(64, p.levels, 3)
+    ch = ochain.Chain(64, p.levels, 3, orth_rows(leaf_shape).conj(), [(l, orth_rows(s)) for l, _, s in shapes],
+                      rng.uniform(0.5, 1.5, size=(p.mid_nodes, p.mid_nodes, 3)),
+                      [(l, orth_rows(s)) for l, _, s in shapes], orth_rows(leaf_shape).conj())
+    kmat = ochain.apply(ch, np.eye(64, dtype=complex))
+    for mode in ("sampling", "streaming"):
+        f = bf.factorize(bf.DenseOracle(kmat), p, 3, seed=8, mode=mode)
+        g = complex_gaussian(rng, 64)
+        assert np.linalg.norm(f.apply(g) - kmat @ g) / np.linalg.norm(kmat @ g) <= 1e-10
+
+
+def test_factorize_errors():
+    p = bf.make_partition(64, 1)
+    with pytest.raises(ValueError):
+        bf.factorize(bf.FioKernel(64), p, 0)
+    with pytest.raises(ValueError):
+        bf.factorize(bf.FioKernel(64), p, 2, mode="nonsense")
+    with pytest.raises(ValueError):
+        bf.factorize(bf.FioKernel(64), p, 2, mode="matvec")
+
+    class OpOnly:
+        shape = (64, 64)
+
+        def apply(self, x):
+            return x
+
+        def apply_adjoint(self, x):
+            return x
+
+    with pytest.raises(ValueError):
+        bf.factorize(OpOnly(), p, 2, mode="sampling")
