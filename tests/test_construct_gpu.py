@@ -57,9 +57,15 @@ def gpu_pivots(a, k, tol, pairwise):
 def test_pivots_reference_kats():
     """pivots.npz holds select_pivot_columns outputs of the reference itself."""
     d = golden("pivots.npz")
-    for tag in ("gauss", "dups", "rank1", "zero"):
+    for tag in ("gauss", "dups", "zero"):
         a, k, tol = d[f"{tag}_a"], int(d[f"{tag}_k"]), float(d[f"{tag}_tol"])
         assert gpu_pivots(a, k, tol, pairwise=False) == list(d[f"{tag}_piv"]), tag
+    # rank-1 + 1e-13 noise: after the first pick the downdated residual estimates are
+    # rounding noise (~eps |a|^2, far above the 1e-22 floor), so later picks depend on the
+    # BLAS summation order (SURVEY.md §8(a) c4). Only the numerically determined pick is pinned.
+    a, k, tol = d["rank1_a"], int(d["rank1_k"]), float(d["rank1_tol"])
+    got = gpu_pivots(a, k, tol, pairwise=False)
+    assert got[0] == int(d["rank1_piv"][0]) and len(got) >= 1
     # fio: (48 x 1024) rows-sampled FIO block, r=16 picks
     a = d["fio_a"]
     got = gpu_pivots(a, int(d["fio_k"]), 0.0, pairwise=False)
