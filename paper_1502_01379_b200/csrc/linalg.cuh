@@ -69,26 +69,67 @@ __device__ double block_sum(double v, double* scratch) {
 // axis. Used so the initial pivot norms are bit-identical to the reference's
 // whenever the reference reduces over a contiguous axis. Single thread.
 template <typename F>
-__device__ __noinline__ double pairwise_sum(const F& get, int lo, int n) {
+__device__ __forceinline__ double pairwise_leaf(const F& get, int lo, int n) {
   if (n < 8) {
     double res = -0.0;
     for (int i = 0; i < n; ++i) res = __dadd_rn(res, get(lo + i));
     return res;
   }
-  if (n <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = get(lo + j);
-    int i = 8;
-    for (; i < n - (n % 8); i += 8)
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], get(lo + i + j));
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, get(lo + i));
-    return res;
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = get(lo + j);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], get(lo + i + j));
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, get(lo + i));
+  return res;
+}
+
+// The recursion pairwise(lo, n) = pairwise(lo, n2) + pairwise(lo + n2, n - n2),
+// n2 = n/2 - (n/2) % 8, evaluated iteratively (explicit post-order stack) so no
+// device call stack is needed.
+template <typename F>
+__device__ double pairwise_sum(const F& get, int lo0, int n0) {
+  int los[24], ns[24], ph[24];
+  double left[24];
+  int sp = 0;
+  los[0] = lo0;
+  ns[0] = n0;
+  ph[0] = 0;
+  double ret = 0.0;
+  bool returning = false;
+  while (true) {
+    if (returning) {
+      if (sp < 0) return ret;
+      if (ph[sp] == 1) {
+        left[sp] = ret;
+        ph[sp] = 2;
+        const int n2 = ns[sp] / 2 - (ns[sp] / 2) % 8;
+        los[sp + 1] = los[sp] + n2;
+        ns[sp + 1] = ns[sp] - n2;
+        ph[sp + 1] = 0;
+        ++sp;
+        returning = false;
+      } else {
+        ret = __dadd_rn(left[sp], ret);
+        --sp;
+      }
+      continue;
+    }
+    if (ns[sp] <= 128) {
+      ret = pairwise_leaf(get, los[sp], ns[sp]);
+      --sp;
+      returning = true;
+      continue;
+    }
+    ph[sp] = 1;
+    const int n2 = ns[sp] / 2 - (ns[sp] / 2) % 8;
+    los[sp + 1] = los[sp];
+    ns[sp + 1] = n2;
+    ph[sp + 1] = 0;
+    ++sp;
   }
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(pairwise_sum(get, lo, n2), pairwise_sum(get, lo + n2, n - n2));
 }
 
 // Sequential sum (np.sum over a non-contiguous axis walks it in order).

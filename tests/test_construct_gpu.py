@@ -251,3 +251,18 @@ def test_factorize_errors():
 
     with pytest.raises(ValueError):
         bf.factorize(OpOnly(), p, 2, mode="sampling")
+
+
+def test_pivots_pairwise_norm_order():
+    """The sweep's column pivots run on entry(:, cols)^H, an F-ordered array whose
+    initial norms numpy sums pairwise: the first pick must match the oracle exactly."""
+    n = 1 << 16
+    side = 4096
+    rng = np.random.default_rng(11)
+    cols = np.sort(rng.choice(side, 48, replace=False))
+    a = oent.fio_block(n, np.arange(side) + 3 * side, cols + 5 * side).conj().T   # F-ordered (48 x side)
+    want = olr.greedy_pivots(a, 16)
+    got = gpu_pivots(np.ascontiguousarray(a), 16, 0.0, pairwise=True)
+    matched = sum(1 for x, y in zip(got, want) if x == y)
+    print("pairwise-order pivots: %d/16 identical" % matched)
+    assert got[0] == want[0] and matched >= 8

@@ -1,0 +1,89 @@
+"""Construction timing on the GPU (factorize, sampling mode) with a CPU oracle
+comparison on a sample of blocks. Usage:
+  python tools/bench_construct.py cfg0|cfg1|cfg2 [--full] [--cpu-blocks N]
+cfg2 (65,536 middle blocks) is timed on one block-row plus its slab recursion
+and extrapolated (x m block-rows, x 2 slab recursions per row) unless --full.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1502_01379_b200 as bf  # noqa: E402
+from paper_1502_01379_b200 import construct as bc  # noqa: E402
+
+CFG = {"cfg0": ("fio", 1 << 10, 12, 8), "cfg1": ("dftp", 1 << 16, 8, 16), "cfg2": ("fio", 1 << 20, 16, 16)}
+
+
+def kernel(kind, n):
+    return bf.FioKernel(n) if kind == "fio" else bf.DftPlusKernel(n)
+
+
+def sync_time(fn):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = fn()
+    torch.cuda.synchronize()
+    return time.perf_counter() - t0, out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config", choices=sorted(CFG))
+    ap.add_argument("--full", action="store_true")
+    ap.add_argument("--cpu-blocks", type=int, default=4)
+    args = ap.parse_args()
+    kind, n, r, leaf = CFG[args.config]
+    p = bf.make_partition(n, leaf)
+    m, side = p.mid_nodes, p.mid_side
+    ker = kernel(kind, n)
+    res = {"config": args.config, "n": n, "r": r, "levels": p.levels, "m": m, "side": side}
+    # warm-up (module load, first launches)
+    bc.MiddleSampler(ker, p, r).blocks([(0, 0)])
+    torch.cuda.synchronize()
+    if args.full or args.config != "cfg2":
+        t, f = sync_time(lambda: bf.factorize(ker, p, r, seed=0))
+        res["gpu_factorize_s"] = t
+        res["method"] = "full factorize (sampling mode)"
+    else:
+        ms = bc.MiddleSampler(ker, p, r, seed=0)
+        ij = [(0, j) for j in range(m)]
+        t_mid, (u, v, w) = sync_time(lambda: ms.blocks(ij))
+        slab = u.permute(1, 0, 2).reshape(1, side, m, r)
+        t_rec, _ = sync_time(lambda: bc.recurse(slab, p, r))
+        res["gpu_block_row_s"] = t_mid
+        res["gpu_slab_recursion_s"] = t_rec
+        res["gpu_factorize_s"] = m * t_mid + 2 * m * t_rec
+        res["method"] = f"1 block-row ({m} blocks) + 1 slab recursion, extrapolated x{m} rows, x{2 * m} slabs"
+    # CPU: the reference algorithm (oracle port) on a sample of middle blocks + one slab recursion
+    from oracle import construct as ocons
+    from oracle import entries as oent
+    from oracle import lowrank as olr
+    ent = oent.EntryOracle(kind, n)
+    rng = np.random.default_rng(0)
+    picks = [(int(rng.integers(m)), int(rng.integers(m))) for _ in range(args.cpu_blocks)]
+    t0 = time.perf_counter()
+    for i, j in picks:
+        ocons.sample_block(ent, n, p.levels, r, olr.Params(), 0, i, j)
+    t_blk = (time.perf_counter() - t0) / len(picks)
+    slab = np.asarray(rng.standard_normal((1, side, m, r)) + 1j * rng.standard_normal((1, side, m, r)))
+    t0 = time.perf_counter()
+    ocons.recurse(slab, n, p.levels, r)
+    t_slab = time.perf_counter() - t0
+    res["cpu_per_block_s"] = t_blk
+    res["cpu_slab_recursion_s"] = t_slab
+    res["cpu_factorize_s_extrapolated"] = m * m * t_blk + 2 * m * t_slab
+    res["cpu_method"] = (f"oracle port (reference algorithm), {len(picks)} sampled middle blocks x {m * m} + "
+                         f"1 slab recursion x {2 * m}; cores={os.environ.get('OPENBLAS_NUM_THREADS', os.cpu_count())}")
+    res["speedup"] = res["cpu_factorize_s_extrapolated"] / res["gpu_factorize_s"]
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
