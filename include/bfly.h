@@ -117,6 +117,28 @@ int bf_apply_timed(const bf_plan* plan, const void* in, void* out, uint32_t k, i
                    void* workspace, uint64_t workspace_bytes, void* stream, bf_timer* timer);
 int bf_timer_read(bf_timer* timer, float* launch_ms, uint32_t* steps, uint32_t* launches);
 
+/* ---------------------------------------------------------------------------
+ * Sharded apply across GPUs. Part `part` of `nparts`
+ * (nparts divides m = 2^(levels/2)) owns middle column nodes J and row nodes I
+ * = [part*m/nparts, (part+1)*m/nparts): the V^L/H slices feeding J and the
+ * G/U^L slices fed by I. bf_plan_upload then takes this part's slices in the
+ * reference layout: leaf blocks [part*nb/P, (part+1)*nb/P) and transfer groups
+ * [part*G/P, (part+1)*G/P) of every level (the leading block index carries
+ * the middle node), plus the full (m, m, r) weights. Forward apply of K:
+ *   bf_apply_down(in rows [part*n/P, ...)) -> mid ((m/P)*m*r, k)
+ *   bf_middle_pack(mid) -> send (P, (m/P)^2 r, k), scaled by M's weights
+ *   all-to-all of equal chunks (NCCL) -> recv
+ *   bf_middle_unpack(recv) -> mid' ; bf_apply_up(mid') -> out rows [part*n/P, ...)
+ * adjoint = 1 runs K* the same way (U*, G* down; H, V up). */
+int bf_plan_create_sharded(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, int dtype, int device,
+                           uint32_t part, uint32_t nparts);
+int bf_apply_down(const bf_plan* plan, const void* in, void* mid, uint32_t k, int adjoint,
+                  void* workspace, uint64_t workspace_bytes, void* stream);
+int bf_middle_pack(const bf_plan* plan, const void* mid, void* send, uint32_t k, int adjoint, void* stream);
+int bf_middle_unpack(const bf_plan* plan, const void* recv, void* mid, uint32_t k, int adjoint, void* stream);
+int bf_apply_up(const bf_plan* plan, const void* mid, void* out, uint32_t k, int adjoint,
+                void* workspace, uint64_t workspace_bytes, void* stream);
+
 /* Dense entry block K[rows[a], cols[b]] -> out (nr, nc) complex128 on the
  * device; rows/cols are device int64 arrays. Replaces FioKernel.block
  * (kernels.py:34-38) via BlockView (oracles.py:66-68). */

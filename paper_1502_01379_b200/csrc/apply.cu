@@ -54,6 +54,8 @@ template <typename E>
 int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint64_t P, uint64_t units,
                  const void* in, void* out, uint32_t k, int adjoint, int remap, cudaStream_t st) {
   if (units >= (1ull << 31)) return fail(BF_EINVAL, "level has too many blocks for one launch");
+  if (remap && static_cast<uint64_t>(pl.m) * pl.m * pl.rank >= (1ull << 32))
+    return fail(BF_EINVAL, "middle vector too long for 32-bit remap indices");
   const bool mrhs = k >= kMrhsMinK;
   const Shape sh = mrhs ? kMrhs : kStream;
   LevelArgs a{};
@@ -149,30 +151,103 @@ int timed_op(LaunchRecorder* rec, const Plan& pl, int which, int lvl_idx, int ad
   return rc;
 }
 
+// First half of the chain (factors.py:230-233): lead leaf adjoint, then the
+// down levels L-1 .. h in the adjoint direction. With remap the middle factor
+// is fused into the last level; the result lands in final_dst or (when null)
+// in whichever ping-pong buffer the alternation reaches (returned in *result).
+template <typename E>
+int run_down(const Plan& pl, const void* in, E* bufs[2], void* final_dst, uint32_t k, int adjoint, int remap,
+             cudaStream_t st, LaunchRecorder* rec, const void** result) {
+  const int nl = static_cast<int>(pl.nlev);
+  const int lead = adjoint ? BF_FACTOR_U : BF_FACTOR_V;
+  const int down = adjoint ? BF_FACTOR_G : BF_FACTOR_H;
+  int cur = 0;
+  int rc = timed_op<E>(rec, pl, lead, 0, 1, in, bufs[0], k, 0, st);
+  if (rc) return rc;
+  for (int i = nl - 1; i >= 0; --i) {
+    void* dst = (i == 0 && final_dst) ? final_dst : bufs[cur ^ 1];
+    rc = timed_op<E>(rec, pl, down, i, 1, bufs[cur], dst, k, i == 0 ? remap : 0, st);
+    if (rc) return rc;
+    if (dst == bufs[cur ^ 1]) cur ^= 1;
+  }
+  *result = final_dst ? final_dst : bufs[cur];
+  return 0;
+}
+
+// Second half (factors.py:234-236): up levels h .. L-1 forward, then the trail leaf.
+template <typename E>
+int run_up(const Plan& pl, const void* mid, E* bufs[2], void* out, uint32_t k, int adjoint, cudaStream_t st,
+           LaunchRecorder* rec) {
+  const int nl = static_cast<int>(pl.nlev);
+  const int up = adjoint ? BF_FACTOR_H : BF_FACTOR_G;
+  const int trail = adjoint ? BF_FACTOR_V : BF_FACTOR_U;
+  const void* src = mid;
+  int nxt = (mid == bufs[0]) ? 1 : 0;
+  for (int i = 0; i < nl; ++i) {
+    int rc = timed_op<E>(rec, pl, up, i, 0, src, bufs[nxt], k, 0, st);
+    if (rc) return rc;
+    src = bufs[nxt];
+    nxt ^= 1;
+  }
+  return timed_op<E>(rec, pl, trail, 0, 0, src, out, k, 0, st);
+}
+
 template <typename E>
 int chain(const Plan& pl, const void* in, void* out, uint32_t k, int adjoint, void* ws, cudaStream_t st,
           LaunchRecorder* rec) {
   const uint64_t dk = pl.dim_max * k;
   E* bufs[2] = {static_cast<E*>(ws), static_cast<E*>(ws) + dk};
-  int cur = 0;
-  const int nl = static_cast<int>(pl.nlev);
-  const int lead = adjoint ? BF_FACTOR_U : BF_FACTOR_V;
-  const int down = adjoint ? BF_FACTOR_G : BF_FACTOR_H;
-  const int up = adjoint ? BF_FACTOR_H : BF_FACTOR_G;
-  const int trail = adjoint ? BF_FACTOR_V : BF_FACTOR_U;
-  int rc = timed_op<E>(rec, pl, lead, 0, 1, in, bufs[cur], k, 0, st);
+  const void* mid = nullptr;
+  int rc = run_down<E>(pl, in, bufs, nullptr, k, adjoint, adjoint ? 2 : 1, st, rec, &mid);
   if (rc) return rc;
-  for (int i = nl - 1; i >= 0; --i) {  // levels L-1 .. h, adjoint direction
-    rc = timed_op<E>(rec, pl, down, i, 1, bufs[cur], bufs[cur ^ 1], k, i == 0 ? (adjoint ? 2 : 1) : 0, st);
-    if (rc) return rc;
-    cur ^= 1;
+  return run_up<E>(pl, mid, bufs, out, k, adjoint, st, rec);
+}
+
+// Sharded middle exchange: this part's down-half output
+// mid[(a*m + b)*r + rho][kk] (a: own local node, b: global other node) is packed
+// per destination part e as send[e][a][b - e*mp][rho][kk], scaled by the middle
+// weight (factors.py:180-190); the receiver scatters recv[d][a'][b'][rho][kk]
+// to out[(b'*m + d*mp + a')*r + rho][kk].
+template <typename E>
+__global__ void pack_kernel(const E* __restrict__ mid, E* __restrict__ send, const typename Cx<E>::R* __restrict__ W,
+                            uint32_t m, uint32_t mp, uint32_t r, uint32_t k, uint32_t part, uint32_t nparts,
+                            int adjoint) {
+  const uint64_t per = static_cast<uint64_t>(mp) * mp * r * k;
+  const uint64_t total = per * nparts;
+  for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t e = static_cast<uint32_t>(x / per);
+    uint64_t rem = x - e * per;
+    const uint32_t kk = static_cast<uint32_t>(rem % k);
+    rem /= k;
+    const uint32_t rho = static_cast<uint32_t>(rem % r);
+    rem /= r;
+    const uint32_t bl = static_cast<uint32_t>(rem % mp), a = static_cast<uint32_t>(rem / mp);
+    const uint32_t own = part * mp + a, other = e * mp + bl;
+    // forward: own = column node j, other = row node i, weight W[i, j]; adjoint: own = i, other = j
+    const uint64_t wi = adjoint ? (static_cast<uint64_t>(own) * m + other) : (static_cast<uint64_t>(other) * m + own);
+    const auto w = W[wi * r + rho];
+    const E v = mid[((static_cast<uint64_t>(a) * m + other) * r + rho) * k + kk];
+    send[x] = Cx<E>::make(w * v.x, w * v.y);
   }
-  for (int i = 0; i < nl; ++i) {  // levels h .. L-1, forward direction
-    rc = timed_op<E>(rec, pl, up, i, 0, bufs[cur], bufs[cur ^ 1], k, 0, st);
-    if (rc) return rc;
-    cur ^= 1;
+}
+
+template <typename E>
+__global__ void unpack_kernel(const E* __restrict__ recv, E* __restrict__ out, uint32_t m, uint32_t mp, uint32_t r,
+                              uint32_t k, uint32_t nparts) {
+  const uint64_t per = static_cast<uint64_t>(mp) * mp * r * k;
+  const uint64_t total = per * nparts;
+  for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t d = static_cast<uint32_t>(x / per);
+    uint64_t rem = x - d * per;
+    const uint32_t kk = static_cast<uint32_t>(rem % k);
+    rem /= k;
+    const uint32_t rho = static_cast<uint32_t>(rem % r);
+    rem /= r;
+    const uint32_t b = static_cast<uint32_t>(rem % mp), a = static_cast<uint32_t>(rem / mp);
+    out[((static_cast<uint64_t>(b) * m + d * mp + a) * r + rho) * k + kk] = recv[x];
   }
-  return timed_op<E>(rec, pl, trail, 0, 0, bufs[cur], out, k, 0, st);
 }
 
 }  // namespace
@@ -181,6 +256,46 @@ int plan_apply(const Plan& pl, const void* in, void* out, uint32_t k, int adjoin
                LaunchRecorder* rec) {
   return pl.dtype == BF_C128 ? chain<double2>(pl, in, out, k, adjoint, ws, st, rec)
                              : chain<float2>(pl, in, out, k, adjoint, ws, st, rec);
+}
+
+int plan_apply_half(const Plan& pl, int up, const void* in, void* out, uint32_t k, int adjoint, void* ws,
+                    cudaStream_t st) {
+  const uint64_t dk = pl.dim_max * k;
+  const void* res = nullptr;
+  if (pl.dtype == BF_C128) {
+    double2* bufs[2] = {static_cast<double2*>(ws), static_cast<double2*>(ws) + dk};
+    return up ? run_up<double2>(pl, in, bufs, out, k, adjoint, st, nullptr)
+              : run_down<double2>(pl, in, bufs, out, k, adjoint, 0, st, nullptr, &res);
+  }
+  float2* bufs[2] = {static_cast<float2*>(ws), static_cast<float2*>(ws) + dk};
+  return up ? run_up<float2>(pl, in, bufs, out, k, adjoint, st, nullptr)
+            : run_down<float2>(pl, in, bufs, out, k, adjoint, 0, st, nullptr, &res);
+}
+
+int plan_middle_exchange(const Plan& pl, int unpack, const void* in, void* out, uint32_t k, int adjoint,
+                         cudaStream_t st) {
+  const uint32_t mp = pl.m / pl.nparts;
+  const uint64_t total = static_cast<uint64_t>(mp) * mp * pl.rank * k * pl.nparts;
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, pl.sms * 8ull));
+  if (pl.dtype == BF_C128) {
+    if (unpack)
+      unpack_kernel<double2><<<grid, 256, 0, st>>>(static_cast<const double2*>(in), static_cast<double2*>(out), pl.m,
+                                                   mp, pl.rank, k, pl.nparts);
+    else
+      pack_kernel<double2><<<grid, 256, 0, st>>>(static_cast<const double2*>(in), static_cast<double2*>(out),
+                                                 static_cast<const double*>(pl.weights), pl.m, mp, pl.rank, k,
+                                                 pl.part, pl.nparts, adjoint);
+  } else {
+    if (unpack)
+      unpack_kernel<float2><<<grid, 256, 0, st>>>(static_cast<const float2*>(in), static_cast<float2*>(out), pl.m,
+                                                  mp, pl.rank, k, pl.nparts);
+    else
+      pack_kernel<float2><<<grid, 256, 0, st>>>(static_cast<const float2*>(in), static_cast<float2*>(out),
+                                                static_cast<const float*>(pl.weights), pl.m, mp, pl.rank, k, pl.part,
+                                                pl.nparts, adjoint);
+  }
+  BF_CUDA(cudaGetLastError());
+  return 0;
 }
 
 int plan_apply_factor(const Plan& pl, int which, int lvl_idx, int adjoint, const void* in, void* out, uint32_t k,

@@ -71,8 +71,8 @@ int bf_last_error(char* buf, size_t len) {
   return BF_OK;
 }
 
-int bf_plan_create(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, uint32_t max_rhs, int dtype,
-                   int device) {
+static int create_plan(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, uint32_t max_rhs, int dtype,
+                       int device, uint32_t part, uint32_t nparts) {
   if (!out) return fail(BF_EINVAL, "null plan output pointer");
   *out = nullptr;
   // DyadicPartition.__post_init__ (partition.py:25-34)
@@ -83,6 +83,8 @@ int bf_plan_create(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, ui
   if (levels > 40) return fail(BF_EINVAL, "tree depth too large");
   if (rank < 1) return fail(BF_EINVAL, "rank must be positive");
   if (dtype != BF_C128 && dtype != BF_C64) return fail(BF_EINVAL, "dtype must be BF_C128 or BF_C64");
+  if (nparts < 1 || part >= nparts || ((1ull << (levels / 2)) % nparts) != 0)
+    return fail(BF_EINVAL, "nparts must divide the middle node count and part < nparts");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
     return fail(BF_EINVAL, "no such CUDA device");
@@ -97,6 +99,8 @@ int bf_plan_create(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, ui
   p.rank = rank;
   p.max_rhs = max_rhs ? max_rhs : 1;
   p.m = 1u << p.half;
+  p.part = part;
+  p.nparts = nparts;
   p.side = n / p.m;
   // construct.py:_level_geometry (216-227)
   uint64_t nodes = p.m, rows = p.side;
@@ -104,7 +108,7 @@ int bf_plan_create(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, ui
     LevelGeo g;
     g.level = lvl;
     g.P = 1ull << (levels - lvl - 1);
-    g.G = nodes;
+    g.G = nodes / nparts;  // this part's groups (the leading index carries the middle node)
     g.splits = rows >= 2;
     g.nblocks = g.G * (g.splits ? 2 : 1) * g.P;
     if (g.splits) {
@@ -114,10 +118,10 @@ int bf_plan_create(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, ui
     p.lev.push_back(g);
   }
   p.nlev = static_cast<uint32_t>(p.lev.size());
-  p.leaf_nb = nodes;
+  p.leaf_nb = nodes / nparts;
   p.leaf_n0 = static_cast<uint32_t>(rows);
   const uint64_t full = (1ull << levels) * rank;
-  p.dim_max = full > n ? full : n;
+  p.dim_max = (full > n ? full : n) / nparts;
   {
     DeviceGuard dg(device);
     cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, device);
@@ -129,6 +133,16 @@ int bf_plan_create(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, ui
   }
   *out = h;
   return BF_OK;
+}
+
+int bf_plan_create(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, uint32_t max_rhs, int dtype,
+                   int device) {
+  return create_plan(out, n, levels, rank, max_rhs, dtype, device, 0, 1);
+}
+
+int bf_plan_create_sharded(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, int dtype, int device,
+                           uint32_t part, uint32_t nparts) {
+  return create_plan(out, n, levels, rank, 1, dtype, device, part, nparts);
 }
 
 void bf_plan_destroy(bf_plan* plan) {
@@ -241,8 +255,51 @@ int bf_apply(const bf_plan* plan, const void* in, void* out, uint32_t k, int adj
   if (!in || !out) return fail(BF_EINVAL, "null input/output pointer");
   if (!workspace || workspace_bytes < bf_apply_workspace_bytes(plan, k))
     return fail(BF_EINVAL, "workspace too small (see bf_apply_workspace_bytes)");
+  if (p.nparts != 1) return fail(BF_EINVAL, "sharded plan: use bf_apply_down / bf_middle_pack / bf_apply_up");
   DeviceGuard dg(p.device);
   return plan_apply(p, in, out, k, adjoint ? 1 : 0, workspace, static_cast<cudaStream_t>(stream));
+}
+
+int bf_apply_down(const bf_plan* plan, const void* in, void* mid, uint32_t k, int adjoint, void* workspace,
+                  uint64_t workspace_bytes, void* stream) {
+  if (!plan) return fail(BF_EINVAL, "null plan");
+  const Plan& p = plan->p;
+  if (!p.uploaded) return fail(BF_ESTATE, "plan has no factors (call bf_plan_upload)");
+  if (k < 1 || !in || !mid) return fail(BF_EINVAL, "bad k or null pointer");
+  if (!workspace || workspace_bytes < bf_apply_workspace_bytes(plan, k))
+    return fail(BF_EINVAL, "workspace too small (see bf_apply_workspace_bytes)");
+  DeviceGuard dg(p.device);
+  return plan_apply_half(p, 0, in, mid, k, adjoint ? 1 : 0, workspace, static_cast<cudaStream_t>(stream));
+}
+
+int bf_apply_up(const bf_plan* plan, const void* mid, void* out, uint32_t k, int adjoint, void* workspace,
+                uint64_t workspace_bytes, void* stream) {
+  if (!plan) return fail(BF_EINVAL, "null plan");
+  const Plan& p = plan->p;
+  if (!p.uploaded) return fail(BF_ESTATE, "plan has no factors (call bf_plan_upload)");
+  if (k < 1 || !mid || !out) return fail(BF_EINVAL, "bad k or null pointer");
+  if (!workspace || workspace_bytes < bf_apply_workspace_bytes(plan, k))
+    return fail(BF_EINVAL, "workspace too small (see bf_apply_workspace_bytes)");
+  DeviceGuard dg(p.device);
+  return plan_apply_half(p, 1, mid, out, k, adjoint ? 1 : 0, workspace, static_cast<cudaStream_t>(stream));
+}
+
+int bf_middle_pack(const bf_plan* plan, const void* mid, void* send, uint32_t k, int adjoint, void* stream) {
+  if (!plan) return fail(BF_EINVAL, "null plan");
+  const Plan& p = plan->p;
+  if (!p.uploaded) return fail(BF_ESTATE, "plan has no factors (call bf_plan_upload)");
+  if (k < 1 || !mid || !send) return fail(BF_EINVAL, "bad k or null pointer");
+  DeviceGuard dg(p.device);
+  return plan_middle_exchange(p, 0, mid, send, k, adjoint ? 1 : 0, static_cast<cudaStream_t>(stream));
+}
+
+int bf_middle_unpack(const bf_plan* plan, const void* recv, void* mid, uint32_t k, int adjoint, void* stream) {
+  if (!plan) return fail(BF_EINVAL, "null plan");
+  const Plan& p = plan->p;
+  if (!p.uploaded) return fail(BF_ESTATE, "plan has no factors (call bf_plan_upload)");
+  if (k < 1 || !recv || !mid) return fail(BF_EINVAL, "bad k or null pointer");
+  DeviceGuard dg(p.device);
+  return plan_middle_exchange(p, 1, recv, mid, k, adjoint ? 1 : 0, static_cast<cudaStream_t>(stream));
 }
 
 int bf_timer_create(bf_timer** out, uint32_t max_steps, uint32_t max_launches) {
@@ -282,6 +339,7 @@ int bf_apply_timed(const bf_plan* plan, const void* in, void* out, uint32_t k, i
   if (k < 1 || !in || !out) return fail(BF_EINVAL, "bad k or null pointer");
   if (!workspace || workspace_bytes < bf_apply_workspace_bytes(plan, k))
     return fail(BF_EINVAL, "workspace too small (see bf_apply_workspace_bytes)");
+  if (p.nparts != 1) return fail(BF_EINVAL, "sharded plan: use bf_apply_down / bf_middle_pack / bf_apply_up");
   DeviceGuard dg(p.device);
   LaunchRecorder rec;
   rec.ev = timer->ev.data() + 2ull * timer->steps * timer->max_launches;
@@ -316,6 +374,7 @@ int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint
   if (!p.uploaded) return fail(BF_ESTATE, "plan has no factors (call bf_plan_upload)");
   if (k < 1) return fail(BF_EINVAL, "need at least one right-hand side");
   if (!in_host || !out_host) return fail(BF_EINVAL, "null input/output pointer");
+  if (p.nparts != 1) return fail(BF_EINVAL, "sharded plan: use bf_apply_down / bf_middle_pack / bf_apply_up");
   DeviceGuard dg(p.device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t io = p.n * k * p.elem();

@@ -239,8 +239,8 @@ __device__ __forceinline__ void consume_tile(const LevelArgs& a, uint32_t tile, 
         out[e * a.k + t.k0 + kk] = v;
       } else {
         const uint32_t mr = a.m * a.r;
-        const uint32_t ia = static_cast<uint32_t>(e / mr);
-        const uint32_t rem = static_cast<uint32_t>(e - static_cast<size_t>(ia) * mr);
+        const uint32_t e32 = static_cast<uint32_t>(e), ia = e32 / mr;
+        const uint32_t rem = e32 - ia * mr;
         const uint32_t ib = rem / a.r, rho = rem - ib * a.r;
         const size_t dst = (static_cast<size_t>(ib) * a.m + ia) * a.r + rho;
         const Rl* W = static_cast<const Rl*>(a.mid_w);
@@ -360,8 +360,8 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, uint32_t t
         Rl w = 1;
         if (a.remap != 0) {
           const uint32_t mr = a.m * a.r;
-          const uint32_t ia = static_cast<uint32_t>(e / mr);
-          const uint32_t rem = static_cast<uint32_t>(e - static_cast<size_t>(ia) * mr);
+          const uint32_t e32 = static_cast<uint32_t>(e), ia = e32 / mr;
+          const uint32_t rem = e32 - ia * mr;
           const uint32_t ib = rem / a.r, rho = rem - ib * a.r;
           const size_t dst = (static_cast<size_t>(ib) * a.m + ia) * a.r + rho;
           const Rl* W = static_cast<const Rl*>(a.mid_w);

@@ -23,6 +23,7 @@ struct Plan {
   uint64_t n = 0;
   uint32_t levels = 0, half = 0, rank = 0, max_rhs = 1;
   uint32_t m = 0;            // middle nodes per side, 2^half
+  uint32_t part = 0, nparts = 1;  // sharded plans hold slice `part` of `nparts`
   uint64_t side = 0;         // n / m
   uint32_t nlev = 0;         // transfer levels per side
   std::vector<LevelGeo> lev;
@@ -58,6 +59,10 @@ struct LaunchRecorder {
 
 int plan_apply(const Plan& pl, const void* in, void* out, uint32_t k, int adjoint, void* ws, cudaStream_t st,
                LaunchRecorder* rec = nullptr);
+int plan_apply_half(const Plan& pl, int up, const void* in, void* out, uint32_t k, int adjoint, void* ws,
+                    cudaStream_t st);
+int plan_middle_exchange(const Plan& pl, int unpack, const void* in, void* out, uint32_t k, int adjoint,
+                         cudaStream_t st);
 int plan_apply_factor(const Plan& pl, int which, int lvl_idx, int adjoint, const void* in, void* out, uint32_t k,
                       cudaStream_t st);
 int entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr, const int64_t* cols, uint32_t nc, void* out,
