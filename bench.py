@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
     ap.add_argument("--rhs", type=int, default=0, help="right-hand sides (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="use the node-sharded path even at one rank")
     return ap.parse_args()
 
 
@@ -295,8 +296,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if world > 1 or args.sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
         return run_sharded(args, world, rank, local)
     kern, n, r, leaf, k0 = CONFIGS[args.config]
     k = args.rhs or k0
