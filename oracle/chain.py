@@ -77,12 +77,12 @@ def transfer_forward(b: np.ndarray, w: np.ndarray) -> np.ndarray:
 
 
 def transfer_adjoint(b: np.ndarray, w: np.ndarray) -> np.ndarray:
-    """factors.py:131-142 (sum over the two row halves t of a splitting level)."""
+    """factors.py:131-142 (sum over the row parts t of a splitting level; 2 in 1-D, 4 on quadtrees)."""
     k = w.shape[-1]
     bh = np.conj(b).swapaxes(-1, -2)
     if b.ndim == 5:
-        groups, _, pairs, r, c = b.shape
-        win = w.reshape(groups, 2, pairs, r, k)
+        groups, nt, pairs, r, c = b.shape
+        win = w.reshape(groups, nt, pairs, r, k)
         return np.matmul(bh, win).sum(axis=1).reshape(-1, k)
     nodes, pairs, r, c = b.shape
     return np.matmul(bh, w.reshape(nodes, pairs, r, k)).reshape(-1, k)

@@ -45,3 +45,51 @@ class EntryOracle:
     def block(self, rows, cols):
         fn = fio_block if self.kind == "fio" else dftp_block
         return fn(self.n, rows, cols)
+
+
+def morton_decode(z, bits: int):
+    """Z-order index -> (a1, a2): bit k of a1 is bit 2k+1 of z, bit k of a2 is bit 2k."""
+    z = np.asarray(z, dtype=np.int64)
+    a1 = np.zeros_like(z)
+    a2 = np.zeros_like(z)
+    for k in range(bits):
+        a2 |= ((z >> (2 * k)) & 1) << k
+        a1 |= ((z >> (2 * k + 1)) & 1) << k
+    return a1, a2
+
+
+def radon2d_block(n_side: int, rows, cols) -> np.ndarray:
+    """BASELINE configs 3/4b: generalized Radon kernel exp(2 pi i Phi) on an n x n grid.
+
+    No reference implementation exists (SPEC.md:8 puts 2-D out of the
+    reference's scope); this restatement defines the convention: indices are
+    Morton (Z-order) numbers so that quadtree nodes are contiguous ranges;
+    x = (a1, a2)/n in [0,1)^2, xi = (b1, b2) - n/2 in [-n/2, n/2)^2,
+    Phi = x.xi + sqrt(c1^2 xi1^2 + c2^2 xi2^2), c1 = (2 + sin 2pi x1 sin 2pi x2)/16,
+    c2 = (2 + cos 2pi x1 cos 2pi x2)/16; one rounding per operation, in this order.
+    """
+    bits = n_side.bit_length() - 1
+    a1, a2 = morton_decode(rows, bits)
+    b1, b2 = morton_decode(cols, bits)
+    x1 = (a1.astype(np.float64) / n_side)[:, None]
+    x2 = (a2.astype(np.float64) / n_side)[:, None]
+    xi1 = (b1.astype(np.float64) - n_side / 2.0)[None, :]
+    xi2 = (b2.astype(np.float64) - n_side / 2.0)[None, :]
+    t1, t2 = TWO_PI * x1, TWO_PI * x2
+    c1 = (2.0 + np.sin(t1) * np.sin(t2)) / 16.0
+    c2 = (2.0 + np.cos(t1) * np.cos(t2)) / 16.0
+    speed = np.sqrt((c1 * c1) * (xi1 * xi1) + (c2 * c2) * (xi2 * xi2))
+    phase = (x1 * xi1 + x2 * xi2) + speed
+    return np.exp(2j * np.pi * phase)
+
+
+class Radon2DOracle:
+    """Entry oracle of the 2-D generalized Radon kernel on an n_side^2 grid (Morton order)."""
+
+    def __init__(self, n_side: int):
+        self.n_side = n_side
+        self.n = n_side * n_side
+        self.shape = (self.n, self.n)
+
+    def block(self, rows, cols):
+        return radon2d_block(self.n_side, rows, cols)

@@ -42,20 +42,33 @@ def node_range(n: int, levels: int, lvl: int, i: int) -> range:
     return range(lo, hi)
 
 
-def level_geometry(n: int, levels: int, r: int):
+def level_geometry(n: int, levels: int, r: int, branching: int = 2):
     """Per-level transfer-array shapes and the leaf shape (construct.py:216-227).
 
     Returns ``([(lvl, splits, shape), ...] ascending from half, leaf_shape)``.
+    ``branching`` = 4 is the quadtree generalisation (BASELINE configs 3/4b; no
+    reference code — DESIGN.md "2-D"): b row parts, b*r-wide blocks.
     """
+    b = branching
     half = levels // 2
-    nodes, rows = 2 ** half, n // 2 ** half
+    nodes, rows = b ** half, n // b ** half
     table = []
     for lvl in range(half, levels):
-        pairs = 2 ** (levels - lvl - 1)
-        if rows >= 2:
-            table.append((lvl, True, (nodes, 2, pairs, r, 2 * r)))
-            nodes *= 2
-            rows //= 2
+        pairs = b ** (levels - lvl - 1)
+        if rows >= b:
+            table.append((lvl, True, (nodes, b, pairs, r, b * r)))
+            nodes *= b
+            rows //= b
         else:
-            table.append((lvl, False, (nodes, pairs, r, 2 * r)))
+            table.append((lvl, False, (nodes, pairs, r, b * r)))
     return table, (nodes, rows, r)
+
+
+def quadtree_levels(n_side: int, leaf_box: int) -> int:
+    """Even quadtree depth with leaf boxes leaf_box x leaf_box on an n_side^2 grid."""
+    if n_side & (n_side - 1) or leaf_box & (leaf_box - 1) or leaf_box > n_side:
+        raise ValueError("grid and leaf box sides must be powers of two")
+    depth = (n_side // leaf_box).bit_length() - 1
+    if depth < 2 or depth % 2:
+        raise ValueError(f"quadtree depth {depth} must be even and >= 2")
+    return depth
