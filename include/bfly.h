@@ -132,6 +132,11 @@ int bf_timer_read(bf_timer* timer, float* launch_ms, uint32_t* steps, uint32_t* 
  * adjoint = 1 runs K* the same way (U*, G* down; H, V up). */
 int bf_plan_create_sharded(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, int dtype, int device,
                            uint32_t part, uint32_t nparts);
+/* General tree: branching 2 (the reference's binary trees) or 4 (quadtrees
+ * over Morton-ordered 2-D grids, BASELINE configs 3/4b; transfer blocks
+ * (G, 4, P, r, 4r)); nparts = 1 for an unsharded plan. */
+int bf_plan_create_tree(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, uint32_t branching,
+                        int dtype, int device, uint32_t part, uint32_t nparts);
 int bf_apply_down(const bf_plan* plan, const void* in, void* mid, uint32_t k, int adjoint,
                   void* workspace, uint64_t workspace_bytes, void* stream);
 int bf_middle_pack(const bf_plan* plan, const void* mid, void* send, uint32_t k, int adjoint, void* stream);

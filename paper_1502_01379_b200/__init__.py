@@ -11,7 +11,8 @@ from .factors import (BlockDiagonalFactor, ButterflyFactors, DevicePlan, MiddleF
 from .construct import (DEFAULT_PARAMS, OversamplingParams, factorize, middle_factorization_sampling,
                         recursive_factor_u, recursive_factor_v)
 from .kernels import DenseOracle, DftPlusKernel, FioKernel, fio_entry
-from .partition import BlockId, DyadicPartition, block_cols, block_rows, level_geometry, make_partition
+from .partition import (BlockId, DyadicPartition, QuadtreePartition, block_cols, block_rows, level_geometry,
+                        make_partition, make_quadtree_partition)
 
 __all__ = [n for n in dir() if not n.startswith("_")]
 __version__ = "0.1.0"

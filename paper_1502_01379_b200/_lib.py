@@ -42,6 +42,7 @@ SIGNATURES = [
     ("bf_recurse_level", _I, [_U32, _U64, _U64, _U64, _P, _P, _P, _P, ctypes.POINTER(_U64), _P]),
     ("bf_select_pivots", _I, [_P, _U32, _U32, _U32, _U32, ctypes.c_double, _I, _P, _P, _P, _U64, _P]),
     ("bf_plan_create_sharded", _I, [ctypes.POINTER(_P), _U64, _U32, _U32, _I, _I, _U32, _U32]),
+    ("bf_plan_create_tree", _I, [ctypes.POINTER(_P), _U64, _U32, _U32, _U32, _I, _I, _U32, _U32]),
     ("bf_apply_down", _I, [_P, _P, _P, _U32, _I, _P, _U64, _P]),
     ("bf_middle_pack", _I, [_P, _P, _P, _U32, _I, _P]),
     ("bf_middle_unpack", _I, [_P, _P, _P, _U32, _I, _P]),

@@ -51,8 +51,35 @@ constexpr Shape kMrhs{2, 8, 1, 100 * 1024};
 constexpr uint32_t kMrhsMinK = 8;
 
 template <typename E>
+int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint32_t ntot, uint32_t t0,
+                   int accumulate, uint64_t P, uint64_t units, const void* in, void* out, uint32_t k, int adjoint,
+                   int remap, cudaStream_t st);
+
+// One factor launch. A unit's nt blocks normally share one tile; when they do
+// not fit a shared-memory stage (quadtree rank 25: 4 x 25 x 100 complex128 =
+// 160 KB) the blocks are split into t-ranges, one launch each: forward outputs
+// are disjoint per t, adjoint partial sums accumulate into the output.
+template <typename E>
 int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint64_t P, uint64_t units,
                  const void* in, void* out, uint32_t k, int adjoint, int remap, cudaStream_t st) {
+  const Shape sh = k >= kMrhsMinK ? kMrhs : kStream;
+  uint32_t nt_tile = nt;
+  auto tile_elems = [&](uint64_t t) { return t * R * C + (adjoint ? t * R : static_cast<uint64_t>(C)); };
+  while (nt_tile > 1 && tile_elems(nt_tile) * sizeof(E) > sh.stage_bytes) nt_tile /= 2;
+  if (nt_tile == nt)
+    return launch_level_t<E>(pl, fac, R, C, nt, nt, 0, 0, P, units, in, out, k, adjoint, remap, st);
+  for (uint32_t t0 = 0; t0 < nt; t0 += nt_tile) {
+    const int rc = launch_level_t<E>(pl, fac, R, C, nt_tile, nt, t0, adjoint && t0 > 0, P, units, in, out, k,
+                                     adjoint, remap, st);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+template <typename E>
+int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint32_t ntot, uint32_t t0,
+                   int accumulate, uint64_t P, uint64_t units, const void* in, void* out, uint32_t k, int adjoint,
+                   int remap, cudaStream_t st) {
   if (units >= (1ull << 31)) return fail(BF_EINVAL, "level has too many blocks for one launch");
   if (remap && static_cast<uint64_t>(pl.m) * pl.m * pl.rank >= (1ull << 32))
     return fail(BF_EINVAL, "middle vector too long for 32-bit remap indices");
@@ -66,6 +93,9 @@ int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32
   a.R = R;
   a.C = C;
   a.nt = nt;
+  a.ntot = ntot;
+  a.t0 = t0;
+  a.accumulate = accumulate;
   a.lgP = ilog2(P);
   a.units = static_cast<uint32_t>(units);
   a.k = k;
@@ -89,7 +119,7 @@ int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32
   const uint64_t tile_rows = kt >= 32 ? (kt >= 128 ? 4 : kt >= 64 ? 8 : 16) : (kt >= 16 ? 16 : 16);
   const uint64_t tile_cols = kt >= 128 ? 128 : kt >= 64 ? 64 : kt >= 32 ? 32 : kt >= 16 ? 16 : 8;
   auto items = [&](uint64_t u) { return u * ((m_out + tile_rows - 1) / tile_rows) * ((kt + tile_cols - 1) / tile_cols) * 32; };
-  while (U * 2 <= units && (U * 2) * (fac_unit + vec_col * kt) * esz <= sh.stage_bytes &&
+  while (nt == ntot && U * 2 <= units && (U * 2) * (fac_unit + vec_col * kt) * esz <= sh.stage_bytes &&
          (!mrhs || items(U) < want_items))
     U *= 2;
   a.kt = kt;
@@ -138,8 +168,8 @@ int factor_op(const Plan& pl, int which, int lvl_idx, int adjoint, const void* i
   if (which == BF_FACTOR_M) return launch_middle<E>(pl, in, out, k, adjoint, st);
   const LevelGeo& lg = pl.lev[lvl_idx];
   const void* fac = which == BF_FACTOR_G ? pl.g_lev[lvl_idx] : pl.h_lev[lvl_idx];
-  return launch_level<E>(pl, fac, pl.rank, 2 * pl.rank, lg.splits ? 2 : 1, lg.P, lg.G * lg.P, in, out, k, adjoint,
-                         remap, st);
+  return launch_level<E>(pl, fac, pl.rank, pl.branch * pl.rank, lg.splits ? pl.branch : 1, lg.P, lg.G * lg.P, in, out,
+                         k, adjoint, remap, st);
 }
 
 template <typename E>

@@ -72,18 +72,20 @@ int bf_last_error(char* buf, size_t len) {
 }
 
 static int create_plan(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, uint32_t max_rhs, int dtype,
-                       int device, uint32_t part, uint32_t nparts) {
+                       int device, uint32_t part, uint32_t nparts, uint32_t branch) {
   if (!out) return fail(BF_EINVAL, "null plan output pointer");
   *out = nullptr;
   // DyadicPartition.__post_init__ (partition.py:25-34)
   if (n < 4 || !is_pow2(n)) return fail(BF_EINVAL, "matrix dimension must be a power of two >= 4");
   if (levels < 2 || levels % 2) return fail(BF_EINVAL, "tree depth must be even and >= 2");
-  if (levels / 2 >= 63 || (1ull << (levels / 2)) > n)
+  if (branch != 2 && branch != 4) return fail(BF_EINVAL, "branching must be 2 (binary tree) or 4 (quadtree)");
+  const uint32_t lb = branch == 4 ? 2 : 1;  // log2(branching)
+  if (branch == 4 && ((63 - __builtin_clzll(n)) % 2)) return fail(BF_EINVAL, "quadtree dimension must be a power of 4");
+  if (levels > 40 || lb * (levels / 2) >= 63 || (1ull << (lb * (levels / 2))) > n)
     return fail(BF_EINVAL, "depth puts more nodes than n on the middle level");
-  if (levels > 40) return fail(BF_EINVAL, "tree depth too large");
   if (rank < 1) return fail(BF_EINVAL, "rank must be positive");
   if (dtype != BF_C128 && dtype != BF_C64) return fail(BF_EINVAL, "dtype must be BF_C128 or BF_C64");
-  if (nparts < 1 || part >= nparts || ((1ull << (levels / 2)) % nparts) != 0)
+  if (nparts < 1 || part >= nparts || ((1ull << (lb * (levels / 2))) % nparts) != 0)
     return fail(BF_EINVAL, "nparts must divide the middle node count and part < nparts");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
@@ -98,7 +100,8 @@ static int create_plan(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank
   p.half = levels / 2;
   p.rank = rank;
   p.max_rhs = max_rhs ? max_rhs : 1;
-  p.m = 1u << p.half;
+  p.branch = branch;
+  p.m = 1u << (lb * p.half);
   p.part = part;
   p.nparts = nparts;
   p.side = n / p.m;
@@ -107,20 +110,20 @@ static int create_plan(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank
   for (uint32_t lvl = p.half; lvl < levels; ++lvl) {
     LevelGeo g;
     g.level = lvl;
-    g.P = 1ull << (levels - lvl - 1);
+    g.P = 1ull << (lb * (levels - lvl - 1));
     g.G = nodes / nparts;  // this part's groups (the leading index carries the middle node)
-    g.splits = rows >= 2;
-    g.nblocks = g.G * (g.splits ? 2 : 1) * g.P;
+    g.splits = rows >= branch;
+    g.nblocks = g.G * (g.splits ? branch : 1) * g.P;
     if (g.splits) {
-      nodes *= 2;
-      rows /= 2;
+      nodes *= branch;
+      rows /= branch;
     }
     p.lev.push_back(g);
   }
   p.nlev = static_cast<uint32_t>(p.lev.size());
   p.leaf_nb = nodes / nparts;
   p.leaf_n0 = static_cast<uint32_t>(rows);
-  const uint64_t full = (1ull << levels) * rank;
+  const uint64_t full = (1ull << (lb * levels)) * rank;
   p.dim_max = (full > n ? full : n) / nparts;
   {
     DeviceGuard dg(device);
@@ -137,12 +140,17 @@ static int create_plan(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank
 
 int bf_plan_create(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, uint32_t max_rhs, int dtype,
                    int device) {
-  return create_plan(out, n, levels, rank, max_rhs, dtype, device, 0, 1);
+  return create_plan(out, n, levels, rank, max_rhs, dtype, device, 0, 1, 2);
 }
 
 int bf_plan_create_sharded(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, int dtype, int device,
                            uint32_t part, uint32_t nparts) {
-  return create_plan(out, n, levels, rank, 1, dtype, device, part, nparts);
+  return create_plan(out, n, levels, rank, 1, dtype, device, part, nparts, 2);
+}
+
+int bf_plan_create_tree(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank, uint32_t branching, int dtype,
+                        int device, uint32_t part, uint32_t nparts) {
+  return create_plan(out, n, levels, rank, 1, dtype, device, part, nparts, branching);
 }
 
 void bf_plan_destroy(bf_plan* plan) {
@@ -164,9 +172,9 @@ int bf_plan_geometry(const bf_plan* plan, uint32_t* nlev, int8_t* splits, uint64
     if (dims) {
       uint64_t* d = dims + 5ull * i;
       if (g.splits) {
-        d[0] = g.G; d[1] = 2; d[2] = g.P; d[3] = p.rank; d[4] = 2ull * p.rank;
+        d[0] = g.G; d[1] = p.branch; d[2] = g.P; d[3] = p.rank; d[4] = static_cast<uint64_t>(p.branch) * p.rank;
       } else {
-        d[0] = g.G; d[1] = g.P; d[2] = p.rank; d[3] = 2ull * p.rank; d[4] = 0;
+        d[0] = g.G; d[1] = g.P; d[2] = p.rank; d[3] = static_cast<uint64_t>(p.branch) * p.rank; d[4] = 0;
       }
     }
   }
@@ -188,7 +196,7 @@ int bf_plan_upload(bf_plan* plan, const void* u_leaf, const void* const* g_level
   const uint64_t leaf_elems = p.leaf_nb * p.leaf_n0 * p.rank;
   const uint64_t w_elems = static_cast<uint64_t>(p.m) * p.m * p.rank;
   uint64_t bytes = 2 * align_up(leaf_elems * es, 256) + align_up(w_elems * rs, 256);
-  for (const LevelGeo& g : p.lev) bytes += 2 * align_up(g.nblocks * p.rank * 2ull * p.rank * es, 256);
+  for (const LevelGeo& g : p.lev) bytes += 2 * align_up(g.nblocks * p.rank * p.branch * p.rank * es, 256);
   if (!p.base) {
     cudaError_t e = cudaMalloc(&p.base, bytes);
     if (e != cudaSuccess) {
@@ -208,8 +216,8 @@ int bf_plan_upload(bf_plan* plan, const void* u_leaf, const void* const* g_level
   p.weights = carve(w_elems * rs);
   p.g_lev.assign(p.nlev, nullptr);
   p.h_lev.assign(p.nlev, nullptr);
-  for (uint32_t i = 0; i < p.nlev; ++i) p.g_lev[i] = carve(p.lev[i].nblocks * p.rank * 2ull * p.rank * es);
-  for (uint32_t i = 0; i < p.nlev; ++i) p.h_lev[i] = carve(p.lev[i].nblocks * p.rank * 2ull * p.rank * es);
+  for (uint32_t i = 0; i < p.nlev; ++i) p.g_lev[i] = carve(p.lev[i].nblocks * p.rank * p.branch * p.rank * es);
+  for (uint32_t i = 0; i < p.nlev; ++i) p.h_lev[i] = carve(p.lev[i].nblocks * p.rank * p.branch * p.rank * es);
 
   cudaStream_t st = nullptr;
   void* tmp = nullptr;
@@ -218,7 +226,7 @@ int bf_plan_upload(bf_plan* plan, const void* u_leaf, const void* const* g_level
   int rc = upload_complex(p, u_leaf, p.u_leaf, leaf_elems, tmp, tmp_elems, st);
   if (!rc) rc = upload_complex(p, v_leaf, p.v_leaf, leaf_elems, tmp, tmp_elems, st);
   for (uint32_t i = 0; !rc && i < p.nlev; ++i) {
-    const uint64_t c = p.lev[i].nblocks * p.rank * 2ull * p.rank;
+    const uint64_t c = p.lev[i].nblocks * p.rank * p.branch * p.rank;
     rc = upload_complex(p, g_levels[i], p.g_lev[i], c, tmp, tmp_elems, st);
     if (!rc) rc = upload_complex(p, h_levels[i], p.h_lev[i], c, tmp, tmp_elems, st);
   }

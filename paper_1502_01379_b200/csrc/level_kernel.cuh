@@ -37,7 +37,9 @@ struct LevelArgs {
   const void* in;     // input vector (rows x k)
   void* out;          // output vector
   const void* mid_w;  // middle weights (m, m, r) in plan real type, when remap != 0
-  uint32_t R, C, nt;
+  uint32_t R, C, nt;  // nt: blocks of a unit held per tile (a t-range of ntot)
+  uint32_t ntot, t0;  // blocks per unit (2 in 1-D, 4 on quadtrees) and the first t of this launch
+  int accumulate;     // adjoint with a t-range split: add into out instead of storing
   uint32_t lgP;       // log2(units per group)
   uint32_t units;
   uint32_t k;         // total right-hand sides (row length of in/out)
@@ -77,13 +79,13 @@ __device__ __forceinline__ TileGeo tile_geo(const LevelArgs& a, uint32_t tile) {
     t.lgPe = a.lgU;
     t.segs = a.nt;
     t.seg_blocks = 1u << a.lgU;
-    t.seg0 = ((g0 * a.nt) << a.lgP) + p0;
+    t.seg0 = ((g0 * a.ntot + a.t0) << a.lgP) + p0;
     t.seg_step = 1u << a.lgP;
   } else {
     t.lgPe = a.lgP;
     t.segs = 1;
     t.seg_blocks = a.nt << a.lgU;
-    t.seg0 = (g0 * a.nt) << a.lgP;
+    t.seg0 = (g0 * a.ntot) << a.lgP;  // (only with nt == ntot, t0 == 0)
     t.seg_step = 0;
   }
   return t;
@@ -189,8 +191,8 @@ __device__ __forceinline__ void consume_tile(const LevelArgs& a, uint32_t tile, 
       }
       const uint32_t rho = rest % a.R;
       rest /= a.R;
-      const uint32_t tt = a.nt == 2 ? (rest & 1) : 0;
-      const uint32_t ul = a.nt == 2 ? (rest >> 1) : rest;
+      const uint32_t tt = rest % a.nt;
+      const uint32_t ul = rest / a.nt;
       const uint32_t slot = ((((ul >> t.lgPe) * a.nt) + tt) << t.lgPe) + (ul & Pe_mask);
       const E* arow = fs + (static_cast<size_t>(slot) * a.R + rho) * a.C;
       const E* x = vs + static_cast<size_t>(ul) * a.C * kc + kk;
@@ -207,7 +209,7 @@ __device__ __forceinline__ void consume_tile(const LevelArgs& a, uint32_t tile, 
       }
       if (j < a.C) acc.mac(0, arow[c], x[static_cast<size_t>(c) * kc]);
       const uint32_t u = t.u0 + ul;
-      const uint32_t q = ((((u >> a.lgP) * a.nt) + tt) << a.lgP) + (u & P_mask);
+      const uint32_t q = ((((u >> a.lgP) * a.ntot) + a.t0 + tt) << a.lgP) + (u & P_mask);
       out[(static_cast<size_t>(q) * a.R + rho) * a.k + t.k0 + kk] = acc.sum();
     }
   } else {
@@ -236,7 +238,8 @@ __device__ __forceinline__ void consume_tile(const LevelArgs& a, uint32_t tile, 
       const E v = acc.sum_conj();
       const size_t e = static_cast<size_t>(t.u0 + ul) * a.C + c;
       if (a.remap == 0) {
-        out[e * a.k + t.k0 + kk] = v;
+        E& o_ = out[e * a.k + t.k0 + kk];
+        o_ = a.accumulate ? Cx<E>::make(o_.x + v.x, o_.y + v.y) : v;
       } else {
         const uint32_t mr = a.m * a.r;
         const uint32_t e32 = static_cast<uint32_t>(e), ia = e32 / mr;
@@ -245,7 +248,8 @@ __device__ __forceinline__ void consume_tile(const LevelArgs& a, uint32_t tile, 
         const size_t dst = (static_cast<size_t>(ib) * a.m + ia) * a.r + rho;
         const Rl* W = static_cast<const Rl*>(a.mid_w);
         const Rl w = a.remap == 1 ? W[dst] : W[(static_cast<size_t>(ia) * a.m + ib) * a.r + rho];
-        out[dst * a.k + t.k0 + kk] = Cx<E>::make(w * v.x, w * v.y);
+        E& o_ = out[dst * a.k + t.k0 + kk];
+        o_ = a.accumulate ? Cx<E>::make(o_.x + w * v.x, o_.y + w * v.y) : Cx<E>::make(w * v.x, w * v.y);
       }
     }
   }
@@ -323,7 +327,7 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, uint32_t t
         const uint32_t o = row0 + i;
         if (o >= m_out) break;
         const uint32_t tt = o / a.R, rho = o - tt * a.R;
-        const uint32_t q = ((((u >> a.lgP) * a.nt) + tt) << a.lgP) + (u & P_mask);
+        const uint32_t q = ((((u >> a.lgP) * a.ntot) + a.t0 + tt) << a.lgP) + (u & P_mask);
         E* dst = out + (static_cast<size_t>(q) * a.R + rho) * a.k + t.k0 + col0;
 #pragma unroll
         for (int j = 0; j < TN; ++j)
@@ -371,7 +375,10 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, uint32_t t
         E* dst = out + e * a.k + t.k0 + col0;
 #pragma unroll
         for (int j = 0; j < TN; ++j)
-          if (colok[j]) dst[j * LC] = Cx<E>::make(w * re[i][j], w * im[i][j]);
+          if (colok[j]) {
+            const E v = Cx<E>::make(w * re[i][j], w * im[i][j]);
+            dst[j * LC] = a.accumulate ? Cx<E>::make(dst[j * LC].x + v.x, dst[j * LC].y + v.y) : v;
+          }
       }
     }
   }

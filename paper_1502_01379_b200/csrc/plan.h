@@ -23,6 +23,7 @@ struct Plan {
   uint64_t n = 0;
   uint32_t levels = 0, half = 0, rank = 0, max_rhs = 1;
   uint32_t m = 0;            // middle nodes per side, 2^half
+  uint32_t branch = 2;       // tree branching: 2 (reference, 1-D), 4 (quadtree, BASELINE configs 3/4b)
   uint32_t part = 0, nparts = 1;  // sharded plans hold slice `part` of `nparts`
   uint64_t side = 0;         // n / m
   uint32_t nlev = 0;         // transfer levels per side

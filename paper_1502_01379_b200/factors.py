@@ -80,25 +80,28 @@ class TransferFactor:
 
     @property
     def shape(self):
-        r, p = self.rank, self.pairs
+        r, p, c = self.rank, self.pairs, self.blocks.shape[-1]
         if self.splits:
-            return (2 * self.blocks.shape[0] * p * r,) * 2
+            g, nt = self.blocks.shape[0], self.blocks.shape[1]
+            return (nt * g * p * r, g * p * c)
         nodes = self.blocks.shape[0]
-        return (nodes * p * r, 2 * nodes * p * r)
+        return (nodes * p * r, nodes * p * c)
 
     def iter_blocks(self):
-        """Block offsets exactly as factors.py:97-112 (the .bfac header order)."""
+        """Block offsets exactly as factors.py:97-112 (the .bfac header order); nt row
+        parts and c = nt*r columns per block (nt = 2 in the reference, 4 on quadtrees)."""
         b = _np(self.blocks)
-        r, p = self.rank, self.pairs
+        r, p, c = self.rank, self.pairs, b.shape[-1]
         if self.splits:
+            nt = b.shape[1]
             for g in range(b.shape[0]):
-                for t in range(2):
+                for t in range(nt):
                     for j in range(p):
-                        yield (2 * g + t) * p * r + j * r, g * 2 * p * r + 2 * j * r, b[g, t, j]
+                        yield (nt * g + t) * p * r + j * r, g * p * c + j * c, b[g, t, j]
         else:
             for node in range(b.shape[0]):
                 for j in range(p):
-                    yield node * p * r + j * r, node * 2 * p * r + 2 * j * r, b[node, j]
+                    yield node * p * r + j * r, node * p * c + j * c, b[node, j]
 
     def dense(self) -> np.ndarray:
         out = np.zeros(self.shape, dtype=np.complex128)
@@ -165,8 +168,9 @@ class DevicePlan:
         self.torch_dtype = torch.complex128 if dtype == "c128" else torch.complex64
         self.np_dtype = np.complex128 if dtype == "c128" else np.complex64
         h = ctypes.c_void_p()
-        _lib.check(lib.bf_plan_create(ctypes.byref(h), f.n, f.partition.levels, f.rank, 1,
-                                      _DTYPES[dtype], self.device), "bf_plan_create")
+        _lib.check(lib.bf_plan_create_tree(ctypes.byref(h), f.n, f.partition.levels, f.rank,
+                                           getattr(f.partition, "branching", 2), _DTYPES[dtype], self.device, 0, 1),
+                   "bf_plan_create_tree")
         self._h = h
         self._lib = lib
         self._check_geometry(f)
@@ -299,9 +303,9 @@ class DevicePlan:
             return rows_in
         shp = self._shapes[level - self._half]
         if len(shp) == 5:
-            rows = cols = 2 * shp[0] * shp[2] * shp[3]
+            rows, cols = shp[0] * shp[1] * shp[2] * shp[3], shp[0] * shp[2] * shp[4]
         else:
-            rows, cols = shp[0] * shp[1] * shp[2], 2 * shp[0] * shp[1] * shp[2]
+            rows, cols = shp[0] * shp[1] * shp[2], shp[0] * shp[1] * shp[3]
         return cols if adjoint else rows
 
 
@@ -383,9 +387,9 @@ def factors_equal(a: ButterflyFactors, b: ButterflyFactors) -> bool:
     return all(tuple(x.shape) == tuple(y.shape) and np.array_equal(_np(x), _np(y)) for x, y in pairs)
 
 
-def from_arrays(n, levels, rank, u_leaf, g_levels, weights, h_levels, v_leaf) -> ButterflyFactors:
+def from_arrays(n, levels, rank, u_leaf, g_levels, weights, h_levels, v_leaf, partition=None) -> ButterflyFactors:
     """Assemble a chain from raw arrays; g_levels/h_levels are [(level, blocks)] ascending."""
-    p = DyadicPartition(int(n), int(levels))
+    p = partition if partition is not None else DyadicPartition(int(n), int(levels))
     return ButterflyFactors(p, int(rank), BlockDiagonalFactor(u_leaf),
                             tuple(TransferFactor(int(l), b) for l, b in g_levels), MiddleFactor(weights),
                             tuple(TransferFactor(int(l), b) for l, b in h_levels), BlockDiagonalFactor(v_leaf))

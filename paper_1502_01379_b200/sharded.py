@@ -99,9 +99,9 @@ class ShardedPlan(ShardedApply):
         self.device = torch.cuda.current_device() if device is None else int(device)
         self.tdt = torch.complex128 if dtype == "c128" else torch.complex64
         h = ctypes.c_void_p()
-        _lib.check(self.lib.bf_plan_create_sharded(ctypes.byref(h), p.n, p.levels, r,
-                                                   _lib.BF_C128 if dtype == "c128" else _lib.BF_C64, self.device,
-                                                   part, nparts), "bf_plan_create_sharded")
+        _lib.check(self.lib.bf_plan_create_tree(ctypes.byref(h), p.n, p.levels, r, getattr(p, "branching", 2),
+                                                _lib.BF_C128 if dtype == "c128" else _lib.BF_C64, self.device,
+                                                part, nparts), "bf_plan_create_tree")
         self._h = h
         shapes, leaf_shape = level_geometry(p, r)
         keep = []

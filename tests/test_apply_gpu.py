@@ -191,3 +191,21 @@ def test_entries_match_reference_golden():
                               ctypes.c_void_p(cols.data_ptr()), cols.numel(), ctypes.c_void_p(out.data_ptr()), None))
     torch.cuda.synchronize()
     assert np.max(np.abs(out.cpu().numpy() - d["dftp"])) <= 4e-16   # exact phase; sin/cos ulps only
+
+
+@pytest.mark.parametrize("n_side,leaf,r,k", [
+    (64, 4, 8, 3),        # quadtree depth 4
+    (256, 4, 25, 16),     # BASELINE config 3 geometry: n=256, leaf 4x4, r=25, 16 RHS
+    (128, 2, 25, 1),      # r=25 one RHS: t-range split of the 4 x 25 x 100 block units
+])
+def test_quadtree_geometries(n_side, leaf, r, k):
+    """2-D (branching 4) chains against the oracle's quadtree restatement (parity unpinned:
+    no reference 2-D code exists)."""
+    p = bf.make_quadtree_partition(n_side, leaf)
+    f = synthetic_chain(p, r, seed=n_side + r)
+    oc = oracle_of(f)
+    g = complex_gaussian(np.random.default_rng(k), (p.n, k))
+    gd = torch.from_numpy(g).cuda()
+    assert rel(f.plan().apply(gd), ochain.apply(oc, g)) <= TOL128
+    assert rel(f.plan().apply(gd, adjoint=True), ochain.apply(oc, g, adjoint=True)) <= TOL128
+    assert rel(f.plan("c64").apply(gd).to(torch.complex128), ochain.apply(oc, g)) <= TOL64

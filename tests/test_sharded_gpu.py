@@ -61,3 +61,14 @@ def test_sharded_plan_rejects_full_apply_and_bad_parts():
     assert rc == _lib.BF_EINVAL
     with pytest.raises(ValueError):
         ShardedPlan.from_factors(f, 0, 3)
+
+
+def test_sharded_quadtree_steps():
+    p = bf.make_quadtree_partition(64, 4)
+    f = synthetic_chain(p, 8, seed=4)
+    plans = [ShardedPlan.from_factors(f, d, 4) for d in range(4)]
+    g = torch.from_numpy(complex_gaussian(np.random.default_rng(2), (p.n, 2))).cuda()
+    for adjoint in (False, True):
+        want = f.plan().apply(g, adjoint=adjoint)
+        got = emulate(plans, g, adjoint)
+        assert (torch.linalg.norm(got - want) / torch.linalg.norm(want)).item() <= 1e-13
