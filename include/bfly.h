@@ -54,6 +54,7 @@ extern "C" {
 #define BF_KERNEL_FIO 0  /* exp(2 pi i (x xi + c(x)|xi|)), x=i/N, xi=j-N/2 (kernels.py:27-38) */
 #define BF_KERNEL_DFTP 1 /* exp(+2 pi i (j k mod N)/N) — BASELINE config 1                   */
 #define BF_KERNEL_DENSE 2 /* explicit n x n complex128 matrix on the device (DenseOracle)    */
+#define BF_KERNEL_RADON2D 3 /* 2-D generalized Radon, n = n_side^2 Morton indices (cfg 3/4b)   */
 
 typedef struct bf_plan bf_plan;
 
@@ -163,22 +164,26 @@ int bf_entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr,
  * branch). dense: device n x n complex128 for BF_KERNEL_DENSE, else NULL.
  * Outputs (device): u_out, v_out (nblocks, side, r) complex128 = u0*sigma0,
  * v0*sigma0; w_out (nblocks, r) f64 = floored_inverse(sigma0) — exactly what
- * construct.py:63-65 scatters into U^h, V^h and M. Requires r*(q+1) <= 64.
+ * construct.py:63-65 scatters into U^h, V^h and M. branching 2 (binary tree)
+ * or 4 (quadtree, middle blocks = contiguous Morton ranges). Requires
+ * r*(q+1) <= 128 (shared-memory small matrices up to 64, global above).
  */
-uint64_t bf_middle_workspace_bytes(uint64_t n, uint32_t levels, uint32_t rank, uint32_t nblocks);
-int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t rank, uint32_t q_over,
-                     uint32_t iters, const void* dense, uint32_t nblocks, const int32_t* block_ij,
+uint64_t bf_middle_workspace_bytes(uint64_t n, uint32_t levels, uint32_t branching, uint32_t rank,
+                                   uint32_t q_over, uint32_t nblocks);
+int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branching, uint32_t rank,
+                     uint32_t q_over, uint32_t iters, const void* dense, uint32_t nblocks, const int32_t* block_ij,
                      const int32_t* draws, void* u_out, void* v_out, double* w_out,
                      void* workspace, uint64_t ws_bytes, void* stream);
 
-/* One level of _recurse (construct.py:127-163): cur (nb, rows, groups, r)
- * complex128 -> transfer blocks (nb, 2, groups/2, r, 2r) when rows >= 2 (SVD
- * of each (rows/2 x 2r) stack; keep = min(r, rows/2)) or (nb, groups/2, r, 2r)
- * when rows == 1, and the next cur (2nb, rows/2, groups/2, r) or
- * (nb, 1, groups/2, r). With workspace == NULL, *ws_bytes receives the
- * scratch size. Requires 2r <= 64. */
-int bf_recurse_level(uint32_t rank, uint64_t nb, uint64_t rows, uint64_t groups, const void* cur,
-                     void* blocks, void* next, void* workspace, uint64_t* ws_bytes, void* stream);
+/* One level of _recurse (construct.py:127-163) with branching b (2; 4 on
+ * quadtrees): cur (nb, rows, groups, r) complex128 -> transfer blocks
+ * (nb, b, groups/b, r, b r) when rows >= b (SVD of each (rows/b x b r) stack;
+ * keep = min(r, rows/b)) or (nb, groups/b, r, b r) when rows < b, and the next
+ * cur (b nb, rows/b, groups/b, r) or (nb, 1, groups/b, r). With workspace ==
+ * NULL, *ws_bytes receives the scratch size. Requires b r <= 128. */
+int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t rows, uint64_t groups,
+                     const void* cur, void* blocks, void* next, void* workspace, uint64_t* ws_bytes,
+                     void* stream);
 
 /* Greedy pivoted column selection (select_pivot_columns, lowrank.py:102-129)
  * on a batch of device matrices a (batch, m, n) complex128 row-major with

@@ -10,7 +10,7 @@ from .factors import (BlockDiagonalFactor, ButterflyFactors, DevicePlan, MiddleF
                       TransferFactor, factors_equal, from_arrays)
 from .construct import (DEFAULT_PARAMS, OversamplingParams, factorize, middle_factorization_sampling,
                         recursive_factor_u, recursive_factor_v)
-from .kernels import DenseOracle, DftPlusKernel, FioKernel, fio_entry
+from .kernels import DenseOracle, DftPlusKernel, FioKernel, Radon2DKernel, fio_entry
 from .partition import (BlockId, DyadicPartition, QuadtreePartition, block_cols, block_rows, level_geometry,
                         make_partition, make_quadtree_partition)
 

@@ -87,7 +87,7 @@ class _DeviceOracle:
         self.dense = None
         kid = getattr(oracle, "kernel_id", None)
         name = type(oracle).__name__
-        if kid in (_lib.BF_KERNEL_FIO, _lib.BF_KERNEL_DFTP):
+        if kid in (_lib.BF_KERNEL_FIO, _lib.BF_KERNEL_DFTP, _lib.BF_KERNEL_RADON2D):
             self.kernel_id = kid
         elif name == "FioKernel" and getattr(oracle, "n", None) == n:   # the reference's own class
             self.kernel_id = _lib.BF_KERNEL_FIO
@@ -112,6 +112,7 @@ class MiddleSampler:
         if self.side < r:
             raise ValueError(f"middle blocks are {self.side} wide, below rank {r}")
         self.dev = _DeviceOracle(oracle, p.n)
+        self.branching = getattr(p, "branching", 2)
         self.dense_branch = r * params.q >= self.side
 
     def blocks(self, ij):
@@ -128,12 +129,14 @@ class MiddleSampler:
             draws_d = None
         else:
             draws_d = torch.from_numpy(draw_tables(self.seed, side, r, self.params, ij.tolist())).cuda()
-        wsb = int(self.lib.bf_middle_workspace_bytes(self.p.n, self.p.levels, r, nb))
+        wsb = int(self.lib.bf_middle_workspace_bytes(self.p.n, self.p.levels, self.branching, r, self.params.q, nb))
+        if wsb == 0:
+            raise ValueError("geometry/rank not supported by the batched sampling kernels (need r*(q+1) <= 128)")
         ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
         dense = ctypes.c_void_p(self.dev.dense.data_ptr()) if self.dev.dense is not None else None
         stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-        rc = self.lib.bf_middle_blocks(self.dev.kernel_id, self.p.n, self.p.levels, r, self.params.q,
-                                       self.params.iters, dense, nb, ctypes.c_void_p(ij_d.data_ptr()),
+        rc = self.lib.bf_middle_blocks(self.dev.kernel_id, self.p.n, self.p.levels, self.branching, r,
+                                       self.params.q, self.params.iters, dense, nb, ctypes.c_void_p(ij_d.data_ptr()),
                                        ctypes.c_void_p(draws_d.data_ptr()) if draws_d is not None else None,
                                        ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(v.data_ptr()),
                                        ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(ws.data_ptr()), wsb, stream)
@@ -146,7 +149,8 @@ class MiddleSampler:
 
     def batch_rows(self) -> int:
         """Block-rows per launch: enough CTAs to fill the GPU, bounded workspace."""
-        per_block = max(1, int(self.lib.bf_middle_workspace_bytes(self.p.n, self.p.levels, self.r, 1)))
+        per_block = max(1, int(self.lib.bf_middle_workspace_bytes(self.p.n, self.p.levels, self.branching, self.r,
+                                                                  self.params.q, 1)))
         by_mem = max(1, (4 << 30) // (per_block * self.m))
         return max(1, min(self.m, max(1, 592 // self.m), by_mem))
 
@@ -156,21 +160,22 @@ def recurse(cur, p: DyadicPartition, r: int):
     torch = _lib.require_cuda()
     lib = _lib.load()
     stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    b = getattr(p, "branching", 2)
     pieces = []
     cur = cur.contiguous()
     for lvl in range(p.half, p.levels):
         nb, rows, groups, _ = cur.shape
-        pairs = groups // 2
-        if rows >= 2:
-            blocks = torch.empty((nb, 2, pairs, r, 2 * r), dtype=torch.complex128, device="cuda")
-            nxt = torch.empty((2 * nb, rows // 2, pairs, r), dtype=torch.complex128, device="cuda")
+        pairs = groups // b
+        if rows >= b:
+            blocks = torch.empty((nb, b, pairs, r, b * r), dtype=torch.complex128, device="cuda")
+            nxt = torch.empty((b * nb, rows // b, pairs, r), dtype=torch.complex128, device="cuda")
         else:
-            blocks = torch.empty((nb, pairs, r, 2 * r), dtype=torch.complex128, device="cuda")
+            blocks = torch.empty((nb, pairs, r, b * r), dtype=torch.complex128, device="cuda")
             nxt = torch.empty((nb, 1, pairs, r), dtype=torch.complex128, device="cuda")
         need = ctypes.c_uint64(0)
-        _lib.check(lib.bf_recurse_level(r, nb, rows, groups, None, None, None, None, ctypes.byref(need), stream))
+        _lib.check(lib.bf_recurse_level(r, b, nb, rows, groups, None, None, None, None, ctypes.byref(need), stream))
         ws = torch.empty(max(int(need.value), 16), dtype=torch.uint8, device="cuda")
-        _lib.check(lib.bf_recurse_level(r, nb, rows, groups, ctypes.c_void_p(cur.data_ptr()),
+        _lib.check(lib.bf_recurse_level(r, b, nb, rows, groups, ctypes.c_void_p(cur.data_ptr()),
                                         ctypes.c_void_p(blocks.data_ptr()), ctypes.c_void_p(nxt.data_ptr()),
                                         ctypes.c_void_p(ws.data_ptr()), ctypes.byref(need), stream),
                    "bf_recurse_level")

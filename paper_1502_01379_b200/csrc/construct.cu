@@ -24,20 +24,22 @@
 
 namespace bfly {
 
-constexpr int kMaxSet = 64;  // |rows|, |cols| <= r*q + r (r <= 16 at q = 3)
+constexpr int kSetCap = 128;  // |rows|, |cols| <= r*q + r (r <= 32 at q = 3)
+constexpr int kSmemSet = 64;  // small matrices live in shared memory when the set size S <= 64
 
 struct BlockState {
   int64_t r0, c0;
   int32_t nrows, ncols, nskr, nskc, tc, tr, t, pad;
-  int32_t rows[kMaxSet], cols[kMaxSet];
-  int32_t skr[kMaxSet], skc[kMaxSet];
-  int32_t pivc[kMaxSet], pivr[kMaxSet];
+  int32_t rows[kSetCap], cols[kSetCap];
+  int32_t skr[kSetCap], skc[kSetCap];
+  int32_t pivc[kSetCap], pivr[kSetCap];
 };
 
 struct MidArgs {
   EntrySrc src;
   int64_t side;
   int r, rqs, iters, nblocks;
+  int S;                  // set capacity of this launch (64 or 128); strides of the per-block buffers
   BlockState* st;
   const int32_t* draws;   // (nblocks, 2*(iters+1), rqs)
   double2* wide;          // (nblocks, S, side)
@@ -66,7 +68,7 @@ __global__ void k_init(MidArgs a, const int32_t* ij) {
 // set = sorted unique(draw[slot] U skeleton)  (np.union1d)
 __global__ void k_union(MidArgs a, int slot, int which) {
   BlockState& s = a.st[blockIdx.x];
-  __shared__ int32_t vals[2 * kMaxSet];
+  __shared__ int32_t vals[2 * kSetCap];
   const int32_t* d = a.draws + (static_cast<int64_t>(blockIdx.x) * 2 * (a.iters + 1) + slot) * a.rqs;
   const int nsk = which == kRows ? s.nskr : s.nskc;
   const int32_t* sk = which == kRows ? s.skr : s.skc;
@@ -110,7 +112,7 @@ __global__ void k_union(MidArgs a, int slot, int which) {
 __global__ void k_fill_wide(MidArgs a, int which) {
   const BlockState& s = a.st[blockIdx.x];
   const int nr = which == kRows ? s.nrows : s.ncols;
-  double2* W = a.wide + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  double2* W = a.wide + static_cast<int64_t>(blockIdx.x) * a.S * a.side;
   const int64_t total = nr * a.side;
   for (int64_t x = blockIdx.y * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < total;
        x += static_cast<int64_t>(gridDim.y) * blockDim.x) {
@@ -122,12 +124,12 @@ __global__ void k_fill_wide(MidArgs a, int which) {
 }
 
 // Greedy column pivoting (select_pivot_columns, lowrank.py:102-129) on W
-// (nr x ncols, row-major, nr <= kMaxSet), k picks, CTA-cooperative. Initial
+// (nr x ncols, row-major, nr <= kSetCap), k picks, CTA-cooperative. Initial
 // norms sum over rows in the reference's order: sequential when the
 // reference's matrix is C-ordered, numpy pairwise when it is F-ordered.
 // Residual norms are downdated, never recomputed; ties within 2*PIVOT_TIE
 // go to the lowest index. Returns the pick count; picks in pick order.
-// Shared: norms (ncols doubles), q (kMaxSet), red (32 doubles), redi (32 ints).
+// Shared: norms (ncols doubles), q (kSetCap), red (32 doubles), redi (32 ints).
 __device__ int pivot_rows_core(double2* W, int nr, int ncols, int k, double rel_tol, bool pairwise, double* norms,
                                double2* q, double* red, int* redi, int* picks) {
   for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
@@ -185,13 +187,13 @@ __device__ int pivot_rows_core(double2* W, int nr, int ncols, int k, double rel_
 __global__ void k_pivot_wide(MidArgs a, int which) {
   extern __shared__ double smem_d[];
   double* norms = smem_d;                                       // side
-  double2* q = reinterpret_cast<double2*>(norms + a.side);      // kMaxSet
-  double* red = reinterpret_cast<double*>(q + kMaxSet);         // 32
+  double2* q = reinterpret_cast<double2*>(norms + a.side);      // kSetCap
+  double* red = reinterpret_cast<double*>(q + kSetCap);         // 32
   int* redi = reinterpret_cast<int*>(red + 32);                 // 32
-  int* picks = redi + 32;                                       // kMaxSet
+  int* picks = redi + 32;                                       // kSetCap
   BlockState& s = a.st[blockIdx.x];
   const int nr = which == kRows ? s.nrows : s.ncols;
-  double2* W = a.wide + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  double2* W = a.wide + static_cast<int64_t>(blockIdx.x) * a.S * a.side;
   const int npick = pivot_rows_core(W, nr, static_cast<int>(a.side), a.r, 0.0, which == kCols, norms, q, red, redi,
                                     picks);
   // skeleton = sorted(picks)
@@ -210,13 +212,13 @@ __global__ void k_pivot_wide(MidArgs a, int which) {
 }
 
 // Standalone batched pivot selection (bf_select_pivots): matrices (batch, m, n)
-// complex128 row-major, m <= kMaxSet, copied to scratch then pivoted in place.
+// complex128 row-major, m <= kSetCap, copied to scratch then pivoted in place.
 __global__ void k_select_pivots(const double2* A, double2* scratch, int m, int n, int k, double rel_tol, int pairwise,
                                 int32_t* pivots, int32_t* counts) {
   extern __shared__ double smem_d[];
   double* norms = smem_d;
   double2* q = reinterpret_cast<double2*>(norms + n + (n & 1));
-  double* red = reinterpret_cast<double*>(q + kMaxSet);
+  double* red = reinterpret_cast<double*>(q + kSetCap);
   int* redi = reinterpret_cast<int*>(red + 32);
   int* picks = redi + 32;
   const int64_t off = static_cast<int64_t>(blockIdx.x) * m * n;
@@ -234,7 +236,7 @@ __global__ void k_select_pivots(const double2* A, double2* scratch, int m, int n
 __global__ void k_fill_tall(MidArgs a, int which, int use_piv, double2* dst_base) {
   const BlockState& s = a.st[blockIdx.x];
   const int ncol = use_piv ? (which == kCols ? s.tc : s.tr) : (which == kCols ? s.ncols : s.nrows);
-  double2* T = dst_base + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  double2* T = dst_base + static_cast<int64_t>(blockIdx.x) * a.S * a.side;
   const int64_t total = ncol * a.side;
   for (int64_t x = blockIdx.y * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < total;
        x += static_cast<int64_t>(gridDim.y) * blockDim.x) {
@@ -249,14 +251,14 @@ __global__ void k_fill_tall(MidArgs a, int which, int use_piv, double2* dst_base
 // Greedy pivoting on the tall T (side x nc, column-major), up to kmax picks,
 // rel_tol = BASIS_TRIM; pick order kept (orthonormal_columns, lowrank.py:132-154).
 __global__ void k_pivot_tall(MidArgs a, int which) {
-  __shared__ double norms[kMaxSet];
-  __shared__ int picks[kMaxSet];
+  __shared__ double norms[kSetCap];
+  __shared__ int picks[kSetCap];
   __shared__ int s_j, s_stop;
   __shared__ double s_sq;
   BlockState& s = a.st[blockIdx.x];
   const int nc = which == kCols ? s.ncols : s.nrows;
   const int side = static_cast<int>(a.side);
-  double2* T = a.tall + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  double2* T = a.tall + static_cast<int64_t>(blockIdx.x) * a.S * a.side;
   double2* q = a.qbuf + static_cast<int64_t>(blockIdx.x) * a.side;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int c = threadIdx.x; c < nc; c += blockDim.x) {
@@ -328,12 +330,12 @@ __global__ void k_pivot_tall(MidArgs a, int which) {
 // columns (the reference uses np.linalg.qr; only span(Q) reaches the factors,
 // see DESIGN.md "Construction parity").
 __global__ void k_cgs2(MidArgs a, int which) {
-  __shared__ double2 coef[kMaxSet];
+  __shared__ double2 coef[kSetCap];
   __shared__ double red[32];
   const BlockState& s = a.st[blockIdx.x];
   const int t = which == kCols ? s.tc : s.tr;
   const int side = static_cast<int>(a.side);
-  double2* Q = (which == kCols ? a.qc : a.qr) + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  double2* Q = (which == kCols ? a.qc : a.qr) + static_cast<int64_t>(blockIdx.x) * a.S * a.side;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int p = 0; p < t; ++p) {
     double2* x = Q + static_cast<int64_t>(p) * side;
@@ -370,10 +372,10 @@ __global__ void k_cgs2(MidArgs a, int which) {
   }
 }
 
-// pinv_floored (lowrank.py:90-94) of M (m x n, shared) into P (n x m, global, row-major).
+// pinv_floored (lowrank.py:90-94) of M (m x n) into P (n x m, row-major, ld S).
 __device__ void pinv_small(const double2* M, int m, int n, int ld, double2* P, double2* U, double2* V, double* sig,
-                           double2* W, double2* Vt, int* flag, int* perm, double* ssc) {
-  svd_small(M, m, n, ld, U, kMaxSet, V, kMaxSet, sig, W, Vt, flag, perm, ssc);
+                           double2* W, double2* Vt, int* flag, int* perm, double* ssc, int S) {
+  svd_small(M, m, n, ld, U, S, V, S, sig, W, Vt, flag, perm, ssc);
   const int sn = min(m, n);
   double smax = 0;
   for (int k = 0; k < sn; ++k) smax = fmax(smax, sig[k]);
@@ -384,37 +386,51 @@ __device__ void pinv_small(const double2* M, int m, int n, int ld, double2* P, d
     for (int k = 0; k < sn; ++k) {
       const double fi = floored_inv(sig[k], smax);
       if (fi == 0.0) continue;
-      const double2 g = cmul(V[c * kMaxSet + k], cconj(U[aa * kMaxSet + k]));
+      const double2 g = cmul(V[c * S + k], cconj(U[aa * S + k]));
       acc.x += fi * g.x;
       acc.y += fi * g.y;
     }
-    P[c * kMaxSet + aa] = acc;
+    P[c * S + aa] = acc;
   }
   __syncthreads();
 }
 
+// Per-block small-matrix scratch (global): svd U, svd V, P1, P2, U_M, V_M, and — when the
+// set capacity S exceeds 64 — the three work matrices that otherwise live in shared memory.
+struct SmallBufs {
+  double2 *sU, *sV, *P1, *P2, *UM, *VM, *Mb, *W, *Vt;
+};
+__device__ __forceinline__ SmallBufs small_bufs(const MidArgs& a, double2* smem) {
+  const int64_t SS = static_cast<int64_t>(a.S) * a.S;
+  double2* scr = a.scr + static_cast<int64_t>(blockIdx.x) * 9 * SS;
+  SmallBufs b;
+  b.sU = scr;
+  b.sV = scr + SS;
+  b.P1 = scr + 2 * SS;
+  b.P2 = scr + 3 * SS;
+  b.UM = scr + 4 * SS;
+  b.VM = scr + 5 * SS;
+  const bool sh = a.S <= kSmemSet;
+  b.Mb = sh ? smem : scr + 6 * SS;
+  b.W = sh ? smem + SS : scr + 7 * SS;
+  b.Vt = sh ? smem + 2 * SS : scr + 8 * SS;
+  return b;
+}
+
 // mid = pinv(qc[rows, :tc]) @ K(rows, cols) @ pinv(qr[cols, :tr]^H); SVD(mid)
-// (lowrank.py:257, 284-293). Results: U_M (tc x s) in scr[4], V_M (tr x s) in
-// scr[5], sigma in sig, kept rank t = min(r, s) in state.
+// (lowrank.py:257, 284-293). Results: U_M (tc x s), V_M (tr x s), sigma, and the
+// kept rank t = min(r, s) in the block state.
 __global__ void k_mid(MidArgs a) {
   extern __shared__ double2 sm2[];
-  double2* Mb = sm2;                       // 64 x 64
-  double2* W = Mb + kMaxSet * kMaxSet;     // 64 x 64
-  double2* Vt = W + kMaxSet * kMaxSet;     // 64 x 64
-  __shared__ int flag, perm[kMaxSet];
-  __shared__ double ssc[kMaxSet], sg[kMaxSet];
+  __shared__ int flag, perm[kSetCap];
+  __shared__ double ssc[kSetCap], sg[kSetCap];
   BlockState& s = a.st[blockIdx.x];
-  const int side = static_cast<int>(a.side);
+  const int side = static_cast<int>(a.side), S = a.S;
   const int nrw = s.nrows, ncl = s.ncols, tc = s.tc, tr = s.tr;
-  double2* scr = a.scr + static_cast<int64_t>(blockIdx.x) * 6 * kMaxSet * kMaxSet;
-  double2* sU = scr;                          // svd scratch U
-  double2* sV = scr + 1 * kMaxSet * kMaxSet;  // svd scratch V
-  double2* P1 = scr + 2 * kMaxSet * kMaxSet;  // tc x nrows, later T1 = P1 Er (tc x ncols)
-  double2* P2 = scr + 3 * kMaxSet * kMaxSet;  // ncols x tr
-  double2* UM = scr + 4 * kMaxSet * kMaxSet;
-  double2* VM = scr + 5 * kMaxSet * kMaxSet;
-  const double2* QC = a.qc + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
-  const double2* QR = a.qr + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  const SmallBufs bb = small_bufs(a, sm2);
+  double2 *Mb = bb.Mb, *W = bb.W, *Vt = bb.Vt, *P1 = bb.P1, *P2 = bb.P2;
+  const double2* QC = a.qc + static_cast<int64_t>(blockIdx.x) * S * a.side;
+  const double2* QR = a.qr + static_cast<int64_t>(blockIdx.x) * S * a.side;
   if (tc == 0 || tr == 0) {
     if (threadIdx.x == 0) s.t = 0;
     return;
@@ -422,32 +438,32 @@ __global__ void k_mid(MidArgs a) {
   // P1 = pinv(qc[rows, :])
   for (int x = threadIdx.x; x < nrw * tc; x += blockDim.x) {
     const int i = x / tc, l = x % tc;
-    Mb[i * kMaxSet + l] = QC[static_cast<int64_t>(l) * side + s.rows[i]];
+    Mb[i * S + l] = QC[static_cast<int64_t>(l) * side + s.rows[i]];
   }
   __syncthreads();
-  pinv_small(Mb, nrw, tc, kMaxSet, P1, sU, sV, sg, W, Vt, &flag, perm, ssc);
+  pinv_small(Mb, nrw, tc, S, P1, bb.sU, bb.sV, sg, W, Vt, &flag, perm, ssc, S);
   // P2 = pinv(qr[cols, :]^H)   (tr x ncols) -> (ncols x tr)
   for (int x = threadIdx.x; x < tr * ncl; x += blockDim.x) {
     const int l = x / ncl, c = x % ncl;
-    Mb[l * kMaxSet + c] = cconj(QR[static_cast<int64_t>(l) * side + s.cols[c]]);
+    Mb[l * S + c] = cconj(QR[static_cast<int64_t>(l) * side + s.cols[c]]);
   }
   __syncthreads();
-  pinv_small(Mb, tr, ncl, kMaxSet, P2, sU, sV, sg, W, Vt, &flag, perm, ssc);
+  pinv_small(Mb, tr, ncl, S, P2, bb.sU, bb.sV, sg, W, Vt, &flag, perm, ssc, S);
   // Er = K(rows, cols) into Mb ; T1 = P1 @ Er (tc x ncols) into W
   for (int x = threadIdx.x; x < nrw * ncl; x += blockDim.x) {
     const int i = x / ncl, c = x % ncl;
-    Mb[i * kMaxSet + c] = entry_eval(a.src, s.r0 + s.rows[i], s.c0 + s.cols[c]);
+    Mb[i * S + c] = entry_eval(a.src, s.r0 + s.rows[i], s.c0 + s.cols[c]);
   }
   __syncthreads();
   for (int x = threadIdx.x; x < tc * ncl; x += blockDim.x) {
     const int l = x / ncl, c = x % ncl;
     double2 acc = make_double2(0, 0);
     for (int i = 0; i < nrw; ++i) {
-      const double2 g = cmul(P1[l * kMaxSet + i], Mb[i * kMaxSet + c]);
+      const double2 g = cmul(P1[l * S + i], Mb[i * S + c]);
       acc.x += g.x;
       acc.y += g.y;
     }
-    W[l * kMaxSet + c] = acc;
+    W[l * S + c] = acc;
   }
   __syncthreads();
   // mid = T1 @ P2 (tc x tr) into Mb
@@ -455,15 +471,15 @@ __global__ void k_mid(MidArgs a) {
     const int l = x / tr, m2 = x % tr;
     double2 acc = make_double2(0, 0);
     for (int c = 0; c < ncl; ++c) {
-      const double2 g = cmul(W[l * kMaxSet + c], P2[c * kMaxSet + m2]);
+      const double2 g = cmul(W[l * S + c], P2[c * S + m2]);
       acc.x += g.x;
       acc.y += g.y;
     }
-    Mb[l * kMaxSet + m2] = acc;
+    Mb[l * S + m2] = acc;
   }
   __syncthreads();
-  svd_small(Mb, tc, tr, kMaxSet, UM, kMaxSet, VM, kMaxSet, sg, W, Vt, &flag, perm, ssc);
-  double* sig = a.sig + static_cast<int64_t>(blockIdx.x) * kMaxSet;
+  svd_small(Mb, tc, tr, S, bb.UM, S, bb.VM, S, sg, W, Vt, &flag, perm, ssc);
+  double* sig = a.sig + static_cast<int64_t>(blockIdx.x) * S;
   const int sn = min(tc, tr);
   for (int k = threadIdx.x; k < sn; k += blockDim.x) sig[k] = sg[k];
   if (threadIdx.x == 0) s.t = min(a.r, sn);
@@ -472,23 +488,18 @@ __global__ void k_mid(MidArgs a) {
 // Dense branch (r*q >= side, lowrank.py:231-234): truncated SVD of the whole block.
 __global__ void k_dense(MidArgs a) {
   extern __shared__ double2 sm2[];
-  double2* Mb = sm2;
-  double2* W = Mb + kMaxSet * kMaxSet;
-  double2* Vt = W + kMaxSet * kMaxSet;
-  __shared__ int flag, perm[kMaxSet];
-  __shared__ double ssc[kMaxSet], sg[kMaxSet];
+  __shared__ int flag, perm[kSetCap];
+  __shared__ double ssc[kSetCap], sg[kSetCap];
   BlockState& s = a.st[blockIdx.x];
-  const int side = static_cast<int>(a.side);
-  double2* scr = a.scr + static_cast<int64_t>(blockIdx.x) * 6 * kMaxSet * kMaxSet;
-  double2* UM = scr + 4 * kMaxSet * kMaxSet;
-  double2* VM = scr + 5 * kMaxSet * kMaxSet;
+  const int side = static_cast<int>(a.side), S = a.S;
+  const SmallBufs bb = small_bufs(a, sm2);
   for (int x = threadIdx.x; x < side * side; x += blockDim.x) {
     const int i = x / side, j = x % side;
-    Mb[i * kMaxSet + j] = entry_eval(a.src, s.r0 + i, s.c0 + j);
+    bb.Mb[i * S + j] = entry_eval(a.src, s.r0 + i, s.c0 + j);
   }
   __syncthreads();
-  svd_small(Mb, side, side, kMaxSet, UM, kMaxSet, VM, kMaxSet, sg, W, Vt, &flag, perm, ssc);
-  double* sig = a.sig + static_cast<int64_t>(blockIdx.x) * kMaxSet;
+  svd_small(bb.Mb, side, side, S, bb.UM, S, bb.VM, S, sg, bb.W, bb.Vt, &flag, perm, ssc);
+  double* sig = a.sig + static_cast<int64_t>(blockIdx.x) * S;
   for (int k = threadIdx.x; k < side; k += blockDim.x) sig[k] = sg[k];
   if (threadIdx.x == 0) {
     s.t = a.r;
@@ -501,15 +512,16 @@ __global__ void k_dense(MidArgs a) {
 // vanish from u0*sigma0 / v0*sigma0, construct.py:63-65), and W = floored_inverse(sigma0).
 __global__ void k_assemble(MidArgs a) {
   const BlockState& s = a.st[blockIdx.x];
-  const int side = static_cast<int>(a.side);
+  const int side = static_cast<int>(a.side), S = a.S;
   const int r = a.r, t = s.t;
   const bool dense = s.tc < 0;
-  const double2* scr = a.scr + static_cast<int64_t>(blockIdx.x) * 6 * kMaxSet * kMaxSet;
-  const double2* UM = scr + 4 * kMaxSet * kMaxSet;
-  const double2* VM = scr + 5 * kMaxSet * kMaxSet;
-  const double* sig = a.sig + static_cast<int64_t>(blockIdx.x) * kMaxSet;
-  const double2* QC = a.qc + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
-  const double2* QR = a.qr + static_cast<int64_t>(blockIdx.x) * kMaxSet * a.side;
+  const int64_t SS = static_cast<int64_t>(S) * S;
+  const double2* scr = a.scr + static_cast<int64_t>(blockIdx.x) * 9 * SS;
+  const double2* UM = scr + 4 * SS;
+  const double2* VM = scr + 5 * SS;
+  const double* sig = a.sig + static_cast<int64_t>(blockIdx.x) * S;
+  const double2* QC = a.qc + static_cast<int64_t>(blockIdx.x) * S * a.side;
+  const double2* QR = a.qr + static_cast<int64_t>(blockIdx.x) * S * a.side;
   double2* uo = a.u_out + static_cast<int64_t>(blockIdx.x) * a.side * r;
   double2* vo = a.v_out + static_cast<int64_t>(blockIdx.x) * a.side * r;
   const int64_t total = static_cast<int64_t>(side) * r;
@@ -519,16 +531,16 @@ __global__ void k_assemble(MidArgs a) {
     double2 u = make_double2(0, 0), v = make_double2(0, 0);
     if (rho < t) {
       if (dense) {
-        u = UM[i * kMaxSet + rho];
-        v = VM[i * kMaxSet + rho];
+        u = UM[i * S + rho];
+        v = VM[i * S + rho];
       } else {
         for (int l = 0; l < s.tc; ++l) {
-          const double2 g = cmul(QC[static_cast<int64_t>(l) * side + i], UM[l * kMaxSet + rho]);
+          const double2 g = cmul(QC[static_cast<int64_t>(l) * side + i], UM[l * S + rho]);
           u.x += g.x;
           u.y += g.y;
         }
         for (int l = 0; l < s.tr; ++l) {
-          const double2 g = cmul(QR[static_cast<int64_t>(l) * side + i], VM[l * kMaxSet + rho]);
+          const double2 g = cmul(QR[static_cast<int64_t>(l) * side + i], VM[l * S + rho]);
           v.x += g.x;
           v.y += g.y;
         }
@@ -548,26 +560,26 @@ __global__ void k_assemble(MidArgs a) {
   }
 }
 
-
 // ---------------------------------------------------------------- recursion
 // One level of _recurse (construct.py:127-163) for problems [p0, p0 + np):
-// splitting levels factor (half x 2r) stacks, merge-only levels (1 x 2r) rows.
+// splitting levels factor (part x b r) stacks (b = branching: 2, or 4 on
+// quadtrees), merge-only levels (1 x b r) rows.
 struct RecArgs {
   const double2* cur;   // (nb, rows, groups, r)
   double2* nxt;         // next cur
   double2* g;           // transfer blocks of this level
-  double2* scr;         // per-problem (half x 2r) scratch for the QR route
+  double2* scr;         // per-problem scratch
   int64_t nb, rows, pairs;
-  int r;
+  int r, b, S;          // rank, branching, small-matrix capacity (64: shared memory; 128: global)
   int64_t p0;
 };
 
-__device__ void householder_r(double2* A, int m, int n, double2* R, double* red) {
-  // A (m x n) row-major in global scratch, overwritten by reflectors; R (n x n) shared, ld kMaxSet.
+__device__ void householder_r(double2* A, int m, int n, double2* R, int ldr, double* red) {
+  // A (m x n) row-major in global scratch, overwritten by reflectors; R (n x n), ld ldr.
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   __shared__ double2 s_beta;
   __shared__ double s_vn2;
-  for (int i = threadIdx.x; i < n * kMaxSet; i += blockDim.x) R[i] = make_double2(0, 0);
+  for (int i = threadIdx.x; i < n * ldr; i += blockDim.x) R[i] = make_double2(0, 0);
   for (int p = 0; p < n; ++p) {
     double part = 0;
     for (int i = p + threadIdx.x; i < m; i += blockDim.x) part += A[i * n + p].x * A[i * n + p].x + A[i * n + p].y * A[i * n + p].y;
@@ -602,61 +614,64 @@ __device__ void householder_r(double2* A, int m, int n, double2* R, double* red)
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) R[p * kMaxSet + p] = vn2 > 0 ? s_beta : A[p * n + p];
-    for (int j = p + 1 + threadIdx.x; j < n; j += blockDim.x) R[p * kMaxSet + j] = A[p * n + j];
+    if (threadIdx.x == 0) R[p * ldr + p] = vn2 > 0 ? s_beta : A[p * n + p];
+    for (int j = p + 1 + threadIdx.x; j < n; j += blockDim.x) R[p * ldr + j] = A[p * n + j];
     __syncthreads();
   }
 }
 
-// Per-problem global scratch: [Ac: max(half, 64) x 2r][Ug: 64 x 64][Vg: 64 x 64].
-__device__ __forceinline__ int64_t rec_scratch_elems(int64_t half, int n2) {
-  return (half > kMaxSet ? half : kMaxSet) * n2 + 2 * kMaxSet * kMaxSet;
+// Per-problem global scratch: [Ac: max(part, S) x w][Ug: S x S][Vg: S x S][Mb, W, Vt: S x S each when S > 64].
+__device__ __host__ __forceinline__ int64_t rec_scratch_elems(int64_t part, int w, int S) {
+  return (part > S ? part : S) * w + 5ll * S * S;
 }
 
 __global__ void k_recurse_split(RecArgs a) {
   extern __shared__ double2 sm2[];
-  double2* Mb = sm2;                    // input / R
-  double2* W = Mb + kMaxSet * kMaxSet;  // svd work
-  double2* Vt = W + kMaxSet * kMaxSet;  // svd work
-  __shared__ int flag, perm[kMaxSet];
-  __shared__ double ssc[kMaxSet], sg[kMaxSet], red[32];
+  __shared__ int flag, perm[kSetCap];
+  __shared__ double ssc[kSetCap], sg[kSetCap], red[32];
   const int64_t prob = a.p0 + blockIdx.x;
-  const int64_t pairs = a.pairs, half = a.rows / 2;
-  const int n2 = 2 * a.r, r = a.r;
-  const int64_t b = prob / (2 * pairs), t = (prob / pairs) % 2, p = prob % pairs;
-  // paired = cur.reshape(nb, rows, pairs, 2r); stack t takes rows [t*half, (t+1)*half)
-  auto src = [&](int64_t row, int c) { return a.cur[((b * a.rows + t * half + row) * pairs + p) * n2 + c]; };
-  const int keep = static_cast<int>(half < r ? half : r);
-  double2* Ac = a.scr + static_cast<int64_t>(blockIdx.x) * rec_scratch_elems(half, n2);
-  double2* Ug = Ac + (half > kMaxSet ? half : kMaxSet) * n2;
-  double2* Vg = Ug + kMaxSet * kMaxSet;
-  const int64_t out_base = ((b * 2 + t) * half) * pairs + p;  // new_u.transpose(0,1,3,2,4) row (b,t,row=0,p)
-  if (half <= kMaxSet) {
-    for (int x = threadIdx.x; x < half * n2; x += blockDim.x) Mb[(x / n2) * kMaxSet + x % n2] = src(x / n2, x % n2);
+  const int b = a.b, S = a.S;
+  const int64_t pairs = a.pairs, part = a.rows / b;
+  const int w = b * a.r, r = a.r;
+  const int64_t gb = prob / (b * pairs), t = (prob / pairs) % b, p = prob % pairs;
+  // paired = cur.reshape(nb, rows, pairs, b r); stack t takes rows [t*part, (t+1)*part)
+  auto src = [&](int64_t row, int c) { return a.cur[((gb * a.rows + t * part + row) * pairs + p) * w + c]; };
+  const int keep = static_cast<int>(part < r ? part : r);
+  const int64_t SS = static_cast<int64_t>(S) * S;
+  double2* Ac = a.scr + static_cast<int64_t>(blockIdx.x) * rec_scratch_elems(part, w, S);
+  double2* Ug = Ac + (part > S ? part : S) * w;
+  double2* Vg = Ug + SS;
+  const bool sh = S <= kSmemSet;
+  double2* Mb = sh ? sm2 : Vg + SS;
+  double2* W = sh ? sm2 + SS : Vg + 2 * SS;
+  double2* Vt = sh ? sm2 + 2 * SS : Vg + 3 * SS;
+  const int64_t out_base = ((gb * b + t) * part) * pairs + p;  // new_u.transpose(0,1,3,2,4): row (gb,t,row=0,p)
+  if (part <= S) {
+    for (int x = threadIdx.x; x < part * w; x += blockDim.x) Mb[(x / w) * S + x % w] = src(x / w, x % w);
     __syncthreads();
-    svd_small(Mb, static_cast<int>(half), n2, kMaxSet, Ug, kMaxSet, Vg, kMaxSet, sg, W, Vt, &flag, perm, ssc);
-    for (int x = threadIdx.x; x < half * r; x += blockDim.x) {
+    svd_small(Mb, static_cast<int>(part), w, S, Ug, S, Vg, S, sg, W, Vt, &flag, perm, ssc);
+    for (int x = threadIdx.x; x < part * r; x += blockDim.x) {
       const int row = x / r, rho = x % r;
       double2 u = make_double2(0, 0);
-      if (rho < keep) u = make_double2(Ug[row * kMaxSet + rho].x * sg[rho], Ug[row * kMaxSet + rho].y * sg[rho]);
+      if (rho < keep) u = make_double2(Ug[row * S + rho].x * sg[rho], Ug[row * S + rho].y * sg[rho]);
       a.nxt[(out_base + row * pairs) * r + rho] = u;
     }
   } else {
     // tall stack: Householder R, SVD of R gives sigma and V; new_u = A V[:, :keep] (= uu ss)
-    for (int64_t x = threadIdx.x; x < half * n2; x += blockDim.x) Ac[x] = src(x / n2, static_cast<int>(x % n2));
+    for (int64_t x = threadIdx.x; x < part * w; x += blockDim.x) Ac[x] = src(x / w, static_cast<int>(x % w));
     __syncthreads();
-    householder_r(Ac, static_cast<int>(half), n2, Mb, red);
+    householder_r(Ac, static_cast<int>(part), w, Mb, S, red);
     __syncthreads();
-    svd_small(Mb, n2, n2, kMaxSet, Ug, kMaxSet, Vg, kMaxSet, sg, W, Vt, &flag, perm, ssc);
-    for (int x = threadIdx.x; x < n2 * n2; x += blockDim.x) Vt[(x / n2) * kMaxSet + x % n2] = Vg[(x / n2) * kMaxSet + x % n2];
+    svd_small(Mb, w, w, S, Ug, S, Vg, S, sg, W, Vt, &flag, perm, ssc);
+    for (int x = threadIdx.x; x < w * w; x += blockDim.x) Vt[(x / w) * S + x % w] = Vg[(x / w) * S + x % w];
     __syncthreads();
-    for (int64_t x = threadIdx.x; x < half * r; x += blockDim.x) {
+    for (int64_t x = threadIdx.x; x < part * r; x += blockDim.x) {
       const int64_t row = x / r;
       const int rho = static_cast<int>(x % r);
       double2 u = make_double2(0, 0);
       if (rho < keep)
-        for (int c = 0; c < n2; ++c) {
-          const double2 g = cmul(src(row, c), Vt[c * kMaxSet + rho]);
+        for (int c = 0; c < w; ++c) {
+          const double2 g = cmul(src(row, c), Vt[c * S + rho]);
           u.x += g.x;
           u.y += g.y;
         }
@@ -664,32 +679,32 @@ __global__ void k_recurse_split(RecArgs a) {
     }
   }
   __syncthreads();
-  // transfer block G = vh[:keep] zero-padded to (r x 2r): G[rho][c] = conj(V[c][rho])
-  double2* G = a.g + prob * static_cast<int64_t>(r) * n2;
-  for (int x = threadIdx.x; x < r * n2; x += blockDim.x) {
-    const int rho = x / n2, c = x % n2;
-    G[x] = rho < keep ? cconj(Vg[c * kMaxSet + rho]) : make_double2(0, 0);
+  // transfer block G = vh[:keep] zero-padded to (r x b r): G[rho][c] = conj(V[c][rho])
+  double2* G = a.g + prob * static_cast<int64_t>(r) * w;
+  for (int x = threadIdx.x; x < r * w; x += blockDim.x) {
+    const int rho = x / w, c = x % w;
+    G[x] = rho < keep ? cconj(Vg[c * S + rho]) : make_double2(0, 0);
   }
 }
 
 __global__ void k_recurse_merge(RecArgs a, int64_t nprob) {
-  // (1 x 2r) rows: sigma = |row|, vh = row / sigma; new_u = (sigma, 0, ..., 0)
+  // (1 x b r) rows: sigma = |row|, vh = row / sigma; new_u = (sigma, 0, ..., 0)
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int64_t prob = a.p0 + warp;
   if (prob >= a.p0 + nprob) return;
-  const int n2 = 2 * a.r, r = a.r;
-  const double2* row = a.cur + prob * n2;
+  const int w = a.b * a.r, r = a.r;
+  const double2* row = a.cur + prob * w;
   double acc = 0;
-  for (int c = lane; c < n2; c += 32) acc += row[c].x * row[c].x + row[c].y * row[c].y;
+  for (int c = lane; c < w; c += 32) acc += row[c].x * row[c].x + row[c].y * row[c].y;
   const double sgm = sqrt(warp_sum(acc));
-  double2* G = a.g + prob * static_cast<int64_t>(r) * n2;
-  for (int x = lane; x < r * n2; x += 32) {
-    const int rho = x / n2, c = x % n2;
+  double2* G = a.g + prob * static_cast<int64_t>(r) * w;
+  for (int x = lane; x < r * w; x += 32) {
+    const int rho = x / w, c = x % w;
     G[x] = (rho == 0 && sgm > 0) ? make_double2(row[c].x / sgm, row[c].y / sgm) : make_double2(0, 0);
   }
-  const int64_t b = prob / a.pairs, p = prob % a.pairs;
+  const int64_t gb = prob / a.pairs, p = prob % a.pairs;
   for (int rho = lane; rho < r; rho += 32)
-    a.nxt[(b * a.pairs + p) * r + rho] = make_double2(rho == 0 ? sgm : 0.0, 0);
+    a.nxt[(gb * a.pairs + p) * r + rho] = make_double2(rho == 0 ? sgm : 0.0, 0);
 }
 
 }  // namespace bfly
@@ -698,8 +713,14 @@ using namespace bfly;
 
 namespace {
 
-uint64_t mid_ws_layout(uint64_t side, uint32_t nblocks, uint64_t* off) {
-  const uint64_t S = kMaxSet;
+// Set capacity for a launch: |rows|, |cols| <= r q + r (or side in the dense branch).
+int set_capacity(uint64_t side, uint32_t rank, uint32_t q_over) {
+  const uint64_t rq = static_cast<uint64_t>(rank) * q_over;
+  const uint64_t need = rq >= side ? side : rq + rank;
+  return need <= static_cast<uint64_t>(kSmemSet) ? kSmemSet : (need <= static_cast<uint64_t>(kSetCap) ? kSetCap : -1);
+}
+
+uint64_t mid_ws_layout(uint64_t side, uint32_t nblocks, int S, uint64_t* off) {
   uint64_t o = 0;
   auto take = [&](uint64_t bytes) {
     const uint64_t r = o;
@@ -712,41 +733,55 @@ uint64_t mid_ws_layout(uint64_t side, uint32_t nblocks, uint64_t* off) {
   off[3] = take(16ull * nblocks * S * side);  // qc
   off[4] = take(16ull * nblocks * S * side);  // qr
   off[5] = take(16ull * nblocks * side);      // qbuf
-  off[6] = take(16ull * nblocks * 6 * S * S); // scr
+  off[6] = take(16ull * nblocks * 9 * S * S); // small-matrix scratch
   off[7] = take(8ull * nblocks * S);          // sig
   return o;
+}
+
+bool tree_geometry(uint64_t n, uint32_t levels, uint32_t branching, uint64_t* m, uint64_t* side) {
+  if (branching != 2 && branching != 4) return false;
+  const uint32_t lb = branching == 4 ? 2 : 1;
+  if (n < 4 || (n & (n - 1)) || levels < 2 || levels % 2 || levels > 40) return false;
+  if (branching == 4 && ((63 - __builtin_clzll(n)) % 2)) return false;
+  if (lb * (levels / 2) >= 63 || (1ull << (lb * (levels / 2))) > n) return false;
+  *m = 1ull << (lb * (levels / 2));
+  *side = n / *m;
+  return true;
 }
 
 }  // namespace
 
 extern "C" {
 
-uint64_t bf_middle_workspace_bytes(uint64_t n, uint32_t levels, uint32_t rank, uint32_t nblocks) {
-  (void)rank;
-  uint64_t off[8];
-  return mid_ws_layout(n >> (levels / 2), nblocks, off);
+uint64_t bf_middle_workspace_bytes(uint64_t n, uint32_t levels, uint32_t branching, uint32_t rank, uint32_t q_over,
+                                   uint32_t nblocks) {
+  uint64_t m = 0, side = 0, off[8];
+  if (!tree_geometry(n, levels, branching, &m, &side)) return 0;
+  const int S = set_capacity(side, rank, q_over ? q_over : 1);
+  if (S < 0) return 0;
+  return mid_ws_layout(side, nblocks, S, off);
 }
 
-int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t rank, uint32_t q_over, uint32_t iters,
-                     const void* dense, uint32_t nblocks, const int32_t* block_ij, const int32_t* draws,
+int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branching, uint32_t rank, uint32_t q_over,
+                     uint32_t iters, const void* dense, uint32_t nblocks, const int32_t* block_ij, const int32_t* draws,
                      void* u_out, void* v_out, double* w_out, void* workspace, uint64_t ws_bytes, void* stream) {
-  if (kernel_id < BF_KERNEL_FIO || kernel_id > BF_KERNEL_DENSE) return fail(BF_EINVAL, "unknown entry kernel id");
+  if (kernel_id < BF_KERNEL_FIO || kernel_id > BF_KERNEL_RADON2D) return fail(BF_EINVAL, "unknown entry kernel id");
   if (kernel_id == BF_KERNEL_DENSE && !dense) return fail(BF_EINVAL, "dense oracle needs a matrix pointer");
-  if (n < 4 || (n & (n - 1)) || levels < 2 || levels % 2 || (1ull << (levels / 2)) > n)
-    return fail(BF_EINVAL, "bad partition geometry");
+  uint64_t m = 0, side = 0;
+  if (!tree_geometry(n, levels, branching, &m, &side)) return fail(BF_EINVAL, "bad partition geometry");
+  if (kernel_id == BF_KERNEL_RADON2D && branching != 4) return fail(BF_EINVAL, "the 2-D kernel needs a quadtree");
   if (rank < 1 || q_over < 1 || iters < 1) return fail(BF_EINVAL, "bad rank / oversampling parameters");
-  const uint64_t side = n >> (levels / 2);
   if (side < rank) return fail(BF_EINVAL, "middle blocks are narrower than the rank");
   const uint64_t rq = static_cast<uint64_t>(rank) * q_over;
   const bool dense_branch = rq >= side;  // lowrank.py:231-234
   const uint64_t rqs = rq < side ? rq : side;
-  if (dense_branch ? side > kMaxSet : rqs + rank > kMaxSet)
-    return fail(BF_EINVAL, "rank too large for the batched sampling kernels (need r*(q+1) <= 64)");
+  const int S = set_capacity(side, rank, q_over);
+  if (S < 0) return fail(BF_EINVAL, "rank too large for the batched sampling kernels (need r*(q+1) <= 128)");
   if (!nblocks) return BF_OK;
   if (!block_ij || (!dense_branch && !draws) || !u_out || !v_out || !w_out || !workspace)
     return fail(BF_EINVAL, "null pointer");
   uint64_t off[8];
-  if (ws_bytes < mid_ws_layout(side, nblocks, off)) return fail(BF_EINVAL, "middle workspace too small");
+  if (ws_bytes < mid_ws_layout(side, nblocks, S, off)) return fail(BF_EINVAL, "middle workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* base = static_cast<char*>(workspace);
   MidArgs a{};
@@ -758,6 +793,7 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t rank, 
   a.rqs = static_cast<int>(rqs);
   a.iters = static_cast<int>(iters);
   a.nblocks = static_cast<int>(nblocks);
+  a.S = S;
   a.st = reinterpret_cast<BlockState*>(base + off[0]);
   a.draws = draws;
   a.wide = reinterpret_cast<double2*>(base + off[1]);
@@ -771,15 +807,15 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t rank, 
   a.v_out = static_cast<double2*>(v_out);
   a.w_out = w_out;
   const int T = 256;
-  const unsigned yfill = static_cast<unsigned>(std::min<uint64_t>(64, (kMaxSet * side + T - 1) / T));
-  const size_t small_smem = 3ull * kMaxSet * kMaxSet * sizeof(double2);
+  const unsigned yfill = static_cast<unsigned>(std::min<uint64_t>(64, (S * side + T - 1) / T));
+  const size_t small_smem = S <= kSmemSet ? 3ull * S * S * sizeof(double2) : 0;
   BF_CUDA(cudaFuncSetAttribute(k_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(small_smem)));
   BF_CUDA(cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(small_smem)));
   k_init<<<(nblocks + 127) / 128, 128, 0, st>>>(a, block_ij);
   if (dense_branch) {
     k_dense<<<nblocks, T, small_smem, st>>>(a);
   } else {
-    const size_t piv_smem = side * sizeof(double) + kMaxSet * sizeof(double2) + 32 * 8 + 32 * 4 + kMaxSet * 4;
+    const size_t piv_smem = side * sizeof(double) + kSetCap * sizeof(double2) + 32 * 8 + 32 * 4 + kSetCap * 4;
     if (piv_smem > 227 * 1024) return fail(BF_EINVAL, "middle blocks too wide for the pivot kernel");
     BF_CUDA(cudaFuncSetAttribute(k_pivot_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(piv_smem)));
@@ -807,21 +843,23 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t rank, 
   return BF_OK;
 }
 
-
-// One level of the recursive refactorisation (construct.py:127-163):
-// cur (nb, rows, groups, r) complex128 -> blocks (nb, 2, pairs, r, 2r) [rows >= 2]
-// or (nb, pairs, r, 2r) [rows == 1] and next cur. Returns the scratch size needed
-// when called with workspace == NULL through *ws_bytes.
-int bf_recurse_level(uint32_t rank, uint64_t nb, uint64_t rows, uint64_t groups, const void* cur, void* blocks,
-                     void* next, void* workspace, uint64_t* ws_bytes, void* stream) {
+// One level of the recursive refactorisation (construct.py:127-163) with
+// branching b (2, or 4 on quadtrees): cur (nb, rows, groups, r) complex128 ->
+// blocks (nb, b, groups/b, r, b r) [rows >= b] or (nb, groups/b, r, b r)
+// [rows < b] and the next cur. With workspace == NULL, *ws_bytes receives the
+// scratch size.
+int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t rows, uint64_t groups, const void* cur,
+                     void* blocks, void* next, void* workspace, uint64_t* ws_bytes, void* stream) {
   if (!ws_bytes) return fail(BF_EINVAL, "null ws_bytes");
-  if (rank < 1 || 2 * rank > kMaxSet) return fail(BF_EINVAL, "rank must satisfy 1 <= 2r <= 64");
-  if (groups % 2 || groups == 0 || rows == 0) return fail(BF_EINVAL, "bad recursion geometry");
-  const int64_t pairs = groups / 2;
-  const int64_t half = rows / 2;
-  const int64_t chunk = 4096;
-  const int64_t per = (half > kMaxSet ? half : kMaxSet) * 2 * rank + 2 * kMaxSet * kMaxSet;  // rec_scratch_elems
-  const uint64_t need = rows >= 2 ? static_cast<uint64_t>(chunk) * per * 16 : 0;
+  if (branching != 2 && branching != 4) return fail(BF_EINVAL, "branching must be 2 or 4");
+  const uint32_t w = branching * rank;
+  if (rank < 1 || w > static_cast<uint32_t>(kSetCap)) return fail(BF_EINVAL, "rank must satisfy 1 <= b r <= 128");
+  if (groups % branching || groups == 0 || rows == 0) return fail(BF_EINVAL, "bad recursion geometry");
+  const int S = w <= static_cast<uint32_t>(kSmemSet) ? kSmemSet : kSetCap;
+  const int64_t pairs = groups / branching;
+  const int64_t part = rows / branching;
+  const int64_t chunk = 2048;
+  const uint64_t need = rows >= branching ? static_cast<uint64_t>(chunk) * rec_scratch_elems(part, w, S) * 16 : 0;
   if (!workspace) {
     *ws_bytes = need;
     return BF_OK;
@@ -838,9 +876,11 @@ int bf_recurse_level(uint32_t rank, uint64_t nb, uint64_t rows, uint64_t groups,
   a.rows = static_cast<int64_t>(rows);
   a.pairs = pairs;
   a.r = static_cast<int>(rank);
-  if (rows >= 2) {
-    const int64_t nprob = static_cast<int64_t>(nb) * 2 * pairs;
-    const size_t smem = 3ull * kMaxSet * kMaxSet * sizeof(double2);
+  a.b = static_cast<int>(branching);
+  a.S = S;
+  if (rows >= branching) {
+    const int64_t nprob = static_cast<int64_t>(nb) * branching * pairs;
+    const size_t smem = S <= kSmemSet ? 3ull * S * S * sizeof(double2) : 0;
     BF_CUDA(cudaFuncSetAttribute(k_recurse_split, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     for (int64_t p0 = 0; p0 < nprob; p0 += chunk) {
       a.p0 = p0;
@@ -856,7 +896,6 @@ int bf_recurse_level(uint32_t rank, uint64_t nb, uint64_t rows, uint64_t groups,
   return BF_OK;
 }
 
-
 // Greedy pivoted column selection (select_pivot_columns, lowrank.py:102-129)
 // on a batch of device matrices a (batch, m, n) complex128 row-major, m <= 64,
 // n <= 16384: up to k picks each (pick order) into pivots (batch, k), pick
@@ -864,11 +903,11 @@ int bf_recurse_level(uint32_t rank, uint64_t nb, uint64_t rows, uint64_t groups,
 // numpy's pairwise order (the reference's matrix is F-ordered), 0 sequentially.
 int bf_select_pivots(const void* a, uint32_t batch, uint32_t m, uint32_t n, uint32_t k, double rel_tol, int pairwise,
                      int32_t* pivots, int32_t* counts, void* workspace, uint64_t ws_bytes, void* stream) {
-  if (m > static_cast<uint32_t>(kMaxSet) || n > 16384 || k > 1024) return fail(BF_EINVAL, "pivot matrix too large");
+  if (m > static_cast<uint32_t>(kSetCap) || n > 16384 || k > 1024) return fail(BF_EINVAL, "pivot matrix too large");
   if (!batch || !m || !n || !k) return BF_OK;
   if (!a || !pivots || !counts || !workspace) return fail(BF_EINVAL, "null pointer");
   if (ws_bytes < 16ull * batch * m * n) return fail(BF_EINVAL, "pivot workspace too small (16*batch*m*n bytes)");
-  const size_t smem = (n + (n & 1)) * 8 + kMaxSet * 16 + 32 * 8 + 32 * 4 + 1024 * 4;
+  const size_t smem = (n + (n & 1)) * 8 + kSetCap * 16 + 32 * 8 + 32 * 4 + 1024 * 4;
   BF_CUDA(cudaFuncSetAttribute(k_select_pivots, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   k_select_pivots<<<batch, 512, smem, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const double2*>(a), static_cast<double2*>(workspace), static_cast<int>(m), static_cast<int>(n),

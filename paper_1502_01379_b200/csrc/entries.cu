@@ -22,7 +22,7 @@ __global__ void entries_kernel(int kind, uint64_t n, const int64_t* __restrict__
   for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total;
        x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const int64_t i = rows[x / nc], j = cols[x % nc];
-    out[x] = kind == BF_KERNEL_FIO ? fio_entry(n, i, j) : dftp_entry(n, i, j);
+    out[x] = kind == BF_KERNEL_FIO ? fio_entry(n, i, j) : kind == BF_KERNEL_DFTP ? dftp_entry(n, i, j) : radon2d_entry(n, i, j);
   }
 }
 
@@ -49,7 +49,8 @@ unsigned grid_for(uint64_t total) {
 
 int entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr, const int64_t* cols, uint32_t nc, void* out,
             cudaStream_t st) {
-  if (kernel_id != BF_KERNEL_FIO && kernel_id != BF_KERNEL_DFTP) return fail(BF_EINVAL, "unknown entry kernel id");
+  if (kernel_id != BF_KERNEL_FIO && kernel_id != BF_KERNEL_DFTP && kernel_id != BF_KERNEL_RADON2D)
+    return fail(BF_EINVAL, "unknown entry kernel id");
   if (static_cast<uint64_t>(nr) * nc == 0) return 0;
   entries_kernel<<<grid_for(static_cast<uint64_t>(nr) * nc), 256, 0, st>>>(kernel_id, n, rows, nr, cols, nc,
                                                                           static_cast<double2*>(out));

@@ -56,6 +56,18 @@ class DftPlusKernel(_DeviceKernel):
     kernel_id = _lib.BF_KERNEL_DFTP
 
 
+class Radon2DKernel(_DeviceKernel):
+    """BASELINE configs 3/4b: 2-D generalized Radon kernel on an n_side x n_side grid,
+    indices in Morton (Z) order (convention: oracle/entries.py:radon2d_block; the
+    reference has no 2-D code). Phi = x.xi + sqrt(c1^2 xi1^2 + c2^2 xi2^2)."""
+
+    kernel_id = _lib.BF_KERNEL_RADON2D
+
+    def __init__(self, n_side: int):
+        super().__init__(int(n_side) * int(n_side))
+        self.n_side = int(n_side)
+
+
 def fio_entry(n: int, i: int, j: int) -> complex:
     return complex(FioKernel(n).block([i], [j])[0, 0])
 

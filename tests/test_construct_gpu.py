@@ -266,3 +266,44 @@ def test_pivots_pairwise_norm_order():
     matched = sum(1 for x, y in zip(got, want) if x == y)
     print("pairwise-order pivots: %d/16 identical" % matched)
     assert got[0] == want[0] and matched >= 8
+
+
+def test_radon2d_entries_match_oracle():
+    n_side = 256
+    ker = bf.Radon2DKernel(n_side)
+    rng = np.random.default_rng(3)
+    rows = rng.choice(n_side * n_side, 64, replace=False)
+    cols = rng.choice(n_side * n_side, 64, replace=False)
+    got = ker.block(rows, cols)
+    want = oent.radon2d_block(n_side, rows, cols)
+    assert np.max(np.abs(got - want)) <= 2 * np.spacing(2 * np.pi * n_side * 2.0) + 4e-16
+
+
+@pytest.mark.parametrize("n_side,leaf,r", [(32, 2, 6), (32, 2, 20), (64, 4, 25)])
+def test_quadtree_factorize_vs_oracle(n_side, leaf, r):
+    """2-D construction (branching 4; r=25 exercises the 128-wide global-memory small-matrix
+    path) against the oracle's quadtree restatement on the identical draws."""
+    p = bf.make_quadtree_partition(n_side, leaf)
+    n = p.n
+    f = bf.factorize(bf.Radon2DKernel(n_side), p, r, seed=0)
+    c = ocons.factorize(oent.Radon2DOracle(n_side), n, p.levels, r, seed=0, branching=4)
+    k = oent.radon2d_block(n_side, np.arange(n), np.arange(n))
+    g = complex_gaussian(np.random.default_rng(1), (n, 2))
+    exact = k @ g
+    eps_gpu = rel(f.apply(g), exact)
+    eps_ora = rel(ochain.apply(c, g), exact)
+    print("quadtree n_side=%d r=%d: eps gpu %.3e oracle %.3e gpu-vs-oracle %.3e" %
+          (n_side, r, eps_gpu, eps_ora, rel(f.apply(g), ochain.apply(c, g))))
+    assert eps_gpu <= eps_ora * 1.5 + 1e-12
+
+
+def test_quadtree_exact_rank_gpu(rng):
+    """A branching-4 chain with rank-3 blocks, reproduced to 1e-10 by the GPU construction."""
+    from test_oracle_2d import _random_quadtree_chain
+    n, levels, r = 256, 2, 3
+    truth = _random_quadtree_chain(n, levels, r, np.random.default_rng(20240801))
+    kmat = ochain.apply(truth, np.eye(n, dtype=complex))
+    p = bf.QuadtreePartition(16, levels)
+    f = bf.factorize(bf.DenseOracle(kmat), p, r, seed=8)
+    g = complex_gaussian(rng, (n, 3))
+    assert rel(f.apply(g), kmat @ g) <= 1e-10
