@@ -32,11 +32,22 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (kernel, n, r, leaf, default rhs)
+    # name: (kernel, n, r, leaf, default rhs); 2-D (radon) configs give the grid side
+    # as leaf = leaf box side and n = n_side^2 (quadtree over Morton-ordered points)
     "cfg0": ("fio", 1 << 10, 12, 8, 1),
     "cfg1": ("dftp", 1 << 16, 8, 16, 64),
     "cfg2": ("fio", 1 << 20, 16, 16, 1),
+    "cfg3": ("radon2d", 1 << 16, 25, 4, 16),
+    "cfg4a": ("fio", 1 << 24, 16, 16, 64),
+    "cfg4b": ("radon2d", 1 << 20, 25, 4, 16),
 }
+
+
+def partition_for(kern, n, leaf):
+    import paper_1502_01379_b200 as bf
+    if kern == "radon2d":
+        return bf.make_quadtree_partition(int(round(n ** 0.5)), leaf)
+    return bf.make_partition(n, leaf)
 METRIC = "BF apply complex-samples/s (N*nRHS/s)"
 
 
@@ -155,7 +166,7 @@ def run_reference(args):
     k = args.rhs or k0
     from paper_1502_01379_b200.partition import make_partition
     from paper_1502_01379_b200.synthetic import synthetic_chain
-    p = make_partition(n, leaf)
+    p = partition_for(kern, n, leaf)
     fh = synthetic_chain(p, r, seed=20240801)
     g = rhs_input(n, k)
     from oracle import chain as ochain
@@ -179,7 +190,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": val, "unit": "samples/s", "n_gpus": args.gpus,
         "steps": len(times), "warmup": min(args.warmup, 1), "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": f"{args.config} FIO N={n} r={r} leaf={leaf} k={k} c128 (oracle port)",
+        "config": {"workload": f"{args.config} {kern.upper()} N={n} r={r} leaf={leaf} k={k} c128 (oracle port)",
                    "n": n, "rank": r, "rhs": k},
         "cpu_baseline": {"value": val, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": val, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -200,10 +211,10 @@ def run_sharded(args, world, rank, local):
     kern, n, r, leaf, k0 = CONFIGS[args.config]
     k = args.rhs or k0
     esz = 16 if args.dtype == "c128" else 8
-    p = bf.make_partition(n, leaf)
-    f = synthetic_chain(p, r, seed=20240801, device="cuda")   # identical chain on every rank; keep this rank's slice
-    sp = ShardedPlan.from_factors(f, rank, world, dtype=args.dtype)
-    del f
+    p = partition_for(kern, n, leaf)
+    from paper_1502_01379_b200.synthetic import synthetic_slices
+    sp = ShardedPlan(p, r, rank, world, synthetic_slices(p, r, rank, world, seed=20240801, device="cuda"),
+                     dtype=args.dtype)
     torch.cuda.empty_cache()
     tdt = torch.complex128 if args.dtype == "c128" else torch.complex64
     nl = n // world
@@ -297,6 +308,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1 or args.sharded:
+        os.environ["NCCL_DEBUG"] = "WARN"   # keep stdout to the one JSON line
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29511")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
@@ -304,7 +316,7 @@ def main():
     kern, n, r, leaf, k0 = CONFIGS[args.config]
     k = args.rhs or k0
     esz = 16 if args.dtype == "c128" else 8
-    p = bf.make_partition(n, leaf)
+    p = partition_for(kern, n, leaf)
     f = synthetic_chain(p, r, seed=20240801 + rank, device="cuda")
     plan = f.plan(args.dtype)
     lib = _lib.load()

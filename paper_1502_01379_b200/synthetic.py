@@ -66,3 +66,26 @@ def to_host(f: ButterflyFactors) -> ButterflyFactors:
                             MiddleFactor(h(f.middle.weights)),
                             tuple(TransferFactor(t.level, h(t.blocks)) for t in f.h_chain),
                             BlockDiagonalFactor(h(f.v_outer.blocks)))
+
+
+def synthetic_slices(p, r: int, part: int, nparts: int, seed: int = 20240801, device=None) -> dict:
+    """One part's factor slices (the ``shard_slices`` layout) drawn directly, seeded per part,
+    for chains too large to materialise whole (BASELINE config 4a: 180 GB in complex128).
+    Equivalent in distribution to slicing a synthetic chain; weights are shared by all parts."""
+    import torch
+    shapes, leaf_shape = level_geometry(p, r)
+    gen = torch.Generator(device=device or "cpu")
+    gen.manual_seed(seed * 1009 + part)
+    dev = device or "cpu"
+
+    def draw(shape):
+        shape = (shape[0] // nparts,) + tuple(shape[1:])
+        t = torch.randn(shape + (2,), dtype=torch.float64, device=dev, generator=gen)
+        t.mul_(1.0 / np.sqrt(2.0 * shape[-1]))
+        return torch.view_as_complex(t)
+
+    wgen = torch.Generator(device=dev)
+    wgen.manual_seed(seed)
+    weights = torch.rand((p.mid_nodes, p.mid_nodes, r), dtype=torch.float64, device=dev, generator=wgen).add_(0.5)
+    return {"v_leaf": draw(leaf_shape), "h": [(lvl, draw(s)) for lvl, _, s in shapes], "weights": weights,
+            "g": [(lvl, draw(s)) for lvl, _, s in shapes], "u_leaf": draw(leaf_shape)}
