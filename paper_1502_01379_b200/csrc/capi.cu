@@ -1,5 +1,6 @@
 // capi.cu — the extern "C" boundary declared in include/bfly.h.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -92,6 +93,8 @@ static int create_plan(bf_plan** out, uint64_t n, uint32_t levels, uint32_t rank
     return fail(BF_EINVAL, "no such CUDA device");
   bf_plan* h = new (std::nothrow) bf_plan();
   if (!h) return fail(BF_ENOMEM, "host allocation failed");
+  const char* ng = std::getenv("BF_NO_GRAPHS");
+  h->graphs_enabled = !(ng && ng[0] && ng[0] != '0');
   Plan& p = h->p;
   p.device = device;
   p.dtype = dtype;
@@ -155,10 +158,10 @@ int bf_plan_create_tree(bf_plan** out, uint64_t n, uint32_t levels, uint32_t ran
 
 void bf_plan_destroy(bf_plan* plan) {
   if (!plan) return;
-  if (plan->p.base) {
-    DeviceGuard dg(plan->p.device);
-    cudaFree(plan->p.base);
-  }
+  DeviceGuard dg(plan->p.device);
+  for (auto& gentry : plan->graphs) cudaGraphExecDestroy(gentry.exec);
+  if (plan->own_stream) cudaStreamDestroy(plan->own_stream);
+  if (plan->p.base) cudaFree(plan->p.base);
   delete plan;
 }
 
@@ -265,7 +268,47 @@ int bf_apply(const bf_plan* plan, const void* in, void* out, uint32_t k, int adj
     return fail(BF_EINVAL, "workspace too small (see bf_apply_workspace_bytes)");
   if (p.nparts != 1) return fail(BF_EINVAL, "sharded plan: use bf_apply_down / bf_middle_pack / bf_apply_up");
   DeviceGuard dg(p.device);
-  return plan_apply(p, in, out, k, adjoint ? 1 : 0, workspace, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!plan->graphs_enabled) return plan_apply(p, in, out, k, adjoint ? 1 : 0, workspace, st);
+  // The chain is a fixed sequence of 2 + 2(L-h) launches: replay it as one CUDA
+  // graph per (buffers, k, direction, stream). A NULL stream is the legacy default
+  // stream, which cannot be captured; the graph then runs on a plan-owned blocking
+  // stream, which the legacy stream orders against implicitly.
+  std::lock_guard<std::mutex> lock(plan->gmu);
+  cudaStream_t run = st;
+  if (!run) {
+    if (!plan->own_stream) BF_CUDA(cudaStreamCreate(&plan->own_stream));
+    run = plan->own_stream;
+  }
+  for (const auto& gentry : plan->graphs)
+    if (gentry.in == in && gentry.out == out && gentry.ws == workspace && gentry.k == k && gentry.adjoint == adjoint &&
+        gentry.stream == st) {
+      BF_CUDA(cudaGraphLaunch(gentry.exec, run));
+      return BF_OK;
+    }
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  BF_CUDA(cudaStreamIsCapturing(run, &cap));
+  if (cap != cudaStreamCaptureStatusNone) return plan_apply(p, in, out, k, adjoint ? 1 : 0, workspace, st);
+  BF_CUDA(cudaStreamBeginCapture(run, cudaStreamCaptureModeThreadLocal));
+  const int rc = plan_apply(p, in, out, k, adjoint ? 1 : 0, workspace, run);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(run, &graph);
+  if (rc) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) return cuda_fail(ei, "cudaGraphInstantiate");
+  if (plan->graphs.size() >= 16) {
+    cudaGraphExecDestroy(plan->graphs.front().exec);
+    plan->graphs.erase(plan->graphs.begin());
+  }
+  plan->graphs.push_back({in, out, workspace, k, adjoint, st, exec});
+  BF_CUDA(cudaGraphLaunch(exec, run));
+  return BF_OK;
 }
 
 int bf_apply_down(const bf_plan* plan, const void* in, void* mid, uint32_t k, int adjoint, void* workspace,

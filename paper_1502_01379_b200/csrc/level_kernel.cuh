@@ -222,6 +222,19 @@ __device__ __forceinline__ void consume_tile(const LevelArgs& a, uint32_t tile, 
       }
       const uint32_t c = rest % a.C;
       const uint32_t ul = rest / a.C;
+      // destination (and, with the fused middle factor, its weight) first: the weight's
+      // global load then overlaps the dot product instead of trailing it
+      size_t dst = static_cast<size_t>(t.u0 + ul) * a.C + c;
+      Rl w = 1;
+      if (a.remap != 0) {
+        const uint32_t mr = a.m * a.r;
+        const uint32_t e32 = static_cast<uint32_t>(dst), ia = e32 / mr;
+        const uint32_t rem = e32 - ia * mr;
+        const uint32_t ib = rem / a.r, rho = rem - ib * a.r;
+        dst = (static_cast<size_t>(ib) * a.m + ia) * a.r + rho;
+        const Rl* W = static_cast<const Rl*>(a.mid_w);
+        w = a.remap == 1 ? __ldg(W + dst) : __ldg(W + (static_cast<size_t>(ia) * a.m + ib) * a.r + rho);
+      }
       const uint32_t base = (((ul >> t.lgPe) * a.nt) << t.lgPe) + (ul & Pe_mask);
       Acc8<E> acc;
       for (uint32_t tt = 0; tt < a.nt; ++tt) {
@@ -236,21 +249,8 @@ __device__ __forceinline__ void consume_tile(const LevelArgs& a, uint32_t tile, 
         if (rho < a.R) acc.mac(0, acol[static_cast<size_t>(rho) * a.C], y[static_cast<size_t>(rho) * kc]);
       }
       const E v = acc.sum_conj();
-      const size_t e = static_cast<size_t>(t.u0 + ul) * a.C + c;
-      if (a.remap == 0) {
-        E& o_ = out[e * a.k + t.k0 + kk];
-        o_ = a.accumulate ? Cx<E>::make(o_.x + v.x, o_.y + v.y) : v;
-      } else {
-        const uint32_t mr = a.m * a.r;
-        const uint32_t e32 = static_cast<uint32_t>(e), ia = e32 / mr;
-        const uint32_t rem = e32 - ia * mr;
-        const uint32_t ib = rem / a.r, rho = rem - ib * a.r;
-        const size_t dst = (static_cast<size_t>(ib) * a.m + ia) * a.r + rho;
-        const Rl* W = static_cast<const Rl*>(a.mid_w);
-        const Rl w = a.remap == 1 ? W[dst] : W[(static_cast<size_t>(ia) * a.m + ib) * a.r + rho];
-        E& o_ = out[dst * a.k + t.k0 + kk];
-        o_ = a.accumulate ? Cx<E>::make(o_.x + w * v.x, o_.y + w * v.y) : Cx<E>::make(w * v.x, w * v.y);
-      }
+      E& o_ = out[dst * a.k + t.k0 + kk];
+      o_ = a.accumulate ? Cx<E>::make(o_.x + w * v.x, o_.y + w * v.y) : Cx<E>::make(w * v.x, w * v.y);
     }
   }
 }
@@ -285,7 +285,9 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, uint32_t t
     const uint32_t cg = it % ncg;
     const uint32_t rest = it / ncg;
     const uint32_t rg = rest % nrg, ul = rest / nrg;
-    const uint32_t col0 = cg * LC * TN + lc, row0 = (rg * LR + lr) * TM;
+    // rows of this lane: rb + lr + LR*i (interleaved, so the LR row groups of a warp read
+    // adjacent A columns / rows and land in different banks)
+    const uint32_t col0 = cg * LC * TN + lc, rb = rg * LR * TM + lr;
     const uint32_t base = (((ul >> t.lgPe) * a.nt) << t.lgPe) + (ul & Pe_mask);
     bool colok[TN];
 #pragma unroll
@@ -300,7 +302,7 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, uint32_t t
       const E* arow[TM];
 #pragma unroll
       for (int i = 0; i < TM; ++i) {
-        const uint32_t o = min(row0 + i, m_out - 1);
+        const uint32_t o = min(rb + LR * i, m_out - 1);
         const uint32_t tt = o / a.R, rho = o - tt * a.R;
         arow[i] = fs + (static_cast<size_t>(base + (tt << t.lgPe)) * a.R + rho) * a.C;
       }
@@ -324,7 +326,7 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, uint32_t t
       const uint32_t u = t.u0 + ul;
 #pragma unroll
       for (int i = 0; i < TM; ++i) {
-        const uint32_t o = row0 + i;
+        const uint32_t o = rb + LR * i;
         if (o >= m_out) break;
         const uint32_t tt = o / a.R, rho = o - tt * a.R;
         const uint32_t q = ((((u >> a.lgP) * a.ntot) + a.t0 + tt) << a.lgP) + (u & P_mask);
@@ -345,7 +347,7 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, uint32_t t
           const E* acol = fs + row * a.C;
 #pragma unroll
           for (int i = 0; i < TM; ++i) {
-            const E av = acol[min(row0 + i, m_out - 1)];
+            const E av = acol[min(rb + LR * i, m_out - 1)];
 #pragma unroll
             for (int j = 0; j < TN; ++j) {  // conj(av) * yv
               re[i][j] = fma(av.x, yv[j].x, re[i][j]);
@@ -358,7 +360,7 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, uint32_t t
       }
 #pragma unroll
       for (int i = 0; i < TM; ++i) {
-        const uint32_t c = row0 + i;
+        const uint32_t c = rb + LR * i;
         if (c >= m_out) break;
         size_t e = static_cast<size_t>(t.u0 + ul) * a.C + c;
         Rl w = 1;

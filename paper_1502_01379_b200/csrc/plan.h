@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <vector>
 
 #include "../../include/bfly.h"
@@ -75,6 +76,20 @@ int convert_f64_to_f32(const void* src, void* dst, uint64_t count, cudaStream_t 
 
 struct bf_plan {
   bfly::Plan p;
+  // bf_apply graph cache (the plan itself stays immutable; the cache is guarded)
+  struct GraphEntry {
+    const void* in;
+    void* out;
+    void* ws;
+    uint32_t k;
+    int adjoint;
+    cudaStream_t stream;
+    cudaGraphExec_t exec;
+  };
+  bool graphs_enabled = true;
+  mutable std::mutex gmu;
+  mutable std::vector<GraphEntry> graphs;
+  mutable cudaStream_t own_stream = nullptr;
 };
 
 struct bf_timer {
