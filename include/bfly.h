@@ -185,6 +185,16 @@ int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t ro
                      const void* cur, void* blocks, void* next, void* workspace, uint64_t* ws_bytes,
                      void* stream);
 
+/* Direct sampled-row sums y = K[rows, :] g (rows: device int64 (nr); g, y:
+ * device complex128 (n, k) and (nr, k)) with entries evaluated on the fly:
+ * the ground truth of the reference's accuracy metric eps_a
+ * (RowSampledReference.rows, bench.py:44-46; estimate_eps_a_info 90-97).
+ * Deterministic (fixed-order partial sums in a workspace of
+ * bf_sampled_rows_workspace(n, nr, k) bytes). */
+uint64_t bf_sampled_rows_workspace(uint64_t n, uint32_t nr, uint32_t k);
+int bf_sampled_rows(int kernel_id, uint64_t n, const void* dense, const int64_t* rows, uint32_t nr,
+                    const void* g, uint32_t k, void* out, void* workspace, uint64_t ws_bytes, void* stream);
+
 /* Greedy pivoted column selection (select_pivot_columns, lowrank.py:102-129)
  * on a batch of device matrices a (batch, m, n) complex128 row-major with
  * m <= 64: up to k picks each, in pick order, into pivots (batch, k) and pick

@@ -11,6 +11,7 @@ from .factors import (BlockDiagonalFactor, ButterflyFactors, DevicePlan, MiddleF
 from .construct import (DEFAULT_PARAMS, OversamplingParams, factorize, middle_factorization_sampling,
                         recursive_factor_u, recursive_factor_v)
 from .kernels import DenseOracle, DftPlusKernel, FioKernel, Radon2DKernel, fio_entry
+from .metrics import RowSampledReference, estimate_eps_a, estimate_eps_a_info
 from .partition import (BlockId, DyadicPartition, QuadtreePartition, block_cols, block_rows, level_geometry,
                         make_partition, make_quadtree_partition)
 

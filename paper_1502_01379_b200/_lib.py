@@ -47,6 +47,8 @@ SIGNATURES = [
     ("bf_middle_pack", _I, [_P, _P, _P, _U32, _I, _P]),
     ("bf_middle_unpack", _I, [_P, _P, _P, _U32, _I, _P]),
     ("bf_apply_up", _I, [_P, _P, _P, _U32, _I, _P, _U64, _P]),
+    ("bf_sampled_rows_workspace", _U64, [_U64, _U32, _U32]),
+    ("bf_sampled_rows", _I, [_I, _U64, _P, _P, _U32, _P, _U32, _P, _P, _U64, _P]),
     ("bf_entries", _I, [_I, _U64, _P, _U32, _P, _U32, _P, _P]),
 ]
 

@@ -467,6 +467,18 @@ int bf_apply_factor(const bf_plan* plan, int which, uint32_t level, int adjoint,
   return plan_apply_factor(p, which, idx, adjoint ? 1 : 0, in, out, k, static_cast<cudaStream_t>(stream));
 }
 
+uint64_t bf_sampled_rows_workspace(uint64_t n, uint32_t nr, uint32_t k) { return sampled_rows_workspace(n, nr, k); }
+
+int bf_sampled_rows(int kernel_id, uint64_t n, const void* dense, const int64_t* rows, uint32_t nr, const void* g,
+                    uint32_t k, void* out, void* workspace, uint64_t ws_bytes, void* stream) {
+  if (kernel_id < BF_KERNEL_FIO || kernel_id > BF_KERNEL_RADON2D) return fail(BF_EINVAL, "unknown entry kernel id");
+  if (kernel_id == BF_KERNEL_DENSE && !dense) return fail(BF_EINVAL, "dense oracle needs a matrix pointer");
+  if (n < 1 || k < 1) return fail(BF_EINVAL, "n and k must be positive");
+  if (!nr) return BF_OK;
+  if (!rows || !g || !out || !workspace) return fail(BF_EINVAL, "null pointer");
+  return sampled_rows(kernel_id, n, dense, rows, nr, g, k, out, workspace, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
 int bf_entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr, const int64_t* cols, uint32_t nc,
                void* out, void* stream) {
   if (n < 1) return fail(BF_EINVAL, "n must be positive");

@@ -73,3 +73,87 @@ int convert_f64_to_f32(const void* src, void* dst, uint64_t count, cudaStream_t 
 }
 
 }  // namespace bfly
+
+namespace bfly {
+namespace {
+
+// y[s][kk] = sum_j K(rows[s], j) g[j][kk]: the direct O(|S| N) row sums the reference's
+// accuracy metric compares against (RowSampledReference.rows, bench.py:44-46), with the
+// entries evaluated on the fly. One CTA per (sampled row, column chunk); partial sums in a
+// fixed order (deterministic), combined by the host wrapper's second pass.
+__global__ void sampled_rows_kernel(EntrySrc src, const int64_t* __restrict__ rows, uint32_t nr,
+                                    const double2* __restrict__ g, uint32_t k, uint64_t chunk,
+                                    double2* __restrict__ partial) {
+  const uint32_t s = blockIdx.x;
+  const uint64_t j0 = static_cast<uint64_t>(blockIdx.y) * chunk;
+  const uint64_t j1 = min(src.n, j0 + chunk);
+  __shared__ double2 red[32][8];
+  for (uint32_t k0 = 0; k0 < k; k0 += 8) {
+    double2 acc[8];
+    for (int q = 0; q < 8; ++q) acc[q] = make_double2(0, 0);
+    for (uint64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+      const double2 kv = entry_eval(src, rows[s], static_cast<int64_t>(j));
+      for (int q = 0; q < 8 && k0 + q < k; ++q) {
+        const double2 gv = g[j * k + k0 + q];
+        acc[q].x += kv.x * gv.x - kv.y * gv.y;
+        acc[q].y += kv.x * gv.y + kv.y * gv.x;
+      }
+    }
+    for (int q = 0; q < 8; ++q) {
+      double x = acc[q].x, y = acc[q].y;
+      for (int o = 16; o; o >>= 1) {
+        x += __shfl_xor_sync(0xffffffffu, x, o);
+        y += __shfl_xor_sync(0xffffffffu, y, o);
+      }
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][q] = make_double2(x, y);
+    }
+    __syncthreads();
+    if (threadIdx.x < 8 && k0 + threadIdx.x < k) {
+      double2 t = make_double2(0, 0);
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+        t.x += red[w][threadIdx.x].x;
+        t.y += red[w][threadIdx.x].y;
+      }
+      partial[(static_cast<uint64_t>(blockIdx.y) * nr + s) * k + k0 + threadIdx.x] = t;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void sum_partials(const double2* __restrict__ partial, uint32_t nchunks, uint64_t per,
+                             double2* __restrict__ out) {
+  for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < per;
+       x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    double2 t = make_double2(0, 0);
+    for (uint32_t c = 0; c < nchunks; ++c) {
+      t.x += partial[c * per + x].x;
+      t.y += partial[c * per + x].y;
+    }
+    out[x] = t;
+  }
+}
+
+}  // namespace
+
+int sampled_rows(int kernel_id, uint64_t n, const void* dense, const int64_t* rows, uint32_t nr, const void* g,
+                 uint32_t k, void* out, void* workspace, uint64_t ws_bytes, cudaStream_t st) {
+  const uint64_t chunk = 8192;
+  const uint32_t nchunks = static_cast<uint32_t>((n + chunk - 1) / chunk);
+  const uint64_t need = 16ull * nchunks * nr * k;
+  if (ws_bytes < need) return fail(BF_EINVAL, "sampled-rows workspace too small");
+  EntrySrc src{kernel_id, n, static_cast<const double2*>(dense)};
+  sampled_rows_kernel<<<dim3(nr, nchunks), 256, 0, st>>>(src, rows, nr, static_cast<const double2*>(g), k, chunk,
+                                                         static_cast<double2*>(workspace));
+  const uint64_t per = static_cast<uint64_t>(nr) * k;
+  sum_partials<<<static_cast<unsigned>((per + 255) / 256), 256, 0, st>>>(static_cast<const double2*>(workspace),
+                                                                         nchunks, per, static_cast<double2*>(out));
+  BF_CUDA(cudaGetLastError());
+  return 0;
+}
+
+uint64_t sampled_rows_workspace(uint64_t n, uint32_t nr, uint32_t k) {
+  const uint64_t chunk = 8192;
+  return 16ull * ((n + chunk - 1) / chunk) * nr * k;
+}
+
+}  // namespace bfly

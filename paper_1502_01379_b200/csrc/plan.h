@@ -69,6 +69,9 @@ int plan_apply_factor(const Plan& pl, int which, int lvl_idx, int adjoint, const
                       cudaStream_t st);
 int entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr, const int64_t* cols, uint32_t nc, void* out,
             cudaStream_t st);
+int sampled_rows(int kernel_id, uint64_t n, const void* dense, const int64_t* rows, uint32_t nr, const void* g,
+                 uint32_t k, void* out, void* workspace, uint64_t ws_bytes, cudaStream_t st);
+uint64_t sampled_rows_workspace(uint64_t n, uint32_t nr, uint32_t k);
 int convert_c128_to_c64(const void* src, void* dst, uint64_t count, cudaStream_t st);
 int convert_f64_to_f32(const void* src, void* dst, uint64_t count, cudaStream_t st);
 

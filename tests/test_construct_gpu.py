@@ -307,3 +307,24 @@ def test_quadtree_exact_rank_gpu(rng):
     f = bf.factorize(bf.DenseOracle(kmat), p, r, seed=8)
     g = complex_gaussian(rng, (n, 3))
     assert rel(f.apply(g), kmat @ g) <= 1e-10
+
+
+def test_eps_a_matches_reference_golden():
+    """estimate_eps_a of the reference's own cfg0 factors with the GPU row sums equals the
+    value the reference computed (bench.py:90-97, seeded as _run_row does, 208-211)."""
+    d = golden("apply_cfg0_fio_n1024_r12_leaf8.npz")
+    f = bf.from_arrays(int(d["n"]), int(d["levels"]), int(d["rank"]), d["u_leaf"],
+                       [(int(l), d[f"g_{int(l)}"]) for l in d["g_lvls"]], d["weights"],
+                       [(int(l), d[f"h_{int(l)}"]) for l in d["h_lvls"]], d["v_leaf"])
+    ref = bf.RowSampledReference(bf.FioKernel(f.n))
+    eps = bf.estimate_eps_a(f, ref, 256, np.random.SeedSequence(0, spawn_key=(4, 0)))
+    assert abs(eps - float(d["eps_a"])) <= 1e-10 * float(d["eps_a"])
+    # direct row sums against the oracle's dense rows, DFT(+) and 2-D kernels too
+    rng = np.random.default_rng(4)
+    for ker, blk, n in ((bf.DftPlusKernel(4096), lambda r, c: oent.dftp_block(4096, r, c), 4096),
+                        (bf.Radon2DKernel(64), lambda r, c: oent.radon2d_block(64, r, c), 4096)):
+        rows = np.sort(rng.choice(n, 40, replace=False))
+        g = complex_gaussian(rng, (n, 3))
+        got = bf.RowSampledReference(ker).rows(g, rows)
+        want = blk(rows, np.arange(n)) @ g
+        assert rel(got, want) <= 1e-12
