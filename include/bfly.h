@@ -39,6 +39,7 @@ extern "C" {
 #define BF_ENOMEM 3
 #define BF_EORACLE 4
 #define BF_ESTATE 5
+#define BF_EFORMAT 6 /* malformed .bfac file: Python FormatError (storage.py:40-45) */
 
 #define BF_C128 0 /* complex128 factors + vectors (the reference's dtype, factors.py:222) */
 #define BF_C64 1  /* opt-in complex64 mode (fp32 arithmetic) */
@@ -144,6 +145,17 @@ int bf_middle_pack(const bf_plan* plan, const void* mid, void* send, uint32_t k,
 int bf_middle_unpack(const bf_plan* plan, const void* recv, void* mid, uint32_t k, int adjoint, void* stream);
 int bf_apply_up(const bf_plan* plan, const void* mid, void* out, uint32_t k, int adjoint,
                 void* workspace, uint64_t workspace_bytes, void* stream);
+
+/* The reference's .bfac factor file (storage.py:1-186) straight to/from a
+ * device plan: records stream through a pinned buffer; one kernel per chunk
+ * checks every block header against the geometry (mismatch -> BF_EFORMAT,
+ * message carries the byte offset) and transposes the column-major payloads
+ * into the plan layout. save -> load -> save is byte-identical
+ * (save_factors/load_factors, storage.py:79-167). bf_plan_export copies one
+ * factor array (reference layout, plan dtype) to dst. */
+int bf_plan_load_bfac(bf_plan** out, const char* path, int dtype, int device);
+int bf_plan_save_bfac(const bf_plan* plan, const char* path);
+int bf_plan_export(const bf_plan* plan, int which, uint32_t level, void* dst, uint64_t dst_bytes, void* stream);
 
 /* Dense entry block K[rows[a], cols[b]] -> out (nr, nc) complex128 on the
  * device; rows/cols are device int64 arrays. Replaces FioKernel.block

@@ -148,9 +148,24 @@ def gen_geometry(bf):
     print("geometry.npz")
 
 
+def gen_bfac(bf):
+    """A .bfac file and a vector file written by the reference's storage.py."""
+    p = bf.make_partition(128, 0.25)
+    f = bf.factorize(bf.FioKernel(128), p, 4, seed=9)
+    bf.save_factors(f, os.path.join(OUT, "fio_n128_r4_leaf025.bfac"))
+    g = bf.lowrank.complex_normal(np.random.default_rng(3), (128,))
+    bf.write_vector(os.path.join(OUT, "g128.vec"), g)
+    bf.write_vector(os.path.join(OUT, "u128.vec"), f.apply(g))
+    p = bf.make_partition(1024, 16)
+    f = bf.factorize(bf.FioKernel(1024), p, 8, seed=2)
+    bf.save_factors(f, os.path.join(OUT, "fio_n1024_r8_leaf16.bfac"))
+    print("bfac fixtures")
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     bf = _ref()
+    gen_bfac(bf)
     gen_geometry(bf)
     gen_entries(bf)
     gen_pivots(bf)

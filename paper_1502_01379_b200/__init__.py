@@ -12,6 +12,7 @@ from .construct import (DEFAULT_PARAMS, OversamplingParams, factorize, middle_fa
                         recursive_factor_u, recursive_factor_v)
 from .kernels import DenseOracle, DftPlusKernel, FioKernel, Radon2DKernel, fio_entry
 from .metrics import RowSampledReference, estimate_eps_a, estimate_eps_a_info
+from .storage import FormatError, load_factors, read_vector, save_factors, write_vector
 from .partition import (BlockId, DyadicPartition, QuadtreePartition, block_cols, block_rows, level_geometry,
                         make_partition, make_quadtree_partition)
 

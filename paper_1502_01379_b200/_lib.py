@@ -13,7 +13,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbfly.so")
 
-BF_OK, BF_EINVAL, BF_ECUDA, BF_ENOMEM, BF_EORACLE, BF_ESTATE = range(6)
+BF_OK, BF_EINVAL, BF_ECUDA, BF_ENOMEM, BF_EORACLE, BF_ESTATE, BF_EFORMAT = range(7)
 BF_C128, BF_C64 = 0, 1
 BF_FACTOR_V, BF_FACTOR_H, BF_FACTOR_M, BF_FACTOR_G, BF_FACTOR_U = range(5)
 BF_KERNEL_FIO, BF_KERNEL_DFTP, BF_KERNEL_DENSE, BF_KERNEL_RADON2D = 0, 1, 2, 3
@@ -49,6 +49,9 @@ SIGNATURES = [
     ("bf_apply_up", _I, [_P, _P, _P, _U32, _I, _P, _U64, _P]),
     ("bf_sampled_rows_workspace", _U64, [_U64, _U32, _U32]),
     ("bf_sampled_rows", _I, [_I, _U64, _P, _P, _U32, _P, _U32, _P, _P, _U64, _P]),
+    ("bf_plan_load_bfac", _I, [ctypes.POINTER(_P), ctypes.c_char_p, _I, _I]),
+    ("bf_plan_save_bfac", _I, [_P, ctypes.c_char_p]),
+    ("bf_plan_export", _I, [_P, _I, _U32, _P, _U64, _P]),
     ("bf_entries", _I, [_I, _U64, _P, _U32, _P, _U32, _P, _P]),
 ]
 
@@ -57,6 +60,14 @@ _lib = None
 
 class OracleError(RuntimeError):
     """Raised when an oracle fails (reference oracles.py:18-19)."""
+
+
+class FormatError(ValueError):
+    """Malformed factor or vector file; ``offset`` is the failing byte (storage.py:40-45)."""
+
+    def __init__(self, message: str, offset: int):
+        super().__init__(message if "(at byte" in message else f"{message} (at byte {offset})")
+        self.offset = offset
 
 
 def load(path: str = LIB_PATH) -> ctypes.CDLL:
@@ -93,6 +104,10 @@ def check(rc: int, what: str = "") -> None:
         raise ValueError(msg)
     if rc == BF_EORACLE:
         raise OracleError(msg)
+    if rc == BF_EFORMAT:
+        import re
+        m = re.search(r"\(at byte (\d+)\)", msg)
+        raise FormatError(msg, int(m.group(1)) if m else -1)
     if rc == BF_ENOMEM:
         raise MemoryError(msg)
     raise RuntimeError(msg)

@@ -193,6 +193,19 @@ class DevicePlan:
                                       h_ptrs, ptr(f.v_outer.blocks)), "bf_plan_upload")
         del keep
 
+    @classmethod
+    def adopt(cls, f: "ButterflyFactors", handle, dtype: str, device: int) -> "DevicePlan":
+        """Wrap an already uploaded bf_plan (e.g. one built by bf_plan_load_bfac)."""
+        import torch
+        pl = cls.__new__(cls)
+        pl._lib = _lib.load()
+        pl._h = handle
+        pl.n, pl.dtype, pl.device = f.n, dtype, device
+        pl.torch_dtype = torch.complex128 if dtype == "c128" else torch.complex64
+        pl.np_dtype = np.complex128 if dtype == "c128" else np.complex64
+        pl._check_geometry(f)
+        return pl
+
     def _check_geometry(self, f):
         nl = ctypes.c_uint32()
         self._lib.bf_plan_geometry(self._h, ctypes.byref(nl), None, None, None)
