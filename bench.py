@@ -62,6 +62,7 @@ def parse():
     ap.add_argument("--rhs", type=int, default=0, help="right-hand sides (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the node-sharded path even at one rank")
+    ap.add_argument("--no-also", action="store_true", help="skip the companion configs[1] measurement")
     return ap.parse_args()
 
 
@@ -195,6 +196,38 @@ def run_reference(args):
         "cpu_baseline": {"value": val, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": val, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+def companion_cfg1(steps, warm):
+    """BASELINE configs[1]: DFT(+) N=2^16, r=8, leaf 16 (L=12), 64 RHS, complex128 — value,
+    FP64 rate and the CPU reference apply on the identical factors (oracle port, 1 apply)."""
+    import torch
+
+    from paper_1502_01379_b200.synthetic import synthetic_chain, to_host
+    kern, n, r, leaf, k = CONFIGS["cfg1"]
+    p = partition_for(kern, n, leaf)
+    f = synthetic_chain(p, r, seed=20240801, device="cuda")
+    plan = f.plan("c128")
+    g_host = rhs_input(n, k)
+    g = torch.from_numpy(g_host).cuda()
+    out = torch.empty_like(g)
+    ws = torch.empty(plan.workspace_bytes(k), dtype=torch.uint8, device="cuda")
+    for _ in range(warm):
+        plan.apply(g, out=out, workspace=ws)
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        plan.apply(g, out=out, workspace=ws)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    _, flops = algorithmic(f, k, 16)
+    t_cpu, nrun = time_cpu(to_host(f), g_host, budget_s=10.0, max_steps=2)
+    return {"workload": f"cfg1 DFTP N={n} r={r} leaf={leaf} (L={p.levels}) k={k} c128", "value": n * k / (ms / 1e3),
+            "unit": "samples/s", "ms_per_step": ms, "fp64_tflops": flops / (ms / 1e3) / 1e12,
+            "cpu_reference_value": n * k / t_cpu, "cpu_reference_ms": t_cpu * 1e3}
 
 
 def run_sharded(args, world, rank, local):
@@ -416,6 +449,12 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    # companion workload: BASELINE configs[1] (DFT(+) N=2^16, r=8, 64 RHS), device-timed through bf_apply
+    also = None
+    if rank == 0 and world == 1 and args.config == "cfg2" and not args.no_also:
+        del ws
+        also = companion_cfg1(steps, warm)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
@@ -453,6 +492,7 @@ def main():
             "gpu_launches": nlaunch * steps,
             "clocks": clk,
             "cpu_baseline": cpu,
+            "also": also,
         }
         print(json.dumps(rec))
     if world > 1:

@@ -146,6 +146,8 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   return 0;
 }
 
+}  // namespace
+
 template <typename E>
 int launch_middle(const Plan& pl, const void* in, void* out, uint32_t k, int adjoint, cudaStream_t st) {
   const uint64_t total = static_cast<uint64_t>(pl.m) * pl.m * pl.rank * k;
@@ -156,6 +158,8 @@ int launch_middle(const Plan& pl, const void* in, void* out, uint32_t k, int adj
   BF_CUDA(cudaGetLastError());
   return 0;
 }
+
+namespace {
 
 // One factor op, dispatched by kind. `lvl_idx` indexes the plan's level table.
 template <typename E>
@@ -332,6 +336,80 @@ int plan_apply_factor(const Plan& pl, int which, int lvl_idx, int adjoint, const
                       cudaStream_t st) {
   return pl.dtype == BF_C128 ? factor_op<double2>(pl, which, lvl_idx, adjoint, in, out, k, 0, st)
                              : factor_op<float2>(pl, which, lvl_idx, adjoint, in, out, k, 0, st);
+}
+
+}  // namespace bfly
+
+namespace bfly {
+
+// A part view of a full plan: the slice of every factor that middle nodes
+// [part m/P, (part+1) m/P) own, as pointer offsets into the
+// full plan's storage — no copies. Used to pipeline host transfers with compute.
+Plan part_view(const Plan& full, uint32_t part, uint32_t nparts) {
+  Plan v = full;
+  v.part = part;
+  v.nparts = nparts;
+  v.base = nullptr;
+  v.base_bytes = 0;
+  const uint64_t es = full.elem();
+  v.leaf_nb = full.leaf_nb / nparts;
+  v.dim_max = full.dim_max / nparts;
+  const uint64_t leaf_bytes = v.leaf_nb * full.leaf_n0 * full.rank * es;
+  v.u_leaf = static_cast<char*>(full.u_leaf) + part * leaf_bytes;
+  v.v_leaf = static_cast<char*>(full.v_leaf) + part * leaf_bytes;
+  for (uint32_t i = 0; i < full.nlev; ++i) {
+    v.lev[i].G = full.lev[i].G / nparts;
+    v.lev[i].nblocks = full.lev[i].nblocks / nparts;
+    const uint64_t lb = v.lev[i].nblocks * full.rank * full.branch * full.rank * es;
+    v.g_lev[i] = static_cast<char*>(full.g_lev[i]) + part * lb;
+    v.h_lev[i] = static_cast<char*>(full.h_lev[i]) + part * lb;
+  }
+  return v;
+}
+
+// Host-buffer apply with the transfers pipelined against compute (captured into
+// a graph by the caller): chunk c's H2D copy (stream cp) overlaps the down half
+// of chunk c-1 (stream run); the middle factor runs once on the full middle
+// vector; chunk e's D2H overlaps the up half of chunk e+1.
+int plan_apply_host_pipelined(const Plan& pl, const void* in_host, void* out_host, void* din, void* dout, void* mid,
+                              void* mid2, void* ws, uint32_t k, int adjoint, uint32_t chunks, cudaStream_t run,
+                              cudaStream_t cp, cudaEvent_t* ev) {
+  const uint64_t es = pl.elem();
+  const uint64_t rows_c = pl.n / chunks;
+  const uint64_t mid_rows_c = static_cast<uint64_t>(pl.m) * pl.m * pl.rank / chunks;
+  // ev[0]: fork; ev[1 .. chunks]: inputs landed; ev[chunks+1 .. 2 chunks]: outputs ready; ev[2 chunks+1]: join
+  BF_CUDA(cudaEventRecord(ev[0], run));
+  BF_CUDA(cudaStreamWaitEvent(cp, ev[0], 0));
+  for (uint32_t c = 0; c < chunks; ++c) {
+    const uint64_t off = c * rows_c * k * es;
+    BF_CUDA(cudaMemcpyAsync(static_cast<char*>(din) + off, static_cast<const char*>(in_host) + off, rows_c * k * es,
+                            cudaMemcpyHostToDevice, cp));
+    BF_CUDA(cudaEventRecord(ev[1 + c], cp));
+  }
+  for (uint32_t c = 0; c < chunks; ++c) {
+    BF_CUDA(cudaStreamWaitEvent(run, ev[1 + c], 0));
+    const Plan v = part_view(pl, c, chunks);
+    int rc = plan_apply_half(v, 0, static_cast<char*>(din) + c * rows_c * k * es,
+                             static_cast<char*>(mid) + c * mid_rows_c * k * es, k, adjoint, ws, run);
+    if (rc) return rc;
+  }
+  int rc = pl.dtype == BF_C128 ? launch_middle<double2>(pl, mid, mid2, k, adjoint, run)
+                               : launch_middle<float2>(pl, mid, mid2, k, adjoint, run);
+  if (rc) return rc;
+  for (uint32_t e = 0; e < chunks; ++e) {
+    const Plan v = part_view(pl, e, chunks);
+    const uint64_t off = e * rows_c * k * es;
+    rc = plan_apply_half(v, 1, static_cast<char*>(mid2) + e * mid_rows_c * k * es, static_cast<char*>(dout) + off, k,
+                         adjoint, ws, run);
+    if (rc) return rc;
+    BF_CUDA(cudaEventRecord(ev[1 + chunks + e], run));
+    BF_CUDA(cudaStreamWaitEvent(cp, ev[1 + chunks + e], 0));
+    BF_CUDA(cudaMemcpyAsync(static_cast<char*>(out_host) + off, static_cast<char*>(dout) + off, rows_c * k * es,
+                            cudaMemcpyDeviceToHost, cp));
+  }
+  BF_CUDA(cudaEventRecord(ev[1 + 2 * chunks], cp));
+  BF_CUDA(cudaStreamWaitEvent(run, ev[1 + 2 * chunks], 0));
+  return 0;
 }
 
 }  // namespace bfly

@@ -150,6 +150,11 @@ void bf_plan_destroy(bf_plan* plan) {
   if (!plan) return;
   DeviceGuard dg(plan->p.device);
   for (auto& gentry : plan->graphs) cudaGraphExecDestroy(gentry.exec);
+  if (plan->host_in) cudaFree(plan->host_in);
+  if (plan->host_out) cudaFree(plan->host_out);
+  if (plan->host_ws) cudaFree(plan->host_ws);
+  for (auto e : plan->pipe_events) cudaEventDestroy(e);
+  if (plan->copy_stream) cudaStreamDestroy(plan->copy_stream);
   if (plan->own_stream) cudaStreamDestroy(plan->own_stream);
   if (plan->p.base) cudaFree(plan->p.base);
   delete plan;
@@ -247,24 +252,13 @@ uint64_t bf_apply_workspace_bytes(const bf_plan* plan, uint32_t k) {
   return 2ull * plan->p.dim_max * (k ? k : 1) * plan->p.elem();
 }
 
-int bf_apply(const bf_plan* plan, const void* in, void* out, uint32_t k, int adjoint, void* workspace,
-             uint64_t workspace_bytes, void* stream) {
-  if (!plan) return fail(BF_EINVAL, "null plan");
+// The chain is a fixed sequence of 2 + 2(L-h) launches: replay it as one CUDA
+// graph per (buffers, k, direction, stream). A NULL stream is the legacy default
+// stream, which cannot be captured; the graph then runs on a plan-owned blocking
+// stream, which the legacy stream orders against implicitly. Caller holds gmu.
+static int apply_graph_locked(const bf_plan* plan, const void* in, void* out, uint32_t k, int adjoint,
+                              void* workspace, cudaStream_t st) {
   const Plan& p = plan->p;
-  if (!p.uploaded) return fail(BF_ESTATE, "plan has no factors (call bf_plan_upload)");
-  if (k < 1) return fail(BF_EINVAL, "need at least one right-hand side");
-  if (!in || !out) return fail(BF_EINVAL, "null input/output pointer");
-  if (!workspace || workspace_bytes < bf_apply_workspace_bytes(plan, k))
-    return fail(BF_EINVAL, "workspace too small (see bf_apply_workspace_bytes)");
-  if (p.nparts != 1) return fail(BF_EINVAL, "sharded plan: use bf_apply_down / bf_middle_pack / bf_apply_up");
-  DeviceGuard dg(p.device);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (!plan->graphs_enabled) return plan_apply(p, in, out, k, adjoint ? 1 : 0, workspace, st);
-  // The chain is a fixed sequence of 2 + 2(L-h) launches: replay it as one CUDA
-  // graph per (buffers, k, direction, stream). A NULL stream is the legacy default
-  // stream, which cannot be captured; the graph then runs on a plan-owned blocking
-  // stream, which the legacy stream orders against implicitly.
-  std::lock_guard<std::mutex> lock(plan->gmu);
   cudaStream_t run = st;
   if (!run) {
     if (!plan->own_stream) BF_CUDA(cudaStreamCreate(&plan->own_stream));
@@ -299,6 +293,23 @@ int bf_apply(const bf_plan* plan, const void* in, void* out, uint32_t k, int adj
   plan->graphs.push_back({in, out, workspace, k, adjoint, st, exec});
   BF_CUDA(cudaGraphLaunch(exec, run));
   return BF_OK;
+}
+
+int bf_apply(const bf_plan* plan, const void* in, void* out, uint32_t k, int adjoint, void* workspace,
+             uint64_t workspace_bytes, void* stream) {
+  if (!plan) return fail(BF_EINVAL, "null plan");
+  const Plan& p = plan->p;
+  if (!p.uploaded) return fail(BF_ESTATE, "plan has no factors (call bf_plan_upload)");
+  if (k < 1) return fail(BF_EINVAL, "need at least one right-hand side");
+  if (!in || !out) return fail(BF_EINVAL, "null input/output pointer");
+  if (!workspace || workspace_bytes < bf_apply_workspace_bytes(plan, k))
+    return fail(BF_EINVAL, "workspace too small (see bf_apply_workspace_bytes)");
+  if (p.nparts != 1) return fail(BF_EINVAL, "sharded plan: use bf_apply_down / bf_middle_pack / bf_apply_up");
+  DeviceGuard dg(p.device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!plan->graphs_enabled) return plan_apply(p, in, out, k, adjoint ? 1 : 0, workspace, st);
+  std::lock_guard<std::mutex> lock(plan->gmu);
+  return apply_graph_locked(plan, in, out, k, adjoint, workspace, st);
 }
 
 int bf_apply_down(const bf_plan* plan, const void* in, void* mid, uint32_t k, int adjoint, void* workspace,
@@ -420,24 +431,88 @@ int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t io = p.n * k * p.elem();
   const uint64_t wsb = bf_apply_workspace_bytes(plan, k);
-  void *din = nullptr, *dout = nullptr, *ws = nullptr;
-  BF_CUDA(cudaMallocAsync(&din, io, st));
-  BF_CUDA(cudaMallocAsync(&dout, io, st));
-  BF_CUDA(cudaMallocAsync(&ws, wsb, st));
-  int rc = 0;
-  cudaError_t e = cudaMemcpyAsync(din, in_host, io, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) rc = cuda_fail(e, "H2D input");
-  if (!rc) rc = plan_apply(p, din, dout, k, adjoint ? 1 : 0, ws, st);
-  if (!rc) {
-    e = cudaMemcpyAsync(out_host, dout, io, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) rc = cuda_fail(e, "D2H output");
+  // persistent device buffers (grown on demand) keep the pointers stable, so the chain
+  // replays from the graph cache; the plan mutex serialises host applies on one plan
+  std::lock_guard<std::mutex> lock(plan->gmu);
+  cudaStream_t run = st;
+  if (!run) {
+    if (!plan->own_stream) BF_CUDA(cudaStreamCreate(&plan->own_stream));
+    run = plan->own_stream;
   }
-  cudaFreeAsync(din, st);
-  cudaFreeAsync(dout, st);
-  cudaFreeAsync(ws, st);
-  e = cudaStreamSynchronize(st);
+  // large transfers: pipeline H2D/D2H chunks (per middle-node range) against the chain
+  const uint32_t chunks = p.m >= 8 ? 8 : 1;
+  // (graph capture of a memcpy needs page-locked host memory)
+  auto pinned = [](const void* ptr) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool pipelined =
+      plan->graphs_enabled && chunks > 1 && io >= (4ull << 20) && pinned(in_host) && pinned(out_host);
+  const uint64_t mid_bytes = static_cast<uint64_t>(p.m) * p.m * p.rank * k * p.elem();
+  const uint64_t need_ws = pipelined ? 2 * mid_bytes + 2 * (p.dim_max / chunks) * k * p.elem() : wsb;
+  if (plan->host_io_bytes < io || plan->host_ws_bytes < need_ws) {
+    BF_CUDA(cudaStreamSynchronize(run));
+    if (plan->host_in) cudaFree(plan->host_in);
+    if (plan->host_out) cudaFree(plan->host_out);
+    if (plan->host_ws) cudaFree(plan->host_ws);
+    plan->host_in = plan->host_out = plan->host_ws = nullptr;
+    plan->host_io_bytes = plan->host_ws_bytes = 0;
+    BF_CUDA(cudaMalloc(&plan->host_in, io));
+    BF_CUDA(cudaMalloc(&plan->host_out, io));
+    BF_CUDA(cudaMalloc(&plan->host_ws, need_ws));
+    plan->host_io_bytes = io;
+    plan->host_ws_bytes = need_ws;
+  }
+  if (pipelined) {
+    if (!plan->copy_stream) BF_CUDA(cudaStreamCreateWithFlags(&plan->copy_stream, cudaStreamNonBlocking));
+    if (plan->pipe_events.empty()) {
+      plan->pipe_events.assign(2 * chunks + 2, nullptr);
+      for (auto& e : plan->pipe_events) BF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    void* const key_ws = reinterpret_cast<void*>(static_cast<uintptr_t>(1));  // marks the pipelined graph
+    for (const auto& gentry : plan->graphs)
+      if (gentry.in == in_host && gentry.out == out_host && gentry.ws == key_ws && gentry.k == k &&
+          gentry.adjoint == adjoint && gentry.stream == run) {
+        BF_CUDA(cudaGraphLaunch(gentry.exec, run));
+        BF_CUDA(cudaStreamSynchronize(run));
+        return BF_OK;
+      }
+    char* w = static_cast<char*>(plan->host_ws);
+    BF_CUDA(cudaStreamBeginCapture(run, cudaStreamCaptureModeThreadLocal));
+    const int rc = plan_apply_host_pipelined(p, in_host, out_host, plan->host_in, plan->host_out, w, w + mid_bytes,
+                                             w + 2 * mid_bytes, k, adjoint ? 1 : 0, chunks, run, plan->copy_stream,
+                                             plan->pipe_events.data());
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(run, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture (host pipeline)");
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) return cuda_fail(ei, "cudaGraphInstantiate (host pipeline)");
+    if (plan->graphs.size() >= 16) {
+      cudaGraphExecDestroy(plan->graphs.front().exec);
+      plan->graphs.erase(plan->graphs.begin());
+    }
+    plan->graphs.push_back({in_host, out_host, key_ws, k, adjoint ? 1 : 0, run, exec});
+    BF_CUDA(cudaGraphLaunch(exec, run));
+    BF_CUDA(cudaStreamSynchronize(run));
+    return BF_OK;
+  }
+  BF_CUDA(cudaMemcpyAsync(plan->host_in, in_host, io, cudaMemcpyHostToDevice, run));
+  int rc = plan->graphs_enabled
+               ? apply_graph_locked(plan, plan->host_in, plan->host_out, k, adjoint ? 1 : 0, plan->host_ws, run)
+               : plan_apply(p, plan->host_in, plan->host_out, k, adjoint ? 1 : 0, plan->host_ws, run);
   if (rc) return rc;
-  if (e != cudaSuccess) return cuda_fail(e, "bf_apply_host");
+  BF_CUDA(cudaMemcpyAsync(out_host, plan->host_out, io, cudaMemcpyDeviceToHost, run));
+  BF_CUDA(cudaStreamSynchronize(run));
   return BF_OK;
 }
 

@@ -65,6 +65,10 @@ int plan_apply_half(const Plan& pl, int up, const void* in, void* out, uint32_t 
                     cudaStream_t st);
 int plan_middle_exchange(const Plan& pl, int unpack, const void* in, void* out, uint32_t k, int adjoint,
                          cudaStream_t st);
+Plan part_view(const Plan& full, uint32_t part, uint32_t nparts);
+int plan_apply_host_pipelined(const Plan& pl, const void* in_host, void* out_host, void* din, void* dout, void* mid,
+                              void* mid2, void* ws, uint32_t k, int adjoint, uint32_t chunks, cudaStream_t run,
+                              cudaStream_t cp, cudaEvent_t* ev);
 int plan_apply_factor(const Plan& pl, int which, int lvl_idx, int adjoint, const void* in, void* out, uint32_t k,
                       cudaStream_t st);
 int entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr, const int64_t* cols, uint32_t nc, void* out,
@@ -93,6 +97,13 @@ struct bf_plan {
   mutable std::mutex gmu;
   mutable std::vector<GraphEntry> graphs;
   mutable cudaStream_t own_stream = nullptr;
+  // bf_apply_host device buffers
+  mutable void* host_in = nullptr;
+  mutable void* host_out = nullptr;
+  mutable void* host_ws = nullptr;
+  mutable uint64_t host_io_bytes = 0, host_ws_bytes = 0;
+  mutable cudaStream_t copy_stream = nullptr;      // host pipeline transfers
+  mutable std::vector<cudaEvent_t> pipe_events;
 };
 
 struct bf_timer {
