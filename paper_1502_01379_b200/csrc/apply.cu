@@ -6,6 +6,7 @@
 //   adjoint:  U^L*  -> G^{L-1}* .. G^{h}*  -> M* -> H^{h} .. H^{L-1} -> V^L
 // with M (or M*) fused into the epilogue of the last adjoint-direction level.
 #include <algorithm>
+#include <cstdlib>
 
 #include "level_kernel.cuh"
 #include "plan.h"
@@ -32,6 +33,14 @@ __global__ void middle_kernel(const E* __restrict__ in, E* __restrict__ out,
     const E v = in[src * k + kk];
     out[x] = Cx<E>::make(w * v.x, w * v.y);
   }
+}
+
+bool dmma_disabled() {
+  static const bool off = [] {
+    const char* v = std::getenv("BF_NO_DMMA");
+    return v && v[0] && v[0] != '0';
+  }();
+  return off;
 }
 
 uint32_t ilog2(uint64_t x) {
@@ -133,6 +142,7 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   // every bulk copy must move a multiple of 16 bytes between 16-byte aligned addresses:
   // complex128 always does; complex64 needs even block sizes and, when a row is split
   // into k-tiles, even k and kt.
+  a.use_dmma = mrhs && esz == 16 && kt >= 16 && !dmma_disabled();
   a.bulk = aligned && (esz == 16 || (R % 2 == 0 && C % 2 == 0 && (a.ktiles == 1 || (k % 2 == 0 && kt % 2 == 0))));
   const size_t smem = 128 + static_cast<size_t>(sh.stages) * a.stage_elems * esz;
   if (smem > 227 * 1024) return fail(BF_EINVAL, "rank too large: one block pair exceeds the shared-memory stage");

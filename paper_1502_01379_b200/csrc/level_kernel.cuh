@@ -28,6 +28,8 @@
 // order when lanes walk rows of a block) — and store straight to global.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace bfly {
@@ -52,6 +54,7 @@ struct LevelArgs {
   int remap;          // 0 none, 1 middle forward, 2 middle adjoint
   uint32_t m, r;      // middle geometry (remap)
   int bulk;           // 1: 16-byte aligned, use the TMA bulk engine
+  int use_dmma;       // many-RHS complex128: FP64 tensor-core (mma.sync f64) consumer
 };
 
 struct TileGeo {
@@ -386,10 +389,157 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, uint32_t t
   }
 }
 
+// ---------------------------------------------------------------- FP64 tensor cores
+// mma.sync m8n8k4 f64 (DMMA): A fragment A[lane/4][lane%4], B fragment
+// B[lane%4][lane/4], C/D fragment C[lane/4][2(lane%4) + q] (layout confirmed on
+// B200 by tools/dmma_layout.cu).
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Many-RHS consumer on the FP64 tensor pipe (complex128). Each unit is the
+// complex GEMM of consume_tile_mrhs, split into 4 real DMMAs per k-step
+// (re += Ar Xr - Ai Xi, im += Ar Xi + Ai Xr); a warp owns MT x NT 8x8 tiles.
+template <int MT, int NT>
+__device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, uint32_t tile, const double2* st, int warp,
+                                                  int lane, int nwarps) {
+  const TileGeo t = tile_geo(a, tile);
+  const uint32_t blk = a.R * a.C;
+  const uint32_t U = 1u << a.lgU;
+  const uint32_t Pe_mask = (1u << t.lgPe) - 1;
+  const double2* fs = st;
+  const double2* vs = st + static_cast<size_t>(a.nt) * U * blk;
+  double2* out = static_cast<double2*>(a.out);
+  const uint32_t kc = t.kc;
+  const uint32_t P_mask = (1u << a.lgP) - 1;
+  const uint32_t m_out = a.adjoint ? a.C : a.nt * a.R;
+  const uint32_t kdim = a.adjoint ? a.nt * a.R : a.C;
+  const uint32_t nmt = (m_out + MT * 8 - 1) / (MT * 8), nnt = (kc + NT * 8 - 1) / (NT * 8);
+  const uint32_t items = U * nmt * nnt;
+  const uint32_t lr = lane >> 2, lk = lane & 3;
+  for (uint32_t it = warp; it < items; it += nwarps) {
+    const uint32_t ntile = it % nnt;
+    const uint32_t rest = it / nnt;
+    const uint32_t mt = rest % nmt, ul = rest / nmt;
+    const uint32_t m0 = mt * MT * 8, n0 = ntile * NT * 8;
+    const uint32_t base = (((ul >> t.lgPe) * a.nt) << t.lgPe) + (ul & Pe_mask);
+    double cr[MT][NT][2], ci[MT][NT][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0;
+    // forward: the A rows this lane reads are fixed (m = m0 + 8i + lane/4)
+    uint32_t arow[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const uint32_t m = min(m0 + 8 * i + lr, m_out - 1);
+      const uint32_t tt = m / a.R, rho = m - tt * a.R;
+      arow[i] = (base + (tt << t.lgPe)) * a.R + rho;
+    }
+    for (uint32_t k0 = 0; k0 < kdim; k0 += 4) {
+      const uint32_t kk = k0 + lk;
+      const bool kok = kk < kdim;
+      // adjoint: the k index runs over block rows j = (t, rho)
+      uint32_t jrow = 0;
+      if (a.adjoint) {
+        const uint32_t kj = kok ? kk : 0;
+        const uint32_t tt = kj / a.R, rho = kj - tt * a.R;
+        jrow = (base + (tt << t.lgPe)) * a.R + rho;
+      }
+      double ar[MT], ai[MT], nai[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const uint32_t m = m0 + 8 * i + lr;
+        double2 v = make_double2(0, 0);
+        if (kok && m < m_out) {
+          if (!a.adjoint) {
+            v = fs[static_cast<size_t>(arow[i]) * a.C + kk];
+          } else {
+            v = fs[static_cast<size_t>(jrow) * a.C + m];
+            v.y = -v.y;  // A^H
+          }
+        }
+        ar[i] = v.x;
+        ai[i] = v.y;
+        nai[i] = -v.y;
+      }
+      double br[NT], bi[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const uint32_t n = n0 + 8 * j + lr;
+        double2 v = make_double2(0, 0);
+        if (kok && n < kc) {
+          const size_t row = a.adjoint ? jrow : static_cast<size_t>(ul) * a.C + kk;
+          v = vs[row * kc + n];
+        }
+        br[j] = v.x;
+        bi[j] = v.y;
+      }
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          dmma(cr[i][j][0], cr[i][j][1], ar[i], br[j]);
+          dmma(cr[i][j][0], cr[i][j][1], nai[i], bi[j]);
+          dmma(ci[i][j][0], ci[i][j][1], ar[i], bi[j]);
+          dmma(ci[i][j][0], ci[i][j][1], ai[i], br[j]);
+        }
+    }
+    // epilogue: element (m0 + 8i + lane/4, n0 + 8j + 2(lane%4) + q)
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const uint32_t m = m0 + 8 * i + lr;
+      if (m >= m_out) continue;
+      size_t rowbase;
+      double w = 1;
+      if (!a.adjoint) {
+        const uint32_t u = t.u0 + ul;
+        const uint32_t tt = m / a.R, rho = m - tt * a.R;
+        const uint32_t q = ((((u >> a.lgP) * a.ntot) + a.t0 + tt) << a.lgP) + (u & P_mask);
+        rowbase = (static_cast<size_t>(q) * a.R + rho) * a.k + t.k0;
+      } else {
+        size_t e = static_cast<size_t>(t.u0 + ul) * a.C + m;
+        if (a.remap != 0) {
+          const uint32_t mr = a.m * a.r;
+          const uint32_t e32 = static_cast<uint32_t>(e), ia = e32 / mr;
+          const uint32_t rem = e32 - ia * mr;
+          const uint32_t ib = rem / a.r, rho = rem - ib * a.r;
+          const size_t dst = (static_cast<size_t>(ib) * a.m + ia) * a.r + rho;
+          const double* W = static_cast<const double*>(a.mid_w);
+          w = a.remap == 1 ? W[dst] : W[(static_cast<size_t>(ia) * a.m + ib) * a.r + rho];
+          e = dst;
+        }
+        rowbase = e * a.k + t.k0;
+      }
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const uint32_t n = n0 + 8 * j + 2 * lk + q;
+          if (n >= kc) continue;
+          const double2 v = make_double2(w * cr[i][j][q], w * ci[i][j][q]);
+          double2& o = out[rowbase + n];
+          o = (a.adjoint && a.accumulate) ? make_double2(o.x + v.x, o.y + v.y) : v;
+        }
+    }
+  }
+}
+
 // Register-tile shapes of the many-RHS consumer, picked by right-hand sides per tile.
 template <typename E>
 __device__ __forceinline__ void consume_tile_mrhs_any(const LevelArgs& a, uint32_t tile, const E* st, int warp,
                                                       int lane, int nwarps) {
+  if constexpr (std::is_same<E, double2>::value) {
+    if (a.use_dmma) {  // complex128: the FP64 tensor pipe
+      if (a.kt >= 32)
+        consume_tile_dmma<2, 4>(a, tile, st, warp, lane, nwarps);
+      else
+        consume_tile_dmma<2, 2>(a, tile, st, warp, lane, nwarps);
+      return;
+    }
+  }
   if (a.kt >= 128)
     consume_tile_mrhs<E, 4, 4, 32>(a, tile, st, warp, lane, nwarps);
   else if (a.kt >= 64)
