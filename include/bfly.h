@@ -141,6 +141,15 @@ int bf_plan_create_tree(bf_plan** out, uint64_t n, uint32_t levels, uint32_t ran
                         int dtype, int device, uint32_t part, uint32_t nparts);
 int bf_apply_down(const bf_plan* plan, const void* in, void* mid, uint32_t k, int adjoint,
                   void* workspace, uint64_t workspace_bytes, void* stream);
+/* Fused variant of bf_apply_down + bf_middle_pack + all-to-all: the last
+ * level's epilogue applies the middle weights and stores every output straight
+ * into the receive buffer of the part that owns it — peers[d] is part d's
+ * receive buffer (P, (m/P)^2 r, k), mapped into this process (CUDA IPC /
+ * symmetric memory over NVLink; plain device buffers when the parts share one
+ * GPU). After every part's push has completed (a cross-part barrier), each part
+ * runs bf_middle_unpack on its own receive buffer. */
+int bf_apply_down_push(const bf_plan* plan, const void* in, void* const* peers, uint32_t k, int adjoint,
+                       void* workspace, uint64_t workspace_bytes, void* stream);
 int bf_middle_pack(const bf_plan* plan, const void* mid, void* send, uint32_t k, int adjoint, void* stream);
 int bf_middle_unpack(const bf_plan* plan, const void* recv, void* mid, uint32_t k, int adjoint, void* stream);
 int bf_apply_up(const bf_plan* plan, const void* mid, void* out, uint32_t k, int adjoint,

@@ -44,6 +44,7 @@ SIGNATURES = [
     ("bf_plan_create_sharded", _I, [ctypes.POINTER(_P), _U64, _U32, _U32, _I, _I, _U32, _U32]),
     ("bf_plan_create_tree", _I, [ctypes.POINTER(_P), _U64, _U32, _U32, _U32, _I, _I, _U32, _U32]),
     ("bf_apply_down", _I, [_P, _P, _P, _U32, _I, _P, _U64, _P]),
+    ("bf_apply_down_push", _I, [_P, _P, ctypes.POINTER(_P), _U32, _I, _P, _U64, _P]),
     ("bf_middle_pack", _I, [_P, _P, _P, _U32, _I, _P]),
     ("bf_middle_unpack", _I, [_P, _P, _P, _U32, _I, _P]),
     ("bf_apply_up", _I, [_P, _P, _P, _U32, _I, _P, _U64, _P]),

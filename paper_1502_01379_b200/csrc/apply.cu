@@ -62,7 +62,7 @@ constexpr uint32_t kMrhsMinK = 8;
 template <typename E>
 int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint32_t ntot, uint32_t t0,
                    int accumulate, uint64_t P, uint64_t units, const void* in, void* out, uint32_t k, int adjoint,
-                   int remap, cudaStream_t st);
+                   int remap, cudaStream_t st, void* const* peers);
 
 // One factor launch. A unit's nt blocks normally share one tile; when they do
 // not fit a shared-memory stage (quadtree rank 25: 4 x 25 x 100 complex128 =
@@ -70,16 +70,17 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
 // are disjoint per t, adjoint partial sums accumulate into the output.
 template <typename E>
 int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint64_t P, uint64_t units,
-                 const void* in, void* out, uint32_t k, int adjoint, int remap, cudaStream_t st) {
+                 const void* in, void* out, uint32_t k, int adjoint, int remap, cudaStream_t st,
+                 void* const* peers = nullptr) {
   const Shape sh = k >= kMrhsMinK ? kMrhs : kStream;
   uint32_t nt_tile = nt;
   auto tile_elems = [&](uint64_t t) { return t * R * C + (adjoint ? t * R : static_cast<uint64_t>(C)); };
   while (nt_tile > 1 && tile_elems(nt_tile) * sizeof(E) > sh.stage_bytes) nt_tile /= 2;
   if (nt_tile == nt)
-    return launch_level_t<E>(pl, fac, R, C, nt, nt, 0, 0, P, units, in, out, k, adjoint, remap, st);
+    return launch_level_t<E>(pl, fac, R, C, nt, nt, 0, 0, P, units, in, out, k, adjoint, remap, st, peers);
   for (uint32_t t0 = 0; t0 < nt; t0 += nt_tile) {
     const int rc = launch_level_t<E>(pl, fac, R, C, nt_tile, nt, t0, adjoint && t0 > 0, P, units, in, out, k,
-                                     adjoint, remap, st);
+                                     adjoint, remap, st, peers);
     if (rc) return rc;
   }
   return 0;
@@ -88,7 +89,7 @@ int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32
 template <typename E>
 int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint32_t ntot, uint32_t t0,
                    int accumulate, uint64_t P, uint64_t units, const void* in, void* out, uint32_t k, int adjoint,
-                   int remap, cudaStream_t st) {
+                   int remap, cudaStream_t st, void* const* peers) {
   if (units >= (1ull << 31)) return fail(BF_EINVAL, "level has too many blocks for one launch");
   if (remap && static_cast<uint64_t>(pl.m) * pl.m * pl.rank >= (1ull << 32))
     return fail(BF_EINVAL, "middle vector too long for 32-bit remap indices");
@@ -112,6 +113,12 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   a.remap = remap;
   a.m = pl.m;
   a.r = pl.rank;
+  a.part = pl.part;
+  a.mp = pl.m / pl.nparts;
+  if (remap >= 3) {
+    if (!peers || pl.nparts > 8) return fail(BF_EINVAL, "peer push needs <= 8 receive buffers");
+    for (uint32_t d = 0; d < pl.nparts; ++d) a.peers[d] = peers[d];
+  }
   const uint64_t esz = sizeof(E);
   const uint64_t fac_unit = static_cast<uint64_t>(nt) * R * C;
   const uint64_t vec_col = adjoint ? static_cast<uint64_t>(nt) * R : C;  // vector elems per unit per rhs
@@ -174,7 +181,7 @@ namespace {
 // One factor op, dispatched by kind. `lvl_idx` indexes the plan's level table.
 template <typename E>
 int factor_op(const Plan& pl, int which, int lvl_idx, int adjoint, const void* in, void* out, uint32_t k, int remap,
-              cudaStream_t st) {
+              cudaStream_t st, void* const* peers = nullptr) {
   if (which == BF_FACTOR_V || which == BF_FACTOR_U) {
     const void* fac = which == BF_FACTOR_V ? pl.v_leaf : pl.u_leaf;
     return launch_level<E>(pl, fac, pl.leaf_n0, pl.rank, 1, 1, pl.leaf_nb, in, out, k, adjoint, 0, st);
@@ -183,14 +190,14 @@ int factor_op(const Plan& pl, int which, int lvl_idx, int adjoint, const void* i
   const LevelGeo& lg = pl.lev[lvl_idx];
   const void* fac = which == BF_FACTOR_G ? pl.g_lev[lvl_idx] : pl.h_lev[lvl_idx];
   return launch_level<E>(pl, fac, pl.rank, pl.branch * pl.rank, lg.splits ? pl.branch : 1, lg.P, lg.G * lg.P, in, out,
-                         k, adjoint, remap, st);
+                         k, adjoint, remap, st, peers);
 }
 
 template <typename E>
 int timed_op(LaunchRecorder* rec, const Plan& pl, int which, int lvl_idx, int adjoint, const void* in, void* out,
-             uint32_t k, int remap, cudaStream_t st) {
+             uint32_t k, int remap, cudaStream_t st, void* const* peers = nullptr) {
   int rc = rec ? rec->before(st) : 0;
-  if (!rc) rc = factor_op<E>(pl, which, lvl_idx, adjoint, in, out, k, remap, st);
+  if (!rc) rc = factor_op<E>(pl, which, lvl_idx, adjoint, in, out, k, remap, st, peers);
   if (!rc && rec) rc = rec->after(st);
   return rc;
 }
@@ -201,7 +208,7 @@ int timed_op(LaunchRecorder* rec, const Plan& pl, int which, int lvl_idx, int ad
 // in whichever ping-pong buffer the alternation reaches (returned in *result).
 template <typename E>
 int run_down(const Plan& pl, const void* in, E* bufs[2], void* final_dst, uint32_t k, int adjoint, int remap,
-             cudaStream_t st, LaunchRecorder* rec, const void** result) {
+             cudaStream_t st, LaunchRecorder* rec, const void** result, void* const* peers = nullptr) {
   const int nl = static_cast<int>(pl.nlev);
   const int lead = adjoint ? BF_FACTOR_U : BF_FACTOR_V;
   const int down = adjoint ? BF_FACTOR_G : BF_FACTOR_H;
@@ -210,7 +217,7 @@ int run_down(const Plan& pl, const void* in, E* bufs[2], void* final_dst, uint32
   if (rc) return rc;
   for (int i = nl - 1; i >= 0; --i) {
     void* dst = (i == 0 && final_dst) ? final_dst : bufs[cur ^ 1];
-    rc = timed_op<E>(rec, pl, down, i, 1, bufs[cur], dst, k, i == 0 ? remap : 0, st);
+    rc = timed_op<E>(rec, pl, down, i, 1, bufs[cur], dst, k, i == 0 ? remap : 0, st, i == 0 ? peers : nullptr);
     if (rc) return rc;
     if (dst == bufs[cur ^ 1]) cur ^= 1;
   }
@@ -314,6 +321,21 @@ int plan_apply_half(const Plan& pl, int up, const void* in, void* out, uint32_t 
   float2* bufs[2] = {static_cast<float2*>(ws), static_cast<float2*>(ws) + dk};
   return up ? run_up<float2>(pl, in, bufs, out, k, adjoint, st, nullptr)
             : run_down<float2>(pl, in, bufs, out, k, adjoint, 0, st, nullptr, &res);
+}
+
+// Sharded down half whose last level stores its outputs, middle weights
+// applied, straight into every part's receive buffer (remap 3/4).
+int plan_apply_down_push(const Plan& pl, const void* in, void* const* peers, uint32_t k, int adjoint, void* ws,
+                         cudaStream_t st) {
+  const uint64_t dk = pl.dim_max * k;
+  const void* res = nullptr;
+  const int remap = adjoint ? 4 : 3;
+  if (pl.dtype == BF_C128) {
+    double2* bufs[2] = {static_cast<double2*>(ws), static_cast<double2*>(ws) + dk};
+    return run_down<double2>(pl, in, bufs, nullptr, k, adjoint, remap, st, nullptr, &res, peers);
+  }
+  float2* bufs[2] = {static_cast<float2*>(ws), static_cast<float2*>(ws) + dk};
+  return run_down<float2>(pl, in, bufs, nullptr, k, adjoint, remap, st, nullptr, &res, peers);
 }
 
 int plan_middle_exchange(const Plan& pl, int unpack, const void* in, void* out, uint32_t k, int adjoint,

@@ -336,6 +336,20 @@ int bf_apply_up(const bf_plan* plan, const void* mid, void* out, uint32_t k, int
   return plan_apply_half(p, 1, mid, out, k, adjoint ? 1 : 0, workspace, static_cast<cudaStream_t>(stream));
 }
 
+int bf_apply_down_push(const bf_plan* plan, const void* in, void* const* peers, uint32_t k, int adjoint,
+                       void* workspace, uint64_t workspace_bytes, void* stream) {
+  if (!plan) return fail(BF_EINVAL, "null plan");
+  const Plan& p = plan->p;
+  if (!p.uploaded) return fail(BF_ESTATE, "plan has no factors (call bf_plan_upload)");
+  if (k < 1 || !in || !peers) return fail(BF_EINVAL, "bad k or null pointer");
+  for (uint32_t d = 0; d < p.nparts; ++d)
+    if (!peers[d]) return fail(BF_EINVAL, "null peer receive buffer");
+  if (!workspace || workspace_bytes < bf_apply_workspace_bytes(plan, k))
+    return fail(BF_EINVAL, "workspace too small (see bf_apply_workspace_bytes)");
+  DeviceGuard dg(p.device);
+  return plan_apply_down_push(p, in, peers, k, adjoint ? 1 : 0, workspace, static_cast<cudaStream_t>(stream));
+}
+
 int bf_middle_pack(const bf_plan* plan, const void* mid, void* send, uint32_t k, int adjoint, void* stream) {
   if (!plan) return fail(BF_EINVAL, "null plan");
   const Plan& p = plan->p;

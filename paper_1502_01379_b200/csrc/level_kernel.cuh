@@ -51,11 +51,46 @@ struct LevelArgs {
   uint32_t ntiles;    // (units / U) * ktiles
   uint32_t stage_elems;
   int adjoint;
-  int remap;          // 0 none, 1 middle forward, 2 middle adjoint
+  int remap;          // 0 none, 1 middle forward, 2 middle adjoint, 3/4 the same pushed to peers
   uint32_t m, r;      // middle geometry (remap)
+  uint32_t part, mp;  // remap 3/4: this part and middle nodes per part
+  void* peers[8];     // remap 3/4: receive buffers of every part, [sender][own][other local][rho][k]
   int bulk;           // 1: 16-byte aligned, use the TMA bulk engine
   int use_dmma;       // many-RHS complex128: FP64 tensor-core (mma.sync f64) consumer
 };
+
+
+// Destination row (the element for right-hand side 0) and middle weight of
+// output e of the last adjoint-direction level. remap 1/2 fuse the middle
+// factor (factors.py:180-190): e = (a, b, rho) -> (b, a, rho), weight W[b,a] /
+// W[a,b]. remap 3/4 do the same for one part of a sharded chain and store
+// straight into the owning part's receive buffer (peer memory over NVLink on a
+// multi-GPU box): a = own local node, b = global other node, receiver part
+// b / mp, slot [sender][own][b mod mp][rho] — the layout bf_middle_pack + an
+// all-to-all would produce, with no pack kernel and no collective.
+template <typename E>
+__device__ __forceinline__ E* remap_row(const LevelArgs& a, size_t e, typename Cx<E>::R* w) {
+  using Rl = typename Cx<E>::R;
+  E* out = static_cast<E*>(a.out);
+  if (a.remap == 0) {
+    *w = 1;
+    return out + e * a.k;
+  }
+  const Rl* W = static_cast<const Rl*>(a.mid_w);
+  const uint32_t mr = a.m * a.r;
+  const uint32_t e32 = static_cast<uint32_t>(e), ia = e32 / mr;
+  const uint32_t rem = e32 - ia * mr;
+  const uint32_t ib = rem / a.r, rho = rem - ib * a.r;
+  if (a.remap <= 2) {
+    const size_t dst = (static_cast<size_t>(ib) * a.m + ia) * a.r + rho;
+    *w = a.remap == 1 ? __ldg(W + dst) : __ldg(W + (static_cast<size_t>(ia) * a.m + ib) * a.r + rho);
+    return out + dst * a.k;
+  }
+  const uint32_t own = a.part * a.mp + ia, d = ib / a.mp, bl = ib - d * a.mp;
+  *w = a.remap == 3 ? __ldg(W + (static_cast<size_t>(ib) * a.m + own) * a.r + rho)
+                    : __ldg(W + (static_cast<size_t>(own) * a.m + ib) * a.r + rho);
+  return static_cast<E*>(a.peers[d]) + ((static_cast<size_t>(own) * a.mp + bl) * a.r + rho) * a.k;
+}
 
 struct TileGeo {
   uint32_t u0;        // first unit
@@ -227,17 +262,8 @@ __device__ __forceinline__ void consume_tile(const LevelArgs& a, uint32_t tile, 
       const uint32_t ul = rest / a.C;
       // destination (and, with the fused middle factor, its weight) first: the weight's
       // global load then overlaps the dot product instead of trailing it
-      size_t dst = static_cast<size_t>(t.u0 + ul) * a.C + c;
-      Rl w = 1;
-      if (a.remap != 0) {
-        const uint32_t mr = a.m * a.r;
-        const uint32_t e32 = static_cast<uint32_t>(dst), ia = e32 / mr;
-        const uint32_t rem = e32 - ia * mr;
-        const uint32_t ib = rem / a.r, rho = rem - ib * a.r;
-        dst = (static_cast<size_t>(ib) * a.m + ia) * a.r + rho;
-        const Rl* W = static_cast<const Rl*>(a.mid_w);
-        w = a.remap == 1 ? __ldg(W + dst) : __ldg(W + (static_cast<size_t>(ia) * a.m + ib) * a.r + rho);
-      }
+      Rl w;
+      E* orow = remap_row<E>(a, static_cast<size_t>(t.u0 + ul) * a.C + c, &w);
       const uint32_t base = (((ul >> t.lgPe) * a.nt) << t.lgPe) + (ul & Pe_mask);
       Acc8<E> acc;
       for (uint32_t tt = 0; tt < a.nt; ++tt) {
@@ -252,7 +278,7 @@ __device__ __forceinline__ void consume_tile(const LevelArgs& a, uint32_t tile, 
         if (rho < a.R) acc.mac(0, acol[static_cast<size_t>(rho) * a.C], y[static_cast<size_t>(rho) * kc]);
       }
       const E v = acc.sum_conj();
-      E& o_ = out[dst * a.k + t.k0 + kk];
+      E& o_ = orow[t.k0 + kk];
       o_ = a.accumulate ? Cx<E>::make(o_.x + w * v.x, o_.y + w * v.y) : Cx<E>::make(w * v.x, w * v.y);
     }
   }
@@ -365,19 +391,8 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, uint32_t t
       for (int i = 0; i < TM; ++i) {
         const uint32_t c = rb + LR * i;
         if (c >= m_out) break;
-        size_t e = static_cast<size_t>(t.u0 + ul) * a.C + c;
-        Rl w = 1;
-        if (a.remap != 0) {
-          const uint32_t mr = a.m * a.r;
-          const uint32_t e32 = static_cast<uint32_t>(e), ia = e32 / mr;
-          const uint32_t rem = e32 - ia * mr;
-          const uint32_t ib = rem / a.r, rho = rem - ib * a.r;
-          const size_t dst = (static_cast<size_t>(ib) * a.m + ia) * a.r + rho;
-          const Rl* W = static_cast<const Rl*>(a.mid_w);
-          w = a.remap == 1 ? W[dst] : W[(static_cast<size_t>(ia) * a.m + ib) * a.r + rho];
-          e = dst;
-        }
-        E* dst = out + e * a.k + t.k0 + col0;
+        Rl w;
+        E* dst = remap_row<E>(a, static_cast<size_t>(t.u0 + ul) * a.C + c, &w) + t.k0 + col0;
 #pragma unroll
         for (int j = 0; j < TN; ++j)
           if (colok[j]) {
@@ -492,26 +507,15 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, uint32_t t
     for (int i = 0; i < MT; ++i) {
       const uint32_t m = m0 + 8 * i + lr;
       if (m >= m_out) continue;
-      size_t rowbase;
+      double2* orow;
       double w = 1;
       if (!a.adjoint) {
         const uint32_t u = t.u0 + ul;
         const uint32_t tt = m / a.R, rho = m - tt * a.R;
         const uint32_t q = ((((u >> a.lgP) * a.ntot) + a.t0 + tt) << a.lgP) + (u & P_mask);
-        rowbase = (static_cast<size_t>(q) * a.R + rho) * a.k + t.k0;
+        orow = out + (static_cast<size_t>(q) * a.R + rho) * a.k + t.k0;
       } else {
-        size_t e = static_cast<size_t>(t.u0 + ul) * a.C + m;
-        if (a.remap != 0) {
-          const uint32_t mr = a.m * a.r;
-          const uint32_t e32 = static_cast<uint32_t>(e), ia = e32 / mr;
-          const uint32_t rem = e32 - ia * mr;
-          const uint32_t ib = rem / a.r, rho = rem - ib * a.r;
-          const size_t dst = (static_cast<size_t>(ib) * a.m + ia) * a.r + rho;
-          const double* W = static_cast<const double*>(a.mid_w);
-          w = a.remap == 1 ? W[dst] : W[(static_cast<size_t>(ia) * a.m + ib) * a.r + rho];
-          e = dst;
-        }
-        rowbase = e * a.k + t.k0;
+        orow = remap_row<double2>(a, static_cast<size_t>(t.u0 + ul) * a.C + m, &w) + t.k0;
       }
 #pragma unroll
       for (int j = 0; j < NT; ++j)
@@ -520,7 +524,7 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, uint32_t t
           const uint32_t n = n0 + 8 * j + 2 * lk + q;
           if (n >= kc) continue;
           const double2 v = make_double2(w * cr[i][j][q], w * ci[i][j][q]);
-          double2& o = out[rowbase + n];
+          double2& o = orow[n];
           o = (a.adjoint && a.accumulate) ? make_double2(o.x + v.x, o.y + v.y) : v;
         }
     }

@@ -63,6 +63,8 @@ int plan_apply(const Plan& pl, const void* in, void* out, uint32_t k, int adjoin
                LaunchRecorder* rec = nullptr);
 int plan_apply_half(const Plan& pl, int up, const void* in, void* out, uint32_t k, int adjoint, void* ws,
                     cudaStream_t st);
+int plan_apply_down_push(const Plan& pl, const void* in, void* const* peers, uint32_t k, int adjoint, void* ws,
+                         cudaStream_t st);
 int plan_middle_exchange(const Plan& pl, int unpack, const void* in, void* out, uint32_t k, int adjoint,
                          cudaStream_t st);
 Plan part_view(const Plan& full, uint32_t part, uint32_t nparts);

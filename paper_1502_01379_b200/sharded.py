@@ -177,3 +177,57 @@ class ShardedPlan(ShardedApply):
         _lib.check(self.lib.bf_apply_up(self._h, ctypes.c_void_p(mid.data_ptr()), ctypes.c_void_p(out.data_ptr()), k,
                                         int(adjoint), ctypes.c_void_p(ws.data_ptr()), wsb, self._stream()))
         return out
+
+
+def _push_methods():
+    """Attach the fused down+exchange step to ShardedPlan (kept separate for readability)."""
+
+    def down_push(self, x, adjoint, peers):
+        """Down half whose last level stores (weights applied) straight into every part's
+        receive buffer: peers[d] = device address of part d's receive buffer."""
+        import torch
+        x = x.reshape(self.n_local, -1).to(self.tdt).contiguous()
+        k = x.shape[1]
+        ws, wsb = self._ws(k)
+        arr = (ctypes.c_void_p * self.nparts)(*[int(p_) for p_ in peers])
+        _lib.check(self.lib.bf_apply_down_push(self._h, ctypes.c_void_p(x.data_ptr()), arr, k, int(adjoint),
+                                               ctypes.c_void_p(ws.data_ptr()), wsb, self._stream()),
+                   "bf_apply_down_push")
+        del torch
+
+    def push_buffer(self, k):
+        """Symmetric receive buffer (nparts * chunk_rows, k) shared over NVLink, cached per k."""
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        cache = self.__dict__.setdefault("_push_cache", {})
+        if k not in cache:
+            rows = self.nparts * self.chunk_rows
+            width = 2 if self.tdt == torch.complex128 else 1  # complex128 as pairs of float64
+            buf = symm.empty((rows * k * width,), dtype=torch.float64 if width == 2 else torch.complex64,
+                             device=f"cuda:{self.device}")
+            group = self.group if self.group is not None else dist.group.WORLD
+            hdl = symm.rendezvous(buf, group)
+            cache[k] = (buf, hdl, list(hdl.buffer_ptrs))
+        return cache[k]
+
+    def apply_push(self, g_local, adjoint: bool = False):
+        """Sharded apply with the middle exchange fused into the last down level (peer stores)."""
+        import torch
+        if g_local.shape[0] != self.n_local:
+            raise ValueError(f"local input length {g_local.shape[0]} != {self.n_local}")
+        k = g_local.reshape(self.n_local, -1).shape[1]
+        buf, hdl, ptrs = self.push_buffer(k)
+        hdl.barrier()                       # every part is done reading its buffer (previous apply)
+        self.down_push(g_local, adjoint, ptrs)
+        hdl.barrier()                       # every part's stores into this buffer have landed
+        recv = buf.view(torch.complex128) if self.tdt == torch.complex128 else buf
+        recv = recv.view(self.nparts * self.chunk_rows, k)
+        return self.up(self.unpack(recv, adjoint), adjoint)
+
+    ShardedPlan.down_push = down_push
+    ShardedPlan.push_buffer = push_buffer
+    ShardedPlan.apply_push = apply_push
+
+
+_push_methods()
