@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the node-sharded path even at one rank")
     ap.add_argument("--no-also", action="store_true", help="skip the companion configs[1] measurement")
+    ap.add_argument("--exchange", default="push", choices=["push", "nccl"],
+                    help="N>1 middle exchange: fused peer stores (symmetric memory) or pack + NCCL all-to-all")
     return ap.parse_args()
 
 
@@ -255,8 +257,24 @@ def run_sharded(args, world, rank, local):
     g = torch.from_numpy(np.ascontiguousarray(g_host)).to("cuda").to(tdt)
     stream = torch.cuda.current_stream()
     steps, warm = args.steps, max(args.warmup, 3)
+    exchange = args.exchange
+    if exchange == "push":
+        # fused path: validate once against pack + NCCL all-to-all, fall back if unavailable or different
+        try:
+            ref_out = sp.apply(g)
+            push_out = sp.apply_push(g)
+            torch.cuda.synchronize()
+            ok = torch.equal(ref_out, push_out)
+            flag = torch.tensor([1 if ok else 0], device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) != 1:
+                exchange = "nccl (push validation failed)"
+        except Exception as exc:  # symmetric memory / IPC not available
+            exchange = f"nccl (push unavailable: {type(exc).__name__})"
+    use_push = exchange == "push"
+    run = sp.apply_push if use_push else sp.apply
     for _ in range(warm):
-        sp.apply(g)
+        run(g)
     torch.cuda.synchronize()
     dist.barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
@@ -268,12 +286,22 @@ def run_sharded(args, world, rank, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(steps):
-        mid = sp.down(g, False)
-        send = sp.pack(mid, False)
-        ev[i][0].record(stream)
-        recv = sp.exchange(send)
-        ev[i][1].record(stream)
-        sp.up(sp.unpack(recv, False), False)
+        if use_push:
+            buf, hdl, ptrs = sp.push_buffer(g.shape[1])
+            hdl.barrier()
+            sp.down_push(g, False, ptrs)      # the exchange is fused into this launch's stores
+            ev[i][0].record(stream)
+            hdl.barrier()                     # only the wait for the peers' stores is separable
+            ev[i][1].record(stream)
+            recv = (buf.view(torch.complex128) if sp.tdt == torch.complex128 else buf).view(-1, g.shape[1])
+            sp.up(sp.unpack(recv, False), False)
+        else:
+            mid = sp.down(g, False)
+            send = sp.pack(mid, False)
+            ev[i][0].record(stream)
+            recv = sp.exchange(send)
+            ev[i][1].record(stream)
+            sp.up(sp.unpack(recv, False), False)
     e1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
@@ -289,7 +317,7 @@ def run_sharded(args, world, rank, local):
     t0 = time.perf_counter()
     e2e_steps = max(3, min(steps, 10))
     for _ in range(e2e_steps):
-        o_pin.copy_(sp.apply(g_pin.to("cuda", non_blocking=True)))
+        o_pin.copy_(run(g_pin.to("cuda", non_blocking=True)))
     torch.cuda.synchronize()
     e2e = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device="cuda")
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
@@ -301,18 +329,21 @@ def run_sharded(args, world, rank, local):
         a2a_bytes = esz * (world - 1) * sp.chunk_rows * k
         hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)) \
             if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
-        achieved = fac_bytes / ((ms_step - a2a_ms) / 1e3) / 1e9
+        achieved = fac_bytes / (((ms_step - a2a_ms) if not use_push else ms_step) / 1e3) / 1e9
         print(json.dumps({
             "metric": METRIC, "value": n * k / (ms_step / 1e3), "unit": "samples/s", "n_gpus": world,
             "steps": steps, "warmup": warm, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": f"{args.config} {kern.upper()} N={n} r={r} leaf={leaf} (L={p.levels}) k={k} "
-                                   f"{args.dtype}, sharded over {world} GPUs (middle nodes), NCCL all-to-all at M",
+                                   f"{args.dtype}, sharded over {world} GPUs (middle nodes), exchange at M: {exchange}",
                        "n": n, "rank": r, "levels": p.levels, "rhs": k, "parallelism": f"node-sharded{world}",
                        "l2": "inputs larger than L2 (each rank streams its factor slice every step)"},
-            "a2a_ms_per_step": a2a_ms, "a2a_bytes_per_rank": a2a_bytes,
+            "exchange": exchange,
+            "a2a_ms_per_step": None if use_push else a2a_ms,
+            "exchange_wait_ms_per_step": a2a_ms if use_push else None, "a2a_bytes_per_rank": a2a_bytes,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": None, "kernel": "local chain (down + up) per rank, exchange excluded",
+                         "traffic": None, "kernel": "local chain (down + up) per rank" +
+                         (" incl. fused peer stores" if use_push else ", all-to-all excluded"),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
             "e2e": {"value": n * k / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": n * k * esz,
                     "d2h_bytes_per_step": n * k * esz, "ms_per_step": e2e_s * 1e3},
