@@ -226,3 +226,35 @@ def test_pinned_host_pipeline_bitwise(n, leaf, r, k):
         for _ in range(2):      # first call captures the pipeline graph, second replays it
             host = pl.apply(g_pin.numpy(), adjoint=adjoint, out=o_pin.numpy())
             assert np.array_equal(host, dev)
+
+
+@pytest.mark.parametrize("n,levels,r,k", [
+    (4, 2, 1, 1),       # smallest partition: m = 2, side = 2
+    (4, 2, 2, 3),
+    (16, 8, 3, 2),      # leaf 1/16: the middle level itself is merge-only (side = 1)
+    (64, 12, 2, 5),     # leaf 1/64, every level merge-only
+    (32, 10, 4, 9),     # many-RHS kernels on merge-only levels
+])
+def test_edge_geometries(n, levels, r, k):
+    p = bf.DyadicPartition(n, levels)
+    f = synthetic_chain(p, r, seed=n * levels + r)
+    oc = oracle_of(f)
+    g = complex_gaussian(np.random.default_rng(k), (n, k))
+    gd = torch.from_numpy(g).cuda()
+    assert rel(f.plan().apply(gd), ochain.apply(oc, g)) <= TOL128
+    assert rel(f.plan().apply(gd, adjoint=True), ochain.apply(oc, g, adjoint=True)) <= TOL128
+    assert rel(f.plan("c64").apply(gd).to(torch.complex128), ochain.apply(oc, g)) <= TOL64
+    # shapes: (n,) -> (n,), (n, 1) -> (n, 1)
+    assert f.apply(g[:, 0]).shape == (n,) and f.apply(g[:, :1]).shape == (n, 1)
+
+
+def test_plan_rejects_mismatched_factors():
+    p = bf.make_partition(256, 16)
+    f = synthetic_chain(p, 4, seed=1)
+    bad = bf.ButterflyFactors(p, 4, f.u_outer, f.g_chain[:-1], f.middle, f.h_chain, f.v_outer)
+    with pytest.raises(ValueError):
+        bad.apply(np.zeros(256))
+    wrong = bf.ButterflyFactors(p, 4, bf.BlockDiagonalFactor(f.u_outer.blocks[:, :, :3]), f.g_chain, f.middle,
+                                f.h_chain, f.v_outer)
+    with pytest.raises(ValueError):
+        wrong.apply(np.zeros(256))
