@@ -221,7 +221,7 @@ int bf_sampled_rows(int kernel_id, uint64_t n, const void* dense, const int64_t*
  * m <= 64: up to k picks each, in pick order, into pivots (batch, k) and pick
  * counts into counts (batch); rel_tol as the reference's. pairwise = 1 sums
  * the initial column norms in numpy's pairwise order (the reference matrix is
- * F-ordered), 0 sequentially (C-ordered). Workspace >= 16*batch*m*n bytes. */
+ * F-ordered), 0 sequentially (C-ordered). Workspace >= 16*batch*min(k,m)*n bytes. */
 int bf_select_pivots(const void* a, uint32_t batch, uint32_t m, uint32_t n, uint32_t k, double rel_tol,
                      int pairwise, int32_t* pivots, int32_t* counts, void* workspace,
                      uint64_t ws_bytes, void* stream);

@@ -114,6 +114,14 @@ class MiddleSampler:
         self.dev = _DeviceOracle(oracle, p.n)
         self.branching = getattr(p, "branching", 2)
         self.dense_branch = r * params.q >= self.side
+        self._all_draws = None
+
+    def prepare_draws(self):
+        """Draw tables of every middle block up front (process pool), consumed per batch."""
+        if not self.dense_branch and self._all_draws is None:
+            m = self.m
+            self._all_draws = draw_tables(self.seed, self.side, self.r, self.params,
+                                          [(i, j) for i in range(m) for j in range(m)])
 
     def blocks(self, ij):
         """(u0*sigma0, v0*sigma0, floored_inverse(sigma0)) for blocks ij, on the device."""
@@ -127,6 +135,8 @@ class MiddleSampler:
         ij_d = torch.from_numpy(np.ascontiguousarray(ij)).cuda()
         if self.dense_branch:
             draws_d = None
+        elif self._all_draws is not None:
+            draws_d = torch.from_numpy(np.ascontiguousarray(self._all_draws[ij[:, 0] * self.m + ij[:, 1]])).cuda()
         else:
             draws_d = torch.from_numpy(draw_tables(self.seed, side, r, self.params, ij.tolist())).cuda()
         wsb = int(self.lib.bf_middle_workspace_bytes(self.p.n, self.p.levels, self.branching, r, self.params.q, nb))
@@ -250,6 +260,8 @@ def factorize(oracle, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0,
         raise ValueError(f"unknown mode {mode!r}")
     torch = _lib.require_cuda()
     ms = MiddleSampler(oracle, p, r, params, seed)
+    if ms.m * ms.m >= 1024:
+        ms.prepare_draws()
     m, side = ms.m, ms.side
     shapes, leaf_shape = level_geometry(p, r)
     weights = torch.zeros((m, m, r), dtype=torch.float64, device="cuda")

@@ -130,8 +130,8 @@ __global__ void k_fill_wide(MidArgs a, int which) {
 // Residual norms are downdated, never recomputed; ties within 2*PIVOT_TIE
 // go to the lowest index. Returns the pick count; picks in pick order.
 // Shared: norms (ncols doubles), q (kSetCap), red (32 doubles), redi (32 ints).
-__device__ int pivot_rows_core(double2* W, int nr, int ncols, int k, double rel_tol, bool pairwise, double* norms,
-                               double2* q, double* red, int* redi, int* picks) {
+__device__ int pivot_rows_core(const double2* W, int nr, int ncols, int k, double rel_tol, bool pairwise,
+                               double* norms, double2* q, double* red, int* redi, int* picks, double2* Rm) {
   for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
     auto get = [&](int i) { return abs2(W[static_cast<int64_t>(i) * ncols + c]); };
     norms[c] = pairwise ? pairwise_sum(get, 0, nr) : sequential_sum(get, nr);
@@ -153,28 +153,30 @@ __device__ int pivot_rows_core(double2* W, int nr, int ncols, int k, double rel_
       if (norms[c] >= thr) li = min(li, c);
     const int j = block_min_int(li, redi);
     const double sq = sqrt(norms[j]);
-    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
-      const double2 w = W[static_cast<int64_t>(i) * ncols + j];
-      q[i] = make_double2(__ddiv_rn(w.x, sq), __ddiv_rn(w.y, sq));
-    }
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) q[i] = W[static_cast<int64_t>(i) * ncols + j];
     if (threadIdx.x == 0) picks[npick] = j;
-    ++npick;
     __syncthreads();
+    // left-looking form of the Gram-Schmidt step: with q = work_j / sqrt(norms_j),
+    // q^H work_c = (w_j^H w_c - sum_l conj(P_lj) P_lc) / sqrt(norms_j), so W stays
+    // read-only and only the projection rows P (k x ncols) are written
+    double2* prow = Rm + static_cast<int64_t>(npick) * ncols;
     for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
-      double2 pr = make_double2(0, 0);
+      double2 g = make_double2(0, 0);
       for (int i = 0; i < nr; ++i) {
-        const double2 g = cmulc(q[i], W[static_cast<int64_t>(i) * ncols + c]);
-        pr.x += g.x;
-        pr.y += g.y;
+        const double2 t = cmulc(q[i], W[static_cast<int64_t>(i) * ncols + c]);
+        g.x += t.x;
+        g.y += t.y;
       }
-      for (int i = 0; i < nr; ++i) {
-        double2& w = W[static_cast<int64_t>(i) * ncols + c];
-        const double2 d = cmul(q[i], pr);
-        w.x -= d.x;
-        w.y -= d.y;
+      for (int l = 0; l < npick; ++l) {
+        const double2 t = cmulc(Rm[static_cast<int64_t>(l) * ncols + j], Rm[static_cast<int64_t>(l) * ncols + c]);
+        g.x -= t.x;
+        g.y -= t.y;
       }
+      const double2 pr = make_double2(__ddiv_rn(g.x, sq), __ddiv_rn(g.y, sq));
+      prow[c] = pr;
       norms[c] = fmax(__dsub_rn(norms[c], abs2(pr)), 0.0);
     }
+    ++npick;
     __syncthreads();
     if (threadIdx.x == 0) norms[j] = 0.0;
     __syncthreads();
@@ -194,8 +196,9 @@ __global__ void k_pivot_wide(MidArgs a, int which) {
   BlockState& s = a.st[blockIdx.x];
   const int nr = which == kRows ? s.nrows : s.ncols;
   double2* W = a.wide + static_cast<int64_t>(blockIdx.x) * a.S * a.side;
+  double2* Rm = a.tall + static_cast<int64_t>(blockIdx.x) * a.S * a.side;  // projection rows (r x side)
   const int npick = pivot_rows_core(W, nr, static_cast<int>(a.side), a.r, 0.0, which == kCols, norms, q, red, redi,
-                                    picks);
+                                    picks, Rm);
   // skeleton = sorted(picks)
   if (threadIdx.x == 0) {
     int32_t* sk = which == kRows ? s.skc : s.skr;
@@ -222,9 +225,8 @@ __global__ void k_select_pivots(const double2* A, double2* scratch, int m, int n
   int* redi = reinterpret_cast<int*>(red + 32);
   int* picks = redi + 32;
   const int64_t off = static_cast<int64_t>(blockIdx.x) * m * n;
-  for (int64_t x = threadIdx.x; x < static_cast<int64_t>(m) * n; x += blockDim.x) scratch[off + x] = A[off + x];
-  __syncthreads();
-  const int np = pivot_rows_core(scratch + off, m, n, k, rel_tol, pairwise != 0, norms, q, red, redi, picks);
+  double2* Rm = scratch + static_cast<int64_t>(blockIdx.x) * min(k, m) * n;
+  const int np = pivot_rows_core(A + off, m, n, k, rel_tol, pairwise != 0, norms, q, red, redi, picks, Rm);
   for (int i = threadIdx.x; i < np; i += blockDim.x) pivots[static_cast<int64_t>(blockIdx.x) * k + i] = picks[i];
   if (threadIdx.x == 0) counts[blockIdx.x] = np;
 }
@@ -250,7 +252,19 @@ __global__ void k_fill_tall(MidArgs a, int which, int use_piv, double2* dst_base
 
 // Greedy pivoting on the tall T (side x nc, column-major), up to kmax picks,
 // rel_tol = BASIS_TRIM; pick order kept (orthonormal_columns, lowrank.py:132-154).
-__global__ void k_pivot_tall(MidArgs a, int which) {
+// Greedy pivoting of the tall T (side x nc, column-major; orthonormal_columns,
+// lowrank.py:132-154) through its Gram matrix: G = T^H T in one pass over T
+// (row chunks staged in shared memory), then the pivoted Cholesky recurrence
+// on G, which reproduces select_pivot_columns' (lowrank.py:102-129) Gram-Schmidt
+// step for step: with q = work_j / sqrt(norms_j), the projections are
+// proj_c = (G_jc - sum_l conj(P_lj) P_lc) / sqrt(norms_j) and the norms are
+// downdated by |proj_c|^2. The initial norms keep the reference's exact
+// summation order; the first pick is therefore bitwise the reference's.
+// Past the numerical rank both this and the reference pick rounding noise.
+constexpr int kGramChunk = 32;
+
+__global__ void __launch_bounds__(512) k_pivot_tall(MidArgs a, int which) {
+  extern __shared__ double2 tsm[];
   __shared__ double norms[kSetCap];
   __shared__ int picks[kSetCap];
   __shared__ int s_j, s_stop;
@@ -258,15 +272,76 @@ __global__ void k_pivot_tall(MidArgs a, int which) {
   BlockState& s = a.st[blockIdx.x];
   const int nc = which == kCols ? s.ncols : s.nrows;
   const int side = static_cast<int>(a.side);
-  double2* T = a.tall + static_cast<int64_t>(blockIdx.x) * a.S * a.side;
-  double2* q = a.qbuf + static_cast<int64_t>(blockIdx.x) * a.side;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int S = a.S;
+  const double2* T = a.tall + static_cast<int64_t>(blockIdx.x) * S * a.side;
   for (int c = threadIdx.x; c < nc; c += blockDim.x) {
     const double2* col = T + static_cast<int64_t>(c) * side;
     auto get = [&](int i) { return abs2(col[i]); };
     norms[c] = which == kCols ? sequential_sum(get, side) : pairwise_sum(get, 0, side);
   }
+  double2* chunk = tsm;                                           // kGramChunk x S
+  const int64_t SS = static_cast<int64_t>(S) * S;
+  double2* gscr = a.scr + static_cast<int64_t>(blockIdx.x) * 9 * SS;
+  double2* G = S <= kSmemSet ? tsm + kGramChunk * S : gscr;       // S x S
+  double2* Rm = S <= kSmemSet ? G + SS : gscr + SS;               // picks x S
+  // ---- Gram matrix: 4x4 register tiles over the upper block triangle, mirrored at the end
+  const int nc4 = (nc + 3) / 4;
+  const int ntiles = nc4 * (nc4 + 1) / 2;
+  for (int tile0 = 0; tile0 < ntiles; tile0 += blockDim.x) {
+    const int tid = tile0 + threadIdx.x;
+    int ta = 0, rem = tid;
+    if (tid < ntiles)
+      while (rem >= nc4 - ta) {
+        rem -= nc4 - ta;
+        ++ta;
+      }
+    const int tb = ta + rem;
+    double2 acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = make_double2(0, 0);
+    for (int r0 = 0; r0 < side; r0 += kGramChunk) {
+      const int rows = min(kGramChunk, side - r0);
+      __syncthreads();
+      for (int x = threadIdx.x; x < nc4 * 4 * kGramChunk; x += blockDim.x) {
+        const int c = x / kGramChunk, i = x % kGramChunk;
+        chunk[i * S + c] = (i < rows && c < nc) ? T[static_cast<int64_t>(c) * side + r0 + i] : make_double2(0, 0);
+      }
+      __syncthreads();
+      if (tid < ntiles)
+        for (int i = 0; i < rows; ++i) {
+          double2 xa[4], xb[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            xa[u] = chunk[i * S + 4 * ta + u];
+            xb[u] = chunk[i * S + 4 * tb + u];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const double2 g = cmulc(xa[u], xb[v]);
+              acc[u][v].x += g.x;
+              acc[u][v].y += g.y;
+            }
+        }
+    }
+    if (tid < ntiles) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int ra = 4 * ta + u, cb = 4 * tb + v;
+          if (ra < nc && cb < nc && ra <= cb) {
+            G[ra * S + cb] = acc[u][v];
+            G[cb * S + ra] = cconj(acc[u][v]);
+          }
+        }
+    }
+  }
   __syncthreads();
+  // ---- pivoted Cholesky recurrence == the greedy Gram-Schmidt pivoting
   const int width = max(a.r, min(s.nrows, s.ncols) - a.r);
   const int kmax = min(min(width, side), min(side, nc));
   double mx0 = 0.0;
@@ -291,27 +366,19 @@ __global__ void k_pivot_tall(MidArgs a, int which) {
     if (s_stop) break;
     const int j = s_j;
     const double sq = s_sq;
-    const double2* cj = T + static_cast<int64_t>(j) * side;
-    for (int i = threadIdx.x; i < side; i += blockDim.x)
-      q[i] = make_double2(__ddiv_rn(cj[i].x, sq), __ddiv_rn(cj[i].y, sq));
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+      double2 v = G[j * S + c];
+      for (int l = 0; l < it; ++l) {
+        const double2 d = cmulc(Rm[l * S + j], Rm[l * S + c]);
+        v.x -= d.x;
+        v.y -= d.y;
+      }
+      Rm[it * S + c] = make_double2(__ddiv_rn(v.x, sq), __ddiv_rn(v.y, sq));
+    }
     ++npick;
     __syncthreads();
-    for (int c = warp; c < nc; c += nw) {
-      double2* col = T + static_cast<int64_t>(c) * side;
-      double2 pr = make_double2(0, 0);
-      for (int i = lane; i < side; i += 32) {
-        const double2 g = cmulc(q[i], col[i]);
-        pr.x += g.x;
-        pr.y += g.y;
-      }
-      pr = warp_sum2(pr);
-      for (int i = lane; i < side; i += 32) {
-        const double2 d = cmul(q[i], pr);
-        col[i].x -= d.x;
-        col[i].y -= d.y;
-      }
-      if (lane == 0) norms[c] = fmax(__dsub_rn(norms[c], abs2(pr)), 0.0);
-    }
+    for (int c = threadIdx.x; c < nc; c += blockDim.x)
+      norms[c] = fmax(__dsub_rn(norms[c], abs2(Rm[it * S + c])), 0.0);
     __syncthreads();
     if (threadIdx.x == 0) norms[j] = 0.0;
     __syncthreads();
@@ -829,9 +896,12 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
     }
     k_union<<<nblocks, 128, 0, st>>>(a, 2 * iters, kRows);
     k_union<<<nblocks, 128, 0, st>>>(a, 2 * iters + 1, kCols);
+    const size_t tall_smem = (static_cast<size_t>(kGramChunk) * S + (S <= kSmemSet ? 2ull * S * S : 0)) * 16;
+    BF_CUDA(cudaFuncSetAttribute(k_pivot_tall, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(tall_smem)));
     for (int which : {kCols, kRows}) {
       k_fill_tall<<<dim3(nblocks, yfill), T, 0, st>>>(a, which, 0, a.tall);
-      k_pivot_tall<<<nblocks, 512, 0, st>>>(a, which);
+      k_pivot_tall<<<nblocks, 512, tall_smem, st>>>(a, which);
       k_fill_tall<<<dim3(nblocks, yfill), T, 0, st>>>(a, which, 1, which == kCols ? a.qc : a.qr);
       k_cgs2<<<nblocks, 512, 0, st>>>(a, which);
     }
@@ -906,7 +976,8 @@ int bf_select_pivots(const void* a, uint32_t batch, uint32_t m, uint32_t n, uint
   if (m > static_cast<uint32_t>(kSetCap) || n > 16384 || k > 1024) return fail(BF_EINVAL, "pivot matrix too large");
   if (!batch || !m || !n || !k) return BF_OK;
   if (!a || !pivots || !counts || !workspace) return fail(BF_EINVAL, "null pointer");
-  if (ws_bytes < 16ull * batch * m * n) return fail(BF_EINVAL, "pivot workspace too small (16*batch*m*n bytes)");
+  const uint64_t kk = k < m ? k : m;
+  if (ws_bytes < 16ull * batch * kk * n) return fail(BF_EINVAL, "pivot workspace too small (16*batch*min(k,m)*n bytes)");
   const size_t smem = (n + (n & 1)) * 8 + kSetCap * 16 + 32 * 8 + 32 * 4 + 1024 * 4;
   BF_CUDA(cudaFuncSetAttribute(k_select_pivots, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   k_select_pivots<<<batch, 512, smem, static_cast<cudaStream_t>(stream)>>>(
