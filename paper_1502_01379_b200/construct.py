@@ -228,12 +228,20 @@ def middle_factorization_sampling(entry, p: DyadicPartition, r: int, params=DEFA
             BlockDiagonalFactor(v.reshape(m, side, m * r)))
 
 
-def _place(chain, leaf, k, leaf_k, pieces):
+def _place(chain, leaf, k0, cnt, leaf_k, pieces):
+    """Scatter the recursion of slabs k0 .. k0+cnt-1 (node-major) into the full chain."""
     for lvl, blocks in pieces:
-        nb = blocks.shape[0]
-        chain[lvl][k * nb:(k + 1) * nb] = blocks
-    nb = leaf_k.shape[0]
-    leaf[k * nb:(k + 1) * nb] = leaf_k
+        nb = blocks.shape[0] // cnt
+        chain[lvl][k0 * nb:(k0 + cnt) * nb] = blocks
+    nb = leaf_k.shape[0] // cnt
+    leaf[k0 * nb:(k0 + cnt) * nb] = leaf_k
+
+
+def recursion_batch(m: int, side: int, r: int) -> int:
+    """Slabs per recursion launch: >= 2048 first-level problems (the level kernels
+    are latency-bound per problem, so the GPU needs many in flight), <= 4 GiB of slabs."""
+    slab_bytes = 16 * side * m * r
+    return max(1, min(m, -(-2048 // m), (4 << 30) // max(1, slab_bytes)))
 
 
 def factorize(oracle, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0,
@@ -272,11 +280,15 @@ def factorize(oracle, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0,
     for axis in ("u", "v"):
         chain = {lvl: torch.zeros(shape, dtype=torch.complex128, device="cuda") for lvl, _, shape in shapes}
         leaf = torch.zeros(leaf_shape, dtype=torch.complex128, device="cuda")
+        kb = recursion_batch(m, side, r)
         if axis == "v" and mode == "sampling":
-            for k in range(m):
-                leaf_k, pieces = recurse(v_full[k:k + 1], p, r)
-                _place(chain, leaf, k, leaf_k, pieces)
+            for k0 in range(0, m, kb):
+                cnt = min(kb, m - k0)
+                leaf_k, pieces = recurse(v_full[k0:k0 + cnt], p, r)
+                _place(chain, leaf, k0, cnt, leaf_k, pieces)
         else:
+            buf = torch.empty((kb, side, m, r), dtype=torch.complex128, device="cuda")
+            filled, k_first = 0, 0
             step = ms.batch_rows()
             for k0 in range(0, m, step):
                 ks = range(k0, min(m, k0 + step))
@@ -285,14 +297,20 @@ def factorize(oracle, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0,
                 for idx, k in enumerate(ks):
                     sl = slice(idx * m, (idx + 1) * m)
                     if axis == "u":
-                        slab = uu[sl].permute(1, 0, 2).reshape(1, side, m, r)      # slab[0, :, j, :]
+                        buf[filled] = uu[sl].permute(1, 0, 2)                      # slab[:, j, :]
                         weights[k] = ww[sl]
                         if v_full is not None:
                             v_full[:, :, k, :] = vv[sl]                            # v[j, :, i=k, :]
                     else:
-                        slab = vv[sl].permute(1, 0, 2).reshape(1, side, m, r)      # slab[0, :, i, :]
-                    leaf_k, pieces = recurse(slab, p, r)
-                    _place(chain, leaf, k, leaf_k, pieces)
+                        buf[filled] = vv[sl].permute(1, 0, 2)                      # slab[:, i, :]
+                    if filled == 0:
+                        k_first = k
+                    filled += 1
+                    if filled == kb or k == m - 1:
+                        leaf_k, pieces = recurse(buf[:filled], p, r)
+                        _place(chain, leaf, k_first, filled, leaf_k, pieces)
+                        filled = 0
+            del buf
         sides.append((BlockDiagonalFactor(leaf), tuple(TransferFactor(lvl, chain[lvl]) for lvl, _, _ in shapes)))
     del v_full
     (u_outer, g_chain), (v_outer, h_chain) = sides

@@ -687,9 +687,124 @@ __device__ void householder_r(double2* A, int m, int n, double2* R, int ldr, dou
   }
 }
 
+
+// One warp: Householder QR of B (rows x n) in shared memory, COLUMN-major with
+// an odd leading dimension ldb (element (i, c) at B[c * ldb + i]): the norm of
+// column p is a lane-strided reduction over contiguous elements, and the
+// reflector is applied with one lane per trailing column (lane j walks rows of
+// column j at stride 1 while v_i is a broadcast) — no shuffles in the update
+// and no bank conflicts (odd ldb). On return rows 0..n-1 hold R.
+__device__ void warp_householder(double2* B, int ldb, int rows, int n) {
+  const int lane = threadIdx.x & 31;
+  for (int p = 0; p < n && p < rows; ++p) {
+    double2* vp = B + p * ldb;
+    double s2 = 0;
+    for (int i = p + lane; i < rows; i += 32) s2 += vp[i].x * vp[i].x + vp[i].y * vp[i].y;
+    s2 = warp_sum(s2);
+    const double2 al = vp[p];
+    const double nx = sqrt(s2), aa = hypot(al.x, al.y);
+    const double2 beta = aa > 0 ? make_double2(-al.x / aa * nx, -al.y / aa * nx) : make_double2(-nx, 0);
+    const double2 v0 = make_double2(al.x - beta.x, al.y - beta.y);
+    const double vn2 = s2 - aa * aa + v0.x * v0.x + v0.y * v0.y;
+    __syncwarp();
+    if (lane == 0) vp[p] = v0;
+    __syncwarp();
+    if (vn2 > 0) {
+      const double f = 2.0 / vn2;
+      for (int j = p + 1 + lane; j < n; j += 32) {
+        double2* cj = B + j * ldb;
+        double2 w0 = make_double2(0, 0), w1 = make_double2(0, 0);
+        int i = p;
+        for (; i + 1 < rows; i += 2) {
+          const double2 g0 = cmulc(vp[i], cj[i]), g1 = cmulc(vp[i + 1], cj[i + 1]);
+          w0.x += g0.x;
+          w0.y += g0.y;
+          w1.x += g1.x;
+          w1.y += g1.y;
+        }
+        if (i < rows) {
+          const double2 g0 = cmulc(vp[i], cj[i]);
+          w0.x += g0.x;
+          w0.y += g0.y;
+        }
+        const double2 w = make_double2((w0.x + w1.x) * f, (w0.y + w1.y) * f);
+        for (i = p; i < rows; ++i) {
+          const double2 d = cmul(vp[i], w);
+          cj[i].x -= d.x;
+          cj[i].y -= d.y;
+        }
+      }
+    }
+    __syncwarp();
+    for (int i = p + 1 + lane; i < rows; i += 32) vp[i] = make_double2(0, 0);
+    if (lane == 0) vp[p] = vn2 > 0 ? beta : al;
+    __syncwarp();
+  }
+}
+
+// R factor of a tall (part x n) stack by TSQR in shared memory: warps stream
+// row chunks into [R_acc; chunk] buffers (column-major, odd ld) and QR them (no
+// block barriers), then combine their R's pairwise. Leaves R (n x n, row-major)
+// in Rout (ld ldr). smem must hold nwu * tsqr_ld(n, ch) * n complex values.
+__device__ __host__ __forceinline__ int tsqr_ld(int n, int ch) { return (n + ch) | 1; }
+
+template <typename F>
+__device__ void tsqr_r(const F& src, int64_t part, int n, double2* smem, int nwu, int ch, double2* Rout, int ldr) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ldb = tsqr_ld(n, ch);
+  double2* B = smem + static_cast<int64_t>(warp) * ldb * n;
+  const int64_t nchunks = (part + ch - 1) / ch;
+  if (warp < nwu) {
+    for (int x = lane; x < ldb * n; x += 32) B[x] = make_double2(0, 0);
+    for (int64_t cidx = warp; cidx < nchunks; cidx += nwu) {
+      const int64_t r0 = cidx * ch;
+      const int rows = static_cast<int>((part - r0) < ch ? (part - r0) : ch);
+      __syncwarp();
+      for (int x = lane; x < rows * n; x += 32) {
+        const int i = x / n, c = x % n;
+        B[c * ldb + n + i] = src(r0 + i, c);
+      }
+      __syncwarp();
+      warp_householder(B, ldb, n + rows, n);
+    }
+  }
+  __syncthreads();
+  for (int step = 1; step < nwu; step *= 2) {
+    if (warp < nwu && warp % (2 * step) == 0 && warp + step < nwu) {
+      const double2* B2 = smem + static_cast<int64_t>(warp + step) * ldb * n;
+      for (int x = lane; x < n * n; x += 32) {
+        const int c = x / n, i = x % n;
+        B[c * ldb + n + i] = B2[c * ldb + i];
+      }
+      __syncwarp();
+      warp_householder(B, ldb, 2 * n, n);
+    }
+    __syncthreads();
+  }
+  // R of warp 0 -> Rout (through registers: Rout may overlap the warp buffers)
+  double2 vals[16];
+  int cnt = 0;
+  const int ldb0 = tsqr_ld(n, ch);
+  for (int x = threadIdx.x; x < n * n && cnt < 16; x += blockDim.x) vals[cnt++] = smem[(x % n) * ldb0 + x / n];
+  __syncthreads();
+  cnt = 0;
+  for (int x = threadIdx.x; x < n * n && cnt < 16; x += blockDim.x) {
+    const int i = x / n, c = x % n;
+    Rout[i * ldr + c] = i <= c ? vals[cnt] : make_double2(0, 0);
+    ++cnt;
+  }
+  __syncthreads();
+}
+
 // Per-problem global scratch: [Ac: max(part, S) x w][Ug: S x S][Vg: S x S][Mb, W, Vt: S x S each when S > 64].
 __device__ __host__ __forceinline__ int64_t rec_scratch_elems(int64_t part, int w, int S) {
-  return (part > S ? part : S) * w + 5ll * S * S;
+  // shared-memory problems (S <= kSmemSet) keep only U and V in global scratch
+  return S <= kSmemSet ? 2ll * S * S : (part > S ? part : S) * w + 5ll * S * S;
+}
+
+// dynamic shared memory of k_recurse_split when S <= kSmemSet (see its layout)
+__device__ __host__ __forceinline__ int64_t rec_smem_elems(int w, int S) {
+  return static_cast<int64_t>(S) * (w + 1) + static_cast<int64_t>(S) * w + static_cast<int64_t>(w) * (w + 1);
 }
 
 __global__ void k_recurse_split(RecArgs a) {
@@ -706,17 +821,20 @@ __global__ void k_recurse_split(RecArgs a) {
   const int keep = static_cast<int>(part < r ? part : r);
   const int64_t SS = static_cast<int64_t>(S) * S;
   double2* Ac = a.scr + static_cast<int64_t>(blockIdx.x) * rec_scratch_elems(part, w, S);
-  double2* Ug = Ac + (part > S ? part : S) * w;
+  double2* Ug = S <= kSmemSet ? Ac : Ac + (part > S ? part : S) * w;
   double2* Vg = Ug + SS;
   const bool sh = S <= kSmemSet;
+  // shared layout (S <= 64): Mb (S x (w+1)) | W (S x w) | Vt (w x (w+1)), odd row
+  // strides (rec_smem_elems); global scratch (S = 128) keeps stride S
+  const int ldm = sh ? w + 1 : S;
   double2* Mb = sh ? sm2 : Vg + SS;
-  double2* W = sh ? sm2 + SS : Vg + 2 * SS;
-  double2* Vt = sh ? sm2 + 2 * SS : Vg + 3 * SS;
+  double2* W = sh ? sm2 + S * ldm : Vg + 2 * SS;
+  double2* Vt = sh ? W + S * w : Vg + 3 * SS;
   const int64_t out_base = ((gb * b + t) * part) * pairs + p;  // new_u.transpose(0,1,3,2,4): row (gb,t,row=0,p)
   if (part <= S) {
-    for (int x = threadIdx.x; x < part * w; x += blockDim.x) Mb[(x / w) * S + x % w] = src(x / w, x % w);
+    for (int x = threadIdx.x; x < part * w; x += blockDim.x) Mb[(x / w) * ldm + x % w] = src(x / w, x % w);
     __syncthreads();
-    svd_small(Mb, static_cast<int>(part), w, S, Ug, S, Vg, S, sg, W, Vt, &flag, perm, ssc);
+    svd_small(Mb, static_cast<int>(part), w, ldm, Ug, S, Vg, S, sg, W, Vt, &flag, perm, ssc);
     for (int x = threadIdx.x; x < part * r; x += blockDim.x) {
       const int row = x / r, rho = x % r;
       double2 u = make_double2(0, 0);
@@ -724,13 +842,22 @@ __global__ void k_recurse_split(RecArgs a) {
       a.nxt[(out_base + row * pairs) * r + rho] = u;
     }
   } else {
-    // tall stack: Householder R, SVD of R gives sigma and V; new_u = A V[:, :keep] (= uu ss)
-    for (int64_t x = threadIdx.x; x < part * w; x += blockDim.x) Ac[x] = src(x / w, static_cast<int>(x % w));
-    __syncthreads();
-    householder_r(Ac, static_cast<int>(part), w, Mb, S, red);
-    __syncthreads();
-    svd_small(Mb, w, w, S, Ug, S, Vg, S, sg, W, Vt, &flag, perm, ssc);
-    for (int x = threadIdx.x; x < w * w; x += blockDim.x) Vt[(x / w) * S + x % w] = Vg[(x / w) * S + x % w];
+    // tall stack: R factor (TSQR in shared memory when the stack width fits, else a
+    // Householder pass in global memory); the SVD of R gives sigma and V; new_u = A V[:, :keep]
+    if (sh) {
+      const int ch = 32;
+      const int per = tsqr_ld(w, ch) * w;
+      int nwu = static_cast<int>(rec_smem_elems(w, S) / per);
+      nwu = nwu < 1 ? 1 : (nwu > static_cast<int>(blockDim.x >> 5) ? static_cast<int>(blockDim.x >> 5) : nwu);
+      tsqr_r(src, part, w, sm2, nwu, ch, Mb, ldm);
+    } else {
+      for (int64_t x = threadIdx.x; x < part * w; x += blockDim.x) Ac[x] = src(x / w, static_cast<int>(x % w));
+      __syncthreads();
+      householder_r(Ac, static_cast<int>(part), w, Mb, ldm, red);
+      __syncthreads();
+    }
+    svd_small(Mb, w, w, ldm, Ug, S, Vg, S, sg, W, Vt, &flag, perm, ssc);
+    for (int x = threadIdx.x; x < w * w; x += blockDim.x) Vt[(x / w) * ldm + x % w] = Vg[(x / w) * S + x % w];
     __syncthreads();
     for (int64_t x = threadIdx.x; x < part * r; x += blockDim.x) {
       const int64_t row = x / r;
@@ -738,7 +865,7 @@ __global__ void k_recurse_split(RecArgs a) {
       double2 u = make_double2(0, 0);
       if (rho < keep)
         for (int c = 0; c < w; ++c) {
-          const double2 g = cmul(src(row, c), Vt[c * S + rho]);
+          const double2 g = cmul(src(row, c), Vt[c * ldm + rho]);
           u.x += g.x;
           u.y += g.y;
         }
@@ -950,7 +1077,7 @@ int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t ro
   a.S = S;
   if (rows >= branching) {
     const int64_t nprob = static_cast<int64_t>(nb) * branching * pairs;
-    const size_t smem = S <= kSmemSet ? 3ull * S * S * sizeof(double2) : 0;
+    const size_t smem = S <= kSmemSet ? rec_smem_elems(static_cast<int>(w), S) * sizeof(double2) : 0;
     BF_CUDA(cudaFuncSetAttribute(k_recurse_split, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     for (int64_t p0 = 0; p0 < nprob; p0 += chunk) {
       a.p0 = p0;

@@ -141,18 +141,24 @@ __device__ double sequential_sum(const F& get, int n) {
 }
 
 // ---------------------------------------------------------------- Jacobi SVD
-// One-sided (Hestenes) Jacobi on the columns of A (m x n, m >= n, row-major
-// in shared memory, leading dimension lda). On return A holds U*Sigma
-// (unsorted, unnormalised) and V (n x n, ldv) the accumulated unitary. Pairs
-// run in round-robin tournament order, one warp per pair; every reduction
-// has a fixed order, so the result is deterministic.
+// One-sided (Hestenes) Jacobi on the columns of A (m x n, m >= n) held
+// COLUMN-major in shared memory (element (i, c) at A[c * lda + i]) so the 32
+// lanes of a warp touch 32 consecutive elements of a column: no bank
+// conflicts. On return A holds U*Sigma (unsorted, unnormalised) and V (n x n,
+// also column-major, ldv) the accumulated unitary. Pairs run in round-robin
+// tournament order, one warp per pair; every reduction has a fixed order, so
+// the result is deterministic.
+#ifdef BF_JACOBI_STATS
+__device__ int g_jacobi_sweeps;
+#endif
 __device__ void jacobi_cols(double2* A, int m, int n, int lda, double2* V, int ldv, int* flag) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
-    const int r = i / n, c = i % n;
-    V[r * ldv + c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+    const int c = i / n, r = i % n;
+    V[c * ldv + r] = make_double2(r == c ? 1.0 : 0.0, 0.0);
   }
   const int nn = n + (n & 1);  // tournament over an even count (a dummy column if n is odd)
+  const double tol = (m > 8 ? m : 8) * 2.220446049250313e-16;
   for (int sweep = 0; sweep < 60; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
@@ -163,10 +169,12 @@ __device__ void jacobi_cols(double2* A, int m, int n, int lda, double2* V, int l
         int b = 1 + (nn - 2 - pi + round) % (nn - 1);
         if (a > b) { const int t = a; a = b; b = t; }
         if (b >= n) continue;
+        double2* ca = A + a * lda;
+        double2* cb = A + b * lda;
         double al = 0, be = 0;
         double2 ga = make_double2(0, 0);
         for (int i = lane; i < m; i += 32) {
-          const double2 x = A[i * lda + a], y = A[i * lda + b];
+          const double2 x = ca[i], y = cb[i];
           al += x.x * x.x + x.y * x.y;
           be += y.x * y.x + y.y * y.y;
           const double2 g = cmulc(x, y);
@@ -176,53 +184,64 @@ __device__ void jacobi_cols(double2* A, int m, int n, int lda, double2* V, int l
         al = warp_sum(al);
         be = warp_sum(be);
         ga = warp_sum2(ga);
-        const double gabs = hypot(ga.x, ga.y);
-        if (gabs == 0.0 || gabs <= 1e-15 * sqrt(al) * sqrt(be)) continue;
+        // converged pair: |a^H b| <= m eps |a| |b| (the rounding level of the dot product
+        // itself; a tighter test can keep rotating noise and never terminate)
+        const double g2 = ga.x * ga.x + ga.y * ga.y;
+        if (g2 == 0.0 || g2 <= tol * tol * al * be) continue;
         if (lane == 0) *flag = 1;
-        const double zeta = (be - al) / (2.0 * gabs);
-        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-        const double2 ph = make_double2(ga.x / gabs, -ga.y / gabs);  // e^{-i phi}
+        // rotation from one rsqrt / sqrt / div / rsqrt chain (the pair's latency
+        // is the Jacobi's critical path)
+        const double ig = rsqrt(g2);
+        const double zeta = (be - al) * 0.5 * ig;
+        const double az = fabs(zeta), sgn = zeta >= 0 ? 1.0 : -1.0;
+        const double t = az > 1e150 ? sgn * 0.5 / az : sgn / (az + sqrt(1.0 + zeta * zeta));
+        const double c = rsqrt(1.0 + t * t), s = c * t;
+        const double2 ph = make_double2(ga.x * ig, -ga.y * ig);  // e^{-i phi}
         // [a', b'] = [a, b] [[c, s], [-s e^{-i phi}, c e^{-i phi}]]
         for (int i = lane; i < m; i += 32) {
-          const double2 x = A[i * lda + a], y = cmul(A[i * lda + b], ph);
-          A[i * lda + a] = make_double2(c * x.x - s * y.x, c * x.y - s * y.y);
-          A[i * lda + b] = make_double2(s * x.x + c * y.x, s * x.y + c * y.y);
+          const double2 x = ca[i], y = cmul(cb[i], ph);
+          ca[i] = make_double2(c * x.x - s * y.x, c * x.y - s * y.y);
+          cb[i] = make_double2(s * x.x + c * y.x, s * x.y + c * y.y);
         }
+        double2* va = V + a * ldv;
+        double2* vb = V + b * ldv;
         for (int i = lane; i < n; i += 32) {
-          const double2 x = V[i * ldv + a], y = cmul(V[i * ldv + b], ph);
-          V[i * ldv + a] = make_double2(c * x.x - s * y.x, c * x.y - s * y.y);
-          V[i * ldv + b] = make_double2(s * x.x + c * y.x, s * x.y + c * y.y);
+          const double2 x = va[i], y = cmul(vb[i], ph);
+          va[i] = make_double2(c * x.x - s * y.x, c * x.y - s * y.y);
+          vb[i] = make_double2(s * x.x + c * y.x, s * x.y + c * y.y);
         }
       }
       __syncthreads();
     }
     const int any = *flag;
     __syncthreads();
+#ifdef BF_JACOBI_STATS
+    if (threadIdx.x == 0) atomicAdd(&g_jacobi_sweeps, 1);
+#endif
     if (!any) break;
   }
 }
 
 // Thin SVD of a small matrix M (m x n) given in shared memory (row-major, ld).
-// Produces s = min(m, n) singular values sorted descending (ties by index),
-// U (m x s, ldu) and V (n x s, ldv) with orthonormal columns where sigma > 0
-// (zero columns otherwise). Work buffers: W (max(m,n) x min(m,n)), Vt
-// (min x min) shared; flag/perm small shared scratch (perm >= 64 ints).
+// Outputs U (m x k), sig (k), Vo (n x k) with k = min(m, n), singular values in
+// descending order (ties by column index). W (max*min) and Vt (min*min) are
+// shared-memory work buffers (used column-major); flag/perm/ssc are shared scratch.
 __device__ void svd_small(const double2* M, int m, int n, int ld, double2* U, int ldu, double2* Vo, int ldv,
                           double* sig, double2* W, double2* Vt, int* flag, int* perm, double* ssc) {
   const bool tall = m >= n;
   const int rr = tall ? m : n, cc = tall ? n : m;  // work on M (tall) or M^H
+  // W column-major: W(r, c) = W[c * rr + r]
   for (int i = threadIdx.x; i < rr * cc; i += blockDim.x) {
-    const int r = i / cc, c = i % cc;
-    W[r * cc + c] = tall ? M[r * ld + c] : cconj(M[c * ld + r]);
+    const int c = i / rr, r = i % rr;
+    W[c * rr + r] = tall ? M[r * ld + c] : cconj(M[c * ld + r]);
   }
   __syncthreads();
-  jacobi_cols(W, rr, cc, cc, Vt, cc, flag);
+  jacobi_cols(W, rr, cc, rr, Vt, cc, flag);
   __syncthreads();
   // column norms (fixed order) and descending order
   for (int c = threadIdx.x >> 5; c < cc; c += blockDim.x >> 5) {
     double acc = 0;
-    for (int i = threadIdx.x & 31; i < rr; i += 32) acc += W[i * cc + c].x * W[i * cc + c].x + W[i * cc + c].y * W[i * cc + c].y;
+    for (int i = threadIdx.x & 31; i < rr; i += 32) acc += W[c * rr + i].x * W[c * rr + i].x + W[c * rr + i].y * W[c * rr + i].y;
     acc = warp_sum(acc);
     if ((threadIdx.x & 31) == 0) ssc[c] = sqrt(acc);
   }
@@ -241,14 +260,14 @@ __device__ void svd_small(const double2* M, int m, int n, int ld, double2* U, in
   double2* R = tall ? Vo : U;
   const int ldr = tall ? ldv : ldu;
   for (int i = threadIdx.x; i < rr * cc; i += blockDim.x) {
-    const int r = i / cc, k = i % cc, c = perm[k];
+    const int k = i / rr, r = i % rr, c = perm[k];
     const double sg = ssc[c];
-    const double2 w = W[r * cc + c];
+    const double2 w = W[c * rr + r];
     L[r * ldl + k] = sg > 0 ? make_double2(w.x / sg, w.y / sg) : make_double2(0, 0);
   }
   for (int i = threadIdx.x; i < cc * cc; i += blockDim.x) {
-    const int r = i / cc, k = i % cc, c = perm[k];
-    R[r * ldr + k] = Vt[r * cc + c];
+    const int k = i / cc, r = i % cc, c = perm[k];
+    R[r * ldr + k] = Vt[c * cc + r];
   }
   __syncthreads();
 }

@@ -328,3 +328,26 @@ def test_eps_a_matches_reference_golden():
         got = bf.RowSampledReference(ker).rows(g, rows)
         want = blk(rows, np.arange(n)) @ g
         assert rel(got, want) <= 1e-12
+
+
+@pytest.mark.parametrize("n,leaf,r,b", [(4096, 16, 8, 2), (4096, 8, 16, 2), (1 << 12, 4, 6, 4)])
+def test_recursion_tall_stacks_vs_oracle(n, leaf, r, b):
+    """Stacks taller than 64 rows go through the shared-memory TSQR R factor; the per-slab
+    reconstruction U^L G^{L-1}..G^h must match the oracle's _recurse on identical input."""
+    p = bf.make_partition(n, leaf) if b == 2 else bf.make_quadtree_partition(int(round(n ** 0.5)), leaf)
+    m, side = p.mid_nodes, p.mid_side
+    rng = np.random.default_rng(n + r)
+    u_h = complex_gaussian(rng, (m, side, m * r))
+    u_h[:, :, :r] *= 1e-3                                  # a spread of column scales
+    leaf_o, pieces_o = ocons.recurse(u_h.reshape(m, side, m, r), n, p.levels, r, branching=b)
+    outer, chain = bf.recursive_factor_u(bf.BlockDiagonalFactor(u_h), p, r)
+
+    def recon(leaf_blocks, pieces):
+        full = bf.BlockDiagonalFactor(leaf_blocks).dense()
+        for lvl, blk in reversed(pieces):
+            full = full @ bf.TransferFactor(lvl, blk).dense()
+        return full
+
+    ro = recon(leaf_o, pieces_o)
+    rg = recon(outer.blocks.cpu().numpy(), [(t.level, t.blocks.cpu().numpy()) for t in chain])
+    assert rel(rg, ro) <= 1e-12

@@ -57,15 +57,17 @@ def main():
         ij = [(0, j) for j in range(m)]
         ms.blocks(ij)                                       # warm: workspace allocation, first launches
         t_mid, (u, v, w) = sync_time(lambda: ms.blocks(ij))
-        slab = u.permute(1, 0, 2).reshape(1, side, m, r)
+        kb = bc.recursion_batch(m, side, r)               # slabs per recursion launch (factorize's batching)
+        slab = u.permute(1, 0, 2).reshape(1, side, m, r).expand(kb, side, m, r).contiguous()
         bc.recurse(slab, p, r)
         t_rec, _ = sync_time(lambda: bc.recurse(slab, p, r))
         res["gpu_draw_tables_s"] = t_draws
         res["gpu_block_row_s"] = t_mid
-        res["gpu_slab_recursion_s"] = t_rec
-        res["gpu_factorize_s"] = t_draws + m * t_mid + 2 * m * t_rec
+        res["gpu_slab_batch"] = kb
+        res["gpu_slab_batch_recursion_s"] = t_rec
+        res["gpu_factorize_s"] = t_draws + m * t_mid + 2 * m / kb * t_rec
         res["method"] = (f"host draw tables (all blocks) + 1 block-row ({m} blocks) x{m} rows + "
-                         f"1 slab recursion x{2 * m} slabs (warm timings)")
+                         f"1 recursion of {kb} slabs x{2 * m // kb} batches (warm timings)")
     # CPU: the reference algorithm (oracle port) on a sample of middle blocks + one slab recursion
     from oracle import construct as ocons
     from oracle import entries as oent
