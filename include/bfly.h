@@ -196,6 +196,27 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
                      const int32_t* draws, void* u_out, void* v_out, double* w_out,
                      void* workspace, uint64_t ws_bytes, void* stream);
 
+/* Matvec-mode middle level (middle_factorization_matvec, construct.py:89-124;
+ * per block svd_from_probes, lowrank.py:204-216): the rank-r SVD of `nblocks`
+ * middle blocks finished from stored probe products only. All device,
+ * complex128 row-major:
+ *   k_cols (n x ldc) = K @ col_probe; block (i, j) reads rows [i side, (i+1) side),
+ *          columns [j width, (j+1) width)           (y_col = Z C)
+ *   k_rows (n x ldr) = K^H @ row_probe; block (i, j) reads rows [j side, ...),
+ *          columns [i width, ...)                    (y_row = Z* R)
+ *   row_probe (m, side, width): the diagonal blocks of the row probe (R).
+ * Per block: greedy pivots of y_col / y_row (k = width, rel_tol 0), the
+ * orthonormal bases of the pivot columns padded with canonical columns
+ * (orthonormal_columns, lowrank.py:132-154), mid = pinv_floored(R* Q_col)
+ * (y_row* Q_row), its SVD truncated to r (_assemble, lowrank.py:284-293).
+ * Outputs as bf_middle_blocks. Requires r <= width <= min(side, 128). */
+uint64_t bf_probe_workspace_bytes(uint64_t n, uint32_t levels, uint32_t branching, uint32_t rank, uint32_t width,
+                                  uint32_t nblocks);
+int bf_middle_probes(uint64_t n, uint32_t levels, uint32_t branching, uint32_t rank, uint32_t width,
+                     uint32_t nblocks, const int32_t* block_ij, const void* k_cols, uint64_t ldc,
+                     const void* k_rows, uint64_t ldr, const void* row_probe, void* u_out, void* v_out,
+                     double* w_out, void* workspace, uint64_t ws_bytes, void* stream);
+
 /* One level of _recurse (construct.py:127-163) with branching b (2; 4 on
  * quadtrees): cur (nb, rows, groups, r) complex128 -> transfer blocks
  * (nb, b, groups/b, r, b r) when rows >= b (SVD of each (rows/b x b r) stack;

@@ -6,10 +6,12 @@ from __future__ import annotations
 import numpy as np
 
 from .chain import Chain
-from .lowrank import Params, Triple, floored_inverse, sampling_svd
+from .lowrank import Params, Triple, complex_normal, floored_inverse, probe_svd, sampling_svd
 from .partition import level_geometry, node_range
 
 SAMPLING_DOMAIN = 0   # construct.py:26
+COL_PROBE_DOMAIN = 1  # construct.py:27
+ROW_PROBE_DOMAIN = 2  # construct.py:28
 
 
 def block_rng(seed, *key) -> np.random.Generator:
@@ -60,6 +62,56 @@ def middle_level(entry, n, levels, r, params=Params(), seed=0, branching=2):
     return u, w, v
 
 
+def probe_blocks(n: int, levels: int, r: int, width: int, seed, domain, branching: int = 2) -> np.ndarray:
+    """The diagonal blocks (m, side, width) of block_diagonal_probe (construct.py:78-86):
+    block j drawn from block_rng(seed, domain, j)."""
+    m, side = middle_geometry(n, levels, r, branching)
+    return np.stack([complex_normal(block_rng(seed, domain, j), (side, width)) for j in range(m)])
+
+
+def block_diagonal_probe(n: int, levels: int, r: int, width: int, seed, domain, branching: int = 2) -> np.ndarray:
+    """(n, m*width) probe, block j at rows j*side, columns j*width (construct.py:78-86)."""
+    blocks = probe_blocks(n, levels, r, width, seed, domain, branching)
+    m, side, _ = blocks.shape
+    probe = np.zeros((n, m * width), dtype=np.complex128)
+    for j in range(m):
+        probe[j * side:(j + 1) * side, j * width:(j + 1) * width] = blocks[j]
+    return probe
+
+
+def apply_chunked(apply_fn, block: np.ndarray, chunk: int = 128) -> np.ndarray:
+    """_apply_chunked (construct.py:71-75)."""
+    if block.shape[1] <= chunk:
+        return apply_fn(block)
+    return np.concatenate([apply_fn(block[:, c:c + chunk]) for c in range(0, block.shape[1], chunk)], axis=1)
+
+
+def middle_level_matvec(op, n, levels, r, params=Params(), seed=0, branching=2):
+    """U^h, W, V^h from black-box applies of K and K* (middle_factorization_matvec,
+    construct.py:89-124): one block-diagonal probe per side covers every block,
+    then each block's SVD is finished from the stored products (probe_svd)."""
+    m, side = middle_geometry(n, levels, r, branching)
+    width = min(r + params.p, side)
+    col_probe = block_diagonal_probe(n, levels, r, width, seed, COL_PROBE_DOMAIN, branching)
+    row_probe = block_diagonal_probe(n, levels, r, width, seed, ROW_PROBE_DOMAIN, branching)
+    k_cols = apply_chunked(op.apply, col_probe)
+    k_rows = apply_chunked(op.apply_adjoint, row_probe)
+    u = np.zeros((m, side, m, r), dtype=np.complex128)
+    v = np.zeros((m, side, m, r), dtype=np.complex128)
+    w = np.zeros((m, m, r))
+    for i in range(m):
+        rows = slice(i * side, (i + 1) * side)
+        r_block = row_probe[rows, i * width:(i + 1) * width]
+        for j in range(m):
+            cols = slice(j * side, (j + 1) * side)
+            t = probe_svd(k_cols[rows, j * width:(j + 1) * width], k_rows[cols, i * width:(i + 1) * width],
+                          r_block, r)
+            u[i, :, j, :] = t.u0 * t.sigma0
+            v[j, :, i, :] = t.v0 * t.sigma0
+            w[i, j] = floored_inverse(t.sigma0)
+    return u, w, v
+
+
 def recurse(cur: np.ndarray, n: int, levels: int, r: int, branching: int = 2):
     """Level-by-level batched SVD refactorization (construct.py:127-163).
 
@@ -97,12 +149,19 @@ def recurse(cur: np.ndarray, n: int, levels: int, r: int, branching: int = 2):
     return np.ascontiguousarray(cur[:, :, 0, :]), pieces
 
 
-def factorize(entry, n: int, levels: int, r: int, params=Params(), seed=0, branching: int = 2) -> Chain:
-    """Full sampling-mode construction (construct.py:184-213, mode="sampling"); branching 4 = quadtree."""
+def factorize(entry, n: int, levels: int, r: int, params=Params(), seed=0, branching: int = 2,
+              mode: str = "sampling") -> Chain:
+    """Full construction (construct.py:184-213): mode "sampling" (entry oracle; branching 4 =
+    quadtree) or "matvec" (operator oracle with .apply / .apply_adjoint on (n, k) arrays)."""
     if r < 1:
         raise ValueError(f"rank must be positive, got {r}")
     m, side = middle_geometry(n, levels, r, branching)
-    u, w, v = middle_level(entry, n, levels, r, params, seed, branching)
+    if mode == "matvec":
+        u, w, v = middle_level_matvec(entry, n, levels, r, params, seed, branching)
+    elif mode == "sampling":
+        u, w, v = middle_level(entry, n, levels, r, params, seed, branching)
+    else:
+        raise ValueError(f"unknown mode {mode!r}")
     u_leaf, g_levels = recurse(u.reshape(m, side, m, r), n, levels, r, branching)
     v_leaf, h_levels = recurse(v.reshape(m, side, m, r), n, levels, r, branching)
     return Chain(n, levels, r, u_leaf, g_levels, w, h_levels, v_leaf)

@@ -162,9 +162,47 @@ def gen_bfac(bf):
     print("bfac fixtures")
 
 
+def gen_matvec(bf):
+    """Matvec-mode construction (construct.py:89-124) on (a) a dense FIO operator and
+    (b) the composition K F K of a sampling-built chain (the paper's experiment):
+    probe products, per-block triples and the full factor chains."""
+    from butterfly.construct import _COL_PROBE_DOMAIN, _ROW_PROBE_DOMAIN, block_diagonal_probe
+    n, leaf, r, seed = 256, 1, 8, 4
+    p = bf.make_partition(n, leaf)
+    mat = bf.kernels.dense_matrix(bf.FioKernel(n), n)
+    op = bf.DenseOracle(mat)
+    f = bf.factorize(op, p, r, seed=seed, mode="matvec")
+    width = min(r + bf.lowrank.DEFAULT_PARAMS.p, p.mid_side)
+    d = {"n": n, "levels": p.levels, "rank": r, "seed": seed, "width": width}
+    d.update(_chain_arrays(f))
+    d["col_probe"] = block_diagonal_probe(p, width, seed, _COL_PROBE_DOMAIN)
+    d["row_probe"] = block_diagonal_probe(p, width, seed, _ROW_PROBE_DOMAIN)
+    u_h, mid, v_h = bf.middle_factorization_matvec(op, p, r, seed=seed)
+    d.update(u_h=u_h.blocks, v_h=v_h.blocks, w_h=mid.weights)
+    rng = np.random.default_rng(np.random.SeedSequence(seed, spawn_key=(4, 0)))
+    g = bf.lowrank.complex_normal(rng, (n, 2))
+    d.update(g=g, fwd=f.apply(g), adj=f.apply_adjoint(g))
+    np.savez_compressed(os.path.join(OUT, "matvec_dense_fio_n256_r8_leaf1.npz"), **d)
+    # composition: inner chain by sampling, composed operator, matvec chain
+    inner = bf.factorize(bf.FioKernel(n), p, r, seed=0)
+    comp = bf.ComposedOperator(inner)
+    f2 = bf.factorize(comp, p, r, seed=0, mode="matvec")
+    d = {"n": n, "levels": p.levels, "rank": r, "seed": 0}
+    d.update(_chain_arrays(inner, "inner_"))
+    d.update(_chain_arrays(f2))
+    d.update(g=g, comp_fwd=comp.apply(g), comp_adj=comp.apply_adjoint(g), fwd=f2.apply(g))
+    d["eps_a"] = bf.bench.estimate_eps_a(f2, bf.bench.OperatorReference(comp), 256,
+                                         np.random.SeedSequence(0, spawn_key=(4, 0)))
+    np.savez_compressed(os.path.join(OUT, "matvec_composed_fio_n256_r8_leaf1.npz"), **d)
+    print("matvec fixtures, composed eps_a", d["eps_a"])
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     bf = _ref()
+    if len(sys.argv) > 1 and sys.argv[1] == "matvec":
+        gen_matvec(bf)
+        return
     gen_bfac(bf)
     gen_geometry(bf)
     gen_entries(bf)
@@ -178,6 +216,7 @@ def main():
                   [(0, 0), (2, 5), (7, 3)])
     gen_construct(bf, "construct_fio_n1024_r8_leaf1.npz", bf.FioKernel(1024), 1024, 1, 8, 3,
                   [(0, 0), (17, 30)])
+    gen_matvec(bf)
 
 
 if __name__ == "__main__":

@@ -126,6 +126,22 @@ def assemble(mid, q_col, q_row, r) -> Triple:
                   complete_basis(q_row @ vhm[:t].conj().T, r))
 
 
+def complex_normal(rng: np.random.Generator, shape) -> np.ndarray:
+    """Independent N(0,1) real and imaginary parts, real block drawn first (lowrank.py:97-99)."""
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+def probe_svd(y_col, y_row, r_row, r) -> Triple:
+    """Rank-r SVD of a block from stored probe products only (svd_from_probes,
+    lowrank.py:204-216): y_col = Z C, y_row = Z* R and the row probe R; the
+    middle matrix solves R* Q_col M ~ y_row* Q_row in the floored least squares."""
+    width = min(y_col.shape[1], y_col.shape[0], y_row.shape[0])
+    q_col = pivoted_basis(y_col, width)
+    q_row = pivoted_basis(y_row, width)
+    mid = pinv_floored(r_row.conj().T @ q_col) @ (y_row.conj().T @ q_row)
+    return assemble(mid, q_col, q_row, r)
+
+
 def draw_tables(rng, m: int, n: int, r: int, params: Params = Params()):
     """The 8 RNG draws of one sampling SVD, in consumption order (lowrank.py:237-251).
 

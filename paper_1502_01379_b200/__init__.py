@@ -8,10 +8,12 @@ through the C ABI of include/bfly.h.
 from ._lib import OracleError
 from .factors import (BlockDiagonalFactor, ButterflyFactors, DevicePlan, MiddleFactor, NnzReport,
                       TransferFactor, factors_equal, from_arrays)
-from .construct import (DEFAULT_PARAMS, OversamplingParams, factorize, middle_factorization_sampling,
-                        recursive_factor_u, recursive_factor_v)
-from .kernels import DenseOracle, DftPlusKernel, FioKernel, Radon2DKernel, fio_entry
-from .metrics import RowSampledReference, estimate_eps_a, estimate_eps_a_info
+from .construct import (DEFAULT_PARAMS, OversamplingParams, block_diagonal_probe, factorize,
+                        middle_factorization_matvec, middle_factorization_sampling, recursive_factor_u,
+                        recursive_factor_v)
+from .kernels import (ComposedOperator, DenseOracle, DftPlusKernel, FioKernel, Radon2DKernel, composed_matvec,
+                      dft_apply, fio_entry)
+from .metrics import OperatorReference, RowSampledReference, estimate_eps_a, estimate_eps_a_info
 from .storage import FormatError, load_factors, read_vector, save_factors, write_vector
 from .partition import (BlockId, DyadicPartition, QuadtreePartition, block_cols, block_rows, level_geometry,
                         make_partition, make_quadtree_partition)

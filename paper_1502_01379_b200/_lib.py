@@ -39,6 +39,9 @@ SIGNATURES = [
     ("bf_timer_read", _I, [_P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(_U32), ctypes.POINTER(_U32)]),
     ("bf_middle_workspace_bytes", _U64, [_U64, _U32, _U32, _U32, _U32, _U32]),
     ("bf_middle_blocks", _I, [_I, _U64, _U32, _U32, _U32, _U32, _U32, _P, _U32, _P, _P, _P, _P, _P, _P, _U64, _P]),
+    ("bf_probe_workspace_bytes", _U64, [_U64, _U32, _U32, _U32, _U32, _U32]),
+    ("bf_middle_probes", _I, [_U64, _U32, _U32, _U32, _U32, _U32, _P, _P, _U64, _P, _U64, _P, _P, _P, _P, _P, _U64,
+                              _P]),
     ("bf_recurse_level", _I, [_U32, _U32, _U64, _U64, _U64, _P, _P, _P, _P, ctypes.POINTER(_U64), _P]),
     ("bf_select_pivots", _I, [_P, _U32, _U32, _U32, _U32, ctypes.c_double, _I, _P, _P, _P, _U64, _P]),
     ("bf_plan_create_sharded", _I, [ctypes.POINTER(_P), _U64, _U32, _U32, _I, _I, _U32, _U32]),

@@ -5,7 +5,10 @@ with every numeric stage in libbfly.so:
 * middle level: ``bf_middle_blocks`` — one CTA per block runs the randomized
   sampling SVD (lowrank.py:219-258) on entries evaluated on the device;
 * recursion: ``bf_recurse_level`` — batched SVD of the (rows/2 x 2r) stacks
-  (construct.py:127-163).
+  (construct.py:127-163);
+* matvec mode: probe products through the operator oracle (device-resident for
+  this package's own chains and ComposedOperator), then ``bf_middle_probes`` —
+  one CTA per block finishes svd_from_probes (lowrank.py:204-216).
 
 The host keeps only geometry and the random draws: each block's
 ``rng.choice`` draws come from the reference's own generator
@@ -29,7 +32,9 @@ from .factors import BlockDiagonalFactor, ButterflyFactors, MiddleFactor, Transf
 from .kernels import is_entry_oracle, is_operator_oracle
 from .partition import DyadicPartition, level_geometry
 
-SAMPLING_DOMAIN = 0  # construct.py:26
+SAMPLING_DOMAIN = 0   # construct.py:26
+COL_PROBE_DOMAIN = 1  # construct.py:27
+ROW_PROBE_DOMAIN = 2  # construct.py:28
 
 
 @dataclass(frozen=True)
@@ -165,6 +170,107 @@ class MiddleSampler:
         return max(1, min(self.m, max(1, 592 // self.m), by_mem))
 
 
+def complex_normal(rng: np.random.Generator, shape) -> np.ndarray:
+    """Independent N(0,1) real and imaginary parts, real block drawn first (lowrank.py:97-99)."""
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+def probe_blocks(p: DyadicPartition, width: int, seed, domain) -> np.ndarray:
+    """Diagonal blocks (m, side, width) of block_diagonal_probe (construct.py:78-86), drawn
+    on the host with the reference's generator block_rng(seed, domain, j) so the probes
+    are the reference's bit for bit."""
+    m, side = p.mid_nodes, p.mid_side
+    return np.stack([complex_normal(block_rng(seed, domain, j), (side, width)) for j in range(m)])
+
+
+def block_diagonal_probe(p: DyadicPartition, width: int, seed, domain) -> np.ndarray:
+    """(n, m*width) Gaussian probe with one (side x width) block per middle node (construct.py:78-86)."""
+    blocks = probe_blocks(p, width, seed, domain)
+    m, side, _ = blocks.shape
+    probe = np.zeros((p.n, m * width), dtype=np.complex128)
+    for j in range(m):
+        probe[j * side:(j + 1) * side, j * width:(j + 1) * width] = blocks[j]
+    return probe
+
+
+def _probe_products(op, blocks_d, p: DyadicPartition, width: int, adjoint: bool, chunk: int = 128):
+    """K @ probe (or K* @ probe) as a device (n, m*width) array, 128 probe columns per
+    application (_apply_chunked, construct.py:71-75). Device operators (ButterflyFactors,
+    ComposedOperator: ``accepts_device``) get device probes; any other operator oracle is
+    called on host chunks, the products uploaded."""
+    torch = _lib.require_cuda()
+    m, side = p.mid_nodes, p.mid_side
+    ncol = m * width
+    out = torch.empty((p.n, ncol), dtype=torch.complex128, device="cuda")
+    fn = op.apply_adjoint if adjoint else op.apply
+    on_device = bool(getattr(op, "accepts_device", False))
+    for c0 in range(0, ncol, chunk):
+        c1 = min(ncol, c0 + chunk)
+        probe = torch.zeros((p.n, c1 - c0), dtype=torch.complex128, device="cuda")
+        for j in range(c0 // width, (c1 - 1) // width + 1):
+            lo, hi = max(c0, j * width), min(c1, (j + 1) * width)
+            probe[j * side:(j + 1) * side, lo - c0:hi - c0] = blocks_d[j, :, lo - j * width:hi - j * width]
+        try:
+            if on_device:
+                y = fn(probe)
+            else:
+                y = torch.as_tensor(np.ascontiguousarray(fn(probe.cpu().numpy()), dtype=np.complex128)).cuda()
+        except Exception as exc:
+            raise _lib.OracleError("operator oracle failed on the probe block") from exc
+        out[:, c0:c1] = y
+    return out
+
+
+def middle_factorization_matvec(op, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0):
+    """U^h, M, V^h from black-box applications of K and K* (construct.py:89-124), device tensors.
+
+    One block-diagonal probe per side covers every middle block; each block's rank-r SVD is
+    then finished from the stored products on the device (``bf_middle_probes``: pivots,
+    bases, floored least squares and the middle SVD of svd_from_probes, lowrank.py:204-216)."""
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    m, side = p.mid_nodes, p.mid_side
+    if side < r:
+        raise ValueError(f"middle blocks are {side} wide, below rank {r}")
+    width = min(r + params.p, side)
+    branching = getattr(p, "branching", 2)
+    col_d = torch.as_tensor(probe_blocks(p, width, seed, COL_PROBE_DOMAIN)).cuda()
+    row_d = torch.as_tensor(probe_blocks(p, width, seed, ROW_PROBE_DOMAIN)).cuda().contiguous()
+    k_cols = _probe_products(op, col_d, p, width, adjoint=False)
+    k_rows = _probe_products(op, row_d, p, width, adjoint=True)
+    del col_d
+    u = torch.zeros((m, side, m, r), dtype=torch.complex128, device="cuda")
+    v = torch.zeros_like(u)
+    w = torch.zeros((m, m, r), dtype=torch.float64, device="cuda")
+    per_block = max(1, int(lib.bf_probe_workspace_bytes(p.n, p.levels, branching, r, width, 1)))
+    if int(lib.bf_probe_workspace_bytes(p.n, p.levels, branching, r, width, 1)) == 0:
+        raise ValueError(f"probe width {width} not supported by the batched probe kernels (<= 128)")
+    step_rows = max(1, min(m, (2 << 30) // (per_block * m)))
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for i0 in range(0, m, step_rows):
+        rows = range(i0, min(m, i0 + step_rows))
+        ij = np.array([(i, j) for i in rows for j in range(m)], dtype=np.int32)
+        nb = ij.shape[0]
+        ub = torch.empty((nb, side, r), dtype=torch.complex128, device="cuda")
+        vb = torch.empty_like(ub)
+        wb = torch.empty((nb, r), dtype=torch.float64, device="cuda")
+        ij_d = torch.from_numpy(ij).cuda()
+        wsb = int(lib.bf_probe_workspace_bytes(p.n, p.levels, branching, r, width, nb))
+        ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+        _lib.check(lib.bf_middle_probes(p.n, p.levels, branching, r, width, nb, ctypes.c_void_p(ij_d.data_ptr()),
+                                        ctypes.c_void_p(k_cols.data_ptr()), m * width,
+                                        ctypes.c_void_p(k_rows.data_ptr()), m * width,
+                                        ctypes.c_void_p(row_d.data_ptr()), ctypes.c_void_p(ub.data_ptr()),
+                                        ctypes.c_void_p(vb.data_ptr()), ctypes.c_void_p(wb.data_ptr()),
+                                        ctypes.c_void_p(ws.data_ptr()), wsb, stream), "bf_middle_probes")
+        k = len(rows)
+        u[i0:i0 + k] = ub.reshape(k, m, side, r).permute(0, 2, 1, 3)          # u[i, :, j, :]
+        v[:, :, i0:i0 + k, :] = vb.reshape(k, m, side, r).permute(1, 2, 0, 3)  # v[j, :, i, :]
+        w[i0:i0 + k] = wb.reshape(k, m, r)
+    return (BlockDiagonalFactor(u.reshape(m, side, m * r)), MiddleFactor(w),
+            BlockDiagonalFactor(v.reshape(m, side, m * r)))
+
+
 def recurse(cur, p: DyadicPartition, r: int):
     """_recurse (construct.py:127-163) on a device stack (nodes, rows, groups, r)."""
     torch = _lib.require_cuda()
@@ -201,6 +307,23 @@ def recursive_factor_u(u_h: BlockDiagonalFactor, p: DyadicPartition, r: int):
     cur = blocks.to(torch.complex128).reshape(p.mid_nodes, p.mid_side, p.mid_nodes, r)
     leaf, pieces = recurse(cur, p, r)
     return BlockDiagonalFactor(leaf), tuple(TransferFactor(lvl, b) for lvl, b in pieces)
+
+
+def _recurse_full(h: BlockDiagonalFactor, p: DyadicPartition, r: int):
+    """recursive_factor_u over the whole (m, side, m r) middle factor, slabs batched per
+    launch as in factorize (the reference recurses all m slabs at once, construct.py:171-176)."""
+    torch = _lib.require_cuda()
+    m, side = p.mid_nodes, p.mid_side
+    cur = h.blocks.reshape(m, side, m, r)
+    shapes, leaf_shape = level_geometry(p, r)
+    chain = {lvl: torch.zeros(shape, dtype=torch.complex128, device="cuda") for lvl, _, shape in shapes}
+    leaf = torch.zeros(leaf_shape, dtype=torch.complex128, device="cuda")
+    kb = recursion_batch(m, side, r)
+    for k0 in range(0, m, kb):
+        cnt = min(kb, m - k0)
+        leaf_k, pieces = recurse(cur[k0:k0 + cnt], p, r)
+        _place(chain, leaf, k0, cnt, leaf_k, pieces)
+    return BlockDiagonalFactor(leaf), tuple(TransferFactor(lvl, chain[lvl]) for lvl, _, _ in shapes)
 
 
 def recursive_factor_v(v_h: BlockDiagonalFactor, p: DyadicPartition, r: int):
@@ -251,7 +374,8 @@ def factorize(oracle, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0,
     mode="sampling"   entry oracle; every middle block sampled once (V^h held on the device);
     mode="streaming"  entry oracle; one middle block row/column at a time, O(n log n) memory,
                       each block sampled twice — bitwise identical to "sampling";
-    mode="matvec"     operator-oracle construction: not part of this hot path.
+    mode="matvec"     operator oracle (.apply / .apply_adjoint); block-diagonal probes, every
+                      block finished from the probe products on the device (construct.py:89-124).
     """
     if params is None:
         params = DEFAULT_PARAMS
@@ -259,14 +383,15 @@ def factorize(oracle, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0,
         raise ValueError(f"rank must be positive, got {r}")
     if mode in ("sampling", "streaming") and not is_entry_oracle(oracle):
         raise ValueError(f"mode={mode!r} needs an entry oracle")
-    if mode == "matvec":
-        if not is_operator_oracle(oracle):
-            raise ValueError("mode='matvec' needs an operator oracle")
-        raise NotImplementedError("mode='matvec' (probe construction) is outside the B200 hot path; "
-                                  "see DESIGN.md 'Out of scope'")
-    if mode not in ("sampling", "streaming"):
+    if mode == "matvec" and not is_operator_oracle(oracle):
+        raise ValueError("mode='matvec' needs an operator oracle")
+    if mode not in ("sampling", "streaming", "matvec"):
         raise ValueError(f"unknown mode {mode!r}")
     torch = _lib.require_cuda()
+    if mode == "matvec":
+        u_h, middle, v_h = middle_factorization_matvec(oracle, p, r, params, seed)
+        (u_outer, g_chain), (v_outer, h_chain) = (_recurse_full(u_h, p, r), _recurse_full(v_h, p, r))
+        return ButterflyFactors(p, r, u_outer, g_chain, middle, h_chain, v_outer)
     ms = MiddleSampler(oracle, p, r, params, seed)
     if ms.m * ms.m >= 1024:
         ms.prepare_draws()

@@ -52,6 +52,12 @@ struct MidArgs {
   double2* u_out;         // (nblocks, side, r)  u0 * sigma0
   double2* v_out;         // (nblocks, side, r)  v0 * sigma0
   double* w_out;          // (nblocks, r)        floored_inverse(sigma0)
+  // matvec mode (bf_middle_probes): probe width (0 = sampling mode) and the products
+  int probe_w;
+  const double2* kc;      // (n, ldc)  K @ col_probe
+  const double2* kr;      // (n, ldr)  K^H @ row_probe
+  const double2* rprobe;  // (m, side, probe_w) row-probe diagonal blocks
+  int64_t ldc, ldr;
 };
 
 enum { kRows = 0, kCols = 1 };
@@ -277,7 +283,9 @@ __global__ void __launch_bounds__(512) k_pivot_tall(MidArgs a, int which) {
   for (int c = threadIdx.x; c < nc; c += blockDim.x) {
     const double2* col = T + static_cast<int64_t>(c) * side;
     auto get = [&](int i) { return abs2(col[i]); };
-    norms[c] = which == kCols ? sequential_sum(get, side) : pairwise_sum(get, 0, side);
+    // np.sum over axis 0: sequential for C-ordered copies (entry(all, cols), and the
+    // probe products in matvec mode), pairwise for the F-ordered entry(rows, all)^H
+    norms[c] = (which == kCols || a.probe_w > 0) ? sequential_sum(get, side) : pairwise_sum(get, 0, side);
   }
   double2* chunk = tsm;                                           // kGramChunk x S
   const int64_t SS = static_cast<int64_t>(S) * S;
@@ -342,11 +350,13 @@ __global__ void __launch_bounds__(512) k_pivot_tall(MidArgs a, int which) {
   }
   __syncthreads();
   // ---- pivoted Cholesky recurrence == the greedy Gram-Schmidt pivoting
-  const int width = max(a.r, min(s.nrows, s.ncols) - a.r);
+  // sampling mode: k = min(width, side), rel_tol = BASIS_TRIM (lowrank.py:252-256);
+  // matvec mode: k = probe width, rel_tol = 0 (svd_from_probes, lowrank.py:213-214)
+  const int width = a.probe_w > 0 ? a.probe_w : max(a.r, min(s.nrows, s.ncols) - a.r);
   const int kmax = min(min(width, side), min(side, nc));
   double mx0 = 0.0;
   for (int c = 0; c < nc; ++c) mx0 = fmax(mx0, norms[c]);
-  const double floor_v = kBasisTrim * kBasisTrim * mx0;
+  const double floor_v = a.probe_w > 0 ? 0.0 : kBasisTrim * kBasisTrim * mx0;
   int npick = 0;
   for (int it = 0; it < kmax; ++it) {
     if (threadIdx.x == 0) {
@@ -625,6 +635,107 @@ __global__ void k_assemble(MidArgs a) {
     const int rho = threadIdx.x;
     a.w_out[static_cast<int64_t>(blockIdx.x) * r + rho] = rho < t ? floored_inv(sig[rho], smax) : 0.0;
   }
+}
+
+// ---------------------------------------------------------------- matvec mode
+// Probe product slices of block (i, j) into the tall buffer (side x width,
+// column-major): kCols y_col = k_cols[i side + row, j w + c], kRows y_row =
+// k_rows[j side + row, i w + c] (construct.py:114-118).
+__global__ void k_fill_probe(MidArgs a, int which) {
+  BlockState& s = a.st[blockIdx.x];
+  const int w = a.probe_w;
+  const int64_t bi = s.r0 / a.side, bj = s.c0 / a.side;
+  double2* T = a.tall + static_cast<int64_t>(blockIdx.x) * a.S * a.side;
+  const int64_t total = static_cast<int64_t>(w) * a.side;
+  for (int64_t x = blockIdx.y * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<int64_t>(gridDim.y) * blockDim.x) {
+    const int c = static_cast<int>(x / a.side);
+    const int64_t row = x - c * a.side;
+    T[x] = which == kCols ? a.kc[(bi * a.side + row) * a.ldc + bj * w + c]
+                          : a.kr[(bj * a.side + row) * a.ldr + bi * w + c];
+  }
+  if (blockIdx.y == 0 && threadIdx.x == 0) {
+    if (which == kCols)
+      s.ncols = w;
+    else
+      s.nrows = w;
+  }
+}
+
+// Basis input of orthonormal_columns(y, width) (lowrank.py:143-154): the pivot
+// columns in pick order, then canonical columns e_0, e_1, ... up to `width`.
+__global__ void k_sel_probe(MidArgs a, int which) {
+  BlockState& s = a.st[blockIdx.x];
+  const int w = a.probe_w;
+  const int npick = which == kCols ? s.tc : s.tr;
+  const int32_t* piv = which == kCols ? s.pivc : s.pivr;
+  const double2* T = a.tall + static_cast<int64_t>(blockIdx.x) * a.S * a.side;
+  double2* Q = (which == kCols ? a.qc : a.qr) + static_cast<int64_t>(blockIdx.x) * a.S * a.side;
+  const int64_t total = static_cast<int64_t>(w) * a.side;
+  for (int64_t x = blockIdx.y * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<int64_t>(gridDim.y) * blockDim.x) {
+    const int c = static_cast<int>(x / a.side);
+    const int64_t row = x - c * a.side;
+    Q[x] = c < npick ? T[static_cast<int64_t>(piv[c]) * a.side + row]
+                     : make_double2(row == c - npick ? 1.0 : 0.0, 0.0);
+  }
+}
+
+__global__ void k_set_probe_counts(MidArgs a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.nblocks) return;
+  a.st[b].tc = a.st[b].tr = a.probe_w;
+}
+
+// mid = pinv_floored(R* Q_col) (y_row* Q_row) and its SVD (svd_from_probes,
+// lowrank.py:215; _assemble 284-293). The tall buffer still holds y_row.
+__global__ void k_mid_probe(MidArgs a) {
+  extern __shared__ double2 sm2[];
+  __shared__ int flag, perm[kSetCap];
+  __shared__ double ssc[kSetCap], sg[kSetCap];
+  BlockState& s = a.st[blockIdx.x];
+  const int side = static_cast<int>(a.side), S = a.S, w = a.probe_w;
+  const int64_t bi = s.r0 / a.side;
+  const SmallBufs bb = small_bufs(a, sm2);
+  double2 *Mb = bb.Mb, *W = bb.W, *Vt = bb.Vt, *P1 = bb.P1;
+  const double2* QC = a.qc + static_cast<int64_t>(blockIdx.x) * S * a.side;
+  const double2* QR = a.qr + static_cast<int64_t>(blockIdx.x) * S * a.side;
+  const double2* YR = a.tall + static_cast<int64_t>(blockIdx.x) * S * a.side;
+  const double2* R = a.rprobe + bi * a.side * w;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // A1 = R^H Q_col into Mb, A2 = y_row^H Q_row into P2 (both w x w, ld S)
+  for (int pq = warp; pq < 2 * w * w; pq += nw) {
+    const bool second = pq >= w * w;
+    const int x = second ? pq - w * w : pq, ra = x / w, cb = x % w;
+    double2 acc = make_double2(0, 0);
+    for (int row = lane; row < side; row += 32) {
+      const double2 l = second ? YR[static_cast<int64_t>(ra) * side + row] : R[static_cast<int64_t>(row) * w + ra];
+      const double2 g = cmulc(l, second ? QR[static_cast<int64_t>(cb) * side + row]
+                                        : QC[static_cast<int64_t>(cb) * side + row]);
+      acc.x += g.x;
+      acc.y += g.y;
+    }
+    acc = warp_sum2(acc);
+    if (lane == 0) (second ? bb.P2 : Mb)[ra * S + cb] = acc;
+  }
+  __syncthreads();
+  pinv_small(Mb, w, w, S, P1, bb.sU, bb.sV, sg, W, Vt, &flag, perm, ssc, S);
+  // mid = P1 @ A2 into Mb
+  for (int x = threadIdx.x; x < w * w; x += blockDim.x) {
+    const int l = x / w, c = x % w;
+    double2 acc = make_double2(0, 0);
+    for (int k = 0; k < w; ++k) {
+      const double2 g = cmul(P1[l * S + k], bb.P2[k * S + c]);
+      acc.x += g.x;
+      acc.y += g.y;
+    }
+    Mb[l * S + c] = acc;
+  }
+  __syncthreads();
+  svd_small(Mb, w, w, S, bb.UM, S, bb.VM, S, sg, W, Vt, &flag, perm, ssc);
+  double* sig = a.sig + static_cast<int64_t>(blockIdx.x) * S;
+  for (int k = threadIdx.x; k < w; k += blockDim.x) sig[k] = sg[k];
+  if (threadIdx.x == 0) s.t = min(a.r, w);
 }
 
 // ---------------------------------------------------------------- recursion
@@ -1034,6 +1145,77 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
     }
     k_mid<<<nblocks, T, small_smem, st>>>(a);
   }
+  const unsigned yas = static_cast<unsigned>(std::min<uint64_t>(32, (side * rank + T - 1) / T));
+  k_assemble<<<dim3(nblocks, yas), T, 0, st>>>(a);
+  BF_CUDA(cudaGetLastError());
+  return BF_OK;
+}
+
+uint64_t bf_probe_workspace_bytes(uint64_t n, uint32_t levels, uint32_t branching, uint32_t rank, uint32_t width,
+                                  uint32_t nblocks) {
+  uint64_t m = 0, side = 0, off[8];
+  if (!tree_geometry(n, levels, branching, &m, &side)) return 0;
+  if (width < 1 || width > static_cast<uint32_t>(kSetCap)) return 0;
+  const int S = width <= static_cast<uint32_t>(kSmemSet) ? kSmemSet : kSetCap;
+  return mid_ws_layout(side, nblocks, S, off);
+}
+
+int bf_middle_probes(uint64_t n, uint32_t levels, uint32_t branching, uint32_t rank, uint32_t width,
+                     uint32_t nblocks, const int32_t* block_ij, const void* k_cols, uint64_t ldc,
+                     const void* k_rows, uint64_t ldr, const void* row_probe, void* u_out, void* v_out,
+                     double* w_out, void* workspace, uint64_t ws_bytes, void* stream) {
+  uint64_t m = 0, side = 0;
+  if (!tree_geometry(n, levels, branching, &m, &side)) return fail(BF_EINVAL, "bad partition geometry");
+  if (rank < 1 || side < rank) return fail(BF_EINVAL, "middle blocks are narrower than the rank");
+  if (width < rank || width > side || width > static_cast<uint32_t>(kSetCap))
+    return fail(BF_EINVAL, "probe width must satisfy r <= width <= min(side, 128)");
+  if (ldc < m * width || ldr < m * width) return fail(BF_EINVAL, "probe products narrower than m * width");
+  if (!nblocks) return BF_OK;
+  if (!block_ij || !k_cols || !k_rows || !row_probe || !u_out || !v_out || !w_out || !workspace)
+    return fail(BF_EINVAL, "null pointer");
+  const int S = width <= static_cast<uint32_t>(kSmemSet) ? kSmemSet : kSetCap;
+  uint64_t off[8];
+  if (ws_bytes < mid_ws_layout(side, nblocks, S, off)) return fail(BF_EINVAL, "probe workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(workspace);
+  MidArgs a{};
+  a.side = static_cast<int64_t>(side);
+  a.r = static_cast<int>(rank);
+  a.nblocks = static_cast<int>(nblocks);
+  a.S = S;
+  a.st = reinterpret_cast<BlockState*>(base + off[0]);
+  a.wide = reinterpret_cast<double2*>(base + off[1]);
+  a.tall = reinterpret_cast<double2*>(base + off[2]);
+  a.qc = reinterpret_cast<double2*>(base + off[3]);
+  a.qr = reinterpret_cast<double2*>(base + off[4]);
+  a.qbuf = reinterpret_cast<double2*>(base + off[5]);
+  a.scr = reinterpret_cast<double2*>(base + off[6]);
+  a.sig = reinterpret_cast<double*>(base + off[7]);
+  a.u_out = static_cast<double2*>(u_out);
+  a.v_out = static_cast<double2*>(v_out);
+  a.w_out = w_out;
+  a.probe_w = static_cast<int>(width);
+  a.kc = static_cast<const double2*>(k_cols);
+  a.kr = static_cast<const double2*>(k_rows);
+  a.rprobe = static_cast<const double2*>(row_probe);
+  a.ldc = static_cast<int64_t>(ldc);
+  a.ldr = static_cast<int64_t>(ldr);
+  const int T = 256;
+  const unsigned yfill = static_cast<unsigned>(std::min<uint64_t>(64, (width * side + T - 1) / T));
+  const size_t small_smem = S <= kSmemSet ? 3ull * S * S * sizeof(double2) : 0;
+  const size_t tall_smem = (static_cast<size_t>(kGramChunk) * S + (S <= kSmemSet ? 2ull * S * S : 0)) * 16;
+  BF_CUDA(cudaFuncSetAttribute(k_mid_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(small_smem)));
+  BF_CUDA(cudaFuncSetAttribute(k_pivot_tall, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(tall_smem)));
+  k_init<<<(nblocks + 127) / 128, 128, 0, st>>>(a, block_ij);
+  for (int which : {kCols, kRows}) {
+    k_fill_probe<<<dim3(nblocks, yfill), T, 0, st>>>(a, which);
+    k_pivot_tall<<<nblocks, 512, tall_smem, st>>>(a, which);
+    k_sel_probe<<<dim3(nblocks, yfill), T, 0, st>>>(a, which);
+  }
+  k_set_probe_counts<<<(nblocks + 127) / 128, 128, 0, st>>>(a);
+  for (int which : {kCols, kRows}) k_cgs2<<<nblocks, 512, 0, st>>>(a, which);
+  k_mid_probe<<<nblocks, T, small_smem, st>>>(a);
   const unsigned yas = static_cast<unsigned>(std::min<uint64_t>(32, (side * rank + T - 1) / T));
   k_assemble<<<dim3(nblocks, yas), T, 0, st>>>(a);
   BF_CUDA(cudaGetLastError());

@@ -334,6 +334,7 @@ class ButterflyFactors:
     h_chain: tuple
     v_outer: BlockDiagonalFactor
     _plans: dict = field(default_factory=dict, compare=False, repr=False)
+    accepts_device = True   # operator-oracle protocol: apply() takes torch CUDA tensors too
 
     @property
     def n(self) -> int:

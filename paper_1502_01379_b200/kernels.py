@@ -7,6 +7,11 @@
   reference has no such class (its DftKernel is centered and negative-sign,
   kernels.py:87-97).
 * ``DenseOracle`` — an explicit matrix (reference oracles.py:39-54).
+* ``ComposedOperator`` — K F K around a factored chain, the operator oracle of
+  the paper's composition experiment (reference kernels.py:129-150); with
+  ``dft_apply`` (kernels.py:100-112). Accepts NumPy arrays (host result) or
+  torch CUDA tensors (device result: the chain applies run in libbfly.so and
+  the FFT in cuFFT), so the matvec construction never leaves the device.
 
 ``block`` evaluates on the GPU through ``bf_entries`` (libbfly.so) and
 returns a NumPy array; ``DenseOracle.block`` is a plain lookup.
@@ -89,6 +94,69 @@ class DenseOracle:
 
     def apply_adjoint(self, x):
         return self.matrix.conj().T @ x
+
+
+def _is_device(x) -> bool:
+    return hasattr(x, "is_cuda") and x.is_cuda
+
+
+def dft_apply(n: int, g, direction: str = "forward"):
+    """Centered DFT (or its inverse) with the (-1)^j modulation (reference kernels.py:100-112).
+    NumPy in -> NumPy out; torch CUDA in -> torch CUDA out (cuFFT)."""
+    if direction not in ("forward", "inverse"):
+        raise ValueError(f"unknown direction {direction!r}")
+    if _is_device(g):
+        import torch
+        if g.shape[0] != n:
+            raise ValueError(f"input length {g.shape[0]} != {n}")
+        g = g.to(torch.complex128)
+        signs = torch.where(torch.arange(n, device=g.device) % 2 == 0, 1.0, -1.0).to(torch.float64)
+        if g.ndim > 1:
+            signs = signs[:, None]
+        if direction == "forward":
+            return torch.fft.fft(signs * g, dim=0)
+        return signs * torch.fft.ifft(g, dim=0)
+    g = np.asarray(g, dtype=np.complex128)
+    if g.shape[0] != n:
+        raise ValueError(f"input length {g.shape[0]} != {n}")
+    signs = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    if g.ndim > 1:
+        signs = signs[:, None]
+    if direction == "forward":
+        return np.fft.fft(signs * g, axis=0)
+    return signs * np.fft.ifft(g, axis=0)
+
+
+class ComposedOperator:
+    """K F K as a black-box operator: two factored applies around an FFT
+    (reference kernels.py:129-150)."""
+
+    accepts_device = True
+
+    def __init__(self, k_factors):
+        self.k_factors = k_factors
+
+    @property
+    def n(self) -> int:
+        return self.k_factors.n
+
+    @property
+    def shape(self):
+        return (self.n, self.n)
+
+    def apply(self, x):
+        k = self.k_factors
+        return k.apply(dft_apply(self.n, k.apply(x), "forward"))
+
+    def apply_adjoint(self, x):
+        k = self.k_factors
+        inner = dft_apply(self.n, k.apply_adjoint(x), "inverse") * self.n
+        return k.apply_adjoint(inner)
+
+
+def composed_matvec(c: ComposedOperator, g, adjoint: bool = False):
+    """reference kernels.py:153-154."""
+    return c.apply_adjoint(g) if adjoint else c.apply(g)
 
 
 def is_entry_oracle(oracle) -> bool:

@@ -46,6 +46,19 @@ class RowSampledReference:
         return res[:, 0] if vec else res
 
 
+class OperatorReference:
+    """Ground truth from a fast black-box operator, e.g. a ComposedOperator (bench.py:60-72)."""
+
+    def __init__(self, op):
+        self.op = op
+
+    def rows(self, g, sample):
+        out = self.op.apply(g)
+        if hasattr(out, "is_cuda"):
+            out = out.cpu().numpy()
+        return np.asarray(out)[sample]
+
+
 def sampled_relative_error(u_approx, u_exact):
     """(error, used_absolute_fallback) of the sampled l2 ratio metric (bench.py:75-81)."""
     diff = float(np.linalg.norm(u_approx - u_exact))

@@ -19,13 +19,14 @@ def golden(name):
     return dict(np.load(os.path.join(GOLDEN, name), allow_pickle=False))
 
 
-def chain_from_golden(d):
+def chain_from_golden(d, prefix=""):
     from oracle.chain import Chain
-    g_lvls = [int(x) for x in d["g_lvls"]]
-    h_lvls = [int(x) for x in d["h_lvls"]]
-    return Chain(int(d["n"]), int(d["levels"]), int(d["rank"]), d["u_leaf"],
-                 [(l, d[f"g_{l}"]) for l in g_lvls], d["weights"],
-                 [(l, d[f"h_{l}"]) for l in h_lvls], d["v_leaf"])
+    p = prefix
+    g_lvls = [int(x) for x in d[p + "g_lvls"]]
+    h_lvls = [int(x) for x in d[p + "h_lvls"]]
+    return Chain(int(d[p + "n"]), int(d[p + "levels"]), int(d[p + "rank"]), d[p + "u_leaf"],
+                 [(l, d[f"{p}g_{l}"]) for l in g_lvls], d[p + "weights"],
+                 [(l, d[f"{p}h_{l}"]) for l in h_lvls], d[p + "v_leaf"])
 
 
 def complex_gaussian(rng, shape):
