@@ -18,7 +18,8 @@ sys.path.insert(0, ROOT)
 import paper_1502_01379_b200 as bf  # noqa: E402
 from paper_1502_01379_b200 import construct as bc  # noqa: E402
 
-CFG = {"cfg0": ("fio", 1 << 10, 12, 8), "cfg1": ("dftp", 1 << 16, 8, 16), "cfg2": ("fio", 1 << 20, 16, 16)}
+CFG = {"cfg0": ("fio", 1 << 10, 12, 8), "cfg1": ("dftp", 1 << 16, 8, 16), "cfg2": ("fio", 1 << 20, 16, 16),
+       "comp1024": ("fio", 1 << 10, 12, 0.25)}
 
 
 def kernel(kind, n):
@@ -33,12 +34,49 @@ def sync_time(fn):
     return time.perf_counter() - t0, out
 
 
+def bench_matvec(args):
+    """matvec mode on the composition operator K F K (the paper's experiment,
+    reference test_acceptance.py:75-96): inner chain K by the GPU sampling
+    construction (untimed), then factorize(ComposedOperator(K), mode="matvec")
+    timed on the GPU and through the oracle port (== reference, bitwise) on the CPU."""
+    from oracle import chain as ochain
+    from oracle import construct as ocons
+    from oracle import operators as oops
+    from paper_1502_01379_b200.synthetic import to_host
+    kind, n, r, leaf = CFG[args.config]
+    p = bf.make_partition(n, leaf)
+    inner = bf.factorize(kernel(kind, n), p, r, seed=7)
+    comp = bf.ComposedOperator(inner)
+    bf.factorize(comp, p, r, seed=0, mode="matvec")          # warm-up
+    t, f = sync_time(lambda: bf.factorize(comp, p, r, seed=0, mode="matvec"))
+    eps = bf.estimate_eps_a(f, bf.OperatorReference(comp), 256, np.random.SeedSequence(0, spawn_key=(4, 0)))
+    h = to_host(inner)
+    chain = ochain.Chain(n, p.levels, r, h.u_outer.blocks, [(x.level, x.blocks) for x in h.g_chain],
+                         h.middle.weights, [(x.level, x.blocks) for x in h.h_chain], h.v_outer.blocks)
+    t0 = time.perf_counter()
+    c = ocons.factorize(oops.Composed(chain), n, p.levels, r, seed=0, mode="matvec")
+    t_cpu = time.perf_counter() - t0
+    rng = np.random.default_rng(3)
+    g = rng.standard_normal((n, 2)) + 1j * rng.standard_normal((n, 2))
+    want = ochain.apply(c, g)
+    got = f.apply(g)
+    res = {"config": args.config, "mode": "matvec", "operator": "ComposedOperator(K F K)", "n": n, "r": r,
+           "levels": p.levels, "gpu_factorize_s": t, "cpu_factorize_s": t_cpu,
+           "cpu_method": f"oracle port (== reference bitwise), cores={os.cpu_count()}",
+           "speedup": t_cpu / t, "eps_a": eps,
+           "rel_vs_oracle_chain": float(np.linalg.norm(got - want) / np.linalg.norm(want))}
+    print(json.dumps(res))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config", choices=sorted(CFG))
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--cpu-blocks", type=int, default=4)
+    ap.add_argument("--mode", choices=["sampling", "matvec"], default="sampling")
     args = ap.parse_args()
+    if args.mode == "matvec":
+        return bench_matvec(args)
     kind, n, r, leaf = CFG[args.config]
     p = bf.make_partition(n, leaf)
     m, side = p.mid_nodes, p.mid_side
