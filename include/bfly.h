@@ -172,6 +172,16 @@ int bf_plan_export(const bf_plan* plan, int which, uint32_t level, void* dst, ui
 int bf_entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr,
                const int64_t* cols, uint32_t nc, void* out, void* stream);
 
+/* Hankel-kernel rows (HankelKernel, kernels.py:45-84; hankel1_orders,
+ * bessel.py:178-230): out[t, m] = H1_m(x[t]) = J_m + i Y_m for m = 0..max_order,
+ * complex128 rows of stride ld. x: device float64 (nx), all > 0. start: the
+ * backward-recurrence start the reference computes for this batch,
+ * int(max(x + 10 cbrt(x) + 40)) but at least max_order + 15 (host-computed, so
+ * the J sweep is bit-identical to the reference's). Synchronises `stream` (it
+ * reports invalid x). */
+int bf_hankel_orders(const double* x, uint32_t nx, uint32_t max_order, int64_t start, void* out, uint64_t ld,
+                     void* stream);
+
 /* ---------------------------------------------------------------------------
  * Sampling construction (construct.py:43-68, lowrank.py:219-258, construct.py:127-163).
  *

@@ -38,13 +38,48 @@ class EntryOracle:
     """``.shape`` + ``.block(rows, cols)`` — the reference entry-oracle protocol (oracles.py:5-10)."""
 
     def __init__(self, kind: str, n: int):
-        if kind not in ("fio", "dftp"):
+        if kind not in ("fio", "dftp", "hankel"):
             raise ValueError(f"unknown kernel {kind!r}")
         self.kind, self.n, self.shape = kind, n, (n, n)
+        if kind == "hankel":
+            self._hk = HankelOracle(n)
 
     def block(self, rows, cols):
+        if self.kind == "hankel":
+            return self._hk.block(rows, cols)
         fn = fio_block if self.kind == "fio" else dftp_block
         return fn(self.n, rows, cols)
+
+
+class HankelOracle:
+    """HankelKernel (kernels.py:45-84): H1_j(x_i), x_i = n + (2 pi/3) i. For n <= 4096
+    rows are cached, missing rows swept in sorted batches of 256 to order n-1 (so a
+    row's last bits depend on which rows it was swept with, as in the reference);
+    above, every call sweeps its rows to order max(cols)."""
+
+    CACHE_CAP = 4096   # kernels.py:20
+
+    def __init__(self, n: int, cache=None):
+        self.n, self.shape = n, (n, n)
+        self._cache = n <= self.CACHE_CAP if cache is None else cache
+        self._rows = {}
+
+    def block(self, rows, cols):
+        from .bessel import hankel1_orders, hankel_points
+        rows = np.asarray(rows, dtype=np.intp)
+        cols = np.asarray(cols, dtype=np.intp)
+        if not self._cache:
+            return np.ascontiguousarray(hankel1_orders(hankel_points(self.n, rows), int(cols.max(initial=0)))[:, cols])
+        missing = sorted(set(int(i) for i in rows) - self._rows.keys())
+        for lo in range(0, len(missing), 256):
+            batch = missing[lo:lo + 256]
+            table = hankel1_orders(hankel_points(self.n, batch), self.n - 1)
+            for b, i in enumerate(batch):
+                self._rows[i] = table[b]
+        out = np.empty((rows.size, cols.size), dtype=np.complex128)
+        for a, i in enumerate(rows):
+            out[a] = self._rows[int(i)][cols]
+        return out
 
 
 def morton_decode(z, bits: int):

@@ -197,11 +197,39 @@ def gen_matvec(bf):
     print("matvec fixtures, composed eps_a", d["eps_a"])
 
 
+def gen_hankel(bf):
+    """Bessel seeds, an order sweep, rows of the cached HankelKernel(1024) table and the
+    criterion-2 accuracy of the reference's own sampling construction on it."""
+    from butterfly import bessel as rb
+    d = {}
+    xs = np.concatenate([np.linspace(0.05, 5.0, 311), np.linspace(5.001, 2e4, 311)])
+    d["seed_x"] = xs
+    d["j0"], d["j1"], d["y0"], d["y1"] = rb.bessel_j0(xs), rb.bessel_j1(xs), rb.bessel_y0(xs), rb.bessel_y1(xs)
+    x = 256 + (2 * np.pi / 3) * np.arange(0, 256, 37, dtype=float)
+    d["sweep_x"], d["sweep"] = x, rb.hankel1_orders(x, 255)
+    n = 1024
+    ker = bf.HankelKernel(n)
+    rows = np.arange(0, n, 61)
+    d["table_n"], d["table_rows"] = n, rows
+    d["table"] = ker.block(np.arange(n), np.arange(n))[rows]
+    d["entry_64_3_5"] = bf.kernels.hankel_entry(64, 3, 5)
+    p = bf.make_partition(n, 0.25)
+    for r in (4, 6):
+        f = bf.factorize(ker, p, r, seed=0, mode="sampling")
+        d[f"eps_r{r}"] = bf.bench.estimate_eps_a(f, bf.bench.RowSampledReference(ker), 256,
+                                                 np.random.SeedSequence(0, spawn_key=(4, 0)))
+    np.savez_compressed(os.path.join(OUT, "hankel.npz"), **d)
+    print("hankel.npz eps", d["eps_r4"], d["eps_r6"])
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     bf = _ref()
     if len(sys.argv) > 1 and sys.argv[1] == "matvec":
         gen_matvec(bf)
+        return
+    if len(sys.argv) > 1 and sys.argv[1] == "hankel":
+        gen_hankel(bf)
         return
     gen_bfac(bf)
     gen_geometry(bf)
@@ -217,6 +245,7 @@ def main():
     gen_construct(bf, "construct_fio_n1024_r8_leaf1.npz", bf.FioKernel(1024), 1024, 1, 8, 3,
                   [(0, 0), (17, 30)])
     gen_matvec(bf)
+    gen_hankel(bf)
 
 
 if __name__ == "__main__":

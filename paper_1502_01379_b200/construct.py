@@ -21,13 +21,16 @@ reference (pkg/tests/test_construct.py:197-202).
 from __future__ import annotations
 
 import ctypes
+import multiprocessing
 import os
+import warnings
 from concurrent.futures import ProcessPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _lib
+from ._draws import block_rng, draws_for
 from .factors import BlockDiagonalFactor, ButterflyFactors, MiddleFactor, TransferFactor
 from .kernels import is_entry_oracle, is_operator_oracle
 from .partition import DyadicPartition, level_geometry
@@ -53,19 +56,7 @@ class OversamplingParams:
 DEFAULT_PARAMS = OversamplingParams()
 
 
-def block_rng(seed, *key) -> np.random.Generator:
-    """Independent generator for one construction sub-task (construct.py:31-33)."""
-    return np.random.default_rng(np.random.SeedSequence(seed, spawn_key=key))
-
-
-def _draws_for(args):
-    seed, side, rqs, iters, blocks = args
-    out = np.empty((len(blocks), 2 * (iters + 1), rqs), dtype=np.int32)
-    for b, (i, j) in enumerate(blocks):
-        rng = block_rng(seed, SAMPLING_DOMAIN, int(i), int(j))
-        for s in range(2 * (iters + 1)):  # row, col, row, col, ... (lowrank.py:237-251)
-            out[b, s] = rng.choice(side, size=rqs, replace=False)
-    return out
+_draws_for = draws_for
 
 
 def draw_tables(seed, side: int, r: int, params: OversamplingParams, blocks) -> np.ndarray:
@@ -76,8 +67,13 @@ def draw_tables(seed, side: int, r: int, params: OversamplingParams, blocks) -> 
         return _draws_for((seed, side, rqs, params.iters, blocks))
     workers = min(16, os.cpu_count() or 1)
     chunks = [blocks[k::workers] for k in range(workers)]
-    with ProcessPoolExecutor(workers) as ex:
-        parts = list(ex.map(_draws_for, [(seed, side, rqs, params.iters, c) for c in chunks]))
+    # fork workers: they run NumPy only (never CUDA) on their own block lists. "spawn" /
+    # "forkserver" would re-execute the caller's __main__ script in every worker.
+    with warnings.catch_warnings():
+        warnings.filterwarnings("ignore", message=".*use of fork\\(\\) may lead to deadlocks.*",
+                                category=DeprecationWarning)
+        with ProcessPoolExecutor(workers, mp_context=multiprocessing.get_context("fork")) as ex:
+            parts = list(ex.map(_draws_for, [(seed, side, rqs, params.iters, c) for c in chunks]))
     out = np.empty((len(blocks), 2 * (params.iters + 1), rqs), dtype=np.int32)
     for k, part in enumerate(parts):
         out[k::workers] = part
@@ -94,6 +90,14 @@ class _DeviceOracle:
         name = type(oracle).__name__
         if kid in (_lib.BF_KERNEL_FIO, _lib.BF_KERNEL_DFTP, _lib.BF_KERNEL_RADON2D):
             self.kernel_id = kid
+        elif hasattr(oracle, "device_table"):
+            # entry tables built on the device (HankelKernel): read as a dense source
+            self.dense = oracle.device_table()
+            self.kernel_id = _lib.BF_KERNEL_DENSE
+        elif name == "HankelKernel" and getattr(oracle, "n", None) == n:  # the reference's own class
+            from .kernels import HankelKernel
+            self.dense = HankelKernel(n, cache=True).device_table()
+            self.kernel_id = _lib.BF_KERNEL_DENSE
         elif name == "FioKernel" and getattr(oracle, "n", None) == n:   # the reference's own class
             self.kernel_id = _lib.BF_KERNEL_FIO
         else:

@@ -73,6 +73,87 @@ class Radon2DKernel(_DeviceKernel):
         self.n_side = int(n_side)
 
 
+def sweep_start(x, max_order: int) -> int:
+    """Backward-recurrence start of a batch of points, as the reference computes it
+    (bessel.py:196-197): int(max(x + 10 cbrt(x) + 40)), at least max_order + 15."""
+    x = np.atleast_1d(np.asarray(x, dtype=float))
+    return max(int(np.max(x + 10.0 * np.cbrt(x) + 40.0)), int(max_order) + 15)
+
+
+def hankel1_orders_device(x, max_order: int, out=None):
+    """H1_m(x), m = 0..max_order, for a batch of points on the device (bf_hankel_orders):
+    the reference's hankel1_orders (bessel.py:225-230) with the batch's own start.
+    x: NumPy float64 (nx,). Returns a torch CUDA (nx, max_order + 1) complex128 tensor."""
+    torch = _lib.require_cuda()
+    x = np.atleast_1d(np.asarray(x, dtype=np.float64))
+    if (x <= 0).any():
+        raise ValueError("order sweep requires x > 0")
+    if out is None:
+        out = torch.empty((x.size, max_order + 1), dtype=torch.complex128, device="cuda")
+    xd = torch.as_tensor(x).cuda()
+    _lib.check(_lib.load().bf_hankel_orders(ctypes.c_void_p(xd.data_ptr()), x.size, int(max_order),
+                                            sweep_start(x, max_order), ctypes.c_void_p(out.data_ptr()),
+                                            out.stride(0), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+               "bf_hankel_orders")
+    return out
+
+
+class HankelKernel:
+    """K[i, j] = H1_j(x_i), x_i = n + (2 pi / 3) i (reference kernels.py:45-84), on the device.
+
+    Cached (n <= TABLE_CAP, the default): the whole n x n table is built once on the
+    device, sorted rows in batches of 256 with one order sweep each — exactly how the
+    reference's row cache fills from empty on block(arange(n), arange(n)) — and the
+    construction reads it as a dense entry source. Uncached: each block() call sweeps
+    its own rows to order max(cols), as the reference's uncached path does."""
+
+    TABLE_CAP = 1 << 15   # 16 GiB of complex128 table
+
+    def __init__(self, n: int, cache: bool | None = None):
+        self.n = int(n)
+        self.shape = (self.n, self.n)
+        self._cache = self.n <= self.TABLE_CAP if cache is None else bool(cache)
+        self._table = None
+
+    def point(self, i: int) -> float:
+        return self.n + (2.0 * np.pi / 3.0) * i
+
+    def points(self, rows) -> np.ndarray:
+        return self.n + (2.0 * np.pi / 3.0) * np.asarray(rows, dtype=np.intp).astype(float)
+
+    def device_table(self):
+        """The (n, n) complex128 table on the device (built on first use)."""
+        if self._table is None:
+            torch = _lib.require_cuda()
+            n = self.n
+            table = torch.empty((n, n), dtype=torch.complex128, device="cuda")
+            for lo in range(0, n, 256):
+                hi = min(n, lo + 256)
+                hankel1_orders_device(self.points(np.arange(lo, hi)), n - 1, out=table[lo:hi])
+            self._table = table
+        return self._table
+
+    def block(self, rows, cols) -> np.ndarray:
+        torch = _lib.require_cuda()
+        rows = np.asarray(rows, dtype=np.intp).reshape(-1)
+        cols = np.asarray(cols, dtype=np.intp).reshape(-1)
+        if rows.size == 0 or cols.size == 0:
+            return np.zeros((rows.size, cols.size), dtype=np.complex128)
+        if self._cache:
+            t = self.device_table()
+            r = torch.as_tensor(rows).cuda()
+            c = torch.as_tensor(cols).cuda()
+            return t[r][:, c].cpu().numpy()
+        table = hankel1_orders_device(self.points(rows), int(cols.max(initial=0)))
+        return table[:, torch.as_tensor(cols).cuda()].cpu().numpy()
+
+
+def hankel_entry(n: int, i: int, j: int) -> complex:
+    """H1_j(x_i) by one sweep at the single point (reference kernels.py:82-84)."""
+    x = n + (2.0 * np.pi / 3.0) * i
+    return complex(hankel1_orders_device(np.array([x]), j)[0, j].item())
+
+
 def fio_entry(n: int, i: int, j: int) -> complex:
     return complex(FioKernel(n).block([i], [j])[0, 0])
 
