@@ -353,6 +353,16 @@ def run_sharded(args, world, rank, local):
     dist.destroy_process_group()
 
 
+def _ncu_traffic(config, dtype, k):
+    """dram__bytes_read.sum + dram__bytes_write.sum per level-kernel launch from the committed
+    `ncu --set full` capture of this workload (profiles/r01_level_kernel_traffic.json), else None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_level_kernel_traffic.json")
+    if (config, dtype, k) != ("cfg2", "c128", 1) or not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        return json.load(fh).get("traffic_bytes_per_launch")
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -510,7 +520,8 @@ def main():
                        "l2": "inputs larger than L2: each step streams "
                              f"{alg_bytes / 1e9:.2f} GB of factors (L2 126 MB)"},
             "roofline": {"bound": "hbm", "achieved": tr_bytes / (tr_ms / 1e3) / 1e9, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": tr_bytes / (tr_ms / 1e3) / 1e9 / hbm_peak, "traffic": None,
+                         "unit": "GB/s", "frac": tr_bytes / (tr_ms / 1e3) / 1e9 / hbm_peak,
+                         "traffic": _ncu_traffic(args.config, args.dtype, k),
                          "kernel": "level_kernel (transfer levels G/H)", "kernel_share_of_step": share,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
             "chain_roofline": {"algorithmic_bytes": alg_bytes, "algorithmic_flops": alg_flops,
