@@ -59,6 +59,16 @@ constexpr Shape kStream{3, 2, 2, 34 * 1024 + 512};
 constexpr Shape kMrhs{2, 8, 1, 100 * 1024};
 constexpr uint32_t kMrhsMinK = 8;
 
+// Programmatic dependent launch between consecutive level kernels (the next
+// level's prologue overlaps the previous one's tail); BF_NO_PDL=1 turns it off.
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BF_NO_PDL");
+    return !(e && *e && *e != '0');
+  }();
+  return on;
+}
+
 template <typename E>
 int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint32_t ntot, uint32_t t0,
                    int accumulate, uint64_t P, uint64_t units, const void* in, void* out, uint32_t k, int adjoint,
@@ -158,8 +168,17 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const uint64_t per_sm = smem * sh.ctas_per_sm <= 227 * 1024 ? sh.ctas_per_sm : 1;
   const uint64_t grid = std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(pl.sms) * per_sm);
-  kern<<<static_cast<unsigned>(grid), (sh.ncw + 1) * 32, smem, st>>>(a);
-  BF_CUDA(cudaGetLastError());
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3((sh.ncw + 1) * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BF_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   return 0;
 }
 

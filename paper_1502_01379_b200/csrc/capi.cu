@@ -454,7 +454,11 @@ int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint
     run = plan->own_stream;
   }
   // large transfers: pipeline H2D/D2H chunks (per middle-node range) against the chain
-  const uint32_t chunks = p.m >= 8 ? 8 : 1;
+  uint32_t chunks = p.m >= 4 ? 4 : 1;  // measured best at cfg2 (tools/e2e_probe.py: 1 2.11 ms, 4 1.86, 8 1.98, 16 2.49)
+  if (const char* env = getenv("BF_PIPE_CHUNKS")) {  // tuning knob: power of two <= m
+    const long v = strtol(env, nullptr, 10);
+    if (v >= 1 && v <= static_cast<long>(p.m) && (v & (v - 1)) == 0) chunks = static_cast<uint32_t>(v);
+  }
   // (graph capture of a memcpy needs page-locked host memory)
   auto pinned = [](const void* ptr) {
     cudaPointerAttributes at{};

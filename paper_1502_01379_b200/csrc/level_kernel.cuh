@@ -572,6 +572,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) level_kernel(const Level
     fence_mbar_init();
   }
   __syncthreads();
+  // programmatic dependent launch: let the next level's CTAs launch as ours retire
+  // (they wait below), and wait for the previous level to finish and flush before
+  // touching its output (our input) or its input (our output buffer). Both are
+  // no-ops when the launch carries no programmatic-serialization attribute.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (warp == NCW) {
     const uint64_t pol = policy_evict_first();
     uint32_t it = 0;
