@@ -149,31 +149,33 @@ __device__ __forceinline__ void stage_rows(E* dst, const E* src, uint32_t rows, 
   }
 }
 
+// Factor part of a tile (bulk path): arm the stage barrier with the whole tile's
+// byte count and start the block copies. Factors are constant across the chain,
+// so this may run before the dependency wait on the previous level.
 template <typename E>
-__device__ __forceinline__ void produce_tile(const LevelArgs& a, uint32_t tile, E* st, uint64_t* full, int lane,
-                                             uint64_t pol) {
-  const TileGeo t = tile_geo(a, tile);
+__device__ __forceinline__ void produce_factors(const LevelArgs& a, const TileGeo& t, E* st, uint64_t* full, int lane,
+                                                uint64_t pol) {
   const uint32_t blk = a.R * a.C;
   const E* fac = static_cast<const E*>(a.fac);
+  const uint32_t U = 1u << a.lgU;
+  const uint32_t vec_rows = a.adjoint ? a.nt * U * a.R : U * a.C;
+  const uint32_t bytes = (a.nt * U * blk + vec_rows * t.kc) * static_cast<uint32_t>(sizeof(E));
+  if (lane == 0) mbar_arrive_expect_tx(full, bytes);
+  __syncwarp();
+  if (lane < static_cast<int>(t.segs))
+    bulk_g2s(st + static_cast<size_t>(lane) * t.seg_blocks * blk,
+             fac + static_cast<size_t>(t.seg0 + lane * t.seg_step) * blk, t.seg_blocks * blk * sizeof(E), full, pol);
+}
+
+// Vector part of a tile: the input rows the tile's blocks multiply (the previous
+// level's output).
+template <typename E>
+__device__ __forceinline__ void produce_vectors(const LevelArgs& a, const TileGeo& t, E* st, uint64_t* full,
+                                                int lane) {
+  const uint32_t blk = a.R * a.C;
   const E* in = static_cast<const E*>(a.in);
   const uint32_t U = 1u << a.lgU;
   E* vs = st + static_cast<size_t>(a.nt) * U * blk;
-  const uint32_t vec_rows = a.adjoint ? a.nt * U * a.R : U * a.C;
-  if (a.bulk) {
-    const uint32_t bytes = (a.nt * U * blk + vec_rows * t.kc) * static_cast<uint32_t>(sizeof(E));
-    if (lane == 0) mbar_arrive_expect_tx(full, bytes);
-    __syncwarp();
-    if (lane < static_cast<int>(t.segs))
-      bulk_g2s(st + static_cast<size_t>(lane) * t.seg_blocks * blk,
-               fac + static_cast<size_t>(t.seg0 + lane * t.seg_step) * blk, t.seg_blocks * blk * sizeof(E), full,
-               pol);
-  } else {
-    for (uint32_t s = 0; s < t.segs; ++s) {
-      const E* src = fac + static_cast<size_t>(t.seg0 + s * t.seg_step) * blk;
-      E* dst = st + static_cast<size_t>(s) * t.seg_blocks * blk;
-      for (uint32_t i = lane; i < t.seg_blocks * blk; i += 32) dst[i] = src[i];
-    }
-  }
   if (!a.adjoint) {  // C-side chunk of the U units: contiguous rows u0*C ..
     stage_rows(vs, in + static_cast<size_t>(t.u0) * a.C * a.k + t.k0, U * a.C, t.kc, a.k, full, lane, a.bulk, 2);
   } else {           // R-side chunks, same segment structure as the blocks
@@ -182,6 +184,24 @@ __device__ __forceinline__ void produce_tile(const LevelArgs& a, uint32_t tile, 
                  in + static_cast<size_t>(t.seg0 + s * t.seg_step) * a.R * a.k + t.k0, t.seg_blocks * a.R, t.kc,
                  a.k, full, lane, a.bulk, 2 + s);
   }
+}
+
+template <typename E>
+__device__ __forceinline__ void produce_tile(const LevelArgs& a, uint32_t tile, E* st, uint64_t* full, int lane,
+                                             uint64_t pol) {
+  const TileGeo t = tile_geo(a, tile);
+  const uint32_t blk = a.R * a.C;
+  if (a.bulk) {
+    produce_factors<E>(a, t, st, full, lane, pol);
+  } else {
+    const E* fac = static_cast<const E*>(a.fac);
+    for (uint32_t s = 0; s < t.segs; ++s) {
+      const E* src = fac + static_cast<size_t>(t.seg0 + s * t.seg_step) * blk;
+      E* dst = st + static_cast<size_t>(s) * t.seg_blocks * blk;
+      for (uint32_t i = lane; i < t.seg_blocks * blk; i += 32) dst[i] = src[i];
+    }
+  }
+  produce_vectors<E>(a, t, st, full, lane);
   if (!a.bulk) {
     __syncwarp();
     if (lane == 0) mbar_arrive(full);
@@ -572,21 +592,33 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) level_kernel(const Level
     fence_mbar_init();
   }
   __syncthreads();
-  // programmatic dependent launch: let the next level's CTAs launch as ours retire
-  // (they wait below), and wait for the previous level to finish and flush before
-  // touching its output (our input) or its input (our output buffer). Both are
-  // no-ops when the launch carries no programmatic-serialization attribute.
+  // programmatic dependent launch: let the next level's CTAs launch as ours retire,
+  // and wait for the previous level to finish and flush before touching its output
+  // (our input) or its input (our output buffer); only constant factor blocks are
+  // fetched before the wait. No-ops without the programmatic-serialization attribute.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (warp == NCW) {
     const uint64_t pol = policy_evict_first();
+    // the first STAGES tiles' factor blocks are constant: start them before the wait
+    uint32_t pre = 0;
+    if (a.bulk)
+      for (uint32_t tile = blockIdx.x; tile < a.ntiles && pre < STAGES; tile += gridDim.x, ++pre)
+        produce_factors<E>(a, tile_geo(a, tile), stage0 + static_cast<size_t>(pre) * a.stage_elems, &full[pre], lane,
+                           pol);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     uint32_t it = 0;
     for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
       const uint32_t s = it % STAGES;
+      E* st = stage0 + static_cast<size_t>(s) * a.stage_elems;
+      if (it < pre) {
+        produce_vectors<E>(a, tile_geo(a, tile), st, &full[s], lane);
+        continue;
+      }
       if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-      produce_tile<E>(a, tile, stage0 + static_cast<size_t>(s) * a.stage_elems, &full[s], lane, pol);
+      produce_tile<E>(a, tile, st, &full[s], lane, pol);
     }
   } else {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     uint32_t it = 0;
     for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
       const uint32_t s = it % STAGES;
