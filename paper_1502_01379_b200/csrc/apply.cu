@@ -125,9 +125,10 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   a.r = pl.rank;
   a.part = pl.part;
   a.mp = pl.m / pl.nparts;
+  PeerArgs pa{};
   if (remap >= 3) {
     if (!peers || pl.nparts > 8) return fail(BF_EINVAL, "peer push needs <= 8 receive buffers");
-    for (uint32_t d = 0; d < pl.nparts; ++d) a.peers[d] = peers[d];
+    for (uint32_t d = 0; d < pl.nparts; ++d) pa.peers[d] = peers[d];
   }
   const uint64_t esz = sizeof(E);
   const uint64_t fac_unit = static_cast<uint64_t>(nt) * R * C;
@@ -163,8 +164,14 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   a.bulk = aligned && (esz == 16 || (R % 2 == 0 && C % 2 == 0 && (a.ktiles == 1 || (k % 2 == 0 && kt % 2 == 0))));
   const size_t smem = 128 + static_cast<size_t>(sh.stages) * a.stage_elems * esz;
   if (smem > 227 * 1024) return fail(BF_EINVAL, "rank too large: one block pair exceeds the shared-memory stage");
-  void (*kern)(LevelArgs) = mrhs ? level_kernel<E, kMrhs.stages, kMrhs.ncw, kMrhs.ctas_per_sm, 1>
-                                 : level_kernel<E, kStream.stages, kStream.ncw, kStream.ctas_per_sm, 0>;
+  // the peer-push epilogue (remap 3/4) is its own instantiation: compiled into the common
+  // kernels it costs the many-RHS paths registers and ~8% (cfg2 k=256)
+  const bool push = remap >= 3;
+  void (*kern)(LevelArgs, PeerArgs) =
+      mrhs ? (push ? level_kernel<E, kMrhs.stages, kMrhs.ncw, kMrhs.ctas_per_sm, 1, true>
+                   : level_kernel<E, kMrhs.stages, kMrhs.ncw, kMrhs.ctas_per_sm, 1, false>)
+           : (push ? level_kernel<E, kStream.stages, kStream.ncw, kStream.ctas_per_sm, 0, true>
+                   : level_kernel<E, kStream.stages, kStream.ncw, kStream.ctas_per_sm, 0, false>);
   BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const uint64_t per_sm = smem * sh.ctas_per_sm <= 227 * 1024 ? sh.ctas_per_sm : 1;
   const uint64_t grid = std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(pl.sms) * per_sm);
@@ -178,7 +185,7 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  BF_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  BF_CUDA(cudaLaunchKernelEx(&cfg, kern, a, pa));
   return 0;
 }
 

@@ -54,9 +54,15 @@ struct LevelArgs {
   int remap;          // 0 none, 1 middle forward, 2 middle adjoint, 3/4 the same pushed to peers
   uint32_t m, r;      // middle geometry (remap)
   uint32_t part, mp;  // remap 3/4: this part and middle nodes per part
-  void* peers[8];     // remap 3/4: receive buffers of every part, [sender][own][other local][rho][k]
   int bulk;           // 1: 16-byte aligned, use the TMA bulk engine
   int use_dmma;       // many-RHS complex128: FP64 tensor-core (mma.sync f64) consumer
+};
+
+// remap 3/4 receive buffers of every part ([sender][own][other local][rho][k]); a
+// separate kernel parameter read only by the PUSH instantiation — inside LevelArgs
+// the 64 bytes cost the many-RHS kernels a register spill and ~8%
+struct PeerArgs {
+  void* peers[8];
 };
 
 
@@ -68,8 +74,8 @@ struct LevelArgs {
 // multi-GPU box): a = own local node, b = global other node, receiver part
 // b / mp, slot [sender][own][b mod mp][rho] — the layout bf_middle_pack + an
 // all-to-all would produce, with no pack kernel and no collective.
-template <typename E>
-__device__ __forceinline__ E* remap_row(const LevelArgs& a, size_t e, typename Cx<E>::R* w) {
+template <typename E, bool PUSH>
+__device__ __forceinline__ E* remap_row(const LevelArgs& a, const PeerArgs& pa, size_t e, typename Cx<E>::R* w) {
   using Rl = typename Cx<E>::R;
   E* out = static_cast<E*>(a.out);
   if (a.remap == 0) {
@@ -86,10 +92,20 @@ __device__ __forceinline__ E* remap_row(const LevelArgs& a, size_t e, typename C
     *w = a.remap == 1 ? __ldg(W + dst) : __ldg(W + (static_cast<size_t>(ia) * a.m + ib) * a.r + rho);
     return out + dst * a.k;
   }
+  if constexpr (!PUSH) {
+    return out;  // remap 3/4 only run in the PUSH instantiation
+  } else {
   const uint32_t own = a.part * a.mp + ia, d = ib / a.mp, bl = ib - d * a.mp;
   *w = a.remap == 3 ? __ldg(W + (static_cast<size_t>(ib) * a.m + own) * a.r + rho)
                     : __ldg(W + (static_cast<size_t>(own) * a.m + ib) * a.r + rho);
-  return static_cast<E*>(a.peers[d]) + ((static_cast<size_t>(own) * a.mp + bl) * a.r + rho) * a.k;
+  // select the peer pointer without a dynamic index into the parameter block (which
+  // would force a local-memory copy of it)
+  E* base = nullptr;
+#pragma unroll
+  for (uint32_t q = 0; q < 8; ++q)
+    if (q == d) base = static_cast<E*>(pa.peers[q]);
+  return base + ((static_cast<size_t>(own) * a.mp + bl) * a.r + rho) * a.k;
+  }
 }
 
 struct TileGeo {
@@ -227,8 +243,8 @@ struct Acc8 {
   }
 };
 
-template <typename E>
-__device__ __forceinline__ void consume_tile(const LevelArgs& a, uint32_t tile, const E* st, int ct, int nct) {
+template <typename E, bool PUSH>
+__device__ __forceinline__ void consume_tile(const LevelArgs& a, const PeerArgs& pa, uint32_t tile, const E* st, int ct, int nct) {
   using Rl = typename Cx<E>::R;
   const TileGeo t = tile_geo(a, tile);
   const uint32_t blk = a.R * a.C;
@@ -283,7 +299,7 @@ __device__ __forceinline__ void consume_tile(const LevelArgs& a, uint32_t tile, 
       // destination (and, with the fused middle factor, its weight) first: the weight's
       // global load then overlaps the dot product instead of trailing it
       Rl w;
-      E* orow = remap_row<E>(a, static_cast<size_t>(t.u0 + ul) * a.C + c, &w);
+      E* orow = remap_row<E, PUSH>(a, pa, static_cast<size_t>(t.u0 + ul) * a.C + c, &w);
       const uint32_t base = (((ul >> t.lgPe) * a.nt) << t.lgPe) + (ul & Pe_mask);
       Acc8<E> acc;
       for (uint32_t tt = 0; tt < a.nt; ++tt) {
@@ -312,8 +328,8 @@ __device__ __forceinline__ void consume_tile(const LevelArgs& a, uint32_t tile, 
 // operand load of the warp is a contiguous, bank-conflict-free span and the A
 // operand is (nearly) a broadcast. Per inner step: TM + TN shared loads feed
 // 4*TM*TN FP64 FMAs — FMA-pipe bound, not shared-memory bound.
-template <typename E, int TM, int TN, int LC>
-__device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, uint32_t tile, const E* st, int warp, int lane,
+template <typename E, int TM, int TN, int LC, bool PUSH>
+__device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, const PeerArgs& pa, uint32_t tile, const E* st, int warp, int lane,
                                                   int nwarps) {
   using Rl = typename Cx<E>::R;
   constexpr int LR = 32 / LC;
@@ -412,7 +428,7 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, uint32_t t
         const uint32_t c = rb + LR * i;
         if (c >= m_out) break;
         Rl w;
-        E* dst = remap_row<E>(a, static_cast<size_t>(t.u0 + ul) * a.C + c, &w) + t.k0 + col0;
+        E* dst = remap_row<E, PUSH>(a, pa, static_cast<size_t>(t.u0 + ul) * a.C + c, &w) + t.k0 + col0;
 #pragma unroll
         for (int j = 0; j < TN; ++j)
           if (colok[j]) {
@@ -437,8 +453,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // Many-RHS consumer on the FP64 tensor pipe (complex128). Each unit is the
 // complex GEMM of consume_tile_mrhs, split into 4 real DMMAs per k-step
 // (re += Ar Xr - Ai Xi, im += Ar Xi + Ai Xr); a warp owns MT x NT 8x8 tiles.
-template <int MT, int NT>
-__device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, uint32_t tile, const double2* st, int warp,
+template <int MT, int NT, bool PUSH>
+__device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const PeerArgs& pa, uint32_t tile, const double2* st, int warp,
                                                   int lane, int nwarps) {
   const TileGeo t = tile_geo(a, tile);
   const uint32_t blk = a.R * a.C;
@@ -534,8 +550,21 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, uint32_t t
         const uint32_t tt = m / a.R, rho = m - tt * a.R;
         const uint32_t q = ((((u >> a.lgP) * a.ntot) + a.t0 + tt) << a.lgP) + (u & P_mask);
         orow = out + (static_cast<size_t>(q) * a.R + rho) * a.k + t.k0;
+      } else if (a.remap >= 3) {
+        orow = remap_row<double2, PUSH>(a, pa, static_cast<size_t>(t.u0 + ul) * a.C + m, &w) + t.k0;
       } else {
-        orow = remap_row<double2>(a, static_cast<size_t>(t.u0 + ul) * a.C + m, &w) + t.k0;
+        size_t e = static_cast<size_t>(t.u0 + ul) * a.C + m;
+        if (a.remap != 0) {
+          const uint32_t mr = a.m * a.r;
+          const uint32_t e32 = static_cast<uint32_t>(e), ia = e32 / mr;
+          const uint32_t rem = e32 - ia * mr;
+          const uint32_t ib = rem / a.r, rho = rem - ib * a.r;
+          const size_t dst = (static_cast<size_t>(ib) * a.m + ia) * a.r + rho;
+          const double* W = static_cast<const double*>(a.mid_w);
+          w = a.remap == 1 ? W[dst] : W[(static_cast<size_t>(ia) * a.m + ib) * a.r + rho];
+          e = dst;
+        }
+        orow = out + e * a.k + t.k0;
       }
 #pragma unroll
       for (int j = 0; j < NT; ++j)
@@ -552,33 +581,33 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, uint32_t t
 }
 
 // Register-tile shapes of the many-RHS consumer, picked by right-hand sides per tile.
-template <typename E>
-__device__ __forceinline__ void consume_tile_mrhs_any(const LevelArgs& a, uint32_t tile, const E* st, int warp,
+template <typename E, bool PUSH>
+__device__ __forceinline__ void consume_tile_mrhs_any(const LevelArgs& a, const PeerArgs& pa, uint32_t tile, const E* st, int warp,
                                                       int lane, int nwarps) {
   if constexpr (std::is_same<E, double2>::value) {
     if (a.use_dmma) {  // complex128: the FP64 tensor pipe
       if (a.kt >= 32)
-        consume_tile_dmma<2, 4>(a, tile, st, warp, lane, nwarps);
+        consume_tile_dmma<2, 4, PUSH>(a, pa, tile, st, warp, lane, nwarps);
       else
-        consume_tile_dmma<2, 2>(a, tile, st, warp, lane, nwarps);
+        consume_tile_dmma<2, 2, PUSH>(a, pa, tile, st, warp, lane, nwarps);
       return;
     }
   }
   if (a.kt >= 128)
-    consume_tile_mrhs<E, 4, 4, 32>(a, tile, st, warp, lane, nwarps);
+    consume_tile_mrhs<E, 4, 4, 32, PUSH>(a, pa, tile, st, warp, lane, nwarps);
   else if (a.kt >= 64)
-    consume_tile_mrhs<E, 8, 2, 32>(a, tile, st, warp, lane, nwarps);
+    consume_tile_mrhs<E, 8, 2, 32, PUSH>(a, pa, tile, st, warp, lane, nwarps);
   else if (a.kt >= 32)
-    consume_tile_mrhs<E, 16, 1, 32>(a, tile, st, warp, lane, nwarps);
+    consume_tile_mrhs<E, 16, 1, 32, PUSH>(a, pa, tile, st, warp, lane, nwarps);
   else if (a.kt >= 16)
-    consume_tile_mrhs<E, 8, 1, 16>(a, tile, st, warp, lane, nwarps);
+    consume_tile_mrhs<E, 8, 1, 16, PUSH>(a, pa, tile, st, warp, lane, nwarps);
   else
-    consume_tile_mrhs<E, 4, 1, 8>(a, tile, st, warp, lane, nwarps);
+    consume_tile_mrhs<E, 4, 1, 8, PUSH>(a, pa, tile, st, warp, lane, nwarps);
 }
 
 // MRHS = 0: streaming consumer (one output per thread); MRHS = 1: register-tiled GEMM consumer.
-template <typename E, int STAGES, int NCW, int MINB, int MRHS>
-__global__ void __launch_bounds__((NCW + 1) * 32, MINB) level_kernel(const LevelArgs a) {
+template <typename E, int STAGES, int NCW, int MINB, int MRHS, bool PUSH>
+__global__ void __launch_bounds__((NCW + 1) * 32, MINB) level_kernel(const LevelArgs a, const PeerArgs pa) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + STAGES;
@@ -624,9 +653,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) level_kernel(const Level
       const uint32_t s = it % STAGES;
       mbar_wait(&full[s], (it / STAGES) & 1);
       if (MRHS)
-        consume_tile_mrhs_any<E>(a, tile, stage0 + static_cast<size_t>(s) * a.stage_elems, warp, lane, NCW);
+        consume_tile_mrhs_any<E, PUSH>(a, pa, tile, stage0 + static_cast<size_t>(s) * a.stage_elems, warp, lane, NCW);
       else
-        consume_tile<E>(a, tile, stage0 + static_cast<size_t>(s) * a.stage_elems, threadIdx.x, NCW * 32);
+        consume_tile<E, PUSH>(a, pa, tile, stage0 + static_cast<size_t>(s) * a.stage_elems, threadIdx.x, NCW * 32);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
