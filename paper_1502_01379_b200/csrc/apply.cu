@@ -56,6 +56,13 @@ struct Shape {
   uint32_t stage_bytes;
 };
 constexpr Shape kStream{3, 2, 2, 34 * 1024 + 512};
+// complex64 streams half the bytes per output: twice the consumer warps keep the
+// same per-SM output rate at the same stage size
+constexpr Shape kStream64{3, 4, 2, 34 * 1024 + 512};
+template <typename E>
+constexpr Shape stream_shape() {
+  return sizeof(E) == 8 ? kStream64 : kStream;
+}
 constexpr Shape kMrhs{2, 8, 1, 100 * 1024};
 constexpr uint32_t kMrhsMinK = 8;
 
@@ -82,7 +89,7 @@ template <typename E>
 int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint64_t P, uint64_t units,
                  const void* in, void* out, uint32_t k, int adjoint, int remap, cudaStream_t st,
                  void* const* peers = nullptr) {
-  const Shape sh = k >= kMrhsMinK ? kMrhs : kStream;
+  const Shape sh = k >= kMrhsMinK ? kMrhs : stream_shape<E>();
   uint32_t nt_tile = nt;
   auto tile_elems = [&](uint64_t t) { return t * R * C + (adjoint ? t * R : static_cast<uint64_t>(C)); };
   while (nt_tile > 1 && tile_elems(nt_tile) * sizeof(E) > sh.stage_bytes) nt_tile /= 2;
@@ -104,7 +111,8 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   if (remap && static_cast<uint64_t>(pl.m) * pl.m * pl.rank >= (1ull << 32))
     return fail(BF_EINVAL, "middle vector too long for 32-bit remap indices");
   const bool mrhs = k >= kMrhsMinK;
-  const Shape sh = mrhs ? kMrhs : kStream;
+  constexpr Shape ks = stream_shape<E>();
+  const Shape sh = mrhs ? kMrhs : ks;
   LevelArgs a{};
   a.fac = fac;
   a.in = in;
@@ -170,8 +178,8 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   void (*kern)(LevelArgs, PeerArgs) =
       mrhs ? (push ? level_kernel<E, kMrhs.stages, kMrhs.ncw, kMrhs.ctas_per_sm, 1, true>
                    : level_kernel<E, kMrhs.stages, kMrhs.ncw, kMrhs.ctas_per_sm, 1, false>)
-           : (push ? level_kernel<E, kStream.stages, kStream.ncw, kStream.ctas_per_sm, 0, true>
-                   : level_kernel<E, kStream.stages, kStream.ncw, kStream.ctas_per_sm, 0, false>);
+           : (push ? level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, true>
+                   : level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, false>);
   BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const uint64_t per_sm = smem * sh.ctas_per_sm <= 227 * 1024 ? sh.ctas_per_sm : 1;
   const uint64_t grid = std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(pl.sms) * per_sm);
