@@ -6,6 +6,7 @@
 //   adjoint:  U^L*  -> G^{L-1}* .. G^{h}*  -> M* -> H^{h} .. H^{L-1} -> V^L
 // with M (or M*) fused into the epilogue of the last adjoint-direction level.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "level_kernel.cuh"
@@ -180,9 +181,17 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
                    : level_kernel<E, kMrhs.stages, kMrhs.ncw, kMrhs.ctas_per_sm, 1, false>)
            : (push ? level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, true>
                    : level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, false>);
-  BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   const uint64_t per_sm = smem * sh.ctas_per_sm <= 227 * 1024 ? sh.ctas_per_sm : 1;
   const uint64_t grid = std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(pl.sms) * per_sm);
+  static const bool dbg = [] {
+    const char* e = getenv("BF_DEBUG_LAUNCH");
+    return e && *e && *e != '0';
+  }();
+  if (dbg)
+    fprintf(stderr, "[bf] level_kernel %s%s R=%u C=%u nt=%u units=%llu k=%u kt=%u U=%llu ntiles=%u grid=%llu smem=%zu dmma=%d\n",
+            mrhs ? "mrhs" : "stream", push ? "+push" : "", R, C, nt, static_cast<unsigned long long>(units), k, kt,
+            static_cast<unsigned long long>(U), a.ntiles, static_cast<unsigned long long>(grid), smem, a.use_dmma);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3((sh.ncw + 1) * 32);

@@ -94,6 +94,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+// ---------------------------------------------------------------- launch limits
+// Dynamic shared memory opt-in set once to the sm_100a maximum for every kernel
+// (not per launch to the launch's own size): concurrent launches of one kernel
+// with different sizes cannot race on the attribute, and a profiler replaying a
+// captured graph node in isolation sees an attribute large enough for it.
+constexpr int kMaxDynSmem = 227 * 1024;
+
 // ---------------------------------------------------------------- device scope
 // Makes `dev` current for the scope and restores the caller's device after.
 struct DeviceGuardScope {

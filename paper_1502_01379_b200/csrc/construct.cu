@@ -1114,16 +1114,15 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
   const int T = 256;
   const unsigned yfill = static_cast<unsigned>(std::min<uint64_t>(64, (S * side + T - 1) / T));
   const size_t small_smem = S <= kSmemSet ? 3ull * S * S * sizeof(double2) : 0;
-  BF_CUDA(cudaFuncSetAttribute(k_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(small_smem)));
-  BF_CUDA(cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(small_smem)));
+  BF_CUDA(cudaFuncSetAttribute(k_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  BF_CUDA(cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   k_init<<<(nblocks + 127) / 128, 128, 0, st>>>(a, block_ij);
   if (dense_branch) {
     k_dense<<<nblocks, T, small_smem, st>>>(a);
   } else {
     const size_t piv_smem = side * sizeof(double) + kSetCap * sizeof(double2) + 32 * 8 + 32 * 4 + kSetCap * 4;
     if (piv_smem > 227 * 1024) return fail(BF_EINVAL, "middle blocks too wide for the pivot kernel");
-    BF_CUDA(cudaFuncSetAttribute(k_pivot_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(piv_smem)));
+    BF_CUDA(cudaFuncSetAttribute(k_pivot_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     for (uint32_t sw = 0; sw < iters; ++sw) {
       k_union<<<nblocks, 128, 0, st>>>(a, 2 * sw, kRows);
       k_fill_wide<<<dim3(nblocks, yfill), T, 0, st>>>(a, kRows);
@@ -1135,8 +1134,7 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
     k_union<<<nblocks, 128, 0, st>>>(a, 2 * iters, kRows);
     k_union<<<nblocks, 128, 0, st>>>(a, 2 * iters + 1, kCols);
     const size_t tall_smem = (static_cast<size_t>(kGramChunk) * S + (S <= kSmemSet ? 2ull * S * S : 0)) * 16;
-    BF_CUDA(cudaFuncSetAttribute(k_pivot_tall, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(tall_smem)));
+    BF_CUDA(cudaFuncSetAttribute(k_pivot_tall, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     for (int which : {kCols, kRows}) {
       k_fill_tall<<<dim3(nblocks, yfill), T, 0, st>>>(a, which, 0, a.tall);
       k_pivot_tall<<<nblocks, 512, tall_smem, st>>>(a, which);
@@ -1204,9 +1202,8 @@ int bf_middle_probes(uint64_t n, uint32_t levels, uint32_t branching, uint32_t r
   const unsigned yfill = static_cast<unsigned>(std::min<uint64_t>(64, (width * side + T - 1) / T));
   const size_t small_smem = S <= kSmemSet ? 3ull * S * S * sizeof(double2) : 0;
   const size_t tall_smem = (static_cast<size_t>(kGramChunk) * S + (S <= kSmemSet ? 2ull * S * S : 0)) * 16;
-  BF_CUDA(cudaFuncSetAttribute(k_mid_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(small_smem)));
-  BF_CUDA(cudaFuncSetAttribute(k_pivot_tall, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(tall_smem)));
+  BF_CUDA(cudaFuncSetAttribute(k_mid_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  BF_CUDA(cudaFuncSetAttribute(k_pivot_tall, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   k_init<<<(nblocks + 127) / 128, 128, 0, st>>>(a, block_ij);
   for (int which : {kCols, kRows}) {
     k_fill_probe<<<dim3(nblocks, yfill), T, 0, st>>>(a, which);
@@ -1260,7 +1257,7 @@ int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t ro
   if (rows >= branching) {
     const int64_t nprob = static_cast<int64_t>(nb) * branching * pairs;
     const size_t smem = S <= kSmemSet ? rec_smem_elems(static_cast<int>(w), S) * sizeof(double2) : 0;
-    BF_CUDA(cudaFuncSetAttribute(k_recurse_split, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    BF_CUDA(cudaFuncSetAttribute(k_recurse_split, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     for (int64_t p0 = 0; p0 < nprob; p0 += chunk) {
       a.p0 = p0;
       const int64_t cnt = std::min<int64_t>(chunk, nprob - p0);
@@ -1288,7 +1285,7 @@ int bf_select_pivots(const void* a, uint32_t batch, uint32_t m, uint32_t n, uint
   const uint64_t kk = k < m ? k : m;
   if (ws_bytes < 16ull * batch * kk * n) return fail(BF_EINVAL, "pivot workspace too small (16*batch*min(k,m)*n bytes)");
   const size_t smem = (n + (n & 1)) * 8 + kSetCap * 16 + 32 * 8 + 32 * 4 + 1024 * 4;
-  BF_CUDA(cudaFuncSetAttribute(k_select_pivots, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  BF_CUDA(cudaFuncSetAttribute(k_select_pivots, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   k_select_pivots<<<batch, 512, smem, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const double2*>(a), static_cast<double2*>(workspace), static_cast<int>(m), static_cast<int>(n),
       static_cast<int>(k), rel_tol, pairwise, pivots, counts);
