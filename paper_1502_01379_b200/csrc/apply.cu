@@ -67,6 +67,15 @@ constexpr Shape stream_shape() {
 constexpr Shape kMrhs{2, 8, 1, 100 * 1024};
 constexpr uint32_t kMrhsMinK = 8;
 
+// Padded shared-memory rows for the DMMA consumer (BF_NO_PAD=1 turns them off).
+bool pad_disabled() {
+  static const bool off = [] {
+    const char* e = getenv("BF_NO_PAD");
+    return e && *e && *e != '0';
+  }();
+  return off;
+}
+
 // Programmatic dependent launch between consecutive level kernels (the next
 // level's prologue overlaps the previous one's tail); BF_NO_PDL=1 turns it off.
 bool pdl_enabled() {
@@ -171,6 +180,30 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   // into k-tiles, even k and kt.
   a.use_dmma = mrhs && esz == 16 && kt >= 16 && !dmma_disabled();
   a.bulk = aligned && (esz == 16 || (R % 2 == 0 && C % 2 == 0 && (a.ktiles == 1 || (k % 2 == 0 && kt % 2 == 0))));
+  a.fld = C;
+  a.vld = 0;
+  if (a.use_dmma && a.bulk && a.ktiles > 1 && !pad_disabled()) {  // rows are copied one by one anyway
+    // DMMA fragment loads: a quarter warp reads rows (lane/4) x k-slots (lane%4) of a
+    // factor block and k-rows x columns of the vector tile; row strides = 4 (forward
+    // A), 2 (adjoint A, vectors) mod 8 sixteen-byte units put the 8 lanes of every
+    // quarter warp on distinct bank groups (unpadded: 2- to 4-way conflicts)
+    auto pad_to = [](uint64_t x, uint64_t target) { return x + (target + 8 - x % 8) % 8; };
+    const uint64_t fld = pad_to(C, adjoint ? 2 : 4), vld = pad_to(kt, 2);
+    const uint64_t vrows = adjoint ? static_cast<uint64_t>(nt) * R : C;
+    uint64_t Up = U;
+    auto padded = [&](uint64_t u) { return u * (static_cast<uint64_t>(nt) * R * fld + vrows * vld); };
+    while (Up > 1 && 128 + sh.stages * padded(Up) * esz > static_cast<uint64_t>(kMaxDynSmem)) Up /= 2;
+    if (128 + sh.stages * padded(Up) * esz <= static_cast<uint64_t>(kMaxDynSmem)) {
+      U = Up;
+      a.lgU = ilog2(U);
+      a.ntiles = static_cast<uint32_t>((units / U) * a.ktiles);
+      a.fld = static_cast<uint32_t>(fld);
+      a.vld = static_cast<uint32_t>(vld);
+      uint64_t st2 = padded(U);
+      if (st2 & 1) ++st2;
+      a.stage_elems = static_cast<uint32_t>(st2);
+    }
+  }
   const size_t smem = 128 + static_cast<size_t>(sh.stages) * a.stage_elems * esz;
   if (smem > 227 * 1024) return fail(BF_EINVAL, "rank too large: one block pair exceeds the shared-memory stage");
   // the peer-push epilogue (remap 3/4) is its own instantiation: compiled into the common

@@ -56,6 +56,10 @@ struct LevelArgs {
   uint32_t part, mp;  // remap 3/4: this part and middle nodes per part
   int bulk;           // 1: 16-byte aligned, use the TMA bulk engine
   int use_dmma;       // many-RHS complex128: FP64 tensor-core (mma.sync f64) consumer
+  // shared-memory row strides (elements) of the staged factor rows (fld, default C)
+  // and vector rows (vld, 0 = the tile's kc). The DMMA consumer pads them so its
+  // fragment loads hit 8 distinct 16-byte bank groups per quarter warp.
+  uint32_t fld, vld;
 };
 
 // remap 3/4 receive buffers of every part ([sender][own][other local][rho][k]); a
@@ -145,22 +149,22 @@ __device__ __forceinline__ TileGeo tile_geo(const LevelArgs& a, uint32_t tile) {
   return t;
 }
 
-// Copy `rows` rows of `kc` elements (source row stride k) into contiguous smem.
+// Copy `rows` rows of `kc` elements (source row stride k) into smem rows of stride ld.
 template <typename E>
-__device__ __forceinline__ void stage_rows(E* dst, const E* src, uint32_t rows, uint32_t kc, uint32_t k,
+__device__ __forceinline__ void stage_rows(E* dst, const E* src, uint32_t rows, uint32_t kc, uint32_t k, uint32_t ld,
                                            uint64_t* bar, int lane, int bulk, int lane_base) {
   if (bulk) {
-    if (kc == k) {
+    if (kc == k && ld == kc) {
       if (lane == lane_base) bulk_g2s(dst, src, rows * kc * static_cast<uint32_t>(sizeof(E)), bar);
     } else {
       for (uint32_t i = lane; i < rows; i += 32)
-        bulk_g2s(dst + static_cast<size_t>(i) * kc, src + static_cast<size_t>(i) * k, kc * sizeof(E), bar);
+        bulk_g2s(dst + static_cast<size_t>(i) * ld, src + static_cast<size_t>(i) * k, kc * sizeof(E), bar);
     }
   } else {
     const uint32_t total = rows * kc;
     for (uint32_t idx = lane; idx < total; idx += 32) {
       const uint32_t i = kc == 1 ? idx : idx / kc, j = kc == 1 ? 0 : idx - (idx / kc) * kc;
-      dst[idx] = src[static_cast<size_t>(i) * k + j];
+      dst[static_cast<size_t>(i) * ld + j] = src[static_cast<size_t>(i) * k + j];
     }
   }
 }
@@ -178,9 +182,19 @@ __device__ __forceinline__ void produce_factors(const LevelArgs& a, const TileGe
   const uint32_t bytes = (a.nt * U * blk + vec_rows * t.kc) * static_cast<uint32_t>(sizeof(E));
   if (lane == 0) mbar_arrive_expect_tx(full, bytes);
   __syncwarp();
-  if (lane < static_cast<int>(t.segs))
-    bulk_g2s(st + static_cast<size_t>(lane) * t.seg_blocks * blk,
-             fac + static_cast<size_t>(t.seg0 + lane * t.seg_step) * blk, t.seg_blocks * blk * sizeof(E), full, pol);
+  if (a.fld == a.C) {
+    if (lane < static_cast<int>(t.segs))
+      bulk_g2s(st + static_cast<size_t>(lane) * t.seg_blocks * blk,
+               fac + static_cast<size_t>(t.seg0 + lane * t.seg_step) * blk, t.seg_blocks * blk * sizeof(E), full, pol);
+  } else {  // padded rows: one copy per block row
+    const uint32_t seg_rows = t.seg_blocks * a.R;
+    for (uint32_t row = lane; row < t.segs * seg_rows; row += 32) {
+      const uint32_t sg = row / seg_rows, rr = row - sg * seg_rows;
+      bulk_g2s(st + static_cast<size_t>(row) * a.fld,
+               fac + static_cast<size_t>(t.seg0 + sg * t.seg_step) * blk + static_cast<size_t>(rr) * a.C,
+               a.C * static_cast<uint32_t>(sizeof(E)), full, pol);
+    }
+  }
 }
 
 // Vector part of a tile: the input rows the tile's blocks multiply (the previous
@@ -188,17 +202,17 @@ __device__ __forceinline__ void produce_factors(const LevelArgs& a, const TileGe
 template <typename E>
 __device__ __forceinline__ void produce_vectors(const LevelArgs& a, const TileGeo& t, E* st, uint64_t* full,
                                                 int lane) {
-  const uint32_t blk = a.R * a.C;
   const E* in = static_cast<const E*>(a.in);
   const uint32_t U = 1u << a.lgU;
-  E* vs = st + static_cast<size_t>(a.nt) * U * blk;
+  E* vs = st + static_cast<size_t>(a.nt) * U * a.R * a.fld;
+  const uint32_t ld = a.vld ? a.vld : t.kc;
   if (!a.adjoint) {  // C-side chunk of the U units: contiguous rows u0*C ..
-    stage_rows(vs, in + static_cast<size_t>(t.u0) * a.C * a.k + t.k0, U * a.C, t.kc, a.k, full, lane, a.bulk, 2);
+    stage_rows(vs, in + static_cast<size_t>(t.u0) * a.C * a.k + t.k0, U * a.C, t.kc, a.k, ld, full, lane, a.bulk, 2);
   } else {           // R-side chunks, same segment structure as the blocks
     for (uint32_t s = 0; s < t.segs; ++s)
-      stage_rows(vs + static_cast<size_t>(s) * t.seg_blocks * a.R * t.kc,
+      stage_rows(vs + static_cast<size_t>(s) * t.seg_blocks * a.R * ld,
                  in + static_cast<size_t>(t.seg0 + s * t.seg_step) * a.R * a.k + t.k0, t.seg_blocks * a.R, t.kc,
-                 a.k, full, lane, a.bulk, 2 + s);
+                 a.k, ld, full, lane, a.bulk, 2 + s);
   }
 }
 
@@ -457,13 +471,13 @@ template <int MT, int NT, bool PUSH>
 __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const PeerArgs& pa, uint32_t tile, const double2* st, int warp,
                                                   int lane, int nwarps) {
   const TileGeo t = tile_geo(a, tile);
-  const uint32_t blk = a.R * a.C;
   const uint32_t U = 1u << a.lgU;
   const uint32_t Pe_mask = (1u << t.lgPe) - 1;
   const double2* fs = st;
-  const double2* vs = st + static_cast<size_t>(a.nt) * U * blk;
+  const double2* vs = st + static_cast<size_t>(a.nt) * U * a.R * a.fld;
   double2* out = static_cast<double2*>(a.out);
   const uint32_t kc = t.kc;
+  const uint32_t fld = a.fld, vld = a.vld ? a.vld : kc;
   const uint32_t P_mask = (1u << a.lgP) - 1;
   const uint32_t m_out = a.adjoint ? a.C : a.nt * a.R;
   const uint32_t kdim = a.adjoint ? a.nt * a.R : a.C;
@@ -506,9 +520,9 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
         double2 v = make_double2(0, 0);
         if (kok && m < m_out) {
           if (!a.adjoint) {
-            v = fs[static_cast<size_t>(arow[i]) * a.C + kk];
+            v = fs[static_cast<size_t>(arow[i]) * fld + kk];
           } else {
-            v = fs[static_cast<size_t>(jrow) * a.C + m];
+            v = fs[static_cast<size_t>(jrow) * fld + m];
             v.y = -v.y;  // A^H
           }
         }
@@ -523,7 +537,7 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
         double2 v = make_double2(0, 0);
         if (kok && n < kc) {
           const size_t row = a.adjoint ? jrow : static_cast<size_t>(ul) * a.C + kk;
-          v = vs[row * kc + n];
+          v = vs[row * vld + n];
         }
         br[j] = v.x;
         bi[j] = v.y;
