@@ -459,7 +459,7 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, const Peer
 // B[lane%4][lane/4], C/D fragment C[lane/4][2(lane%4) + q] (layout confirmed on
 // B200 by tools/dmma_layout.cu).
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
@@ -542,13 +542,20 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
         br[j] = v.x;
         bi[j] = v.y;
       }
+      // two passes over the tiles: the two products accumulated into one register pair
+      // are 2 MT NT instructions apart, not back to back
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
           dmma(cr[i][j][0], cr[i][j][1], ar[i], br[j]);
-          dmma(cr[i][j][0], cr[i][j][1], nai[i], bi[j]);
           dmma(ci[i][j][0], ci[i][j][1], ar[i], bi[j]);
+        }
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          dmma(cr[i][j][0], cr[i][j][1], nai[i], bi[j]);
           dmma(ci[i][j][0], ci[i][j][1], ai[i], br[j]);
         }
     }
