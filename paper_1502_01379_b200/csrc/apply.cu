@@ -214,7 +214,7 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
                    : level_kernel<E, kMrhs.stages, kMrhs.ncw, kMrhs.ctas_per_sm, 1, false>)
            : (push ? level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, true>
                    : level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, false>);
-  BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  BF_CUDA(allow_max_dyn_smem(kern));
   const uint64_t per_sm = smem * sh.ctas_per_sm <= 227 * 1024 ? sh.ctas_per_sm : 1;
   const uint64_t grid = std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(pl.sms) * per_sm);
   static const bool dbg = [] {

@@ -101,6 +101,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // captured graph node in isolation sees an attribute large enough for it.
 constexpr int kMaxDynSmem = 227 * 1024;
 
+// Opt a kernel in to the largest dynamic shared memory its static shared memory leaves.
+template <typename Kernel>
+inline cudaError_t allow_max_dyn_smem(Kernel* kern) {
+  cudaFuncAttributes fa{};
+  const cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kMaxDynSmem - static_cast<int>(fa.sharedSizeBytes));
+}
+
 // ---------------------------------------------------------------- device scope
 // Makes `dev` current for the scope and restores the caller's device after.
 struct DeviceGuardScope {

@@ -16,6 +16,7 @@
 // 132-154), the floored least-squares middle matrix and its SVD (k_mid,
 // lowrank.py:90-94, 257, 284-293) and the scaled factors (k_assemble).
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "entry_eval.cuh"
@@ -445,6 +446,118 @@ __global__ void k_cgs2(MidArgs a, int which) {
     const double nrm = sqrt(block_sum(part, red));
     const double inv = nrm > 0 ? 1.0 / nrm : 0.0;
     for (int i = threadIdx.x; i < side; i += blockDim.x) x[i] = make_double2(x[i].x * inv, x[i].y * inv);
+    __syncthreads();
+  }
+}
+
+// Block classical Gram-Schmidt with reorthogonalisation (BCGS2): the same
+// orthonormal basis as k_cgs2 up to rounding (only span(Q) reaches the
+// factors), with the columns processed in panels of `pw` held in shared memory.
+// Per panel, twice: project the panel against all previous columns (one pass
+// over Q[:, :j0] computes every panel column's coefficients, one more applies
+// them), then classical Gram-Schmidt inside the panel. k_cgs2 reads each
+// previous column ~6 times per new column from global memory; here each previous
+// column is read 4 times per panel.
+constexpr int kPanelMax = 8;
+
+__global__ void __launch_bounds__(512) k_bcgs2(MidArgs a, int which, int pw) {
+  extern __shared__ double2 pan[];  // pw columns of length side
+  __shared__ double2 coef[kSetCap][kPanelMax];
+  __shared__ double red[2 * 32];
+  const BlockState& s = a.st[blockIdx.x];
+  const int t = which == kCols ? s.tc : s.tr;
+  const int side = static_cast<int>(a.side);
+  double2* Q = (which == kCols ? a.qc : a.qr) + static_cast<int64_t>(blockIdx.x) * a.S * a.side;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j0 = 0; j0 < t; j0 += pw) {
+    const int nb = min(pw, t - j0);
+    for (int x = threadIdx.x; x < nb * side; x += blockDim.x) pan[x] = Q[static_cast<int64_t>(j0) * side + x];
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+      if (j0 > 0) {
+        // C = Q[:, :j0]^H pan, one warp per previous column
+        for (int l = warp; l < j0; l += nw) {
+          const double2* ql = Q + static_cast<int64_t>(l) * side;
+          double2 acc[kPanelMax];
+#pragma unroll
+          for (int b = 0; b < kPanelMax; ++b) acc[b] = make_double2(0, 0);
+          for (int i = lane; i < side; i += 32) {
+            const double2 q = ql[i];
+#pragma unroll
+            for (int b = 0; b < kPanelMax; ++b)
+              if (b < nb) {
+                const double2 g = cmulc(q, pan[b * side + i]);
+                acc[b].x += g.x;
+                acc[b].y += g.y;
+              }
+          }
+#pragma unroll
+          for (int b = 0; b < kPanelMax; ++b)
+            if (b < nb) {
+              const double2 v = warp_sum2(acc[b]);
+              if (lane == 0) coef[l][b] = v;
+            }
+        }
+        __syncthreads();
+        // pan -= Q[:, :j0] C, one thread per row
+        for (int i = threadIdx.x; i < side; i += blockDim.x) {
+          double2 v[kPanelMax];
+#pragma unroll
+          for (int b = 0; b < kPanelMax; ++b) v[b] = b < nb ? pan[b * side + i] : make_double2(0, 0);
+          for (int l = 0; l < j0; ++l) {
+            const double2 q = Q[static_cast<int64_t>(l) * side + i];
+#pragma unroll
+            for (int b = 0; b < kPanelMax; ++b) {
+              const double2 d = cmul(q, coef[l][b]);
+              v[b].x -= d.x;
+              v[b].y -= d.y;
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < kPanelMax; ++b)
+            if (b < nb) pan[b * side + i] = v[b];
+        }
+        __syncthreads();
+      }
+      // classical Gram-Schmidt inside the panel
+      for (int c = 0; c < nb; ++c) {
+        double2* xc = pan + c * side;
+        for (int cc = 0; cc < c; ++cc) {
+          const double2* xq = pan + cc * side;
+          double2 acc = make_double2(0, 0);
+          for (int i = threadIdx.x; i < side; i += blockDim.x) {
+            const double2 g = cmulc(xq[i], xc[i]);
+            acc.x += g.x;
+            acc.y += g.y;
+          }
+          acc = warp_sum2(acc);
+          __syncthreads();
+          if (lane == 0) {
+            red[warp] = acc.x;
+            red[32 + warp] = acc.y;
+          }
+          __syncthreads();
+          double2 cf = make_double2(0, 0);
+          for (int w2 = 0; w2 < nw; ++w2) {
+            cf.x += red[w2];
+            cf.y += red[32 + w2];
+          }
+          for (int i = threadIdx.x; i < side; i += blockDim.x) {
+            const double2 d = cmul(xq[i], cf);
+            xc[i].x -= d.x;
+            xc[i].y -= d.y;
+          }
+        }
+        __syncthreads();
+        double part = 0;
+        for (int i = threadIdx.x; i < side; i += blockDim.x) part += xc[i].x * xc[i].x + xc[i].y * xc[i].y;
+        const double nrm = sqrt(block_sum(part, red));
+        const double inv = nrm > 0 ? 1.0 / nrm : 0.0;
+        for (int i = threadIdx.x; i < side; i += blockDim.x) xc[i] = make_double2(xc[i].x * inv, xc[i].y * inv);
+        __syncthreads();
+      }
+    }
+    for (int x = threadIdx.x; x < nb * side; x += blockDim.x) Q[static_cast<int64_t>(j0) * side + x] = pan[x];
     __syncthreads();
   }
 }
@@ -1043,6 +1156,20 @@ uint64_t mid_ws_layout(uint64_t side, uint32_t nblocks, int S, uint64_t* off) {
   return o;
 }
 
+// Orthonormal bases of the selected columns: BCGS2 with a shared-memory panel of up to
+// kPanelMax columns when at least two fit, else column-by-column CGS2.
+void launch_basis(const MidArgs& a, uint32_t nblocks, int which, cudaStream_t st) {
+  const int64_t col_bytes = a.side * static_cast<int64_t>(sizeof(double2));
+  int pw = static_cast<int>(std::min<int64_t>(kPanelMax, (200 * 1024) / col_bytes));
+  if (getenv("BF_CGS2")) pw = 0;
+  if (pw >= 2) {
+    allow_max_dyn_smem(k_bcgs2);
+    k_bcgs2<<<nblocks, 512, static_cast<size_t>(pw) * col_bytes, st>>>(a, which, pw);
+  } else {
+    k_cgs2<<<nblocks, 512, 0, st>>>(a, which);
+  }
+}
+
 bool tree_geometry(uint64_t n, uint32_t levels, uint32_t branching, uint64_t* m, uint64_t* side) {
   if (branching != 2 && branching != 4) return false;
   const uint32_t lb = branching == 4 ? 2 : 1;
@@ -1114,15 +1241,15 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
   const int T = 256;
   const unsigned yfill = static_cast<unsigned>(std::min<uint64_t>(64, (S * side + T - 1) / T));
   const size_t small_smem = S <= kSmemSet ? 3ull * S * S * sizeof(double2) : 0;
-  BF_CUDA(cudaFuncSetAttribute(k_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-  BF_CUDA(cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  BF_CUDA(allow_max_dyn_smem(k_mid));
+  BF_CUDA(allow_max_dyn_smem(k_dense));
   k_init<<<(nblocks + 127) / 128, 128, 0, st>>>(a, block_ij);
   if (dense_branch) {
     k_dense<<<nblocks, T, small_smem, st>>>(a);
   } else {
     const size_t piv_smem = side * sizeof(double) + kSetCap * sizeof(double2) + 32 * 8 + 32 * 4 + kSetCap * 4;
     if (piv_smem > 227 * 1024) return fail(BF_EINVAL, "middle blocks too wide for the pivot kernel");
-    BF_CUDA(cudaFuncSetAttribute(k_pivot_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    BF_CUDA(allow_max_dyn_smem(k_pivot_wide));
     for (uint32_t sw = 0; sw < iters; ++sw) {
       k_union<<<nblocks, 128, 0, st>>>(a, 2 * sw, kRows);
       k_fill_wide<<<dim3(nblocks, yfill), T, 0, st>>>(a, kRows);
@@ -1134,12 +1261,12 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
     k_union<<<nblocks, 128, 0, st>>>(a, 2 * iters, kRows);
     k_union<<<nblocks, 128, 0, st>>>(a, 2 * iters + 1, kCols);
     const size_t tall_smem = (static_cast<size_t>(kGramChunk) * S + (S <= kSmemSet ? 2ull * S * S : 0)) * 16;
-    BF_CUDA(cudaFuncSetAttribute(k_pivot_tall, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    BF_CUDA(allow_max_dyn_smem(k_pivot_tall));
     for (int which : {kCols, kRows}) {
       k_fill_tall<<<dim3(nblocks, yfill), T, 0, st>>>(a, which, 0, a.tall);
       k_pivot_tall<<<nblocks, 512, tall_smem, st>>>(a, which);
       k_fill_tall<<<dim3(nblocks, yfill), T, 0, st>>>(a, which, 1, which == kCols ? a.qc : a.qr);
-      k_cgs2<<<nblocks, 512, 0, st>>>(a, which);
+      launch_basis(a, nblocks, which, st);
     }
     k_mid<<<nblocks, T, small_smem, st>>>(a);
   }
@@ -1202,8 +1329,8 @@ int bf_middle_probes(uint64_t n, uint32_t levels, uint32_t branching, uint32_t r
   const unsigned yfill = static_cast<unsigned>(std::min<uint64_t>(64, (width * side + T - 1) / T));
   const size_t small_smem = S <= kSmemSet ? 3ull * S * S * sizeof(double2) : 0;
   const size_t tall_smem = (static_cast<size_t>(kGramChunk) * S + (S <= kSmemSet ? 2ull * S * S : 0)) * 16;
-  BF_CUDA(cudaFuncSetAttribute(k_mid_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-  BF_CUDA(cudaFuncSetAttribute(k_pivot_tall, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  BF_CUDA(allow_max_dyn_smem(k_mid_probe));
+  BF_CUDA(allow_max_dyn_smem(k_pivot_tall));
   k_init<<<(nblocks + 127) / 128, 128, 0, st>>>(a, block_ij);
   for (int which : {kCols, kRows}) {
     k_fill_probe<<<dim3(nblocks, yfill), T, 0, st>>>(a, which);
@@ -1211,7 +1338,7 @@ int bf_middle_probes(uint64_t n, uint32_t levels, uint32_t branching, uint32_t r
     k_sel_probe<<<dim3(nblocks, yfill), T, 0, st>>>(a, which);
   }
   k_set_probe_counts<<<(nblocks + 127) / 128, 128, 0, st>>>(a);
-  for (int which : {kCols, kRows}) k_cgs2<<<nblocks, 512, 0, st>>>(a, which);
+  for (int which : {kCols, kRows}) launch_basis(a, nblocks, which, st);
   k_mid_probe<<<nblocks, T, small_smem, st>>>(a);
   const unsigned yas = static_cast<unsigned>(std::min<uint64_t>(32, (side * rank + T - 1) / T));
   k_assemble<<<dim3(nblocks, yas), T, 0, st>>>(a);
@@ -1257,7 +1384,7 @@ int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t ro
   if (rows >= branching) {
     const int64_t nprob = static_cast<int64_t>(nb) * branching * pairs;
     const size_t smem = S <= kSmemSet ? rec_smem_elems(static_cast<int>(w), S) * sizeof(double2) : 0;
-    BF_CUDA(cudaFuncSetAttribute(k_recurse_split, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    BF_CUDA(allow_max_dyn_smem(k_recurse_split));
     for (int64_t p0 = 0; p0 < nprob; p0 += chunk) {
       a.p0 = p0;
       const int64_t cnt = std::min<int64_t>(chunk, nprob - p0);
@@ -1285,7 +1412,7 @@ int bf_select_pivots(const void* a, uint32_t batch, uint32_t m, uint32_t n, uint
   const uint64_t kk = k < m ? k : m;
   if (ws_bytes < 16ull * batch * kk * n) return fail(BF_EINVAL, "pivot workspace too small (16*batch*min(k,m)*n bytes)");
   const size_t smem = (n + (n & 1)) * 8 + kSetCap * 16 + 32 * 8 + 32 * 4 + 1024 * 4;
-  BF_CUDA(cudaFuncSetAttribute(k_select_pivots, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  BF_CUDA(allow_max_dyn_smem(k_select_pivots));
   k_select_pivots<<<batch, 512, smem, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const double2*>(a), static_cast<double2*>(workspace), static_cast<int>(m), static_cast<int>(n),
       static_cast<int>(k), rel_tol, pairwise, pivots, counts);
