@@ -966,6 +966,109 @@ __device__ void warp_householder(double2* B, int ldb, int rows, int n) {
   }
 }
 
+// Register-resident TSQR for stacks up to 32 columns wide: lane j of a warp
+// keeps column j of its running R in registers (R[p][j] for p = 0..31, p
+// unrolled), the incoming row chunk sits in shared memory (column-major, odd
+// leading dimension: conflict-free). Reflector p acts on [R[p][:]; chunk]
+// only — the rows of R below p are zero in column p — so a chunk of `ch` rows
+// costs ~2 ch complex FMAs per column per step instead of ~2 (n + ch). Every
+// warp of the CTA streams its own chunks; the warps' R's are then merged
+// pairwise by treating one R as the next warp's chunk.
+constexpr int kTsqrCh = 32;
+
+// Fold the chunk C (rows x n, column-major, leading dimension ldc, in shared
+// memory) into the lane-distributed R.
+__device__ __forceinline__ void tsqr_fold(double2 (&Rc)[32], double2* C, int ldc, int rows, int n) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int p = 0; p < 32; ++p) {
+    if (p >= n) break;
+    const double2* cp = C + p * ldc;
+    double s2 = 0;
+    for (int i = lane; i < rows; i += 32) s2 += cp[i].x * cp[i].x + cp[i].y * cp[i].y;
+    s2 = warp_sum(s2);
+    double2 al;
+    al.x = __shfl_sync(0xffffffffu, Rc[p].x, p);
+    al.y = __shfl_sync(0xffffffffu, Rc[p].y, p);
+    if (s2 == 0.0) continue;  // the chunk column is already zero: nothing to reflect
+    const double aa = hypot(al.x, al.y), nx = sqrt(aa * aa + s2);
+    const double2 beta = aa > 0 ? make_double2(-al.x / aa * nx, -al.y / aa * nx) : make_double2(-nx, 0);
+    const double2 v0 = make_double2(al.x - beta.x, al.y - beta.y);
+    const double f = 2.0 / (v0.x * v0.x + v0.y * v0.y + s2);
+    if (lane > p && lane < n) {
+      double2* cj = C + lane * ldc;
+      double2 d0 = cmulc(v0, Rc[p]), d1 = make_double2(0, 0);
+      int i = 0;
+      for (; i + 1 < rows; i += 2) {
+        const double2 g0 = cmulc(cp[i], cj[i]), g1 = cmulc(cp[i + 1], cj[i + 1]);
+        d0.x += g0.x;
+        d0.y += g0.y;
+        d1.x += g1.x;
+        d1.y += g1.y;
+      }
+      if (i < rows) {
+        const double2 g0 = cmulc(cp[i], cj[i]);
+        d0.x += g0.x;
+        d0.y += g0.y;
+      }
+      const double2 wj = make_double2((d0.x + d1.x) * f, (d0.y + d1.y) * f);
+      const double2 u = cmul(v0, wj);
+      Rc[p].x -= u.x;
+      Rc[p].y -= u.y;
+      for (i = 0; i < rows; ++i) {
+        const double2 d = cmul(cp[i], wj);
+        cj[i].x -= d.x;
+        cj[i].y -= d.y;
+      }
+    }
+    if (lane == p) Rc[p] = beta;
+    __syncwarp();
+  }
+}
+
+// R (n x n, n <= 32) of the tall (part x n) stack into Rout (row-major, ld ldr).
+// smem: nwarps * (kTsqrCh + 1) * n complex values.
+template <typename F>
+__device__ void tsqr_reg(const F& src, int64_t part, int n, double2* smem, double2* Rout, int ldr) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int ldc = kTsqrCh + 1;
+  double2* C = smem + static_cast<int64_t>(warp) * ldc * n;
+  double2 Rc[32];
+#pragma unroll
+  for (int p = 0; p < 32; ++p) Rc[p] = make_double2(0, 0);
+  const int64_t nchunks = (part + kTsqrCh - 1) / kTsqrCh;
+  for (int64_t cidx = warp; cidx < nchunks; cidx += nw) {
+    const int64_t r0 = cidx * kTsqrCh;
+    const int rows = static_cast<int>((part - r0) < kTsqrCh ? (part - r0) : kTsqrCh);
+    __syncwarp();
+    for (int x = lane; x < rows * n; x += 32) {
+      const int i = x / n, c = x % n;
+      C[c * ldc + i] = src(r0 + i, c);
+    }
+    __syncwarp();
+    tsqr_fold(Rc, C, ldc, rows, n);
+  }
+  // pairwise merge: warp w + step hands its R (as an n-row chunk) to warp w
+  for (int step = 1; step < nw; step *= 2) {
+    __syncthreads();
+    if (warp % (2 * step) == step && lane < n) {
+#pragma unroll
+      for (int p = 0; p < 32; ++p)
+        if (p < n) C[lane * ldc + p] = Rc[p];
+    }
+    __syncthreads();
+    if (warp % (2 * step) == 0 && warp + step < nw)
+      tsqr_fold(Rc, smem + static_cast<int64_t>(warp + step) * ldc * n, ldc, n, n);
+  }
+  __syncthreads();
+  if (warp == 0 && lane < n) {
+#pragma unroll
+    for (int p = 0; p < 32; ++p)
+      if (p < n) Rout[p * ldr + lane] = p <= lane ? Rc[p] : make_double2(0, 0);
+  }
+  __syncthreads();
+}
+
 // R factor of a tall (part x n) stack by TSQR in shared memory: warps stream
 // row chunks into [R_acc; chunk] buffers (column-major, odd ld) and QR them (no
 // block barriers), then combine their R's pairwise. Leaves R (n x n, row-major)
@@ -1068,7 +1171,9 @@ __global__ void k_recurse_split(RecArgs a) {
   } else {
     // tall stack: R factor (TSQR in shared memory when the stack width fits, else a
     // Householder pass in global memory); the SVD of R gives sigma and V; new_u = A V[:, :keep]
-    if (sh) {
+    if (sh && w <= 32) {
+      tsqr_reg(src, part, w, sm2, Mb, ldm);
+    } else if (sh) {
       const int ch = 32;
       const int per = tsqr_ld(w, ch) * w;
       int nwu = static_cast<int>(rec_smem_elems(w, S) / per);
@@ -1383,7 +1488,9 @@ int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t ro
   a.S = S;
   if (rows >= branching) {
     const int64_t nprob = static_cast<int64_t>(nb) * branching * pairs;
-    const size_t smem = S <= kSmemSet ? rec_smem_elems(static_cast<int>(w), S) * sizeof(double2) : 0;
+    size_t smem = S <= kSmemSet ? rec_smem_elems(static_cast<int>(w), S) * sizeof(double2) : 0;
+    if (S <= kSmemSet && w <= 32 && part > S)  // register TSQR: every warp streams its own chunk
+      smem = std::max<size_t>(smem, 8ull * (kTsqrCh + 1) * w * sizeof(double2));
     BF_CUDA(allow_max_dyn_smem(k_recurse_split));
     for (int64_t p0 = 0; p0 < nprob; p0 += chunk) {
       a.p0 = p0;
