@@ -1134,6 +1134,10 @@ __device__ __host__ __forceinline__ int64_t rec_smem_elems(int w, int S) {
   return static_cast<int64_t>(S) * (w + 1) + static_cast<int64_t>(S) * w + static_cast<int64_t>(w) * (w + 1);
 }
 
+// TALL = false: stacks of at most S rows (direct Jacobi); TALL = true: taller stacks
+// (TSQR first). Separate instantiations keep the register TSQR's 128-register R
+// column out of the small-stack kernel, which then fits more CTAs per SM.
+template <bool TALL>
 __global__ void k_recurse_split(RecArgs a) {
   extern __shared__ double2 sm2[];
   __shared__ int flag, perm[kSetCap];
@@ -1158,7 +1162,10 @@ __global__ void k_recurse_split(RecArgs a) {
   double2* W = sh ? sm2 + S * ldm : Vg + 2 * SS;
   double2* Vt = sh ? W + S * w : Vg + 3 * SS;
   const int64_t out_base = ((gb * b + t) * part) * pairs + p;  // new_u.transpose(0,1,3,2,4): row (gb,t,row=0,p)
-  if (part <= S) {
+  // stacks up to S rows go straight to the Jacobi SVD; taller ones through a TSQR first
+  // (the register TSQR for stacks up to 32 columns wide)
+  const bool wreg = sh && w <= 32;
+  if constexpr (!TALL) {
     for (int x = threadIdx.x; x < part * w; x += blockDim.x) Mb[(x / w) * ldm + x % w] = src(x / w, x % w);
     __syncthreads();
     svd_small(Mb, static_cast<int>(part), w, ldm, Ug, S, Vg, S, sg, W, Vt, &flag, perm, ssc);
@@ -1171,7 +1178,7 @@ __global__ void k_recurse_split(RecArgs a) {
   } else {
     // tall stack: R factor (TSQR in shared memory when the stack width fits, else a
     // Householder pass in global memory); the SVD of R gives sigma and V; new_u = A V[:, :keep]
-    if (sh && w <= 32) {
+    if (wreg) {
       tsqr_reg(src, part, w, sm2, Mb, ldm);
     } else if (sh) {
       const int ch = 32;
@@ -1491,11 +1498,13 @@ int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t ro
     size_t smem = S <= kSmemSet ? rec_smem_elems(static_cast<int>(w), S) * sizeof(double2) : 0;
     if (S <= kSmemSet && w <= 32 && part > S)  // register TSQR: every warp streams its own chunk
       smem = std::max<size_t>(smem, 8ull * (kTsqrCh + 1) * w * sizeof(double2));
-    BF_CUDA(allow_max_dyn_smem(k_recurse_split));
+    const bool tall = part > S;
+    void (*kern)(RecArgs) = tall ? k_recurse_split<true> : k_recurse_split<false>;
+    BF_CUDA(allow_max_dyn_smem(kern));
     for (int64_t p0 = 0; p0 < nprob; p0 += chunk) {
       a.p0 = p0;
       const int64_t cnt = std::min<int64_t>(chunk, nprob - p0);
-      k_recurse_split<<<static_cast<unsigned>(cnt), 256, smem, st>>>(a);
+      kern<<<static_cast<unsigned>(cnt), 256, smem, st>>>(a);
     }
   } else {
     const int64_t nprob = static_cast<int64_t>(nb) * pairs;

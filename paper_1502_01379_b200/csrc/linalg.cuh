@@ -272,6 +272,145 @@ __device__ void svd_small(const double2* M, int m, int n, int ld, double2* U, in
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- warp Jacobi SVD
+// Round-robin partner of column j in round r over nn (even) columns: i + j = r
+// (mod nn - 1) pairs i with j; the column with 2 j = r pairs with nn - 1.
+__device__ __forceinline__ int rr_partner(int j, int r, int nn) {
+  const int q = nn - 1;
+  if (j >= nn) return j;
+  if (j == q) return (r * (nn >> 1)) % q;
+  int p = (r - j) % q;
+  if (p < 0) p += q;
+  return p == j ? q : p;
+}
+
+// One warp: one-sided Jacobi SVD of a small matrix. Lane j holds column j of the
+// worked (tall, rr >= cc, rr, cc <= 32) matrix in registers and column j of V in
+// the shared scratch Vs (column-major, odd leading dimension 33: conflict-free);
+// each round every lane fetches its partner's column by shuffles and both lanes of
+// a pair evaluate the same rotation from the same fixed-order sums (deterministic,
+// identical in both lanes). The worked matrix is M (tall) or M^H (wide) with
+// M(i, c) = src[i * rs + c * cs]. Outputs exactly as svd_small: U (m x k), sig
+// (k), Vo (n x k), k = min(m, n), singular values descending (ties by index).
+// Vs: 2 * 32 * 33 complex values of shared memory owned by this warp.
+constexpr int kWarpSvdLd = 33;
+
+__device__ void warp_svd(const double2* src, int m, int n, int rs, int cs, double2* U, int ldu, double2* Vo,
+                         int ldv, double* sig, double2* Vs) {
+  const int lane = threadIdx.x & 31;
+  const bool tall = m >= n;
+  const int rr = tall ? m : n, cc = tall ? n : m;  // worked matrix: rr x cc, columns on lanes
+  double2 a[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    double2 x = make_double2(0, 0);
+    if (lane < cc && k < rr) x = tall ? src[k * rs + lane * cs] : cconj(src[lane * rs + k * cs]);
+    a[k] = x;
+  }
+  // V double-buffered in shared memory: a rotated lane writes its new column to the
+  // other buffer and flips `cur`; a partner reads the slot of the buffer `cur` names
+  constexpr int kVbuf = 32 * kWarpSvdLd;
+  int cur = 0;
+  for (int k = 0; k < cc; ++k) Vs[lane * kWarpSvdLd + k] = make_double2(k == lane ? 1.0 : 0.0, 0.0);
+  __syncwarp();
+  const int nn = cc + (cc & 1);
+  const double tol = (rr > 8 ? rr : 8) * 2.220446049250313e-16;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    bool rotated = false;
+    for (int round = 0; round < nn - 1; ++round) {
+      const int pj = rr_partner(lane, round, nn);
+      const bool valid = lane < cc && pj < cc;
+      const bool low = lane < pj;
+      // own / partner sums; the pair's lower column is "x": both lanes then hold the
+      // same (al, be, g) bit for bit (the upper lane's cross sum is the exact conjugate)
+      double no = 0, np = 0;
+      double2 d = make_double2(0, 0);
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        double2 pk;
+        pk.x = __shfl_sync(0xffffffffu, a[k].x, pj);
+        pk.y = __shfl_sync(0xffffffffu, a[k].y, pj);
+        if (k < rr) {
+          // explicitly rounded (no FMA contraction): the upper lane's terms are then the
+          // exact conjugates of the lower lane's, and both norms the same sums
+          no = __dadd_rn(no, __dadd_rn(__dmul_rn(a[k].x, a[k].x), __dmul_rn(a[k].y, a[k].y)));
+          np = __dadd_rn(np, __dadd_rn(__dmul_rn(pk.x, pk.x), __dmul_rn(pk.y, pk.y)));
+          d.x = __dadd_rn(d.x, __dadd_rn(__dmul_rn(a[k].x, pk.x), __dmul_rn(a[k].y, pk.y)));
+          d.y = __dadd_rn(d.y, __dsub_rn(__dmul_rn(a[k].x, pk.y), __dmul_rn(a[k].y, pk.x)));
+        }
+      }
+      const double al = low ? no : np, be = low ? np : no;
+      const double2 g = low ? d : cconj(d);
+      const double g2 = g.x * g.x + g.y * g.y;
+      const bool rot = valid && !(g2 == 0.0 || g2 <= tol * tol * al * be);
+      if (rot) rotated = true;
+      // own' = ca own + cb partner: the lower lane (own = x) takes ca = c, cb = -s e^{-i phi};
+      // the upper (own = y) ca = c e^{-i phi}, cb = s — [x', y'] = [x, y] [[c, s],
+      // [-s e^{-i phi}, c e^{-i phi}]]. Every lane shuffles (uniform control flow).
+      double2 ca = make_double2(1, 0), cb = make_double2(0, 0);
+      if (rot) {
+        const double ig = rsqrt(g2);
+        const double zeta = (be - al) * 0.5 * ig;
+        const double az = fabs(zeta), sgn = zeta >= 0 ? 1.0 : -1.0;
+        const double t = az > 1e150 ? sgn * 0.5 / az : sgn / (az + sqrt(1.0 + zeta * zeta));
+        const double c = rsqrt(1.0 + t * t), s_ = c * t;
+        const double2 ph = make_double2(g.x * ig, -g.y * ig);  // e^{-i phi}
+        ca = low ? make_double2(c, 0) : make_double2(c * ph.x, c * ph.y);
+        cb = low ? make_double2(-s_ * ph.x, -s_ * ph.y) : make_double2(s_, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        double2 pk;
+        pk.x = __shfl_sync(0xffffffffu, a[k].x, pj);
+        pk.y = __shfl_sync(0xffffffffu, a[k].y, pj);
+        if (rot && k < rr) {
+          const double2 u = cmul(ca, a[k]), w = cmul(cb, pk);
+          a[k] = make_double2(u.x + w.x, u.y + w.y);
+        }
+      }
+      // V columns: read mine and the partner's current ones, write mine to the other buffer
+      const int pcur = __shfl_sync(0xffffffffu, cur, pj);
+      if (rot) {
+        const double2* vm = Vs + cur * kVbuf + lane * kWarpSvdLd;
+        const double2* vp = Vs + pcur * kVbuf + pj * kWarpSvdLd;
+        double2* vn = Vs + (cur ^ 1) * kVbuf + lane * kWarpSvdLd;
+        for (int k = 0; k < cc; ++k) {
+          const double2 u = cmul(ca, vm[k]), w = cmul(cb, vp[k]);
+          vn[k] = make_double2(u.x + w.x, u.y + w.y);
+        }
+        cur ^= 1;
+      }
+      __syncwarp();
+    }
+    if (!__any_sync(0xffffffffu, rotated)) break;
+  }
+  // column norms (fixed order), descending rank (ties by index)
+  double nrm = 0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    if (k < rr) nrm += a[k].x * a[k].x + a[k].y * a[k].y;
+  nrm = lane < cc ? sqrt(nrm) : -1.0;
+  int rank = 0;
+  for (int d = 0; d < cc; ++d) {
+    const double o = __shfl_sync(0xffffffffu, nrm, d);
+    rank += (o > nrm) || (o == nrm && d < lane);
+  }
+  if (lane < cc) {
+    sig[rank] = nrm;
+    // left vectors of the worked matrix: a / sigma ; right vectors: V
+    double2* L = tall ? U : Vo;
+    const int ldl = tall ? ldu : ldv;
+    double2* R = tall ? Vo : U;
+    const int ldr = tall ? ldv : ldu;
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      if (k < rr) L[k * ldl + rank] = nrm > 0 ? make_double2(a[k].x / nrm, a[k].y / nrm) : make_double2(0, 0);
+    const double2* vm = Vs + cur * kVbuf + lane * kWarpSvdLd;
+    for (int k = 0; k < cc; ++k) R[k * ldr + rank] = vm[k];
+  }
+  __syncwarp();
+}
+
 // floored_inverse (lowrank.py:79-87): 1/sigma where sigma > PINV_FLOOR * max, else 0.
 __device__ __forceinline__ double floored_inv(double s, double smax) {
   return s > kPinvFloor * smax ? 1.0 / s : 0.0;
