@@ -860,6 +860,7 @@ struct RecArgs {
   double2* nxt;         // next cur
   double2* g;           // transfer blocks of this level
   double2* scr;         // per-problem scratch
+  double2* rbuf;        // tall stacks up to 32 wide: R (w x w, row-major) per problem of the chunk
   int64_t nb, rows, pairs;
   int r, b, S;          // rank, branching, small-matrix capacity (64: shared memory; 128: global)
   int64_t p0;
@@ -1134,11 +1135,25 @@ __device__ __host__ __forceinline__ int64_t rec_smem_elems(int w, int S) {
   return static_cast<int64_t>(S) * (w + 1) + static_cast<int64_t>(S) * w + static_cast<int64_t>(w) * (w + 1);
 }
 
+// Register TSQR of every tall stack (up to 32 wide) of the chunk: R -> a.rbuf.
+// Its own kernel: the 128-register R columns would otherwise cap the SVD kernel
+// at one CTA per SM; here all 8 warps stream chunks, there the Jacobi runs 2 per SM.
+__global__ void k_recurse_tsqr(RecArgs a) {
+  extern __shared__ double2 sm2[];
+  const int64_t prob = a.p0 + blockIdx.x;
+  const int b = a.b;
+  const int64_t pairs = a.pairs, part = a.rows / b;
+  const int w = b * a.r;
+  const int64_t gb = prob / (b * pairs), t = (prob / pairs) % b, p = prob % pairs;
+  auto src = [&](int64_t row, int c) { return a.cur[((gb * a.rows + t * part + row) * pairs + p) * w + c]; };
+  tsqr_reg(src, part, w, sm2, a.rbuf + static_cast<int64_t>(blockIdx.x) * w * w, w);
+}
+
 // TALL = false: stacks of at most S rows (direct Jacobi); TALL = true: taller stacks
-// (TSQR first). Separate instantiations keep the register TSQR's 128-register R
-// column out of the small-stack kernel, which then fits more CTAs per SM.
+// (R from k_recurse_tsqr when the stack is at most 32 wide, else a TSQR / Householder
+// pass here).
 template <bool TALL>
-__global__ void k_recurse_split(RecArgs a) {
+__global__ void __launch_bounds__(256, 2) k_recurse_split(RecArgs a) {
   extern __shared__ double2 sm2[];
   __shared__ int flag, perm[kSetCap];
   __shared__ double ssc[kSetCap], sg[kSetCap], red[32];
@@ -1179,7 +1194,9 @@ __global__ void k_recurse_split(RecArgs a) {
     // tall stack: R factor (TSQR in shared memory when the stack width fits, else a
     // Householder pass in global memory); the SVD of R gives sigma and V; new_u = A V[:, :keep]
     if (wreg) {
-      tsqr_reg(src, part, w, sm2, Mb, ldm);
+      const double2* R = a.rbuf + static_cast<int64_t>(blockIdx.x) * w * w;
+      for (int x = threadIdx.x; x < w * w; x += blockDim.x) Mb[(x / w) * ldm + x % w] = R[x];
+      __syncthreads();
     } else if (sh) {
       const int ch = 32;
       const int per = tsqr_ld(w, ch) * w;
@@ -1474,7 +1491,9 @@ int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t ro
   const int64_t pairs = groups / branching;
   const int64_t part = rows / branching;
   const int64_t chunk = 2048;
-  const uint64_t need = rows >= branching ? static_cast<uint64_t>(chunk) * rec_scratch_elems(part, w, S) * 16 : 0;
+  const bool reg_tsqr = rows >= branching && S <= kSmemSet && w <= 32 && part > S;
+  const uint64_t scr_bytes = rows >= branching ? static_cast<uint64_t>(chunk) * rec_scratch_elems(part, w, S) * 16 : 0;
+  const uint64_t need = scr_bytes + (reg_tsqr ? static_cast<uint64_t>(chunk) * w * w * 16 : 0);
   if (!workspace) {
     *ws_bytes = need;
     return BF_OK;
@@ -1495,15 +1514,17 @@ int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t ro
   a.S = S;
   if (rows >= branching) {
     const int64_t nprob = static_cast<int64_t>(nb) * branching * pairs;
-    size_t smem = S <= kSmemSet ? rec_smem_elems(static_cast<int>(w), S) * sizeof(double2) : 0;
-    if (S <= kSmemSet && w <= 32 && part > S)  // register TSQR: every warp streams its own chunk
-      smem = std::max<size_t>(smem, 8ull * (kTsqrCh + 1) * w * sizeof(double2));
+    const size_t smem = S <= kSmemSet ? rec_smem_elems(static_cast<int>(w), S) * sizeof(double2) : 0;
+    const size_t tsqr_smem = 8ull * (kTsqrCh + 1) * w * sizeof(double2);  // every warp streams its own chunk
+    a.rbuf = reg_tsqr ? reinterpret_cast<double2*>(static_cast<char*>(workspace) + scr_bytes) : nullptr;
+    if (reg_tsqr) BF_CUDA(allow_max_dyn_smem(k_recurse_tsqr));
     const bool tall = part > S;
     void (*kern)(RecArgs) = tall ? k_recurse_split<true> : k_recurse_split<false>;
     BF_CUDA(allow_max_dyn_smem(kern));
     for (int64_t p0 = 0; p0 < nprob; p0 += chunk) {
       a.p0 = p0;
       const int64_t cnt = std::min<int64_t>(chunk, nprob - p0);
+      if (reg_tsqr) k_recurse_tsqr<<<static_cast<unsigned>(cnt), 256, tsqr_smem, st>>>(a);
       kern<<<static_cast<unsigned>(cnt), 256, smem, st>>>(a);
     }
   } else {
