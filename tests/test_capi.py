@@ -66,3 +66,37 @@ def test_error_mapping():
         _lib.check(_lib.BF_ENOMEM)
     with pytest.raises(RuntimeError):
         _lib.check(_lib.BF_ECUDA)
+
+
+def test_construction_entry_points_validate_without_a_gpu():
+    """Argument checks of the construction / Hankel entry points fail with BF_EINVAL
+    before any device work (reference-side errors: ValueError)."""
+    lib = _lib.load()
+    # workspace queries: 0 for unsupported geometry, > 0 otherwise
+    assert lib.bf_middle_workspace_bytes(1000, 6, 2, 4, 3, 1) == 0
+    assert lib.bf_middle_workspace_bytes(1024, 6, 2, 4, 3, 1) > 0
+    assert lib.bf_probe_workspace_bytes(1024, 6, 2, 4, 9, 1) > 0
+    assert lib.bf_probe_workspace_bytes(1024, 6, 2, 4, 0, 1) == 0
+    assert lib.bf_probe_workspace_bytes(1024, 6, 2, 4, 200, 1) == 0
+    nul = None
+    # width outside [r, min(side, 128)], rank above side, too-narrow products, bad geometry
+    for args in ((1024, 6, 2, 4, 3, 4), (1024, 6, 2, 4, 20, 4), (1024, 6, 2, 40, 40, 4), (1000, 6, 2, 4, 9, 4)):
+        n, levels, b, r, width, nblocks = args
+        rc = lib.bf_middle_probes(n, levels, b, r, width, nblocks, nul, nul, 8 * width, nul, 8 * width, nul, nul, nul,
+                                  nul, nul, 0, nul)
+        assert rc == _lib.BF_EINVAL, args
+    # products narrower than m * width (m = 8 middle nodes at n=1024, L=6)
+    rc = lib.bf_middle_probes(1024, 6, 2, 4, 9, 4, nul, nul, 8 * 9 - 1, nul, 8 * 9, nul, nul, nul, nul, nul, 0, nul)
+    assert rc == _lib.BF_EINVAL
+    # Hankel sweeps: null pointers, row stride below the order count, start below max_order + 15
+    assert lib.bf_hankel_orders(nul, 4, 7, 100, nul, 8, nul) == _lib.BF_EINVAL
+    buf = (ctypes.c_double * 4)()
+    assert lib.bf_hankel_orders(buf, 4, 7, 100, buf, 7, nul) == _lib.BF_EINVAL
+    assert lib.bf_hankel_orders(buf, 4, 7, 10, buf, 8, nul) == _lib.BF_EINVAL
+    assert lib.bf_hankel_orders(buf, 0, 7, 100, buf, 8, nul) == _lib.BF_OK   # empty batch: no work
+    # recursion: bad branching / geometry
+    need = ctypes.c_uint64(0)
+    assert lib.bf_recurse_level(4, 3, 1, 16, 8, nul, nul, nul, nul, ctypes.byref(need), nul) == _lib.BF_EINVAL
+    assert lib.bf_recurse_level(4, 2, 1, 16, 7, nul, nul, nul, nul, ctypes.byref(need), nul) == _lib.BF_EINVAL
+    assert lib.bf_recurse_level(4, 2, 1, 16, 8, nul, nul, nul, nul, ctypes.byref(need), nul) == _lib.BF_OK
+    assert need.value > 0
