@@ -64,7 +64,7 @@ template <typename E>
 constexpr Shape stream_shape() {
   return sizeof(E) == 8 ? kStream64 : kStream;
 }
-constexpr Shape kMrhs{2, 8, 1, 100 * 1024};
+constexpr Shape kMrhs{2, 8, 1, 112 * 1024};
 constexpr uint32_t kMrhsMinK = 8;
 
 // Padded shared-memory rows for the DMMA consumer (BF_NO_PAD=1 turns them off).
