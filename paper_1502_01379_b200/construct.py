@@ -124,13 +124,17 @@ class MiddleSampler:
         self.branching = getattr(p, "branching", 2)
         self.dense_branch = r * params.q >= self.side
         self._all_draws = None
+        self._row0 = 0
 
-    def prepare_draws(self):
-        """Draw tables of every middle block up front (process pool), consumed per batch."""
+    def prepare_draws(self, rows=None):
+        """Draw tables of the middle blocks of block rows `rows` (default: all) up front
+        (process pool), consumed per batch."""
         if not self.dense_branch and self._all_draws is None:
             m = self.m
+            rows = range(m) if rows is None else rows
+            self._row0 = rows.start
             self._all_draws = draw_tables(self.seed, self.side, self.r, self.params,
-                                          [(i, j) for i in range(m) for j in range(m)])
+                                          [(i, j) for i in rows for j in range(m)])
 
     def blocks(self, ij):
         """(u0*sigma0, v0*sigma0, floored_inverse(sigma0)) for blocks ij, on the device."""
@@ -145,7 +149,8 @@ class MiddleSampler:
         if self.dense_branch:
             draws_d = None
         elif self._all_draws is not None:
-            draws_d = torch.from_numpy(np.ascontiguousarray(self._all_draws[ij[:, 0] * self.m + ij[:, 1]])).cuda()
+            idx = (ij[:, 0] - self._row0) * self.m + ij[:, 1]
+            draws_d = torch.from_numpy(np.ascontiguousarray(self._all_draws[idx])).cuda()
         else:
             draws_d = torch.from_numpy(draw_tables(self.seed, side, r, self.params, ij.tolist())).cuda()
         wsb = int(self.lib.bf_middle_workspace_bytes(self.p.n, self.p.levels, self.branching, r, self.params.q, nb))
@@ -444,3 +449,109 @@ def factorize(oracle, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0,
     del v_full
     (u_outer, g_chain), (v_outer, h_chain) = sides
     return ButterflyFactors(p, r, u_outer, g_chain, MiddleFactor(weights), h_chain, v_outer)
+
+
+def _dist_exchange(group=None):
+    """All-to-all of equal per-part chunks (leading dim = parts) over torch.distributed."""
+    def run(send):
+        import torch
+        import torch.distributed as dist
+        recv = torch.empty_like(send)
+        sr = torch.view_as_real(send) if send.is_complex() else send
+        rr = torch.view_as_real(recv) if recv.is_complex() else recv
+        dist.all_to_all_single(rr.reshape(-1), sr.reshape(-1), group=group)
+        return recv
+
+    def gather(rows):
+        import torch
+        import torch.distributed as dist
+        out = [torch.empty_like(rows) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(out, rows.contiguous(), group=group)
+        return torch.cat(out)
+
+    return run, gather
+
+
+def factorize_part(oracle, p: DyadicPartition, r: int, part: int, nparts: int, params=DEFAULT_PARAMS, seed=0,
+                   exchange=None, gather=None, device="cuda", blocks_fn=None, recurse_fn=None) -> dict:
+    """Part `part` of `nparts` of a node-sharded sampling construction (SURVEY.md §8(e):
+    "construction shards trivially over (i, j) middle blocks"): returns the slices
+    ``sharded.shard_slices(factorize(...), part, nparts)`` would cut — bit for bit, since
+    every block draws from its own SeedSequence(seed, spawn_key=(0, i, j)).
+
+    Part d computes the middle blocks of its rows i in I_d (all columns j) and recurses
+    its U slabs into its G / U^L slices. Each block's v0 sigma0 belongs to the owner of
+    column j: one all-to-all per row step moves (m/P) x side x r complex values to every
+    part; the V slabs a part then holds are recursed into its H / V^L slices. The weight
+    rows are all-gathered (the sharded apply scales by W[:, J_d] in its pack / push).
+
+    exchange(send (P, ...)) -> recv (P, ...) and gather(rows) -> all rows default to
+    torch.distributed (NCCL on GPUs); blocks_fn / recurse_fn default to the device
+    kernels (tests substitute host fakes to check the orchestration)."""
+    import torch
+    m, side = p.mid_nodes, p.mid_side
+    if m % nparts:
+        raise ValueError(f"{nparts} parts do not divide the {m} middle nodes")
+    if r < 1:
+        raise ValueError(f"rank must be positive, got {r}")
+    mp = m // nparts
+    own = range(part * mp, (part + 1) * mp)
+    if exchange is None or gather is None:
+        if nparts == 1:
+            exchange, gather = (lambda x: x.clone()), (lambda x: x)
+        else:
+            exchange, gather = _dist_exchange()
+    if blocks_fn is None:
+        if not is_entry_oracle(oracle):
+            raise ValueError("the sharded construction needs an entry oracle")
+        ms = MiddleSampler(oracle, p, r, params, seed)
+        if mp * m >= 1024:
+            ms.prepare_draws(own)
+        blocks_fn, step = ms.blocks, ms.batch_rows()
+    else:
+        step = max(1, min(mp, 2))
+    recurse_fn = recurse if recurse_fn is None else recurse_fn
+    shapes, leaf_shape = level_geometry(p, r)
+    cplx = torch.complex128
+
+    def part_chain():
+        chain = {lvl: torch.zeros((shape[0] // nparts,) + tuple(shape[1:]), dtype=cplx, device=device)
+                 for lvl, _, shape in shapes}
+        leaf = torch.zeros((leaf_shape[0] // nparts,) + tuple(leaf_shape[1:]), dtype=cplx, device=device)
+        return chain, leaf
+
+    w_rows = torch.zeros((mp, m, r), dtype=torch.float64, device=device)
+    v_slabs = torch.zeros((mp, side, m, r), dtype=cplx, device=device)   # [j local, row, i, rho]
+    u_chain, u_leaf = part_chain()
+    kb = recursion_batch(m, side, r)
+    buf = torch.empty((min(kb, mp), side, m, r), dtype=cplx, device=device)
+    filled, first = 0, 0
+    for s0 in range(0, mp, step):
+        rows = list(own[s0:s0 + step])
+        uu, vv, ww = blocks_fn([(i, j) for i in rows for j in range(m)])
+        nr = len(rows)
+        vv = vv.reshape(nr, nparts, mp, side, r)                  # [row i, owner e of j, j local, ., .]
+        recv = exchange(vv.permute(1, 0, 2, 3, 4).contiguous())   # [source e, row step, j local (mine), ., .]
+        for e in range(nparts):
+            for idx in range(nr):
+                v_slabs[:, :, e * mp + s0 + idx, :] = recv[e, idx]
+        for idx, i in enumerate(rows):
+            sl = slice(idx * m, (idx + 1) * m)
+            w_rows[i - own.start] = ww[sl]
+            buf[filled] = uu[sl].permute(1, 0, 2)                  # slab[:, j, :]
+            if filled == 0:
+                first = i - own.start
+            filled += 1
+            if filled == buf.shape[0] or i == own[-1]:
+                leaf_k, pieces = recurse_fn(buf[:filled], p, r)
+                _place(u_chain, u_leaf, first, filled, leaf_k, pieces)
+                filled = 0
+    del buf
+    weights = gather(w_rows)
+    v_chain, v_leaf = part_chain()
+    for k0 in range(0, mp, kb):
+        cnt = min(kb, mp - k0)
+        leaf_k, pieces = recurse_fn(v_slabs[k0:k0 + cnt], p, r)
+        _place(v_chain, v_leaf, k0, cnt, leaf_k, pieces)
+    return {"u_leaf": u_leaf, "v_leaf": v_leaf, "weights": weights,
+            "g": [(lvl, u_chain[lvl]) for lvl, _, _ in shapes], "h": [(lvl, v_chain[lvl]) for lvl, _, _ in shapes]}

@@ -93,3 +93,72 @@ def test_fused_push_exchange_emulated(n, leaf, r, k, P):
         want = f.plan().apply(g, adjoint=adjoint)
         assert (torch.linalg.norm(got - want) / torch.linalg.norm(want)).item() <= 1e-13
         assert torch.equal(got, emulate(plans, g, adjoint))
+
+
+class _Loopback:
+    """In-process stand-in for the all-to-all / all-gather of factorize_part: parts run in
+    Python threads on one GPU and meet at host barriers (no kernel waits on another)."""
+
+    def __init__(self, n):
+        import threading
+        self.n, self.bar, self.slots = n, threading.Barrier(n), [None] * n
+
+    def exchange(self, part):
+        def run(send):
+            torch.cuda.synchronize()
+            self.slots[part] = send
+            self.bar.wait()
+            recv = torch.stack([self.slots[e][part].clone() for e in range(self.n)])
+            torch.cuda.synchronize()
+            self.bar.wait()
+            return recv
+        return run
+
+    def gather(self, part):
+        def run(rows):
+            torch.cuda.synchronize()
+            self.slots[part] = rows
+            self.bar.wait()
+            out = torch.cat([self.slots[e].clone() for e in range(self.n)])
+            torch.cuda.synchronize()
+            self.bar.wait()
+            return out
+        return run
+
+
+@pytest.mark.parametrize("n,leaf,r,nparts", [(1024, 8, 12, 2), (4096, 16, 8, 4)])
+def test_sharded_construction_bitwise_equal_to_factorize(n, leaf, r, nparts):
+    """factorize_part's slices == shard_slices(factorize(...)) bit for bit (every block has
+    its own SeedSequence, so the split over parts cannot change a number)."""
+    import threading
+
+    from paper_1502_01379_b200 import construct as bc
+    from paper_1502_01379_b200.sharded import shard_slices
+    p = bf.make_partition(n, leaf)
+    ker = bf.FioKernel(n)
+    full = bf.factorize(ker, p, r, seed=3)
+    lb = _Loopback(nparts)
+    out = [None] * nparts
+    errs = []
+
+    def work(d):
+        try:
+            out[d] = bc.factorize_part(ker, p, r, d, nparts, seed=3, exchange=lb.exchange(d), gather=lb.gather(d))
+        except Exception as exc:  # surfaced below
+            errs.append(exc)
+            lb.bar.abort()
+
+    ths = [threading.Thread(target=work, args=(d,)) for d in range(nparts)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=600)
+    assert not errs, errs
+    for d in range(nparts):
+        want = shard_slices(full, d, nparts)
+        got = out[d]
+        assert torch.equal(got["weights"], want["weights"])
+        assert torch.equal(got["u_leaf"], want["u_leaf"]) and torch.equal(got["v_leaf"], want["v_leaf"])
+        for key in ("g", "h"):
+            for (l1, b1), (l2, b2) in zip(got[key], want[key]):
+                assert l1 == l2 and torch.equal(b1, b2), (key, l1)
