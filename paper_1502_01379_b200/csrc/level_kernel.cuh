@@ -329,7 +329,11 @@ __device__ __forceinline__ void consume_tile(const LevelArgs& a, const PeerArgs&
       }
       const E v = acc.sum_conj();
       E& o_ = orow[t.k0 + kk];
-      o_ = a.accumulate ? Cx<E>::make(o_.x + w * v.x, o_.y + w * v.y) : Cx<E>::make(w * v.x, w * v.y);
+      // explicit branch: a select would let the compiler load o_ on every store
+      if (a.accumulate)
+        o_ = Cx<E>::make(o_.x + w * v.x, o_.y + w * v.y);
+      else
+        o_ = Cx<E>::make(w * v.x, w * v.y);
     }
   }
 }
@@ -447,7 +451,10 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, const Peer
         for (int j = 0; j < TN; ++j)
           if (colok[j]) {
             const E v = Cx<E>::make(w * re[i][j], w * im[i][j]);
-            dst[j * LC] = a.accumulate ? Cx<E>::make(dst[j * LC].x + v.x, dst[j * LC].y + v.y) : v;
+            if (a.accumulate)
+              dst[j * LC] = Cx<E>::make(dst[j * LC].x + v.x, dst[j * LC].y + v.y);
+            else
+              dst[j * LC] = v;
           }
       }
     }
@@ -595,7 +602,10 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
           if (n >= kc) continue;
           const double2 v = make_double2(w * cr[i][j][q], w * ci[i][j][q]);
           double2& o = orow[n];
-          o = (a.adjoint && a.accumulate) ? make_double2(o.x + v.x, o.y + v.y) : v;
+          if (a.adjoint && a.accumulate)
+            o = make_double2(o.x + v.x, o.y + v.y);
+          else
+            o = v;
         }
     }
   }
