@@ -169,7 +169,8 @@ __device__ int pivot_rows_core(const double2* W, int nr, int ncols, int k, doubl
     double2* prow = Rm + static_cast<int64_t>(npick) * ncols;
     for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
       double2 g = make_double2(0, 0);
-      for (int i = 0; i < nr; ++i) {
+#pragma unroll 8
+      for (int i = 0; i < nr; ++i) {  // unrolled: 8 independent loads in flight per thread
         const double2 t = cmulc(q[i], W[static_cast<int64_t>(i) * ncols + c]);
         g.x += t.x;
         g.y += t.y;
@@ -481,6 +482,7 @@ __global__ void __launch_bounds__(512) k_bcgs2(MidArgs a, int which, int pw) {
           double2 acc[kPanelMax];
 #pragma unroll
           for (int b = 0; b < kPanelMax; ++b) acc[b] = make_double2(0, 0);
+#pragma unroll 4
           for (int i = lane; i < side; i += 32) {
             const double2 q = ql[i];
 #pragma unroll
@@ -504,6 +506,7 @@ __global__ void __launch_bounds__(512) k_bcgs2(MidArgs a, int which, int pw) {
           double2 v[kPanelMax];
 #pragma unroll
           for (int b = 0; b < kPanelMax; ++b) v[b] = b < nb ? pan[b * side + i] : make_double2(0, 0);
+#pragma unroll 4
           for (int l = 0; l < j0; ++l) {
             const double2 q = Q[static_cast<int64_t>(l) * side + i];
 #pragma unroll
