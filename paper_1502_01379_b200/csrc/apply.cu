@@ -6,10 +6,12 @@
 //   adjoint:  U^L*  -> G^{L-1}* .. G^{h}*  -> M* -> H^{h} .. H^{L-1} -> V^L
 // with M (or M*) fused into the epilogue of the last adjoint-direction level.
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
 #include "level_kernel.cuh"
+#include "pair_kernel.cuh"
 #include "plan.h"
 
 namespace bfly {
@@ -254,6 +256,79 @@ int launch_middle(const Plan& pl, const void* in, void* out, uint32_t k, int adj
 
 namespace {
 
+// Level pairs (pair_kernel.cuh): two adjacent splitting transfer levels i, i + 1 of a
+// binary-tree complex128 plan in one kernel when the whole item (8 blocks + 2C vector
+// rows, all right-hand sides) double-buffers in shared memory next to the 2C-row
+// intermediate. BF_NO_PAIR=1 turns it off.
+bool pair_disabled() {
+  static const bool off = [] {
+    const char* e = getenv("BF_NO_PAIR");
+    return e && *e && *e != '0';
+  }();
+  return off;
+}
+
+constexpr int kPairStages = 2, kPairNcw = 8;
+
+struct PairGeo {
+  uint32_t fld, vld, stage_elems;
+  size_t smem;
+};
+
+bool pair_geometry(const Plan& pl, int i, uint32_t k, int adjoint, PairGeo* pg) {
+  // k >= 64: below, the single-level kernel is faster (cfg1 at k = 32: 0.18 vs 0.20 ms)
+  if (pair_disabled() || pl.dtype != BF_C128 || pl.branch != 2 || k < 64 || k > 256) return false;
+  if (i < 0 || i + 1 >= static_cast<int>(pl.nlev)) return false;
+  const LevelGeo& A = pl.lev[i];
+  const LevelGeo& B = pl.lev[i + 1];
+  if (!A.splits || !B.splits || A.P < 2 || B.G != 2 * A.G || 2 * B.P != A.P) return false;
+  const uint64_t R = pl.rank, C = 2 * R;
+  auto pad_to = [](uint64_t x, uint64_t target) { return x + (target + 8 - x % 8) % 8; };
+  const uint64_t fld = pad_to(C, adjoint ? 2 : 4), vld = pad_to(k, 2);
+  uint64_t stage = 8 * R * fld + 2 * C * vld;
+  if (stage & 1) ++stage;
+  const uint64_t smem = 128 + (kPairStages * stage + 2 * C * vld) * sizeof(double2);
+  if (smem > static_cast<uint64_t>(kMaxDynSmem)) return false;
+  pg->fld = static_cast<uint32_t>(fld);
+  pg->vld = static_cast<uint32_t>(vld);
+  pg->stage_elems = static_cast<uint32_t>(stage);
+  pg->smem = smem;
+  return true;
+}
+
+int launch_pair(const Plan& pl, const void* fac_a, const void* fac_b, int i, const void* in, void* out, uint32_t k,
+                int adjoint, const PairGeo& pg, cudaStream_t st) {
+  const LevelGeo& A = pl.lev[i];
+  PairArgs a{};
+  a.fac_a = static_cast<const double2*>(fac_a);
+  a.fac_b = static_cast<const double2*>(fac_b);
+  a.in = static_cast<const double2*>(in);
+  a.out = static_cast<double2*>(out);
+  a.r = pl.rank;
+  a.ga = static_cast<uint32_t>(A.G);
+  a.pa = static_cast<uint32_t>(A.P);
+  a.k = k;
+  a.adjoint = adjoint;
+  a.nitems = static_cast<uint32_t>(A.G * A.P / 2);
+  a.fld = pg.fld;
+  a.vld = pg.vld;
+  a.stage_elems = pg.stage_elems;
+  auto* kern = pair_kernel<kPairStages, kPairNcw>;
+  BF_CUDA(allow_max_dyn_smem(kern));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min<uint32_t>(a.nitems, static_cast<uint32_t>(pl.sms)));
+  cfg.blockDim = dim3((kPairNcw + 1) * 32);
+  cfg.dynamicSmemBytes = pg.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BF_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  return 0;
+}
+
 // One factor op, dispatched by kind. `lvl_idx` indexes the plan's level table.
 template <typename E>
 int factor_op(const Plan& pl, int which, int lvl_idx, int adjoint, const void* in, void* out, uint32_t k, int remap,
@@ -292,6 +367,21 @@ int run_down(const Plan& pl, const void* in, E* bufs[2], void* final_dst, uint32
   int rc = timed_op<E>(rec, pl, lead, 0, 1, in, bufs[0], k, 0, st);
   if (rc) return rc;
   for (int i = nl - 1; i >= 0; --i) {
+    // levels i and i - 1 as one pair kernel (not in instrumented runs: per-level timing;
+    // not for the remapped / pushed last level)
+    PairGeo pg{};
+    const int lo = i - 1;
+    if (!rec && std::is_same<E, double2>::value && lo >= 0 && !(lo == 0 && (remap || peers)) &&
+        pair_geometry(pl, lo, k, 1, &pg)) {
+      void* dst = (lo == 0 && final_dst) ? final_dst : bufs[cur ^ 1];
+      const void* fa = down == BF_FACTOR_G ? pl.g_lev[lo] : pl.h_lev[lo];
+      const void* fb = down == BF_FACTOR_G ? pl.g_lev[i] : pl.h_lev[i];
+      rc = launch_pair(pl, fa, fb, lo, bufs[cur], dst, k, 1, pg, st);
+      if (rc) return rc;
+      if (dst == bufs[cur ^ 1]) cur ^= 1;
+      --i;
+      continue;
+    }
     void* dst = (i == 0 && final_dst) ? final_dst : bufs[cur ^ 1];
     rc = timed_op<E>(rec, pl, down, i, 1, bufs[cur], dst, k, i == 0 ? remap : 0, st, i == 0 ? peers : nullptr);
     if (rc) return rc;
@@ -311,6 +401,17 @@ int run_up(const Plan& pl, const void* mid, E* bufs[2], void* out, uint32_t k, i
   const void* src = mid;
   int nxt = (mid == bufs[0]) ? 1 : 0;
   for (int i = 0; i < nl; ++i) {
+    PairGeo pg{};
+    if (!rec && std::is_same<E, double2>::value && pair_geometry(pl, i, k, 0, &pg)) {
+      const void* fa = up == BF_FACTOR_G ? pl.g_lev[i] : pl.h_lev[i];
+      const void* fb = up == BF_FACTOR_G ? pl.g_lev[i + 1] : pl.h_lev[i + 1];
+      int rc = launch_pair(pl, fa, fb, i, src, bufs[nxt], k, 0, pg, st);
+      if (rc) return rc;
+      src = bufs[nxt];
+      nxt ^= 1;
+      ++i;
+      continue;
+    }
     int rc = timed_op<E>(rec, pl, up, i, 0, src, bufs[nxt], k, 0, st);
     if (rc) return rc;
     src = bufs[nxt];

@@ -140,6 +140,9 @@ def test_per_factor_parity(case):
     (1 << 12, 16, 16, 33),    # many-RHS, k not a multiple of the 4-wide register tile
     (1 << 14, 4, 25, 16),     # rank 25 (the 2D configs' rank), 16 RHS
     (1 << 10, 16, 12, 300),   # many RHS: k split across tiles
+    (1 << 12, 4, 6, 64),      # fused level pairs (pair_kernel): r=6, padded rows
+    (1 << 14, 16, 8, 128),    # fused level pairs at 128 RHS
+    (1 << 12, 1, 4, 96),      # fused pairs, odd number of splitting levels per half
 ])
 def test_synthetic_geometries(n, leaf, r, k):
     p = bf.make_partition(n, leaf)
