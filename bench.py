@@ -79,6 +79,20 @@ def algorithmic(f, k, esz):
     return esz * (nnz - nm) + esz // 2 * nm + 2 * esz * f.n * k, 8 * k * (nnz - nm) + 2 * k * nm
 
 
+def launch_flops(f, k):
+    """Algorithmic flops of each launch of the forward chain (8 per complex multiply-add,
+    2 per real-weight scaling of the fused middle factor), in launch order."""
+    p = f.partition
+    nb, n0, r = f.u_outer.blocks.shape
+    out = [("V*", 8 * k * nb * n0 * r)]
+    for tf in reversed(f.h_chain):
+        out.append((f"H{tf.level}*", 8 * k * tf.nnz + (2 * k * f.middle.nnz if tf.level == p.half else 0)))
+    for tf in f.g_chain:
+        out.append((f"G{tf.level}", 8 * k * tf.nnz))
+    out.append(("U", 8 * k * nb * n0 * r))
+    return out
+
+
 def launch_bytes(f, k, esz):
     """Algorithmic bytes of each launch of the forward chain, in launch order:
     factor bytes + input vector + output vector (M is fused into the last H* launch)."""
@@ -487,6 +501,22 @@ def main():
     tr_bytes = sum(b for _, b, _ in tr) / len(tr)
     tr_ms = sum(t for _, _, t in tr) / len(tr)
     share = sum(t for _, _, t in tr) / max(per_launch.sum(), 1e-9)
+    roof = {"bound": "hbm", "achieved": tr_bytes / (tr_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+            "frac": tr_bytes / (tr_ms / 1e3) / 1e9 / hbm_peak,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
+    if k >= 8 and args.dtype == "c128":
+        # many right-hand sides: the transfer levels are FP64 tensor-core (DMMA) bound
+        # (SURVEY.md §8(d)); algorithmic flops (8 per complex multiply-add) per launch
+        lf = launch_flops(f, k)
+        tr_fl = sum(fl for (name, fl) in lf if name[0] in "GH") / len(tr)
+        fp64 = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))
+        dmma_peak = float(fp64["dmma_m8n8k4_tflops"])
+        roof = {"bound": "tensor", "achieved": tr_fl / (tr_ms / 1e3) / 1e12, "peak": dmma_peak, "unit": "TFLOP/s",
+                "frac": tr_fl / (tr_ms / 1e3) / 1e12 / dmma_peak,
+                "peak_source": "profiles/r01_fp64_peaks.json dmma_m8n8k4_tflops (FP64 tensor pipe measured on "
+                               "this pool's B200 by tools/fp64_peak.cu; MEASURED_PEAKS.json has no FP64 figure)",
+                "note": "complex products run as 3 real DMMAs (Gauss form), so the algorithmic rate can exceed "
+                        "the 4-product tensor-pipe rate by up to 4/3"}
 
     # end to end through the public API with pinned host buffers
     g_pin = torch.empty((n, k), dtype=tdt, pin_memory=True)
@@ -541,11 +571,8 @@ def main():
                        "n": n, "rank": r, "levels": p.levels, "rhs": k, "parallelism": f"replicas{world}",
                        "l2": "inputs larger than L2: each step streams "
                              f"{alg_bytes / 1e9:.2f} GB of factors (L2 126 MB)"},
-            "roofline": {"bound": "hbm", "achieved": tr_bytes / (tr_ms / 1e3) / 1e9, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": tr_bytes / (tr_ms / 1e3) / 1e9 / hbm_peak,
-                         "traffic": _ncu_traffic(args.config, args.dtype, k),
-                         "kernel": "level_kernel (transfer levels G/H)", "kernel_share_of_step": share,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+            "roofline": dict(roof, traffic=_ncu_traffic(args.config, args.dtype, k),
+                             kernel="level_kernel (transfer levels G/H)", kernel_share_of_step=share),
             "chain_roofline": {"algorithmic_bytes": alg_bytes, "algorithmic_flops": alg_flops,
                                "achieved_gbs": alg_bytes / (ms_step / 1e3) / 1e9,
                                "frac": alg_bytes / (ms_step / 1e3) / 1e9 / hbm_peak},

@@ -46,6 +46,15 @@ bool dmma_disabled() {
   return off;
 }
 
+// BF_NO_GAUSS=1: four real DMMAs per complex k-step instead of the 3-multiplication form
+bool gauss_disabled() {
+  static const bool off = [] {
+    const char* v = std::getenv("BF_NO_GAUSS");
+    return v && v[0] && v[0] != '0';
+  }();
+  return off;
+}
+
 uint32_t ilog2(uint64_t x) {
   uint32_t l = 0;
   while ((1ull << (l + 1)) <= x) ++l;
@@ -67,7 +76,63 @@ constexpr Shape stream_shape() {
   return sizeof(E) == 8 ? kStream64 : kStream;
 }
 constexpr Shape kMrhs{2, 8, 1, 112 * 1024};
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
+// Many-RHS pipeline shape: depth (<= 8) and stage budget are launch arguments of the
+// STAGES = 0 instantiation (BF_MRHS_STAGES, BF_MRHS_STAGE_KB override them).
+Shape mrhs_shape() {
+  static const Shape s = [] {
+    Shape x = kMrhs;
+    x.stages = std::min(8, std::max(2, env_int("BF_MRHS_STAGES", kMrhs.stages)));
+    x.stage_bytes = static_cast<uint32_t>(env_int("BF_MRHS_STAGE_KB", kMrhs.stage_bytes / 1024)) * 1024;
+    x.ncw = env_int("BF_MRHS_NCW", 0);  // 0: per launch (mrhs_warps)
+    return x;
+  }();
+  return s;
+}
 constexpr uint32_t kMrhsMinK = 8;
+constexpr Shape kTout{3, 8, 1, 0};
+int tout_stages() {
+  static const int n = std::min(8, std::max(2, env_int("BF_TOUT_STAGES", kTout.stages)));
+  return n;
+}
+
+// The DMMA consumer stores its outputs from registers (MRHS = 1) unless BF_TOUT=1 selects
+// the TMA-stored output tiles (MRHS = 2; measured slower at cfg2 k = 256: its 3 stages
+// plus 2 output tiles force 64-RHS tiles, and small tiles lose more than the stores gain)
+bool tout_disabled() {
+  static const bool off = env_int("BF_TOUT", 0) == 0;
+  return off;
+}
+
+using LevelKernel = void (*)(LevelArgs, PeerArgs);
+
+// complex128 3-multiplication DMMA kernels, one instantiation per warp tile (dt):
+// MRHS = 2 (TMA-stored outputs) or 1 (register stores) with 8 or 16 consumer warps
+template <typename E>
+LevelKernel dmma_kernel(bool tout, int ncw, uint32_t dt) {
+  if constexpr (std::is_same<E, double2>::value) {
+    if (tout) {
+      static const LevelKernel t[3] = {level_kernel<double2, 0, 8, 1, 2, false, 0>,
+                                       level_kernel<double2, 0, 8, 1, 2, false, 1>,
+                                       level_kernel<double2, 0, 8, 1, 2, false, 2>};
+      return t[dt];
+    }
+    static const LevelKernel r8[3] = {level_kernel<double2, 0, 8, 1, 1, false, 0>,
+                                      level_kernel<double2, 0, 8, 1, 1, false, 1>,
+                                      level_kernel<double2, 0, 8, 1, 1, false, 2>};
+    static const LevelKernel r16[3] = {level_kernel<double2, 0, 16, 1, 1, false, 0>,
+                                       level_kernel<double2, 0, 16, 1, 1, false, 1>,
+                                       level_kernel<double2, 0, 16, 1, 1, false, 2>};
+    return ncw == 16 ? r16[dt] : r8[dt];
+  } else {
+    return nullptr;
+  }
+}
 
 // Padded shared-memory rows for the DMMA consumer (BF_NO_PAD=1 turns them off).
 bool pad_disabled() {
@@ -101,7 +166,7 @@ template <typename E>
 int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint64_t P, uint64_t units,
                  const void* in, void* out, uint32_t k, int adjoint, int remap, cudaStream_t st,
                  void* const* peers = nullptr) {
-  const Shape sh = k >= kMrhsMinK ? kMrhs : stream_shape<E>();
+  const Shape sh = k >= kMrhsMinK ? mrhs_shape() : stream_shape<E>();
   uint32_t nt_tile = nt;
   auto tile_elems = [&](uint64_t t) { return t * R * C + (adjoint ? t * R : static_cast<uint64_t>(C)); };
   while (nt_tile > 1 && tile_elems(nt_tile) * sizeof(E) > sh.stage_bytes) nt_tile /= 2;
@@ -124,7 +189,11 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
     return fail(BF_EINVAL, "middle vector too long for 32-bit remap indices");
   const bool mrhs = k >= kMrhsMinK;
   constexpr Shape ks = stream_shape<E>();
-  const Shape sh = mrhs ? kMrhs : ks;
+  Shape sh = mrhs ? mrhs_shape() : ks;
+  // complex128 DMMA consumers: 16 warps for the wide quadtree blocks (C = 4r = 100: long
+  // k loops, few warp items per tile; cfg3 0.75 -> 0.59 ms, cfg4b 14.6 -> 11.0 ms), 8
+  // otherwise (cfg2 k = 256: 43.9 vs 47.3 ms; cfg1 0.26 vs 0.32 ms)
+  if (mrhs) sh.ncw = sh.ncw == 16 || sh.ncw == 8 ? sh.ncw : (C > 64 ? 16 : 8);
   LevelArgs a{};
   a.fac = fac;
   a.in = in;
@@ -180,7 +249,7 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   // every bulk copy must move a multiple of 16 bytes between 16-byte aligned addresses:
   // complex128 always does; complex64 needs even block sizes and, when a row is split
   // into k-tiles, even k and kt.
-  a.use_dmma = mrhs && esz == 16 && kt >= 16 && !dmma_disabled();
+  a.use_dmma = mrhs && esz == 16 && kt >= 16 && !dmma_disabled() ? (gauss_disabled() ? 1 : 2) : 0;
   a.bulk = aligned && (esz == 16 || (R % 2 == 0 && C % 2 == 0 && (a.ktiles == 1 || (k % 2 == 0 && kt % 2 == 0))));
   a.fld = C;
   a.vld = 0;
@@ -206,18 +275,75 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
       a.stage_elems = static_cast<uint32_t>(st2);
     }
   }
-  const size_t smem = 128 + static_cast<size_t>(sh.stages) * a.stage_elems * esz;
+  // MRHS = 2 (complex128 DMMA, plain stores or the fused middle remap): 3 stages plus two
+  // shared-memory output tiles drained by TMA bulk stores. Tile shape refit from scratch:
+  // the largest kt (<= 128) whose 3 padded stages + 2 output tiles fit, then as many units
+  // per tile as keep the 8 consumer warps busy.
+  bool tout = a.use_dmma && a.bulk && !accumulate && remap < 3 && !tout_disabled();
+  int stages = sh.stages;
+  if (tout) {
+    auto pad_to = [](uint64_t x, uint64_t target) { return x + (target + 8 - x % 8) % 8; };
+    const uint64_t fld = pad_to(C, adjoint ? 2 : 4);
+    const uint64_t vrows = adjoint ? static_cast<uint64_t>(nt) * R : C;
+    const uint64_t avail = static_cast<uint64_t>(kMaxDynSmem) - 128;
+    bool ok = false;
+    for (uint32_t kt2 = std::min<uint32_t>(k, 128); kt2 >= 16; kt2 /= 2) {
+      const uint32_t kt4 = (kt2 + 3) / 4 * 4;
+      const uint64_t vld = pad_to(kt4, 2), old = kt4 | 1;
+      auto bytes = [&](uint64_t u) {
+        uint64_t stg = u * (static_cast<uint64_t>(nt) * R * fld + vrows * vld);
+        stg += stg & 1;
+        return (tout_stages() * stg + 2 * u * m_out * old) * esz;
+      };
+      if (bytes(1) > avail) continue;
+      const uint64_t nn = kt4 >= 32 ? 32 : 16;  // DMMA warp tile columns (NT x 8)
+      auto witems = [&](uint64_t u) { return u * ((m_out + 15) / 16) * ((kt4 + nn - 1) / nn); };
+      uint64_t U2 = 1;
+      while (nt == ntot && U2 * 2 <= units && witems(U2) < 2 * static_cast<uint64_t>(kTout.ncw) &&
+             bytes(U2 * 2) <= avail)
+        U2 *= 2;
+      uint64_t stg = U2 * (static_cast<uint64_t>(nt) * R * fld + vrows * vld);
+      stg += stg & 1;
+      a.kt = std::min<uint32_t>(kt4, k);
+      a.ktiles = (k + a.kt - 1) / a.kt;
+      a.lgU = ilog2(U2);
+      a.ntiles = static_cast<uint32_t>((units / U2) * a.ktiles);
+      a.fld = static_cast<uint32_t>(fld);
+      a.vld = static_cast<uint32_t>(vld);
+      a.old = static_cast<uint32_t>(old);
+      a.out_elems = static_cast<uint32_t>(U2 * m_out * old);
+      a.stage_elems = static_cast<uint32_t>(stg);
+      U = U2;
+      ok = true;
+      break;
+    }
+    tout = ok;
+    if (tout) stages = tout_stages();
+  }
+  a.stages = static_cast<uint32_t>(stages);
+  if (a.use_dmma) {  // warp tile: the largest that still gives every consumer warp an item
+    const uint64_t ncw = tout ? kTout.ncw : (a.use_dmma == 2 && remap < 3) ? sh.ncw : kMrhs.ncw;
+    auto di = [&](uint64_t mt, uint64_t n8) {
+      return U * ((m_out + 8 * mt - 1) / (8 * mt)) * ((a.kt + 8 * n8 - 1) / (8 * n8));
+    };
+    a.dtile = a.kt >= 32 && di(2, 4) >= ncw ? 0 : (di(2, 2) >= ncw || a.kt < 16) ? 1 : 2;
+    const int forced = env_int("BF_DTILE", -1);
+    if (forced >= 0 && forced <= 2) a.dtile = static_cast<uint32_t>(forced);
+  }
+  const size_t smem = 128 + static_cast<size_t>(stages) * a.stage_elems * esz + (tout ? 2ull * a.out_elems * esz : 0);
   if (smem > 227 * 1024) return fail(BF_EINVAL, "rank too large: one block pair exceeds the shared-memory stage");
   // the peer-push epilogue (remap 3/4) is its own instantiation: compiled into the common
   // kernels it costs the many-RHS paths registers and ~8% (cfg2 k=256)
   const bool push = remap >= 3;
-  void (*kern)(LevelArgs, PeerArgs) =
-      mrhs ? (push ? level_kernel<E, kMrhs.stages, kMrhs.ncw, kMrhs.ctas_per_sm, 1, true>
-                   : level_kernel<E, kMrhs.stages, kMrhs.ncw, kMrhs.ctas_per_sm, 1, false>)
+  const int kncw = tout ? kTout.ncw : (mrhs && (push || a.use_dmma != 2)) ? kMrhs.ncw : sh.ncw;
+  LevelKernel kern =
+      a.use_dmma == 2 && !push ? dmma_kernel<E>(tout, kncw, a.dtile)
+      : mrhs ? (push ? level_kernel<E, 0, kMrhs.ncw, kMrhs.ctas_per_sm, 1, true>
+                     : level_kernel<E, 0, kMrhs.ncw, kMrhs.ctas_per_sm, 1, false>)
            : (push ? level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, true>
                    : level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, false>);
   BF_CUDA(allow_max_dyn_smem(kern));
-  const uint64_t per_sm = smem * sh.ctas_per_sm <= 227 * 1024 ? sh.ctas_per_sm : 1;
+  const uint64_t per_sm = !tout && smem * sh.ctas_per_sm <= 227 * 1024 ? sh.ctas_per_sm : 1;
   const uint64_t grid = std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(pl.sms) * per_sm);
   static const bool dbg = [] {
     const char* e = getenv("BF_DEBUG_LAUNCH");
@@ -226,10 +352,11 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   if (dbg)
     fprintf(stderr, "[bf] level_kernel %s%s R=%u C=%u nt=%u units=%llu k=%u kt=%u U=%llu ntiles=%u grid=%llu smem=%zu dmma=%d\n",
             mrhs ? "mrhs" : "stream", push ? "+push" : "", R, C, nt, static_cast<unsigned long long>(units), k, kt,
-            static_cast<unsigned long long>(U), a.ntiles, static_cast<unsigned long long>(grid), smem, a.use_dmma);
+            static_cast<unsigned long long>(U), a.ntiles, static_cast<unsigned long long>(grid), smem,
+            a.use_dmma + (tout ? 10 : 0));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3((sh.ncw + 1) * 32);
+  cfg.blockDim = dim3((kncw + 1) * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -313,7 +440,7 @@ int launch_pair(const Plan& pl, const void* fac_a, const void* fac_b, int i, con
   a.fld = pg.fld;
   a.vld = pg.vld;
   a.stage_elems = pg.stage_elems;
-  auto* kern = pair_kernel<kPairStages, kPairNcw>;
+  auto* kern = gauss_disabled() ? pair_kernel<kPairStages, kPairNcw, false> : pair_kernel<kPairStages, kPairNcw, true>;
   BF_CUDA(allow_max_dyn_smem(kern));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(std::min<uint32_t>(a.nitems, static_cast<uint32_t>(pl.sms)));

@@ -55,11 +55,16 @@ struct LevelArgs {
   uint32_t m, r;      // middle geometry (remap)
   uint32_t part, mp;  // remap 3/4: this part and middle nodes per part
   int bulk;           // 1: 16-byte aligned, use the TMA bulk engine
-  int use_dmma;       // many-RHS complex128: FP64 tensor-core (mma.sync f64) consumer
+  int use_dmma;       // many-RHS complex128: FP64 tensor-core (mma.sync f64) consumer; 2 = 3-mult (Gauss) products
   // shared-memory row strides (elements) of the staged factor rows (fld, default C)
   // and vector rows (vld, 0 = the tile's kc). The DMMA consumer pads them so its
   // fragment loads hit 8 distinct 16-byte bank groups per quarter warp.
   uint32_t fld, vld;
+  // MRHS = 2 (DMMA consumer, outputs through shared memory + TMA bulk stores): output
+  // tile row stride (odd: conflict-free fragment writes) and elements per output buffer
+  uint32_t old, out_elems;
+  uint32_t stages;    // pipeline depth when the kernel's STAGES template argument is 0 (<= 8)
+  uint32_t dtile;     // DMMA warp tile: 0 = 2 x 4, 1 = 2 x 2, 2 = 1 x 2 (8 x 8 tiles)
 };
 
 // remap 3/4 receive buffers of every part ([sender][own][other local][rho][k]); a
@@ -462,6 +467,11 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, const Peer
 }
 
 // ---------------------------------------------------------------- FP64 tensor cores
+// -x by a sign-bit flip on the integer pipe (a DADD would queue behind DMMAs on the FP64 datapath)
+__device__ __forceinline__ double neg(double x) {
+  return __hiloint2double(__double2hiint(x) ^ static_cast<int>(0x80000000u), __double2loint(x));
+}
+
 // mma.sync m8n8k4 f64 (DMMA): A fragment A[lane/4][lane%4], B fragment
 // B[lane%4][lane/4], C/D fragment C[lane/4][2(lane%4) + q] (layout confirmed on
 // B200 by tools/dmma_layout.cu).
@@ -474,9 +484,15 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // Many-RHS consumer on the FP64 tensor pipe (complex128). Each unit is the
 // complex GEMM of consume_tile_mrhs, split into 4 real DMMAs per k-step
 // (re += Ar Xr - Ai Xi, im += Ar Xi + Ai Xr); a warp owns MT x NT 8x8 tiles.
-template <int MT, int NT, bool PUSH>
+//
+// GAUSS: the 3-multiplication complex product (T1 = Ar Xr, T2 = Ai Xi, T3 = (Ar + Ai)
+// (Xr + Xi); re = T1 - T2, im = T3 - T1 - T2): 3 DMMAs per complex k-step instead of
+// 4, and every accumulator is updated once per k-step (no back-to-back dependent
+// DMMAs). The operand sums are two DADDs on the otherwise idle FP64 pipe; the
+// rounding stays O(eps |A| |X|) per term.
+template <int MT, int NT, bool PUSH, bool GAUSS>
 __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const PeerArgs& pa, uint32_t tile, const double2* st, int warp,
-                                                  int lane, int nwarps) {
+                                                  int lane, int nwarps, double2* ob) {
   const TileGeo t = tile_geo(a, tile);
   const uint32_t U = 1u << a.lgU;
   const uint32_t Pe_mask = (1u << t.lgPe) - 1;
@@ -497,11 +513,18 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
     const uint32_t mt = rest % nmt, ul = rest / nmt;
     const uint32_t m0 = mt * MT * 8, n0 = ntile * NT * 8;
     const uint32_t base = (((ul >> t.lgPe) * a.nt) << t.lgPe) + (ul & Pe_mask);
-    double cr[MT][NT][2], ci[MT][NT][2];
+    // GAUSS: cr = T1, ci = T2, cs = T3; else cr = re, ci = im (cs unused)
+    double cr[MT][NT][2], ci[MT][NT][2], cs[GAUSS ? MT : 1][GAUSS ? NT : 1][2];
 #pragma unroll
     for (int i = 0; i < MT; ++i)
 #pragma unroll
       for (int j = 0; j < NT; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0;
+    if constexpr (GAUSS) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) cs[i][j][0] = cs[i][j][1] = 0;
+    }
     // forward: the A rows this lane reads are fixed (m = m0 + 8i + lane/4)
     uint32_t arow[MT];
 #pragma unroll
@@ -517,8 +540,8 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
       uint32_t jrow = 0;
       if (a.adjoint) {
         const uint32_t kj = kok ? kk : 0;
-        const uint32_t tt = kj / a.R, rho = kj - tt * a.R;
-        jrow = (base + (tt << t.lgPe)) * a.R + rho;
+        const uint32_t tt = (kj >= a.R) + (kj >= 2 * a.R) + (kj >= 3 * a.R);  // nt <= 4: no division
+        jrow = (base + (tt << t.lgPe)) * a.R + (kj - tt * a.R);
       }
       double ar[MT], ai[MT], nai[MT];
 #pragma unroll
@@ -530,12 +553,12 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
             v = fs[static_cast<size_t>(arow[i]) * fld + kk];
           } else {
             v = fs[static_cast<size_t>(jrow) * fld + m];
-            v.y = -v.y;  // A^H
+            v.y = neg(v.y);  // A^H
           }
         }
         ar[i] = v.x;
         ai[i] = v.y;
-        nai[i] = -v.y;
+        nai[i] = neg(v.y);
       }
       double br[NT], bi[NT];
 #pragma unroll
@@ -549,24 +572,75 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
         br[j] = v.x;
         bi[j] = v.y;
       }
-      // two passes over the tiles: the two products accumulated into one register pair
-      // are 2 MT NT instructions apart, not back to back
+      if constexpr (GAUSS) {
+        double as[MT], bs[NT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) as[i] = ar[i] + ai[i];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) bs[j] = br[j] + bi[j];
+        // T1, T2 of every tile first: the operand sums (DADD, which waits for the FP64
+        // datapath behind queued DMMAs) are not needed until 2 MT NT DMMAs later
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            dmma(cr[i][j][0], cr[i][j][1], ar[i], br[j]);
+            dmma(ci[i][j][0], ci[i][j][1], ai[i], bi[j]);
+          }
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma(cs[i][j][0], cs[i][j][1], as[i], bs[j]);
+      } else {
+        // two passes over the tiles: the two products accumulated into one register pair
+        // are 2 MT NT instructions apart, not back to back
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            dmma(cr[i][j][0], cr[i][j][1], ar[i], br[j]);
+            dmma(ci[i][j][0], ci[i][j][1], ar[i], bi[j]);
+          }
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            dmma(cr[i][j][0], cr[i][j][1], nai[i], bi[j]);
+            dmma(ci[i][j][0], ci[i][j][1], ai[i], br[j]);
+          }
+      }
+    }
+    if constexpr (GAUSS) {  // (T1, T2, T3) -> (re, im)
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          dmma(cr[i][j][0], cr[i][j][1], ar[i], br[j]);
-          dmma(ci[i][j][0], ci[i][j][1], ar[i], bi[j]);
-        }
+        for (int j = 0; j < NT; ++j)
 #pragma unroll
-      for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          dmma(cr[i][j][0], cr[i][j][1], nai[i], bi[j]);
-          dmma(ci[i][j][0], ci[i][j][1], ai[i], br[j]);
-        }
+          for (int q = 0; q < 2; ++q) {
+            const double t1 = cr[i][j][q], t2 = ci[i][j][q];
+            cr[i][j][q] = t1 - t2;
+            ci[i][j][q] = cs[i][j][q] - t1 - t2;
+          }
     }
     // epilogue: element (m0 + 8i + lane/4, n0 + 8j + 2(lane%4) + q)
+    if (ob) {  // into the shared-memory output tile (row ul * m_out + m); TMA stores it
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const uint32_t m = m0 + 8 * i + lr;
+        if (m >= m_out) continue;
+        double w = 1;
+        if (a.adjoint && a.remap) remap_row<double2, false>(a, pa, static_cast<size_t>(t.u0 + ul) * a.C + m, &w);
+        double2* orow = ob + static_cast<size_t>(ul * m_out + m) * a.old;
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const uint32_t n = n0 + 8 * j + 2 * lk + q;
+            if (n < kc) orow[n] = make_double2(w * cr[i][j][q], w * ci[i][j][q]);
+          }
+      }
+      continue;
+    }
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
       const uint32_t m = m0 + 8 * i + lr;
@@ -612,15 +686,34 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
 }
 
 // Register-tile shapes of the many-RHS consumer, picked by right-hand sides per tile.
-template <typename E, bool PUSH>
+// DT >= 0: a complex128 instantiation with only the 3-multiplication DMMA consumer of
+// warp tile DT (0 = 2 x 4, 1 = 2 x 2, 2 = 1 x 2), so the register allocation is that
+// variant's alone; DT = -1 dispatches at run time (4-product DMMA, FFMA, complex64).
+template <typename E, bool PUSH, int DT = -1>
 __device__ __forceinline__ void consume_tile_mrhs_any(const LevelArgs& a, const PeerArgs& pa, uint32_t tile, const E* st, int warp,
-                                                      int lane, int nwarps) {
+                                                      int lane, int nwarps, E* ob = nullptr) {
+  if constexpr (DT >= 0 && std::is_same<E, double2>::value) {
+    constexpr int MT = DT == 2 ? 1 : 2, NT = DT == 0 ? 4 : 2;
+    consume_tile_dmma<MT, NT, PUSH, true>(a, pa, tile, st, warp, lane, nwarps, ob);
+    return;
+  }
   if constexpr (std::is_same<E, double2>::value) {
-    if (a.use_dmma) {  // complex128: the FP64 tensor pipe
-      if (a.kt >= 32)
-        consume_tile_dmma<2, 4, PUSH>(a, pa, tile, st, warp, lane, nwarps);
+    if (a.use_dmma == 2) {  // complex128: the FP64 tensor pipe, 3-multiplication products
+      if (a.dtile == 0)
+        consume_tile_dmma<2, 4, PUSH, true>(a, pa, tile, st, warp, lane, nwarps, ob);
+      else if (a.dtile == 1)
+        consume_tile_dmma<2, 2, PUSH, true>(a, pa, tile, st, warp, lane, nwarps, ob);
       else
-        consume_tile_dmma<2, 2, PUSH>(a, pa, tile, st, warp, lane, nwarps);
+        consume_tile_dmma<1, 2, PUSH, true>(a, pa, tile, st, warp, lane, nwarps, ob);
+      return;
+    }
+    if (a.use_dmma) {  // complex128: the FP64 tensor pipe, 4 real products per complex step
+      if (a.dtile == 0)
+        consume_tile_dmma<2, 4, PUSH, false>(a, pa, tile, st, warp, lane, nwarps, ob);
+      else if (a.dtile == 1)
+        consume_tile_dmma<2, 2, PUSH, false>(a, pa, tile, st, warp, lane, nwarps, ob);
+      else
+        consume_tile_dmma<1, 2, PUSH, false>(a, pa, tile, st, warp, lane, nwarps, ob);
       return;
     }
   }
@@ -636,16 +729,53 @@ __device__ __forceinline__ void consume_tile_mrhs_any(const LevelArgs& a, const 
     consume_tile_mrhs<E, 4, 1, 8, PUSH>(a, pa, tile, st, warp, lane, nwarps);
 }
 
-// MRHS = 0: streaming consumer (one output per thread); MRHS = 1: register-tiled GEMM consumer.
-template <typename E, int STAGES, int NCW, int MINB, int MRHS, bool PUSH>
+// MRHS = 2: the output tile of `tile` (rows ul * m_out + m in shared memory, stride
+// a.old) to its global rows, one TMA bulk store per row, issued by the lanes of
+// one warp; each lane commits its own bulk group.
+template <typename E>
+__device__ __forceinline__ void store_tile_rows(const LevelArgs& a, const PeerArgs& pa, uint32_t tile, const E* ob, int lane) {
+  const TileGeo t = tile_geo(a, tile);
+  const uint32_t U = 1u << a.lgU;
+  const uint32_t m_out = a.adjoint ? a.C : a.nt * a.R;
+  const uint32_t P_mask = (1u << a.lgP) - 1;
+  E* out = static_cast<E*>(a.out);
+  for (uint32_t row = lane; row < U * m_out; row += 32) {
+    const uint32_t ul = row / m_out, m = row - ul * m_out;
+    E* dst;
+    if (!a.adjoint) {
+      const uint32_t u = t.u0 + ul;
+      const uint32_t tt = m / a.R, rho = m - tt * a.R;
+      const uint32_t q = ((((u >> a.lgP) * a.ntot) + a.t0 + tt) << a.lgP) + (u & P_mask);
+      dst = out + (static_cast<size_t>(q) * a.R + rho) * a.k + t.k0;
+    } else {
+      typename Cx<E>::R w;
+      dst = remap_row<E, false>(a, pa, static_cast<size_t>(t.u0 + ul) * a.C + m, &w) + t.k0;
+    }
+    bulk_s2g(dst, ob + static_cast<size_t>(row) * a.old, t.kc * static_cast<uint32_t>(sizeof(E)));
+  }
+  bulk_commit();
+}
+
+template <int NCW>
+__device__ __forceinline__ void consumer_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory");
+}
+
+// MRHS = 0: streaming consumer (one output per thread); MRHS = 1: register-tiled GEMM
+// consumer; MRHS = 2: the DMMA consumer with outputs staged in two shared-memory
+// buffers and written by TMA bulk stores, so a tile's stores drain while the next
+// tile computes (no register-to-global store phase in the consumer warps).
+template <typename E, int STAGES, int NCW, int MINB, int MRHS, bool PUSH, int DT = -1>
 __global__ void __launch_bounds__((NCW + 1) * 32, MINB) level_kernel(const LevelArgs a, const PeerArgs pa) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
-  uint64_t* empty = full + STAGES;
+  // STAGES = 0: the depth is a launch argument (a.stages <= 8; 16 barriers fit the 128-byte header)
+  const uint32_t S = STAGES ? STAGES : a.stages;
+  uint64_t* empty = full + (STAGES ? STAGES : 8);
   E* stage0 = reinterpret_cast<E*>(smem_raw + 128);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (uint32_t s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCW);
     }
@@ -659,36 +789,54 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) level_kernel(const Level
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (warp == NCW) {
     const uint64_t pol = policy_evict_first();
-    // the first STAGES tiles' factor blocks are constant: start them before the wait
+    // the first S tiles' factor blocks are constant: start them before the wait
     uint32_t pre = 0;
     if (a.bulk)
-      for (uint32_t tile = blockIdx.x; tile < a.ntiles && pre < STAGES; tile += gridDim.x, ++pre)
+      for (uint32_t tile = blockIdx.x; tile < a.ntiles && pre < S; tile += gridDim.x, ++pre)
         produce_factors<E>(a, tile_geo(a, tile), stage0 + static_cast<size_t>(pre) * a.stage_elems, &full[pre], lane,
                            pol);
     asm volatile("griddepcontrol.wait;" ::: "memory");
     uint32_t it = 0;
     for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
-      const uint32_t s = it % STAGES;
+      const uint32_t s = it % S;
       E* st = stage0 + static_cast<size_t>(s) * a.stage_elems;
       if (it < pre) {
         produce_vectors<E>(a, tile_geo(a, tile), st, &full[s], lane);
         continue;
       }
-      if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+      if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
       produce_tile<E>(a, tile, st, &full[s], lane, pol);
     }
   } else {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     uint32_t it = 0;
     for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
-      const uint32_t s = it % STAGES;
-      mbar_wait(&full[s], (it / STAGES) & 1);
-      if (MRHS)
-        consume_tile_mrhs_any<E, PUSH>(a, pa, tile, stage0 + static_cast<size_t>(s) * a.stage_elems, warp, lane, NCW);
-      else
+      const uint32_t s = it % S;
+      mbar_wait(&full[s], (it / S) & 1);
+      if constexpr (MRHS == 2) {
+        // output buffer it & 1 was last stored by tile it - 2: its reads must be done
+        if (warp == 0) bulk_wait_read<1>();
+        consumer_bar<NCW>();
+        E* ob = stage0 + static_cast<size_t>(S) * a.stage_elems + (it & 1) * static_cast<size_t>(a.out_elems);
+        consume_tile_mrhs_any<E, PUSH, DT>(a, pa, tile, stage0 + static_cast<size_t>(s) * a.stage_elems, warp, lane,
+                                           NCW, ob);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        fence_proxy_async_smem();
+        consumer_bar<NCW>();
+        if (warp == 0) store_tile_rows<E>(a, pa, tile, ob, lane);
+        continue;
+      } else if (MRHS) {
+        consume_tile_mrhs_any<E, PUSH, DT>(a, pa, tile, stage0 + static_cast<size_t>(s) * a.stage_elems, warp, lane,
+                                           NCW);
+      } else {
         consume_tile<E, PUSH>(a, pa, tile, stage0 + static_cast<size_t>(s) * a.stage_elems, threadIdx.x, NCW * 32);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if constexpr (MRHS == 2) {
+      if (warp == 0) bulk_wait_all();
     }
   }
 }

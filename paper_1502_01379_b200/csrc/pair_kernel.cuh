@@ -42,7 +42,8 @@ __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256
 // warps as 8 x 16 output tiles (m8n8k4 f64: 4 real products per complex step). The K
 // range is nseg segments of klen (the two stacked blocks of an adjoint level), so the
 // accessors get (segment, offset) without any division in the inner loop.
-template <typename AF, typename XF, typename YF>
+// GAUSS: 3 DMMAs per complex step (see consume_tile_dmma in level_kernel.cuh).
+template <bool GAUSS, typename AF, typename XF, typename YF>
 __device__ __forceinline__ void pair_gemms(int ngemm, int M, int nseg, int klen, int N, const AF& aload,
                                            const XF& xload, const YF& ystore, int warp, int lane, int nwarps) {
   const int mtl = (M + 7) / 8, ntl = (N + 15) / 16;
@@ -52,7 +53,7 @@ __device__ __forceinline__ void pair_gemms(int ngemm, int M, int nseg, int klen,
     const int gi = it / (mtl * ntl), rest = it - gi * mtl * ntl;
     const int m0 = (rest / ntl) * 8, n0 = (rest % ntl) * 16;
     const int m = m0 + lr;
-    double cr[2][2] = {{0, 0}, {0, 0}}, ci[2][2] = {{0, 0}, {0, 0}};
+    double cr[2][2] = {{0, 0}, {0, 0}}, ci[2][2] = {{0, 0}, {0, 0}}, cs[2][2] = {{0, 0}, {0, 0}};
     for (int sg = 0; sg < nseg; ++sg)
       for (int k0 = 0; k0 < klen; k0 += 4) {
         const int kk = k0 + lk;
@@ -64,17 +65,37 @@ __device__ __forceinline__ void pair_gemms(int ngemm, int M, int nseg, int klen,
           const int n = n0 + 8 * j + lr;
           b[j] = (kok && n < N) ? xload(gi, sg, kk, n) : make_double2(0, 0);
         }
+        if constexpr (GAUSS) {  // cr = T1, ci = T2, cs = T3
+          const double as = a.x + a.y;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          pair_dmma(cr[j][0], cr[j][1], a.x, b[j].x);
-          pair_dmma(ci[j][0], ci[j][1], a.x, b[j].y);
-        }
+          for (int j = 0; j < 2; ++j) {
+            pair_dmma(cr[j][0], cr[j][1], a.x, b[j].x);
+            pair_dmma(ci[j][0], ci[j][1], a.y, b[j].y);
+            pair_dmma(cs[j][0], cs[j][1], as, b[j].x + b[j].y);
+          }
+        } else {
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          pair_dmma(cr[j][0], cr[j][1], -a.y, b[j].y);
-          pair_dmma(ci[j][0], ci[j][1], a.y, b[j].x);
+          for (int j = 0; j < 2; ++j) {
+            pair_dmma(cr[j][0], cr[j][1], a.x, b[j].x);
+            pair_dmma(ci[j][0], ci[j][1], a.x, b[j].y);
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            pair_dmma(cr[j][0], cr[j][1], -a.y, b[j].y);
+            pair_dmma(ci[j][0], ci[j][1], a.y, b[j].x);
+          }
         }
       }
+    if constexpr (GAUSS) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const double t1 = cr[j][q], t2 = ci[j][q];
+          cr[j][q] = t1 - t2;
+          ci[j][q] = cs[j][q] - t1 - t2;
+        }
+    }
     if (m < M) {
 #pragma unroll
       for (int j = 0; j < 2; ++j)
@@ -118,7 +139,7 @@ __device__ __forceinline__ void pair_produce(const PairArgs& a, uint32_t item, d
   }
 }
 
-template <int STAGES, int NCW>
+template <int STAGES, int NCW, bool GAUSS>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1) pair_kernel(const PairArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -158,14 +179,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) pair_kernel(const PairArgs 
     auto blk = [&](uint32_t b) { return st + static_cast<size_t>(b) * R * fld; };
     if (!a.adjoint) {
       // level A: Y(t, u) = B_A(g, t, 2q + u) X_u  ->  mi rows t C + u R + m
-      pair_gemms(
+      pair_gemms<GAUSS>(
           4, R, 1, C, K, [&](int gi, int m, int, int kk) { return blk(gi)[m * fld + kk]; },
           [&](int gi, int, int kk, int n) { return vs[((gi & 1) * C + kk) * vld + n]; },
           [&](int gi, int m, int n, double2 v) { mi[((gi >> 1) * C + (gi & 1) * R + m) * vld + n] = v; }, warp, lane,
           NCW);
       consumers_sync();
       // level B: Y(t, t') = B_B(2g + t, t', q) mi_t  ->  out rows ((2g + t) 2 + t') P_B + q
-      pair_gemms(
+      pair_gemms<GAUSS>(
           4, R, 1, C, K, [&](int gi, int m, int, int kk) { return blk(4 + gi)[m * fld + kk]; },
           [&](int gi, int, int kk, int n) { return mi[((gi >> 1) * C + kk) * vld + n]; },
           [&](int gi, int m, int n, double2 v) {
@@ -175,7 +196,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) pair_kernel(const PairArgs 
           warp, lane, NCW);
     } else {
       // level B*: Y(t) = sum_t' B_B(2g + t, t', q)^H in(2g + t, t', q)  ->  mi rows t C + c
-      pair_gemms(
+      pair_gemms<GAUSS>(
           2, C, 2, R, K,
           [&](int gi, int m, int sg, int kk) {
             const double2 v = blk(4 + 2 * gi + sg)[kk * fld + m];
@@ -185,7 +206,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) pair_kernel(const PairArgs 
           [&](int gi, int m, int n, double2 v) { mi[(gi * C + m) * vld + n] = v; }, warp, lane, NCW);
       consumers_sync();
       // level A*: Y(u) = sum_t B_A(g, t, 2q + u)^H mi_t[u R ..]  ->  out rows (g P_A + 2q + u) C + c
-      pair_gemms(
+      pair_gemms<GAUSS>(
           2, C, 2, R, K,
           [&](int gi, int m, int sg, int kk) {
             const double2 v = blk(2 * sg + gi)[kk * fld + m];
