@@ -128,7 +128,10 @@ LevelKernel dmma_kernel(bool tout, int ncw, uint32_t dt) {
     static const LevelKernel r16[3] = {level_kernel<double2, 0, 16, 1, 1, false, 0>,
                                        level_kernel<double2, 0, 16, 1, 1, false, 1>,
                                        level_kernel<double2, 0, 16, 1, 1, false, 2>};
-    return ncw == 16 ? r16[dt] : r8[dt];
+    static const LevelKernel r4[3] = {level_kernel<double2, 0, 4, 2, 1, false, 0>,
+                                      level_kernel<double2, 0, 4, 2, 1, false, 1>,
+                                      level_kernel<double2, 0, 4, 2, 1, false, 2>};
+    return ncw == 16 ? r16[dt] : ncw == 4 ? r4[dt] : r8[dt];
   } else {
     return nullptr;
   }
@@ -193,7 +196,8 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   // complex128 DMMA consumers: 16 warps for the wide quadtree blocks (C = 4r = 100: long
   // k loops, few warp items per tile; cfg3 0.75 -> 0.59 ms, cfg4b 14.6 -> 11.0 ms), 8
   // otherwise (cfg2 k = 256: 43.9 vs 47.3 ms; cfg1 0.26 vs 0.32 ms)
-  if (mrhs) sh.ncw = sh.ncw == 16 || sh.ncw == 8 ? sh.ncw : (C > 64 ? 16 : 8);
+  if (mrhs) sh.ncw = sh.ncw == 16 || sh.ncw == 8 || sh.ncw == 4 ? sh.ncw : (C > 64 ? 16 : 8);
+  if (mrhs && sh.ncw == 4) sh.ctas_per_sm = 2;  // two independent 4-warp CTAs per SM
   LevelArgs a{};
   a.fac = fac;
   a.in = in;
@@ -343,7 +347,7 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
            : (push ? level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, true>
                    : level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, false>);
   BF_CUDA(allow_max_dyn_smem(kern));
-  const uint64_t per_sm = !tout && smem * sh.ctas_per_sm <= 227 * 1024 ? sh.ctas_per_sm : 1;
+  const uint64_t per_sm = !tout && (kncw == sh.ncw) && smem * sh.ctas_per_sm <= 227 * 1024 ? sh.ctas_per_sm : 1;
   const uint64_t grid = std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(pl.sms) * per_sm);
   static const bool dbg = [] {
     const char* e = getenv("BF_DEBUG_LAUNCH");
@@ -397,34 +401,102 @@ bool pair_disabled() {
 
 constexpr int kPairStages = 2, kPairNcw = 8;
 
+// k-chunked pairs (pair_chunk_kernel) only with BF_CHUNK_PAIR=1: at cfg2 k = 256 they
+// halve the vector traffic but run 47.3 ms against 43.8 ms for single levels (32-RHS
+// chunks leave each warp 8 x 16 GEMM slices with 6 DMMAs per k-step: latency bound)
+bool chunk_pair_disabled() {
+  static const bool off = env_int("BF_CHUNK_PAIR", 0) == 0;
+  return off;
+}
+
 struct PairGeo {
   uint32_t fld, vld, stage_elems;
   size_t smem;
+  bool chunk;             // k-chunked kernel (factor blocks once per item, input rows in chunks)
+  uint32_t kc, nch, stages;
 };
 
 bool pair_geometry(const Plan& pl, int i, uint32_t k, int adjoint, PairGeo* pg) {
   // k >= 64: below, the single-level kernel is faster (cfg1 at k = 32: 0.18 vs 0.20 ms)
-  if (pair_disabled() || pl.dtype != BF_C128 || pl.branch != 2 || k < 64 || k > 256) return false;
+  if (pair_disabled() || pl.dtype != BF_C128 || pl.branch != 2 || k < 64) return false;
   if (i < 0 || i + 1 >= static_cast<int>(pl.nlev)) return false;
   const LevelGeo& A = pl.lev[i];
   const LevelGeo& B = pl.lev[i + 1];
   if (!A.splits || !B.splits || A.P < 2 || B.G != 2 * A.G || 2 * B.P != A.P) return false;
   const uint64_t R = pl.rank, C = 2 * R;
   auto pad_to = [](uint64_t x, uint64_t target) { return x + (target + 8 - x % 8) % 8; };
-  const uint64_t fld = pad_to(C, adjoint ? 2 : 4), vld = pad_to(k, 2);
-  uint64_t stage = 8 * R * fld + 2 * C * vld;
-  if (stage & 1) ++stage;
-  const uint64_t smem = 128 + (kPairStages * stage + 2 * C * vld) * sizeof(double2);
-  if (smem > static_cast<uint64_t>(kMaxDynSmem)) return false;
+  const uint64_t fld = pad_to(C, adjoint ? 2 : 4);
   pg->fld = static_cast<uint32_t>(fld);
-  pg->vld = static_cast<uint32_t>(vld);
-  pg->stage_elems = static_cast<uint32_t>(stage);
-  pg->smem = smem;
-  return true;
+  pg->chunk = false;
+  if (k <= 256) {  // whole right-hand-side range per stage, double-buffered
+    const uint64_t vld = pad_to(k, 2);
+    uint64_t stage = 8 * R * fld + 2 * C * vld;
+    if (stage & 1) ++stage;
+    const uint64_t smem = 128 + (kPairStages * stage + 2 * C * vld) * sizeof(double2);
+    if (smem <= static_cast<uint64_t>(kMaxDynSmem)) {
+      pg->vld = static_cast<uint32_t>(vld);
+      pg->stage_elems = static_cast<uint32_t>(stage);
+      pg->smem = smem;
+      return true;
+    }
+  }
+  if (chunk_pair_disabled()) return false;
+  // k-chunked: factor buffer + a ring of 32-RHS input chunks + the chunk intermediate
+  const uint64_t kc = 32, vld = pad_to(kc, 2), stage = 2 * C * vld;
+  for (uint64_t S = 4; S >= 2; --S) {
+    const uint64_t smem = 128 + (8 * R * fld + S * stage + kPairNcw * C * 9) * sizeof(double2);
+    if (smem > static_cast<uint64_t>(kMaxDynSmem)) continue;
+    pg->chunk = true;
+    pg->kc = static_cast<uint32_t>(kc);
+    pg->nch = static_cast<uint32_t>((k + kc - 1) / kc);
+    pg->stages = static_cast<uint32_t>(S);
+    pg->vld = static_cast<uint32_t>(vld);
+    pg->stage_elems = static_cast<uint32_t>(stage);
+    pg->smem = smem;
+    return true;
+  }
+  return false;
+}
+
+int launch_pair_chunk(const Plan& pl, const void* fac_a, const void* fac_b, int i, const void* in, void* out,
+                      uint32_t k, int adjoint, const PairGeo& pg, cudaStream_t st) {
+  const LevelGeo& A = pl.lev[i];
+  PairChunkArgs a{};
+  a.fac_a = static_cast<const double2*>(fac_a);
+  a.fac_b = static_cast<const double2*>(fac_b);
+  a.in = static_cast<const double2*>(in);
+  a.out = static_cast<double2*>(out);
+  a.r = pl.rank;
+  a.ga = static_cast<uint32_t>(A.G);
+  a.pa = static_cast<uint32_t>(A.P);
+  a.k = k;
+  a.kc = pg.kc;
+  a.nch = pg.nch;
+  a.adjoint = adjoint;
+  a.nitems = static_cast<uint32_t>(A.G * A.P / 2);
+  a.fld = pg.fld;
+  a.vld = pg.vld;
+  a.stages = pg.stages;
+  a.stage_elems = pg.stage_elems;
+  auto* kern = gauss_disabled() ? pair_chunk_kernel<kPairNcw, false> : pair_chunk_kernel<kPairNcw, true>;
+  BF_CUDA(allow_max_dyn_smem(kern));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min<uint32_t>(a.nitems, static_cast<uint32_t>(pl.sms)));
+  cfg.blockDim = dim3((kPairNcw + 1) * 32);
+  cfg.dynamicSmemBytes = pg.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BF_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  return 0;
 }
 
 int launch_pair(const Plan& pl, const void* fac_a, const void* fac_b, int i, const void* in, void* out, uint32_t k,
                 int adjoint, const PairGeo& pg, cudaStream_t st) {
+  if (pg.chunk) return launch_pair_chunk(pl, fac_a, fac_b, i, in, out, k, adjoint, pg, st);
   const LevelGeo& A = pl.lev[i];
   PairArgs a{};
   a.fac_a = static_cast<const double2*>(fac_a);

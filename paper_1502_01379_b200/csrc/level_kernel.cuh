@@ -467,11 +467,6 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, const Peer
 }
 
 // ---------------------------------------------------------------- FP64 tensor cores
-// -x by a sign-bit flip on the integer pipe (a DADD would queue behind DMMAs on the FP64 datapath)
-__device__ __forceinline__ double neg(double x) {
-  return __hiloint2double(__double2hiint(x) ^ static_cast<int>(0x80000000u), __double2loint(x));
-}
-
 // mma.sync m8n8k4 f64 (DMMA): A fragment A[lane/4][lane%4], B fragment
 // B[lane%4][lane/4], C/D fragment C[lane/4][2(lane%4) + q] (layout confirmed on
 // B200 by tools/dmma_layout.cu).

@@ -200,7 +200,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) pair_kernel(const PairArgs 
           2, C, 2, R, K,
           [&](int gi, int m, int sg, int kk) {
             const double2 v = blk(4 + 2 * gi + sg)[kk * fld + m];
-            return make_double2(v.x, -v.y);
+            return make_double2(v.x, neg(v.y));
           },
           [&](int gi, int sg, int kk, int n) { return vs[((gi * 2 + sg) * R + kk) * vld + n]; },
           [&](int gi, int m, int n, double2 v) { mi[(gi * C + m) * vld + n] = v; }, warp, lane, NCW);
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) pair_kernel(const PairArgs 
           2, C, 2, R, K,
           [&](int gi, int m, int sg, int kk) {
             const double2 v = blk(2 * sg + gi)[kk * fld + m];
-            return make_double2(v.x, -v.y);
+            return make_double2(v.x, neg(v.y));
           },
           [&](int gi, int sg, int kk, int n) { return mi[(sg * C + gi * R + kk) * vld + n]; },
           [&](int gi, int m, int n, double2 v) {
@@ -221,6 +221,246 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) pair_kernel(const PairArgs 
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     consumers_sync();  // mi is reused by the next item's first level
+  }
+}
+
+}  // namespace bfly
+
+namespace bfly {
+
+// ---------------------------------------------------------------- k-chunked level pairs
+// The same two-level fusion when an item's full right-hand-side range does not fit a
+// stage (cfg2 k = 256, r = 16: 8 blocks + 64 rows x 256 RHS = 330 KB): the item's 8
+// factor blocks are loaded once into their own buffer, and the input rows stream
+// through a ring in chunks of kc right-hand sides; per chunk, level A's outputs stay
+// in shared memory (mi) for level B. The chain's intermediate vectors are read and
+// written once per pair instead of once per level.
+struct PairChunkArgs {
+  const double2* fac_a;
+  const double2* fac_b;
+  const double2* in;
+  double2* out;
+  uint32_t r, ga, pa;
+  uint32_t k;            // right-hand sides (row length of in / out)
+  uint32_t kc, nch;      // chunk width, chunks per item
+  int adjoint;
+  uint32_t nitems;
+  uint32_t fld, vld;     // shared-memory row strides of block rows and chunk rows
+  uint32_t stages;       // ring depth (<= 4)
+  uint32_t stage_elems;  // 2 C x vld
+};
+
+__device__ __forceinline__ void pair_chunk_factors(const PairChunkArgs& a, uint32_t item, double2* fs, uint64_t* bar,
+                                                   int lane, uint64_t pol) {
+  const uint32_t R = a.r, C = 2 * a.r, pb = a.pa / 2;
+  const uint32_t g = item / pb, q = item - g * pb;
+  if (lane == 0) mbar_arrive_expect_tx(bar, 8 * R * C * static_cast<uint32_t>(sizeof(double2)));
+  __syncwarp();
+  for (uint32_t row = lane; row < 8 * R; row += 32) {
+    const uint32_t b = row / R, rr = row - b * R;
+    const uint32_t lvl = b >> 2, t = (b >> 1) & 1, v = b & 1;
+    const double2* src = lvl == 0 ? a.fac_a + (static_cast<size_t>((g * 2 + t) * a.pa + 2 * q + v) * R + rr) * C
+                                  : a.fac_b + (static_cast<size_t>(((2 * g + t) * 2 + v) * pb + q) * R + rr) * C;
+    bulk_g2s(fs + static_cast<size_t>(row) * a.fld, src, C * static_cast<uint32_t>(sizeof(double2)), bar, pol);
+  }
+}
+
+__device__ __forceinline__ void pair_chunk_vectors(const PairChunkArgs& a, uint32_t item, uint32_t c, double2* vs,
+                                                   uint64_t* bar, int lane) {
+  const uint32_t R = a.r, C = 2 * a.r, pb = a.pa / 2;
+  const uint32_t g = item / pb, q = item - g * pb;
+  const uint32_t k0 = c * a.kc, kw = min(a.kc, a.k - k0);
+  if (lane == 0) mbar_arrive_expect_tx(bar, 2 * C * kw * static_cast<uint32_t>(sizeof(double2)));
+  __syncwarp();
+  for (uint32_t row = lane; row < 2 * C; row += 32) {
+    size_t grow;
+    if (!a.adjoint) {
+      grow = static_cast<size_t>(g * a.pa + 2 * q) * C + row;
+    } else {
+      const uint32_t ch = row / R, rr = row - ch * R, t = ch >> 1, tp = ch & 1;
+      grow = static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q) * R + rr;
+    }
+    bulk_g2s(vs + static_cast<size_t>(row) * a.vld, a.in + grow * a.k + k0, kw * static_cast<uint32_t>(sizeof(double2)),
+             bar);
+  }
+}
+
+// One warp's share of a chunk: ngemm complex GEMMs Y_g (M x 8) = A_g (M x K) X_g (K x 8)
+// for the 8 right-hand-side columns n0 .. n0 + 7 (of N), all M rows (MT 8-row tiles per
+// pass, 3 DMMAs per complex k-step with GAUSS), K as nseg segments of klen.
+template <bool GAUSS, typename AF, typename XF, typename YF>
+__device__ __forceinline__ void warp_gemm_cols(int ngemm, int M, int nseg, int klen, int n0, int N, const AF& aload,
+                                               const XF& xload, const YF& ystore, int lane) {
+  constexpr int MT = 2;
+  const int lr = lane >> 2, lk = lane & 3;
+  const int n = n0 + lr;
+  for (int gi = 0; gi < ngemm; ++gi)
+    for (int m0 = 0; m0 < M; m0 += 8 * MT) {
+      double cr[MT][2] = {}, ci[MT][2] = {}, cs[MT][2] = {};
+      for (int sg = 0; sg < nseg; ++sg)
+        for (int k0 = 0; k0 < klen; k0 += 4) {
+          const int kk = k0 + lk;
+          const bool kok = kk < klen;
+          double2 av[MT];
+#pragma unroll
+          for (int i = 0; i < MT; ++i) {
+            const int m = m0 + 8 * i + lr;
+            av[i] = (kok && m < M) ? aload(gi, m, sg, kk) : make_double2(0, 0);
+          }
+          const double2 b = (kok && n < N) ? xload(gi, sg, kk, n) : make_double2(0, 0);
+          if constexpr (GAUSS) {
+            const double bs = b.x + b.y;
+#pragma unroll
+            for (int i = 0; i < MT; ++i) {
+              pair_dmma(cr[i][0], cr[i][1], av[i].x, b.x);
+              pair_dmma(ci[i][0], ci[i][1], av[i].y, b.y);
+            }
+#pragma unroll
+            for (int i = 0; i < MT; ++i) pair_dmma(cs[i][0], cs[i][1], av[i].x + av[i].y, bs);
+          } else {
+#pragma unroll
+            for (int i = 0; i < MT; ++i) {
+              pair_dmma(cr[i][0], cr[i][1], av[i].x, b.x);
+              pair_dmma(ci[i][0], ci[i][1], av[i].x, b.y);
+            }
+#pragma unroll
+            for (int i = 0; i < MT; ++i) {
+              pair_dmma(cr[i][0], cr[i][1], neg(av[i].y), b.y);
+              pair_dmma(ci[i][0], ci[i][1], av[i].y, b.x);
+            }
+          }
+        }
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int m = m0 + 8 * i + lr;
+        if (m >= M) continue;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int nn = n0 + 2 * lk + q;
+          if (nn >= N) continue;
+          double re = cr[i][q], im = ci[i][q];
+          if constexpr (GAUSS) {
+            re = cr[i][q] - ci[i][q];
+            im = cs[i][q] - cr[i][q] - ci[i][q];
+          }
+          ystore(gi, m, nn, make_double2(re, im));
+        }
+      }
+    }
+}
+
+// Consumers: warp w owns right-hand-side columns 8 (w % 4) .. + 7 of every chunk and one
+// half of the pair's dataflow (forward: t = w / 4, whose level-B outputs depend only on
+// level-A outputs with the same t; adjoint: u = w / 4, the u-half rows of both level-B*
+// outputs feed exactly the level-A* output u). Each warp's intermediate (C x 8, row
+// stride 9: conflict-free fragment stores and loads) is private, so the two levels are
+// separated by __syncwarp only and warps never wait for each other.
+template <int NCW, bool GAUSS>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1) pair_chunk_kernel(const PairChunkArgs a) {
+  static_assert(NCW == 8, "4 column slices x 2 halves");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [4]
+  uint64_t* empty = full + 4;                               // [4]
+  uint64_t* ffull = full + 8;
+  uint64_t* fempty = full + 9;
+  const uint32_t R = a.r, C = 2 * a.r, pb = a.pa / 2, K = a.k, S = a.stages;
+  double2* fs = reinterpret_cast<double2*>(smem_raw + 128);
+  double2* ring = fs + static_cast<size_t>(8) * R * a.fld;
+  double2* mis = ring + static_cast<size_t>(S) * a.stage_elems;  // NCW private C x 9 intermediates
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    mbar_init(ffull, 1);
+    mbar_init(fempty, NCW);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint32_t fld = a.fld, vld = a.vld;
+  if (warp == NCW) {
+    const uint64_t pol = policy_evict_first();
+    uint32_t it = 0, ii = 0;
+    for (uint32_t item = blockIdx.x; item < a.nitems; item += gridDim.x, ++ii) {
+      if (ii > 0) mbar_wait(fempty, (ii - 1) & 1);
+      pair_chunk_factors(a, item, fs, ffull, lane, pol);  // constant: may precede the dependency wait
+      if (ii == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+      for (uint32_t c = 0; c < a.nch; ++c, ++it) {
+        const uint32_t s = it % S;
+        if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
+        pair_chunk_vectors(a, item, c, ring + static_cast<size_t>(s) * a.stage_elems, &full[s], lane);
+      }
+    }
+    return;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int n0 = (warp & 3) * 8, half = warp >> 2;
+  double2* mi = mis + static_cast<size_t>(warp) * C * 9;
+  uint32_t it = 0, ii = 0;
+  auto blk = [&](uint32_t b) { return fs + static_cast<size_t>(b) * R * fld; };
+  for (uint32_t item = blockIdx.x; item < a.nitems; item += gridDim.x, ++ii) {
+    const uint32_t g = item / pb, q = item - g * pb;
+    mbar_wait(ffull, ii & 1);
+    for (uint32_t c = 0; c < a.nch; ++c, ++it) {
+      const uint32_t s = it % S;
+      mbar_wait(&full[s], (it / S) & 1);
+      const double2* vs = ring + static_cast<size_t>(s) * a.stage_elems;
+      const uint32_t k0 = c * a.kc;
+      const int kw = static_cast<int>(min(a.kc, K - k0));
+      if (n0 < kw) {
+        if (!a.adjoint) {
+          const uint32_t t = half;
+          // level A, t fixed: Y_u = B_A(g, t, 2q + u) X_u  ->  mi rows u R + m
+          warp_gemm_cols<GAUSS>(
+              2, R, 1, C, n0, kw, [&](int u, int m, int, int kk) { return blk(2 * t + u)[m * fld + kk]; },
+              [&](int u, int, int kk, int n) { return vs[(u * C + kk) * vld + n]; },
+              [&](int u, int m, int n, double2 v) { mi[(u * R + m) * 9 + (n - n0)] = v; }, lane);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);  // this warp's reads of the chunk are done
+          // level B: Z_t' = B_B(2g + t, t', q) mi  ->  out rows ((2g + t) 2 + t') P_B + q
+          warp_gemm_cols<GAUSS>(
+              2, R, 1, C, n0, kw, [&](int tp, int m, int, int kk) { return blk(4 + 2 * t + tp)[m * fld + kk]; },
+              [&](int, int, int kk, int n) { return mi[kk * 9 + (n - n0)]; },
+              [&](int tp, int m, int n, double2 v) {
+                a.out[(static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q) * R + m) * K + k0 + n] = v;
+              },
+              lane);
+        } else {
+          const uint32_t u = half;
+          // level B*, rows u R .. u R + R of Y_t = sum_t' B_B(2g + t, t', q)^H in(2g + t, t', q)
+          warp_gemm_cols<GAUSS>(
+              2, R, 2, R, n0, kw,
+              [&](int t, int m, int tp, int kk) {
+                const double2 v = blk(4 + 2 * t + tp)[kk * fld + u * R + m];
+                return make_double2(v.x, neg(v.y));
+              },
+              [&](int t, int tp, int kk, int n) { return vs[((t * 2 + tp) * R + kk) * vld + n]; },
+              [&](int t, int m, int n, double2 v) { mi[(t * R + m) * 9 + (n - n0)] = v; }, lane);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+          // level A*: out_u = sum_t B_A(g, t, 2q + u)^H Y_t[u half]  ->  rows (g P_A + 2q + u) C + m
+          warp_gemm_cols<GAUSS>(
+              1, C, 2, R, n0, kw,
+              [&](int, int m, int t, int kk) {
+                const double2 v = blk(2 * t + u)[kk * fld + m];
+                return make_double2(v.x, neg(v.y));
+              },
+              [&](int, int t, int kk, int n) { return mi[(t * R + kk) * 9 + (n - n0)]; },
+              [&](int, int m, int n, double2 v) {
+                a.out[(static_cast<size_t>(g * a.pa + 2 * q + u) * C + m) * K + k0 + n] = v;
+              },
+              lane);
+        }
+        __syncwarp();  // mi is rewritten by the next chunk
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(fempty);  // the item's factor blocks are consumed
   }
 }
 

@@ -6,6 +6,8 @@ Tolerances (BASELINE.json north_star): relative 2-norm <= 1e-11 for complex128,
 pkg/tests/test_factors.py:16-51.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -18,6 +20,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 TOL128, TOL64 = 1e-11, 1e-5
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN_APPLY = ["apply_fio_n256_r8_leaf025.npz", "apply_cfg0_fio_n1024_r12_leaf8.npz",
                 "apply_dftp_n1024_r8_leaf16.npz"]
 
@@ -143,6 +146,8 @@ def test_per_factor_parity(case):
     (1 << 12, 4, 6, 64),      # fused level pairs (pair_kernel): r=6, padded rows
     (1 << 14, 16, 8, 128),    # fused level pairs at 128 RHS
     (1 << 12, 1, 4, 96),      # fused pairs, odd number of splitting levels per half
+    (1 << 14, 16, 16, 64),    # r=16, 64 RHS (pairs do not fit a stage: single levels)
+    (1 << 12, 16, 16, 70),    # same, k not a multiple of the DMMA tiles
 ])
 def test_synthetic_geometries(n, leaf, r, k):
     p = bf.make_partition(n, leaf)
@@ -153,6 +158,39 @@ def test_synthetic_geometries(n, leaf, r, k):
     assert rel(f.plan().apply(gd), ochain.apply(oc, g)) <= TOL128
     assert rel(f.plan().apply(gd, adjoint=True), ochain.apply(oc, g, adjoint=True)) <= TOL128
     assert rel(f.plan("c64").apply(gd).to(torch.complex128), ochain.apply(oc, g)) <= TOL64
+
+
+@pytest.mark.parametrize("n,leaf,r,k", [
+    (1 << 14, 16, 16, 64),    # k-chunked level pairs (pair_chunk_kernel): r=16, 2 chunks of 32 RHS
+    (1 << 12, 16, 16, 70),    # partial last chunk (6 RHS) and idle column slices
+    (1 << 10, 16, 12, 300),   # r=12, 10 chunks
+])
+def test_chunked_pairs_opt_in(n, leaf, r, k):
+    """The k-chunked pair kernel is opt-in (BF_CHUNK_PAIR=1, read once per process): run the
+    oracle comparison in a child process with it enabled."""
+    import subprocess
+    import sys
+    code = f"""
+import numpy as np, torch, sys
+sys.path[:0] = [{ROOT!r}, {os.path.join(ROOT, "tests")!r}]
+import paper_1502_01379_b200 as bf
+from paper_1502_01379_b200.synthetic import synthetic_chain
+from conftest import complex_gaussian
+from test_apply_gpu import oracle_of, rel
+from oracle import chain as ochain
+p = bf.make_partition({n}, {leaf})
+f = synthetic_chain(p, {r}, seed={n + r})
+oc = oracle_of(f)
+g = complex_gaussian(np.random.default_rng({k}), ({n}, {k}))
+gd = torch.from_numpy(g).cuda()
+e1 = rel(f.plan().apply(gd), ochain.apply(oc, g))
+e2 = rel(f.plan().apply(gd, adjoint=True), ochain.apply(oc, g, adjoint=True))
+assert e1 <= 1e-11 and e2 <= 1e-11, (e1, e2)
+print("ok", e1, e2)
+"""
+    env = dict(os.environ, BF_CHUNK_PAIR="1")
+    r_ = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, cwd=ROOT)
+    assert r_.returncode == 0 and "ok" in r_.stdout, r_.stderr[-2000:]
 
 
 def test_config2_geometry_k1():
