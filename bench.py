@@ -270,8 +270,9 @@ def run_sharded(args, world, rank, local):
     esz = 16 if args.dtype == "c128" else 8
     # weak scaling (default): every GPU keeps the single-GPU config's size, the chain grows
     # with the GPU count (cfg2 per GPU -> N = 2^20 x GPUs; at 8 GPUs 2^23). 2-D configs
-    # (quadtrees over n_side^2 points) scale strongly.
-    weak = args.scaling == "weak" and kern != "radon2d"
+    # (quadtrees over n_side^2 points) and cfg4a (BASELINE's fixed N = 2^24 sharded
+    # config) scale strongly.
+    weak = args.scaling == "weak" and kern != "radon2d" and args.config != "cfg4a"
     if weak:
         n *= world
     p = partition_for(kern, n, leaf)

@@ -75,6 +75,7 @@ def main():
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--cpu-blocks", type=int, default=4)
     ap.add_argument("--mode", choices=["sampling", "matvec"], default="sampling")
+    ap.add_argument("--rows", type=int, default=0, help="cfg2: block-rows per middle launch (default: factorize's)")
     args = ap.parse_args()
     if args.mode == "matvec":
         return bench_matvec(args)
@@ -93,9 +94,13 @@ def main():
     else:
         ms = bc.MiddleSampler(ker, p, r, seed=0)
         t_draws, _ = sync_time(ms.prepare_draws)          # all 65,536 blocks' tables, process pool
-        ij = [(0, j) for j in range(m)]
+        rows = args.rows or ms.batch_rows()
+        ij = [(i, j) for i in range(rows) for j in range(m)]
         ms.blocks(ij)                                       # warm: workspace allocation, first launches
         t_mid, (u, v, w) = sync_time(lambda: ms.blocks(ij))
+        t_mid /= rows
+        u = u[:m]
+        res["gpu_rows_per_launch"] = rows
         kb = bc.recursion_batch(m, side, r)               # slabs per recursion launch (factorize's batching)
         slab = u.permute(1, 0, 2).reshape(1, side, m, r).expand(kb, side, m, r).contiguous()
         bc.recurse(slab, p, r)
