@@ -19,6 +19,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "entry_eval.cuh"
 #include "linalg.cuh"
 #include "plan.h"
@@ -209,6 +211,116 @@ __global__ void k_pivot_wide(MidArgs a, int which) {
                                     picks, Rm);
   // skeleton = sorted(picks)
   if (threadIdx.x == 0) {
+    int32_t* sk = which == kRows ? s.skc : s.skr;
+    for (int i = 0; i < npick; ++i) {
+      int rank = 0;
+      for (int m = 0; m < npick; ++m) rank += picks[m] < picks[i];
+      sk[rank] = picks[i];
+    }
+    if (which == kRows)
+      s.nskc = npick;
+    else
+      s.nskr = npick;
+  }
+}
+
+// Cluster form of k_pivot_wide for wide samples (side >= 1024): a cluster of CL CTAs
+// shares one block, CTA c owning columns [c side/CL, (c+1) side/CL). With one CTA per SM
+// only 148/CL blocks are in flight, so their samples (|rows| x side complex: 4 MB at
+// cfg2) stay L2-resident across the r passes of the greedy loop instead of streaming
+// from HBM on every pick. Per pick the column maximum and the first index above the
+// tie threshold are exchanged through distributed shared memory: max and min are
+// exact, and every column's arithmetic is the single-CTA kernel's, so the picks (and
+// the construction) are bitwise identical to k_pivot_wide.
+template <int CL>
+__global__ void __launch_bounds__(512, 1) k_pivot_wide_cl(MidArgs a, int which) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ double smem_d[];
+  const int cr = static_cast<int>(cluster.block_rank());
+  const int blk = blockIdx.x / CL;
+  const int ncols = static_cast<int>(a.side);
+  const int c0 = cr * ncols / CL, c1 = (cr + 1) * ncols / CL, nloc = c1 - c0;
+  double* norms = smem_d;                                             // nloc (own columns)
+  double2* q = reinterpret_cast<double2*>(norms + ((nloc + 1) & ~1));  // kSetCap
+  double* red = reinterpret_cast<double*>(q + kSetCap);               // 32
+  int* redi = reinterpret_cast<int*>(red + 32);                       // 32
+  __shared__ double cl_val[CL];                                       // per-CTA maxima
+  __shared__ int cl_idx[CL];                                          // per-CTA first index >= thr
+  __shared__ double cl_nrm[CL];                                       // and its norm
+  __shared__ int picks[kSetCap];
+  BlockState& s = a.st[blk];
+  const int nr = which == kRows ? s.nrows : s.ncols;
+  const bool pairwise = which == kCols;
+  const double2* W = a.wide + static_cast<int64_t>(blk) * a.S * a.side;
+  double2* Rm = a.tall + static_cast<int64_t>(blk) * a.S * a.side;
+  auto put_val = [&](double v) {  // every CTA gets this CTA's value in slot cr
+    if (threadIdx.x < CL) *cluster.map_shared_rank(&cl_val[cr], threadIdx.x) = v;
+  };
+  for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+    auto get = [&](int i) { return abs2(W[static_cast<int64_t>(i) * ncols + c]); };
+    norms[c - c0] = pairwise ? pairwise_sum(get, 0, nr) : sequential_sum(get, nr);
+  }
+  const int k = min(a.r, min(nr, ncols));
+  cluster.sync();  // every CTA of the cluster is running before any DSMEM store
+  int npick = 0;
+  // two cluster barriers per pick: the maxima are read before a CTA arrives at the second,
+  // the first indices before it arrives at the next pick's first, so single buffers do
+  for (int it = 0; it < k; ++it) {
+    double lm = 0.0;
+    for (int c = threadIdx.x; c < nloc; c += blockDim.x) lm = fmax(lm, norms[c]);
+    lm = block_max(lm, red);
+    put_val(lm);
+    cluster.sync();
+    double best = 0.0;
+    for (int x = 0; x < CL; ++x) best = fmax(best, cl_val[x]);
+    if (best <= 0.0) break;  // rel_tol = 0 in the sweeps (lowrank.py:237-243); identical in every CTA
+    const double thr = __dmul_rn(best, 1.0 - 2.0 * kPivotTie);
+    int li = INT_MAX;
+    for (int c = threadIdx.x; c < nloc; c += blockDim.x)
+      if (norms[c] >= thr) li = min(li, c);
+    li = block_min_int(li, redi);
+    if (threadIdx.x < CL) {
+      *cluster.map_shared_rank(&cl_idx[cr], threadIdx.x) = li == INT_MAX ? INT_MAX : c0 + li;
+      *cluster.map_shared_rank(&cl_nrm[cr], threadIdx.x) = li == INT_MAX ? 0.0 : norms[li];
+    }
+    cluster.sync();  // also orders the previous picks' projection rows (global) before their reads
+    int j = INT_MAX;
+    double nj = 0.0;
+    for (int x = 0; x < CL; ++x)
+      if (cl_idx[x] < j) {
+        j = cl_idx[x];
+        nj = cl_nrm[x];
+      }
+    const double sq = sqrt(nj);
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) q[i] = W[static_cast<int64_t>(i) * ncols + j];
+    if (threadIdx.x == 0) picks[npick] = j;
+    __syncthreads();
+    double2* prow = Rm + static_cast<int64_t>(npick) * ncols;
+    for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+      double2 g = make_double2(0, 0);
+#pragma unroll 8
+      for (int i = 0; i < nr; ++i) {
+        const double2 t = cmulc(q[i], W[static_cast<int64_t>(i) * ncols + c]);
+        g.x += t.x;
+        g.y += t.y;
+      }
+      for (int l = 0; l < npick; ++l) {
+        const double2 t = cmulc(Rm[static_cast<int64_t>(l) * ncols + j], Rm[static_cast<int64_t>(l) * ncols + c]);
+        g.x -= t.x;
+        g.y -= t.y;
+      }
+      const double2 pr = make_double2(__ddiv_rn(g.x, sq), __ddiv_rn(g.y, sq));
+      prow[c] = pr;
+      norms[c - c0] = fmax(__dsub_rn(norms[c - c0], abs2(pr)), 0.0);
+    }
+    ++npick;
+    __syncthreads();
+    if (threadIdx.x == 0 && j >= c0 && j < c1) norms[j - c0] = 0.0;
+    __syncthreads();
+  }
+  cluster.sync();  // projection rows complete before any CTA exits (DSMEM lifetime)
+  if (cr == 0 && threadIdx.x == 0) {
     int32_t* sk = which == kRows ? s.skc : s.skr;
     for (int i = 0; i < npick; ++i) {
       int rank = 0;
@@ -1315,6 +1427,50 @@ bool tree_geometry(uint64_t n, uint32_t levels, uint32_t branching, uint64_t* m,
 
 }  // namespace
 
+namespace {
+
+int env_int_c(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
+// Greedy sweep pivots: the cluster kernel (k_pivot_wide_cl) for samples of >= 1024
+// columns, one CTA per SM (shared-memory request above half the SM) so that only
+// 148/CL blocks' samples are live in L2; BF_NO_PIVOT_CLUSTER=1 keeps one CTA per block.
+template <int CL>
+cudaError_t launch_pivot_cl(const MidArgs& a, int which, int nblocks, cudaStream_t st) {
+  auto* kern = k_pivot_wide_cl<CL>;
+  const int per_sm = std::max(1, std::min(4, env_int_c("BF_PIVOT_CTAS_PER_SM", 1)));
+  const size_t need = static_cast<size_t>((a.side / CL + 2) * sizeof(double) + kSetCap * sizeof(double2) + 32 * 8 + 32 * 4);
+  const size_t smem = std::max(need, static_cast<size_t>(228 * 1024 / (per_sm + 1) + 1024));
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(nblocks) * CL);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, which);
+}
+
+cudaError_t launch_pivot_wide(const MidArgs& a, int which, int nblocks, size_t piv_smem, cudaStream_t st) {
+  static const bool off = env_int_c("BF_NO_PIVOT_CLUSTER", 0) != 0;
+  if (!off && a.side >= 4096) return launch_pivot_cl<8>(a, which, nblocks, st);
+  if (!off && a.side >= 2048) return launch_pivot_cl<4>(a, which, nblocks, st);
+  if (!off && a.side >= 1024) return launch_pivot_cl<2>(a, which, nblocks, st);
+  k_pivot_wide<<<nblocks, 512, piv_smem, st>>>(a, which);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
 extern "C" {
 
 uint64_t bf_middle_workspace_bytes(uint64_t n, uint32_t levels, uint32_t branching, uint32_t rank, uint32_t q_over,
@@ -1385,10 +1541,10 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
     for (uint32_t sw = 0; sw < iters; ++sw) {
       k_union<<<nblocks, 128, 0, st>>>(a, 2 * sw, kRows);
       k_fill_wide<<<dim3(nblocks, yfill), T, 0, st>>>(a, kRows);
-      k_pivot_wide<<<nblocks, 512, piv_smem, st>>>(a, kRows);
+      BF_CUDA(launch_pivot_wide(a, kRows, nblocks, piv_smem, st));
       k_union<<<nblocks, 128, 0, st>>>(a, 2 * sw + 1, kCols);
       k_fill_wide<<<dim3(nblocks, yfill), T, 0, st>>>(a, kCols);
-      k_pivot_wide<<<nblocks, 512, piv_smem, st>>>(a, kCols);
+      BF_CUDA(launch_pivot_wide(a, kCols, nblocks, piv_smem, st));
     }
     k_union<<<nblocks, 128, 0, st>>>(a, 2 * iters, kRows);
     k_union<<<nblocks, 128, 0, st>>>(a, 2 * iters + 1, kCols);
