@@ -325,6 +325,7 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
     if (tout) stages = tout_stages();
   }
   a.stages = static_cast<uint32_t>(stages);
+  a.dbg_nomath = env_int("BF_DBG_NOMATH", 0);
   if (a.use_dmma) {  // warp tile: the largest that still gives every consumer warp an item
     const uint64_t ncw = tout ? kTout.ncw : (a.use_dmma == 2 && remap < 3) ? sh.ncw : kMrhs.ncw;
     auto di = [&](uint64_t mt, uint64_t n8) {

@@ -65,6 +65,7 @@ struct LevelArgs {
   uint32_t old, out_elems;
   uint32_t stages;    // pipeline depth when the kernel's STAGES template argument is 0 (<= 8)
   uint32_t dtile;     // DMMA warp tile: 0 = 2 x 4, 1 = 2 x 2, 2 = 1 x 2 (8 x 8 tiles)
+  int dbg_nomath;     // BF_DBG_NOMATH=1 (diagnostics only): DMMA consumers skip the k loop
 };
 
 // remap 3/4 receive buffers of every part ([sender][own][other local][rho][k]); a
@@ -498,7 +499,7 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
   const uint32_t fld = a.fld, vld = a.vld ? a.vld : kc;
   const uint32_t P_mask = (1u << a.lgP) - 1;
   const uint32_t m_out = a.adjoint ? a.C : a.nt * a.R;
-  const uint32_t kdim = a.adjoint ? a.nt * a.R : a.C;
+  const uint32_t kdim = a.dbg_nomath ? 0 : a.adjoint ? a.nt * a.R : a.C;
   const uint32_t nmt = (m_out + MT * 8 - 1) / (MT * 8), nnt = (kc + NT * 8 - 1) / (NT * 8);
   const uint32_t items = U * nmt * nnt;
   const uint32_t lr = lane >> 2, lk = lane & 3;
