@@ -262,7 +262,7 @@ def run_sharded(args, world, rank, local):
     import torch.distributed as dist
 
     import paper_1502_01379_b200 as bf
-    from paper_1502_01379_b200.sharded import ShardedPlan
+    from paper_1502_01379_b200.sharded import PUSH_BARRIER_TIMEOUT_MS, ShardedPlan
     from paper_1502_01379_b200.synthetic import synthetic_chain
 
     kern, n, r, leaf, k0 = CONFIGS[args.config]
@@ -317,10 +317,10 @@ def run_sharded(args, world, rank, local):
     for i in range(steps):
         if use_push:
             buf, hdl, ptrs = sp.push_buffer(g.shape[1])
-            hdl.barrier()
+            hdl.barrier(timeout_ms=PUSH_BARRIER_TIMEOUT_MS)
             sp.down_push(g, False, ptrs)      # the exchange is fused into this launch's stores
             ev[i][0].record(stream)
-            hdl.barrier()                     # only the wait for the peers' stores is separable
+            hdl.barrier(timeout_ms=PUSH_BARRIER_TIMEOUT_MS)  # only the wait for the peers' stores is separable
             ev[i][1].record(stream)
             recv = (buf.view(torch.complex128) if sp.tdt == torch.complex128 else buf).view(-1, g.shape[1])
             sp.up(sp.unpack(recv, False), False)

@@ -40,6 +40,11 @@ def shard_slices(f: ButterflyFactors, part: int, nparts: int) -> dict:
             "g": [(t.level, cut(t.blocks)) for t in f.g_chain], "h": [(t.level, cut(t.blocks)) for t in f.h_chain]}
 
 
+
+# Symmetric-memory barriers of the fused push exchange trap after this long instead of
+# spinning forever when a peer never arrives (a hung multi-GPU job is worse than a failed one).
+PUSH_BARRIER_TIMEOUT_MS = 120_000
+
 class ShardedApply:
     """Exchange orchestration of the sharded chain; subclasses provide the local steps."""
 
@@ -218,9 +223,9 @@ def _push_methods():
             raise ValueError(f"local input length {g_local.shape[0]} != {self.n_local}")
         k = g_local.reshape(self.n_local, -1).shape[1]
         buf, hdl, ptrs = self.push_buffer(k)
-        hdl.barrier()                       # every part is done reading its buffer (previous apply)
+        hdl.barrier(timeout_ms=PUSH_BARRIER_TIMEOUT_MS)  # every part is done reading its buffer (previous apply)
         self.down_push(g_local, adjoint, ptrs)
-        hdl.barrier()                       # every part's stores into this buffer have landed
+        hdl.barrier(timeout_ms=PUSH_BARRIER_TIMEOUT_MS)  # every part's stores into this buffer have landed
         recv = buf.view(torch.complex128) if self.tdt == torch.complex128 else buf
         recv = recv.view(self.nparts * self.chunk_rows, k)
         return self.up(self.unpack(recv, adjoint), adjoint)
