@@ -351,3 +351,34 @@ def test_recursion_tall_stacks_vs_oracle(n, leaf, r, b):
     ro = recon(leaf_o, pieces_o)
     rg = recon(outer.blocks.cpu().numpy(), [(t.level, t.blocks.cpu().numpy()) for t in chain])
     assert rel(rg, ro) <= 1e-12
+
+
+@pytest.mark.parametrize("n,r,rows", [(1 << 16, 8, [3]), (1 << 18, 16, [0]), (1 << 20, 16, [7])])
+def test_cluster_pivots_bitwise(tmp_path, n, r, rows):
+    """The cluster form of the sweep pivots (k_pivot_wide_cl: 2 / 4 / 8 CTAs per block at
+    side 1024 / 2048 / 4096) against the one-CTA kernel (BF_NO_PIVOT_CLUSTER=1, read once
+    per process, hence child processes): the middle factors of whole block-rows are
+    bitwise identical."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_1502_01379_b200 as bf
+from paper_1502_01379_b200 import construct as bc
+p = bf.make_partition({n}, 16)
+ms = bc.MiddleSampler(bf.FioKernel({n}), p, {r}, seed=0)
+u, v, w = ms.blocks([(i, j) for i in {rows!r} for j in range(p.mid_nodes)])
+np.savez(sys.argv[1], u=u.cpu().numpy(), v=v.cpu().numpy(), w=w.cpu().numpy())
+"""
+    res = {}
+    for tag, flag in (("cluster", "0"), ("single", "1")):
+        path = str(tmp_path / f"{tag}.npz")
+        env = dict(os.environ, BF_NO_PIVOT_CLUSTER=flag)
+        out = subprocess.run([sys.executable, "-c", code, path], env=env, capture_output=True, text=True, cwd=root)
+        assert out.returncode == 0, out.stderr[-2000:]
+        res[tag] = np.load(path)
+    for key in ("u", "v", "w"):
+        assert np.array_equal(res["cluster"][key], res["single"][key]), key
