@@ -113,9 +113,24 @@ using LevelKernel = void (*)(LevelArgs, PeerArgs);
 
 // complex128 3-multiplication DMMA kernels, one instantiation per warp tile (dt):
 // MRHS = 2 (TMA-stored outputs) or 1 (register stores) with 8 or 16 consumer warps
+// BF_NO_INPLACE=1: many-RHS DMMA consumers store their outputs from registers (MRHS = 1)
+bool inplace_disabled() {
+  static const bool off = env_int("BF_NO_INPLACE", 0) != 0;
+  return off;
+}
+
 template <typename E>
-LevelKernel dmma_kernel(bool tout, int ncw, uint32_t dt) {
+LevelKernel dmma_kernel(bool tout, int ncw, uint32_t dt, bool inplace = false) {
   if constexpr (std::is_same<E, double2>::value) {
+    if (inplace) {  // MRHS = 3: outputs in place of the stage's vector rows, stored by the producer's TMA
+      static const LevelKernel p8[3] = {level_kernel<double2, 0, 8, 1, 3, false, 0>,
+                                        level_kernel<double2, 0, 8, 1, 3, false, 1>,
+                                        level_kernel<double2, 0, 8, 1, 3, false, 2>};
+      static const LevelKernel p16[3] = {level_kernel<double2, 0, 16, 1, 3, false, 0>,
+                                         level_kernel<double2, 0, 16, 1, 3, false, 1>,
+                                         level_kernel<double2, 0, 16, 1, 3, false, 2>};
+      return ncw == 16 ? p16[dt] : p8[dt];
+    }
     if (tout) {
       static const LevelKernel t[3] = {level_kernel<double2, 0, 8, 1, 2, false, 0>,
                                        level_kernel<double2, 0, 8, 1, 2, false, 1>,
@@ -228,7 +243,8 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   const uint64_t vec_col = adjoint ? static_cast<uint64_t>(nt) * R : C;  // vector elems per unit per rhs
   const uint64_t m_out = adjoint ? C : static_cast<uint64_t>(nt) * R;
   // right-hand sides per tile: all of them unless one unit no longer fits a stage
-  uint32_t kt = mrhs ? std::min<uint32_t>(k, 128) : k;
+  static const uint32_t kt_max = static_cast<uint32_t>(std::max(8, env_int("BF_MRHS_KT_MAX", 128)));
+  uint32_t kt = mrhs ? std::min<uint32_t>(k, kt_max) : k;
   while (kt > 1 && (fac_unit + vec_col * kt) * esz > sh.stage_bytes) kt = (kt + 1) / 2;
   if (mrhs && kt > 4) kt = (kt + 3) / 4 * 4;
   if (esz == 8 && kt > 1 && (kt & 1)) ++kt;
@@ -326,6 +342,7 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   }
   a.stages = static_cast<uint32_t>(stages);
   a.dbg_nomath = env_int("BF_DBG_NOMATH", 0);
+  a.dbg_noload = mrhs ? env_int("BF_DBG_NOLOAD", 0) : 0;
   if (a.use_dmma) {  // warp tile: the largest that still gives every consumer warp an item
     const uint64_t ncw = tout ? kTout.ncw : (a.use_dmma == 2 && remap < 3) ? sh.ncw : kMrhs.ncw;
     auto di = [&](uint64_t mt, uint64_t n8) {
@@ -341,8 +358,19 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   // kernels it costs the many-RHS paths registers and ~8% (cfg2 k=256)
   const bool push = remap >= 3;
   const int kncw = tout ? kTout.ncw : (mrhs && (push || a.use_dmma != 2)) ? kMrhs.ncw : sh.ncw;
+  // in-place outputs (MRHS = 3): every consumer warp holds at most one warp item per tile,
+  // the outputs fit the tile's vector rows, and the rows have one stride in every tile
+  bool inplace = false;
+  if (a.use_dmma == 2 && !push && !tout && !accumulate && a.bulk && !inplace_disabled() && (kncw == 8 || kncw == 16) &&
+      m_out <= vec_col && (a.vld != 0 || a.ktiles == 1)) {
+    const uint64_t mt = a.dtile == 2 ? 1 : 2, n8 = a.dtile == 0 ? 4 : 2;
+    const uint64_t items = U * ((m_out + 8 * mt - 1) / (8 * mt)) * ((a.kt + 8 * n8 - 1) / (8 * n8));
+    inplace = items <= static_cast<uint64_t>(kncw);
+  }
+  a.inplace = inplace ? 1 : 0;
+  a.old = inplace ? (a.vld ? a.vld : a.kt) : a.old;
   LevelKernel kern =
-      a.use_dmma == 2 && !push ? dmma_kernel<E>(tout, kncw, a.dtile)
+      a.use_dmma == 2 && !push ? dmma_kernel<E>(tout, kncw, a.dtile, inplace)
       : mrhs ? (push ? level_kernel<E, 0, kMrhs.ncw, kMrhs.ctas_per_sm, 1, true>
                      : level_kernel<E, 0, kMrhs.ncw, kMrhs.ctas_per_sm, 1, false>)
            : (push ? level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, true>
@@ -358,7 +386,7 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
     fprintf(stderr, "[bf] level_kernel %s%s R=%u C=%u nt=%u units=%llu k=%u kt=%u U=%llu ntiles=%u grid=%llu smem=%zu dmma=%d\n",
             mrhs ? "mrhs" : "stream", push ? "+push" : "", R, C, nt, static_cast<unsigned long long>(units), k, kt,
             static_cast<unsigned long long>(U), a.ntiles, static_cast<unsigned long long>(grid), smem,
-            a.use_dmma + (tout ? 10 : 0));
+            a.use_dmma + (tout ? 10 : 0) + (inplace ? 20 : 0));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3((kncw + 1) * 32);

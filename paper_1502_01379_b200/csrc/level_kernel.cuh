@@ -65,7 +65,9 @@ struct LevelArgs {
   uint32_t old, out_elems;
   uint32_t stages;    // pipeline depth when the kernel's STAGES template argument is 0 (<= 8)
   uint32_t dtile;     // DMMA warp tile: 0 = 2 x 4, 1 = 2 x 2, 2 = 1 x 2 (8 x 8 tiles)
-  int dbg_nomath;     // BF_DBG_NOMATH=1 (diagnostics only): DMMA consumers skip the k loop
+  int dbg_nomath;     // BF_DBG_NOMATH=1 (diagnostics only): many-RHS consumers skip their k loops
+  int dbg_noload;     // BF_DBG_NOLOAD=1 (diagnostics only): the producer moves no data (compute + stores only)
+  int inplace;        // MRHS = 3: outputs overwrite the stage's vector rows (one warp item per warp)
 };
 
 // remap 3/4 receive buffers of every part ([sender][own][other local][rho][k]); a
@@ -396,7 +398,7 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, const Peer
         arow[i] = fs + (static_cast<size_t>(base + (tt << t.lgPe)) * a.R + rho) * a.C;
       }
       const E* x = vs + static_cast<size_t>(ul) * a.C * kc + col0;
-      for (uint32_t c = 0; c < a.C; ++c) {
+      for (uint32_t c = 0, ce = a.dbg_nomath ? 0 : a.C; c < ce; ++c) {
         E xv[TN];
 #pragma unroll
         for (int j = 0; j < TN; ++j) xv[j] = colok[j] ? x[static_cast<size_t>(c) * kc + j * LC] : Cx<E>::make(0, 0);
@@ -425,7 +427,7 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, const Peer
           if (colok[j]) dst[j * LC] = Cx<E>::make(re[i][j], im[i][j]);
       }
     } else {
-      for (uint32_t tt = 0; tt < a.nt; ++tt) {
+      for (uint32_t tt = 0, te = a.dbg_nomath ? 0 : a.nt; tt < te; ++tt) {
         const uint32_t r0 = (base + (tt << t.lgPe)) * a.R;
         for (uint32_t rho = 0; rho < a.R; ++rho) {
           const size_t row = static_cast<size_t>(r0 + rho);
@@ -503,7 +505,11 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
   const uint32_t nmt = (m_out + MT * 8 - 1) / (MT * 8), nnt = (kc + NT * 8 - 1) / (NT * 8);
   const uint32_t items = U * nmt * nnt;
   const uint32_t lr = lane >> 2, lk = lane & 3;
-  for (uint32_t it = warp; it < items; it += nwarps) {
+  // in place (MRHS = 3): one round, every consumer warp (items <= warps, host-checked)
+  // meets the barrier that ends all reads of the stage before any output overwrites it
+  const bool inplace = ob != nullptr && a.inplace;
+  for (uint32_t it = warp; inplace ? it == static_cast<uint32_t>(warp) : it < items; it += nwarps) {
+    const bool act = it < items;
     const uint32_t ntile = it % nnt;
     const uint32_t rest = it / nnt;
     const uint32_t mt = rest % nmt, ul = rest / nmt;
@@ -529,7 +535,8 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
       const uint32_t tt = m / a.R, rho = m - tt * a.R;
       arow[i] = (base + (tt << t.lgPe)) * a.R + rho;
     }
-    for (uint32_t k0 = 0; k0 < kdim; k0 += 4) {
+    const uint32_t kd = act ? kdim : 0;
+    for (uint32_t k0 = 0; k0 < kd; k0 += 4) {
       const uint32_t kk = k0 + lk;
       const bool kok = kk < kdim;
       // adjoint: the k index runs over block rows j = (t, rho)
@@ -619,6 +626,8 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
           }
     }
     // epilogue: element (m0 + 8i + lane/4, n0 + 8j + 2(lane%4) + q)
+    if (inplace) asm volatile("bar.sync 1, %0;" ::"r"(nwarps * 32) : "memory");
+    if (ob && !act) continue;
     if (ob) {  // into the shared-memory output tile (row ul * m_out + m); TMA stores it
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
@@ -801,7 +810,32 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) level_kernel(const Level
         continue;
       }
       if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
+      if constexpr (MRHS == 3) {
+        // tile it - S left its outputs in this stage's vector rows: store them (TMA), and
+        // reuse the stage once the engine has read them
+        if (it >= S) {
+          const uint32_t prev = tile - S * gridDim.x;
+          store_tile_rows<E>(a, pa, prev, st + static_cast<size_t>(a.nt) * (1u << a.lgU) * a.R * a.fld, lane);
+          bulk_wait_read<0>();
+        }
+      }
+      if (a.dbg_noload) {
+        if (lane == 0) mbar_arrive(&full[s]);
+        continue;
+      }
       produce_tile<E>(a, tile, st, &full[s], lane, pol);
+    }
+    if constexpr (MRHS == 3) {  // the last S tiles' outputs
+      const uint32_t first = it > S ? it - S : 0;
+      for (uint32_t j = first; j < it; ++j) {
+        const uint32_t s = j % S;
+        mbar_wait(&empty[s], (j / S) & 1);
+        store_tile_rows<E>(a, pa, blockIdx.x + j * gridDim.x,
+                           stage0 + static_cast<size_t>(s) * a.stage_elems +
+                               static_cast<size_t>(a.nt) * (1u << a.lgU) * a.R * a.fld,
+                           lane);
+      }
+      bulk_wait_all();
     }
   } else {
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -809,7 +843,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) level_kernel(const Level
     for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
       const uint32_t s = it % S;
       mbar_wait(&full[s], (it / S) & 1);
-      if constexpr (MRHS == 2) {
+      if constexpr (MRHS == 3) {
+        E* stg = stage0 + static_cast<size_t>(s) * a.stage_elems;
+        consume_tile_mrhs_any<E, PUSH, DT>(a, pa, tile, stg, warp, lane, NCW,
+                                           stg + static_cast<size_t>(a.nt) * (1u << a.lgU) * a.R * a.fld);
+        fence_proxy_async_smem();  // the outputs (generic proxy) are read by the TMA store (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        continue;
+      } else if constexpr (MRHS == 2) {
         // output buffer it & 1 was last stored by tile it - 2: its reads must be done
         if (warp == 0) bulk_wait_read<1>();
         consumer_bar<NCW>();
