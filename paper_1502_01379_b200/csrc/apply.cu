@@ -361,7 +361,8 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   // in-place outputs (MRHS = 3): every consumer warp holds at most one warp item per tile,
   // the outputs fit the tile's vector rows, and the rows have one stride in every tile
   bool inplace = false;
-  if (a.use_dmma == 2 && !push && !tout && !accumulate && a.bulk && !inplace_disabled() && (kncw == 8 || kncw == 16) &&
+  // (8-warp shapes only: the 16-warp quadtree levels measured 2-5% slower in place)
+  if (a.use_dmma == 2 && !push && !tout && !accumulate && a.bulk && !inplace_disabled() && kncw == 8 &&
       m_out <= vec_col && (a.vld != 0 || a.ktiles == 1)) {
     const uint64_t mt = a.dtile == 2 ? 1 : 2, n8 = a.dtile == 0 ? 4 : 2;
     const uint64_t items = U * ((m_out + 8 * mt - 1) / (8 * mt)) * ((a.kt + 8 * n8 - 1) / (8 * n8));

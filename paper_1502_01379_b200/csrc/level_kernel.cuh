@@ -536,45 +536,9 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
       arow[i] = (base + (tt << t.lgPe)) * a.R + rho;
     }
     const uint32_t kd = act ? kdim : 0;
-    for (uint32_t k0 = 0; k0 < kd; k0 += 4) {
-      const uint32_t kk = k0 + lk;
-      const bool kok = kk < kdim;
-      // adjoint: the k index runs over block rows j = (t, rho)
-      uint32_t jrow = 0;
-      if (a.adjoint) {
-        const uint32_t kj = kok ? kk : 0;
-        const uint32_t tt = (kj >= a.R) + (kj >= 2 * a.R) + (kj >= 3 * a.R);  // nt <= 4: no division
-        jrow = (base + (tt << t.lgPe)) * a.R + (kj - tt * a.R);
-      }
-      double ar[MT], ai[MT], nai[MT];
-#pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        const uint32_t m = m0 + 8 * i + lr;
-        double2 v = make_double2(0, 0);
-        if (kok && m < m_out) {
-          if (!a.adjoint) {
-            v = fs[static_cast<size_t>(arow[i]) * fld + kk];
-          } else {
-            v = fs[static_cast<size_t>(jrow) * fld + m];
-            v.y = neg(v.y);  // A^H
-          }
-        }
-        ar[i] = v.x;
-        ai[i] = v.y;
-        nai[i] = neg(v.y);
-      }
-      double br[NT], bi[NT];
-#pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        const uint32_t n = n0 + 8 * j + lr;
-        double2 v = make_double2(0, 0);
-        if (kok && n < kc) {
-          const size_t row = a.adjoint ? jrow : static_cast<size_t>(ul) * a.C + kk;
-          v = vs[row * vld + n];
-        }
-        br[j] = v.x;
-        bi[j] = v.y;
-      }
+    // one complex k-step from fragments (ar + i ai of A, br + i bi of X)
+    auto mma_step = [&](const double (&ar)[MT], const double (&ai)[MT], const double (&br)[NT],
+                        const double (&bi)[NT]) {
       if constexpr (GAUSS) {
         double as[MT], bs[NT];
 #pragma unroll
@@ -595,6 +559,9 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
 #pragma unroll
           for (int j = 0; j < NT; ++j) dmma(cs[i][j][0], cs[i][j][1], as[i], bs[j]);
       } else {
+        double nai[MT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) nai[i] = neg(ai[i]);
         // two passes over the tiles: the two products accumulated into one register pair
         // are 2 MT NT instructions apart, not back to back
 #pragma unroll
@@ -611,6 +578,97 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
             dmma(cr[i][j][0], cr[i][j][1], nai[i], bi[j]);
             dmma(ci[i][j][0], ci[i][j][1], ai[i], br[j]);
           }
+      }
+    };
+    // Full tiles (every fragment in range, k steps inside one block for the adjoint):
+    // no predicates, pointer increments only (cfg2: m_out = 32, kc = 128, k = 32).
+    const bool full = (m_out % (8 * MT)) == 0 && (kc % (8 * NT)) == 0 && (a.R % 4) == 0 && (a.C % 4) == 0;
+    if (full && !a.adjoint) {
+      const double2* ap[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) ap[i] = fs + static_cast<size_t>(arow[i]) * fld + lk;
+      const double2* bp = vs + (static_cast<size_t>(ul) * a.C + lk) * vld + n0 + lr;
+      const size_t bstep = 4 * static_cast<size_t>(vld);
+      for (uint32_t k0 = 0; k0 < kd; k0 += 4, bp += bstep) {
+        double ar[MT], ai[MT], br[NT], bi[NT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const double2 v = ap[i][k0];
+          ar[i] = v.x;
+          ai[i] = v.y;
+        }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const double2 v = bp[8 * j];
+          br[j] = v.x;
+          bi[j] = v.y;
+        }
+        mma_step(ar, ai, br, bi);
+      }
+    } else if (full) {  // adjoint: k runs over block rows (t, rho)
+      const uint32_t ntk = kd ? a.nt : 0;
+      for (uint32_t tt = 0; tt < ntk; ++tt) {
+        const size_t row0 = static_cast<size_t>(base + (tt << t.lgPe)) * a.R + lk;
+        const double2* ap = fs + row0 * fld + m0 + lr;
+        const double2* bp = vs + row0 * vld + n0 + lr;
+        const size_t astep = 4 * static_cast<size_t>(fld), bstep = 4 * static_cast<size_t>(vld);
+        for (uint32_t rho0 = 0; rho0 < a.R; rho0 += 4, ap += astep, bp += bstep) {
+          double ar[MT], ai[MT], br[NT], bi[NT];
+#pragma unroll
+          for (int i = 0; i < MT; ++i) {
+            const double2 v = ap[8 * i];
+            ar[i] = v.x;
+            ai[i] = neg(v.y);  // A^H
+          }
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const double2 v = bp[8 * j];
+            br[j] = v.x;
+            bi[j] = v.y;
+          }
+          mma_step(ar, ai, br, bi);
+        }
+      }
+    } else {
+      for (uint32_t k0 = 0; k0 < kd; k0 += 4) {
+        const uint32_t kk = k0 + lk;
+        const bool kok = kk < kdim;
+        // adjoint: the k index runs over block rows j = (t, rho)
+        uint32_t jrow = 0;
+        if (a.adjoint) {
+          const uint32_t kj = kok ? kk : 0;
+          const uint32_t tt = (kj >= a.R) + (kj >= 2 * a.R) + (kj >= 3 * a.R);  // nt <= 4: no division
+          jrow = (base + (tt << t.lgPe)) * a.R + (kj - tt * a.R);
+        }
+        double ar[MT], ai[MT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const uint32_t m = m0 + 8 * i + lr;
+          double2 v = make_double2(0, 0);
+          if (kok && m < m_out) {
+            if (!a.adjoint) {
+              v = fs[static_cast<size_t>(arow[i]) * fld + kk];
+            } else {
+              v = fs[static_cast<size_t>(jrow) * fld + m];
+              v.y = neg(v.y);  // A^H
+            }
+          }
+          ar[i] = v.x;
+          ai[i] = v.y;
+        }
+        double br[NT], bi[NT];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const uint32_t n = n0 + 8 * j + lr;
+          double2 v = make_double2(0, 0);
+          if (kok && n < kc) {
+            const size_t row = a.adjoint ? jrow : static_cast<size_t>(ul) * a.C + kk;
+            v = vs[row * vld + n];
+          }
+          br[j] = v.x;
+          bi[j] = v.y;
+        }
+        mma_step(ar, ai, br, bi);
       }
     }
     if constexpr (GAUSS) {  // (T1, T2, T3) -> (re, im)
