@@ -254,6 +254,35 @@ def companion_cfg1(steps, warm):
             "cpu_reference_value": n * k / t_cpu, "cpu_reference_ms": t_cpu * 1e3}
 
 
+def companion_many_rhs(plan, f, n, steps, warm, k=256):
+    """BASELINE configs[2]'s 256-RHS complex128 apply on the same cfg2 plan: device time,
+    algorithmic FP64 rate and its fraction of the measured DMMA peak."""
+    import torch
+    g = torch.from_numpy(rhs_input(n, k)).cuda()
+    out = torch.empty_like(g)
+    ws = torch.empty(plan.workspace_bytes(k), dtype=torch.uint8, device="cuda")
+    for _ in range(max(2, min(warm, 3))):
+        plan.apply(g, out=out, workspace=ws)
+    stream = torch.cuda.current_stream()
+    nsteps = max(3, min(steps, 10))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(nsteps):
+        plan.apply(g, out=out, workspace=ws)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / nsteps
+    _, flops = algorithmic(f, k, 16)
+    peak = float(json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))["dmma_m8n8k4_tflops"])
+    tf = flops / (ms / 1e3) / 1e12
+    del g, out, ws
+    torch.cuda.empty_cache()
+    return {"workload": f"cfg2 k={k} c128 (same plan)", "value": n * k / (ms / 1e3), "unit": "samples/s",
+            "ms_per_step": ms, "steps": nsteps, "fp64_tflops_algorithmic": tf, "dmma_peak_tflops": peak,
+            "frac": tf / peak}
+
+
 def run_sharded(args, world, rank, local):
     """N > 1: the same workload sharded over the ranks (strong scaling): each rank
     owns m/N middle nodes per side, runs its down half, the middle factor is one
@@ -548,6 +577,8 @@ def main():
     if rank == 0 and world == 1 and args.config == "cfg2" and not args.no_also:
         del ws
         also = companion_cfg1(steps, warm)
+        if args.dtype == "c128" and k == 1:
+            also = {**also, "cfg2_k256": companion_many_rhs(plan, f, n, steps, warm)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
