@@ -113,6 +113,14 @@ using LevelKernel = void (*)(LevelArgs, PeerArgs);
 
 // complex128 3-multiplication DMMA kernels, one instantiation per warp tile (dt):
 // MRHS = 2 (TMA-stored outputs) or 1 (register stores) with 8 or 16 consumer warps
+template <typename E>
+LevelKernel ffma16_kernel() {
+  if constexpr (std::is_same<E, float2>::value)
+    return level_kernel<float2, 0, 16, 1, 1, false>;
+  else
+    return nullptr;
+}
+
 // BF_NO_INPLACE=1: many-RHS DMMA consumers store their outputs from registers (MRHS = 1)
 bool inplace_disabled() {
   static const bool off = env_int("BF_NO_INPLACE", 0) != 0;
@@ -243,7 +251,10 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   const uint64_t vec_col = adjoint ? static_cast<uint64_t>(nt) * R : C;  // vector elems per unit per rhs
   const uint64_t m_out = adjoint ? C : static_cast<uint64_t>(nt) * R;
   // right-hand sides per tile: all of them unless one unit no longer fits a stage
-  static const uint32_t kt_max = static_cast<uint32_t>(std::max(8, env_int("BF_MRHS_KT_MAX", 128)));
+  // right-hand sides per tile: up to 128 (complex128) / 256 (complex64: a whole 256-RHS
+  // row range in one contiguous copy; cfg2 c64 k=256 34.5 -> 30.2 ms)
+  static const int kt_env = env_int("BF_MRHS_KT_MAX", 0);
+  const uint32_t kt_max = kt_env > 0 ? static_cast<uint32_t>(std::max(8, kt_env)) : (sizeof(E) == 8 ? 256u : 128u);
   uint32_t kt = mrhs ? std::min<uint32_t>(k, kt_max) : k;
   while (kt > 1 && (fac_unit + vec_col * kt) * esz > sh.stage_bytes) kt = (kt + 1) / 2;
   if (mrhs && kt > 4) kt = (kt + 3) / 4 * 4;
@@ -270,7 +281,10 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   // complex128 always does; complex64 needs even block sizes and, when a row is split
   // into k-tiles, even k and kt.
   a.use_dmma = mrhs && esz == 16 && kt >= 16 && !dmma_disabled() ? (gauss_disabled() ? 1 : 2) : 0;
-  a.bulk = aligned && (esz == 16 || (R % 2 == 0 && C % 2 == 0 && (a.ktiles == 1 || (k % 2 == 0 && kt % 2 == 0))));
+  // complex64: blocks of an even element count (R C even) keep every block start 16-byte
+  // aligned, and an even k (and kt) every vector row (cfg3/cfg4b: R = 25, C = 100)
+  a.bulk = aligned && (esz == 16 || (R % 2 == 0 && C % 2 == 0 && (a.ktiles == 1 || (k % 2 == 0 && kt % 2 == 0))) ||
+                       ((static_cast<uint64_t>(R) * C) % 2 == 0 && k % 2 == 0 && (a.ktiles == 1 || kt % 2 == 0)));
   a.fld = C;
   a.vld = 0;
   if (a.use_dmma && a.bulk && a.ktiles > 1 && !pad_disabled()) {  // rows are copied one by one anyway
@@ -357,7 +371,10 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   // the peer-push epilogue (remap 3/4) is its own instantiation: compiled into the common
   // kernels it costs the many-RHS paths registers and ~8% (cfg2 k=256)
   const bool push = remap >= 3;
-  const int kncw = tout ? kTout.ncw : (mrhs && (push || a.use_dmma != 2)) ? kMrhs.ncw : sh.ncw;
+  // complex64 FFMA consumers may run 16 warps too (their own instantiation; complex128's
+  // generic kernel stays at 8: it also carries the 4-product DMMA paths)
+  const bool ffma16 = mrhs && !push && a.use_dmma == 0 && sizeof(E) == 8 && sh.ncw == 16;
+  const int kncw = tout ? kTout.ncw : ffma16 ? 16 : (mrhs && (push || a.use_dmma != 2)) ? kMrhs.ncw : sh.ncw;
   // in-place outputs (MRHS = 3): every consumer warp holds at most one warp item per tile,
   // the outputs fit the tile's vector rows, and the rows have one stride in every tile
   bool inplace = false;
@@ -372,8 +389,9 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   a.old = inplace ? (a.vld ? a.vld : a.kt) : a.old;
   LevelKernel kern =
       a.use_dmma == 2 && !push ? dmma_kernel<E>(tout, kncw, a.dtile, inplace)
-      : mrhs ? (push ? level_kernel<E, 0, kMrhs.ncw, kMrhs.ctas_per_sm, 1, true>
-                     : level_kernel<E, 0, kMrhs.ncw, kMrhs.ctas_per_sm, 1, false>)
+      : mrhs ? (push     ? level_kernel<E, 0, kMrhs.ncw, kMrhs.ctas_per_sm, 1, true>
+                : ffma16 ? ffma16_kernel<E>()
+                         : level_kernel<E, 0, kMrhs.ncw, kMrhs.ctas_per_sm, 1, false>)
            : (push ? level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, true>
                    : level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, false>);
   BF_CUDA(allow_max_dyn_smem(kern));

@@ -383,6 +383,7 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, const Peer
     bool colok[TN];
 #pragma unroll
     for (int j = 0; j < TN; ++j) colok[j] = col0 + j * LC < kc;
+    const bool colfull = (kc % (LC * TN)) == 0;
     Rl re[TM][TN], im[TM][TN];
 #pragma unroll
     for (int i = 0; i < TM; ++i)
@@ -398,19 +399,41 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, const Peer
         arow[i] = fs + (static_cast<size_t>(base + (tt << t.lgPe)) * a.R + rho) * a.C;
       }
       const E* x = vs + static_cast<size_t>(ul) * a.C * kc + col0;
-      for (uint32_t c = 0, ce = a.dbg_nomath ? 0 : a.C; c < ce; ++c) {
-        E xv[TN];
+      const uint32_t ce = a.dbg_nomath ? 0 : a.C;
+      if (colfull) {  // every column of the warp tile in range: no predicates, pointer steps
+        const E* xp = x;
+#pragma unroll 4
+        for (uint32_t c = 0; c < ce; ++c, xp += kc) {
+          E xv[TN];
 #pragma unroll
-        for (int j = 0; j < TN; ++j) xv[j] = colok[j] ? x[static_cast<size_t>(c) * kc + j * LC] : Cx<E>::make(0, 0);
+          for (int j = 0; j < TN; ++j) xv[j] = xp[j * LC];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) {
-          const E av = arow[i][c];
+          for (int i = 0; i < TM; ++i) {
+            const E av = arow[i][c];
 #pragma unroll
-          for (int j = 0; j < TN; ++j) {
-            re[i][j] = fma(av.x, xv[j].x, re[i][j]);
-            re[i][j] = fma(-av.y, xv[j].y, re[i][j]);
-            im[i][j] = fma(av.x, xv[j].y, im[i][j]);
-            im[i][j] = fma(av.y, xv[j].x, im[i][j]);
+            for (int j = 0; j < TN; ++j) {
+              re[i][j] = fma(av.x, xv[j].x, re[i][j]);
+              re[i][j] = fma(-av.y, xv[j].y, re[i][j]);
+              im[i][j] = fma(av.x, xv[j].y, im[i][j]);
+              im[i][j] = fma(av.y, xv[j].x, im[i][j]);
+            }
+          }
+        }
+      } else {
+        for (uint32_t c = 0; c < ce; ++c) {
+          E xv[TN];
+#pragma unroll
+          for (int j = 0; j < TN; ++j) xv[j] = colok[j] ? x[static_cast<size_t>(c) * kc + j * LC] : Cx<E>::make(0, 0);
+#pragma unroll
+          for (int i = 0; i < TM; ++i) {
+            const E av = arow[i][c];
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {
+              re[i][j] = fma(av.x, xv[j].x, re[i][j]);
+              re[i][j] = fma(-av.y, xv[j].y, re[i][j]);
+              im[i][j] = fma(av.x, xv[j].y, im[i][j]);
+              im[i][j] = fma(av.y, xv[j].x, im[i][j]);
+            }
           }
         }
       }
@@ -427,7 +450,33 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, const Peer
           if (colok[j]) dst[j * LC] = Cx<E>::make(re[i][j], im[i][j]);
       }
     } else {
-      for (uint32_t tt = 0, te = a.dbg_nomath ? 0 : a.nt; tt < te; ++tt) {
+      uint32_t cidx[TM];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) cidx[i] = min(rb + LR * i, m_out - 1);
+      for (uint32_t tt = 0, te = a.dbg_nomath ? 0 : a.nt; tt < te && colfull; ++tt) {
+        // every column in range: no predicates, pointer steps per block row
+        const uint32_t r0 = (base + (tt << t.lgPe)) * a.R;
+        const E* yp = vs + static_cast<size_t>(r0) * kc + col0;
+        const E* ap = fs + static_cast<size_t>(r0) * a.C;
+#pragma unroll 2
+        for (uint32_t rho = 0; rho < a.R; ++rho, yp += kc, ap += a.C) {
+          E yv[TN];
+#pragma unroll
+          for (int j = 0; j < TN; ++j) yv[j] = yp[j * LC];
+#pragma unroll
+          for (int i = 0; i < TM; ++i) {
+            const E av = ap[cidx[i]];
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {  // conj(av) * yv
+              re[i][j] = fma(av.x, yv[j].x, re[i][j]);
+              re[i][j] = fma(av.y, yv[j].y, re[i][j]);
+              im[i][j] = fma(av.x, yv[j].y, im[i][j]);
+              im[i][j] = fma(-av.y, yv[j].x, im[i][j]);
+            }
+          }
+        }
+      }
+      for (uint32_t tt = 0, te = a.dbg_nomath ? 0 : a.nt; tt < te && !colfull; ++tt) {
         const uint32_t r0 = (base + (tt << t.lgPe)) * a.R;
         for (uint32_t rho = 0; rho < a.R; ++rho) {
           const size_t row = static_cast<size_t>(r0 + rho);
@@ -786,6 +835,8 @@ __device__ __forceinline__ void consume_tile_mrhs_any(const LevelArgs& a, const 
     consume_tile_mrhs<E, 8, 2, 32, PUSH>(a, pa, tile, st, warp, lane, nwarps);
   else if (a.kt >= 32)
     consume_tile_mrhs<E, 16, 1, 32, PUSH>(a, pa, tile, st, warp, lane, nwarps);
+  else if (a.kt >= 16 && (a.adjoint ? a.C : a.nt * a.R) > 64)  // wide quadtree blocks: more, shorter items
+    consume_tile_mrhs<E, 4, 1, 16, PUSH>(a, pa, tile, st, warp, lane, nwarps);
   else if (a.kt >= 16)
     consume_tile_mrhs<E, 8, 1, 16, PUSH>(a, pa, tile, st, warp, lane, nwarps);
   else

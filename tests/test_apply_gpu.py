@@ -250,6 +250,8 @@ def test_quadtree_geometries(n_side, leaf, r, k):
     assert rel(f.plan().apply(gd), ochain.apply(oc, g)) <= TOL128
     assert rel(f.plan().apply(gd, adjoint=True), ochain.apply(oc, g, adjoint=True)) <= TOL128
     assert rel(f.plan("c64").apply(gd).to(torch.complex128), ochain.apply(oc, g)) <= TOL64
+    assert rel(f.plan("c64").apply(gd, adjoint=True).to(torch.complex128),
+               ochain.apply(oc, g, adjoint=True)) <= TOL64
 
 
 @pytest.mark.parametrize("n,leaf,r,k", [(1 << 18, 16, 16, 1), (1 << 16, 16, 8, 64)])
