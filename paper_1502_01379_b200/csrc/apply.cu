@@ -283,8 +283,9 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   a.use_dmma = mrhs && esz == 16 && kt >= 16 && !dmma_disabled() ? (gauss_disabled() ? 1 : 2) : 0;
   // complex64: blocks of an even element count (R C even) keep every block start 16-byte
   // aligned, and an even k (and kt) every vector row (cfg3/cfg4b: R = 25, C = 100)
-  a.bulk = aligned && (esz == 16 || (R % 2 == 0 && C % 2 == 0 && (a.ktiles == 1 || (k % 2 == 0 && kt % 2 == 0))) ||
-                       ((static_cast<uint64_t>(R) * C) % 2 == 0 && k % 2 == 0 && (a.ktiles == 1 || kt % 2 == 0)));
+  const uint64_t vec_unit = adjoint ? static_cast<uint64_t>(R) * k : static_cast<uint64_t>(C) * k;  // chunk stride
+  a.bulk = aligned && (esz == 16 || ((static_cast<uint64_t>(R) * C) % 2 == 0 &&
+                                     (a.ktiles == 1 ? vec_unit % 2 == 0 : (k % 2 == 0 && kt % 2 == 0))));
   a.fld = C;
   a.vld = 0;
   if (a.use_dmma && a.bulk && a.ktiles > 1 && !pad_disabled()) {  // rows are copied one by one anyway
