@@ -829,7 +829,9 @@ __device__ __forceinline__ void consume_tile_mrhs_any(const LevelArgs& a, const 
       return;
     }
   }
-  if (a.kt >= 128)
+  if (a.kt >= 256 && !PUSH)
+    consume_tile_mrhs<E, 4, 8, 32, PUSH>(a, pa, tile, st, warp, lane, nwarps);
+  else if (a.kt >= 128)
     consume_tile_mrhs<E, 4, 4, 32, PUSH>(a, pa, tile, st, warp, lane, nwarps);
   else if (a.kt >= 64)
     consume_tile_mrhs<E, 8, 2, 32, PUSH>(a, pa, tile, st, warp, lane, nwarps);
