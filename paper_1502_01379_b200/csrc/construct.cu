@@ -383,7 +383,7 @@ __global__ void k_fill_tall(MidArgs a, int which, int use_piv, double2* dst_base
 // Past the numerical rank both this and the reference pick rounding noise.
 constexpr int kGramChunk = 32;
 
-__global__ void __launch_bounds__(512) k_pivot_tall(MidArgs a, int which) {
+__global__ void __launch_bounds__(1024) k_pivot_tall(MidArgs a, int which) {
   extern __shared__ double2 tsm[];
   __shared__ double norms[kSetCap];
   __shared__ int picks[kSetCap];
@@ -406,43 +406,64 @@ __global__ void __launch_bounds__(512) k_pivot_tall(MidArgs a, int which) {
   double2* gscr = a.scr + static_cast<int64_t>(blockIdx.x) * 9 * SS;
   double2* G = S <= kSmemSet ? tsm + kGramChunk * S : gscr;       // S x S
   double2* Rm = S <= kSmemSet ? G + SS : gscr + SS;               // picks x S
-  // ---- Gram matrix: 4x4 register tiles over the upper block triangle, mirrored at the end
-  const int nc4 = (nc + 3) / 4;
-  const int ntiles = nc4 * (nc4 + 1) / 2;
+  // ---- Gram matrix: TB x TB register tiles over the upper block triangle, mirrored at the
+  // end. 2 x 2 tiles (528 for 64 columns) keep a 1024-thread CTA busy; each element is
+  // still one thread's sequential sum over the rows.
+  constexpr int TB = 2;
+  const int ncb = (nc + TB - 1) / TB;
+  const int ntiles = ncb * (ncb + 1) / 2;
   for (int tile0 = 0; tile0 < ntiles; tile0 += blockDim.x) {
     const int tid = tile0 + threadIdx.x;
     int ta = 0, rem = tid;
     if (tid < ntiles)
-      while (rem >= nc4 - ta) {
-        rem -= nc4 - ta;
+      while (rem >= ncb - ta) {
+        rem -= ncb - ta;
         ++ta;
       }
     const int tb = ta + rem;
-    double2 acc[4][4];
+    double2 acc[TB][TB];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < TB; ++u)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) acc[u][v] = make_double2(0, 0);
+      for (int v = 0; v < TB; ++v) acc[u][v] = make_double2(0, 0);
+    // row chunks staged through registers one chunk ahead: the next chunk's global loads
+    // are in flight while this one is multiplied (the staging latency was the kernel's
+    // main stall: 60% of samples at the chunk barrier)
+    constexpr int kPre = (kSetCap * kGramChunk + 1023) / 1024;
+    const int nel = ncb * TB * kGramChunk;
+    double2 pre[kPre];
+    auto fetch = [&](int r0) {
+#pragma unroll
+      for (int q = 0; q < kPre; ++q) {
+        const int x = threadIdx.x + q * static_cast<int>(blockDim.x);
+        const int c = x / kGramChunk, i = x % kGramChunk;
+        pre[q] = (x < nel && r0 + i < side && c < nc) ? T[static_cast<int64_t>(c) * side + r0 + i]
+                                                       : make_double2(0, 0);
+      }
+    };
+    fetch(0);
     for (int r0 = 0; r0 < side; r0 += kGramChunk) {
       const int rows = min(kGramChunk, side - r0);
       __syncthreads();
-      for (int x = threadIdx.x; x < nc4 * 4 * kGramChunk; x += blockDim.x) {
-        const int c = x / kGramChunk, i = x % kGramChunk;
-        chunk[i * S + c] = (i < rows && c < nc) ? T[static_cast<int64_t>(c) * side + r0 + i] : make_double2(0, 0);
+#pragma unroll
+      for (int q = 0; q < kPre; ++q) {
+        const int x = threadIdx.x + q * static_cast<int>(blockDim.x);
+        if (x < nel) chunk[(x % kGramChunk) * S + x / kGramChunk] = pre[q];
       }
       __syncthreads();
+      if (r0 + kGramChunk < side) fetch(r0 + kGramChunk);
       if (tid < ntiles)
         for (int i = 0; i < rows; ++i) {
-          double2 xa[4], xb[4];
+          double2 xa[TB], xb[TB];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            xa[u] = chunk[i * S + 4 * ta + u];
-            xb[u] = chunk[i * S + 4 * tb + u];
+          for (int u = 0; u < TB; ++u) {
+            xa[u] = chunk[i * S + TB * ta + u];
+            xb[u] = chunk[i * S + TB * tb + u];
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < TB; ++u)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
+            for (int v = 0; v < TB; ++v) {
               const double2 g = cmulc(xa[u], xb[v]);
               acc[u][v].x += g.x;
               acc[u][v].y += g.y;
@@ -451,10 +472,10 @@ __global__ void __launch_bounds__(512) k_pivot_tall(MidArgs a, int which) {
     }
     if (tid < ntiles) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < TB; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int ra = 4 * ta + u, cb = 4 * tb + v;
+        for (int v = 0; v < TB; ++v) {
+          const int ra = TB * ta + u, cb = TB * tb + v;
           if (ra < nc && cb < nc && ra <= cb) {
             G[ra * S + cb] = acc[u][v];
             G[cb * S + ra] = cconj(acc[u][v]);
@@ -1552,7 +1573,7 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
     BF_CUDA(allow_max_dyn_smem(k_pivot_tall));
     for (int which : {kCols, kRows}) {
       k_fill_tall<<<dim3(nblocks, yfill), T, 0, st>>>(a, which, 0, a.tall);
-      k_pivot_tall<<<nblocks, 512, tall_smem, st>>>(a, which);
+      k_pivot_tall<<<nblocks, 1024, tall_smem, st>>>(a, which);
       k_fill_tall<<<dim3(nblocks, yfill), T, 0, st>>>(a, which, 1, which == kCols ? a.qc : a.qr);
       launch_basis(a, nblocks, which, st);
     }
@@ -1622,7 +1643,7 @@ int bf_middle_probes(uint64_t n, uint32_t levels, uint32_t branching, uint32_t r
   k_init<<<(nblocks + 127) / 128, 128, 0, st>>>(a, block_ij);
   for (int which : {kCols, kRows}) {
     k_fill_probe<<<dim3(nblocks, yfill), T, 0, st>>>(a, which);
-    k_pivot_tall<<<nblocks, 512, tall_smem, st>>>(a, which);
+    k_pivot_tall<<<nblocks, 1024, tall_smem, st>>>(a, which);
     k_sel_probe<<<dim3(nblocks, yfill), T, 0, st>>>(a, which);
   }
   k_set_probe_counts<<<(nblocks + 127) / 128, 128, 0, st>>>(a);
