@@ -301,3 +301,20 @@ def test_plan_rejects_mismatched_factors():
                                 f.h_chain, f.v_outer)
     with pytest.raises(ValueError):
         wrong.apply(np.zeros(256))
+
+
+@pytest.mark.parametrize("leaf", [16, 1, 0.25])
+def test_many_rhs_shape_sweep(leaf):
+    """Many-RHS consumers across warp-tile choices (DMMA 2x4 / 2x2 / 1x2, in-place outputs,
+    k-tiles with partial last tiles, merge-only levels) and the complex64 FFMA tiles."""
+    n = 1 << 12
+    for r in (5, 12, 16):
+        f = synthetic_chain(bf.make_partition(n, leaf), r, seed=7 * r + int(4 * leaf))
+        oc = oracle_of(f)
+        for k in (8, 24, 40, 130):
+            g = complex_gaussian(np.random.default_rng(k + r), (n, k))
+            gd = torch.from_numpy(g).cuda()
+            for adj in (False, True):
+                want = ochain.apply(oc, g, adjoint=adj)
+                assert rel(f.plan().apply(gd, adjoint=adj), want) <= TOL128, (r, k, adj)
+                assert rel(f.plan("c64").apply(gd, adjoint=adj).to(torch.complex128), want) <= TOL64, (r, k, adj)
