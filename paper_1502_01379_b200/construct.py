@@ -423,7 +423,14 @@ def factorize(oracle, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0,
                 leaf_k, pieces = recurse(v_full[k0:k0 + cnt], p, r)
                 _place(chain, leaf, k0, cnt, leaf_k, pieces)
         else:
-            buf = torch.empty((kb, side, m, r), dtype=torch.complex128, device="cuda")
+            # slab recursions run on a side stream, overlapping the next block-rows' middle
+            # kernels (both are latency-bound at low occupancy); two slab buffers alternate
+            main = torch.cuda.current_stream()
+            side_stream = torch.cuda.Stream()
+            bufs = [torch.empty((kb, side, m, r), dtype=torch.complex128, device="cuda") for _ in range(2)]
+            done = [None, None]
+            cb = 0
+            buf = bufs[cb]
             filled, k_first = 0, 0
             step = ms.batch_rows()
             for k0 in range(0, m, step):
@@ -432,6 +439,8 @@ def factorize(oracle, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0,
                 uu, vv, ww = ms.blocks(ij)
                 for idx, k in enumerate(ks):
                     sl = slice(idx * m, (idx + 1) * m)
+                    if filled == 0 and done[cb] is not None:
+                        main.wait_event(done[cb])                                  # buffer free again
                     if axis == "u":
                         buf[filled] = uu[sl].permute(1, 0, 2)                      # slab[:, j, :]
                         weights[k] = ww[sl]
@@ -443,10 +452,18 @@ def factorize(oracle, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0,
                         k_first = k
                     filled += 1
                     if filled == kb or k == m - 1:
-                        leaf_k, pieces = recurse(buf[:filled], p, r)
-                        _place(chain, leaf, k_first, filled, leaf_k, pieces)
+                        side_stream.wait_stream(main)
+                        with torch.cuda.stream(side_stream):
+                            leaf_k, pieces = recurse(buf[:filled], p, r)
+                            _place(chain, leaf, k_first, filled, leaf_k, pieces)
+                            done[cb] = torch.cuda.Event()
+                            done[cb].record(side_stream)
+                        buf.record_stream(side_stream)
+                        cb ^= 1
+                        buf = bufs[cb]
                         filled = 0
-            del buf
+            main.wait_stream(side_stream)
+            del buf, bufs
         sides.append((BlockDiagonalFactor(leaf), tuple(TransferFactor(lvl, chain[lvl]) for lvl, _, _ in shapes)))
     del v_full
     (u_outer, g_chain), (v_outer, h_chain) = sides
