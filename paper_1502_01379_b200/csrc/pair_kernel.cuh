@@ -28,7 +28,27 @@ struct PairArgs {
   uint32_t nitems;       // G_A * P_A / 2
   uint32_t fld, vld;     // shared-memory row strides of block rows and vector rows
   uint32_t stage_elems;  // 8 blocks + 2 C vector rows
+  // adjoint pair ending the down half: the middle factor fused into the level-A* stores
+  // (remap 1 forward chain / 2 adjoint chain, as LevelArgs::remap; factors.py:180-190)
+  int remap;
+  uint32_t m, mr;        // middle nodes, rank of the middle vector
+  const double* mid_w;
 };
+
+// Destination element and weight of middle-vector entry e under the fused middle factor.
+__device__ __forceinline__ size_t pair_remap(const PairArgs& a, size_t e, double* w) {
+  if (!a.remap) {
+    *w = 1;
+    return e;
+  }
+  const uint32_t mrr = a.m * a.mr;
+  const uint32_t e32 = static_cast<uint32_t>(e), ia = e32 / mrr;
+  const uint32_t rem = e32 - ia * mrr;
+  const uint32_t ib = rem / a.mr, rho = rem - ib * a.mr;
+  const size_t dst = (static_cast<size_t>(ib) * a.m + ia) * a.mr + rho;
+  *w = a.remap == 1 ? __ldg(a.mid_w + dst) : __ldg(a.mid_w + (static_cast<size_t>(ia) * a.m + ib) * a.mr + rho);
+  return dst;
+}
 
 __device__ __forceinline__ void pair_dmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -214,7 +234,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) pair_kernel(const PairArgs 
           },
           [&](int gi, int sg, int kk, int n) { return mi[(sg * C + gi * R + kk) * vld + n]; },
           [&](int gi, int m, int n, double2 v) {
-            a.out[(static_cast<size_t>(g * a.pa + 2 * q + gi) * C + m) * K + n] = v;
+            double w;
+            const size_t e = pair_remap(a, static_cast<size_t>(g * a.pa + 2 * q + gi) * C + m, &w);
+            a.out[e * K + n] = make_double2(w * v.x, w * v.y);
           },
           warp, lane, NCW);
     }

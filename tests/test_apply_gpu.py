@@ -165,7 +165,7 @@ def test_synthetic_geometries(n, leaf, r, k):
     (1 << 12, 16, 16, 70),    # partial last chunk (6 RHS) and idle column slices
     (1 << 10, 16, 12, 300),   # r=12, 10 chunks
 ])
-def test_chunked_pairs_opt_in(n, leaf, r, k):
+def test_chunked_pairs_opt_in(n, leaf, r, k, env_flag="BF_CHUNK_PAIR"):
     """The k-chunked pair kernel is opt-in (BF_CHUNK_PAIR=1, read once per process): run the
     oracle comparison in a child process with it enabled."""
     import subprocess
@@ -188,9 +188,15 @@ e2 = rel(f.plan().apply(gd, adjoint=True), ochain.apply(oc, g, adjoint=True))
 assert e1 <= 1e-11 and e2 <= 1e-11, (e1, e2)
 print("ok", e1, e2)
 """
-    env = dict(os.environ, BF_CHUNK_PAIR="1")
+    env = dict(os.environ, **{env_flag: "1"})
     r_ = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, cwd=ROOT)
     assert r_.returncode == 0 and "ok" in r_.stdout, r_.stderr[-2000:]
+
+
+@pytest.mark.parametrize("n,leaf,r,k", [(1 << 16, 16, 8, 64), (1 << 12, 16, 6, 64)])
+def test_remap_pair_opt_in(n, leaf, r, k):
+    """BF_REMAP_PAIR=1: the down half's last pair carries the fused middle factor."""
+    test_chunked_pairs_opt_in(n, leaf, r, k, env_flag="BF_REMAP_PAIR")
 
 
 def test_config2_geometry_k1():
