@@ -95,24 +95,11 @@ Shape mrhs_shape() {
   return s;
 }
 constexpr uint32_t kMrhsMinK = 8;
-constexpr Shape kTout{3, 8, 1, 0};
-int tout_stages() {
-  static const int n = std::min(8, std::max(2, env_int("BF_TOUT_STAGES", kTout.stages)));
-  return n;
-}
-
-// The DMMA consumer stores its outputs from registers (MRHS = 1) unless BF_TOUT=1 selects
-// the TMA-stored output tiles (MRHS = 2; measured slower at cfg2 k = 256: its 3 stages
-// plus 2 output tiles force 64-RHS tiles, and small tiles lose more than the stores gain)
-bool tout_disabled() {
-  static const bool off = env_int("BF_TOUT", 0) == 0;
-  return off;
-}
 
 using LevelKernel = void (*)(LevelArgs, PeerArgs);
 
 // complex128 3-multiplication DMMA kernels, one instantiation per warp tile (dt):
-// MRHS = 2 (TMA-stored outputs) or 1 (register stores) with 8 or 16 consumer warps
+// MRHS = 3 (in-place outputs, TMA-stored) or 1 (register stores) with 8 or 16 consumer warps
 template <typename E>
 LevelKernel ffma16_kernel() {
   if constexpr (std::is_same<E, float2>::value)
@@ -135,7 +122,7 @@ bool inplace_disabled() {
 }
 
 template <typename E>
-LevelKernel dmma_kernel(bool tout, int ncw, uint32_t dt, bool inplace = false) {
+LevelKernel dmma_kernel(int ncw, uint32_t dt, bool inplace) {
   if constexpr (std::is_same<E, double2>::value) {
     if (inplace) {  // MRHS = 3: outputs in place of the stage's vector rows, stored by the producer's TMA
       static const LevelKernel p8[3] = {level_kernel<double2, 0, 8, 1, 3, false, 0>,
@@ -145,12 +132,6 @@ LevelKernel dmma_kernel(bool tout, int ncw, uint32_t dt, bool inplace = false) {
                                          level_kernel<double2, 0, 16, 1, 3, false, 1>,
                                          level_kernel<double2, 0, 16, 1, 3, false, 2>};
       return ncw == 16 ? p16[dt] : p8[dt];
-    }
-    if (tout) {
-      static const LevelKernel t[3] = {level_kernel<double2, 0, 8, 1, 2, false, 0>,
-                                       level_kernel<double2, 0, 8, 1, 2, false, 1>,
-                                       level_kernel<double2, 0, 8, 1, 2, false, 2>};
-      return t[dt];
     }
     static const LevelKernel r8[3] = {level_kernel<double2, 0, 8, 1, 1, false, 0>,
                                       level_kernel<double2, 0, 8, 1, 1, false, 1>,
@@ -317,56 +298,12 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
       a.stage_elems = static_cast<uint32_t>(st2);
     }
   }
-  // MRHS = 2 (complex128 DMMA, plain stores or the fused middle remap): 3 stages plus two
-  // shared-memory output tiles drained by TMA bulk stores. Tile shape refit from scratch:
-  // the largest kt (<= 128) whose 3 padded stages + 2 output tiles fit, then as many units
-  // per tile as keep the 8 consumer warps busy.
-  bool tout = a.use_dmma && a.bulk && !accumulate && remap < 3 && !tout_disabled();
-  int stages = sh.stages;
-  if (tout) {
-    auto pad_to = [](uint64_t x, uint64_t target) { return x + (target + 8 - x % 8) % 8; };
-    const uint64_t fld = pad_to(C, adjoint ? 2 : 4);
-    const uint64_t vrows = adjoint ? static_cast<uint64_t>(nt) * R : C;
-    const uint64_t avail = static_cast<uint64_t>(kMaxDynSmem) - 128;
-    bool ok = false;
-    for (uint32_t kt2 = std::min<uint32_t>(k, 128); kt2 >= 16; kt2 /= 2) {
-      const uint32_t kt4 = (kt2 + 3) / 4 * 4;
-      const uint64_t vld = pad_to(kt4, 2), old = kt4 | 1;
-      auto bytes = [&](uint64_t u) {
-        uint64_t stg = u * (static_cast<uint64_t>(nt) * R * fld + vrows * vld);
-        stg += stg & 1;
-        return (tout_stages() * stg + 2 * u * m_out * old) * esz;
-      };
-      if (bytes(1) > avail) continue;
-      const uint64_t nn = kt4 >= 32 ? 32 : 16;  // DMMA warp tile columns (NT x 8)
-      auto witems = [&](uint64_t u) { return u * ((m_out + 15) / 16) * ((kt4 + nn - 1) / nn); };
-      uint64_t U2 = 1;
-      while (nt == ntot && U2 * 2 <= units && witems(U2) < 2 * static_cast<uint64_t>(kTout.ncw) &&
-             bytes(U2 * 2) <= avail)
-        U2 *= 2;
-      uint64_t stg = U2 * (static_cast<uint64_t>(nt) * R * fld + vrows * vld);
-      stg += stg & 1;
-      a.kt = std::min<uint32_t>(kt4, k);
-      a.ktiles = (k + a.kt - 1) / a.kt;
-      a.lgU = ilog2(U2);
-      a.ntiles = static_cast<uint32_t>((units / U2) * a.ktiles);
-      a.fld = static_cast<uint32_t>(fld);
-      a.vld = static_cast<uint32_t>(vld);
-      a.old = static_cast<uint32_t>(old);
-      a.out_elems = static_cast<uint32_t>(U2 * m_out * old);
-      a.stage_elems = static_cast<uint32_t>(stg);
-      U = U2;
-      ok = true;
-      break;
-    }
-    tout = ok;
-    if (tout) stages = tout_stages();
-  }
+  const int stages = sh.stages;
   a.stages = static_cast<uint32_t>(stages);
   a.dbg_nomath = env_int("BF_DBG_NOMATH", 0);
   a.dbg_noload = mrhs ? env_int("BF_DBG_NOLOAD", 0) : 0;
   if (a.use_dmma) {  // warp tile: the largest that still gives every consumer warp an item
-    const uint64_t ncw = tout ? kTout.ncw : (a.use_dmma == 2 && remap < 3) ? sh.ncw : kMrhs.ncw;
+    const uint64_t ncw = (a.use_dmma == 2 && remap < 3) ? sh.ncw : kMrhs.ncw;
     auto di = [&](uint64_t mt, uint64_t n8) {
       return U * ((m_out + 8 * mt - 1) / (8 * mt)) * ((a.kt + 8 * n8 - 1) / (8 * n8));
     };
@@ -374,7 +311,7 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
     const int forced = env_int("BF_DTILE", -1);
     if (forced >= 0 && forced <= 2) a.dtile = static_cast<uint32_t>(forced);
   }
-  const size_t smem = 128 + static_cast<size_t>(stages) * a.stage_elems * esz + (tout ? 2ull * a.out_elems * esz : 0);
+  const size_t smem = 128 + static_cast<size_t>(stages) * a.stage_elems * esz;
   if (smem > 227 * 1024) return fail(BF_EINVAL, "rank too large: one block pair exceeds the shared-memory stage");
   // the peer-push epilogue (remap 3/4) is its own instantiation: compiled into the common
   // kernels it costs the many-RHS paths registers and ~8% (cfg2 k=256)
@@ -382,12 +319,12 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   // complex64 FFMA consumers may run 16 warps too (their own instantiation; complex128's
   // generic kernel stays at 8: it also carries the 4-product DMMA paths)
   const bool ffma16 = mrhs && !push && a.use_dmma == 0 && sizeof(E) == 8 && sh.ncw == 16;
-  const int kncw = tout ? kTout.ncw : ffma16 ? 16 : (mrhs && (push || a.use_dmma != 2)) ? kMrhs.ncw : sh.ncw;
+  const int kncw = ffma16 ? 16 : (mrhs && (push || a.use_dmma != 2)) ? kMrhs.ncw : sh.ncw;
   // in-place outputs (MRHS = 3): every consumer warp holds at most one warp item per tile,
   // the outputs fit the tile's vector rows, and the rows have one stride in every tile
   bool inplace = false;
   // (8-warp shapes only: the 16-warp quadtree levels measured 2-5% slower in place)
-  if (a.use_dmma == 2 && !push && !tout && !accumulate && a.bulk && !inplace_disabled() && kncw == 8 &&
+  if (a.use_dmma == 2 && !push && !accumulate && a.bulk && !inplace_disabled() && kncw == 8 &&
       m_out <= vec_col && (a.vld != 0 || a.ktiles == 1)) {
     const uint64_t mt = a.dtile == 2 ? 1 : 2, n8 = a.dtile == 0 ? 4 : 2;
     const uint64_t items = U * ((m_out + 8 * mt - 1) / (8 * mt)) * ((a.kt + 8 * n8 - 1) / (8 * n8));
@@ -396,14 +333,14 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   a.inplace = inplace ? 1 : 0;
   a.old = inplace ? (a.vld ? a.vld : a.kt) : a.old;
   LevelKernel kern =
-      a.use_dmma == 2 && !push ? dmma_kernel<E>(tout, kncw, a.dtile, inplace)
+      a.use_dmma == 2 && !push ? dmma_kernel<E>(kncw, a.dtile, inplace)
       : mrhs ? (push     ? level_kernel<E, 0, kMrhs.ncw, kMrhs.ctas_per_sm, 1, true>
                 : ffma16 ? ffma16_kernel<E>()
                          : level_kernel<E, 0, kMrhs.ncw, kMrhs.ctas_per_sm, 1, false>)
            : (push ? level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, true>
                    : level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, false>);
   BF_CUDA(allow_max_dyn_smem(kern));
-  const uint64_t per_sm = !tout && (kncw == sh.ncw) && smem * sh.ctas_per_sm <= 227 * 1024 ? sh.ctas_per_sm : 1;
+  const uint64_t per_sm = (kncw == sh.ncw) && smem * sh.ctas_per_sm <= 227 * 1024 ? sh.ctas_per_sm : 1;
   const uint64_t grid = std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(pl.sms) * per_sm);
   static const bool dbg = [] {
     const char* e = getenv("BF_DEBUG_LAUNCH");
@@ -413,7 +350,7 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
     fprintf(stderr, "[bf] level_kernel %s%s R=%u C=%u nt=%u units=%llu k=%u kt=%u U=%llu ntiles=%u grid=%llu smem=%zu dmma=%d\n",
             mrhs ? "mrhs" : "stream", push ? "+push" : "", R, C, nt, static_cast<unsigned long long>(units), k, kt,
             static_cast<unsigned long long>(U), a.ntiles, static_cast<unsigned long long>(grid), smem,
-            a.use_dmma + (tout ? 10 : 0) + (inplace ? 20 : 0));
+            a.use_dmma + (inplace ? 20 : 0));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3((kncw + 1) * 32);

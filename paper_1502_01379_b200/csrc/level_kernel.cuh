@@ -60,9 +60,9 @@ struct LevelArgs {
   // and vector rows (vld, 0 = the tile's kc). The DMMA consumer pads them so its
   // fragment loads hit 8 distinct 16-byte bank groups per quarter warp.
   uint32_t fld, vld;
-  // MRHS = 2 (DMMA consumer, outputs through shared memory + TMA bulk stores): output
-  // tile row stride (odd: conflict-free fragment writes) and elements per output buffer
-  uint32_t old, out_elems;
+  // MRHS = 3 (DMMA consumer, outputs in place of the stage's vector rows, TMA-stored by
+  // the producer): row stride of the output rows in shared memory
+  uint32_t old;
   uint32_t stages;    // pipeline depth when the kernel's STAGES template argument is 0 (<= 8)
   uint32_t dtile;     // DMMA warp tile: 0 = 2 x 4, 1 = 2 x 2, 2 = 1 x 2 (8 x 8 tiles)
   int dbg_nomath;     // BF_DBG_NOMATH=1 (diagnostics only): many-RHS consumers skip their k loops
@@ -845,7 +845,7 @@ __device__ __forceinline__ void consume_tile_mrhs_any(const LevelArgs& a, const 
     consume_tile_mrhs<E, 4, 1, 8, PUSH>(a, pa, tile, st, warp, lane, nwarps);
 }
 
-// MRHS = 2: the output tile of `tile` (rows ul * m_out + m in shared memory, stride
+// MRHS = 3: the output tile of `tile` (rows ul * m_out + m in shared memory, stride
 // a.old) to its global rows, one TMA bulk store per row, issued by the lanes of
 // one warp; each lane commits its own bulk group.
 template <typename E>
@@ -872,15 +872,10 @@ __device__ __forceinline__ void store_tile_rows(const LevelArgs& a, const PeerAr
   bulk_commit();
 }
 
-template <int NCW>
-__device__ __forceinline__ void consumer_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory");
-}
-
 // MRHS = 0: streaming consumer (one output per thread); MRHS = 1: register-tiled GEMM
-// consumer; MRHS = 2: the DMMA consumer with outputs staged in two shared-memory
-// buffers and written by TMA bulk stores, so a tile's stores drain while the next
-// tile computes (no register-to-global store phase in the consumer warps).
+// consumer; MRHS = 3: the DMMA consumer writing its outputs over the tile's consumed
+// vector rows, which the producer warp stores with TMA bulk copies before refilling the
+// stage (the consumer warps issue no global stores).
 template <typename E, int STAGES, int NCW, int MINB, int MRHS, bool PUSH, int DT = -1>
 __global__ void __launch_bounds__((NCW + 1) * 32, MINB) level_kernel(const LevelArgs a, const PeerArgs pa) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -962,19 +957,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) level_kernel(const Level
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         continue;
-      } else if constexpr (MRHS == 2) {
-        // output buffer it & 1 was last stored by tile it - 2: its reads must be done
-        if (warp == 0) bulk_wait_read<1>();
-        consumer_bar<NCW>();
-        E* ob = stage0 + static_cast<size_t>(S) * a.stage_elems + (it & 1) * static_cast<size_t>(a.out_elems);
-        consume_tile_mrhs_any<E, PUSH, DT>(a, pa, tile, stage0 + static_cast<size_t>(s) * a.stage_elems, warp, lane,
-                                           NCW, ob);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        fence_proxy_async_smem();
-        consumer_bar<NCW>();
-        if (warp == 0) store_tile_rows<E>(a, pa, tile, ob, lane);
-        continue;
       } else if (MRHS) {
         consume_tile_mrhs_any<E, PUSH, DT>(a, pa, tile, stage0 + static_cast<size_t>(s) * a.stage_elems, warp, lane,
                                            NCW);
@@ -983,9 +965,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) level_kernel(const Level
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-    }
-    if constexpr (MRHS == 2) {
-      if (warp == 0) bulk_wait_all();
     }
   }
 }
