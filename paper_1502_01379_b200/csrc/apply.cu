@@ -131,7 +131,10 @@ LevelKernel dmma_kernel(int ncw, uint32_t dt, bool inplace) {
       static const LevelKernel p16[3] = {level_kernel<double2, 0, 16, 1, 3, false, 0>,
                                          level_kernel<double2, 0, 16, 1, 3, false, 1>,
                                          level_kernel<double2, 0, 16, 1, 3, false, 2>};
-      return ncw == 16 ? p16[dt] : p8[dt];
+      static const LevelKernel p4[3] = {level_kernel<double2, 0, 4, 2, 3, false, 0>,
+                                        level_kernel<double2, 0, 4, 2, 3, false, 1>,
+                                        level_kernel<double2, 0, 4, 2, 3, false, 2>};
+      return ncw == 16 ? p16[dt] : ncw == 4 ? p4[dt] : p8[dt];
     }
     static const LevelKernel r8[3] = {level_kernel<double2, 0, 8, 1, 1, false, 0>,
                                       level_kernel<double2, 0, 8, 1, 1, false, 1>,
@@ -207,7 +210,22 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   // complex128 DMMA consumers: 16 warps for the wide quadtree blocks (C = 4r = 100: long
   // k loops, few warp items per tile; cfg3 0.75 -> 0.59 ms, cfg4b 14.6 -> 11.0 ms), 8
   // otherwise (cfg2 k = 256: 43.9 vs 47.3 ms; cfg1 0.26 vs 0.32 ms)
-  if (mrhs) sh.ncw = sh.ncw == 16 || sh.ncw == 8 || sh.ncw == 4 ? sh.ncw : (C > 64 ? 16 : 8);
+  // complex128 DMMA shapes with C <= 64 (binary trees, r <= 32): two independent 4-warp
+  // CTAs per SM on 48 KB stages (k = 64 tiles), each with its own in-place barrier, so the
+  // two CTAs' compute and store phases interleave (cfg2 k=256 41.5 -> 37.6 ms, k=64
+  // 10.8 -> 9.6 ms, k=16 6.1 -> 3.9 ms; cfg1 0.284 -> 0.271 ms)
+  if (mrhs && sh.ncw != 16 && sh.ncw != 8 && sh.ncw != 4) {
+    if (C > 64) {
+      sh.ncw = 16;
+    } else if (sizeof(E) == 16 && !dmma_disabled() && remap < 3 &&
+               (static_cast<uint64_t>(nt) * R * C + (adjoint ? static_cast<uint64_t>(nt) * R : C) * 16) * 16 <=
+                   48 * 1024) {
+      sh.ncw = 4;
+      if (env_int("BF_MRHS_STAGE_KB", 0) == 0) sh.stage_bytes = 48 * 1024;
+    } else {
+      sh.ncw = 8;
+    }
+  }
   if (mrhs && sh.ncw == 4) sh.ctas_per_sm = 2;  // two independent 4-warp CTAs per SM
   LevelArgs a{};
   a.fac = fac;
@@ -324,7 +342,7 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   // the outputs fit the tile's vector rows, and the rows have one stride in every tile
   bool inplace = false;
   // (8-warp shapes only: the 16-warp quadtree levels measured 2-5% slower in place)
-  if (a.use_dmma == 2 && !push && !accumulate && a.bulk && !inplace_disabled() && kncw == 8 &&
+  if (a.use_dmma == 2 && !push && !accumulate && a.bulk && !inplace_disabled() && (kncw == 8 || kncw == 4) &&
       m_out <= vec_col && (a.vld != 0 || a.ktiles == 1)) {
     const uint64_t mt = a.dtile == 2 ? 1 : 2, n8 = a.dtile == 0 ? 4 : 2;
     const uint64_t items = U * ((m_out + 8 * mt - 1) / (8 * mt)) * ((a.kt + 8 * n8 - 1) / (8 * n8));
