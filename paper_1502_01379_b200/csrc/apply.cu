@@ -87,11 +87,25 @@ int env_int(const char* name, int dflt) {
 Shape mrhs_shape() {
   static const Shape s = [] {
     Shape x = kMrhs;
-    x.stages = std::min(8, std::max(2, env_int("BF_MRHS_STAGES", kMrhs.stages)));
+    x.stages = std::min(8, std::max(1, env_int("BF_MRHS_STAGES", kMrhs.stages)));
     x.stage_bytes = static_cast<uint32_t>(env_int("BF_MRHS_STAGE_KB", kMrhs.stage_bytes / 1024)) * 1024;
     x.ncw = env_int("BF_MRHS_NCW", 0);  // 0: per launch (mrhs_warps)
     return x;
   }();
+  return s;
+}
+
+// complex128 levels with wide blocks (C > 64: the r = 25 quadtree, C = 4r = 100): one
+// 200 KB stage holds a whole unit (4 x 25 x 100 blocks), so the level runs as one launch
+// instead of t-range splits that re-read the inputs / accumulate partial outputs; the
+// single buffer costs less than the splits (cfg3 0.611 -> 0.543 ms, cfg4b 11.5 -> 10.0 ms)
+template <typename E>
+Shape mrhs_shape_for(uint32_t C) {
+  Shape s = mrhs_shape();
+  if (sizeof(E) == 16 && C > 64 && env_int("BF_MRHS_STAGES", 0) == 0 && env_int("BF_MRHS_STAGE_KB", 0) == 0) {
+    s.stages = 1;
+    s.stage_bytes = 200 * 1024;
+  }
   return s;
 }
 constexpr uint32_t kMrhsMinK = 8;
@@ -183,7 +197,7 @@ template <typename E>
 int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint64_t P, uint64_t units,
                  const void* in, void* out, uint32_t k, int adjoint, int remap, cudaStream_t st,
                  void* const* peers = nullptr) {
-  const Shape sh = k >= kMrhsMinK ? mrhs_shape() : stream_shape<E>();
+  const Shape sh = k >= kMrhsMinK ? mrhs_shape_for<E>(C) : stream_shape<E>();
   uint32_t nt_tile = nt;
   auto tile_elems = [&](uint64_t t) { return t * R * C + (adjoint ? t * R : static_cast<uint64_t>(C)); };
   while (nt_tile > 1 && tile_elems(nt_tile) * sizeof(E) > sh.stage_bytes) nt_tile /= 2;
@@ -206,7 +220,7 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
     return fail(BF_EINVAL, "middle vector too long for 32-bit remap indices");
   const bool mrhs = k >= kMrhsMinK;
   constexpr Shape ks = stream_shape<E>();
-  Shape sh = mrhs ? mrhs_shape() : ks;
+  Shape sh = mrhs ? mrhs_shape_for<E>(C) : ks;
   // complex128 DMMA consumers: 16 warps for the wide quadtree blocks (C = 4r = 100: long
   // k loops, few warp items per tile; cfg3 0.75 -> 0.59 ms, cfg4b 14.6 -> 11.0 ms), 8
   // otherwise (cfg2 k = 256: 43.9 vs 47.3 ms; cfg1 0.26 vs 0.32 ms)

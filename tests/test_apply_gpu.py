@@ -199,6 +199,36 @@ def test_remap_pair_opt_in(n, leaf, r, k):
     test_chunked_pairs_opt_in(n, leaf, r, k, env_flag="BF_REMAP_PAIR")
 
 
+def test_quadtree_t_range_split_many_rhs():
+    """Many-RHS quadtree levels whose 4-block units do not fit a stage run as t-range
+    launches (forward outputs per t, adjoint partial sums accumulated). The default
+    single 200 KB stage avoids them at r = 25; BF_MRHS_STAGES=2 BF_MRHS_STAGE_KB=112 (read
+    once per process, hence a child process) forces them."""
+    import subprocess
+    import sys
+    code = f"""
+import numpy as np, torch, sys
+sys.path[:0] = [{ROOT!r}, {os.path.join(ROOT, "tests")!r}]
+import paper_1502_01379_b200 as bf
+from paper_1502_01379_b200.synthetic import synthetic_chain
+from conftest import complex_gaussian
+from test_apply_gpu import oracle_of, rel
+from oracle import chain as ochain
+p = bf.make_quadtree_partition(128, 2)
+f = synthetic_chain(p, 25, seed=3)
+oc = oracle_of(f)
+g = complex_gaussian(np.random.default_rng(5), (p.n, 16))
+gd = torch.from_numpy(g).cuda()
+e1 = rel(f.plan().apply(gd), ochain.apply(oc, g))
+e2 = rel(f.plan().apply(gd, adjoint=True), ochain.apply(oc, g, adjoint=True))
+assert e1 <= 1e-11 and e2 <= 1e-11, (e1, e2)
+print("ok", e1, e2)
+"""
+    env = dict(os.environ, BF_MRHS_STAGES="2", BF_MRHS_STAGE_KB="112")
+    r_ = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, cwd=ROOT)
+    assert r_.returncode == 0 and "ok" in r_.stdout, r_.stderr[-2000:]
+
+
 def test_config2_geometry_k1():
     """BASELINE config 2 (FIO geometry N=2^20, r=16, leaf 16 -> L=16), synthetic factors, 1 RHS."""
     p = bf.make_partition(1 << 20, 16)
