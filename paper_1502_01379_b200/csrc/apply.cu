@@ -63,18 +63,32 @@ uint32_t ilog2(uint64_t x) {
 
 // Launch shapes: the streaming kernel (k small: HBM-bound on factor bytes) and
 // the register-tiled many-RHS kernel (k >= kMrhsMinK: FP64-FMA bound).
+#ifndef STREAM64_STAGES
+#define STREAM64_STAGES 3
+#endif
 struct Shape {
   int stages, ncw, ctas_per_sm;
   uint32_t stage_bytes;
 };
-constexpr Shape kStream{3, 2, 2, 34 * 1024 + 512};
+// two stages of 34.5 KB per CTA, four consumer warps, two CTAs per SM (cfg2 k=1: 1.34 ms
+// against 1.416 ms with three stages and two consumer warps; k=2 1.94 vs 3.00 ms; four or
+// more stages stop two CTAs fitting an SM)
+constexpr Shape kStream{2, 4, 2, 34 * 1024 + 512};
 // complex64 streams half the bytes per output: twice the consumer warps keep the
 // same per-SM output rate at the same stage size
-constexpr Shape kStream64{3, 4, 2, 34 * 1024 + 512};
+constexpr Shape kStream64{STREAM64_STAGES, 4, 2, 34 * 1024 + 512};
 template <typename E>
 constexpr Shape stream_shape() {
   return sizeof(E) == 8 ? kStream64 : kStream;
 }
+
+// Experiments only (complex128 streaming levels): BF_STREAM_{STAGES,KB,CTAS,NCW} select a
+// runtime-depth instantiation; unset, the tuned constexpr kStream shape is used.
+struct StreamExp {
+  bool on;
+  Shape s;
+};
+StreamExp stream_exp();
 constexpr Shape kMrhs{2, 8, 1, 112 * 1024};
 
 int env_int(const char* name, int dflt) {
@@ -84,6 +98,23 @@ int env_int(const char* name, int dflt) {
 
 // Many-RHS pipeline shape: depth (<= 8) and stage budget are launch arguments of the
 // STAGES = 0 instantiation (BF_MRHS_STAGES, BF_MRHS_STAGE_KB override them).
+StreamExp stream_exp() {
+  static const StreamExp x = [] {
+    StreamExp e{false, kStream};
+    const int st = env_int("BF_STREAM_STAGES", 0), kb = env_int("BF_STREAM_KB", 0);
+    const int ct = env_int("BF_STREAM_CTAS", 0), nw = env_int("BF_STREAM_NCW", 0);
+    if (st || kb || ct || nw) {
+      e.on = true;
+      if (st) e.s.stages = std::min(8, std::max(1, st));
+      if (kb) e.s.stage_bytes = static_cast<uint32_t>(kb) * 1024;
+      if (ct == 3) e.s.ctas_per_sm = 3;
+      if (nw == 4) e.s.ncw = 4;
+    }
+    return e;
+  }();
+  return x;
+}
+
 Shape mrhs_shape() {
   static const Shape s = [] {
     Shape x = kMrhs;
@@ -221,6 +252,8 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   const bool mrhs = k >= kMrhsMinK;
   constexpr Shape ks = stream_shape<E>();
   Shape sh = mrhs ? mrhs_shape_for<E>(C) : ks;
+  const bool sexp = !mrhs && sizeof(E) == 16 && remap < 3 && stream_exp().on;
+  if (sexp) sh = stream_exp().s;
   // complex128 DMMA consumers: 16 warps for the wide quadtree blocks (C = 4r = 100: long
   // k loops, few warp items per tile; cfg3 0.75 -> 0.59 ms, cfg4b 14.6 -> 11.0 ms), 8
   // otherwise (cfg2 k = 256: 43.9 vs 47.3 ms; cfg1 0.26 vs 0.32 ms)
@@ -370,6 +403,9 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
                 : ffma16 ? ffma16_kernel<E>()
                          : level_kernel<E, 0, kMrhs.ncw, kMrhs.ctas_per_sm, 1, false>)
            : (push ? level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, true>
+              : sexp ? (sh.ncw == 4 ? level_kernel<E, 0, 4, 2, 0, false>
+                        : sh.ctas_per_sm == 3 ? level_kernel<E, 0, 2, 3, 0, false>
+                                              : level_kernel<E, 0, 2, 2, 0, false>)
                    : level_kernel<E, ks.stages, ks.ncw, ks.ctas_per_sm, 0, false>);
   BF_CUDA(allow_max_dyn_smem(kern));
   const uint64_t per_sm = (kncw == sh.ncw) && smem * sh.ctas_per_sm <= 227 * 1024 ? sh.ctas_per_sm : 1;
