@@ -76,7 +76,7 @@ struct Shape {
 constexpr Shape kStream{2, 4, 2, 34 * 1024 + 512};
 // complex64 streams half the bytes per output: twice the consumer warps keep the
 // same per-SM output rate at the same stage size
-constexpr Shape kStream64{STREAM64_STAGES, 4, 2, 34 * 1024 + 512};
+constexpr Shape kStream64{STREAM64_STAGES, 8, 2, 34 * 1024 + 512};
 template <typename E>
 constexpr Shape stream_shape() {
   return sizeof(E) == 8 ? kStream64 : kStream;
