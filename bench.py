@@ -534,6 +534,14 @@ def main():
     roof = {"bound": "hbm", "achieved": tr_bytes / (tr_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
             "frac": tr_bytes / (tr_ms / 1e3) / 1e9 / hbm_peak,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
+    try:  # the levels are read-dominated (factor blocks read once, vectors L2-resident):
+        # their own ceiling is the streaming-read bandwidth, measured on this pool's B200s
+        rd = float(json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))["read_gbs"])
+        roof.update(read_peak=rd, frac_of_read_peak=roof["achieved"] / rd,
+                    read_peak_source="profiles/r01_fp64_peaks.json read_gbs (tools/fp64_peak.cu read_stream; "
+                                     "MEASURED_PEAKS.json hbm_gbs is a copy: half reads, half writes)")
+    except (OSError, KeyError, ValueError):
+        pass
     if k >= 8 and args.dtype == "c128":
         # many right-hand sides: the transfer levels are FP64 tensor-core (DMMA) bound
         # (SURVEY.md §8(d)); algorithmic flops (8 per complex multiply-add) per launch
