@@ -594,7 +594,7 @@ __global__ void k_cgs2(MidArgs a, int which) {
 // column is read 4 times per panel.
 constexpr int kPanelMax = 8;
 
-__global__ void __launch_bounds__(512) k_bcgs2(MidArgs a, int which, int pw) {
+__global__ void __launch_bounds__(1024) k_bcgs2(MidArgs a, int which, int pw) {
   extern __shared__ double2 pan[];  // pw columns of length side
   __shared__ double2 coef[kSetCap][kPanelMax];
   __shared__ double red[2 * 32];
@@ -1429,7 +1429,7 @@ void launch_basis(const MidArgs& a, uint32_t nblocks, int which, cudaStream_t st
   if (getenv("BF_CGS2")) pw = 0;
   if (pw >= 2) {
     allow_max_dyn_smem(k_bcgs2);
-    k_bcgs2<<<nblocks, 512, static_cast<size_t>(pw) * col_bytes, st>>>(a, which, pw);
+    k_bcgs2<<<nblocks, 1024, static_cast<size_t>(pw) * col_bytes, st>>>(a, which, pw);
   } else {
     k_cgs2<<<nblocks, 512, 0, st>>>(a, which);
   }
