@@ -746,7 +746,7 @@ __device__ __forceinline__ SmallBufs small_bufs(const MidArgs& a, double2* smem)
 // mid = pinv(qc[rows, :tc]) @ K(rows, cols) @ pinv(qr[cols, :tr]^H); SVD(mid)
 // (lowrank.py:257, 284-293). Results: U_M (tc x s), V_M (tr x s), sigma, and the
 // kept rank t = min(r, s) in the block state.
-__global__ void k_mid(MidArgs a) {
+__global__ void __launch_bounds__(768) k_mid(MidArgs a) {
   extern __shared__ double2 sm2[];
   __shared__ int flag, perm[kSetCap];
   __shared__ double ssc[kSetCap], sg[kSetCap];
@@ -1577,7 +1577,7 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
       k_fill_tall<<<dim3(nblocks, yfill), T, 0, st>>>(a, which, 1, which == kCols ? a.qc : a.qr);
       launch_basis(a, nblocks, which, st);
     }
-    k_mid<<<nblocks, T, small_smem, st>>>(a);
+    k_mid<<<nblocks, 768, small_smem, st>>>(a);  // 24 warps: a 48-column Jacobi round in one pass
   }
   const unsigned yas = static_cast<unsigned>(std::min<uint64_t>(32, (side * rank + T - 1) / T));
   k_assemble<<<dim3(nblocks, yas), T, 0, st>>>(a);
