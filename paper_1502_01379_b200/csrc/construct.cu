@@ -1289,7 +1289,7 @@ __global__ void k_recurse_tsqr(RecArgs a) {
 // (R from k_recurse_tsqr when the stack is at most 32 wide, else a TSQR / Householder
 // pass here).
 template <bool TALL>
-__global__ void __launch_bounds__(256, 2) k_recurse_split(RecArgs a) {
+__global__ void __launch_bounds__(TALL ? 256 : 512, 2) k_recurse_split(RecArgs a) {
   extern __shared__ double2 sm2[];
   __shared__ int flag, perm[kSetCap];
   __shared__ double ssc[kSetCap], sg[kSetCap], red[32];
@@ -1705,7 +1705,7 @@ int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t ro
       a.p0 = p0;
       const int64_t cnt = std::min<int64_t>(chunk, nprob - p0);
       if (reg_tsqr) k_recurse_tsqr<<<static_cast<unsigned>(cnt), 256, tsqr_smem, st>>>(a);
-      kern<<<static_cast<unsigned>(cnt), 256, smem, st>>>(a);
+      kern<<<static_cast<unsigned>(cnt), tall ? 256 : 512, smem, st>>>(a);  // short stacks: 16 warps, one pass per Jacobi round
     }
   } else {
     const int64_t nprob = static_cast<int64_t>(nb) * pairs;
