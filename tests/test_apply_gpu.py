@@ -148,6 +148,7 @@ def test_per_factor_parity(case):
     (1 << 12, 1, 4, 96),      # fused pairs, odd number of splitting levels per half
     (1 << 14, 16, 16, 64),    # r=16, 64 RHS (pairs do not fit a stage: single levels)
     (1 << 12, 16, 16, 70),    # same, k not a multiple of the DMMA tiles
+    (1 << 12, 16, 16, 256),   # 256 RHS: complex64 in-place FFMA tiles, complex128 two-CTA DMMA
 ])
 def test_synthetic_geometries(n, leaf, r, k):
     p = bf.make_partition(n, leaf)
