@@ -96,6 +96,16 @@ int env_int(const char* name, int dflt) {
   return e && *e ? atoi(e) : dflt;
 }
 
+// Tuning / diagnostic switches read once per process (no getenv on the launch path).
+struct EnvKnobs {
+  int mrhs_stages, mrhs_stage_kb, dbg_nomath, dbg_noload, dtile;
+};
+const EnvKnobs& knobs() {
+  static const EnvKnobs k{env_int("BF_MRHS_STAGES", 0), env_int("BF_MRHS_STAGE_KB", 0), env_int("BF_DBG_NOMATH", 0),
+                          env_int("BF_DBG_NOLOAD", 0), env_int("BF_DTILE", -1)};
+  return k;
+}
+
 // Many-RHS pipeline shape: depth (<= 8) and stage budget are launch arguments of the
 // STAGES = 0 instantiation (BF_MRHS_STAGES, BF_MRHS_STAGE_KB override them).
 StreamExp stream_exp() {
@@ -133,7 +143,7 @@ Shape mrhs_shape() {
 template <typename E>
 Shape mrhs_shape_for(uint32_t C) {
   Shape s = mrhs_shape();
-  if (sizeof(E) == 16 && C > 64 && env_int("BF_MRHS_STAGES", 0) == 0 && env_int("BF_MRHS_STAGE_KB", 0) == 0) {
+  if (sizeof(E) == 16 && C > 64 && knobs().mrhs_stages == 0 && knobs().mrhs_stage_kb == 0) {
     s.stages = 1;
     s.stage_bytes = 200 * 1024;
   }
@@ -268,7 +278,7 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
                (static_cast<uint64_t>(nt) * R * C + (adjoint ? static_cast<uint64_t>(nt) * R : C) * 16) * 16 <=
                    48 * 1024) {
       sh.ncw = 4;
-      if (env_int("BF_MRHS_STAGE_KB", 0) == 0) sh.stage_bytes = 48 * 1024;
+      if (knobs().mrhs_stage_kb == 0) sh.stage_bytes = 48 * 1024;
     } else {
       sh.ncw = 8;
     }
@@ -365,15 +375,15 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   }
   const int stages = sh.stages;
   a.stages = static_cast<uint32_t>(stages);
-  a.dbg_nomath = env_int("BF_DBG_NOMATH", 0);
-  a.dbg_noload = mrhs ? env_int("BF_DBG_NOLOAD", 0) : 0;
+  a.dbg_nomath = knobs().dbg_nomath;
+  a.dbg_noload = mrhs ? knobs().dbg_noload : 0;
   if (a.use_dmma) {  // warp tile: the largest that still gives every consumer warp an item
     const uint64_t ncw = (a.use_dmma == 2 && remap < 3) ? sh.ncw : kMrhs.ncw;
     auto di = [&](uint64_t mt, uint64_t n8) {
       return U * ((m_out + 8 * mt - 1) / (8 * mt)) * ((a.kt + 8 * n8 - 1) / (8 * n8));
     };
     a.dtile = a.kt >= 32 && di(2, 4) >= ncw ? 0 : (di(2, 2) >= ncw || a.kt < 16) ? 1 : 2;
-    const int forced = env_int("BF_DTILE", -1);
+    const int forced = knobs().dtile;
     if (forced >= 0 && forced <= 2) a.dtile = static_cast<uint32_t>(forced);
   }
   const size_t smem = 128 + static_cast<size_t>(stages) * a.stage_elems * esz;
