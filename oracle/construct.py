@@ -170,3 +170,27 @@ def factorize(entry, n: int, levels: int, r: int, params=Params(), seed=0, branc
 def chain_shapes(n: int, levels: int, r: int):
     """Alias of the level geometry used for preallocation (construct.py:216-227)."""
     return level_geometry(n, levels, r)
+
+
+def synthetic_slab(side, m, r, seed):
+    """(1, side, m, r) complex Gaussian slab with a spread of column scales."""
+    rng = np.random.default_rng(seed)
+    slab = rng.standard_normal((1, side, m, r)) + 1j * rng.standard_normal((1, side, m, r))
+    slab *= np.logspace(0, -6, r)[None, None, None, :]
+    return slab
+
+
+def slab_chain_apply(leaf_b, pieces, x):
+    """U^L G^{L-1} .. G^h x for one slab's recursion output (x: (m r, k))."""
+    w = x
+    for lvl, b in pieces:                      # ascending h .. L-1: the G side order
+        if b.ndim == 5:
+            gn, _, pp, rr, c2 = b.shape
+            wv = w.reshape(gn, pp, c2, -1)
+            w = np.einsum("gtprc,gpck->gtprk", b, wv).reshape(-1, x.shape[1])
+        else:
+            gn, pp, rr, c2 = b.shape
+            wv = w.reshape(gn, pp, c2, -1)
+            w = np.einsum("gprc,gpck->gprk", b, wv).reshape(-1, x.shape[1])
+    nb, rows, rr = leaf_b.shape
+    return np.einsum("bir,brk->bik", leaf_b, w.reshape(nb, rr, -1)).reshape(nb * rows, -1)

@@ -128,3 +128,30 @@ class Radon2DOracle:
 
     def block(self, rows, cols):
         return radon2d_block(self.n_side, rows, cols)
+
+
+def _splitmix(x):
+    x = (x + np.uint64(0x9E3779B97F4A7C15)) & np.uint64(0xFFFFFFFFFFFFFFFF)
+    x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+class NoisyOracle:
+    """K(i, j) * (1 + amp * u(i, j)), u in [-1, 1) a fixed hash of (i, j, key). Running a
+    construction on it measures that construction's own sensitivity to entry rounding:
+    the calibrated envelope of SURVEY.md §8(c) stage 4."""
+
+    def __init__(self, base, amp, key):
+        self.base, self.amp, self.key = base, amp, np.uint64(key)
+        self.shape = base.shape
+        self.n = base.shape[1]
+
+    def block(self, rows, cols):
+        a = self.base.block(rows, cols)
+        i = np.asarray(rows, dtype=np.uint64)[:, None]
+        j = np.asarray(cols, dtype=np.uint64)[None, :]
+        with np.errstate(over="ignore"):
+            h = _splitmix(i * np.uint64(self.n) + j + self.key * np.uint64(0x632BE59BD9B4E019))
+        u = (h >> np.uint64(11)).astype(np.float64) * (2.0 ** -52) - 1.0
+        return a * (1.0 + self.amp * u)

@@ -18,6 +18,9 @@ import sys
 import numpy as np
 
 REF = "/root/reference/pkg/src"
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+from oracle.construct import slab_chain_apply, synthetic_slab  # noqa: E402
+from oracle.entries import NoisyOracle  # noqa: E402
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
 
 
@@ -222,9 +225,122 @@ def gen_hankel(bf):
     print("hankel.npz eps", d["eps_r4"], d["eps_r6"])
 
 
+def _trace_block(bf, oracle, p, r, seed, i, j):
+    """_sample_block with every select_pivot_columns call recorded (pick order)."""
+    import butterfly.lowrank as lr
+    from butterfly.construct import _sample_block
+    calls = []
+    orig = lr.select_pivot_columns
+
+    def rec(a, k, rel_tol=0.0):
+        out = orig(a, k, rel_tol)
+        calls.append(list(out))
+        return out
+
+    lr.select_pivot_columns = rec
+    try:
+        apx = _sample_block(oracle, p, r, bf.lowrank.DEFAULT_PARAMS, seed, i, j)
+    finally:
+        lr.select_pivot_columns = orig
+    return apx, calls
+
+
+def gen_config_traces(bf, name, oracle, n, leaf, r, seed, nblocks, amp=1e-15, npert=2):
+    """Middle blocks of a BASELINE config's own geometry, traced on the reference:
+    a phase-invariant signature u0 diag(s0) v0^H X of each block on two fixed probe
+    columns X, the singular values, the final skeleton sets and basis pivots, and the
+    reference's own deviation d_ref under 1e-15 entry noise (npert hashed
+    perturbations) — the calibrated envelope of SURVEY.md §8(c) stage 4."""
+    import time
+    p = bf.make_partition(n, leaf)
+    m, side = p.mid_nodes, p.mid_side
+    rng = np.random.default_rng(1234 + n)
+    if nblocks >= m * m:
+        blocks = [(i, j) for i in range(m) for j in range(m)]
+    else:
+        picks = {(0, 0), (m - 1, m - 1), (m // 2, m // 2), (0, m - 1)}
+        while len(picks) < nblocks:
+            picks.add((int(rng.integers(m)), int(rng.integers(m))))
+        blocks = sorted(picks)
+    x = bf.lowrank.complex_normal(np.random.default_rng(99), (side, 2))
+    d = {"n": n, "levels": p.levels, "rank": r, "seed": seed, "amp": amp, "probe": x,
+         "blocks": np.array(blocks, dtype=np.int64)}
+    t0 = time.time()
+    for (i, j) in blocks:
+        apx, calls = _trace_block(bf, oracle, p, r, seed, i, j)
+        sig = apx.u0 @ (apx.sigma0[:, None] * (apx.v0.conj().T @ x))
+        key = f"b{i}_{j}"
+        d[key + "_sig"] = sig
+        d[key + "_s0"] = apx.sigma0
+        if len(calls) == 8:   # sampling branch: 3 sweeps x 2, then the two basis calls
+            d[key + "_skc"] = np.array(sorted(calls[4]), dtype=np.int64)
+            d[key + "_skr"] = np.array(sorted(calls[5]), dtype=np.int64)
+            d[key + "_pivc"] = np.array(calls[6], dtype=np.int64)
+            d[key + "_pivr"] = np.array(calls[7], dtype=np.int64)
+        dref = []
+        for q in range(npert):
+            apx_q, calls_q = _trace_block(bf, NoisyOracle(oracle, amp, q + 1), p, r, seed, i, j)
+            sig_q = apx_q.u0 @ (apx_q.sigma0[:, None] * (apx_q.v0.conj().T @ x))
+            dref.append(np.linalg.norm(sig_q - sig) / max(np.linalg.norm(sig), 1e-300))
+            if q == 0:
+                d[key + "_flips"] = np.int64(sum(a != b for a, b in zip(calls, calls_q)))
+        d[key + "_dref"] = np.array(dref)
+    np.savez_compressed(os.path.join(OUT, name), **d)
+    drefs = np.array([d[f"b{i}_{j}_dref"].max() for i, j in blocks])
+    print(name, "blocks", len(blocks), "side", side, "d_ref median %.2e max %.2e" % (np.median(drefs), drefs.max()),
+          "%.1f s" % (time.time() - t0))
+
+
+def gen_slab(bf, name, n, leaf, r, seed):
+    """The reference's _recurse on one seeded synthetic slab (1, side, m, r) at a config's
+    geometry: chain signatures U^L G^{L-1}..G^h X on fixed probes (phase-invariant) and
+    the leaf block norms. The slab is regenerated at test time from the same seed."""
+    from butterfly.construct import _recurse
+    p = bf.make_partition(n, leaf)
+    m, side = p.mid_nodes, p.mid_side
+    slab = synthetic_slab(side, m, r, seed)
+    leaf_b, pieces = _recurse(slab, p, r)
+    x = bf.lowrank.complex_normal(np.random.default_rng(seed + 1), (m * r, 2))
+    sig = slab_chain_apply(leaf_b, pieces, x)
+    d = {"n": n, "levels": p.levels, "rank": r, "seed": seed, "probe": x, "sig": sig,
+         "direct": slab.reshape(side, m * r) @ x}
+    np.savez_compressed(os.path.join(OUT, name), **d)
+    print(name, "chain vs slab rel", np.linalg.norm(sig - d["direct"]) / np.linalg.norm(d["direct"]))
+
+
+def gen_eps(bf, name, oracle, n, leaf, r, seed):
+    """eps_a of the reference's full factorize (bench.py:90-97, seeded as _run_row)."""
+    import time
+    p = bf.make_partition(n, leaf)
+    t0 = time.time()
+    f = bf.factorize(oracle, p, r, seed=seed)
+    t_fac = time.time() - t0
+    eps = bf.bench.estimate_eps_a(f, bf.bench.RowSampledReference(oracle), 256,
+                                  np.random.SeedSequence(seed, spawn_key=(4, 0)))
+    np.savez_compressed(os.path.join(OUT, name), n=n, levels=p.levels, rank=r, seed=seed, eps_a=eps,
+                        factorize_s=t_fac)
+    print(name, "eps_a", eps, "factorize %.1f s" % t_fac)
+
+
+def gen_configs(bf):
+    gen_config_traces(bf, "trace_cfg0_fio_n1024_r12_leaf8.npz", bf.FioKernel(1024), 1024, 8, 12, 0, 64)
+    gen_config_traces(bf, "trace_fio_n4096_r8_leaf4.npz", bf.FioKernel(4096), 4096, 4, 8, 0, 24)
+    gen_config_traces(bf, "trace_cfg1_dftp_n65536_r8_leaf16.npz", DftPlus(1 << 16), 1 << 16, 16, 8, 0, 24)
+    gen_config_traces(bf, "trace_cfg2_fio_n1048576_r16_leaf16.npz", bf.FioKernel(1 << 20), 1 << 20, 16, 16, 0, 12)
+    gen_slab(bf, "slab_cfg2_n1048576_r16_leaf16.npz", 1 << 20, 16, 16, 5)
+    gen_eps(bf, "eps_fio_n4096_r12_leaf1.npz", bf.FioKernel(4096), 4096, 1, 12, 0)
+    gen_eps(bf, "eps_dftp_n4096_r8_leaf1.npz", DftPlus(4096), 4096, 1, 8, 0)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     bf = _ref()
+    if len(sys.argv) > 1 and sys.argv[1] == "configs":
+        gen_configs(bf)
+        return
+    if len(sys.argv) > 1 and sys.argv[1] == "cfg1eps":   # ~15 min: the reference's full cfg1 factorize
+        gen_eps(bf, "eps_cfg1_dftp_n65536_r8_leaf16.npz", DftPlus(1 << 16), 1 << 16, 16, 8, 0)
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "matvec":
         gen_matvec(bf)
         return

@@ -136,8 +136,18 @@ class MiddleSampler:
             self._all_draws = draw_tables(self.seed, self.side, self.r, self.params,
                                           [(i, j) for i in rows for j in range(m)])
 
-    def blocks(self, ij):
-        """(u0*sigma0, v0*sigma0, floored_inverse(sigma0)) for blocks ij, on the device."""
+    # BlockState of construct.cu (int64 r0, c0; 8 int32 counters; six int32[128] index sets)
+    _STATE = np.dtype([("r0", "<i8"), ("c0", "<i8"), ("nrows", "<i4"), ("ncols", "<i4"), ("nskr", "<i4"),
+                       ("nskc", "<i4"), ("tc", "<i4"), ("tr", "<i4"), ("t", "<i4"), ("pad", "<i4"),
+                       ("rows", "<i4", 128), ("cols", "<i4", 128), ("skr", "<i4", 128), ("skc", "<i4", 128),
+                       ("pivc", "<i4", 128), ("pivr", "<i4", 128)])
+
+    def blocks(self, ij, trace=False):
+        """(u0*sigma0, v0*sigma0, floored_inverse(sigma0)) for blocks ij, on the device.
+
+        trace=True also returns, per block, the index sets the sampling SVD ended with
+        (lowrank.py:238-256): the last sweep's sorted skeletons Pi_col / Pi_row, the
+        least-squares row/column sets and the two basis pivot lists in pick order."""
         torch = self.torch
         ij = np.asarray(ij, dtype=np.int32).reshape(-1, 2)
         nb = ij.shape[0]
@@ -169,7 +179,18 @@ class MiddleSampler:
             if rc == _lib.BF_EINVAL:
                 raise ValueError(msg)
             raise _lib.OracleError(f"entry oracle failed on middle blocks {ij[:1].tolist()}...: {msg}")
-        return u, v, w
+        if not trace:
+            return u, v, w
+        raw = ws[:nb * self._STATE.itemsize].cpu().numpy().view(self._STATE)
+        tr = []
+        for st in raw:
+            if st["tc"] < 0:        # dense branch: no pivots
+                tr.append({})
+                continue
+            tr.append({"skc": st["skc"][:st["nskc"]].tolist(), "skr": st["skr"][:st["nskr"]].tolist(),
+                       "rows": st["rows"][:st["nrows"]].tolist(), "cols": st["cols"][:st["ncols"]].tolist(),
+                       "pivc": st["pivc"][:st["tc"]].tolist(), "pivr": st["pivr"][:st["tr"]].tolist()})
+        return u, v, w, tr
 
     def batch_rows(self) -> int:
         """Block-rows per launch: enough CTAs to fill the GPU, bounded workspace."""

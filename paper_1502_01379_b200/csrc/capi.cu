@@ -252,6 +252,13 @@ uint64_t bf_apply_workspace_bytes(const bf_plan* plan, uint32_t k) {
   return 2ull * plan->p.dim_max * (k ? k : 1) * plan->p.elem();
 }
 
+// Destroys every cached graph of the plan (caller holds gmu and has synchronised the
+// streams the graphs ran on).
+static void drop_graphs_locked(const bf_plan* plan) {
+  for (auto& gentry : plan->graphs) cudaGraphExecDestroy(gentry.exec);
+  plan->graphs.clear();
+}
+
 // The chain is a fixed sequence of 2 + 2(L-h) launches: replay it as one CUDA
 // graph per (buffers, k, direction, stream). A NULL stream is the legacy default
 // stream, which cannot be captured; the graph then runs on a plan-owned blocking
@@ -474,6 +481,9 @@ int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint
   const uint64_t need_ws = pipelined ? 2 * mid_bytes + 2 * (p.dim_max / chunks) * k * p.elem() : wsb;
   if (plan->host_io_bytes < io || plan->host_ws_bytes < need_ws) {
     BF_CUDA(cudaStreamSynchronize(run));
+    // every cached graph that captured the old device buffers would replay against freed
+    // memory (a k=1 graph found again after a k=4 call grew them): drop them all
+    drop_graphs_locked(plan);
     if (plan->host_in) cudaFree(plan->host_in);
     if (plan->host_out) cudaFree(plan->host_out);
     if (plan->host_ws) cudaFree(plan->host_ws);
@@ -487,7 +497,10 @@ int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint
   }
   if (pipelined) {
     if (!plan->copy_stream) BF_CUDA(cudaStreamCreateWithFlags(&plan->copy_stream, cudaStreamNonBlocking));
-    if (plan->pipe_events.empty()) {
+    if (plan->pipe_events.size() < 2 * chunks + 2) {  // BF_PIPE_CHUNKS is re-read on every call
+      BF_CUDA(cudaStreamSynchronize(run));
+      drop_graphs_locked(plan);  // captured graphs reference the old events
+      for (auto e : plan->pipe_events) cudaEventDestroy(e);
       plan->pipe_events.assign(2 * chunks + 2, nullptr);
       for (auto& e : plan->pipe_events) BF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }

@@ -38,6 +38,9 @@ struct BlockState {
   int32_t pivc[kSetCap], pivr[kSetCap];
 };
 
+// construct.py MiddleSampler._STATE decodes this layout for the staged-parity traces
+static_assert(sizeof(BlockState) == 3120, "BlockState layout is mirrored on the host");
+
 struct MidArgs {
   EntrySrc src;
   int64_t side;

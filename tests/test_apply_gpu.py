@@ -308,6 +308,24 @@ def test_pinned_host_pipeline_bitwise(n, leaf, r, k):
             assert np.array_equal(host, dev)
 
 
+def test_pinned_host_pipeline_regrow():
+    """k=1 -> k=4 -> k=1 on the same pinned buffers: the k=4 call grows the plan's device
+    buffers, so the k=1 graph cached before it must not be replayed against the freed ones."""
+    p = bf.make_partition(1 << 18, 16)
+    f = synthetic_chain(p, 16, seed=3, device="cuda")
+    pl = f.plan()
+    g4 = torch.from_numpy(complex_gaussian(np.random.default_rng(5), (p.n, 4))).pin_memory()
+    o4 = torch.empty_like(g4).pin_memory()
+    g1 = g4[:, :1].contiguous().pin_memory()
+    o1 = torch.empty_like(g1).pin_memory()
+    want1 = pl.apply(g1.cuda()).cpu().numpy()
+    want4 = pl.apply(g4.cuda()).cpu().numpy()
+    for _ in range(2):
+        assert np.array_equal(pl.apply(g1.numpy(), out=o1.numpy()), want1)
+        assert np.array_equal(pl.apply(g4.numpy(), out=o4.numpy()), want4)
+        assert np.array_equal(pl.apply(g1.numpy(), out=o1.numpy()), want1)
+
+
 @pytest.mark.parametrize("n,levels,r,k", [
     (4, 2, 1, 1),       # smallest partition: m = 2, side = 2
     (4, 2, 2, 3),

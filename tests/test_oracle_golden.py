@@ -117,3 +117,50 @@ def test_oracle_factorize_operator_cfg0():
     c = ocons.factorize(oent.EntryOracle("fio", n), n, levels, r, seed=seed)
     assert np.array_equal(c.weights, d["weights"])
     assert rel(ochain.apply(c, d["g"]), d["fwd"]) <= 1e-13
+
+
+@pytest.mark.parametrize("name,count", [
+    ("trace_cfg0_fio_n1024_r12_leaf8.npz", 64),
+    ("trace_fio_n4096_r8_leaf4.npz", 8),
+    ("trace_cfg1_dftp_n65536_r8_leaf16.npz", 4),
+    ("trace_cfg2_fio_n1048576_r16_leaf16.npz", 2),
+])
+def test_oracle_blocks_bitwise_at_config_geometry(name, count):
+    """The oracle's sample_block reproduces the reference's traced middle blocks at the
+    configs' own geometry bit for bit: signature u0 diag(s0) v0^H X, singular values,
+    final skeleton sets and basis pivots."""
+    from threadpoolctl import threadpool_limits
+    d = golden(name)
+    n, levels, r, seed = int(d["n"]), int(d["levels"]), int(d["rank"]), int(d["seed"])
+    ent = oent.EntryOracle("dftp" if "dftp" in name else "fio", n)
+    x = d["probe"]
+    # the fixtures were made with one BLAS thread: LAPACK's SVDs are not bitwise
+    # reproducible across thread counts (1e-14 differences at 2 vs 8 threads)
+    with threadpool_limits(1):
+        _check_blocks(d, ent, n, levels, r, seed, x, count)
+
+
+def _check_blocks(d, ent, n, levels, r, seed, x, count):
+    for b in d["blocks"][:count]:
+        i, j = int(b[0]), int(b[1])
+        key = f"b{i}_{j}"
+        tr = {}
+        t = ocons.sample_block(ent, n, levels, r, olr.Params(), seed, i, j, trace=tr)
+        sig = t.u0 @ (t.sigma0[:, None] * (t.v0.conj().T @ x))
+        assert np.array_equal(sig, d[key + "_sig"]), key
+        assert np.array_equal(t.sigma0, d[key + "_s0"]), key
+        if key + "_skc" in d:
+            assert tr["sk_col"][-1].tolist() == d[key + "_skc"].tolist()
+            assert tr["sk_row"][-1].tolist() == d[key + "_skr"].tolist()
+
+
+def test_oracle_recurse_cfg2_slab_bitwise():
+    """oracle recurse == reference _recurse on a seeded cfg2-geometry slab (1, 4096, 256, 16)."""
+    from threadpoolctl import threadpool_limits
+    d = golden("slab_cfg2_n1048576_r16_leaf16.npz")
+    n, levels, r, seed = int(d["n"]), int(d["levels"]), int(d["rank"]), int(d["seed"])
+    m = 2 ** (levels // 2)
+    slab = ocons.synthetic_slab(n // m, m, r, seed)
+    with threadpool_limits(1):
+        leaf, pieces = ocons.recurse(slab, n, levels, r)
+    assert np.array_equal(ocons.slab_chain_apply(leaf, pieces, d["probe"]), d["sig"])
