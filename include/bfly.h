@@ -172,6 +172,12 @@ int bf_plan_export(const bf_plan* plan, int which, uint32_t level, void* dst, ui
 int bf_entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr,
                const int64_t* cols, uint32_t nc, void* out, void* stream);
 
+/* The per-N table of row-only transcendental terms the FIO and 2-D Radon entries read:
+ * FIO c(x_i) = (2 + sin 2 pi x_i)/8 for i < n (n doubles); 2-D sin and cos of 2 pi a/n_side
+ * for a < n_side (2 n_side doubles: sines then cosines). Sines are correctly rounded
+ * (double-double), hence equal to the reference's NumPy values. out: device, len doubles. */
+int bf_entry_table(int kernel_id, uint64_t n, double* out, uint64_t len, void* stream);
+
 /* Hankel-kernel rows (HankelKernel, kernels.py:45-84; hankel1_orders,
  * bessel.py:178-230): out[t, m] = H1_m(x[t]) = J_m + i Y_m for m = 0..max_order,
  * complex128 rows of stride ld. x: device float64 (nx), all > 0. start: the

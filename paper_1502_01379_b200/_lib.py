@@ -57,6 +57,7 @@ SIGNATURES = [
     ("bf_plan_save_bfac", _I, [_P, ctypes.c_char_p]),
     ("bf_plan_export", _I, [_P, _I, _U32, _P, _U64, _P]),
     ("bf_entries", _I, [_I, _U64, _P, _U32, _P, _U32, _P, _P]),
+    ("bf_entry_table", _I, [_I, _U64, _P, _U64, _P]),
     ("bf_hankel_orders", _I, [_P, _U32, _U32, ctypes.c_int64, _P, _U64, _P]),
 ]
 

@@ -1532,6 +1532,11 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
   a.src.kind = kernel_id;
   a.src.n = n;
   a.src.dense = static_cast<const double2*>(dense);
+  a.src.tab = nullptr;
+  if (kernel_id == BF_KERNEL_FIO || kernel_id == BF_KERNEL_RADON2D) {
+    a.src.tab = row_table(kernel_id, n, static_cast<cudaStream_t>(stream));
+    if (!a.src.tab) return BF_ECUDA;
+  }
   a.side = static_cast<int64_t>(side);
   a.r = static_cast<int>(rank);
   a.rqs = static_cast<int>(rqs);

@@ -5,9 +5,14 @@
 // c(x) = (2 + sin(2 pi x))/8, value exp(2 pi i Phi). The reference evaluates
 // in NumPy with one rounding per operation and no fused multiply-add; every
 // product/sum here uses the _rn intrinsics so nvcc cannot contract them
-// (contraction changes ~22% of phases). Only the final
-// sin/cos may differ from glibc by an ulp or two.
+// (contraction changes ~22% of phases). The row-only term
+// c(x_i) comes from a per-N table of correctly rounded sines (crmath.cuh), equal to
+// NumPy's; only the final sin/cos of the phase may differ from glibc by an ulp.
 // DFTP (BASELINE config 1): exp(+2 pi i (j k mod N)/N), phase exact in int64.
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "common.cuh"
 #include "entry_eval.cuh"
 #include "plan.h"
@@ -16,13 +21,26 @@ namespace bfly {
 
 namespace {
 
-__global__ void entries_kernel(int kind, uint64_t n, const int64_t* __restrict__ rows, uint32_t nr,
+__global__ void entries_kernel(EntrySrc src, const int64_t* __restrict__ rows, uint32_t nr,
                                const int64_t* __restrict__ cols, uint32_t nc, double2* __restrict__ out) {
   const uint64_t total = static_cast<uint64_t>(nr) * nc;
   for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total;
-       x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = rows[x / nc], j = cols[x % nc];
-    out[x] = kind == BF_KERNEL_FIO ? fio_entry(n, i, j) : kind == BF_KERNEL_DFTP ? dftp_entry(n, i, j) : radon2d_entry(n, i, j);
+       x += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[x] = entry_eval(src, rows[x / nc], cols[x % nc]);
+}
+
+__global__ void fio_table_kernel(uint64_t n, double* __restrict__ tab) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    tab[i] = fio_speed(n, i);
+}
+
+__global__ void radon_table_kernel(uint32_t ns, double* __restrict__ tab) {
+  for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < ns; a += gridDim.x * blockDim.x) {
+    double s, c;
+    cr::sincos_cr(__dmul_rn(kTwoPi, __ddiv_rn(static_cast<double>(a), static_cast<double>(ns))), &s, &c);
+    tab[a] = s;
+    tab[ns + a] = c;
   }
 }
 
@@ -47,12 +65,62 @@ unsigned grid_for(uint64_t total) {
 
 }  // namespace
 
+uint64_t row_table_len(int kind, uint64_t n) {
+  if (kind == BF_KERNEL_FIO) return n;
+  if (kind == BF_KERNEL_RADON2D) return 2ull << ((63 - __builtin_clzll(n)) / 2);
+  return 0;
+}
+
+const double* row_table(int kind, uint64_t n, cudaStream_t st) {
+  const uint64_t len = row_table_len(kind, n);
+  if (!len) return nullptr;
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, uint64_t>, double*> cache;  // kept for the process
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cuda_fail(cudaGetLastError(), "cudaGetDevice");
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(dev, kind, n);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  double* tab = nullptr;
+  cudaError_t e = cudaMalloc(&tab, len * sizeof(double));
+  if (e != cudaSuccess) {
+    cuda_fail(e, "cudaMalloc (entry row table)");
+    return nullptr;
+  }
+  // built on its own stream and completed before it is published: any stream may read it
+  cudaStream_t ts = nullptr;
+  e = cudaStreamCreateWithFlags(&ts, cudaStreamNonBlocking);
+  if (e == cudaSuccess) {
+    if (kind == BF_KERNEL_FIO)
+      fio_table_kernel<<<grid_for(n), 256, 0, ts>>>(n, tab);
+    else
+      radon_table_kernel<<<grid_for(len / 2), 256, 0, ts>>>(static_cast<uint32_t>(len / 2), tab);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ts);
+    cudaStreamDestroy(ts);
+  }
+  (void)st;
+  if (e != cudaSuccess) {
+    cudaFree(tab);
+    cuda_fail(e, "entry row table");
+    return nullptr;
+  }
+  cache.emplace(key, tab);
+  return tab;
+}
+
 int entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr, const int64_t* cols, uint32_t nc, void* out,
             cudaStream_t st) {
   if (kernel_id != BF_KERNEL_FIO && kernel_id != BF_KERNEL_DFTP && kernel_id != BF_KERNEL_RADON2D)
     return fail(BF_EINVAL, "unknown entry kernel id");
   if (static_cast<uint64_t>(nr) * nc == 0) return 0;
-  entries_kernel<<<grid_for(static_cast<uint64_t>(nr) * nc), 256, 0, st>>>(kernel_id, n, rows, nr, cols, nc,
+  EntrySrc src{kernel_id, n, nullptr, nullptr};
+  if (row_table_len(kernel_id, n) && !(src.tab = row_table(kernel_id, n, st))) return BF_ECUDA;
+  entries_kernel<<<grid_for(static_cast<uint64_t>(nr) * nc), 256, 0, st>>>(src, rows, nr, cols, nc,
                                                                           static_cast<double2*>(out));
   BF_CUDA(cudaGetLastError());
   return 0;
@@ -141,7 +209,8 @@ int sampled_rows(int kernel_id, uint64_t n, const void* dense, const int64_t* ro
   const uint32_t nchunks = static_cast<uint32_t>((n + chunk - 1) / chunk);
   const uint64_t need = 16ull * nchunks * nr * k;
   if (ws_bytes < need) return fail(BF_EINVAL, "sampled-rows workspace too small");
-  EntrySrc src{kernel_id, n, static_cast<const double2*>(dense)};
+  EntrySrc src{kernel_id, n, static_cast<const double2*>(dense), nullptr};
+  if (row_table_len(kernel_id, n) && !(src.tab = row_table(kernel_id, n, st))) return BF_ECUDA;
   sampled_rows_kernel<<<dim3(nr, nchunks), 256, 0, st>>>(src, rows, nr, static_cast<const double2*>(g), k, chunk,
                                                          static_cast<double2*>(workspace));
   const uint64_t per = static_cast<uint64_t>(nr) * k;
@@ -157,3 +226,15 @@ uint64_t sampled_rows_workspace(uint64_t n, uint32_t nr, uint32_t k) {
 }
 
 }  // namespace bfly
+
+extern "C" int bf_entry_table(int kernel_id, uint64_t n, double* out, uint64_t len, void* stream) {
+  using namespace bfly;
+  const uint64_t need = row_table_len(kernel_id, n);
+  if (!need) return fail(BF_EINVAL, "kernel has no row table (FIO and 2-D Radon only)");
+  if (!out || len < need) return fail(BF_EINVAL, "output shorter than the table");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const double* tab = row_table(kernel_id, n, st);
+  if (!tab) return BF_ECUDA;
+  BF_CUDA(cudaMemcpyAsync(out, tab, need * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  return BF_OK;
+}

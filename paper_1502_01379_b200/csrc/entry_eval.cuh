@@ -4,20 +4,29 @@
 
 #include "common.cuh"
 #include "../../include/bfly.h"
+#include "crmath.cuh"
 
 namespace bfly {
 
 constexpr double kTwoPi = 6.283185307179586;  // fl(2 * pi), the reference's 2.0 * np.pi
 
-__device__ __forceinline__ double2 fio_entry(uint64_t n, int64_t i, int64_t j) {
+// tab[i] = c(x_i) = (2 + sin(2 pi x_i))/8 with a correctly rounded sine (row_table)
+__device__ __forceinline__ double2 fio_entry(uint64_t n, const double* __restrict__ tab, int64_t i, int64_t j) {
   const double nd = static_cast<double>(n);
   const double x = __ddiv_rn(static_cast<double>(i), nd);
   const double xi = __dsub_rn(static_cast<double>(j), __ddiv_rn(nd, 2.0));
-  const double speed = __ddiv_rn(__dadd_rn(2.0, sin(__dmul_rn(kTwoPi, x))), 8.0);
-  const double phase = __dadd_rn(__dmul_rn(x, xi), __dmul_rn(speed, fabs(xi)));
+  const double phase = __dadd_rn(__dmul_rn(x, xi), __dmul_rn(tab[i], fabs(xi)));
   double s, c;
   sincos(__dmul_rn(kTwoPi, phase), &s, &c);
   return make_double2(c, s);
+}
+
+// the table entry itself: the reference's float64 ops on a correctly rounded sine
+__device__ __forceinline__ double fio_speed(uint64_t n, uint64_t i) {
+  const double x = __ddiv_rn(static_cast<double>(i), static_cast<double>(n));
+  double s, c;
+  cr::sincos_cr(__dmul_rn(kTwoPi, x), &s, &c);
+  return __ddiv_rn(__dadd_rn(2.0, s), 8.0);
 }
 
 __device__ __forceinline__ double2 dftp_entry(uint64_t n, int64_t i, int64_t j) {
@@ -42,18 +51,19 @@ __device__ __forceinline__ void morton_decode(uint64_t z, uint32_t bits, uint32_
   *a2 = y;
 }
 
-__device__ __forceinline__ double2 radon2d_entry(uint64_t n, int64_t i, int64_t j) {
+// tab[a] = sin(t), tab[ns + a] = cos(t), t = fl(2 pi a/ns), correctly rounded (row_table)
+__device__ __forceinline__ double2 radon2d_entry(uint64_t n, const double* __restrict__ tab, int64_t i, int64_t j) {
   const uint32_t bits = (63 - __clzll(static_cast<long long>(n))) / 2;
-  const double ns = static_cast<double>(1u << bits);
+  const uint32_t nsi = 1u << bits;
+  const double ns = static_cast<double>(nsi);
   uint32_t a1, a2, b1, b2;
   morton_decode(static_cast<uint64_t>(i), bits, &a1, &a2);
   morton_decode(static_cast<uint64_t>(j), bits, &b1, &b2);
   const double x1 = __ddiv_rn(static_cast<double>(a1), ns), x2 = __ddiv_rn(static_cast<double>(a2), ns);
   const double half = __ddiv_rn(ns, 2.0);
   const double xi1 = __dsub_rn(static_cast<double>(b1), half), xi2 = __dsub_rn(static_cast<double>(b2), half);
-  const double t1 = __dmul_rn(kTwoPi, x1), t2 = __dmul_rn(kTwoPi, x2);
-  const double c1 = __ddiv_rn(__dadd_rn(2.0, __dmul_rn(sin(t1), sin(t2))), 16.0);
-  const double c2 = __ddiv_rn(__dadd_rn(2.0, __dmul_rn(cos(t1), cos(t2))), 16.0);
+  const double c1 = __ddiv_rn(__dadd_rn(2.0, __dmul_rn(tab[a1], tab[a2])), 16.0);
+  const double c2 = __ddiv_rn(__dadd_rn(2.0, __dmul_rn(tab[nsi + a1], tab[nsi + a2])), 16.0);
   const double q = __dadd_rn(__dmul_rn(__dmul_rn(c1, c1), __dmul_rn(xi1, xi1)),
                              __dmul_rn(__dmul_rn(c2, c2), __dmul_rn(xi2, xi2)));
   const double phase = __dadd_rn(__dadd_rn(__dmul_rn(x1, xi1), __dmul_rn(x2, xi2)), __dsqrt_rn(q));
@@ -68,13 +78,19 @@ struct EntrySrc {
   int kind;             // BF_KERNEL_FIO | BF_KERNEL_DFTP | BF_KERNEL_DENSE | BF_KERNEL_RADON2D
   uint64_t n;
   const double2* dense; // BF_KERNEL_DENSE: n x n row-major
+  const double* tab;    // BF_KERNEL_FIO / BF_KERNEL_RADON2D: row_table(kind, n)
 };
 
 __device__ __forceinline__ double2 entry_eval(const EntrySrc& s, int64_t i, int64_t j) {
-  if (s.kind == BF_KERNEL_FIO) return fio_entry(s.n, i, j);
+  if (s.kind == BF_KERNEL_FIO) return fio_entry(s.n, s.tab, i, j);
   if (s.kind == BF_KERNEL_DFTP) return dftp_entry(s.n, i, j);
-  if (s.kind == BF_KERNEL_RADON2D) return radon2d_entry(s.n, i, j);
+  if (s.kind == BF_KERNEL_RADON2D) return radon2d_entry(s.n, s.tab, i, j);
   return s.dense[static_cast<uint64_t>(i) * s.n + j];
 }
+
+// Host side (entries.cu): the per-N table of the row-only transcendental terms, built on
+// the device once per (device, kind, n) and kept for the process (n doubles for FIO,
+// 2 n_side for the 2-D kernel; NULL with the error set on failure).
+const double* row_table(int kind, uint64_t n, cudaStream_t st);
 
 }  // namespace bfly

@@ -53,6 +53,7 @@ def test_null_plan_is_rejected():
     assert lib.bf_apply(None, None, None, 1, 0, None, 0, None) == _lib.BF_EINVAL
     assert lib.bf_apply_factor(None, 0, 0, 0, None, None, 1, None) == _lib.BF_EINVAL
     assert lib.bf_entries(9, 16, None, 0, None, 0, None, None) == _lib.BF_EINVAL
+    assert lib.bf_entry_table(_lib.BF_KERNEL_DFTP, 16, None, 0, None) == _lib.BF_EINVAL
     assert lib.bf_apply_workspace_bytes(None, 4) == 0
     lib.bf_plan_destroy(None)
 

@@ -276,7 +276,9 @@ def test_radon2d_entries_match_oracle():
     cols = rng.choice(n_side * n_side, 64, replace=False)
     got = ker.block(rows, cols)
     want = oent.radon2d_block(n_side, rows, cols)
-    assert np.max(np.abs(got - want)) <= 2 * np.spacing(2 * np.pi * n_side * 2.0) + 4e-16
+    # c1, c2 from the correctly rounded sin/cos table: the phase is bit-identical to the
+    # oracle's, only the final sin/cos may differ by an ulp or two
+    assert np.max(np.abs(got - want)) <= 4.5e-16
 
 
 @pytest.mark.parametrize("n_side,leaf,r", [(32, 2, 6), (32, 2, 20), (64, 4, 25)])
