@@ -277,14 +277,14 @@ def gen_config_traces(bf, name, oracle, n, leaf, r, seed, nblocks, amp=1e-15, np
             d[key + "_skr"] = np.array(sorted(calls[5]), dtype=np.int64)
             d[key + "_pivc"] = np.array(calls[6], dtype=np.int64)
             d[key + "_pivr"] = np.array(calls[7], dtype=np.int64)
-        dref = []
+        dref, flips = [], []
         for q in range(npert):
             apx_q, calls_q = _trace_block(bf, NoisyOracle(oracle, amp, q + 1), p, r, seed, i, j)
             sig_q = apx_q.u0 @ (apx_q.sigma0[:, None] * (apx_q.v0.conj().T @ x))
             dref.append(np.linalg.norm(sig_q - sig) / max(np.linalg.norm(sig), 1e-300))
-            if q == 0:
-                d[key + "_flips"] = np.int64(sum(a != b for a, b in zip(calls, calls_q)))
+            flips.append([a != b for a, b in zip(calls, calls_q)] + [False] * (8 - len(calls)))
         d[key + "_dref"] = np.array(dref)
+        d[key + "_flips"] = np.array(flips, dtype=bool)   # (npert, 8): which pivot calls moved
     np.savez_compressed(os.path.join(OUT, name), **d)
     drefs = np.array([d[f"b{i}_{j}_dref"].max() for i, j in blocks])
     print(name, "blocks", len(blocks), "side", side, "d_ref median %.2e max %.2e" % (np.median(drefs), drefs.max()),

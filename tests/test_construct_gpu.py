@@ -77,9 +77,12 @@ def _block_product(u, s, v):
 
 
 @pytest.mark.parametrize("name,tol_med,tol_max", [
-    ("construct_fio_n128_r4_leaf025.npz", 1e-13, 1e-12),   # dense branch (r q >= side)
-    ("construct_fio_n1024_r8_leaf1.npz", 1e-9, 1e-6),      # sampling branch, accurate leaf
-    ("construct_fio_n1024_r12_leaf8.npz", 1e-9, 1e-4),     # config 0 geometry
+    ("construct_fio_n128_r4_leaf025.npz", 1e-14, 1e-14),   # dense branch (r q >= side): measured 9e-16
+    ("construct_fio_n1024_r8_leaf1.npz", 1e-12, 1e-11),    # sampling, accurate leaf: measured 2e-13 / 1.7e-12
+    # config 0 geometry: measured 9e-13 / 1.0e-7 / 1.8e-12; the 1e-7 block (2, 5) moves by
+    # 1e-8 in the reference itself under 1e-15 entry noise — per-block envelopes for all 64
+    # cfg0 blocks: test_config_parity_gpu.py::test_config_blocks_vs_reference_traces
+    ("construct_fio_n1024_r12_leaf8.npz", 1e-11, 1e-6),
 ])
 def test_middle_blocks_vs_reference_traces(name, tol_med, tol_max):
     d = golden(name)
@@ -265,7 +268,7 @@ def test_pivots_pairwise_norm_order():
     got = gpu_pivots(np.ascontiguousarray(a), 16, 0.0, pairwise=True)
     matched = sum(1 for x, y in zip(got, want) if x == y)
     print("pairwise-order pivots: %d/16 identical" % matched)
-    assert got[0] == want[0] and matched >= 8
+    assert got == want, f"{matched}/16"   # measured 16/16 (the pairwise norm order restated)
 
 
 def test_radon2d_entries_match_oracle():
@@ -276,9 +279,12 @@ def test_radon2d_entries_match_oracle():
     cols = rng.choice(n_side * n_side, 64, replace=False)
     got = ker.block(rows, cols)
     want = oent.radon2d_block(n_side, rows, cols)
-    # c1, c2 from the correctly rounded sin/cos table: the phase is bit-identical to the
-    # oracle's, only the final sin/cos may differ by an ulp or two
-    assert np.max(np.abs(got - want)) <= 4.5e-16
+    # c1, c2 from the correctly rounded sin/cos table: where NumPy's sin/cos are correctly
+    # rounded as well (>= 99% of grid points) the phase is bit-identical to the oracle's
+    # and only the final sin/cos may differ by an ulp or two
+    err = np.abs(got - want)
+    assert np.median(err) <= 2.5e-16
+    assert err.max() <= 2 * np.spacing(2 * np.pi * n_side * 2.0) + 4e-16
 
 
 @pytest.mark.parametrize("n_side,leaf,r", [(32, 2, 6), (32, 2, 20), (64, 4, 25)])
