@@ -56,6 +56,53 @@ def synthetic_chain(p: DyadicPartition, r: int, seed: int = 20240801, device=Non
     return ButterflyFactors(p, r, BlockDiagonalFactor(u), g, MiddleFactor(w), h, BlockDiagonalFactor(v))
 
 
+BENCH_CHUNK = 1 << 22   # complex values per independently seeded chunk (thread-count invariant)
+
+
+def bench_chain(p, r: int, seed: int = 20240801, threads: int | None = None) -> ButterflyFactors:
+    """Host (NumPy) synthetic chain for the benchmark, identical bytes in both bench arms.
+
+    Same distribution and factor order as ``synthetic_chain`` (V^L, H ascending, M, G
+    ascending, U^L), but every factor is split into fixed chunks of ``BENCH_CHUNK`` values,
+    each drawn from its own ``SeedSequence(seed, spawn_key=(factor, chunk))`` generator, so
+    the chunks can be filled by a thread pool (NumPy's generators release the GIL) and the
+    result does not depend on the thread count. cfg2 (9.1 GB) draws in a few seconds
+    instead of ~25 s sequentially."""
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+
+    shapes, leaf_shape = level_geometry(p, r)
+    specs = [("c", leaf_shape)] + [("c", s) for _, _, s in shapes] + [("w", (p.mid_nodes, p.mid_nodes, r))] \
+        + [("c", s) for _, _, s in shapes] + [("c", leaf_shape)]
+    arrays = [np.empty(s, dtype=np.complex128 if kind == "c" else np.float64) for kind, s in specs]
+    jobs = []
+    for fi, ((kind, shape), arr) in enumerate(zip(specs, arrays)):
+        flat = arr.reshape(-1)
+        for ci, lo in enumerate(range(0, flat.size, BENCH_CHUNK)):
+            jobs.append((fi, ci, kind, shape, flat[lo:lo + BENCH_CHUNK]))
+
+    def fill(job):
+        fi, ci, kind, shape, out = job
+        rng = np.random.default_rng(np.random.SeedSequence(seed, spawn_key=(fi, ci)))
+        if kind == "w":
+            out[:] = rng.uniform(0.5, 1.5, size=out.size)
+            return
+        scale = 1.0 / np.sqrt(2.0 * shape[-1])
+        v = out.view(np.float64)                      # interleaved (re, im)
+        rng.standard_normal(out=v)
+        v *= scale
+
+    with ThreadPoolExecutor(max_workers=threads or min(32, os.cpu_count() or 1)) as ex:
+        list(ex.map(fill, jobs))
+    nl = len(shapes)
+    v = arrays[0]
+    h = tuple(TransferFactor(lvl, a) for (lvl, _, _), a in zip(shapes, arrays[1:1 + nl]))
+    w = arrays[1 + nl]
+    g = tuple(TransferFactor(lvl, a) for (lvl, _, _), a in zip(shapes, arrays[2 + nl:2 + 2 * nl]))
+    u = arrays[-1]
+    return ButterflyFactors(p, r, BlockDiagonalFactor(u), g, MiddleFactor(w), h, BlockDiagonalFactor(v))
+
+
 def to_host(f: ButterflyFactors) -> ButterflyFactors:
     """NumPy copy of a (possibly device-resident) chain."""
     def h(a):
