@@ -59,21 +59,13 @@ def synthetic_chain(p: DyadicPartition, r: int, seed: int = 20240801, device=Non
 BENCH_CHUNK = 1 << 22   # complex values per independently seeded chunk (thread-count invariant)
 
 
-def bench_chain(p, r: int, seed: int = 20240801, threads: int | None = None) -> ButterflyFactors:
-    """Host (NumPy) synthetic chain for the benchmark, identical bytes in both bench arms.
-
-    Same distribution and factor order as ``synthetic_chain`` (V^L, H ascending, M, G
-    ascending, U^L), but every factor is split into fixed chunks of ``BENCH_CHUNK`` values,
-    each drawn from its own ``SeedSequence(seed, spawn_key=(factor, chunk))`` generator, so
-    the chunks can be filled by a thread pool (NumPy's generators release the GIL) and the
-    result does not depend on the thread count. cfg2 (9.1 GB) draws in a few seconds
-    instead of ~25 s sequentially."""
+def _fill(specs, seed, key0=(), threads=None):
+    """Allocate and fill [(kind, shape)] ("c": complex Gaussian / sqrt(2 cols), "w": U(0.5, 1.5))
+    chunk by chunk, chunk c of array a from SeedSequence(seed, spawn_key=key0 + (a, c)), on a
+    thread pool (NumPy's generators release the GIL)."""
     from concurrent.futures import ThreadPoolExecutor
     import os
 
-    shapes, leaf_shape = level_geometry(p, r)
-    specs = [("c", leaf_shape)] + [("c", s) for _, _, s in shapes] + [("w", (p.mid_nodes, p.mid_nodes, r))] \
-        + [("c", s) for _, _, s in shapes] + [("c", leaf_shape)]
     arrays = [np.empty(s, dtype=np.complex128 if kind == "c" else np.float64) for kind, s in specs]
     jobs = []
     for fi, ((kind, shape), arr) in enumerate(zip(specs, arrays)):
@@ -83,17 +75,31 @@ def bench_chain(p, r: int, seed: int = 20240801, threads: int | None = None) -> 
 
     def fill(job):
         fi, ci, kind, shape, out = job
-        rng = np.random.default_rng(np.random.SeedSequence(seed, spawn_key=(fi, ci)))
+        rng = np.random.default_rng(np.random.SeedSequence(seed, spawn_key=tuple(key0) + (fi, ci)))
         if kind == "w":
             out[:] = rng.uniform(0.5, 1.5, size=out.size)
             return
-        scale = 1.0 / np.sqrt(2.0 * shape[-1])
         v = out.view(np.float64)                      # interleaved (re, im)
         rng.standard_normal(out=v)
-        v *= scale
+        v *= 1.0 / np.sqrt(2.0 * shape[-1])
 
     with ThreadPoolExecutor(max_workers=threads or min(32, os.cpu_count() or 1)) as ex:
         list(ex.map(fill, jobs))
+    return arrays
+
+
+def bench_chain(p, r: int, seed: int = 20240801, threads: int | None = None) -> ButterflyFactors:
+    """Host (NumPy) synthetic chain for the benchmark, identical bytes in both bench arms.
+
+    Same distribution and factor order as ``synthetic_chain`` (V^L, H ascending, M, G
+    ascending, U^L), but every factor is split into fixed chunks of ``BENCH_CHUNK`` values,
+    each drawn from its own ``SeedSequence(seed, spawn_key=(factor, chunk))`` generator, so
+    the chunks can be filled by a thread pool and the result does not depend on the thread
+    count. cfg2 (9.1 GB) draws in a few seconds instead of ~25 s sequentially."""
+    shapes, leaf_shape = level_geometry(p, r)
+    specs = [("c", leaf_shape)] + [("c", s) for _, _, s in shapes] + [("w", (p.mid_nodes, p.mid_nodes, r))] \
+        + [("c", s) for _, _, s in shapes] + [("c", leaf_shape)]
+    arrays = _fill(specs, seed, threads=threads)
     nl = len(shapes)
     v = arrays[0]
     h = tuple(TransferFactor(lvl, a) for (lvl, _, _), a in zip(shapes, arrays[1:1 + nl]))
@@ -101,6 +107,23 @@ def bench_chain(p, r: int, seed: int = 20240801, threads: int | None = None) -> 
     g = tuple(TransferFactor(lvl, a) for (lvl, _, _), a in zip(shapes, arrays[2 + nl:2 + 2 * nl]))
     u = arrays[-1]
     return ButterflyFactors(p, r, BlockDiagonalFactor(u), g, MiddleFactor(w), h, BlockDiagonalFactor(v))
+
+
+def bench_slices(p, r: int, part: int, nparts: int, seed: int = 20240801, threads: int | None = None) -> dict:
+    """One part's factor slices (the ``shard_slices`` layout: leading index range
+    [part/nparts, (part+1)/nparts) of every factor, full weights) drawn on the host, seeded
+    per part (spawn keys (1000 + part, factor, chunk)); weights as in ``bench_chain``. For
+    chains no host or GPU holds whole (BASELINE config 4a: 180 GB in complex128)."""
+    shapes, leaf_shape = level_geometry(p, r)
+    loc = lambda s: (s[0] // nparts,) + tuple(s[1:])  # noqa: E731
+    specs = [("c", loc(leaf_shape))] + [("c", loc(s)) for _, _, s in shapes] \
+        + [("c", loc(s)) for _, _, s in shapes] + [("c", loc(leaf_shape))]
+    arrays = _fill(specs, seed, key0=(1000 + part,), threads=threads)
+    w = _fill([("w", (p.mid_nodes, p.mid_nodes, r))], seed, key0=(2000,), threads=threads)[0]
+    nl = len(shapes)
+    return {"v_leaf": arrays[0], "h": [(lvl, a) for (lvl, _, _), a in zip(shapes, arrays[1:1 + nl])],
+            "weights": w, "g": [(lvl, a) for (lvl, _, _), a in zip(shapes, arrays[1 + nl:1 + 2 * nl])],
+            "u_leaf": arrays[-1]}
 
 
 def to_host(f: ButterflyFactors) -> ButterflyFactors:
