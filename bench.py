@@ -428,39 +428,38 @@ def run_reference(args):
     }))
 
 
-def run_sharded(args, world, rank, local):
-    """N > 1: the same workload sharded over the ranks (strong scaling): each rank
-    owns m/N middle nodes per side, runs its down half, the middle factor is one
-    NCCL all-to-all (weights fused into the pack), then its up half."""
+def measure_sharded(name, dtype, k, weak, world, rank, local, steps, warm, exchange, e2e=True):
+    """One sharded workload on all ranks: each rank owns m/N middle nodes
+    per side, runs its down half, the middle factor is an exchange (fused peer stores into
+    symmetric memory, or pack + NCCL all-to-all + unpack), then its up half. Device-timed
+    with CUDA events, max over ranks; the exchange (or the wait for the peers' stores) is
+    timed separately. Returns the fields of a JSON line (rank 0) or None."""
     import torch
     import torch.distributed as dist
 
     import paper_1502_01379_b200 as bf
     from paper_1502_01379_b200.sharded import PUSH_BARRIER_TIMEOUT_MS, ShardedPlan
+    from paper_1502_01379_b200.synthetic import synthetic_slices
 
-    kern, n, r, leaf, k0 = CONFIGS[args.config]
-    k = args.rhs or k0
-    esz = 16 if args.dtype == "c128" else 8
-    # weak scaling (default): every GPU keeps the single-GPU config's size, the chain grows
-    # with the GPU count (cfg2 per GPU -> N = 2^20 x GPUs; at 8 GPUs 2^23). 2-D configs
-    # (quadtrees over n_side^2 points) and cfg4a (BASELINE's fixed N = 2^24 sharded
-    # config) scale strongly.
-    weak = args.scaling == "weak" and kern != "radon2d" and args.config != "cfg4a"
+    kern, n, r, leaf, _ = CONFIGS[name]
+    esz = 16 if dtype == "c128" else 8
     if weak:
         n *= world
     p = partition_for(kern, n, leaf)
-    from paper_1502_01379_b200.synthetic import synthetic_slices
-    sp = ShardedPlan(p, r, rank, world, synthetic_slices(p, r, rank, world, seed=20240801, device="cuda"),
-                     dtype=args.dtype)
+    # each rank draws only its own factor slices, on its device (cfg4a: 180 GB in total)
+    sp = ShardedPlan(p, r, rank, world, synthetic_slices(p, r, rank, world, seed=FACTOR_SEED, device="cuda"),
+                     dtype=dtype)
     torch.cuda.empty_cache()
-    tdt = torch.complex128 if args.dtype == "c128" else torch.complex64
+    tdt = torch.complex128 if dtype == "c128" else torch.complex64
     nl = n // world
-    g_host = rhs_input(n, k)[rank * nl:(rank + 1) * nl]
-    g = torch.from_numpy(np.ascontiguousarray(g_host)).to("cuda").to(tdt)
+    if n * k <= (1 << 24):
+        g_host = np.ascontiguousarray(rhs_input(n, k)[rank * nl:(rank + 1) * nl])
+    else:   # this rank's rows only, seeded per rank
+        rng = np.random.default_rng(np.random.SeedSequence(0, spawn_key=(4, 0, rank)))
+        g_host = rng.standard_normal((nl, k)) + 1j * rng.standard_normal((nl, k))
+    g = torch.from_numpy(g_host).to("cuda").to(tdt)
     stream = torch.cuda.current_stream()
-    steps, warm = args.steps, max(args.warmup, 3)
-    exchange = args.exchange
-    if exchange == "push":
+    if exchange == "push" and world > 1:
         # fused path: validate once against pack + NCCL all-to-all, fall back if unavailable or different
         try:
             ref_out = sp.apply(g)
@@ -471,8 +470,11 @@ def run_sharded(args, world, rank, local):
             dist.all_reduce(flag, op=dist.ReduceOp.MIN)
             if int(flag.item()) != 1:
                 exchange = "nccl (push validation failed)"
+            del ref_out, push_out
         except Exception as exc:  # symmetric memory / IPC not available
             exchange = f"nccl (push unavailable: {type(exc).__name__})"
+    elif exchange == "push":
+        exchange = "nccl"      # one rank: nothing to push to
     use_push = exchange == "push"
     run = sp.apply_push if use_push else sp.apply
     for _ in range(warm):
@@ -510,50 +512,131 @@ def run_sharded(args, world, rank, local):
     clk = clocks.stop()
     t = torch.tensor([e0.elapsed_time(e1), sum(a.elapsed_time(b) for a, b in ev)], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_step, a2a_ms = float(t[0]) / steps, float(t[1]) / steps
-    # end to end: this rank's pinned host rows in, result rows back to pinned host memory
-    g_pin = torch.empty((nl, k), dtype=tdt, pin_memory=True)
-    g_pin.copy_(torch.from_numpy(np.ascontiguousarray(g_host)).to(tdt))
-    o_pin = torch.empty((nl, k), dtype=tdt, pin_memory=True)
-    dist.barrier()
-    t0 = time.perf_counter()
-    e2e_steps = max(3, min(steps, 10))
-    for _ in range(e2e_steps):
-        o_pin.copy_(run(g_pin.to("cuda", non_blocking=True)))
-    torch.cuda.synchronize()
-    e2e = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device="cuda")
-    dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
-    e2e_s = float(e2e.item())
-    if rank == 0:
-        shapes, leaf_shape = bf.level_geometry(p, r)
-        fac_elems = 2 * int(np.prod(leaf_shape)) + 2 * sum(int(np.prod(s_)) for _, _, s_ in shapes)
-        fac_bytes = esz * fac_elems // world + (esz // 2) * p.mid_nodes ** 2 * r + 2 * esz * nl * k
-        a2a_bytes = esz * (world - 1) * sp.chunk_rows * k
-        hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)) \
-            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
-        achieved = fac_bytes / (((ms_step - a2a_ms) if not use_push else ms_step) / 1e3) / 1e9
-        print(json.dumps({
-            "metric": METRIC, "value": n * k / (ms_step / 1e3), "unit": "samples/s", "n_gpus": world,
-            "steps": steps, "warmup": warm, "ms_per_step": ms_step, "higher_is_better": True,
+    ms_step, xch_ms = float(t[0]) / steps, float(t[1]) / steps
+    e2e_rec = None
+    if e2e:
+        # end to end: this rank's pinned host rows in, result rows back to pinned host memory
+        g_pin = torch.empty((nl, k), dtype=tdt, pin_memory=True)
+        g_pin.copy_(torch.from_numpy(g_host).to(tdt))
+        o_pin = torch.empty((nl, k), dtype=tdt, pin_memory=True)
+        dist.barrier()
+        t0 = time.perf_counter()
+        e2e_steps = max(3, min(steps, 10))
+        for _ in range(e2e_steps):
+            o_pin.copy_(run(g_pin.to("cuda", non_blocking=True)))
+        torch.cuda.synchronize()
+        e2e_t = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device="cuda")
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        e2e_s = float(e2e_t.item())
+        e2e_rec = {"value": n * k / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": n * k * esz,
+                   "d2h_bytes_per_step": n * k * esz, "ms_per_step": e2e_s * 1e3}
+    del sp, g
+    torch.cuda.empty_cache()
+    if rank != 0:
+        return None
+    shapes, leaf_shape = bf.level_geometry(p, r)
+    fac_elems = 2 * int(np.prod(leaf_shape)) + 2 * sum(int(np.prod(s_)) for _, _, s_ in shapes)
+    nnz_m = p.mid_nodes ** 2 * r
+    per_gpu_bytes = esz * fac_elems // world + (esz // 2) * nnz_m + 2 * esz * nl * k
+    per_gpu_flops = (8 * k * fac_elems + 2 * k * nnz_m) // world
+    a2a_bytes = esz * (world - 1) * sp_chunk_rows(p, r, world) * k
+    hbm, dmma, _ = _peaks()
+    local_ms = ms_step if use_push else ms_step - xch_ms
+    roof = {"achieved_gbs_per_gpu": per_gpu_bytes / (local_ms / 1e3) / 1e9, "hbm_peak": hbm,
+            "achieved_tflops_per_gpu": per_gpu_flops / (local_ms / 1e3) / 1e12, "dmma_peak": dmma,
+            "kernel": "local chain (down + up) per rank" + (" incl. fused peer stores" if use_push else
+                                                            ", exchange excluded")}
+    if k < 8:
+        roof.update(bound="hbm", achieved=roof["achieved_gbs_per_gpu"], peak=hbm, unit="GB/s",
+                    frac=roof["achieved_gbs_per_gpu"] / hbm)
+    else:
+        roof.update(bound="tensor", achieved=roof["achieved_tflops_per_gpu"], peak=dmma, unit="TFLOP/s",
+                    frac=roof["achieved_tflops_per_gpu"] / dmma)
+    return {"value": n * k / (ms_step / 1e3), "unit": "samples/s", "n_gpus": world, "steps": steps, "warmup": warm,
+            "ms_per_step": ms_step, "config": bench_config(name, kern, n, r, leaf, k, p, dtype, world,
+                                                           f"node-sharded{world}"),
             "scaling": "weak" if weak else "strong",
-            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-            "config": bench_config(args.config, kern, n, r, leaf, k, p, args.dtype, world,
-                                   f"node-sharded{world}"),
-            "sharding": f"middle nodes over {world} GPUs, "
-                        f"{'weak scaling: the config per GPU' if weak else 'strong scaling'}, exchange at M: "
-                        f"{exchange}",
-            "exchange": exchange,
-            "a2a_ms_per_step": None if use_push else a2a_ms,
-            "exchange_wait_ms_per_step": a2a_ms if use_push else None, "a2a_bytes_per_rank": a2a_bytes,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": None, "kernel": "local chain (down + up) per rank" +
-                         (" incl. fused peer stores" if use_push else ", all-to-all excluded"),
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
-            "e2e": {"value": n * k / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": n * k * esz,
-                    "d2h_bytes_per_step": n * k * esz, "ms_per_step": e2e_s * 1e3},
-            "gpu_launches": (2 * (p.levels - p.half) + 4) * steps,
-            "clocks": clk, "cpu_baseline": None,
-        }))
+            "sharding": f"middle nodes over {world} GPUs, {'weak scaling: the config per GPU' if weak else 'strong scaling'}"
+                        f", exchange at M: {exchange}",
+            "exchange": exchange, "a2a_ms_per_step": None if use_push else xch_ms,
+            "exchange_wait_ms_per_step": xch_ms if use_push else None, "a2a_bytes_per_rank": a2a_bytes,
+            "roofline": roof, "e2e": e2e_rec, "clocks": clk,
+            "gpu_launches": (2 * (p.levels - p.half) + (2 if use_push else 4)) * steps}
+
+
+def sp_chunk_rows(p, r, world):
+    mp = p.mid_nodes // world
+    return mp * mp * r
+
+
+def single_gpu_ms(name, k, steps, warm):
+    """The unsharded one-GPU apply of a config (the strong-scaling N = 1 point), device-timed."""
+    import torch
+
+    from paper_1502_01379_b200.synthetic import synthetic_chain
+    kern, n, r, leaf, _ = CONFIGS[name]
+    p = partition_for(kern, n, leaf)
+    plan = synthetic_chain(p, r, seed=FACTOR_SEED, device="cuda").plan("c128")
+    g = torch.from_numpy(rhs_input(n, k)).cuda()
+    out = torch.empty_like(g)
+    ws = torch.empty(plan.workspace_bytes(k), dtype=torch.uint8, device="cuda")
+    ms = dev_time(lambda: plan.apply(g, out=out, workspace=ws), steps, warm)
+    del plan, g, out, ws
+    torch.cuda.empty_cache()
+    return ms
+
+
+def run_sharded(args, world, rank, local):
+    """N > 1 (or --sharded): the headline workload sharded over the ranks — weak scaling by
+    default (cfg2 per GPU, N = 2^20 x GPUs), so the driver's per-N values compare — plus,
+    in `also`, BASELINE configs[4]: cfg4b (2-D n = 1024, 16 RHS) strong over the N GPUs with
+    its one-GPU time and scaling efficiency, and cfg4a (N = 2^24, 64 RHS, 180 GB of
+    factors: never on one GPU) at N >= 2, each with the exchange time broken out."""
+    import torch
+    import torch.distributed as dist
+
+    kern, _, _, _, k0 = CONFIGS[args.config]
+    k = args.rhs or k0
+    weak = args.scaling == "weak" and kern != "radon2d" and args.config != "cfg4a"
+    steps, warm = args.steps, max(args.warmup, 3)
+    rec = measure_sharded(args.config, args.dtype, k, weak, world, rank, local, steps, warm, args.exchange)
+    also = None
+    if not args.no_also and args.config == "cfg2":
+        also = {}
+
+        def run(key, fn):
+            try:
+                res = fn()
+            except Exception as exc:   # a companion must not cost the headline line
+                res = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+            if rank == 0:
+                also[key] = res
+
+        def cfg4b():
+            res = measure_sharded("cfg4b", "c128", 16, False, world, rank, local, max(3, min(steps, 10)), 3,
+                                  args.exchange, e2e=False)
+            one = torch.tensor([single_gpu_ms("cfg4b", 16, 5, 3) if rank == 0 else 0.0], device="cuda")
+            dist.broadcast(one, 0)
+            if res is not None:
+                res["one_gpu_ms_per_step"] = float(one.item())
+                res["scaling_efficiency"] = float(one.item()) / (world * res["ms_per_step"])
+            return res
+
+        run("cfg4b_strong", cfg4b)
+        free = torch.tensor([torch.cuda.mem_get_info()[0]], device="cuda", dtype=torch.float64)
+        dist.all_reduce(free, op=dist.ReduceOp.MIN)
+        # cfg4a: 180.5 GB of factors / N per GPU + ~6 vectors of 2^24 x 64 / N complex128
+        need = (180.5e9 + 6 * 17.2e9) / world
+        if world >= 2 and float(free.item()) > 1.1 * need:
+            run("cfg4a_strong", lambda: measure_sharded("cfg4a", "c128", 64, False, world, rank, local,
+                                                         max(3, min(steps, 5)), 2, args.exchange, e2e=False))
+        elif rank == 0:
+            also["cfg4a_strong"] = {"skipped": f"needs ~{need / 1e9:.0f} GB per GPU at {world} GPUs "
+                                               f"({float(free.item()) / 1e9:.0f} GB free)"}
+    if rank == 0:
+        out = {"metric": METRIC, **rec, "higher_is_better": True, "vs_baseline": None, "dtype": args.dtype,
+               "data": "synthetic", "cpu_baseline": None, "also": also}
+        print(json.dumps(out))
     dist.destroy_process_group()
 
 

@@ -56,6 +56,8 @@ extern "C" {
 #define BF_KERNEL_DFTP 1 /* exp(+2 pi i (j k mod N)/N) — BASELINE config 1                   */
 #define BF_KERNEL_DENSE 2 /* explicit n x n complex128 matrix on the device (DenseOracle)    */
 #define BF_KERNEL_RADON2D 3 /* 2-D generalized Radon, n = n_side^2 Morton indices (cfg 3/4b)   */
+#define BF_KERNEL_DFT 4   /* the reference's centered DftKernel exp(-2 pi i (j - N/2) k / N) (kernels.py:87-97) */
+#define BF_KERNEL_TILES 5 /* per-middle-block windows of any entry oracle (bf_middle_blocks_tiled) */
 
 typedef struct bf_plan bf_plan;
 
@@ -211,6 +213,18 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
                      uint32_t q_over, uint32_t iters, const void* dense, uint32_t nblocks, const int32_t* block_ij,
                      const int32_t* draws, void* u_out, void* v_out, double* w_out,
                      void* workspace, uint64_t ws_bytes, void* stream);
+
+/* bf_middle_blocks for any entry oracle (the BlockView protocol, oracles.py:57-68):
+ * the caller evaluates each block's side x side window K[i side + a, j side + b]
+ * (host oracle.block(), or a device producer) and passes the windows stacked as
+ * tiles (ntiles, side, side) complex128 row-major on the device, with slot
+ * (m, m) int32 on the device giving block (i, j)'s tile index (-1 for blocks not
+ * in this call). Every entry a middle block's sampling SVD reads lies in its
+ * window, so the results are those of bf_middle_blocks on the dense matrix. */
+int bf_middle_blocks_tiled(uint64_t n, uint32_t levels, uint32_t branching, uint32_t rank, uint32_t q_over,
+                           uint32_t iters, const void* tiles, const int32_t* slot, uint32_t nblocks,
+                           const int32_t* block_ij, const int32_t* draws, void* u_out, void* v_out, double* w_out,
+                           void* workspace, uint64_t ws_bytes, void* stream);
 
 /* Matvec-mode middle level (middle_factorization_matvec, construct.py:89-124;
  * per block svd_from_probes, lowrank.py:204-216): the rank-r SVD of `nblocks`

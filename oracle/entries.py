@@ -27,6 +27,13 @@ def fio_block(n: int, rows, cols) -> np.ndarray:
     return np.exp(2j * np.pi * phase)
 
 
+def dft_block(n: int, rows, cols) -> np.ndarray:
+    """The reference's centered DftKernel.block (kernels.py:94-97)."""
+    xi = np.asarray(rows, dtype=float)[:, None] - n / 2.0
+    x = np.asarray(cols, dtype=float)[None, :] / n
+    return np.exp(-2j * np.pi * xi * x)
+
+
 def dftp_block(n: int, rows, cols) -> np.ndarray:
     j = np.asarray(rows, dtype=np.int64)[:, None]
     k = np.asarray(cols, dtype=np.int64)[None, :]

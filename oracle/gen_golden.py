@@ -130,6 +130,22 @@ def gen_entries(bf):
     print("entries.npz")
 
 
+def gen_dft(bf):
+    """The reference's centered DftKernel (kernels.py:87-97): entries, and eps_a of its own
+    sampling factorization at N=1024 leaf 1 r=8 (bench.py:84-97)."""
+    from butterfly.kernels import DftKernel
+    rng = np.random.default_rng(11)
+    d = {}
+    for n in (1024, 1 << 16, 1 << 20):
+        rows = np.sort(rng.choice(n, size=64, replace=False))
+        cols = np.sort(rng.choice(n, size=64, replace=False))
+        d[f"dft_{n}_rows"], d[f"dft_{n}_cols"] = rows, cols
+        d[f"dft_{n}"] = DftKernel(n).block(rows, cols)
+    np.savez_compressed(os.path.join(OUT, "dft_entries.npz"), **d)
+    gen_eps(bf, "eps_dft_n1024_r8_leaf1.npz", DftKernel(1024), 1024, 1, 8, 0)
+    print("dft_entries.npz")
+
+
 def gen_geometry(bf):
     from butterfly.construct import _level_geometry
     d = {}
@@ -347,6 +363,9 @@ def main():
     if len(sys.argv) > 1 and sys.argv[1] == "hankel":
         gen_hankel(bf)
         return
+    if len(sys.argv) > 1 and sys.argv[1] == "dft":
+        gen_dft(bf)
+        return
     gen_bfac(bf)
     gen_geometry(bf)
     gen_entries(bf)
@@ -362,6 +381,7 @@ def main():
                   [(0, 0), (17, 30)])
     gen_matvec(bf)
     gen_hankel(bf)
+    gen_dft(bf)
 
 
 if __name__ == "__main__":

@@ -11,7 +11,7 @@ from .factors import (BlockDiagonalFactor, ButterflyFactors, DevicePlan, MiddleF
 from .construct import (DEFAULT_PARAMS, OversamplingParams, block_diagonal_probe, factorize,
                         middle_factorization_matvec, middle_factorization_sampling, recursive_factor_u,
                         recursive_factor_v)
-from .kernels import (ComposedOperator, DenseOracle, DftPlusKernel, FioKernel, HankelKernel, Radon2DKernel,
+from .kernels import (ComposedOperator, DenseOracle, DftKernel, DftPlusKernel, FioKernel, HankelKernel, Radon2DKernel,
                       composed_matvec, dft_apply, fio_entry, hankel1_orders_device, hankel_entry)
 from .metrics import OperatorReference, RowSampledReference, estimate_eps_a, estimate_eps_a_info
 from .storage import FormatError, load_factors, read_vector, save_factors, write_vector

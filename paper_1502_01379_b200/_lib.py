@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libbfly.so")
 BF_OK, BF_EINVAL, BF_ECUDA, BF_ENOMEM, BF_EORACLE, BF_ESTATE, BF_EFORMAT = range(7)
 BF_C128, BF_C64 = 0, 1
 BF_FACTOR_V, BF_FACTOR_H, BF_FACTOR_M, BF_FACTOR_G, BF_FACTOR_U = range(5)
-BF_KERNEL_FIO, BF_KERNEL_DFTP, BF_KERNEL_DENSE, BF_KERNEL_RADON2D = 0, 1, 2, 3
+BF_KERNEL_FIO, BF_KERNEL_DFTP, BF_KERNEL_DENSE, BF_KERNEL_RADON2D, BF_KERNEL_DFT, BF_KERNEL_TILES = range(6)
 
 # (name, restype, argtypes) — must match include/bfly.h
 _P = ctypes.c_void_p
@@ -39,6 +39,8 @@ SIGNATURES = [
     ("bf_timer_read", _I, [_P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(_U32), ctypes.POINTER(_U32)]),
     ("bf_middle_workspace_bytes", _U64, [_U64, _U32, _U32, _U32, _U32, _U32]),
     ("bf_middle_blocks", _I, [_I, _U64, _U32, _U32, _U32, _U32, _U32, _P, _U32, _P, _P, _P, _P, _P, _P, _U64, _P]),
+    ("bf_middle_blocks_tiled", _I, [_U64, _U32, _U32, _U32, _U32, _U32, _P, _P, _U32, _P, _P, _P, _P, _P, _P, _U64,
+                                    _P]),
     ("bf_probe_workspace_bytes", _U64, [_U64, _U32, _U32, _U32, _U32, _U32]),
     ("bf_middle_probes", _I, [_U64, _U32, _U32, _U32, _U32, _U32, _P, _P, _U64, _P, _U64, _P, _P, _P, _P, _P, _U64,
                               _P]),

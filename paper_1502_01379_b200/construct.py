@@ -23,7 +23,6 @@ from __future__ import annotations
 import ctypes
 import multiprocessing
 import os
-import warnings
 from concurrent.futures import ProcessPoolExecutor
 from dataclasses import dataclass
 
@@ -59,6 +58,12 @@ DEFAULT_PARAMS = OversamplingParams()
 _draws_for = draws_for
 
 
+def _draw_context():
+    ctx = multiprocessing.get_context("forkserver")
+    ctx.set_forkserver_preload(["paper_1502_01379_b200._draws"])
+    return ctx
+
+
 def draw_tables(seed, side: int, r: int, params: OversamplingParams, blocks) -> np.ndarray:
     """The reference's per-block rng.choice draws, in consumption order."""
     rqs = min(r * params.q, side)
@@ -67,13 +72,11 @@ def draw_tables(seed, side: int, r: int, params: OversamplingParams, blocks) -> 
         return _draws_for((seed, side, rqs, params.iters, blocks))
     workers = min(16, os.cpu_count() or 1)
     chunks = [blocks[k::workers] for k in range(workers)]
-    # fork workers: they run NumPy only (never CUDA) on their own block lists. "spawn" /
-    # "forkserver" would re-execute the caller's __main__ script in every worker.
-    with warnings.catch_warnings():
-        warnings.filterwarnings("ignore", message=".*use of fork\\(\\) may lead to deadlocks.*",
-                                category=DeprecationWarning)
-        with ProcessPoolExecutor(workers, mp_context=multiprocessing.get_context("fork")) as ex:
-            parts = list(ex.map(_draws_for, [(seed, side, rqs, params.iters, c) for c in chunks]))
+    # workers fork from a fresh forkserver process that has imported only NumPy and
+    # _draws (never torch or CUDA): forking this CUDA-initialised, multi-threaded process
+    # itself could deadlock a worker on a lock some other thread held at fork time
+    with ProcessPoolExecutor(workers, mp_context=_draw_context()) as ex:
+        parts = list(ex.map(_draws_for, [(seed, side, rqs, params.iters, c) for c in chunks]))
     out = np.empty((len(blocks), 2 * (params.iters + 1), rqs), dtype=np.int32)
     for k, part in enumerate(parts):
         out[k::workers] = part
@@ -81,33 +84,61 @@ def draw_tables(seed, side: int, r: int, params: OversamplingParams, blocks) -> 
 
 
 class _DeviceOracle:
-    """What the device needs to evaluate an entry oracle: a kernel id (+ matrix)."""
+    """How the device reads an entry oracle (SURVEY.md §8(b) "entry-oracle plugin protocol").
+
+    * analytic kernels by id (FIO, the config-1 DFT(+), the reference's centered DftKernel,
+      the 2-D Radon kernel), recognised by ``kernel_id`` or, for the reference's own
+      classes, by type name and ``n``;
+    * an explicit matrix (``DenseOracle``) or a cached Hankel table: a dense device source;
+    * anything else with ``.block(rows, cols)`` — including an uncached or too-large
+      Hankel kernel — through per-middle-block windows (``tiles``): each block's
+      side x side window is evaluated (host ``oracle.block`` through the BlockView
+      offsets, oracles.py:57-68, or a device producer) and uploaded batch by batch, so
+      memory stays bounded by the batch instead of the dense n x n matrix."""
 
     def __init__(self, oracle, n):
         torch = _lib.require_cuda()
+        self.oracle, self.n = oracle, n
         self.dense = None
+        self.tiles = None           # callable(list of (i, j), side) -> device (nb, side, side)
         kid = getattr(oracle, "kernel_id", None)
         name = type(oracle).__name__
-        if kid in (_lib.BF_KERNEL_FIO, _lib.BF_KERNEL_DFTP, _lib.BF_KERNEL_RADON2D):
+        if kid in (_lib.BF_KERNEL_FIO, _lib.BF_KERNEL_DFTP, _lib.BF_KERNEL_RADON2D, _lib.BF_KERNEL_DFT):
             self.kernel_id = kid
-        elif hasattr(oracle, "device_table"):
-            # entry tables built on the device (HankelKernel): read as a dense source
-            self.dense = oracle.device_table()
-            self.kernel_id = _lib.BF_KERNEL_DENSE
-        elif name == "HankelKernel" and getattr(oracle, "n", None) == n:  # the reference's own class
-            from .kernels import HankelKernel
-            self.dense = HankelKernel(n, cache=True).device_table()
-            self.kernel_id = _lib.BF_KERNEL_DENSE
         elif name == "FioKernel" and getattr(oracle, "n", None) == n:   # the reference's own class
             self.kernel_id = _lib.BF_KERNEL_FIO
-        else:
-            # explicit matrix (DenseOracle) or any other entry oracle, materialised once
-            mat = getattr(oracle, "matrix", None)
-            if mat is None:
-                idx = np.arange(n)
-                mat = oracle.block(idx, idx)
-            self.dense = torch.as_tensor(np.ascontiguousarray(mat, dtype=np.complex128)).cuda()
+        elif name == "DftKernel" and getattr(oracle, "n", None) == n:   # the reference's own class
+            self.kernel_id = _lib.BF_KERNEL_DFT
+        elif name == "HankelKernel" and getattr(oracle, "n", None) == n:
+            from .kernels import HankelKernel
+            mine = oracle if hasattr(oracle, "device_table") else \
+                HankelKernel(n, cache=bool(getattr(oracle, "_cache_rows", n <= HankelKernel.TABLE_CAP)))
+            if mine._cache and n <= HankelKernel.TABLE_CAP:
+                self.dense = mine.device_table()       # the reference's row cache, filled from empty
+                self.kernel_id = _lib.BF_KERNEL_DENSE
+            else:                                      # uncached rows: one order sweep per window
+                self.tiles = mine.device_windows
+                self.kernel_id = _lib.BF_KERNEL_TILES
+        elif getattr(oracle, "matrix", None) is not None:
+            self.dense = torch.as_tensor(np.ascontiguousarray(oracle.matrix, dtype=np.complex128)).cuda()
             self.kernel_id = _lib.BF_KERNEL_DENSE
+        else:
+            self.tiles = self._host_windows
+            self.kernel_id = _lib.BF_KERNEL_TILES
+
+    def _host_windows(self, blocks, side):
+        torch = _lib.require_cuda()
+        out = np.empty((len(blocks), side, side), dtype=np.complex128)
+        ar = np.arange(side, dtype=np.intp)
+        for b, (i, j) in enumerate(blocks):
+            try:
+                out[b] = self.oracle.block(ar + i * side, ar + j * side)
+            except Exception as exc:
+                raise _lib.OracleError(f"entry oracle failed on middle block ({i}, {j})") from exc
+        return torch.from_numpy(out).cuda()
+
+
+TILE_BUDGET = 2 << 30   # bytes of per-block entry windows uploaded per launch (BF_KERNEL_TILES)
 
 
 class MiddleSampler:
@@ -167,21 +198,43 @@ class MiddleSampler:
         if wsb == 0:
             raise ValueError("geometry/rank not supported by the batched sampling kernels (need r*(q+1) <= 128)")
         ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
-        dense = ctypes.c_void_p(self.dev.dense.data_ptr()) if self.dev.dense is not None else None
         stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-        rc = self.lib.bf_middle_blocks(self.dev.kernel_id, self.p.n, self.p.levels, self.branching, r,
-                                       self.params.q, self.params.iters, dense, nb, ctypes.c_void_p(ij_d.data_ptr()),
-                                       ctypes.c_void_p(draws_d.data_ptr()) if draws_d is not None else None,
-                                       ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(v.data_ptr()),
-                                       ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(ws.data_ptr()), wsb, stream)
-        if rc != _lib.BF_OK:
-            msg = _lib.last_error()
-            if rc == _lib.BF_EINVAL:
-                raise ValueError(msg)
-            raise _lib.OracleError(f"entry oracle failed on middle blocks {ij[:1].tolist()}...: {msg}")
+        P = ctypes.c_void_p
+        if self.dev.tiles is None:
+            dense = P(self.dev.dense.data_ptr()) if self.dev.dense is not None else None
+            rc = self.lib.bf_middle_blocks(self.dev.kernel_id, self.p.n, self.p.levels, self.branching, r,
+                                           self.params.q, self.params.iters, dense, nb, P(ij_d.data_ptr()),
+                                           P(draws_d.data_ptr()) if draws_d is not None else None,
+                                           P(u.data_ptr()), P(v.data_ptr()), P(w.data_ptr()), P(ws.data_ptr()), wsb,
+                                           stream)
+            self._raise(rc, ij)
+            states = ws[:nb * self._STATE.itemsize].cpu().numpy().view(self._STATE) if trace else None
+        else:
+            # per-block entry windows, uploaded in batches bounded by TILE_BUDGET
+            per = max(1, TILE_BUDGET // (16 * side * side))
+            slot = torch.full((self.m * self.m,), -1, dtype=torch.int32, device="cuda")
+            states = []
+            for lo in range(0, nb, per):
+                hi = min(nb, lo + per)
+                sub = [tuple(int(t) for t in x) for x in ij[lo:hi]]
+                tiles = self.dev.tiles(sub, side)
+                slot.fill_(-1)
+                slot[torch.as_tensor([i * self.m + j for i, j in sub], device="cuda")] = \
+                    torch.arange(hi - lo, dtype=torch.int32, device="cuda")
+                rc = self.lib.bf_middle_blocks_tiled(
+                    self.p.n, self.p.levels, self.branching, r, self.params.q, self.params.iters,
+                    P(tiles.data_ptr()), P(slot.data_ptr()), hi - lo, P(ij_d[lo:hi].data_ptr()),
+                    P(draws_d[lo:hi].data_ptr()) if draws_d is not None else None,
+                    P(u[lo:hi].data_ptr()), P(v[lo:hi].data_ptr()), P(w[lo:hi].data_ptr()), P(ws.data_ptr()), wsb,
+                    stream)
+                self._raise(rc, ij[lo:hi])
+                if trace:
+                    states.append(ws[:(hi - lo) * self._STATE.itemsize].cpu().numpy().view(self._STATE).copy())
+                del tiles
+            states = np.concatenate(states) if trace else None
         if not trace:
             return u, v, w
-        raw = ws[:nb * self._STATE.itemsize].cpu().numpy().view(self._STATE)
+        raw = states
         tr = []
         for st in raw:
             if st["tc"] < 0:        # dense branch: no pivots
@@ -191,6 +244,14 @@ class MiddleSampler:
                        "rows": st["rows"][:st["nrows"]].tolist(), "cols": st["cols"][:st["ncols"]].tolist(),
                        "pivc": st["pivc"][:st["tc"]].tolist(), "pivr": st["pivr"][:st["tr"]].tolist()})
         return u, v, w, tr
+
+    @staticmethod
+    def _raise(rc, ij):
+        if rc != _lib.BF_OK:
+            msg = _lib.last_error()
+            if rc == _lib.BF_EINVAL:
+                raise ValueError(msg)
+            raise _lib.OracleError(f"entry oracle failed on middle blocks {ij[:1].tolist()}...: {msg}")
 
     def batch_rows(self) -> int:
         """Block-rows per launch: enough CTAs to fill the GPU, bounded workspace."""

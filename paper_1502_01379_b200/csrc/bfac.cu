@@ -345,6 +345,9 @@ int bf_plan_save_bfac(const bf_plan* plan, const char* path) {
   const Plan& p = plan->p;
   if (!p.uploaded) return fail(BF_ESTATE, "plan has no factors");
   if (p.dtype != BF_C128 || p.nparts != 1) return fail(BF_EINVAL, "only unsharded complex128 plans are saved");
+  // the .bfac header (storage.py:65-93) has no branching field: a quadtree chain saved
+  // there would load back as a binary one and fail its block counts
+  if (p.branch != 2) return fail(BF_EINVAL, ".bfac holds binary-tree chains only (quadtree plan)");
   FileCloser fc{fopen(path, "wb")};
   if (!fc.f) return fail(BF_EINVAL, std::string("cannot create ") + path);
   DeviceGuardScope dg(p.device);

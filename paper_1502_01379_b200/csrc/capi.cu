@@ -567,7 +567,7 @@ uint64_t bf_sampled_rows_workspace(uint64_t n, uint32_t nr, uint32_t k) { return
 
 int bf_sampled_rows(int kernel_id, uint64_t n, const void* dense, const int64_t* rows, uint32_t nr, const void* g,
                     uint32_t k, void* out, void* workspace, uint64_t ws_bytes, void* stream) {
-  if (kernel_id < BF_KERNEL_FIO || kernel_id > BF_KERNEL_RADON2D) return fail(BF_EINVAL, "unknown entry kernel id");
+  if (kernel_id < BF_KERNEL_FIO || kernel_id > BF_KERNEL_DFT) return fail(BF_EINVAL, "unknown entry kernel id");
   if (kernel_id == BF_KERNEL_DENSE && !dense) return fail(BF_EINVAL, "dense oracle needs a matrix pointer");
   if (n < 1 || k < 1) return fail(BF_EINVAL, "n and k must be positive");
   if (!nr) return BF_OK;

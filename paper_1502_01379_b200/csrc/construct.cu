@@ -1506,10 +1506,32 @@ uint64_t bf_middle_workspace_bytes(uint64_t n, uint32_t levels, uint32_t branchi
   return mid_ws_layout(side, nblocks, S, off);
 }
 
+static int middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branching, uint32_t rank,
+                         uint32_t q_over, uint32_t iters, const void* dense, const int32_t* slot, uint32_t nblocks,
+                         const int32_t* block_ij, const int32_t* draws, void* u_out, void* v_out, double* w_out,
+                         void* workspace, uint64_t ws_bytes, void* stream);
+
 int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branching, uint32_t rank, uint32_t q_over,
                      uint32_t iters, const void* dense, uint32_t nblocks, const int32_t* block_ij, const int32_t* draws,
                      void* u_out, void* v_out, double* w_out, void* workspace, uint64_t ws_bytes, void* stream) {
-  if (kernel_id < BF_KERNEL_FIO || kernel_id > BF_KERNEL_RADON2D) return fail(BF_EINVAL, "unknown entry kernel id");
+  if (kernel_id < BF_KERNEL_FIO || kernel_id > BF_KERNEL_DFT) return fail(BF_EINVAL, "unknown entry kernel id");
+  return middle_blocks(kernel_id, n, levels, branching, rank, q_over, iters, dense, nullptr, nblocks, block_ij,
+                       draws, u_out, v_out, w_out, workspace, ws_bytes, stream);
+}
+
+int bf_middle_blocks_tiled(uint64_t n, uint32_t levels, uint32_t branching, uint32_t rank, uint32_t q_over,
+                           uint32_t iters, const void* tiles, const int32_t* slot, uint32_t nblocks,
+                           const int32_t* block_ij, const int32_t* draws, void* u_out, void* v_out, double* w_out,
+                           void* workspace, uint64_t ws_bytes, void* stream) {
+  if (!tiles || !slot) return fail(BF_EINVAL, "tiled middle blocks need tiles and a slot table");
+  return middle_blocks(BF_KERNEL_TILES, n, levels, branching, rank, q_over, iters, tiles, slot, nblocks, block_ij,
+                       draws, u_out, v_out, w_out, workspace, ws_bytes, stream);
+}
+
+static int middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branching, uint32_t rank,
+                         uint32_t q_over, uint32_t iters, const void* dense, const int32_t* slot, uint32_t nblocks,
+                         const int32_t* block_ij, const int32_t* draws, void* u_out, void* v_out, double* w_out,
+                         void* workspace, uint64_t ws_bytes, void* stream) {
   if (kernel_id == BF_KERNEL_DENSE && !dense) return fail(BF_EINVAL, "dense oracle needs a matrix pointer");
   uint64_t m = 0, side = 0;
   if (!tree_geometry(n, levels, branching, &m, &side)) return fail(BF_EINVAL, "bad partition geometry");
@@ -1533,6 +1555,9 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
   a.src.n = n;
   a.src.dense = static_cast<const double2*>(dense);
   a.src.tab = nullptr;
+  a.src.slot = slot;
+  a.src.side = side;
+  a.src.m = m;
   if (kernel_id == BF_KERNEL_FIO || kernel_id == BF_KERNEL_RADON2D) {
     a.src.tab = row_table(kernel_id, n, static_cast<cudaStream_t>(stream));
     if (!a.src.tab) return BF_ECUDA;

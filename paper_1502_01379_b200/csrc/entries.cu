@@ -115,7 +115,8 @@ const double* row_table(int kind, uint64_t n, cudaStream_t st) {
 
 int entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr, const int64_t* cols, uint32_t nc, void* out,
             cudaStream_t st) {
-  if (kernel_id != BF_KERNEL_FIO && kernel_id != BF_KERNEL_DFTP && kernel_id != BF_KERNEL_RADON2D)
+  if (kernel_id != BF_KERNEL_FIO && kernel_id != BF_KERNEL_DFTP && kernel_id != BF_KERNEL_RADON2D &&
+      kernel_id != BF_KERNEL_DFT)
     return fail(BF_EINVAL, "unknown entry kernel id");
   if (static_cast<uint64_t>(nr) * nc == 0) return 0;
   EntrySrc src{kernel_id, n, nullptr, nullptr};

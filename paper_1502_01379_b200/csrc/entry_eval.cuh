@@ -72,19 +72,42 @@ __device__ __forceinline__ double2 radon2d_entry(uint64_t n, const double* __res
   return make_double2(c, s);
 }
 
-// A device-evaluable entry oracle: analytic kernels by id, or an explicit
-// row-major matrix (the reference's DenseOracle, oracles.py:39-54).
+// The reference's centered transform DftKernel.block (kernels.py:87-97):
+// xi = row - n/2, x = col/n, exp(-2j*pi*xi*x) evaluated by NumPy as
+// ((-2j*pi)*xi)*x with complex-by-real products, i.e. angle fl(fl(-fl(2 pi) xi) x)
+// and a real part of +-0 (exp(+-0) = 1 exactly): (cos a, sin a), no FMA.
+__device__ __forceinline__ double2 dft_entry(uint64_t n, int64_t i, int64_t j) {
+  const double xi = __dsub_rn(static_cast<double>(i), 0.5 * static_cast<double>(n));
+  const double x = __ddiv_rn(static_cast<double>(j), static_cast<double>(n));
+  double s, c;
+  sincos(__dmul_rn(__dmul_rn(-kTwoPi, xi), x), &s, &c);
+  return make_double2(c, s);
+}
+
+// A device-evaluable entry oracle: analytic kernels by id, an explicit row-major
+// matrix (the reference's DenseOracle, oracles.py:39-54), or per-middle-block
+// windows of any entry oracle evaluated elsewhere (BF_KERNEL_TILES: the window of
+// block (bi, bj) is tile slot[bi m + bj], side x side row-major).
 struct EntrySrc {
-  int kind;             // BF_KERNEL_FIO | BF_KERNEL_DFTP | BF_KERNEL_DENSE | BF_KERNEL_RADON2D
+  int kind;             // BF_KERNEL_FIO | DFTP | DENSE | RADON2D | DFT | TILES
   uint64_t n;
-  const double2* dense; // BF_KERNEL_DENSE: n x n row-major
+  const double2* dense; // BF_KERNEL_DENSE: n x n row-major; BF_KERNEL_TILES: the tiles
   const double* tab;    // BF_KERNEL_FIO / BF_KERNEL_RADON2D: row_table(kind, n)
+  const int32_t* slot;  // BF_KERNEL_TILES: (m, m) tile index per middle block, -1 = absent
+  uint64_t side, m;     // BF_KERNEL_TILES: middle block side and count per dimension
 };
 
 __device__ __forceinline__ double2 entry_eval(const EntrySrc& s, int64_t i, int64_t j) {
   if (s.kind == BF_KERNEL_FIO) return fio_entry(s.n, s.tab, i, j);
   if (s.kind == BF_KERNEL_DFTP) return dftp_entry(s.n, i, j);
   if (s.kind == BF_KERNEL_RADON2D) return radon2d_entry(s.n, s.tab, i, j);
+  if (s.kind == BF_KERNEL_DFT) return dft_entry(s.n, i, j);
+  if (s.kind == BF_KERNEL_TILES) {
+    const uint64_t bi = static_cast<uint64_t>(i) / s.side, bj = static_cast<uint64_t>(j) / s.side;
+    const uint64_t t = static_cast<uint64_t>(s.slot[bi * s.m + bj]);
+    return s.dense[(t * s.side + (static_cast<uint64_t>(i) - bi * s.side)) * s.side +
+                   (static_cast<uint64_t>(j) - bj * s.side)];
+  }
   return s.dense[static_cast<uint64_t>(i) * s.n + j];
 }
 

@@ -133,6 +133,19 @@ class HankelKernel:
             self._table = table
         return self._table
 
+    def device_windows(self, blocks, side):
+        """(nb, side, side) device windows K[i side + a, j side + b] of middle blocks (i, j),
+        as the uncached reference path evaluates a block: one order sweep of the block's
+        rows up to its last column (kernels.py:63-66)."""
+        torch = _lib.require_cuda()
+        out = torch.empty((len(blocks), side, side), dtype=torch.complex128, device="cuda")
+        for b, (i, j) in enumerate(blocks):
+            rows = np.arange(i * side, (i + 1) * side)
+            table = hankel1_orders_device(self.points(rows), (j + 1) * side - 1)
+            out[b] = table[:, j * side:]
+            del table
+        return out
+
     def block(self, rows, cols) -> np.ndarray:
         torch = _lib.require_cuda()
         rows = np.asarray(rows, dtype=np.intp).reshape(-1)
@@ -156,6 +169,13 @@ def hankel_entry(n: int, i: int, j: int) -> complex:
 
 def fio_entry(n: int, i: int, j: int) -> complex:
     return complex(FioKernel(n).block([i], [j])[0, 0])
+
+
+class DftKernel(_DeviceKernel):
+    """The reference's centered transform F[j, k] = exp(-2 pi i xi_j x_k), xi_j = j - n/2,
+    x_k = k/n (kernels.py:87-97), evaluated on the device with NumPy's rounding order."""
+
+    kernel_id = _lib.BF_KERNEL_DFT
 
 
 class DenseOracle:

@@ -32,6 +32,18 @@ class RowSampledReference:
         vec = g.ndim == 1
         gd = torch.as_tensor(np.ascontiguousarray(g.reshape(n, -1), dtype=np.complex128)).cuda()
         k = gd.shape[1]
+        if self._dev.kernel_id == _lib.BF_KERNEL_TILES:
+            # an entry oracle the device cannot evaluate per entry: its rows K[S, :] through
+            # .block (the reference's own ground truth, bench.py:38-46), chunked to bound
+            # memory, the row sums on the device
+            sample = np.asarray(sample, dtype=np.intp)
+            res = torch.empty((sample.size, k), dtype=torch.complex128, device="cuda")
+            step = max(1, (1 << 27) // n)
+            for lo in range(0, sample.size, step):
+                blk = self.entry.block(sample[lo:lo + step], np.arange(n))
+                res[lo:lo + step] = torch.as_tensor(np.ascontiguousarray(blk, dtype=np.complex128)).cuda() @ gd
+            res = res.cpu().numpy()
+            return res[:, 0] if vec else res
         rows = torch.as_tensor(np.ascontiguousarray(sample, dtype=np.int64)).cuda()
         out = torch.empty((rows.numel(), k), dtype=torch.complex128, device="cuda")
         lib = _lib.load()

@@ -164,3 +164,11 @@ def test_oracle_recurse_cfg2_slab_bitwise():
     with threadpool_limits(1):
         leaf, pieces = ocons.recurse(slab, n, levels, r)
     assert np.array_equal(ocons.slab_chain_apply(leaf, pieces, d["probe"]), d["sig"])
+
+
+def test_dft_entries_match_reference():
+    """The reference's centered DftKernel (kernels.py:87-97), restated bitwise."""
+    d = golden("dft_entries.npz")
+    for n in (1024, 1 << 16, 1 << 20):
+        got = oent.dft_block(n, d[f"dft_{n}_rows"], d[f"dft_{n}_cols"])
+        assert np.array_equal(got, d[f"dft_{n}"])

@@ -70,3 +70,13 @@ def test_format_errors(tmp_path):
     with pytest.raises(bf.FormatError) as e:
         bf.load_factors(bad)
     assert e.value.offset == 28 + 13 + 24
+
+
+def test_save_rejects_quadtree_chain(tmp_path):
+    """The .bfac header carries no branching field (storage.py:65-93): a quadtree chain
+    is refused at save time instead of writing a file that cannot be read back."""
+    from paper_1502_01379_b200.synthetic import synthetic_chain
+    f = synthetic_chain(bf.make_quadtree_partition(32, 2), 4, seed=1)
+    with pytest.raises(ValueError, match="binary-tree"):
+        bf.save_factors(f, tmp_path / "q.bfac")
+    assert not (tmp_path / "q.bfac").exists()
