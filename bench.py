@@ -745,16 +745,24 @@ def main():
     ns, nl = ctypes.c_uint32(), ctypes.c_uint32()
     _lib.check(lib.bf_timer_read(timer, launch_ms, ctypes.byref(ns), ctypes.byref(nl)))
     lib.bf_timer_destroy(timer)
-    per_launch = np.array(launch_ms[:]).reshape(steps, nl.value).mean(axis=0)
-    lb = launch_bytes(f, k, esz)
+    per_launch = np.array(launch_ms[:steps * nl.value]).reshape(steps, nl.value).mean(axis=0)
     alg_bytes, alg_flops = algorithmic(f, k, esz)
+    node = nl.value == 2      # node kernels: each half of the chain is one launch
+    if node:
+        nlaunch = 2
+        lb = [("down half (node kernel)", alg_bytes // 2), ("up half (node kernel)", alg_bytes // 2)]
+        lf_all = [("down half (node kernel)", alg_flops // 2), ("up half (node kernel)", alg_flops // 2)]
+    else:
+        lb = launch_bytes(f, k, esz)
+        lf_all = launch_flops(f, k)
+    dominant = (lambda name: True) if node else (lambda name: name[0] in "GH")
     peaks = {}
     pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(pk_path):
         peaks = json.load(open(pk_path))
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     # dominant kernel: the transfer-level launches (2*(L-h) of the 2+2(L-h) launches)
-    tr = [(name, b, t) for (name, b), t in zip(lb, per_launch) if name[0] in "GH"]
+    tr = [(name, b, t) for (name, b), t in zip(lb, per_launch) if dominant(name)]
     tr_bytes = sum(b for _, b, _ in tr) / len(tr)
     tr_ms = sum(t for _, _, t in tr) / len(tr)
     share = sum(t for _, _, t in tr) / max(per_launch.sum(), 1e-9)
@@ -772,8 +780,7 @@ def main():
     if k >= 8 and args.dtype == "c128":
         # many right-hand sides: the transfer levels are FP64 tensor-core (DMMA) bound
         # (SURVEY.md §8(d)); algorithmic flops (8 per complex multiply-add) per launch
-        lf = launch_flops(f, k)
-        tr_fl = sum(fl for (name, fl) in lf if name[0] in "GH") / len(tr)
+        tr_fl = sum(fl for (name, fl) in lf_all if dominant(name)) / len(tr)
         fp64 = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))
         dmma_peak = float(fp64["dmma_m8n8k4_tflops"])
         roof = {"bound": "tensor", "achieved": tr_fl / (tr_ms / 1e3) / 1e12, "peak": dmma_peak, "unit": "TFLOP/s",
@@ -858,7 +865,8 @@ def main():
             "config": bench_config(args.config, kern, n, r, leaf, k, p, args.dtype, world),
             "rel_err": rel_err,
             "roofline": dict(roof, traffic=_ncu_traffic(args.config, args.dtype, k),
-                             kernel="level_kernel (transfer levels G/H)", kernel_share_of_step=share),
+                             kernel="node_kernel (one launch per half)" if node else
+                             "level_kernel (transfer levels G/H)", kernel_share_of_step=share),
             "chain_roofline": {"algorithmic_bytes": alg_bytes, "algorithmic_flops": alg_flops,
                                "achieved_gbs": alg_bytes / (ms_step / 1e3) / 1e9,
                                "frac": alg_bytes / (ms_step / 1e3) / 1e9 / hbm_peak},

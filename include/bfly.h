@@ -214,6 +214,10 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
                      const int32_t* draws, void* u_out, void* v_out, double* w_out,
                      void* workspace, uint64_t ws_bytes, void* stream);
 
+/* Diagnostics: node kernels (one launch per chain half) stamp %globaltimer per CTA into
+ * dev_buf (u64, >= 2 x m x chunks x 32; NULL turns it off). Not thread-safe; tools only. */
+int bf_debug_node_trace(unsigned long long* dev_buf);
+
 /* bf_middle_blocks for any entry oracle (the BlockView protocol, oracles.py:57-68):
  * the caller evaluates each block's side x side window K[i side + a, j side + b]
  * (host oracle.block(), or a device producer) and passes the windows stacked as

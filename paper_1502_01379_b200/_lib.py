@@ -39,6 +39,7 @@ SIGNATURES = [
     ("bf_timer_read", _I, [_P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(_U32), ctypes.POINTER(_U32)]),
     ("bf_middle_workspace_bytes", _U64, [_U64, _U32, _U32, _U32, _U32, _U32]),
     ("bf_middle_blocks", _I, [_I, _U64, _U32, _U32, _U32, _U32, _U32, _P, _U32, _P, _P, _P, _P, _P, _P, _U64, _P]),
+    ("bf_debug_node_trace", _I, [_P]),
     ("bf_middle_blocks_tiled", _I, [_U64, _U32, _U32, _U32, _U32, _U32, _P, _P, _U32, _P, _P, _P, _P, _P, _P, _U64,
                                     _P]),
     ("bf_probe_workspace_bytes", _U64, [_U64, _U32, _U32, _U32, _U32, _U32]),

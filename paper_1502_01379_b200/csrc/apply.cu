@@ -12,6 +12,7 @@
 
 #include "level_kernel.cuh"
 #include "pair_kernel.cuh"
+#include "node_mma.cuh"
 #include "plan.h"
 
 namespace bfly {
@@ -696,11 +697,203 @@ int run_up(const Plan& pl, const void* mid, E* bufs[2], void* out, uint32_t k, i
   return timed_op<E>(rec, pl, trail, 0, 0, src, out, k, 0, st);
 }
 
+// Node kernels (node_kernel.cuh): the whole down half and the whole up half as one
+// launch each, one CTA per (middle node, chunk of right-hand sides), for chains whose
+// factors sit in L2 (latency bound: BASELINE configs 0 and 1). BF_NO_NODE=1 turns them
+// off; BF_NODE=1 uses them whenever the node vector fits shared memory.
+struct NodeCfg {
+  bool mma, pf;
+  uint32_t kc, nch, vld, threads;
+  int nt;
+  size_t smem;
+  uint32_t ksplit = 1;
+  bool xstage = false;
+  NodeStage stage{};
+};
+
+// Padded row stride (complex values, >= len) for staged factor rows so that one phase of
+// a DMMA A fragment (lanes 0-7: k = lane & 3, m = lane >> 2) touches 8 distinct 16-byte
+// bank groups: `rows_k` = the fragment's k index walks rows (adjoint steps), else columns.
+uint32_t conflict_free_ld(uint32_t len, bool rows_k) {
+  uint32_t best = len, best_conf = 99;
+  for (uint32_t ld = len; ld < len + 8; ++ld) {
+    uint32_t used[8], conf = 0;
+    for (int l = 0; l < 8; ++l) {
+      const uint32_t k = l & 3, m = l >> 2;
+      const uint32_t e = rows_k ? k * ld + m : m * ld + k;
+      used[l] = (e * 4) % 32;
+      for (int j = 0; j < l; ++j)
+        if (used[j] == used[l]) ++conf;
+    }
+    if (conf < best_conf) {
+      best_conf = conf;
+      best = ld;
+    }
+    if (!conf) break;
+  }
+  return best;
+}
+
+constexpr int kNodeMaxGroups = 4;   // staged groups per in-place step (registers: one item per warp each)
+
+constexpr int kNodeMaxIt = 4;       // deferred DMMA items per warp (16 warps)
+constexpr int kNodeMaxOut = 2;      // deferred FMA outputs per thread group (compact code: i-cache)
+constexpr uint64_t kNodeMaxFactorBytes = 512ull << 20;
+
+// Shared memory of a node CTA: mbarriers, the node vector, and (pf) every step's slab.
+size_t node_smem(const Plan& pl, uint32_t vld, bool pf) {
+  const uint64_t NL = 1ull << pl.nlev, R = pl.rank;
+  const uint64_t vbytes = (NL * R * vld * sizeof(double2) + 127) & ~127ull;
+  const uint64_t slabs = (NL * pl.leaf_n0 * R + pl.nlev * NL * 2 * R * R) * sizeof(double2);
+  return 256 + vbytes + (pf ? slabs : 0);
+}
+
+bool node_config(const Plan& pl, uint32_t k, NodeCfg* nc) {
+  static const int mode = env_int("BF_NO_NODE", 0) ? -1 : env_int("BF_NODE", 0);
+  if (mode < 0 || pl.dtype != BF_C128 || pl.branch != 2 || pl.nparts != 1 || !pl.leaf_n0) return false;
+  if (pl.nlev != pl.half || pl.nlev == 0 || pl.nlev > static_cast<uint32_t>(kNodeMaxLev)) return false;
+  for (const LevelGeo& lg : pl.lev)
+    if (!lg.splits) return false;
+  if (mode == 0 && pl.base_bytes > kNodeMaxFactorBytes) return false;
+  const uint64_t NL = 1ull << pl.nlev, rows = NL * pl.rank, R = pl.rank;
+  if (NL != pl.m) return false;
+  const size_t cap = static_cast<size_t>(kMaxDynSmem);
+  if (k >= 8) {
+    // staged many-RHS kernel (node_mma.cuh): vector + two staging halves of factor groups.
+    // Opt-in (BF_NODE_MMA=1): at cfg1 (64 RHS) it measures 398 us per apply against 264 us for
+    // the level / pair kernels — each CTA's groups are too small to cover the staging latency
+    // with two halves next to a 147 KB node vector.
+    static const bool mma_on = env_int("BF_NODE_MMA", 0) != 0;
+    if (!mma_on) return false;
+    const uint32_t n0 = pl.leaf_n0;
+    NodeStage sg{};
+    sg.lda_dn = conflict_free_ld(2 * R, true);
+    sg.lda_up = conflict_free_ld(2 * R, false);
+    sg.lda_ldn = conflict_free_ld(R, true);
+    sg.lda_lup = conflict_free_ld(R, false);
+    uint64_t gu = 1;
+    while ((NL / 2) / gu > static_cast<uint64_t>(kNodeMaxGroups)) gu <<= 1;
+    for (uint32_t kc : {16u, 8u}) {
+      const int nt = kc / 8;
+      // one DMMA item per warp and group in the in-place steps (16 warps)
+      if (gu * ((2 * R + 7) / 8) > 16 || 2 * gu * ((R + 7) / 8) > 16) return false;
+      const uint32_t vld = kc + 2;
+      const uint64_t vbytes = (rows * vld * sizeof(double2) + 127) & ~127ull;
+      const uint64_t lev_elems = 2 * gu * R * std::max(sg.lda_dn, sg.lda_up);
+      const uint64_t avail = cap - 256 - vbytes;
+      if (avail < 2 * lev_elems * sizeof(double2)) continue;
+      const uint64_t half = std::min<uint64_t>(avail / 2 / sizeof(double2), 1ull << 20) & ~7ull;
+      if (half < lev_elems) continue;
+      uint64_t gl_dn = NL, gl_up = NL;
+      while (gl_dn > 1 && gl_dn * n0 * sg.lda_ldn > half) gl_dn >>= 1;
+      while (gl_up > 1 && gl_up * n0 * sg.lda_lup > half) gl_up >>= 1;
+      if (gl_dn * n0 * sg.lda_ldn > half || gl_up * n0 * sg.lda_lup > half) continue;
+      sg.half_elems = static_cast<uint32_t>(half);
+      sg.gu = static_cast<uint32_t>(gu);
+      sg.gl_dn = static_cast<uint32_t>(gl_dn);
+      sg.gl_up = static_cast<uint32_t>(gl_up);
+      NodeCfg c{true, false, kc, (k + kc - 1) / kc, vld, 512, nt, 256 + vbytes + 2 * half * sizeof(double2)};
+      c.stage = sg;
+      *nc = c;
+      return true;
+    }
+    return false;
+  }
+  const uint64_t outs = rows * k;
+  // split each dot product over ks threads while the CTA stays <= 512 threads
+  uint32_t ks = 8;
+  while (ks > 1 && outs * ks > 512) ks >>= 1;
+  const uint64_t groups = std::min<uint64_t>(512 / ks, outs);
+  if ((outs + groups - 1) / groups > static_cast<uint64_t>(kNodeMaxOut)) return false;
+  const uint32_t threads = static_cast<uint32_t>(std::max<uint64_t>(64, ((groups * ks + 31) / 32) * 32));
+  for (bool pf : {true, false}) {
+    size_t smem = node_smem(pl, k, pf);
+    if (smem > cap || (!pf && smem > 200 * 1024)) continue;
+    NodeCfg c{false, pf, k, 1, k, threads, 1, smem};
+    c.ksplit = ks;
+    const size_t xbytes = static_cast<size_t>(pl.side) * k * sizeof(double2);
+    if (pf && smem + xbytes <= cap) {
+      c.xstage = true;
+      c.smem = smem + xbytes;
+    }
+    *nc = c;
+    return true;
+  }
+  return false;
+}
+
+template <int UP>
+void* node_kernel_for(const NodeCfg& nc) {
+  if (nc.mma) return nc.nt == 2 ? (void*)node_mma_kernel<UP, 2, kNodeMaxGroups> : (void*)node_mma_kernel<UP, 1, kNodeMaxGroups>;
+  return nc.pf ? (void*)node_kernel<UP, false, 1, kNodeMaxOut, true> : (void*)node_kernel<UP, false, 1, kNodeMaxOut, false>;
+}
+
+// Diagnostics: when set (bf_debug_node_trace), node kernels stamp %globaltimer per CTA:
+// down half into [0, m nch x 32), up half after it.
+unsigned long long* g_node_trace = nullptr;
+
+int launch_node(const Plan& pl, int up, int adjoint, const void* in, void* out, uint32_t k, const NodeCfg& nc,
+                cudaStream_t st) {
+  NodeArgs a{};
+  const bool fwd_leaf_v = (up == 0) != (adjoint != 0);   // down of the forward chain / up of the adjoint: V
+  a.leaf = static_cast<const double2*>(fwd_leaf_v ? pl.v_leaf : pl.u_leaf);
+  const bool h_side = fwd_leaf_v;
+  for (uint32_t i = 0; i < pl.nlev; ++i)
+    a.lev[i] = static_cast<const double2*>(h_side ? pl.h_lev[i] : pl.g_lev[i]);
+  a.in = static_cast<const double2*>(in);
+  a.out = static_cast<double2*>(out);
+  a.mid_w = static_cast<const double*>(pl.weights);
+  a.n0 = pl.leaf_n0;
+  a.r = pl.rank;
+  a.D = pl.nlev;
+  a.k = k;
+  a.kc = nc.kc;
+  a.nch = nc.nch;
+  a.vld = nc.vld;
+  a.ksplit = nc.ksplit;
+  a.xstage = up ? 0 : nc.xstage;
+  a.remap = adjoint ? 2 : 1;
+  a.trace = g_node_trace ? g_node_trace + (up ? static_cast<size_t>(pl.m) * nc.nch * 32 : 0) : nullptr;
+  void* kp = up ? node_kernel_for<1>(nc) : node_kernel_for<0>(nc);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pl.m * nc.nch);
+  cfg.blockDim = dim3(nc.threads);
+  cfg.dynamicSmemBytes = nc.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (nc.mma) {
+    auto* kern = reinterpret_cast<void (*)(const NodeArgs, const NodeStage)>(kp);
+    BF_CUDA(allow_max_dyn_smem(kern));
+    BF_CUDA(cudaLaunchKernelEx(&cfg, kern, a, nc.stage));
+  } else {
+    auto* kern = reinterpret_cast<void (*)(const NodeArgs)>(kp);
+    BF_CUDA(allow_max_dyn_smem(kern));
+    BF_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  }
+  return 0;
+}
+
 template <typename E>
 int chain(const Plan& pl, const void* in, void* out, uint32_t k, int adjoint, void* ws, cudaStream_t st,
           LaunchRecorder* rec) {
   const uint64_t dk = pl.dim_max * k;
   E* bufs[2] = {static_cast<E*>(ws), static_cast<E*>(ws) + dk};
+  if constexpr (std::is_same<E, double2>::value) {
+    NodeCfg nc{};
+    if (node_config(pl, k, &nc)) {
+      int rc = rec ? rec->before(st) : 0;
+      if (!rc) rc = launch_node(pl, 0, adjoint, in, bufs[0], k, nc, st);
+      if (!rc && rec) rc = rec->after(st);
+      if (!rc && rec) rc = rec->before(st);
+      if (!rc) rc = launch_node(pl, 1, adjoint, bufs[0], out, k, nc, st);
+      if (!rc && rec) rc = rec->after(st);
+      return rc;
+    }
+  }
   const void* mid = nullptr;
   int rc = run_down<E>(pl, in, bufs, nullptr, k, adjoint, adjoint ? 2 : 1, st, rec, &mid);
   if (rc) return rc;
@@ -755,6 +948,11 @@ __global__ void unpack_kernel(const E* __restrict__ recv, E* __restrict__ out, u
 }
 
 }  // namespace
+
+extern "C" int bf_debug_node_trace(unsigned long long* dev_buf) {
+  g_node_trace = dev_buf;
+  return 0;
+}
 
 int plan_apply(const Plan& pl, const void* in, void* out, uint32_t k, int adjoint, void* ws, cudaStream_t st,
                LaunchRecorder* rec) {
