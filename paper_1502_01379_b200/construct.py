@@ -21,9 +21,7 @@ reference (pkg/tests/test_construct.py:197-202).
 from __future__ import annotations
 
 import ctypes
-import multiprocessing
 import os
-from concurrent.futures import ProcessPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -58,29 +56,27 @@ DEFAULT_PARAMS = OversamplingParams()
 _draws_for = draws_for
 
 
-def _draw_context():
-    ctx = multiprocessing.get_context("forkserver")
-    ctx.set_forkserver_preload(["paper_1502_01379_b200._draws"])
-    return ctx
-
-
 def draw_tables(seed, side: int, r: int, params: OversamplingParams, blocks) -> np.ndarray:
     """The reference's per-block rng.choice draws, in consumption order."""
     rqs = min(r * params.q, side)
     blocks = list(blocks)
     if len(blocks) < 2048:
         return _draws_for((seed, side, rqs, params.iters, blocks))
+    # large tables: a fresh helper interpreter (NumPy only) forks its own workers, so this
+    # CUDA-initialised, multi-threaded process is never forked (see _draws.py)
+    import pickle
+    import subprocess
+    import sys
     workers = min(16, os.cpu_count() or 1)
-    chunks = [blocks[k::workers] for k in range(workers)]
-    # workers fork from a fresh forkserver process that has imported only NumPy and
-    # _draws (never torch or CUDA): forking this CUDA-initialised, multi-threaded process
-    # itself could deadlock a worker on a lock some other thread held at fork time
-    with ProcessPoolExecutor(workers, mp_context=_draw_context()) as ex:
-        parts = list(ex.map(_draws_for, [(seed, side, rqs, params.iters, c) for c in chunks]))
-    out = np.empty((len(blocks), 2 * (params.iters + 1), rqs), dtype=np.int32)
-    for k, part in enumerate(parts):
-        out[k::workers] = part
-    return out
+    arr = np.asarray(blocks, dtype=np.int64).reshape(-1, 2)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {**os.environ, "PYTHONPATH": root + os.pathsep + os.environ.get("PYTHONPATH", "")}
+    res = subprocess.run([sys.executable, "-m", "paper_1502_01379_b200._draws"],
+                         input=pickle.dumps((seed, side, rqs, params.iters, arr, workers)),
+                         capture_output=True, env=env, check=False)
+    if res.returncode != 0:
+        raise RuntimeError("draw-table helper failed: " + res.stderr.decode(errors="replace")[-2000:])
+    return np.frombuffer(res.stdout, dtype=np.int32).reshape(len(blocks), 2 * (params.iters + 1), rqs).copy()
 
 
 class _DeviceOracle:

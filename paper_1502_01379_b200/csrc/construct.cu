@@ -385,8 +385,16 @@ __global__ void k_fill_tall(MidArgs a, int which, int use_piv, double2* dst_base
 // summation order; the first pick is therefore bitwise the reference's.
 // Past the numerical rank both this and the reference pick rounding noise.
 constexpr int kGramChunk = 32;
+constexpr int kGramTiles = 3;     // 8 x 8 Gram tiles per warp and pass (64 columns: 36 tiles, 16 warps)
+constexpr int kPivotTallThreads = 512;
 
-__global__ void __launch_bounds__(1024) k_pivot_tall(MidArgs a, int which) {
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kPivotTallThreads) k_pivot_tall(MidArgs a, int which) {
   extern __shared__ double2 tsm[];
   __shared__ double norms[kSetCap];
   __shared__ int picks[kSetCap];
@@ -404,36 +412,40 @@ __global__ void __launch_bounds__(1024) k_pivot_tall(MidArgs a, int which) {
     // probe products in matvec mode), pairwise for the F-ordered entry(rows, all)^H
     norms[c] = (which == kCols || a.probe_w > 0) ? sequential_sum(get, side) : pairwise_sum(get, 0, side);
   }
-  double2* chunk = tsm;                                           // kGramChunk x S
+  const int Sp = S + 2;   // chunk row stride: a DMMA fragment's 4 k-rows land on distinct banks
+  double2* chunk = tsm;                                           // kGramChunk x Sp
   const int64_t SS = static_cast<int64_t>(S) * S;
   double2* gscr = a.scr + static_cast<int64_t>(blockIdx.x) * 9 * SS;
-  double2* G = S <= kSmemSet ? tsm + kGramChunk * S : gscr;       // S x S
+  double2* G = S <= kSmemSet ? tsm + kGramChunk * Sp : gscr;      // S x S
   double2* Rm = S <= kSmemSet ? G + SS : gscr + SS;               // picks x S
-  // ---- Gram matrix: TB x TB register tiles over the upper block triangle, mirrored at the
-  // end. 2 x 2 tiles (528 for 64 columns) keep a 1024-thread CTA busy; each element is
-  // still one thread's sequential sum over the rows.
-  constexpr int TB = 2;
-  const int ncb = (nc + TB - 1) / TB;
-  const int ntiles = ncb * (ncb + 1) / 2;
-  for (int tile0 = 0; tile0 < ntiles; tile0 += blockDim.x) {
-    const int tid = tile0 + threadIdx.x;
-    int ta = 0, rem = tid;
-    if (tid < ntiles)
-      while (rem >= ncb - ta) {
-        rem -= ncb - ta;
+  // ---- Gram matrix T^H T on the FP64 tensor pipe (mma.sync m8n8k4, DMMA): 8 x 8 tiles of
+  // the upper block triangle, up to kGramTiles per warp, accumulated over row chunks
+  // staged through registers one chunk ahead (the next chunk's global loads are in
+  // flight while this one is multiplied); complex products in the 3-multiplication form
+  // (T1 = Re a Re b, T2 = Im a' Im b, T3 = (Re + Im a')(Re + Im b), a' = conj(a)).
+  const int nct = (nc + 7) / 8;
+  const int ntiles = nct * (nct + 1) / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int lr = lane >> 2, lk = lane & 3;
+  for (int tbase = 0; tbase < ntiles; tbase += nw * kGramTiles) {
+  int tta[kGramTiles], ttb[kGramTiles];
+#pragma unroll
+  for (int q = 0; q < kGramTiles; ++q) {
+    int rem = tbase + warp + q * nw, ta = 0;
+    if (rem < ntiles)
+      while (rem >= nct - ta) {
+        rem -= nct - ta;
         ++ta;
       }
-    const int tb = ta + rem;
-    double2 acc[TB][TB];
+    tta[q] = rem < ntiles ? ta : -1;
+    ttb[q] = ta + rem;
+  }
+  double t1[kGramTiles][2], t2[kGramTiles][2], t3[kGramTiles][2];
 #pragma unroll
-    for (int u = 0; u < TB; ++u)
-#pragma unroll
-      for (int v = 0; v < TB; ++v) acc[u][v] = make_double2(0, 0);
-    // row chunks staged through registers one chunk ahead: the next chunk's global loads
-    // are in flight while this one is multiplied (the staging latency was the kernel's
-    // main stall: 60% of samples at the chunk barrier)
-    constexpr int kPre = (kSetCap * kGramChunk + 1023) / 1024;
-    const int nel = ncb * TB * kGramChunk;
+  for (int q = 0; q < kGramTiles; ++q) t1[q][0] = t1[q][1] = t2[q][0] = t2[q][1] = t3[q][0] = t3[q][1] = 0;
+  {
+    constexpr int kPre = (kSetCap * kGramChunk + kPivotTallThreads - 1) / kPivotTallThreads;
+    const int nel = nct * 8 * kGramChunk;
     double2 pre[kPre];
     auto fetch = [&](int r0) {
 #pragma unroll
@@ -446,46 +458,43 @@ __global__ void __launch_bounds__(1024) k_pivot_tall(MidArgs a, int which) {
     };
     fetch(0);
     for (int r0 = 0; r0 < side; r0 += kGramChunk) {
-      const int rows = min(kGramChunk, side - r0);
       __syncthreads();
 #pragma unroll
       for (int q = 0; q < kPre; ++q) {
         const int x = threadIdx.x + q * static_cast<int>(blockDim.x);
-        if (x < nel) chunk[(x % kGramChunk) * S + x / kGramChunk] = pre[q];
+        if (x < nel) chunk[(x % kGramChunk) * Sp + x / kGramChunk] = pre[q];
       }
       __syncthreads();
       if (r0 + kGramChunk < side) fetch(r0 + kGramChunk);
-      if (tid < ntiles)
-        for (int i = 0; i < rows; ++i) {
-          double2 xa[TB], xb[TB];
+#pragma unroll 2
+      for (int k0 = 0; k0 < kGramChunk; k0 += 4) {
+        const double2* row = chunk + (k0 + lk) * Sp + lr;
 #pragma unroll
-          for (int u = 0; u < TB; ++u) {
-            xa[u] = chunk[i * S + TB * ta + u];
-            xb[u] = chunk[i * S + TB * tb + u];
-          }
-#pragma unroll
-          for (int u = 0; u < TB; ++u)
-#pragma unroll
-            for (int v = 0; v < TB; ++v) {
-              const double2 g = cmulc(xa[u], xb[v]);
-              acc[u][v].x += g.x;
-              acc[u][v].y += g.y;
-            }
+        for (int q = 0; q < kGramTiles; ++q) {
+          if (tta[q] < 0) break;
+          const double2 av = row[tta[q] * 8], bv = row[ttb[q] * 8];
+          const double ar = av.x, ai = -av.y;
+          dmma_f64(t1[q][0], t1[q][1], ar, bv.x);
+          dmma_f64(t2[q][0], t2[q][1], ai, bv.y);
+          dmma_f64(t3[q][0], t3[q][1], ar + ai, bv.x + bv.y);
         }
-    }
-    if (tid < ntiles) {
-#pragma unroll
-      for (int u = 0; u < TB; ++u)
-#pragma unroll
-        for (int v = 0; v < TB; ++v) {
-          const int ra = TB * ta + u, cb = TB * tb + v;
-          if (ra < nc && cb < nc && ra <= cb) {
-            G[ra * S + cb] = acc[u][v];
-            G[cb * S + ra] = cconj(acc[u][v]);
-          }
-        }
+      }
     }
   }
+#pragma unroll
+  for (int q = 0; q < kGramTiles; ++q) {
+    if (tta[q] < 0) break;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int ra = tta[q] * 8 + lr, cb = ttb[q] * 8 + 2 * lk + h;
+      const double2 g = make_double2(t1[q][h] - t2[q][h], t3[q][h] - t1[q][h] - t2[q][h]);
+      if (ra < nc && cb < nc && (tta[q] < ttb[q] || ra <= cb)) {
+        G[ra * S + cb] = g;
+        G[cb * S + ra] = cconj(g);
+      }
+    }
+  }
+  }   // tile batches
   __syncthreads();
   // ---- pivoted Cholesky recurrence == the greedy Gram-Schmidt pivoting
   // sampling mode: k = min(width, side), rel_tol = BASIS_TRIM (lowrank.py:252-256);
@@ -1602,11 +1611,11 @@ static int middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t br
     }
     k_union<<<nblocks, 128, 0, st>>>(a, 2 * iters, kRows);
     k_union<<<nblocks, 128, 0, st>>>(a, 2 * iters + 1, kCols);
-    const size_t tall_smem = (static_cast<size_t>(kGramChunk) * S + (S <= kSmemSet ? 2ull * S * S : 0)) * 16;
+    const size_t tall_smem = (static_cast<size_t>(kGramChunk) * (S + 2) + (S <= kSmemSet ? 2ull * S * S : 0)) * 16;
     BF_CUDA(allow_max_dyn_smem(k_pivot_tall));
     for (int which : {kCols, kRows}) {
       k_fill_tall<<<dim3(nblocks, yfill), T, 0, st>>>(a, which, 0, a.tall);
-      k_pivot_tall<<<nblocks, 1024, tall_smem, st>>>(a, which);
+      k_pivot_tall<<<nblocks, kPivotTallThreads, tall_smem, st>>>(a, which);
       k_fill_tall<<<dim3(nblocks, yfill), T, 0, st>>>(a, which, 1, which == kCols ? a.qc : a.qr);
       launch_basis(a, nblocks, which, st);
     }
@@ -1670,13 +1679,13 @@ int bf_middle_probes(uint64_t n, uint32_t levels, uint32_t branching, uint32_t r
   const int T = 256;
   const unsigned yfill = static_cast<unsigned>(std::min<uint64_t>(64, (width * side + T - 1) / T));
   const size_t small_smem = S <= kSmemSet ? 3ull * S * S * sizeof(double2) : 0;
-  const size_t tall_smem = (static_cast<size_t>(kGramChunk) * S + (S <= kSmemSet ? 2ull * S * S : 0)) * 16;
+  const size_t tall_smem = (static_cast<size_t>(kGramChunk) * (S + 2) + (S <= kSmemSet ? 2ull * S * S : 0)) * 16;
   BF_CUDA(allow_max_dyn_smem(k_mid_probe));
   BF_CUDA(allow_max_dyn_smem(k_pivot_tall));
   k_init<<<(nblocks + 127) / 128, 128, 0, st>>>(a, block_ij);
   for (int which : {kCols, kRows}) {
     k_fill_probe<<<dim3(nblocks, yfill), T, 0, st>>>(a, which);
-    k_pivot_tall<<<nblocks, 1024, tall_smem, st>>>(a, which);
+    k_pivot_tall<<<nblocks, kPivotTallThreads, tall_smem, st>>>(a, which);
     k_sel_probe<<<dim3(nblocks, yfill), T, 0, st>>>(a, which);
   }
   k_set_probe_counts<<<(nblocks + 127) / 128, 128, 0, st>>>(a);

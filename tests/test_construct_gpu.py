@@ -79,10 +79,12 @@ def _block_product(u, s, v):
 @pytest.mark.parametrize("name,tol_med,tol_max", [
     ("construct_fio_n128_r4_leaf025.npz", 1e-14, 1e-14),   # dense branch (r q >= side): measured 9e-16
     ("construct_fio_n1024_r8_leaf1.npz", 1e-12, 1e-11),    # sampling, accurate leaf: measured 2e-13 / 1.7e-12
-    # config 0 geometry: measured 9e-13 / 1.0e-7 / 1.8e-12; the 1e-7 block (2, 5) moves by
-    # 1e-8 in the reference itself under 1e-15 entry noise — per-block envelopes for all 64
-    # cfg0 blocks: test_config_parity_gpu.py::test_config_blocks_vs_reference_traces
-    ("construct_fio_n1024_r12_leaf8.npz", 1e-11, 1e-6),
+    # config 0 geometry: measured 4.9e-13 / 5.2e-8 / 4.1e-11 (DMMA Gram; 9e-13 / 1.0e-7 /
+    # 1.8e-12 with the earlier DFMA Gram). All three blocks' basis pivots move in the
+    # reference itself under 1e-15 entry noise (d_ref 1.5e-9 / 9.8e-9 / 3.5e-12), so these
+    # fixed bounds only catch gross errors; the contract is the per-block calibrated envelope
+    # over all 64 cfg0 blocks: test_config_parity_gpu.py::test_config_blocks_vs_reference_traces
+    ("construct_fio_n1024_r12_leaf8.npz", 1e-10, 1e-6),
 ])
 def test_middle_blocks_vs_reference_traces(name, tol_med, tol_max):
     d = golden(name)
