@@ -643,7 +643,7 @@ def run_sharded(args, world, rank, local):
 def _ncu_traffic(config, dtype, k):
     """dram__bytes_read.sum + dram__bytes_write.sum per level-kernel launch from the committed
     `ncu --set full` capture of this workload (profiles/r01_level_kernel_traffic.json), else None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_level_kernel_traffic.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_level_kernel_traffic.json")
     if (config, dtype, k) != ("cfg2", "c128", 1) or not os.path.exists(path):
         return None
     with open(path) as fh:
