@@ -229,7 +229,7 @@ bool pdl_enabled() {
 template <typename E>
 int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint32_t ntot, uint32_t t0,
                    int accumulate, uint64_t P, uint64_t units, const void* in, void* out, uint32_t k, int adjoint,
-                   int remap, cudaStream_t st, void* const* peers);
+                   int remap, cudaStream_t st, void* const* peers, uint32_t tsplit = 1);
 
 // One factor launch. A unit's nt blocks normally share one tile; when they do
 // not fit a shared-memory stage (quadtree rank 25: 4 x 25 x 100 complex128 =
@@ -240,6 +240,16 @@ int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32
                  const void* in, void* out, uint32_t k, int adjoint, int remap, cudaStream_t st,
                  void* const* peers = nullptr) {
   const Shape sh = k >= kMrhsMinK ? mrhs_shape_for<E>(C) : stream_shape<E>();
+  // wide many-RHS forward levels (quadtree r = 25: a unit is 160 KB of blocks), opt-in
+  // BF_WIDE_SPLIT=1: the two t-halves of every unit as consecutive tiles of ONE launch
+  // through two ~113 KB stages (forward outputs of different t are disjoint). Measured
+  // slower than the single-buffered whole-unit stage (cfg3 0.595 vs 0.530 ms, cfg4b 11.5 vs
+  // 9.9 ms): the half-unit warp items, not the exposed loads, set the pace.
+  static const bool wide_split = env_int("BF_WIDE_SPLIT", 0) != 0;
+  if (wide_split && !adjoint && !remap && k >= kMrhsMinK && sizeof(E) == 16 && C > 64 && nt % 2 == 0 &&
+      static_cast<uint64_t>(nt / 2) * R * C + static_cast<uint64_t>(C) * std::min<uint32_t>(k, 16) <=
+          (static_cast<uint64_t>(kMaxDynSmem) - 1024) / 2 / sizeof(E))
+    return launch_level_t<E>(pl, fac, R, C, nt / 2, nt, 0, 0, P, units, in, out, k, adjoint, remap, st, peers, 2);
   uint32_t nt_tile = nt;
   auto tile_elems = [&](uint64_t t) { return t * R * C + (adjoint ? t * R : static_cast<uint64_t>(C)); };
   while (nt_tile > 1 && tile_elems(nt_tile) * sizeof(E) > sh.stage_bytes) nt_tile /= 2;
@@ -256,7 +266,7 @@ int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32
 template <typename E>
 int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint32_t ntot, uint32_t t0,
                    int accumulate, uint64_t P, uint64_t units, const void* in, void* out, uint32_t k, int adjoint,
-                   int remap, cudaStream_t st, void* const* peers) {
+                   int remap, cudaStream_t st, void* const* peers, uint32_t tsplit) {
   if (units >= (1ull << 31)) return fail(BF_EINVAL, "level has too many blocks for one launch");
   if (remap && static_cast<uint64_t>(pl.m) * pl.m * pl.rank >= (1ull << 32))
     return fail(BF_EINVAL, "middle vector too long for 32-bit remap indices");
@@ -265,6 +275,10 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   Shape sh = mrhs ? mrhs_shape_for<E>(C) : ks;
   const bool sexp = !mrhs && sizeof(E) == 16 && remap < 3 && stream_exp().on;
   if (sexp) sh = stream_exp().s;
+  if (tsplit > 1) {   // t-range tiles of one launch: double-buffered half-units
+    sh.stages = 2;
+    sh.stage_bytes = (static_cast<uint32_t>(kMaxDynSmem) - 1024) / 2;
+  }
   // complex128 DMMA consumers: 16 warps for the wide quadtree blocks (C = 4r = 100: long
   // k loops, few warp items per tile; cfg3 0.75 -> 0.59 ms, cfg4b 14.6 -> 11.0 ms), 8
   // otherwise (cfg2 k = 256: 43.9 vs 47.3 ms; cfg1 0.26 vs 0.32 ms)
@@ -336,7 +350,8 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
   a.kt = kt;
   a.ktiles = (k + kt - 1) / kt;
   a.lgU = ilog2(U);
-  a.ntiles = static_cast<uint32_t>((units / U) * a.ktiles);
+  a.tsplit = tsplit;
+  a.ntiles = static_cast<uint32_t>((units / U) * a.ktiles * tsplit);
   uint64_t stage = U * (fac_unit + vec_col * kt);
   if (stage & 1) ++stage;
   a.stage_elems = static_cast<uint32_t>(stage);
@@ -366,7 +381,7 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
     if (128 + sh.stages * padded(Up) * esz <= static_cast<uint64_t>(kMaxDynSmem)) {
       U = Up;
       a.lgU = ilog2(U);
-      a.ntiles = static_cast<uint32_t>((units / U) * a.ktiles);
+      a.ntiles = static_cast<uint32_t>((units / U) * a.ktiles * tsplit);
       a.fld = static_cast<uint32_t>(fld);
       a.vld = static_cast<uint32_t>(vld);
       uint64_t st2 = padded(U);

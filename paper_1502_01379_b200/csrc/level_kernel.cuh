@@ -68,6 +68,7 @@ struct LevelArgs {
   int dbg_nomath;     // BF_DBG_NOMATH=1 (diagnostics only): many-RHS consumers skip their k loops
   int dbg_noload;     // BF_DBG_NOLOAD=1 (diagnostics only): the producer moves no data (compute + stores only)
   int inplace;        // MRHS = 3: outputs overwrite the stage's vector rows (one warp item per warp)
+  uint32_t tsplit;    // forward levels: t-ranges of a unit as separate tiles of one launch (1 = off)
 };
 
 // remap 3/4 receive buffers of every part ([sender][own][other local][rho][k]); a
@@ -128,11 +129,18 @@ struct TileGeo {
   uint32_t seg_blocks;
   uint32_t seg0;      // first global block index of segment 0
   uint32_t seg_step;  // block distance between segments
+  uint32_t t0;        // first t of this tile's t-range
 };
 
 __device__ __forceinline__ TileGeo tile_geo(const LevelArgs& a, uint32_t tile) {
   TileGeo t;
   uint32_t ut = tile, kti = 0;
+  t.t0 = a.t0;
+  if (a.tsplit > 1) {   // forward levels: the t-ranges of a unit are consecutive tiles
+    const uint32_t ts = ut % a.tsplit;
+    ut /= a.tsplit;
+    t.t0 += ts * a.nt;
+  }
   if (a.ktiles > 1) {
     ut = tile / a.ktiles;
     kti = tile - ut * a.ktiles;
@@ -145,7 +153,7 @@ __device__ __forceinline__ TileGeo tile_geo(const LevelArgs& a, uint32_t tile) {
     t.lgPe = a.lgU;
     t.segs = a.nt;
     t.seg_blocks = 1u << a.lgU;
-    t.seg0 = ((g0 * a.ntot + a.t0) << a.lgP) + p0;
+    t.seg0 = ((g0 * a.ntot + t.t0) << a.lgP) + p0;
     t.seg_step = 1u << a.lgP;
   } else {
     t.lgPe = a.lgP;
@@ -305,7 +313,7 @@ __device__ __forceinline__ void consume_tile(const LevelArgs& a, const PeerArgs&
       }
       if (j < a.C) acc.mac(0, arow[c], x[static_cast<size_t>(c) * kc]);
       const uint32_t u = t.u0 + ul;
-      const uint32_t q = ((((u >> a.lgP) * a.ntot) + a.t0 + tt) << a.lgP) + (u & P_mask);
+      const uint32_t q = ((((u >> a.lgP) * a.ntot) + t.t0 + tt) << a.lgP) + (u & P_mask);
       out[(static_cast<size_t>(q) * a.R + rho) * a.k + t.k0 + kk] = acc.sum();
     }
   } else {
@@ -443,7 +451,7 @@ __device__ __forceinline__ void consume_tile_mrhs(const LevelArgs& a, const Peer
         const uint32_t o = rb + LR * i;
         if (o >= m_out) break;
         const uint32_t tt = o / a.R, rho = o - tt * a.R;
-        const uint32_t q = ((((u >> a.lgP) * a.ntot) + a.t0 + tt) << a.lgP) + (u & P_mask);
+        const uint32_t q = ((((u >> a.lgP) * a.ntot) + t.t0 + tt) << a.lgP) + (u & P_mask);
         E* dst = out + (static_cast<size_t>(q) * a.R + rho) * a.k + t.k0 + col0;
 #pragma unroll
         for (int j = 0; j < TN; ++j)
@@ -762,7 +770,7 @@ __device__ __forceinline__ void consume_tile_dmma(const LevelArgs& a, const Peer
       if (!a.adjoint) {
         const uint32_t u = t.u0 + ul;
         const uint32_t tt = m / a.R, rho = m - tt * a.R;
-        const uint32_t q = ((((u >> a.lgP) * a.ntot) + a.t0 + tt) << a.lgP) + (u & P_mask);
+        const uint32_t q = ((((u >> a.lgP) * a.ntot) + t.t0 + tt) << a.lgP) + (u & P_mask);
         orow = out + (static_cast<size_t>(q) * a.R + rho) * a.k + t.k0;
       } else if (a.remap >= 3) {
         orow = remap_row<double2, PUSH>(a, pa, static_cast<size_t>(t.u0 + ul) * a.C + m, &w) + t.k0;
@@ -861,7 +869,7 @@ __device__ __forceinline__ void store_tile_rows(const LevelArgs& a, const PeerAr
     if (!a.adjoint) {
       const uint32_t u = t.u0 + ul;
       const uint32_t tt = m / a.R, rho = m - tt * a.R;
-      const uint32_t q = ((((u >> a.lgP) * a.ntot) + a.t0 + tt) << a.lgP) + (u & P_mask);
+      const uint32_t q = ((((u >> a.lgP) * a.ntot) + t.t0 + tt) << a.lgP) + (u & P_mask);
       dst = out + (static_cast<size_t>(q) * a.R + rho) * a.k + t.k0;
     } else {
       typename Cx<E>::R w;
