@@ -182,14 +182,18 @@ class MiddleSampler:
         u = torch.empty((nb, side, r), dtype=torch.complex128, device="cuda")
         v = torch.empty_like(u)
         w = torch.empty((nb, r), dtype=torch.float64, device="cuda")
-        ij_d = torch.from_numpy(np.ascontiguousarray(ij)).cuda()
+        def upload(arr):   # pinned + non-blocking: the host never waits for queued kernels
+            return torch.from_numpy(np.ascontiguousarray(arr)).pin_memory().cuda(non_blocking=True)
+
+        ij_d = upload(ij)
         if self.dense_branch:
             draws_d = None
         elif self._all_draws is not None:
             idx = (ij[:, 0] - self._row0) * self.m + ij[:, 1]
-            draws_d = torch.from_numpy(np.ascontiguousarray(self._all_draws[idx])).cuda()
+            draws_d = upload(self._all_draws[idx])
         else:
-            draws_d = torch.from_numpy(draw_tables(self.seed, side, r, self.params, ij.tolist())).cuda()
+            # this batch's draws on the host while the device still runs the previous batch
+            draws_d = upload(draw_tables(self.seed, side, r, self.params, ij.tolist()))
         wsb = int(self.lib.bf_middle_workspace_bytes(self.p.n, self.p.levels, self.branching, r, self.params.q, nb))
         if wsb == 0:
             raise ValueError("geometry/rank not supported by the batched sampling kernels (need r*(q+1) <= 128)")
@@ -481,9 +485,9 @@ def factorize(oracle, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0,
         u_h, middle, v_h = middle_factorization_matvec(oracle, p, r, params, seed)
         (u_outer, g_chain), (v_outer, h_chain) = (_recurse_full(u_h, p, r), _recurse_full(v_h, p, r))
         return ButterflyFactors(p, r, u_outer, g_chain, middle, h_chain, v_outer)
+    # each batch draws its own tables on the host (draw_tables) while the device works on
+    # the previous batch: the ~4 s of NumPy draws at cfg2 stay off the critical path
     ms = MiddleSampler(oracle, p, r, params, seed)
-    if ms.m * ms.m >= 1024:
-        ms.prepare_draws()
     m, side = ms.m, ms.side
     shapes, leaf_shape = level_geometry(p, r)
     weights = torch.zeros((m, m, r), dtype=torch.float64, device="cuda")

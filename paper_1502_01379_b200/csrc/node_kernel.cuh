@@ -294,6 +294,7 @@ __device__ __forceinline__ void node_step_fma(const NodeArgs& a, const NodeCtx& 
       const int o = valid ? o0 : 0;
       const int q = o / (M * nc), rest = o - q * M * nc, m = rest / nc, n = rest - m * nc;
       double2 acc = make_double2(0, 0);
+      if constexpr (STORE == kStoreDeferred) node_stamp(a, 26);
       if (valid) {
         for (int sg = 0; sg < nseg; ++sg) {
           const double2* ap;
@@ -309,10 +310,12 @@ __device__ __forceinline__ void node_step_fma(const NodeArgs& a, const NodeCtx& 
           }
         }
       }
+      if constexpr (STORE == kStoreDeferred) node_stamp(a, 27);
       for (int w = KS >> 1; w > 0; w >>= 1) {
         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, w);
         acc.y += __shfl_xor_sync(0xffffffffu, acc.y, w);
       }
+      if constexpr (STORE == kStoreDeferred) node_stamp(a, 28);
       if constexpr (STORE == kStoreDeferred) res[s] = acc;
       else if (valid && sub == 0) node_store<KIND, STORE>(a, c, q, m, n, acc);
     }

@@ -38,7 +38,8 @@ for spec in sys.argv[1:]:
         print(f"{spec} {name}: stamps (us from down start), CTA median / max")
         print("   ", " ".join(f"{i}:{np.nanmedian(rel[:, i]):.2f}/{np.nanmax(rel[:, i]):.2f}"
                                for i in range(23) if not np.all(np.isnan(rel[:, i]))))
-        cyc = t[half, :ctas, 23:26].astype(np.int64)
+        cyc = t[half, :ctas, 23:29].astype(np.int64)
         if cyc[:, 0].any():
-            print("    last deferred step, SM cycles (CTA median): compute", int(np.median(cyc[:, 1] - cyc[:, 0])),
-                  "barrier", int(np.median(cyc[:, 2] - cyc[:, 1])))
+            med = lambda j, i: int(np.median(cyc[:, j] - cyc[:, i]))  # noqa: E731
+            print("    last deferred step, SM cycles (CTA median): setup", med(3, 0), "dot loop", med(4, 3),
+                  "shuffles", med(5, 4), "to barrier", med(1, 5), "barrier", med(2, 1))
