@@ -13,6 +13,7 @@
 #include "level_kernel.cuh"
 #include "pair_kernel.cuh"
 #include "node_mma.cuh"
+#include "tc_kernel.cuh"
 #include "plan.h"
 
 namespace bfly {
@@ -152,6 +153,11 @@ Shape mrhs_shape_for(uint32_t C) {
 }
 constexpr uint32_t kMrhsMinK = 8;
 
+// Diagnostics: when set (bf_debug_node_trace), node kernels stamp %globaltimer per CTA
+// (down half into [0, m nch x 32), up half after it) and the tcgen05 level kernel its CTA
+// 0 tile phases (clock64).
+unsigned long long* g_node_trace = nullptr;
+
 using LevelKernel = void (*)(LevelArgs, PeerArgs);
 
 // complex128 3-multiplication DMMA kernels, one instantiation per warp tile (dt):
@@ -268,6 +274,60 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
                    int accumulate, uint64_t P, uint64_t units, const void* in, void* out, uint32_t k, int adjoint,
                    int remap, cudaStream_t st, void* const* peers, uint32_t tsplit) {
   if (units >= (1ull << 31)) return fail(BF_EINVAL, "level has too many blocks for one launch");
+  if constexpr (std::is_same<E, float2>::value) {
+    // complex64 with >= 128 right-hand sides on tcgen05 (kind::tf32, 3xTF32) tiles of 128 RHS
+    // (tc_kernel.cuh): opt-in BF_TC=1 — slower and less accurate than the FFMA consumer at the
+    // benchmark shapes (cfg2 256 RHS: 46.7 vs 29.4 ms, rel. error 7.7e-6 vs 6.1e-7)
+    static const bool tc_off = env_int("BF_TC", 0) == 0;
+    const uint32_t N = adjoint ? C : nt * R, K = adjoint ? nt * R : C, Kp = (K + 7) / 8 * 8;
+    const uint64_t tc_smem = 2 * 4ull * (128 + 2 * N) * Kp * 4 + static_cast<uint64_t>(K) * 128 * 8;
+    // (bulk copies: even k keeps every 128-RHS row segment 16-byte aligned and sized)
+    if (!tc_off && k >= 128 && k % 2 == 0 && remap < 3 && !accumulate && nt == ntot && N % 16 == 0 && N <= 128 &&
+        2 * N <= 256 && Kp <= 64 && (static_cast<uint64_t>(R) * C) % 2 == 0 &&
+        static_cast<uint64_t>(N) * (Kp / 4) <= static_cast<uint64_t>(kTcBItems) * kTcSplitWarps * 32 &&
+        tc_smem + 1024 <= static_cast<uint64_t>(kMaxDynSmem)) {
+      TcArgs a{};
+      a.fac = static_cast<const float2*>(fac);
+      a.in = static_cast<const float2*>(in);
+      a.out = static_cast<float2*>(out);
+      a.mid_w = static_cast<const float*>(pl.weights);
+      a.R = R;
+      a.C = C;
+      a.nt = nt;
+      a.lgP = ilog2(P);
+      a.units = static_cast<uint32_t>(units);
+      a.k = k;
+      a.ktiles = (k + 127) / 128;
+      a.N = N;
+      a.K = K;
+      a.Kp = Kp;
+      a.adjoint = adjoint;
+      a.remap = remap;
+      a.m = pl.m;
+      a.r = pl.rank;
+      uint32_t cols = 32;
+      while (cols < 4 * N) cols *= 2;   // two accumulators [Re | Im]
+      a.tmem_cols = cols;
+      a.trace = g_node_trace;
+      // tf32 planes + two raw tiles (X rows of 128 RHS, the unit's blocks)
+      const size_t smem = 2 * 4ull * (128 + 2 * N) * Kp * 4 + static_cast<uint64_t>(K) * 128 * 8;
+      BF_CUDA(allow_max_dyn_smem(tc_level_kernel));
+      const uint64_t ntiles = units * a.ktiles;
+      const uint32_t per_sm = 1;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(pl.sms) * per_sm)));
+      cfg.blockDim = dim3(kTcThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      BF_CUDA(cudaLaunchKernelEx(&cfg, tc_level_kernel, a));
+      return 0;
+    }
+  }
   if (remap && static_cast<uint64_t>(pl.m) * pl.m * pl.rank >= (1ull << 32))
     return fail(BF_EINVAL, "middle vector too long for 32-bit remap indices");
   const bool mrhs = k >= kMrhsMinK;
@@ -843,9 +903,6 @@ void* node_kernel_for(const NodeCfg& nc) {
   return nc.pf ? (void*)node_kernel<UP, false, 1, kNodeMaxOut, true> : (void*)node_kernel<UP, false, 1, kNodeMaxOut, false>;
 }
 
-// Diagnostics: when set (bf_debug_node_trace), node kernels stamp %globaltimer per CTA:
-// down half into [0, m nch x 32), up half after it.
-unsigned long long* g_node_trace = nullptr;
 
 int launch_node(const Plan& pl, int up, int adjoint, const void* in, void* out, uint32_t k, const NodeCfg& nc,
                 cudaStream_t st) {

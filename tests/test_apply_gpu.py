@@ -382,3 +382,38 @@ def test_many_rhs_shape_sweep(leaf):
                 want = ochain.apply(oc, g, adjoint=adj)
                 assert rel(f.plan().apply(gd, adjoint=adj), want) <= TOL128, (r, k, adj)
                 assert rel(f.plan("c64").apply(gd, adjoint=adj).to(torch.complex128), want) <= TOL64, (r, k, adj)
+
+
+def test_c64_tensor_core_levels():
+    """complex64 levels on tcgen05 (kind::tf32, 3xTF32 split, accumulators in TMEM;
+    csrc/tc_kernel.cuh), opt-in BF_TC=1, run in a subprocess with the switch set: forward
+    and adjoint within the c64 tolerance of the oracle, partial 128-RHS tiles, leaf and
+    transfer levels, the fused middle factor."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, sys
+sys.path.insert(0, ".")
+import paper_1502_01379_b200 as bf
+from oracle import chain as ochain
+from paper_1502_01379_b200.synthetic import synthetic_chain
+for n, leaf, r, k in [(1 << 12, 16, 16, 128), (1 << 14, 16, 8, 256), (1 << 12, 16, 16, 300), (1 << 12, 1, 4, 130),
+                      (1 << 12, 16, 16, 129)]:
+    p = bf.make_partition(n, leaf)
+    f = synthetic_chain(p, r, seed=n + r + k)
+    oc = ochain.Chain.from_reference(f)
+    rng = np.random.default_rng(k)
+    g = rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k))
+    plan = f.plan("c64")
+    for adj in (False, True):
+        got = plan.apply(torch.from_numpy(g).cuda(), adjoint=adj).to(torch.complex128).cpu().numpy()
+        want = ochain.apply(oc, g, adjoint=adj)
+        err = np.linalg.norm(got - want) / np.linalg.norm(want)
+        assert err <= 1e-5, (n, k, adj, err)
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                         env={**os.environ, "BF_TC": "1"})
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
