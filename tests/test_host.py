@@ -87,3 +87,12 @@ def test_synthetic_chain_is_seeded():
     a, b = synthetic_chain(p, 4, seed=5), synthetic_chain(p, 4, seed=5)
     assert bf.factors_equal(a, b)
     assert np.all((a.middle.weights >= 0.5) & (a.middle.weights <= 1.5))
+
+
+def test_oversampling_params_validate():
+    """lowrank.py:33-48 / reference test_lowrank.py:215-221."""
+    import pytest
+    for kw in ({"p": -1}, {"q": 0}, {"iters": 0}):
+        with pytest.raises(ValueError):
+            bf.OversamplingParams(**kw)
+    assert bf.OversamplingParams() == bf.OversamplingParams(p=5, q=3, iters=3)
