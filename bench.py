@@ -265,6 +265,16 @@ def companion_cfg(name, dtype, rhs, steps, warm, cols=1):
     ws = torch.empty(plan.workspace_bytes(k), dtype=torch.uint8, device="cuda")
     nsteps = max(3, min(steps, 20))
     ms = dev_time(lambda: plan.apply(g, out=out, workspace=ws), nsteps, max(3, warm))
+    graph_ms = None
+    if ms < 0.1:
+        # latency-bound chain: one host call per apply costs more than the device work, so
+        # also time 50 applies captured into one CUDA graph (device time per apply)
+        reps = 50
+        cg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(cg, capture_error_mode="thread_local"):
+            for _ in range(reps):
+                plan.apply(g, out=out, workspace=ws)
+        graph_ms = dev_time(cg.replay, 5, 2) / reps
     t0 = time.perf_counter()
     plan.apply(g_host, out=np.empty_like(g_host, dtype=plan.np_dtype))     # host buffers (pageable)
     e2e_ms = (time.perf_counter() - t0) * 1e3
@@ -275,6 +285,7 @@ def companion_cfg(name, dtype, rhs, steps, warm, cols=1):
     err = rel2(out[:, :cols].cpu().numpy().astype(np.complex128), want)
     res = {"workload": bench_config(name, kern, n, r, leaf, k, p, dtype)["workload"], "value": n * k / (ms / 1e3),
            "unit": "samples/s", "ms_per_step": ms, "steps": nsteps, "roofline": _rate(fh, k, esz, ms),
+           "device_ms_per_apply_graph": graph_ms,
            "rel_err": {"value": err, "columns": cols, "tolerance": 1e-11 if dtype == "c128" else 1e-5},
            "e2e_ms_one_call_pageable": e2e_ms,
            "cpu_reference": {"value": n * cols / t_cpu, "unit": "samples/s", "ms": t_cpu * 1e3, "k": cols,
@@ -846,6 +857,7 @@ def main():
                 also[name] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
             torch.cuda.empty_cache()
 
+        run("cfg0_k1", companion_cfg, "cfg0", "c128", 0, steps, warm)
         run("cfg1_k64", companion_cfg, "cfg1", "c128", 0, steps, warm)
         if args.dtype == "c128" and k == 1:
             run("cfg2_k256", companion_many_rhs, plan, f, n, steps, warm)
