@@ -636,8 +636,11 @@ def run_sharded(args, world, rank, local):
         run("cfg4b_strong", cfg4b)
         free = torch.tensor([torch.cuda.mem_get_info()[0]], device="cuda", dtype=torch.float64)
         dist.all_reduce(free, op=dist.ReduceOp.MIN)
-        # cfg4a: 180.5 GB of factors / N per GPU + ~6 vectors of 2^24 x 64 / N complex128
-        need = (180.5e9 + 6 * 17.2e9) / world
+        # cfg4a: 180.5 GB of factors / N per GPU, ~10 vector buffers of 2^24 x 64 / N complex128
+        # (input, middle, send, receive, unpacked, output, ...) and up to two full-length
+        # workspace vectors; skipped (on every rank alike) rather than risking one rank's OOM
+        # while the others wait in a collective
+        need = (180.5e9 + 10 * 17.2e9) / world + 2 * 17.2e9
         if world >= 2 and float(free.item()) > 1.1 * need:
             run("cfg4a_strong", lambda: measure_sharded("cfg4a", "c128", 64, False, world, rank, local,
                                                          max(3, min(steps, 5)), 2, args.exchange, e2e=False))
