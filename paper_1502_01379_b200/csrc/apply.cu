@@ -561,6 +561,7 @@ struct PairGeo {
   size_t smem;
   bool chunk;             // k-chunked kernel (factor blocks once per item, input rows in chunks)
   uint32_t kc, nch, stages;
+  uint32_t ctas = 1;      // whole-tile pair kernel: CTAs per SM
 };
 
 bool pair_geometry(const Plan& pl, int i, uint32_t k, int adjoint, PairGeo* pg) {
@@ -575,15 +576,33 @@ bool pair_geometry(const Plan& pl, int i, uint32_t k, int adjoint, PairGeo* pg) 
   const uint64_t fld = pad_to(C, adjoint ? 2 : 4);
   pg->fld = static_cast<uint32_t>(fld);
   pg->chunk = false;
-  if (k <= 256) {  // whole right-hand-side range per stage, double-buffered
-    const uint64_t vld = pad_to(k, 2);
-    uint64_t stage = 8 * R * fld + 2 * C * vld;
-    if (stage & 1) ++stage;
-    const uint64_t smem = 128 + (kPairStages * stage + 2 * C * vld) * sizeof(double2);
+  if (k <= 256) {  // whole right-hand-side range per stage (or k / 2 chunks), double-buffered
+    auto smem_for = [&](uint64_t kc, uint64_t* stage_out) {
+      const uint64_t vld = pad_to(kc, 2);
+      uint64_t stage = 8 * R * fld + 2 * C * vld;
+      if (stage & 1) ++stage;
+      *stage_out = stage;
+      return 128 + (kPairStages * stage + 2 * C * vld) * sizeof(double2);
+    };
+    // Right-hand-side chunks are independent items: halving the chunk lets two CTAs share an
+    // SM (18 warps instead of 9 to cover the DMMA and shared-memory latencies) at the cost of
+    // reading each pair's factor blocks once per chunk. BF_PAIR_KC overrides the chunk width.
+    static const int kc_env = env_int("BF_PAIR_KC", 0);
+    uint64_t kc = k, stage = 0;
+    if (kc_env > 0) {
+      kc = std::min<uint64_t>(k, static_cast<uint64_t>(kc_env));
+    } else if (2 * smem_for(k, &stage) > static_cast<uint64_t>(kMaxDynSmem) && k >= 64 &&
+               2 * smem_for((k + 1) / 2, &stage) <= static_cast<uint64_t>(kMaxDynSmem)) {
+      kc = (k + 1) / 2;
+    }
+    const uint64_t smem = smem_for(kc, &stage);
     if (smem <= static_cast<uint64_t>(kMaxDynSmem)) {
-      pg->vld = static_cast<uint32_t>(vld);
+      pg->vld = static_cast<uint32_t>(pad_to(kc, 2));
       pg->stage_elems = static_cast<uint32_t>(stage);
       pg->smem = smem;
+      pg->kc = static_cast<uint32_t>(kc);
+      pg->nch = static_cast<uint32_t>((k + kc - 1) / kc);
+      pg->ctas = 2 * smem <= static_cast<uint64_t>(kMaxDynSmem) ? 2 : 1;
       return true;
     }
   }
@@ -654,8 +673,10 @@ int launch_pair(const Plan& pl, const void* fac_a, const void* fac_b, int i, con
   a.ga = static_cast<uint32_t>(A.G);
   a.pa = static_cast<uint32_t>(A.P);
   a.k = k;
+  a.kc = pg.kc;
+  a.nch = pg.nch;
   a.adjoint = adjoint;
-  a.nitems = static_cast<uint32_t>(A.G * A.P / 2);
+  a.nitems = static_cast<uint32_t>(A.G * A.P / 2 * pg.nch);
   a.fld = pg.fld;
   a.vld = pg.vld;
   a.stage_elems = pg.stage_elems;
@@ -666,7 +687,7 @@ int launch_pair(const Plan& pl, const void* fac_a, const void* fac_b, int i, con
   auto* kern = gauss_disabled() ? pair_kernel<kPairStages, kPairNcw, false> : pair_kernel<kPairStages, kPairNcw, true>;
   BF_CUDA(allow_max_dyn_smem(kern));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(std::min<uint32_t>(a.nitems, static_cast<uint32_t>(pl.sms)));
+  cfg.gridDim = dim3(std::min<uint32_t>(a.nitems, static_cast<uint32_t>(pl.sms) * pg.ctas));
   cfg.blockDim = dim3((kPairNcw + 1) * 32);
   cfg.dynamicSmemBytes = pg.smem;
   cfg.stream = st;

@@ -23,9 +23,10 @@ struct PairArgs {
   const double2* in;
   double2* out;
   uint32_t r, ga, pa;    // rank, level-A geometry
-  uint32_t k;            // right-hand sides (all in one tile)
+  uint32_t k;            // right-hand sides (row length of in / out)
+  uint32_t kc, nch;      // right-hand sides per item and chunks per pair (items = pairs x nch)
   int adjoint;
-  uint32_t nitems;       // G_A * P_A / 2
+  uint32_t nitems;       // G_A * P_A / 2 * nch
   uint32_t fld, vld;     // shared-memory row strides of block rows and vector rows
   uint32_t stage_elems;  // 8 blocks + 2 C vector rows
   // adjoint pair ending the down half: the middle factor fused into the level-A* stores
@@ -130,11 +131,13 @@ __device__ __forceinline__ void pair_gemms(int ngemm, int M, int nseg, int klen,
 
 // Producer: the 8 blocks (level A: (t, u) = (t, p = 2q + u); level B: (t, t') of
 // g' = 2g + t) and the item's input vector rows, one bulk copy per row.
-__device__ __forceinline__ void pair_produce(const PairArgs& a, uint32_t item, double2* st, uint64_t* full, int lane,
-                                             uint64_t pol) {
+__device__ __forceinline__ void pair_produce(const PairArgs& a, uint32_t item_rhs, double2* st, uint64_t* full,
+                                             int lane, uint64_t pol) {
   const uint32_t R = a.r, C = 2 * a.r, pb = a.pa / 2;
+  // items are (pair, right-hand-side chunk): chunks of one pair are independent columns
+  const uint32_t item = item_rhs / a.nch, k0 = (item_rhs - item * a.nch) * a.kc, kw = min(a.kc, a.k - k0);
   const uint32_t g = item / pb, q = item - g * pb;
-  const uint32_t bytes = (8 * R * C + 2 * C * a.k) * static_cast<uint32_t>(sizeof(double2));
+  const uint32_t bytes = (8 * R * C + 2 * C * kw) * static_cast<uint32_t>(sizeof(double2));
   if (lane == 0) mbar_arrive_expect_tx(full, bytes);
   __syncwarp();
   // block rows: 8 blocks x R rows; smem block b = (level, t, u|t') at b * R * fld
@@ -154,13 +157,13 @@ __device__ __forceinline__ void pair_produce(const PairArgs& a, uint32_t item, d
       const uint32_t ch = row / R, rr = row - ch * R, t = ch >> 1, tp = ch & 1;
       grow = static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q) * R + rr;
     }
-    bulk_g2s(vs + static_cast<size_t>(row) * a.vld, a.in + grow * a.k, a.k * static_cast<uint32_t>(sizeof(double2)),
+    bulk_g2s(vs + static_cast<size_t>(row) * a.vld, a.in + grow * a.k + k0, kw * static_cast<uint32_t>(sizeof(double2)),
              full);
   }
 }
 
 template <int STAGES, int NCW, bool GAUSS>
-__global__ void __launch_bounds__((NCW + 1) * 32, 1) pair_kernel(const PairArgs a) {
+__global__ void __launch_bounds__((NCW + 1) * 32, 2) pair_kernel(const PairArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + STAGES;
@@ -177,7 +180,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) pair_kernel(const PairArgs 
   __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const uint32_t R = a.r, C = 2 * a.r, pb = a.pa / 2, K = a.k;
+  const uint32_t R = a.r, C = 2 * a.r, pb = a.pa / 2, KS = a.k;
   const uint32_t fld = a.fld, vld = a.vld;
   if (warp == NCW) {
     const uint64_t pol = policy_evict_first();
@@ -195,7 +198,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) pair_kernel(const PairArgs 
     mbar_wait(&full[s], (it / STAGES) & 1);
     const double2* st = stage0 + static_cast<size_t>(s) * a.stage_elems;
     const double2* vs = st + static_cast<size_t>(8) * R * fld;
-    const uint32_t g = item / pb, q = item - g * pb;
+    const uint32_t pitem = item / a.nch, k0 = (item - pitem * a.nch) * a.kc;
+    const uint32_t K = min(a.kc, KS - k0);     // this item's right-hand sides
+    const uint32_t g = pitem / pb, q = pitem - g * pb;
     auto blk = [&](uint32_t b) { return st + static_cast<size_t>(b) * R * fld; };
     if (!a.adjoint) {
       // level A: Y(t, u) = B_A(g, t, 2q + u) X_u  ->  mi rows t C + u R + m
@@ -211,7 +216,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) pair_kernel(const PairArgs 
           [&](int gi, int, int kk, int n) { return mi[((gi >> 1) * C + kk) * vld + n]; },
           [&](int gi, int m, int n, double2 v) {
             const uint32_t t = gi >> 1, tp = gi & 1;
-            a.out[(static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q) * R + m) * K + n] = v;
+            a.out[(static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q) * R + m) * KS + k0 + n] = v;
           },
           warp, lane, NCW);
     } else {
@@ -236,7 +241,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) pair_kernel(const PairArgs 
           [&](int gi, int m, int n, double2 v) {
             double w;
             const size_t e = pair_remap(a, static_cast<size_t>(g * a.pa + 2 * q + gi) * C + m, &w);
-            a.out[e * K + n] = make_double2(w * v.x, w * v.y);
+            a.out[e * KS + k0 + n] = make_double2(w * v.x, w * v.y);
           },
           warp, lane, NCW);
     }
