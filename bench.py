@@ -221,12 +221,37 @@ def dev_time(fn, steps, warm):
     return e0.elapsed_time(e1) / steps
 
 
+LIVE_PEAKS = {}   # bf_measure_peaks in this process (measure_live_peaks)
+
+
+def measure_live_peaks():
+    """FP64 DMMA / DFMA peaks and streaming-read / copy bandwidth measured in this process on
+    this GPU (bf_measure_peaks over an 8 GiB buffer: far larger than L2), the denominators of the
+    FP64 and read-dominated rooflines; MEASURED_PEAKS.json has neither."""
+    import torch
+
+    from paper_1502_01379_b200 import _lib
+    buf = torch.empty(8 << 30, dtype=torch.uint8, device="cuda")
+    out = (ctypes.c_double * 4)()
+    _lib.check(_lib.load().bf_measure_peaks(out, ctypes.c_void_p(buf.data_ptr()), buf.numel(),
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+               "bf_measure_peaks")
+    del buf
+    torch.cuda.empty_cache()
+    LIVE_PEAKS.update(dmma_tflops=out[0], dfma_tflops=out[1], read_gbs=out[2], copy_gbs=out[3],
+                      how="bf_measure_peaks: mma.sync m8n8k4 f64 loop, DFMA loop, __ldcs read stream over 8 GiB "
+                          "and a 4 GiB device-to-device cudaMemcpyAsync; best of 5 after a warm-up, in this process")
+    return dict(LIVE_PEAKS)
+
+
 def _peaks():
     pk = {}
     if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")):
         pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     fp = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))
-    return float(pk.get("hbm_gbs", 6550.0)), float(fp["dmma_m8n8k4_tflops"]), float(fp["read_gbs"])
+    dmma = LIVE_PEAKS.get("dmma_tflops", float(fp["dmma_m8n8k4_tflops"]))
+    read = LIVE_PEAKS.get("read_gbs", float(fp["read_gbs"]))
+    return float(pk.get("hbm_gbs", 6550.0)), float(dmma), float(read)
 
 
 def _rate(f, k, esz, ms):
@@ -717,6 +742,15 @@ def main():
     for _ in range(warm):
         apply_once()
     torch.cuda.synchronize()
+    live = None
+    if world == 1:
+        try:
+            live = measure_live_peaks()
+        except Exception as exc:  # the file values stand in
+            live = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+        for _ in range(warm):   # back to the apply's steady state after the peak kernels
+            apply_once()
+        torch.cuda.synchronize()
 
     nlaunch = 2 + 2 * len(f.g_chain)
     # timed region: K applies through bf_apply (the chain replays as one CUDA graph)
@@ -783,24 +817,23 @@ def main():
     roof = {"bound": "hbm", "achieved": tr_bytes / (tr_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
             "frac": tr_bytes / (tr_ms / 1e3) / 1e9 / hbm_peak,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
-    try:  # the levels are read-dominated (factor blocks read once, vectors L2-resident):
-        # their own ceiling is the streaming-read bandwidth, measured on this pool's B200s
-        rd = float(json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))["read_gbs"])
-        roof.update(read_peak=rd, frac_of_read_peak=roof["achieved"] / rd,
-                    read_peak_source="profiles/r01_fp64_peaks.json read_gbs (tools/fp64_peak.cu read_stream; "
-                                     "MEASURED_PEAKS.json hbm_gbs is a copy: half reads, half writes)")
-    except (OSError, KeyError, ValueError):
-        pass
+    # the levels are read-dominated (factor blocks read once, vectors L2-resident): their own
+    # ceiling is the streaming-read bandwidth, measured in this process (bf_measure_peaks)
+    _, _, rd = _peaks()
+    roof.update(read_peak=rd, frac_of_read_peak=roof["achieved"] / rd,
+                read_peak_source=("bf_measure_peaks in this run" if "read_gbs" in LIVE_PEAKS else
+                                  "profiles/r01_fp64_peaks.json read_gbs") +
+                " (MEASURED_PEAKS.json hbm_gbs is a copy: half reads, half writes)")
     if k >= 8 and args.dtype == "c128":
         # many right-hand sides: the transfer levels are FP64 tensor-core (DMMA) bound
         # (SURVEY.md §8(d)); algorithmic flops (8 per complex multiply-add) per launch
         tr_fl = sum(fl for (name, fl) in lf_all if dominant(name)) / len(tr)
-        fp64 = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))
-        dmma_peak = float(fp64["dmma_m8n8k4_tflops"])
+        _, dmma_peak, _ = _peaks()
         roof = {"bound": "tensor", "achieved": tr_fl / (tr_ms / 1e3) / 1e12, "peak": dmma_peak, "unit": "TFLOP/s",
                 "frac": tr_fl / (tr_ms / 1e3) / 1e12 / dmma_peak,
-                "peak_source": "profiles/r01_fp64_peaks.json dmma_m8n8k4_tflops (FP64 tensor pipe measured on "
-                               "this pool's B200 by tools/fp64_peak.cu; MEASURED_PEAKS.json has no FP64 figure)",
+                "peak_source": ("bf_measure_peaks in this run" if "dmma_tflops" in LIVE_PEAKS else
+                                "profiles/r01_fp64_peaks.json") +
+                               " (FP64 tensor pipe, mma.sync m8n8k4; MEASURED_PEAKS.json has no FP64 figure)",
                 "note": "complex products run as 3 real DMMAs (Gauss form), so the algorithmic rate can exceed "
                         "the 4-product tensor-pipe rate by up to 4/3"}
 
@@ -894,6 +927,7 @@ def main():
                               "pipeline), median of per-step wall times"},
             "gpu_launches": nlaunch * steps,
             "clocks": clk,
+            "live_peaks": live,
             "cpu_baseline": cpu,
             "also": also,
         }

@@ -214,6 +214,11 @@ int bf_middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t branch
                      const int32_t* draws, void* u_out, void* v_out, double* w_out,
                      void* workspace, uint64_t ws_bytes, void* stream);
 
+/* Roofline denominators measured in the caller's process (bench.py): out[0] FP64 tensor
+ * pipe TF/s (mma.sync m8n8k4), out[1] FP64 FMA TF/s, out[2] streaming-read GB/s, out[3]
+ * copy GB/s (read + write bytes) over `scratch` (device, >= 1 GiB, larger than L2). */
+int bf_measure_peaks(double* out, void* scratch, uint64_t scratch_bytes, void* stream);  /* scratch: 4 GiB+ */
+
 /* Diagnostics: node kernels (one launch per chain half) stamp %globaltimer per CTA into
  * dev_buf (u64, >= 2 x m x chunks x 32; NULL turns it off). Not thread-safe; tools only. */
 int bf_debug_node_trace(unsigned long long* dev_buf);

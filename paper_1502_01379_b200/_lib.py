@@ -40,6 +40,7 @@ SIGNATURES = [
     ("bf_middle_workspace_bytes", _U64, [_U64, _U32, _U32, _U32, _U32, _U32]),
     ("bf_middle_blocks", _I, [_I, _U64, _U32, _U32, _U32, _U32, _U32, _P, _U32, _P, _P, _P, _P, _P, _P, _U64, _P]),
     ("bf_debug_node_trace", _I, [_P]),
+    ("bf_measure_peaks", _I, [_P, _P, _U64, _P]),
     ("bf_middle_blocks_tiled", _I, [_U64, _U32, _U32, _U32, _U32, _U32, _P, _P, _U32, _P, _P, _P, _P, _P, _P, _U64,
                                     _P]),
     ("bf_probe_workspace_bytes", _U64, [_U64, _U32, _U32, _U32, _U32, _U32]),
