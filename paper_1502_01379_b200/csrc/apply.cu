@@ -546,7 +546,12 @@ bool pair_disabled() {
   return off;
 }
 
-constexpr int kPairStages = 2, kPairNcw = 8;
+constexpr int kPairNcw = 8;
+// pipeline depth of the whole-tile pair kernel (2, 3 or 4; BF_PAIR_STAGES overrides)
+int pair_stages() {
+  static const int st = std::max(2, std::min(4, env_int("BF_PAIR_STAGES", 2)));
+  return st;
+}
 
 // k-chunked pairs (pair_chunk_kernel) only with BF_CHUNK_PAIR=1: at cfg2 k = 256 they
 // halve the vector traffic but run 47.3 ms against 43.8 ms for single levels (32-RHS
@@ -573,16 +578,25 @@ bool pair_geometry(const Plan& pl, int i, uint32_t k, int adjoint, PairGeo* pg) 
   if (!A.splits || !B.splits || A.P < 2 || B.G != 2 * A.G || 2 * B.P != A.P) return false;
   const uint64_t R = pl.rank, C = 2 * R;
   auto pad_to = [](uint64_t x, uint64_t target) { return x + (target + 8 - x % 8) % 8; };
-  const uint64_t fld = pad_to(C, adjoint ? 2 : 4);
+  // unpadded factor rows, copied as whole blocks: 6 bulk copies per item instead of one per
+  // block row — the producer warp's copy issue rate, not the DMMA pipe, paced the pairs
+  // (ncu: 29% of consumer stall samples on the stage's full barrier; cfg1 268 -> 239 us).
+  // The A-fragment reads take 2- to 4-way bank conflicts instead. BF_PAIR_FPAD=1 pads again.
+  static const bool fpad = env_int("BF_PAIR_FPAD", 0) != 0;
+  const uint64_t fld = fpad ? pad_to(C, adjoint ? 2 : 4) : C;
   pg->fld = static_cast<uint32_t>(fld);
   pg->chunk = false;
   if (k <= 256) {  // whole right-hand-side range per stage (or k / 2 chunks), double-buffered
+    // BF_PAIR_VPAD=0: unpadded vector rows (whole-k items copy contiguous row runs; measured
+    // slower: 4-way conflicts on the X fragments, cfg1 257.6 vs 239.4 us)
+    static const bool vpad = env_int("BF_PAIR_VPAD", 1) != 0;
+    auto vld_for = [&](uint64_t kc) { return vpad ? pad_to(kc, 2) : kc; };
     auto smem_for = [&](uint64_t kc, uint64_t* stage_out) {
-      const uint64_t vld = pad_to(kc, 2);
+      const uint64_t vld = vld_for(kc);
       uint64_t stage = 8 * R * fld + 2 * C * vld;
       if (stage & 1) ++stage;
       *stage_out = stage;
-      return 128 + (kPairStages * stage + 2 * C * vld) * sizeof(double2);
+      return 128 + (pair_stages() * stage + 2 * C * vld) * sizeof(double2);
     };
     // Right-hand-side chunks are independent items: halving the chunk lets two CTAs share an
     // SM (18 warps instead of 9 to cover the DMMA and shared-memory latencies) at the cost of
@@ -597,7 +611,7 @@ bool pair_geometry(const Plan& pl, int i, uint32_t k, int adjoint, PairGeo* pg) 
     }
     const uint64_t smem = smem_for(kc, &stage);
     if (smem <= static_cast<uint64_t>(kMaxDynSmem)) {
-      pg->vld = static_cast<uint32_t>(pad_to(kc, 2));
+      pg->vld = static_cast<uint32_t>(vld_for(kc));
       pg->stage_elems = static_cast<uint32_t>(stage);
       pg->smem = smem;
       pg->kc = static_cast<uint32_t>(kc);
@@ -684,7 +698,11 @@ int launch_pair(const Plan& pl, const void* fac_a, const void* fac_b, int i, con
   a.m = pl.m;
   a.mr = pl.rank;
   a.mid_w = static_cast<const double*>(pl.weights);
-  auto* kern = gauss_disabled() ? pair_kernel<kPairStages, kPairNcw, false> : pair_kernel<kPairStages, kPairNcw, true>;
+  const int ps = pair_stages();
+  auto* kern = gauss_disabled() ? pair_kernel<2, kPairNcw, false>
+               : ps == 4       ? pair_kernel<4, kPairNcw, true>
+               : ps == 3       ? pair_kernel<3, kPairNcw, true>
+                               : pair_kernel<2, kPairNcw, true>;
   BF_CUDA(allow_max_dyn_smem(kern));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(std::min<uint32_t>(a.nitems, static_cast<uint32_t>(pl.sms) * pg.ctas));

@@ -141,6 +141,18 @@ __device__ __forceinline__ void pair_produce(const PairArgs& a, uint32_t item_rh
   if (lane == 0) mbar_arrive_expect_tx(full, bytes);
   __syncwarp();
   // block rows: 8 blocks x R rows; smem block b = (level, t, u|t') at b * R * fld
+  if (a.fld == C) {   // unpadded blocks: whole-block copies (level A: (g, t, 2q), (g, t, 2q + 1) adjacent)
+    const uint32_t bb = R * C * static_cast<uint32_t>(sizeof(double2));
+    if (lane < 2) {
+      const uint32_t t = lane;
+      bulk_g2s(st + static_cast<size_t>(2 * t) * R * C, a.fac_a + static_cast<size_t>((g * 2 + t) * a.pa + 2 * q) * R * C,
+               2 * bb, full, pol);
+    } else if (lane < 6) {
+      const uint32_t b = lane + 2, t = (b >> 1) & 1, v = b & 1;
+      bulk_g2s(st + static_cast<size_t>(b) * R * C, a.fac_b + static_cast<size_t>(((2 * g + t) * 2 + v) * pb + q) * R * C,
+               bb, full, pol);
+    }
+  } else
   for (uint32_t row = lane; row < 8 * R; row += 32) {
     const uint32_t b = row / R, rr = row - b * R;
     const uint32_t lvl = b >> 2, t = (b >> 1) & 1, v = b & 1;
@@ -149,6 +161,18 @@ __device__ __forceinline__ void pair_produce(const PairArgs& a, uint32_t item_rh
     bulk_g2s(st + static_cast<size_t>(row) * a.fld, src, C * static_cast<uint32_t>(sizeof(double2)), full, pol);
   }
   double2* vs = st + static_cast<size_t>(8) * R * a.fld;
+  if (a.vld == kw && kw == a.k) {   // unpadded whole-k rows: contiguous row runs in one copy each
+    const uint32_t rb = a.k * static_cast<uint32_t>(sizeof(double2));
+    if (!a.adjoint) {
+      if (lane == 0)
+        bulk_g2s(vs, a.in + static_cast<size_t>(g * a.pa + 2 * q) * C * a.k, 2 * C * rb, full);
+    } else if (lane < 4) {
+      const uint32_t t = lane >> 1, tp = lane & 1;
+      bulk_g2s(vs + static_cast<size_t>(lane) * R * a.k,
+               a.in + static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q) * R * a.k, R * rb, full);
+    }
+    return;
+  }
   for (uint32_t row = lane; row < 2 * C; row += 32) {
     size_t grow;
     if (!a.adjoint) {  // units (g, 2q), (g, 2q + 1): 2 C contiguous rows
