@@ -170,10 +170,11 @@ LevelKernel ffma16_kernel() {
     return nullptr;
 }
 
-// BF_REMAP_PAIR=1: the down half's last two levels as one pair kernel with the middle
-// factor fused into its stores (cfg1: 0.287 vs 0.284 ms for the two single launches)
+// The down half's last two levels as one pair kernel with the middle factor fused into its
+// stores (default since the whole-block pair copies: cfg1 234.4 vs 239.4 us; it was 0.287
+// vs 0.284 ms before them). BF_REMAP_PAIR=0 keeps two single launches.
 bool remap_pair_enabled() {
-  static const bool on = env_int("BF_REMAP_PAIR", 0) != 0;
+  static const bool on = env_int("BF_REMAP_PAIR", 1) != 0;
   return on;
 }
 

@@ -196,7 +196,8 @@ print("ok", e1, e2)
 
 @pytest.mark.parametrize("n,leaf,r,k", [(1 << 16, 16, 8, 64), (1 << 12, 16, 6, 64)])
 def test_remap_pair_opt_in(n, leaf, r, k):
-    """BF_REMAP_PAIR=1: the down half's last pair carries the fused middle factor."""
+    """The down half's last pair carries the fused middle factor (the default; this child
+    process sets BF_REMAP_PAIR=1 explicitly)."""
     test_chunked_pairs_opt_in(n, leaf, r, k, env_flag="BF_REMAP_PAIR")
 
 
