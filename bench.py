@@ -358,6 +358,30 @@ def companion_same_plan_c64(f, n, steps, warm, cols=1):
             "rel_err": {"value": err, "columns": cols, "tolerance": 1e-5}}
 
 
+def construction_flops(p, r, q=3, iters=3):
+    """Algorithmic FP64 flops of one sampling-mode factorize (8 per complex multiply-add), an
+    upper-bound model of the reference algorithm's arithmetic with the
+    sample sets at their caps: per middle block (side s, |rows| = |cols| = r (q + 1), basis
+    width t = 3 r) the sweep pivots' projections 2 (iters + 1) x r picks x |rows| s, the two
+    Gram matrices |cols|^2 s, the two bases (CGS2) 2 t^2 s each, the assembly 2 s t r; per
+    recursion level and stack (rows x 2r) a QR 2 rows w^2, a one-sided Jacobi SVD counted as
+    10 sweeps x min(rows, w) w^2, and A V. cfg2: 58 TFLOP middle level + 110 TFLOP recursion."""
+    m, s = p.mid_nodes, p.mid_side
+    rs, t = r * (q + 1), 3 * r
+    per_block = 8 * (2 * (iters + 1) * r * rs * s + 2 * rs * rs * s + 2 * 2 * t * t * s + 2 * s * t * r)
+    mid = per_block * m * m
+    # recursion (construct.py:127-163): per side m slabs of s rows; at level l a slab splits into
+    # 2^l m / 2 x 2 stacks of s / 2^(l+1) rows x 2r columns (the entry count is level-invariant):
+    # QR 2 rows w^2, one-sided Jacobi ~10 min(rows, w) w^2, the product A V rows w r
+    rec, rows, w = 0, s, 2 * r
+    for lvl in range(p.levels - p.half):
+        n_stack = (s // rows) * m
+        mrow = max(1, rows // 2)
+        rec += 8 * n_stack * (2 * mrow * w * w + 10 * min(mrow, w) * w * w + mrow * w * r)
+        rows = max(2, rows // 2)
+    return mid + 2 * m * rec
+
+
 def companion_construction(name, cpu_blocks=2):
     """BASELINE configs[2]'s construction, the reference bench's row (factorize time, eps_a,
     apply time; reference bench.py:202-222): full GPU `factorize` (sampling mode, FIO kernel,
@@ -404,9 +428,16 @@ def companion_construction(name, cpu_blocks=2):
     ocons.recurse(slab, n, p.levels, r)
     t_slab = time.perf_counter() - t3
     cpu_s = m * m * t_blk + 2 * m * t_slab
+    fl = construction_flops(p, r)
+    _, dmma, _ = _peaks()
+    dfma = LIVE_PEAKS.get("dfma_tflops", 36.43)
     return {"workload": f"{name} factorize {kern.upper()} N={n} r={r} leaf={leaf} (L={p.levels}), sampling mode, "
                         "seed 0, full construction on the GPU",
             "factorize_s": t_fac, "eps_a": eps, "eps_a_s": t_eps, "apply_ms_built": ms,
+            "roofline": {"algorithmic_fp64_flops_model": fl, "achieved_tflops": fl / t_fac / 1e12,
+                         "dfma_peak_tflops": dfma, "frac_of_fp64_peak": fl / t_fac / 1e12 / dfma,
+                         "model": "upper bound: sample sets at their caps r(q+1), bases 3r wide "
+                                  "(bench.construction_flops); entry evaluation (sincos) not counted"},
             "cpu_reference": {"factorize_s_extrapolated": cpu_s, "per_block_s": t_blk, "slab_recursion_s": t_slab,
                               "kind": "port", "cores": int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count())),
                               "sample": f"{cpu_blocks} middle blocks x {m * m} + 1 slab recursion x {2 * m}"},
