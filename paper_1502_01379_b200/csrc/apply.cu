@@ -9,11 +9,14 @@
 #include <type_traits>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "level_kernel.cuh"
 #include "pair_kernel.cuh"
 #include "node_mma.cuh"
 #include "tc_kernel.cuh"
+#include "wide_kernel.cuh"
+#include <cudaTypedefs.h>
 #include "plan.h"
 
 namespace bfly {
@@ -238,6 +241,134 @@ int launch_level_t(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint
                    int accumulate, uint64_t P, uint64_t units, const void* in, void* out, uint32_t k, int adjoint,
                    int remap, cudaStream_t st, void* const* peers, uint32_t tsplit = 1);
 
+// Wide many-RHS levels (wide_kernel.cuh): complex128 units whose blocks do not fit a
+// shared-memory stage whole (quadtree rank 25, C = 4r = 100) as a K-pipelined DMMA GEMM,
+// one consumer warp per 8 output rows. BF_NO_WIDE=1 restores the whole-unit stage;
+// BF_WIDE_KT sets the K tile (multiple of 4, default 20).
+bool wide_disabled() {
+  static const bool off = env_int("BF_NO_WIDE", 0) != 0;
+  return off;
+}
+constexpr int kWideNcw = 13;
+
+bool wide_applies(uint32_t R, uint32_t C, uint32_t nt, uint32_t k, int remap, size_t esz) {
+  return esz == 16 && !wide_disabled() && !dmma_disabled() && !gauss_disabled() && k >= kMrhsMinK && remap <= 2 &&
+         C > 64 && nt * R <= 8u * kWideNcw && C <= 8u * kWideNcw;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// 2-D FP64 tensor map over a row-major (rows x cols) array, box (box_cols x box_rows),
+// no swizzle, zero fill out of bounds
+int tmap_2d(CUtensorMap* tm, const void* base, uint64_t cols, uint64_t rows, uint32_t box_cols, uint32_t box_rows,
+            CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
+  const auto enc = tmap_encoder();
+  if (!enc) return fail(BF_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * sizeof(double)};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BF_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return 0;
+}
+
+int launch_wide(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint64_t P, uint64_t units,
+                const void* in, void* out, uint32_t k, int adjoint, int remap, cudaStream_t st) {
+  auto pad_to = [](uint64_t x, uint64_t target) { return x + (target + 8 - x % 8) % 8; };
+  auto up8 = [](uint64_t x) { return (x + 7) / 8 * 8; };  // 128-byte multiples of complex128
+  WideArgs a{};
+  a.out = static_cast<double2*>(out);
+  a.mid_w = static_cast<const double*>(pl.weights);
+  a.R = R;
+  a.C = C;
+  a.nt = nt;
+  a.lgP = ilog2(P);
+  a.k = k;
+  const uint32_t NT = k > 16 ? 4 : k > 8 ? 2 : 1;
+  a.kc = std::min<uint32_t>(k, 8 * NT);
+  a.nkc = (k + a.kc - 1) / a.kc;
+  const uint64_t frows = units * nt * R, vrows = adjoint ? frows : units * C;
+  if (units * a.nkc >= (1ull << 31) || frows >= (1ull << 31) || vrows >= (1ull << 31))
+    return fail(BF_EINVAL, "level has too many blocks for one launch");
+  a.items = static_cast<uint32_t>(units * a.nkc);
+  // K tiles: forward BF_WIDE_KT block columns (multiple of 4, = 4 mod 8 for conflict-free A
+  // fragment rows; default 20), adjoint one whole block (R rows)
+  static const int kt_env = env_int("BF_WIDE_KT", 20);
+  if (!adjoint) {
+    a.KT = std::min<uint32_t>(static_cast<uint32_t>(std::max(4, kt_env / 4 * 4)), (C + 3) / 4 * 4);
+    a.nks = (C + a.KT - 1) / a.KT;
+    a.fst = a.KT;
+    a.fslot = static_cast<uint32_t>(up8(static_cast<uint64_t>(R) * a.KT));
+    a.voff = nt * a.fslot;
+  } else {
+    a.KT = R;
+    a.nks = nt;
+    a.fst = static_cast<uint32_t>(pad_to(C, 2));  // A^H fragment columns: stride 2 mod 8
+    a.fslot = 0;
+    a.voff = static_cast<uint32_t>(up8(static_cast<uint64_t>(R) * a.fst));
+  }
+  a.vst = static_cast<uint32_t>(pad_to(8 * NT, 2));   // B fragment rows: stride 2 mod 8
+  if (2 * a.fst > 256 || 2 * a.vst > 256 || a.KT > 256 || R > 256)
+    return fail(BF_EINVAL, "wide level: tensor box exceeds 256 elements");
+  const uint64_t stage = up8(a.voff + static_cast<uint64_t>(a.KT) * a.vst);
+  a.stage_elems = static_cast<uint32_t>(stage);
+  a.stage_bytes = static_cast<uint32_t>(
+      ((adjoint ? static_cast<uint64_t>(R) * a.fst : static_cast<uint64_t>(nt) * R * a.KT) +
+       static_cast<uint64_t>(a.KT) * a.vst) * sizeof(double2));
+  const uint64_t fit = (static_cast<uint64_t>(kMaxDynSmem) - 128) / (stage * sizeof(double2));
+  static const int st_env = env_int("BF_WIDE_STAGES", 8);
+  a.stages = static_cast<uint32_t>(std::min<uint64_t>(fit, static_cast<uint64_t>(std::max(2, std::min(8, st_env)))));
+  if (a.stages < 2) return fail(BF_EINVAL, "wide level: K tile does not double-buffer");
+  a.adjoint = adjoint;
+  a.remap = remap;
+  a.m = pl.m;
+  a.r = pl.rank;
+  CUtensorMap tmA, tmV;
+  // L2 promotion of the factor boxes (BF_WIDE_PROMO: 0 none, 1 64 B, 2 128 B, 3 256 B)
+  static const int promo = std::max(0, std::min(3, env_int("BF_WIDE_PROMO", 3)));
+  int rc = tmap_2d(&tmA, fac, 2ull * C, frows, adjoint ? 2 * a.fst : 2 * a.KT, R,
+                   static_cast<CUtensorMapL2promotion>(CU_TENSOR_MAP_L2_PROMOTION_NONE + promo));
+  if (!rc) rc = tmap_2d(&tmV, in, 2ull * k, vrows, 2 * a.vst, a.KT);
+  if (rc) return rc;
+  const size_t smem = 128 + static_cast<size_t>(a.stages) * stage * sizeof(double2);
+  void (*kern)(const WideArgs, const CUtensorMap, const CUtensorMap) = nullptr;
+  if (adjoint)
+    kern = NT == 4 ? wide_kernel<kWideNcw, 4, true> : NT == 2 ? wide_kernel<kWideNcw, 2, true> : wide_kernel<kWideNcw, 1, true>;
+  else
+    kern = NT == 4 ? wide_kernel<kWideNcw, 4, false> : NT == 2 ? wide_kernel<kWideNcw, 2, false> : wide_kernel<kWideNcw, 1, false>;
+  BF_CUDA(allow_max_dyn_smem(kern));
+  static const bool dbg = env_int("BF_DEBUG_LAUNCH", 0) != 0;
+  if (dbg)
+    fprintf(stderr, "[bf] wide_kernel R=%u C=%u nt=%u units=%llu k=%u kc=%u NT=%u KT=%u nks=%u stages=%u smem=%zu adj=%d\n", R,
+            C, nt, static_cast<unsigned long long>(units), k, a.kc, NT, a.KT, a.nks, a.stages, smem, adjoint);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min<uint32_t>(a.items, static_cast<uint32_t>(pl.sms)));
+  cfg.blockDim = dim3((kWideNcw + 1) * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BF_CUDA(cudaLaunchKernelEx(&cfg, kern, a, tmA, tmV));
+  return 0;
+}
+
 // One factor launch. A unit's nt blocks normally share one tile; when they do
 // not fit a shared-memory stage (quadtree rank 25: 4 x 25 x 100 complex128 =
 // 160 KB) the blocks are split into t-ranges, one launch each: forward outputs
@@ -246,6 +377,8 @@ template <typename E>
 int launch_level(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_t nt, uint64_t P, uint64_t units,
                  const void* in, void* out, uint32_t k, int adjoint, int remap, cudaStream_t st,
                  void* const* peers = nullptr) {
+  if (wide_applies(R, C, nt, k, remap, sizeof(E)))
+    return launch_wide(pl, fac, R, C, nt, P, units, in, out, k, adjoint, remap, st);
   const Shape sh = k >= kMrhsMinK ? mrhs_shape_for<E>(C) : stream_shape<E>();
   // wide many-RHS forward levels (quadtree r = 25: a unit is 160 KB of blocks), opt-in
   // BF_WIDE_SPLIT=1: the two t-halves of every unit as consecutive tiles of ONE launch

@@ -205,7 +205,8 @@ def test_quadtree_t_range_split_many_rhs():
     """Many-RHS quadtree levels whose 4-block units do not fit a stage run as t-range
     launches (forward outputs per t, adjoint partial sums accumulated). The default
     single 200 KB stage avoids them at r = 25; BF_MRHS_STAGES=2 BF_MRHS_STAGE_KB=112 (read
-    once per process, hence a child process) forces them."""
+    once per process, hence a child process) forces them, with the K-pipelined wide
+    kernel (the default for these levels) turned off by BF_NO_WIDE=1."""
     import subprocess
     import sys
     code = f"""
@@ -226,7 +227,7 @@ e2 = rel(f.plan().apply(gd, adjoint=True), ochain.apply(oc, g, adjoint=True))
 assert e1 <= 1e-11 and e2 <= 1e-11, (e1, e2)
 print("ok", e1, e2)
 """
-    env = dict(os.environ, BF_MRHS_STAGES="2", BF_MRHS_STAGE_KB="112")
+    env = dict(os.environ, BF_MRHS_STAGES="2", BF_MRHS_STAGE_KB="112", BF_NO_WIDE="1")
     r_ = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, cwd=ROOT)
     assert r_.returncode == 0 and "ok" in r_.stdout, r_.stderr[-2000:]
 
@@ -299,6 +300,29 @@ def test_quadtree_geometries(n_side, leaf, r, k):
     assert rel(f.plan("c64").apply(gd).to(torch.complex128), ochain.apply(oc, g)) <= TOL64
     assert rel(f.plan("c64").apply(gd, adjoint=True).to(torch.complex128),
                ochain.apply(oc, g, adjoint=True)) <= TOL64
+
+
+@pytest.mark.parametrize("tree,n,leaf,r,k", [
+    ("quad", 64, 4, 25, 8),       # one 8-column tile per item
+    ("quad", 128, 2, 25, 12),     # ragged right-hand-side tile
+    ("quad", 64, 4, 17, 33),      # C = 68: ragged last K tile; two right-hand-side chunks
+    ("quad", 128, 2, 20, 64),     # 32-column items, two chunks
+    ("bin", 1 << 12, 64, 40, 16),  # binary tree with C = 2r = 80 > 64
+])
+def test_wide_kernel_levels(tree, n, leaf, r, k):
+    """Many-RHS complex128 levels with wide blocks (C > 64) run as the K-pipelined DMMA GEMM
+    (wide_kernel.cuh): forward and adjoint chains (the adjoint chain's last down level carries
+    the fused middle factor) against the oracle, and bitwise run-to-run."""
+    p = bf.make_quadtree_partition(n, leaf) if tree == "quad" else bf.make_partition(n, leaf)
+    f = synthetic_chain(p, r, seed=n + r + k)
+    oc = oracle_of(f)
+    g = complex_gaussian(np.random.default_rng(k), (p.n, k))
+    gd = torch.from_numpy(g).cuda()
+    pl = f.plan()
+    y = pl.apply(gd)
+    assert rel(y, ochain.apply(oc, g)) <= TOL128
+    assert rel(pl.apply(gd, adjoint=True), ochain.apply(oc, g, adjoint=True)) <= TOL128
+    assert torch.equal(pl.apply(gd), y)
 
 
 @pytest.mark.parametrize("n,leaf,r,k", [(1 << 18, 16, 16, 1), (1 << 16, 16, 8, 64)])
