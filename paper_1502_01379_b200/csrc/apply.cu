@@ -808,8 +808,56 @@ int launch_pair_chunk(const Plan& pl, const void* fac_a, const void* fac_b, int 
   return 0;
 }
 
+// Rank-8 fast path of the level pairs (pair8_kernel): warp-owned (t, 16-column) slices, no
+// block barrier between the levels. BF_NO_PAIR8=1 turns it off; BF_PAIR8_STAGES=1 runs one
+// stage per CTA (up to four CTAs per SM) instead of two (measured: cfg1 0.227 vs 0.197 ms).
+int pair8_stages() {
+  static const int st = env_int("BF_PAIR8_STAGES", 2) == 1 ? 1 : 2;
+  return st;
+}
+bool pair8_ok(const Plan& pl, const PairGeo& pg, uint32_t k) {
+  static const bool off = env_int("BF_NO_PAIR8", 0) != 0;
+  return !off && !pg.chunk && !gauss_disabled() && pl.rank == 8 && (pg.kc == 32 || pg.kc == 64) && k % 16 == 0;
+}
+// stage of the leaf-fused pair: 8 unpadded blocks, 4 leaf blocks (16 x 8), the input rows
+uint32_t pair8_leaf_stage(uint32_t vld, int adjoint) { return 8 * 8 * 16 + 4 * 16 * 8 + (adjoint ? 64u : 32u) * vld; }
+size_t pair8_smem(uint32_t stage_elems, uint32_t vld) {
+  return 128 + (static_cast<size_t>(pair8_stages()) * stage_elems + 2 * 16 * vld) * sizeof(double2);
+}
+uint32_t pair8_ctas(uint32_t ncw, int adjoint, size_t smem) {
+  const size_t cap = pair8_stages() == 1 ? (ncw == 4 ? (adjoint ? 3 : 4) : 2) : (ncw == 4 ? 2 : 1);
+  return static_cast<uint32_t>(std::min<size_t>(cap, static_cast<size_t>(kMaxDynSmem) / (smem + 1024)));
+}
+// The leaf factor rides in the pair next to it (the down half's first pair reads the chain
+// input, the up half's last pair writes the chain output): 16-point leaves, unpadded
+// blocks. The right-hand-side chunk (32 or 64) is the one that keeps the most consumer
+// warps per SM with the larger stage. BF_NO_PAIR8_LEAF=1 turns it off.
+bool pair8_leaf_geo(const Plan& pl, const PairGeo& pg, uint32_t k, int adjoint, PairGeo* out) {
+  static const bool off = env_int("BF_NO_PAIR8_LEAF", 0) != 0;
+  if (off || !pair8_ok(pl, pg, k) || pl.leaf_n0 != 16 || pg.fld != 16 || pl.nparts != 1) return false;
+  uint32_t best = 0;
+  for (uint32_t kc : {pg.kc, 64u}) {
+    if (kc > k || kc < pg.kc) continue;
+    const uint32_t vld = pg.vld == pg.kc ? kc : kc + 2;
+    const uint32_t stage = pair8_leaf_stage(vld, adjoint);
+    const size_t smem = pair8_smem(stage, vld);
+    if (smem > static_cast<size_t>(kMaxDynSmem)) continue;
+    const uint32_t warps = pair8_ctas(kc / 8, adjoint, smem) * (kc / 8);
+    if (warps > best) {
+      best = warps;
+      *out = pg;
+      out->kc = kc;
+      out->nch = (k + kc - 1) / kc;
+      out->vld = vld;
+      out->stage_elems = stage;
+      out->smem = smem;
+    }
+  }
+  return best > 0;
+}
+
 int launch_pair(const Plan& pl, const void* fac_a, const void* fac_b, int i, const void* in, void* out, uint32_t k,
-                int adjoint, const PairGeo& pg, cudaStream_t st, int remap = 0) {
+                int adjoint, const PairGeo& pg, cudaStream_t st, int remap = 0, const void* leaf = nullptr) {
   if (pg.chunk) return launch_pair_chunk(pl, fac_a, fac_b, i, in, out, k, adjoint, pg, st);
   const LevelGeo& A = pl.lev[i];
   PairArgs a{};
@@ -832,6 +880,43 @@ int launch_pair(const Plan& pl, const void* fac_a, const void* fac_b, int i, con
   a.m = pl.m;
   a.mr = pl.rank;
   a.mid_w = static_cast<const double*>(pl.weights);
+  // rank 8, 16-column slices (pair8_kernel): warp-owned slices, no block barrier between
+  // the levels; one stage per CTA and up to four CTAs per SM. BF_NO_PAIR8=1 turns it off,
+  // BF_PAIR8_STAGES=2 double-buffers inside the CTA instead.
+  if (pair8_ok(pl, pg, k)) {
+    const int p8_stages = pair8_stages();
+    a.leaf = static_cast<const double2*>(leaf);   // leaf: pg is pair8_leaf_geo's (its stage holds the leaf blocks)
+    const size_t smem = pair8_smem(a.stage_elems, pg.vld);
+    if (smem > static_cast<size_t>(kMaxDynSmem)) return fail(BF_EINVAL, "leaf-fused pair exceeds shared memory");
+    const uint32_t ncw = pg.kc / 8;
+    void (*kern)(const PairArgs);
+    if (leaf)
+      kern = ncw == 4 ? (p8_stages == 2 ? (adjoint ? pair8_kernel<2, true, 4, true> : pair8_kernel<2, false, 4, true>)
+                                        : (adjoint ? pair8_kernel<1, true, 4, true> : pair8_kernel<1, false, 4, true>))
+                      : (p8_stages == 2 ? (adjoint ? pair8_kernel<2, true, 8, true> : pair8_kernel<2, false, 8, true>)
+                                        : (adjoint ? pair8_kernel<1, true, 8, true> : pair8_kernel<1, false, 8, true>));
+    else
+      kern = ncw == 4 ? (p8_stages == 2 ? (adjoint ? pair8_kernel<2, true, 4, false> : pair8_kernel<2, false, 4, false>)
+                                        : (adjoint ? pair8_kernel<1, true, 4, false> : pair8_kernel<1, false, 4, false>))
+                      : (p8_stages == 2 ? (adjoint ? pair8_kernel<2, true, 8, false> : pair8_kernel<2, false, 8, false>)
+                                        : (adjoint ? pair8_kernel<1, true, 8, false> : pair8_kernel<1, false, 8, false>));
+    BF_CUDA(allow_max_dyn_smem(kern));
+    static const int ctas_env = env_int("BF_PAIR8_CTAS", 0);
+    uint32_t ctas = pair8_ctas(ncw, adjoint, smem);
+    if (ctas_env > 0) ctas = std::min<uint32_t>(ctas, static_cast<uint32_t>(ctas_env));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(std::min<uint32_t>(a.nitems, static_cast<uint32_t>(pl.sms) * std::max(1u, ctas)));
+    cfg.blockDim = dim3((ncw + 1) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    BF_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    return 0;
+  }
   const int ps = pair_stages();
   auto* kern = gauss_disabled() ? pair_kernel<2, kPairNcw, false>
                : ps == 4       ? pair_kernel<4, kPairNcw, true>
@@ -887,8 +972,22 @@ int run_down(const Plan& pl, const void* in, E* bufs[2], void* final_dst, uint32
   const int lead = adjoint ? BF_FACTOR_U : BF_FACTOR_V;
   const int down = adjoint ? BF_FACTOR_G : BF_FACTOR_H;
   int cur = 0;
-  int rc = timed_op<E>(rec, pl, lead, 0, 1, in, bufs[0], k, 0, st);
-  if (rc) return rc;
+  int rc = 0;
+  // rank-8 pairs: the lead leaf rides in the first pair (pair8_kernel<.., LEAF>), which then
+  // reads the chain input itself
+  bool leaf_fused = false;
+  PairGeo lpg{};
+  if constexpr (std::is_same<E, double2>::value) {
+    PairGeo pg0{};
+    const int lo0 = nl - 2;
+    if (!rec && lo0 >= 0 && !(lo0 == 0 && (remap >= 3 || peers)) && pair_geometry(pl, lo0, k, 1, &pg0) &&
+        !(lo0 == 0 && remap && (pg0.chunk || !remap_pair_enabled())) && pair8_leaf_geo(pl, pg0, k, 1, &lpg))
+      leaf_fused = true;
+  }
+  if (!leaf_fused) {
+    rc = timed_op<E>(rec, pl, lead, 0, 1, in, bufs[0], k, 0, st);
+    if (rc) return rc;
+  }
   for (int i = nl - 1; i >= 0; --i) {
     // levels i and i - 1 as one pair kernel (not in instrumented runs: per-level timing;
     // not for the remapped / pushed last level)
@@ -901,7 +1000,11 @@ int run_down(const Plan& pl, const void* in, E* bufs[2], void* final_dst, uint32
       void* dst = (lo == 0 && final_dst) ? final_dst : bufs[cur ^ 1];
       const void* fa = down == BF_FACTOR_G ? pl.g_lev[lo] : pl.h_lev[lo];
       const void* fb = down == BF_FACTOR_G ? pl.g_lev[i] : pl.h_lev[i];
-      rc = launch_pair(pl, fa, fb, lo, bufs[cur], dst, k, 1, pg, st, lo == 0 ? remap : 0);
+      if (leaf_fused && i == nl - 1)
+        rc = launch_pair(pl, fa, fb, lo, in, dst, k, 1, lpg, st, lo == 0 ? remap : 0,
+                         lead == BF_FACTOR_U ? pl.u_leaf : pl.v_leaf);
+      else
+        rc = launch_pair(pl, fa, fb, lo, bufs[cur], dst, k, 1, pg, st, lo == 0 ? remap : 0);
       if (rc) return rc;
       if (dst == bufs[cur ^ 1]) cur ^= 1;
       --i;
@@ -930,6 +1033,9 @@ int run_up(const Plan& pl, const void* mid, E* bufs[2], void* out, uint32_t k, i
     if (!rec && std::is_same<E, double2>::value && pair_geometry(pl, i, k, 0, &pg)) {
       const void* fa = up == BF_FACTOR_G ? pl.g_lev[i] : pl.h_lev[i];
       const void* fb = up == BF_FACTOR_G ? pl.g_lev[i + 1] : pl.h_lev[i + 1];
+      PairGeo lpg{};
+      if (i + 2 == nl && pair8_leaf_geo(pl, pg, k, 0, &lpg))   // the trail leaf rides in the last pair
+        return launch_pair(pl, fa, fb, i, src, out, k, 0, lpg, st, 0, trail == BF_FACTOR_U ? pl.u_leaf : pl.v_leaf);
       int rc = launch_pair(pl, fa, fb, i, src, bufs[nxt], k, 0, pg, st);
       if (rc) return rc;
       src = bufs[nxt];

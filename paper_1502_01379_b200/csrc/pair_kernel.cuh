@@ -34,6 +34,10 @@ struct PairArgs {
   int remap;
   uint32_t m, mr;        // middle nodes, rank of the middle vector
   const double* mid_w;
+  // rank-8 fast path with the leaf factor fused (pair8_kernel<.., LEAF>): leaf blocks
+  // (nb, 16, 8); adjoint pairs read `in` as the chain input g, forward pairs write `out`
+  // as the chain output (16 rows per leaf)
+  const double2* leaf;
 };
 
 // Destination element and weight of middle-vector entry e under the fused middle factor.
@@ -272,6 +276,311 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 2) pair_kernel(const PairArgs 
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     consumers_sync();  // mi is reused by the next item's first level
+  }
+}
+
+
+// ---------------------------------------------------------------- rank-8 fast path
+// The same pair for R = 8 (C = 16: BASELINE config 1) with every consumer warp owning one
+// (t, 16-column) slice of the item end to end, so the two levels need no block-wide
+// barrier and all tile geometry is compile-time:
+//   forward  warp (t, n): Y(t, 0), Y(t, 1) (level A, into its own rows of mi) then, after a
+//            __syncwarp, out(t, 0), out(t, 1) (level B reads only mi_t);
+//   adjoint  warp (t, n): mi_t (level B*, one 16 x 16 GEMM over both t'), a 64-thread named
+//            barrier with the other warp of its column slice, then out(u = t) (level A*
+//            reads rows u R .. of both mi_0 and mi_1), and the same barrier again before
+//            mi is rewritten.
+// The 4 k-steps of each GEMM are unrolled with pointer offsets only (no predicates: the
+// host takes this path when kc and k are multiples of 16). 3-multiplication complex
+// products as in pair_gemms. Producer and stage layout are pair_produce's.
+__device__ __forceinline__ void pair_bar(int id) {   // immediate ids: a register id reserves all 16 barriers
+  switch (id) {
+    case 1: asm volatile("bar.sync 1, 64;" ::: "memory"); break;
+    case 2: asm volatile("bar.sync 2, 64;" ::: "memory"); break;
+    case 3: asm volatile("bar.sync 3, 64;" ::: "memory"); break;
+    default: asm volatile("bar.sync 4, 64;" ::: "memory"); break;
+  }
+}
+
+// one complex k-step of an MT x 2 warp tile (8-row tiles i, 8-column tiles j)
+template <int MT>
+__device__ __forceinline__ void pair8_step(double (&t1)[MT][2][2], double (&t2)[MT][2][2], double (&t3)[MT][2][2],
+                                           const double (&ar)[MT], const double (&ai)[MT], const double2 b0,
+                                           const double2 b1) {
+  const double bs0 = b0.x + b0.y, bs1 = b1.x + b1.y;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    pair_dmma(t1[i][0][0], t1[i][0][1], ar[i], b0.x);
+    pair_dmma(t2[i][0][0], t2[i][0][1], ai[i], b0.y);
+    pair_dmma(t1[i][1][0], t1[i][1][1], ar[i], b1.x);
+    pair_dmma(t2[i][1][0], t2[i][1][1], ai[i], b1.y);
+  }
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const double as = ar[i] + ai[i];
+    pair_dmma(t3[i][0][0], t3[i][0][1], as, bs0);
+    pair_dmma(t3[i][1][0], t3[i][1][1], as, bs1);
+  }
+}
+
+// Producer of the leaf-fused rank-8 pair: the 8 transfer blocks (unpadded, whole-block
+// copies), the item's 4 leaf blocks (leaf b = ((2g + t) 2 + t') P_B + q, 16 x 8 each) and
+// the input rows — adjoint: the 4 x 16 rows of g under those leaves (chunk order [t][t']),
+// forward: the pair's 2 C rows as in pair_produce.
+template <bool ADJ>
+__device__ __forceinline__ void pair8_produce_leaf(const PairArgs& a, uint32_t item_rhs, double2* st, uint64_t* full,
+                                                   int lane, uint64_t pol) {
+  constexpr uint32_t R = 8, C = 16, N0 = 16;
+  const uint32_t pb = a.pa / 2;
+  const uint32_t item = item_rhs / a.nch, k0 = (item_rhs - item * a.nch) * a.kc, kw = min(a.kc, a.k - k0);
+  const uint32_t g = item / pb, q = item - g * pb;
+  const uint32_t nrows = ADJ ? 4 * N0 : 2 * C;
+  const uint32_t bytes = (8 * R * C + 4 * N0 * R + nrows * kw) * static_cast<uint32_t>(sizeof(double2));
+  if (lane == 0) mbar_arrive_expect_tx(full, bytes);
+  __syncwarp();
+  const uint32_t bb = R * C * static_cast<uint32_t>(sizeof(double2));
+  if (lane < 2) {
+    const uint32_t t = lane;
+    bulk_g2s(st + static_cast<size_t>(2 * t) * R * C, a.fac_a + static_cast<size_t>((g * 2 + t) * a.pa + 2 * q) * R * C,
+             2 * bb, full, pol);
+  } else if (lane < 6) {
+    const uint32_t b = lane + 2, t = (b >> 1) & 1, v = b & 1;
+    bulk_g2s(st + static_cast<size_t>(b) * R * C, a.fac_b + static_cast<size_t>(((2 * g + t) * 2 + v) * pb + q) * R * C,
+             bb, full, pol);
+  } else if (lane < 10) {
+    const uint32_t ch = lane - 6, t = ch >> 1, tp = ch & 1;
+    bulk_g2s(st + 8 * R * C + ch * N0 * R, a.leaf + static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q) * N0 * R, bb,
+             full, pol);
+  }
+  double2* vs = st + 8 * R * C + 4 * N0 * R;
+  for (uint32_t row = lane; row < nrows; row += 32) {
+    size_t grow;
+    if (!ADJ) {
+      grow = static_cast<size_t>(g * a.pa + 2 * q) * C + row;
+    } else {
+      const uint32_t ch = row / N0, rr = row - ch * N0, t = ch >> 1, tp = ch & 1;
+      grow = static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q) * N0 + rr;
+    }
+    bulk_g2s(vs + static_cast<size_t>(row) * a.vld, a.in + grow * a.k + k0, kw * static_cast<uint32_t>(sizeof(double2)),
+             full);
+  }
+}
+
+template <int STAGES, bool ADJ, int NCW, bool LEAF>
+__global__ void __launch_bounds__((NCW + 1) * 32, STAGES == 1 ? (NCW <= 4 ? (ADJ ? 3 : 4) : 2) : (NCW <= 4 ? 2 : 1))
+    pair8_kernel(const PairArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + STAGES;
+  double2* stage0 = reinterpret_cast<double2*>(smem_raw + 128);
+  double2* mi = stage0 + static_cast<size_t>(STAGES) * a.stage_elems;  // 2 C x vld intermediate
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int ncw = NCW;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], ncw);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  constexpr uint32_t R = 8, C = 16;
+  const uint32_t pb = a.pa / 2, KS = a.k;
+  const uint32_t fld = a.fld, vld = a.vld;
+  if (warp == ncw) {
+    const uint64_t pol = policy_evict_first();
+    uint32_t it = 0;
+    for (uint32_t item = blockIdx.x; item < a.nitems; item += gridDim.x, ++it) {
+      const uint32_t s = it % STAGES;
+      if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+      if constexpr (LEAF)
+        pair8_produce_leaf<ADJ>(a, item, stage0 + static_cast<size_t>(s) * a.stage_elems, &full[s], lane, pol);
+      else
+        pair_produce(a, item, stage0 + static_cast<size_t>(s) * a.stage_elems, &full[s], lane, pol);
+    }
+    return;
+  }
+  const uint32_t t = warp & 1, nn = warp >> 1, n0 = nn * 16;
+  const uint32_t lr = lane >> 2, lk = lane & 3;
+  uint32_t it = 0;
+  for (uint32_t item = blockIdx.x; item < a.nitems; item += gridDim.x, ++it) {
+    const uint32_t s = it % STAGES;
+    mbar_wait(&full[s], (it / STAGES) & 1);
+    double2* st = stage0 + static_cast<size_t>(s) * a.stage_elems;
+    const double2* lf = st + static_cast<size_t>(8) * R * fld;          // LEAF: 4 leaf blocks (16 x 8)
+    double2* vs = st + static_cast<size_t>(8) * R * fld + (LEAF ? 4 * 16 * R : 0);
+    constexpr uint32_t CH = (LEAF && ADJ) ? 16 : R;                      // rows per input chunk (adjoint)
+    const uint32_t pitem = item / a.nch, k0 = (item - pitem * a.nch) * a.kc;
+    const uint32_t K = min(a.kc, KS - k0);
+    const uint32_t g = pitem / pb, q = pitem - g * pb;
+    const bool act = n0 < K;   // K is a multiple of 16: a slice is whole or absent
+    if constexpr (!ADJ) {
+      if (act) {
+        // level A: Y(t, u) = B_A(g, t, 2q + u) X_u  ->  mi rows t C + u R + m
+#pragma unroll
+        for (uint32_t u = 0; u < 2; ++u) {
+          double t1[1][2][2] = {}, t2[1][2][2] = {}, t3[1][2][2] = {};
+          const double2* ap = st + static_cast<size_t>(2 * t + u) * R * fld + lr * fld + lk;
+          const double2* bp = vs + (u * C + lk) * vld + n0 + lr;
+#pragma unroll
+          for (int sk = 0; sk < 4; ++sk) {
+            const double2 av = ap[4 * sk];
+            const double ar[1] = {av.x}, ai[1] = {av.y};
+            pair8_step<1>(t1, t2, t3, ar, ai, bp[4 * sk * vld], bp[4 * sk * vld + 8]);
+          }
+          double2* mo = mi + (t * C + u * R + lr) * vld + n0 + 2 * lk;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq)
+              mo[8 * j + qq] = make_double2(t1[0][j][qq] - t2[0][j][qq], t3[0][j][qq] - t1[0][j][qq] - t2[0][j][qq]);
+        }
+        __syncwarp();
+        // level B: Y(t, t') = B_B(2g + t, t', q) mi_t  ->  out rows ((2g + t) 2 + t') P_B + q
+        double2 yb[2][2][2];   // LEAF: both t' results stay in registers until mi_t is free
+#pragma unroll
+        for (uint32_t tp = 0; tp < 2; ++tp) {
+          double t1[1][2][2] = {}, t2[1][2][2] = {}, t3[1][2][2] = {};
+          const double2* ap = st + static_cast<size_t>(4 + 2 * t + tp) * R * fld + lr * fld + lk;
+          const double2* bp = mi + (t * C + lk) * vld + n0 + lr;
+#pragma unroll
+          for (int sk = 0; sk < 4; ++sk) {
+            const double2 av = ap[4 * sk];
+            const double ar[1] = {av.x}, ai[1] = {av.y};
+            pair8_step<1>(t1, t2, t3, ar, ai, bp[4 * sk * vld], bp[4 * sk * vld + 8]);
+          }
+          double2* o = a.out + (static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q) * R + lr) * KS + k0 + n0 + 2 * lk;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq) {
+              const double2 v = make_double2(t1[0][j][qq] - t2[0][j][qq], t3[0][j][qq] - t1[0][j][qq] - t2[0][j][qq]);
+              if constexpr (LEAF)
+                yb[tp][j][qq] = v;
+              else
+                o[8 * j + qq] = v;
+            }
+        }
+        if constexpr (LEAF) {
+          // trail leaf (factors.py:49-56): rows of leaf b = U_b (16 x 8) Y(t, t'); Y goes through
+          // this warp's own rows of mi (every lane is past its level-B reads first)
+          __syncwarp();
+#pragma unroll
+          for (uint32_t tp = 0; tp < 2; ++tp) {
+            double2* mo = mi + (t * C + tp * R + lr) * vld + n0 + 2 * lk;
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int qq = 0; qq < 2; ++qq) mo[8 * j + qq] = yb[tp][j][qq];
+          }
+          __syncwarp();
+#pragma unroll
+          for (uint32_t tp = 0; tp < 2; ++tp) {
+            double t1[2][2][2] = {}, t2[2][2][2] = {}, t3[2][2][2] = {};
+            const double2* ap = lf + (2 * t + tp) * 16 * R + lr * R + lk;
+            const double2* bp = mi + (t * C + tp * R + lk) * vld + n0 + lr;
+#pragma unroll
+            for (int sk = 0; sk < 2; ++sk) {
+              const double2 a0 = ap[4 * sk], a1 = ap[8 * R + 4 * sk];
+              const double ar[2] = {a0.x, a1.x}, ai[2] = {a0.y, a1.y};
+              pair8_step<2>(t1, t2, t3, ar, ai, bp[4 * sk * vld], bp[4 * sk * vld + 8]);
+            }
+            const size_t b = static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              double2* o = a.out + (b * 16 + 8 * i + lr) * KS + k0 + n0 + 2 * lk;
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int qq = 0; qq < 2; ++qq)
+                  o[8 * j + qq] = make_double2(t1[i][j][qq] - t2[i][j][qq], t3[i][j][qq] - t1[i][j][qq] - t2[i][j][qq]);
+            }
+          }
+        }
+      }
+      __syncwarp();   // every lane is past its mi reads before the next item's level A
+      if (lane == 0) mbar_arrive(&empty[s]);
+    } else {
+      if (act) {
+        if constexpr (LEAF) {
+          // lead leaf adjoint (factors.py:49-56): c(t, t') = V_b^H (8 x 16) g_b, in place over
+          // the first 8 rows of this warp's own 16 x 16 slice of chunk (t, t')
+#pragma unroll
+          for (uint32_t tp = 0; tp < 2; ++tp) {
+            const uint32_t ch = t * 2 + tp;
+            double t1[1][2][2] = {}, t2[1][2][2] = {}, t3[1][2][2] = {};
+            const double2* ap = lf + ch * 16 * R + lk * R + lr;
+            const double2* bp = vs + (ch * 16 + lk) * vld + n0 + lr;
+#pragma unroll
+            for (int sk = 0; sk < 4; ++sk) {
+              const double2 av = ap[4 * sk * R];
+              const double ar[1] = {av.x}, ai[1] = {neg(av.y)};
+              pair8_step<1>(t1, t2, t3, ar, ai, bp[4 * sk * vld], bp[4 * sk * vld + 8]);
+            }
+            __syncwarp();   // every lane has read the chunk before its first rows are overwritten
+            double2* mo = vs + (ch * 16 + lr) * vld + n0 + 2 * lk;
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int qq = 0; qq < 2; ++qq)
+                mo[8 * j + qq] = make_double2(t1[0][j][qq] - t2[0][j][qq], t3[0][j][qq] - t1[0][j][qq] - t2[0][j][qq]);
+          }
+          __syncwarp();
+        }
+        // level B*: mi_t = sum_t' B_B(2g + t, t', q)^H in(2g + t, t', q)
+        double t1[2][2][2] = {}, t2[2][2][2] = {}, t3[2][2][2] = {};
+#pragma unroll
+        for (int sk = 0; sk < 4; ++sk) {
+          const uint32_t tp = sk >> 1, rho = (sk & 1) * 4 + lk;
+          const double2* ap = st + static_cast<size_t>(4 + 2 * t + tp) * R * fld + rho * fld + lr;
+          const double2* bp = vs + ((t * 2 + tp) * CH + rho) * vld + n0 + lr;
+          const double2 a0 = ap[0], a1 = ap[8];
+          const double ar[2] = {a0.x, a1.x}, ai[2] = {neg(a0.y), neg(a1.y)};  // A^H
+          pair8_step<2>(t1, t2, t3, ar, ai, bp[0], bp[8]);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          double2* mo = mi + (t * C + 8 * i + lr) * vld + n0 + 2 * lk;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq)
+              mo[8 * j + qq] = make_double2(t1[i][j][qq] - t2[i][j][qq], t3[i][j][qq] - t1[i][j][qq] - t2[i][j][qq]);
+        }
+      }
+      pair_bar(1 + static_cast<int>(nn));
+      if (act) {
+        // level A*: Y(u) = sum_t2 B_A(g, t2, 2q + u)^H mi_t2[u R ..]  ->  out rows (g P_A + 2q + u) C + c
+        const uint32_t u = t;
+        double t1[2][2][2] = {}, t2[2][2][2] = {}, t3[2][2][2] = {};
+#pragma unroll
+        for (int sk = 0; sk < 4; ++sk) {
+          const uint32_t tt = sk >> 1, rho = (sk & 1) * 4 + lk;
+          const double2* ap = st + static_cast<size_t>(2 * tt + u) * R * fld + rho * fld + lr;
+          const double2* bp = mi + (tt * C + u * R + rho) * vld + n0 + lr;
+          const double2 a0 = ap[0], a1 = ap[8];
+          const double ar[2] = {a0.x, a1.x}, ai[2] = {neg(a0.y), neg(a1.y)};
+          pair8_step<2>(t1, t2, t3, ar, ai, bp[0], bp[8]);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          double w;
+          const size_t e = pair_remap(a, static_cast<size_t>(g * a.pa + 2 * q + u) * C + 8 * i + lr, &w);
+          double2* o = a.out + e * KS + k0 + n0 + 2 * lk;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq)
+              o[8 * j + qq] = make_double2(w * (t1[i][j][qq] - t2[i][j][qq]), w * (t3[i][j][qq] - t1[i][j][qq] - t2[i][j][qq]));
+        }
+      }
+      if constexpr (LEAF) fence_proxy_async_smem();  // in-place leaf outputs before the next bulk copy into the stage
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      pair_bar(1 + static_cast<int>(nn));   // both warps of the slice are past their mi reads
+    }
   }
 }
 

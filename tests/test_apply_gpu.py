@@ -201,6 +201,32 @@ def test_remap_pair_opt_in(n, leaf, r, k):
     test_chunked_pairs_opt_in(n, leaf, r, k, env_flag="BF_REMAP_PAIR")
 
 
+@pytest.mark.parametrize("n,leaf,r,k", [
+    (1 << 16, 16, 8, 64),     # config 1: leaf-fused first / last pair, 32-RHS chunks
+    (1 << 12, 16, 8, 128),    # 64-RHS chunks (8 consumer warps), nl = 4
+    (1 << 10, 16, 8, 64),     # nl = 3 (odd): the up half ends in a single level, no fused trail leaf
+    (1 << 8, 16, 8, 64),      # nl = 2: one pair per half carries both the leaf and the middle factor
+    (1 << 12, 16, 8, 80),     # k a multiple of 16 whose chunk (40) is not: the general pair kernel
+    (1 << 12, 8, 8, 64),      # 8-point leaves: rank-8 pairs without the fused leaf
+])
+def test_rank8_pairs(n, leaf, r, k):
+    """Rank-8 level pairs (pair8_kernel: warp-owned slices, leaf factor fused into the pair
+    next to it) against the oracle, forward and adjoint; BF_NO_PAIR8_LEAF=1 and
+    BF_PAIR8_STAGES=1 (read once per process: child processes) give the same result."""
+    p = bf.make_partition(n, leaf)
+    f = synthetic_chain(p, r, seed=n + k)
+    oc = oracle_of(f)
+    g = complex_gaussian(np.random.default_rng(k), (n, k))
+    gd = torch.from_numpy(g).cuda()
+    assert rel(f.plan().apply(gd), ochain.apply(oc, g)) <= TOL128
+    assert rel(f.plan().apply(gd, adjoint=True), ochain.apply(oc, g, adjoint=True)) <= TOL128
+
+
+@pytest.mark.parametrize("flag", ["BF_NO_PAIR8_LEAF", "BF_NO_PAIR8"])
+def test_rank8_pairs_switches(flag):
+    test_chunked_pairs_opt_in(1 << 12, 16, 8, 64, env_flag=flag)
+
+
 def test_quadtree_t_range_split_many_rhs():
     """Many-RHS quadtree levels whose 4-block units do not fit a stage run as t-range
     launches (forward outputs per t, adjoint partial sums accumulated). The default
