@@ -720,7 +720,11 @@ bool pair_geometry(const Plan& pl, int i, uint32_t k, int adjoint, PairGeo* pg) 
   const uint64_t fld = fpad ? pad_to(C, adjoint ? 2 : 4) : C;
   pg->fld = static_cast<uint32_t>(fld);
   pg->chunk = false;
-  if (k <= 256) {  // whole right-hand-side range per stage (or k / 2 chunks), double-buffered
+  // rank 8 (pair8_kernel): 32-RHS chunks as independent items whatever k is
+  static const bool no_pair8 = env_int("BF_NO_PAIR8", 0) != 0;
+  static const int kc_env0 = env_int("BF_PAIR_KC", 0);
+  const bool p8 = R == 8 && !no_pair8 && !gauss_disabled() && k % 32 == 0 && kc_env0 <= 0;
+  if (k <= 256 || p8) {  // whole right-hand-side range per stage (or k / 2 chunks), double-buffered
     // BF_PAIR_VPAD=0: unpadded vector rows (whole-k items copy contiguous row runs; measured
     // slower: 4-way conflicts on the X fragments, cfg1 257.6 vs 239.4 us)
     static const bool vpad = env_int("BF_PAIR_VPAD", 1) != 0;
@@ -737,7 +741,9 @@ bool pair_geometry(const Plan& pl, int i, uint32_t k, int adjoint, PairGeo* pg) 
     // reading each pair's factor blocks once per chunk. BF_PAIR_KC overrides the chunk width.
     static const int kc_env = env_int("BF_PAIR_KC", 0);
     uint64_t kc = k, stage = 0;
-    if (kc_env > 0) {
+    if (p8) {
+      kc = 32;
+    } else if (kc_env > 0) {
       kc = std::min<uint64_t>(k, static_cast<uint64_t>(kc_env));
     } else if (2 * smem_for(k, &stage) > static_cast<uint64_t>(kMaxDynSmem) && k >= 64 &&
                2 * smem_for((k + 1) / 2, &stage) <= static_cast<uint64_t>(kMaxDynSmem)) {

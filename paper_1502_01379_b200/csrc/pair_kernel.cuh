@@ -135,13 +135,16 @@ __device__ __forceinline__ void pair_gemms(int ngemm, int M, int nseg, int klen,
 
 // Producer: the 8 blocks (level A: (t, u) = (t, p = 2q + u); level B: (t, t') of
 // g' = 2g + t) and the item's input vector rows, one bulk copy per row.
+// what: 1 = arm the barrier and copy the (constant) factor blocks, 2 = the vector rows,
+// 3 = both (the factor part may be issued before the dependency wait on the previous level).
 __device__ __forceinline__ void pair_produce(const PairArgs& a, uint32_t item_rhs, double2* st, uint64_t* full,
-                                             int lane, uint64_t pol) {
+                                             int lane, uint64_t pol, int what = 3) {
   const uint32_t R = a.r, C = 2 * a.r, pb = a.pa / 2;
   // items are (pair, right-hand-side chunk): chunks of one pair are independent columns
   const uint32_t item = item_rhs / a.nch, k0 = (item_rhs - item * a.nch) * a.kc, kw = min(a.kc, a.k - k0);
   const uint32_t g = item / pb, q = item - g * pb;
   const uint32_t bytes = (8 * R * C + 2 * C * kw) * static_cast<uint32_t>(sizeof(double2));
+  if (what & 1) {
   if (lane == 0) mbar_arrive_expect_tx(full, bytes);
   __syncwarp();
   // block rows: 8 blocks x R rows; smem block b = (level, t, u|t') at b * R * fld
@@ -164,6 +167,8 @@ __device__ __forceinline__ void pair_produce(const PairArgs& a, uint32_t item_rh
                                   : a.fac_b + (static_cast<size_t>(((2 * g + t) * 2 + v) * pb + q) * R + rr) * C;
     bulk_g2s(st + static_cast<size_t>(row) * a.fld, src, C * static_cast<uint32_t>(sizeof(double2)), full, pol);
   }
+  }
+  if (!(what & 2)) return;
   double2* vs = st + static_cast<size_t>(8) * R * a.fld;
   if (a.vld == kw && kw == a.k) {   // unpadded whole-k rows: contiguous row runs in one copy each
     const uint32_t rb = a.k * static_cast<uint32_t>(sizeof(double2));
@@ -329,29 +334,32 @@ __device__ __forceinline__ void pair8_step(double (&t1)[MT][2][2], double (&t2)[
 // forward: the pair's 2 C rows as in pair_produce.
 template <bool ADJ>
 __device__ __forceinline__ void pair8_produce_leaf(const PairArgs& a, uint32_t item_rhs, double2* st, uint64_t* full,
-                                                   int lane, uint64_t pol) {
+                                                   int lane, uint64_t pol, int what = 3) {
   constexpr uint32_t R = 8, C = 16, N0 = 16;
   const uint32_t pb = a.pa / 2;
   const uint32_t item = item_rhs / a.nch, k0 = (item_rhs - item * a.nch) * a.kc, kw = min(a.kc, a.k - k0);
   const uint32_t g = item / pb, q = item - g * pb;
   const uint32_t nrows = ADJ ? 4 * N0 : 2 * C;
   const uint32_t bytes = (8 * R * C + 4 * N0 * R + nrows * kw) * static_cast<uint32_t>(sizeof(double2));
-  if (lane == 0) mbar_arrive_expect_tx(full, bytes);
-  __syncwarp();
-  const uint32_t bb = R * C * static_cast<uint32_t>(sizeof(double2));
-  if (lane < 2) {
-    const uint32_t t = lane;
-    bulk_g2s(st + static_cast<size_t>(2 * t) * R * C, a.fac_a + static_cast<size_t>((g * 2 + t) * a.pa + 2 * q) * R * C,
-             2 * bb, full, pol);
-  } else if (lane < 6) {
-    const uint32_t b = lane + 2, t = (b >> 1) & 1, v = b & 1;
-    bulk_g2s(st + static_cast<size_t>(b) * R * C, a.fac_b + static_cast<size_t>(((2 * g + t) * 2 + v) * pb + q) * R * C,
-             bb, full, pol);
-  } else if (lane < 10) {
-    const uint32_t ch = lane - 6, t = ch >> 1, tp = ch & 1;
-    bulk_g2s(st + 8 * R * C + ch * N0 * R, a.leaf + static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q) * N0 * R, bb,
-             full, pol);
+  if (what & 1) {
+    if (lane == 0) mbar_arrive_expect_tx(full, bytes);
+    __syncwarp();
+    const uint32_t bb = R * C * static_cast<uint32_t>(sizeof(double2));
+    if (lane < 2) {
+      const uint32_t t = lane;
+      bulk_g2s(st + static_cast<size_t>(2 * t) * R * C,
+               a.fac_a + static_cast<size_t>((g * 2 + t) * a.pa + 2 * q) * R * C, 2 * bb, full, pol);
+    } else if (lane < 6) {
+      const uint32_t b = lane + 2, t = (b >> 1) & 1, v = b & 1;
+      bulk_g2s(st + static_cast<size_t>(b) * R * C,
+               a.fac_b + static_cast<size_t>(((2 * g + t) * 2 + v) * pb + q) * R * C, bb, full, pol);
+    } else if (lane < 10) {
+      const uint32_t ch = lane - 6, t = ch >> 1, tp = ch & 1;
+      bulk_g2s(st + 8 * R * C + ch * N0 * R, a.leaf + static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q) * N0 * R,
+               bb, full, pol);
+    }
   }
+  if (!(what & 2)) return;
   double2* vs = st + 8 * R * C + 4 * N0 * R;
   for (uint32_t row = lane; row < nrows; row += 32) {
     size_t grow;
@@ -384,24 +392,36 @@ __global__ void __launch_bounds__((NCW + 1) * 32, STAGES == 1 ? (NCW <= 4 ? (ADJ
     fence_mbar_init();
   }
   __syncthreads();
+  // programmatic dependent launch: only the (constant) factor blocks of the first stages
+  // are fetched before the wait on the previous level
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   constexpr uint32_t R = 8, C = 16;
   const uint32_t pb = a.pa / 2, KS = a.k;
   const uint32_t fld = a.fld, vld = a.vld;
   if (warp == ncw) {
     const uint64_t pol = policy_evict_first();
+    auto produce = [&](uint32_t item, uint32_t s, int what) {
+      if constexpr (LEAF)
+        pair8_produce_leaf<ADJ>(a, item, stage0 + static_cast<size_t>(s) * a.stage_elems, &full[s], lane, pol, what);
+      else
+        pair_produce(a, item, stage0 + static_cast<size_t>(s) * a.stage_elems, &full[s], lane, pol, what);
+    };
+    uint32_t pre = 0;
+    for (uint32_t item = blockIdx.x; item < a.nitems && pre < STAGES; item += gridDim.x, ++pre) produce(item, pre, 1);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     uint32_t it = 0;
     for (uint32_t item = blockIdx.x; item < a.nitems; item += gridDim.x, ++it) {
       const uint32_t s = it % STAGES;
-      if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-      if constexpr (LEAF)
-        pair8_produce_leaf<ADJ>(a, item, stage0 + static_cast<size_t>(s) * a.stage_elems, &full[s], lane, pol);
-      else
-        pair_produce(a, item, stage0 + static_cast<size_t>(s) * a.stage_elems, &full[s], lane, pol);
+      if (it >= STAGES) {
+        mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+        produce(item, s, 3);
+      } else {
+        produce(item, s, 2);
+      }
     }
     return;
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t t = warp & 1, nn = warp >> 1, n0 = nn * 16;
   const uint32_t lr = lane >> 2, lk = lane & 3;
   uint32_t it = 0;

@@ -208,6 +208,7 @@ def test_remap_pair_opt_in(n, leaf, r, k):
     (1 << 8, 16, 8, 64),      # nl = 2: one pair per half carries both the leaf and the middle factor
     (1 << 12, 16, 8, 80),     # k a multiple of 16 whose chunk (40) is not: the general pair kernel
     (1 << 12, 8, 8, 64),      # 8-point leaves: rank-8 pairs without the fused leaf
+    (1 << 12, 16, 8, 320),    # 10 chunks of 32 RHS
 ])
 def test_rank8_pairs(n, leaf, r, k):
     """Rank-8 level pairs (pair8_kernel: warp-owned slices, leaf factor fused into the pair
