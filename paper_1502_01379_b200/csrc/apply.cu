@@ -6,6 +6,7 @@
 //   adjoint:  U^L*  -> G^{L-1}* .. G^{h}*  -> M* -> H^{h} .. H^{L-1} -> V^L
 // with M (or M*) fused into the epilogue of the last adjoint-direction level.
 #include <algorithm>
+#include <vector>
 #include <type_traits>
 #include <cstdio>
 #include <cstdlib>
@@ -1413,42 +1414,61 @@ Plan part_view(const Plan& full, uint32_t part, uint32_t nparts) {
 // vector; chunk e's D2H overlaps the up half of chunk e+1.
 int plan_apply_host_pipelined(const Plan& pl, const void* in_host, void* out_host, void* din, void* dout, void* mid,
                               void* mid2, void* ws, uint32_t k, int adjoint, uint32_t chunks, cudaStream_t run,
-                              cudaStream_t cp, cudaEvent_t* ev) {
+                              cudaStream_t cp, cudaEvent_t* ev, uint32_t taper) {
   const uint64_t es = pl.elem();
-  const uint64_t rows_c = pl.n / chunks;
-  const uint64_t mid_rows_c = static_cast<uint64_t>(pl.m) * pl.m * pl.rank / chunks;
-  // ev[0]: fork; ev[1 .. chunks]: inputs landed; ev[chunks+1 .. 2 chunks]: outputs ready; ev[2 chunks+1]: join
+  const uint64_t mid_rows = static_cast<uint64_t>(pl.m) * pl.m * pl.rank;
+  // chunk c = part (first, second) of the middle nodes. Uniform: `chunks` equal parts.
+  // Tapered (taper = T): 1/T, 1/T, 2/T, ... 1/2 on the way down and the mirror image on
+  // the way up, so the first upload and the last download are short and most of the
+  // chain runs in large parts.
+  std::vector<std::pair<uint32_t, uint32_t>> down, up;
+  if (taper >= 4) {
+    down.push_back({0, taper});
+    for (uint32_t T = taper; T >= 2; T /= 2) down.push_back({1, T});
+    for (uint32_t T = 2; T <= taper; T *= 2) up.push_back({T - 2, T});
+    up.push_back({taper - 1, taper});
+  } else {
+    for (uint32_t c = 0; c < chunks; ++c) {
+      down.push_back({c, chunks});
+      up.push_back({c, chunks});
+    }
+  }
+  const uint32_t nc = static_cast<uint32_t>(down.size());
+  // ev[0]: fork; ev[1 .. nc]: inputs landed; ev[nc+1 .. 2 nc]: outputs ready; ev[2 nc+1]: join
   BF_CUDA(cudaEventRecord(ev[0], run));
   BF_CUDA(cudaStreamWaitEvent(cp, ev[0], 0));
-  for (uint32_t c = 0; c < chunks; ++c) {
-    const uint64_t off = c * rows_c * k * es;
+  for (uint32_t c = 0; c < nc; ++c) {
+    const uint64_t rows_c = pl.n / down[c].second;
+    const uint64_t off = down[c].first * rows_c * k * es;
     BF_CUDA(cudaMemcpyAsync(static_cast<char*>(din) + off, static_cast<const char*>(in_host) + off, rows_c * k * es,
                             cudaMemcpyHostToDevice, cp));
     BF_CUDA(cudaEventRecord(ev[1 + c], cp));
   }
-  for (uint32_t c = 0; c < chunks; ++c) {
+  for (uint32_t c = 0; c < nc; ++c) {
     BF_CUDA(cudaStreamWaitEvent(run, ev[1 + c], 0));
-    const Plan v = part_view(pl, c, chunks);
-    int rc = plan_apply_half(v, 0, static_cast<char*>(din) + c * rows_c * k * es,
-                             static_cast<char*>(mid) + c * mid_rows_c * k * es, k, adjoint, ws, run);
+    const Plan v = part_view(pl, down[c].first, down[c].second);
+    const uint64_t rows_c = pl.n / down[c].second, mid_c = mid_rows / down[c].second;
+    int rc = plan_apply_half(v, 0, static_cast<char*>(din) + down[c].first * rows_c * k * es,
+                             static_cast<char*>(mid) + down[c].first * mid_c * k * es, k, adjoint, ws, run);
     if (rc) return rc;
   }
   int rc = pl.dtype == BF_C128 ? launch_middle<double2>(pl, mid, mid2, k, adjoint, run)
                                : launch_middle<float2>(pl, mid, mid2, k, adjoint, run);
   if (rc) return rc;
-  for (uint32_t e = 0; e < chunks; ++e) {
-    const Plan v = part_view(pl, e, chunks);
-    const uint64_t off = e * rows_c * k * es;
-    rc = plan_apply_half(v, 1, static_cast<char*>(mid2) + e * mid_rows_c * k * es, static_cast<char*>(dout) + off, k,
-                         adjoint, ws, run);
+  for (uint32_t e = 0; e < nc; ++e) {
+    const Plan v = part_view(pl, up[e].first, up[e].second);
+    const uint64_t rows_c = pl.n / up[e].second, mid_c = mid_rows / up[e].second;
+    const uint64_t off = up[e].first * rows_c * k * es;
+    rc = plan_apply_half(v, 1, static_cast<char*>(mid2) + up[e].first * mid_c * k * es, static_cast<char*>(dout) + off,
+                         k, adjoint, ws, run);
     if (rc) return rc;
-    BF_CUDA(cudaEventRecord(ev[1 + chunks + e], run));
-    BF_CUDA(cudaStreamWaitEvent(cp, ev[1 + chunks + e], 0));
+    BF_CUDA(cudaEventRecord(ev[1 + nc + e], run));
+    BF_CUDA(cudaStreamWaitEvent(cp, ev[1 + nc + e], 0));
     BF_CUDA(cudaMemcpyAsync(static_cast<char*>(out_host) + off, static_cast<char*>(dout) + off, rows_c * k * es,
                             cudaMemcpyDeviceToHost, cp));
   }
-  BF_CUDA(cudaEventRecord(ev[1 + 2 * chunks], cp));
-  BF_CUDA(cudaStreamWaitEvent(run, ev[1 + 2 * chunks], 0));
+  BF_CUDA(cudaEventRecord(ev[1 + 2 * nc], cp));
+  BF_CUDA(cudaStreamWaitEvent(run, ev[1 + 2 * nc], 0));
   return 0;
 }
 

@@ -466,6 +466,20 @@ int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint
     const long v = strtol(env, nullptr, 10);
     if (v >= 1 && v <= static_cast<long>(p.m) && (v & (v - 1)) == 0) chunks = static_cast<uint32_t>(v);
   }
+  // tapered parts (1/T, 1/T, 2/T, ... 1/2 down, the mirror image up): the first upload and the
+  // last download are 1/T of the vector and most of the chain runs in large parts.
+  // BF_PIPE_TAPER=0 keeps `chunks` equal parts; setting BF_PIPE_CHUNKS does too.
+  uint32_t taper = (p.m >= 8 && !getenv("BF_PIPE_CHUNKS")) ? 8 : 0;
+  if (const char* env = getenv("BF_PIPE_TAPER")) {
+    const long v = strtol(env, nullptr, 10);
+    taper = (v >= 4 && v <= static_cast<long>(p.m) && (v & (v - 1)) == 0) ? static_cast<uint32_t>(v) : 0;
+  }
+  uint32_t nchunk = chunks, biggest = chunks;   // number of parts; the largest part is 1/biggest
+  if (taper) {
+    nchunk = 1;
+    for (uint32_t T = taper; T >= 2; T /= 2) ++nchunk;
+    biggest = 2;
+  }
   // (graph capture of a memcpy needs page-locked host memory)
   auto pinned = [](const void* ptr) {
     cudaPointerAttributes at{};
@@ -478,7 +492,7 @@ int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint
   const bool pipelined =
       plan->graphs_enabled && chunks > 1 && io >= (4ull << 20) && pinned(in_host) && pinned(out_host);
   const uint64_t mid_bytes = static_cast<uint64_t>(p.m) * p.m * p.rank * k * p.elem();
-  const uint64_t need_ws = pipelined ? 2 * mid_bytes + 2 * (p.dim_max / chunks) * k * p.elem() : wsb;
+  const uint64_t need_ws = pipelined ? 2 * mid_bytes + 2 * (p.dim_max / biggest) * k * p.elem() : wsb;
   if (plan->host_io_bytes < io || plan->host_ws_bytes < need_ws) {
     BF_CUDA(cudaStreamSynchronize(run));
     // every cached graph that captured the old device buffers would replay against freed
@@ -497,11 +511,11 @@ int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint
   }
   if (pipelined) {
     if (!plan->copy_stream) BF_CUDA(cudaStreamCreateWithFlags(&plan->copy_stream, cudaStreamNonBlocking));
-    if (plan->pipe_events.size() < 2 * chunks + 2) {  // BF_PIPE_CHUNKS is re-read on every call
+    if (plan->pipe_events.size() < 2 * nchunk + 2) {  // BF_PIPE_CHUNKS is re-read on every call
       BF_CUDA(cudaStreamSynchronize(run));
       drop_graphs_locked(plan);  // captured graphs reference the old events
       for (auto e : plan->pipe_events) cudaEventDestroy(e);
-      plan->pipe_events.assign(2 * chunks + 2, nullptr);
+      plan->pipe_events.assign(2 * nchunk + 2, nullptr);
       for (auto& e : plan->pipe_events) BF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     void* const key_ws = reinterpret_cast<void*>(static_cast<uintptr_t>(1));  // marks the pipelined graph
@@ -516,7 +530,7 @@ int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint
     BF_CUDA(cudaStreamBeginCapture(run, cudaStreamCaptureModeThreadLocal));
     const int rc = plan_apply_host_pipelined(p, in_host, out_host, plan->host_in, plan->host_out, w, w + mid_bytes,
                                              w + 2 * mid_bytes, k, adjoint ? 1 : 0, chunks, run, plan->copy_stream,
-                                             plan->pipe_events.data());
+                                             plan->pipe_events.data(), taper);
     cudaGraph_t graph = nullptr;
     const cudaError_t e = cudaStreamEndCapture(run, &graph);
     if (rc) {

@@ -70,7 +70,7 @@ int plan_middle_exchange(const Plan& pl, int unpack, const void* in, void* out, 
 Plan part_view(const Plan& full, uint32_t part, uint32_t nparts);
 int plan_apply_host_pipelined(const Plan& pl, const void* in_host, void* out_host, void* din, void* dout, void* mid,
                               void* mid2, void* ws, uint32_t k, int adjoint, uint32_t chunks, cudaStream_t run,
-                              cudaStream_t cp, cudaEvent_t* ev);
+                              cudaStream_t cp, cudaEvent_t* ev, uint32_t taper = 0);
 int plan_apply_factor(const Plan& pl, int which, int lvl_idx, int adjoint, const void* in, void* out, uint32_t k,
                       cudaStream_t st);
 int entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr, const int64_t* cols, uint32_t nc, void* out,
