@@ -337,6 +337,148 @@ __global__ void __launch_bounds__(512, 1) k_pivot_wide_cl(MidArgs a, int which) 
   }
 }
 
+// Register form of k_pivot_wide_cl for r <= 16 and at most one column per thread
+// (side / CL <= 512: every cluster shape launch_pivot_wide uses): the projection rows
+// never touch global memory — a thread keeps its own column's projections P_lc in
+// registers, the pivot column's P_lj travel with the pick through distributed shared
+// memory — and a pick costs ONE cluster barrier: every CTA publishes its maximum, its
+// first column within the tie threshold of that maximum, that column's norm and
+// projections; with thr = best (1 - 2 tie) the global pick is the first published column
+// of a CTA whose maximum reaches thr. Only when some CTA's maximum reaches thr but its
+// published column does not (a near-tie between different columns of one CTA) does that
+// pick fall back to the two-barrier exchange with the global threshold. With no global
+// stores inside the loop the barrier's release fence has nothing to flush (ncu:
+// membar + barrier stalls 22% of k_pivot_wide_cl). The arithmetic of every column is
+// k_pivot_wide's, term for term, so picks are bitwise identical.
+constexpr int kPivReg = 16;
+
+template <int CL>
+__global__ void __launch_bounds__(512, 1) k_pivot_wide_cl2(MidArgs a, int which) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cr = static_cast<int>(cluster.block_rank());
+  const int blk = blockIdx.x / CL;
+  const int ncols = static_cast<int>(a.side);
+  const int c0 = cr * ncols / CL, c1 = (cr + 1) * ncols / CL, nloc = c1 - c0;
+  extern __shared__ double2 pcs[];               // own columns' projections P_lc: [l][thread]
+  __shared__ double2 q[kSetCap];
+  __shared__ double red[32];
+  __shared__ int redi[32];
+  __shared__ double cl_val[2][CL];               // per-CTA maxima (double-buffered by pick parity)
+  __shared__ int cl_idx[2][CL];                  // per-CTA first column within the tie of its maximum
+  __shared__ double cl_nrm[2][CL];               // its norm
+  __shared__ double2 cl_pc[2][CL][kPivReg];      // and its projections
+  __shared__ double2 mypc[kPivReg];
+  __shared__ int picks[kSetCap];
+  __shared__ double s_norm;
+  BlockState& s = a.st[blk];
+  const int nr = which == kRows ? s.nrows : s.ncols;
+  const bool pairwise = which == kCols;
+  const double2* W = a.wide + static_cast<int64_t>(blk) * a.S * a.side;
+  const int tid = threadIdx.x;
+  const bool own = tid < nloc;
+  const int c = c0 + tid;
+  double norm = 0.0;
+  if (own) {
+    auto get = [&](int i) { return abs2(W[static_cast<int64_t>(i) * ncols + c]); };
+    norm = pairwise ? pairwise_sum(get, 0, nr) : sequential_sum(get, nr);
+  }
+  double2* pc = pcs + tid;                       // pc[l * 512]
+  const int k = min(a.r, min(nr, ncols));
+  cluster.sync();  // every CTA of the cluster is running before any DSMEM store
+  int npick = 0;
+  // publish this CTA's candidate for a threshold factor: maximum, first column >= thr_of(max)
+  auto publish = [&](int par, double thr_in, bool use_thr_in) {
+    const double lm = block_max(own ? norm : 0.0, red);
+    const double thr = use_thr_in ? thr_in : __dmul_rn(lm, 1.0 - 2.0 * kPivotTie);
+    int li = (own && norm >= thr && lm > 0.0) ? tid : INT_MAX;
+    li = block_min_int(li, redi);
+    if (tid == li) s_norm = norm;
+    if (li != INT_MAX && tid < npick) mypc[tid] = pcs[tid * 512 + li];
+    __syncthreads();
+    if (tid < CL) {
+      *cluster.map_shared_rank(&cl_val[par][cr], tid) = lm;
+      *cluster.map_shared_rank(&cl_idx[par][cr], tid) = li == INT_MAX ? INT_MAX : c0 + li;
+      *cluster.map_shared_rank(&cl_nrm[par][cr], tid) = li == INT_MAX ? 0.0 : s_norm;
+    }
+    if (li != INT_MAX && tid >= 32 && tid < 32 + CL * kPivReg) {
+      const int d = (tid - 32) / kPivReg, l = (tid - 32) % kPivReg;
+      if (l < npick) *cluster.map_shared_rank(&cl_pc[par][cr][l], d) = mypc[l];
+    }
+  };
+  int par = 0;
+  for (int it = 0; it < k; ++it) {
+    publish(par, 0.0, false);
+    cluster.sync();
+    double best = 0.0;
+#pragma unroll
+    for (int x = 0; x < CL; ++x) best = fmax(best, cl_val[par][x]);
+    if (best <= 0.0) break;  // rel_tol = 0 in the sweeps (lowrank.py:237-243); identical in every CTA
+    const double thr = __dmul_rn(best, 1.0 - 2.0 * kPivotTie);
+    bool ambiguous = false;
+#pragma unroll
+    for (int x = 0; x < CL; ++x) ambiguous |= cl_val[par][x] >= thr && !(cl_nrm[par][x] >= thr);
+    int usepar = par;
+    if (ambiguous) {  // (uniform across the cluster) republish with the global threshold
+      usepar = par ^ 1;
+      cluster.sync();   // every CTA has read this pick's first round before the other buffer is rewritten
+      publish(usepar, thr, true);
+      cluster.sync();
+    }
+    int j = INT_MAX, xo = 0;
+#pragma unroll
+    for (int x = 0; x < CL; ++x)
+      if (cl_val[usepar][x] >= thr && cl_idx[usepar][x] < j) {
+        j = cl_idx[usepar][x];
+        xo = x;
+      }
+    const double nj = cl_nrm[usepar][xo];
+    const double sq = sqrt(nj);
+    for (int i = tid; i < nr; i += blockDim.x) q[i] = W[static_cast<int64_t>(i) * ncols + j];
+    if (tid == 0) picks[npick] = j;
+    __syncthreads();
+    if (own) {
+      double2 g = make_double2(0, 0);
+#pragma unroll 8
+      for (int i = 0; i < nr; ++i) {
+        const double2 t = cmulc(q[i], W[static_cast<int64_t>(i) * ncols + c]);
+        g.x += t.x;
+        g.y += t.y;
+      }
+      for (int l = 0; l < npick; ++l) {
+        const double2 t = cmulc(cl_pc[usepar][xo][l], pc[l * 512]);
+        g.x -= t.x;
+        g.y -= t.y;
+      }
+      const double2 pr = make_double2(__ddiv_rn(g.x, sq), __ddiv_rn(g.y, sq));
+      pc[npick * 512] = pr;
+      norm = fmax(__dsub_rn(norm, abs2(pr)), 0.0);
+      if (c == j) norm = 0.0;
+    }
+    ++npick;
+    if (ambiguous) {
+      // both buffers were used by this pick: resynchronise before either is rewritten
+      cluster.sync();
+    } else {
+      par ^= 1;
+    }
+    __syncthreads();   // q and the candidate buffers are free for the next pick
+  }
+  cluster.sync();  // no CTA exits while its shared memory may still be written
+  if (cr == 0 && tid == 0) {
+    int32_t* sk = which == kRows ? s.skc : s.skr;
+    for (int i = 0; i < npick; ++i) {
+      int rank = 0;
+      for (int m = 0; m < npick; ++m) rank += picks[m] < picks[i];
+      sk[rank] = picks[i];
+    }
+    if (which == kRows)
+      s.nskc = npick;
+    else
+      s.nskr = npick;
+  }
+}
+
 // Standalone batched pivot selection (bf_select_pivots): matrices (batch, m, n)
 // complex128 row-major, m <= kSetCap, copied to scratch then pivoted in place.
 __global__ void k_select_pivots(const double2* A, double2* scratch, int m, int n, int k, double rel_tol, int pairwise,
@@ -1652,9 +1794,14 @@ int env_int_c(const char* name, int dflt) {
 // 148/CL blocks' samples are live in L2; BF_NO_PIVOT_CLUSTER=1 keeps one CTA per block.
 template <int CL>
 cudaError_t launch_pivot_cl(const MidArgs& a, int which, int nblocks, cudaStream_t st) {
-  auto* kern = k_pivot_wide_cl<CL>;
+  // register form (one barrier per pick, no global projection rows) when it applies;
+  // BF_PIVOT_CL2=0 keeps the two-barrier kernel
+  static const bool cl2 = env_int_c("BF_PIVOT_CL2", 1) != 0;
+  const bool use2 = cl2 && a.r <= kPivReg && a.side / CL <= 512;
+  void (*kern)(MidArgs, int) = use2 ? k_pivot_wide_cl2<CL> : k_pivot_wide_cl<CL>;
   const int per_sm = std::max(1, std::min(4, env_int_c("BF_PIVOT_CTAS_PER_SM", 1)));
-  const size_t need = static_cast<size_t>((a.side / CL + 2) * sizeof(double) + kSetCap * sizeof(double2) + 32 * 8 + 32 * 4);
+  const size_t need = use2 ? static_cast<size_t>(kPivReg) * 512 * sizeof(double2)
+                           : static_cast<size_t>((a.side / CL + 2) * sizeof(double) + kSetCap * sizeof(double2) + 32 * 8 + 32 * 4);
   const size_t smem = std::max(need, static_cast<size_t>(228 * 1024 / (per_sm + 1) + 1024));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
