@@ -14,6 +14,7 @@
 
 #include "level_kernel.cuh"
 #include "pair_kernel.cuh"
+#include "pair16_kernel.cuh"
 #include "node_mma.cuh"
 #include "tc_kernel.cuh"
 #include "wide_kernel.cuh"
@@ -863,6 +864,76 @@ bool pair8_leaf_geo(const Plan& pl, const PairGeo& pg, uint32_t k, int adjoint, 
   return best > 0;
 }
 
+// Rank-16 pairs with register-fed factors (pair16_kernel.cuh): shared memory holds only
+// the item's vectors (64 rows x 32 right-hand sides per stage) and the pair's intermediate,
+// so two CTAs share an SM. Opt-in (BF_PAIR16=1; 2 = forward pairs only): at config 2 with 256
+// right-hand sides a pair moves 10.0 GB of DRAM traffic instead of 18.2 GB for its two levels,
+// but runs 4.17 ms forward (DMMA pipe 67%) and 5.3 ms adjoint (51%: its two-block K ranges
+// spill registers) against 2 x 2.17 ms — 42.3 vs 38.2 ms per apply. BF_PAIR16_STAGES=3
+// deepens the ring (one CTA per SM: 60.7 ms).
+bool pair16_geometry(const Plan& pl, int i, uint32_t k, int adjoint, PairGeo* pg) {
+  static const int mode = env_int("BF_PAIR16", 0);
+  static const int kmin = env_int("BF_PAIR16_MIN_K", 64);
+  const bool off = mode == 0 || (mode == 2 && adjoint);
+  if (off || pair_disabled() || gauss_disabled() || pl.dtype != BF_C128 || pl.branch != 2 || pl.rank != 16) return false;
+  if (k < static_cast<uint32_t>(kmin) || k % 32 != 0) return false;
+  if (i < 0 || i + 1 >= static_cast<int>(pl.nlev)) return false;
+  const LevelGeo& A = pl.lev[i];
+  const LevelGeo& B = pl.lev[i + 1];
+  if (!A.splits || !B.splits || A.P < 2 || B.G != 2 * A.G || 2 * B.P != A.P) return false;
+  static const int stages = env_int("BF_PAIR16_STAGES", 2) == 3 ? 3 : 2;
+  pg->fld = 32;
+  pg->vld = 34;
+  pg->stage_elems = 64 * 34;
+  pg->kc = 32;
+  pg->nch = k / 32;
+  pg->stages = static_cast<uint32_t>(stages);
+  pg->smem = 128 + static_cast<size_t>(stages + 1) * pg->stage_elems * sizeof(double2);
+  pg->chunk = false;
+  pg->ctas = stages == 2 ? 2 : 1;
+  return true;
+}
+
+int launch_pair16(const Plan& pl, const void* fac_a, const void* fac_b, int i, const void* in, void* out, uint32_t k,
+                  int adjoint, const PairGeo& pg, cudaStream_t st, int remap) {
+  const LevelGeo& A = pl.lev[i];
+  PairArgs a{};
+  a.fac_a = static_cast<const double2*>(fac_a);
+  a.fac_b = static_cast<const double2*>(fac_b);
+  a.in = static_cast<const double2*>(in);
+  a.out = static_cast<double2*>(out);
+  a.r = pl.rank;
+  a.ga = static_cast<uint32_t>(A.G);
+  a.pa = static_cast<uint32_t>(A.P);
+  a.k = k;
+  a.kc = pg.kc;
+  a.nch = pg.nch;
+  a.adjoint = adjoint;
+  a.nitems = static_cast<uint32_t>(A.G * A.P / 2 * pg.nch);
+  a.fld = pg.fld;
+  a.vld = pg.vld;
+  a.stage_elems = pg.stage_elems;
+  a.remap = remap;
+  a.m = pl.m;
+  a.mr = pl.rank;
+  a.mid_w = static_cast<const double*>(pl.weights);
+  void (*kern)(const PairArgs) = pg.stages == 3 ? (adjoint ? pair16_kernel<3, true> : pair16_kernel<3, false>)
+                                                : (adjoint ? pair16_kernel<2, true> : pair16_kernel<2, false>);
+  BF_CUDA(allow_max_dyn_smem(kern));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min<uint32_t>(a.nitems, static_cast<uint32_t>(pl.sms) * pg.ctas));
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = pg.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BF_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  return 0;
+}
+
 int launch_pair(const Plan& pl, const void* fac_a, const void* fac_b, int i, const void* in, void* out, uint32_t k,
                 int adjoint, const PairGeo& pg, cudaStream_t st, int remap = 0, const void* leaf = nullptr) {
   if (pg.chunk) return launch_pair_chunk(pl, fac_a, fac_b, i, in, out, k, adjoint, pg, st);
@@ -1000,6 +1071,17 @@ int run_down(const Plan& pl, const void* in, E* bufs[2], void* final_dst, uint32
     // not for the remapped / pushed last level)
     PairGeo pg{};
     const int lo = i - 1;
+    if (!rec && std::is_same<E, double2>::value && lo >= 0 && !(lo == 0 && (remap >= 3 || peers)) &&
+        pair16_geometry(pl, lo, k, 1, &pg)) {
+      void* dst = (lo == 0 && final_dst) ? final_dst : bufs[cur ^ 1];
+      const void* fa = down == BF_FACTOR_G ? pl.g_lev[lo] : pl.h_lev[lo];
+      const void* fb = down == BF_FACTOR_G ? pl.g_lev[i] : pl.h_lev[i];
+      rc = launch_pair16(pl, fa, fb, lo, bufs[cur], dst, k, 1, pg, st, lo == 0 ? remap : 0);
+      if (rc) return rc;
+      if (dst == bufs[cur ^ 1]) cur ^= 1;
+      --i;
+      continue;
+    }
     // (the last pair may carry the fused middle factor, remap 1/2, not the peer push;
     // the k-chunked pair kernel has no remap epilogue)
     if (!rec && std::is_same<E, double2>::value && lo >= 0 && !(lo == 0 && (remap >= 3 || peers)) &&
@@ -1037,6 +1119,16 @@ int run_up(const Plan& pl, const void* mid, E* bufs[2], void* out, uint32_t k, i
   int nxt = (mid == bufs[0]) ? 1 : 0;
   for (int i = 0; i < nl; ++i) {
     PairGeo pg{};
+    if (!rec && std::is_same<E, double2>::value && pair16_geometry(pl, i, k, 0, &pg)) {
+      const void* fa = up == BF_FACTOR_G ? pl.g_lev[i] : pl.h_lev[i];
+      const void* fb = up == BF_FACTOR_G ? pl.g_lev[i + 1] : pl.h_lev[i + 1];
+      int rc = launch_pair16(pl, fa, fb, i, src, bufs[nxt], k, 0, pg, st, 0);
+      if (rc) return rc;
+      src = bufs[nxt];
+      nxt ^= 1;
+      ++i;
+      continue;
+    }
     if (!rec && std::is_same<E, double2>::value && pair_geometry(pl, i, k, 0, &pg)) {
       const void* fa = up == BF_FACTOR_G ? pl.g_lev[i] : pl.h_lev[i];
       const void* fb = up == BF_FACTOR_G ? pl.g_lev[i + 1] : pl.h_lev[i + 1];

@@ -223,6 +223,14 @@ def test_rank8_pairs(n, leaf, r, k):
     assert rel(f.plan().apply(gd, adjoint=True), ochain.apply(oc, g, adjoint=True)) <= TOL128
 
 
+@pytest.mark.parametrize("n,leaf,r,k", [(1 << 14, 16, 16, 64), (1 << 12, 16, 16, 256), (1 << 10, 16, 16, 96)])
+def test_rank16_pairs_opt_in(n, leaf, r, k):
+    """Rank-16 level pairs with register-fed factor fragments (pair16_kernel, BF_PAIR16=1: read
+    once per process, hence a child process), forward and adjoint, including the fused middle
+    factor in the down half's last pair."""
+    test_chunked_pairs_opt_in(n, leaf, r, k, env_flag="BF_PAIR16")
+
+
 @pytest.mark.parametrize("flag", ["BF_NO_PAIR8_LEAF", "BF_NO_PAIR8"])
 def test_rank8_pairs_switches(flag):
     test_chunked_pairs_opt_in(1 << 12, 16, 8, 64, env_flag=flag)
