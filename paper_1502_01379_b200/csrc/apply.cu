@@ -1018,13 +1018,18 @@ int launch_pair(const Plan& pl, const void* fac_a, const void* fac_b, int i, con
 // One factor op, dispatched by kind. `lvl_idx` indexes the plan's level table.
 template <typename E>
 int factor_op(const Plan& pl, int which, int lvl_idx, int adjoint, const void* in, void* out, uint32_t k, int remap,
-              cudaStream_t st, void* const* peers = nullptr) {
+              cudaStream_t st, void* const* peers = nullptr, bool fold = false) {
   if (which == BF_FACTOR_V || which == BF_FACTOR_U) {
     const void* fac = which == BF_FACTOR_V ? pl.v_leaf : pl.u_leaf;
     return launch_level<E>(pl, fac, pl.leaf_n0, pl.rank, 1, 1, pl.leaf_nb, in, out, k, adjoint, 0, st);
   }
   if (which == BF_FACTOR_M) return launch_middle<E>(pl, in, out, k, adjoint, st);
   const LevelGeo& lg = pl.lev[lvl_idx];
+  if (fold) {  // the outermost level with its leaf factor folded in: blocks (n0 x C)
+    const void* fac = which == BF_FACTOR_G ? pl.g_fold : pl.h_fold;
+    return launch_level<E>(pl, fac, pl.leaf_n0, pl.branch * pl.rank, lg.splits ? pl.branch : 1, lg.P, lg.G * lg.P, in,
+                           out, k, adjoint, remap, st, peers);
+  }
   const void* fac = which == BF_FACTOR_G ? pl.g_lev[lvl_idx] : pl.h_lev[lvl_idx];
   return launch_level<E>(pl, fac, pl.rank, pl.branch * pl.rank, lg.splits ? pl.branch : 1, lg.P, lg.G * lg.P, in, out,
                          k, adjoint, remap, st, peers);
@@ -1032,9 +1037,9 @@ int factor_op(const Plan& pl, int which, int lvl_idx, int adjoint, const void* i
 
 template <typename E>
 int timed_op(LaunchRecorder* rec, const Plan& pl, int which, int lvl_idx, int adjoint, const void* in, void* out,
-             uint32_t k, int remap, cudaStream_t st, void* const* peers = nullptr) {
+             uint32_t k, int remap, cudaStream_t st, void* const* peers = nullptr, bool fold = false) {
   int rc = rec ? rec->before(st) : 0;
-  if (!rc) rc = factor_op<E>(pl, which, lvl_idx, adjoint, in, out, k, remap, st, peers);
+  if (!rc) rc = factor_op<E>(pl, which, lvl_idx, adjoint, in, out, k, remap, st, peers, fold);
   if (!rc && rec) rc = rec->after(st);
   return rc;
 }
@@ -1062,7 +1067,20 @@ int run_down(const Plan& pl, const void* in, E* bufs[2], void* final_dst, uint32
         !(lo0 == 0 && remap && (pg0.chunk || !remap_pair_enabled())) && pair8_leaf_geo(pl, pg0, k, 1, &lpg))
       leaf_fused = true;
   }
-  if (!leaf_fused) {
+  // otherwise the folded outermost level (plan_fold_leaves) reads the chain input, unless
+  // that level runs inside a pair kernel (uniform block shapes)
+  bool fold = false;
+  if (!leaf_fused && pl.h_fold && nl >= 1) {
+    PairGeo pgf{};
+    const int lo0 = nl - 2;
+    bool paired = false;
+    if constexpr (std::is_same<E, double2>::value)
+      paired = !rec && lo0 >= 0 && !(lo0 == 0 && (remap >= 3 || peers)) &&
+               (pair16_geometry(pl, lo0, k, 1, &pgf) ||
+                (pair_geometry(pl, lo0, k, 1, &pgf) && !(lo0 == 0 && remap && (pgf.chunk || !remap_pair_enabled()))));
+    fold = !paired;
+  }
+  if (!leaf_fused && !fold) {
     rc = timed_op<E>(rec, pl, lead, 0, 1, in, bufs[0], k, 0, st);
     if (rc) return rc;
   }
@@ -1071,7 +1089,8 @@ int run_down(const Plan& pl, const void* in, E* bufs[2], void* final_dst, uint32
     // not for the remapped / pushed last level)
     PairGeo pg{};
     const int lo = i - 1;
-    if (!rec && std::is_same<E, double2>::value && lo >= 0 && !(lo == 0 && (remap >= 3 || peers)) &&
+    const bool may_pair = !(fold && i == nl - 1);   // the folded level has its own block shape
+    if (may_pair && !rec && std::is_same<E, double2>::value && lo >= 0 && !(lo == 0 && (remap >= 3 || peers)) &&
         pair16_geometry(pl, lo, k, 1, &pg)) {
       void* dst = (lo == 0 && final_dst) ? final_dst : bufs[cur ^ 1];
       const void* fa = down == BF_FACTOR_G ? pl.g_lev[lo] : pl.h_lev[lo];
@@ -1084,7 +1103,7 @@ int run_down(const Plan& pl, const void* in, E* bufs[2], void* final_dst, uint32
     }
     // (the last pair may carry the fused middle factor, remap 1/2, not the peer push;
     // the k-chunked pair kernel has no remap epilogue)
-    if (!rec && std::is_same<E, double2>::value && lo >= 0 && !(lo == 0 && (remap >= 3 || peers)) &&
+    if (may_pair && !rec && std::is_same<E, double2>::value && lo >= 0 && !(lo == 0 && (remap >= 3 || peers)) &&
         pair_geometry(pl, lo, k, 1, &pg) && !(lo == 0 && remap && (pg.chunk || !remap_pair_enabled()))) {
       void* dst = (lo == 0 && final_dst) ? final_dst : bufs[cur ^ 1];
       const void* fa = down == BF_FACTOR_G ? pl.g_lev[lo] : pl.h_lev[lo];
@@ -1100,6 +1119,13 @@ int run_down(const Plan& pl, const void* in, E* bufs[2], void* final_dst, uint32
       continue;
     }
     void* dst = (i == 0 && final_dst) ? final_dst : bufs[cur ^ 1];
+    if (fold && i == nl - 1) {   // first op of the half: reads the chain input, lands in bufs[0] (or final_dst)
+      if (dst == bufs[cur ^ 1]) dst = bufs[0];
+      rc = timed_op<E>(rec, pl, down, i, 1, in, dst, k, i == 0 ? remap : 0, st, i == 0 ? peers : nullptr, true);
+      if (rc) return rc;
+      cur = 0;
+      continue;
+    }
     rc = timed_op<E>(rec, pl, down, i, 1, bufs[cur], dst, k, i == 0 ? remap : 0, st, i == 0 ? peers : nullptr);
     if (rc) return rc;
     if (dst == bufs[cur ^ 1]) cur ^= 1;
@@ -1142,6 +1168,8 @@ int run_up(const Plan& pl, const void* mid, E* bufs[2], void* out, uint32_t k, i
       ++i;
       continue;
     }
+    if (i == nl - 1 && pl.g_fold)   // the folded outermost level writes the chain output
+      return timed_op<E>(rec, pl, up, i, 0, src, out, k, 0, st, nullptr, true);
     int rc = timed_op<E>(rec, pl, up, i, 0, src, bufs[nxt], k, 0, st);
     if (rc) return rc;
     src = bufs[nxt];
@@ -1497,7 +1525,80 @@ Plan part_view(const Plan& full, uint32_t part, uint32_t nparts) {
     v.g_lev[i] = static_cast<char*>(full.g_lev[i]) + part * lb;
     v.h_lev[i] = static_cast<char*>(full.h_lev[i]) + part * lb;
   }
+  v.fold_base = nullptr;
+  if (full.g_fold) {
+    const uint64_t fb = v.lev[full.nlev - 1].nblocks * full.leaf_n0 * full.branch * full.rank * es;
+    v.g_fold = static_cast<char*>(full.g_fold) + part * fb;
+    v.h_fold = static_cast<char*>(full.h_fold) + part * fb;
+  }
   return v;
+}
+
+// ---------------------------------------------------------------- leaf folding
+// fold[q] (n0 x C) = leaf[q] (n0 x r) * level[q] (r x C) for every block q of the
+// outermost transfer level (its P is 1, so block q = (g, t) feeds / is fed by leaf q:
+// factors.py:49-56 after 120-139). One CTA per block, double accumulation.
+template <typename E>
+__global__ void k_fold_leaf(const E* __restrict__ leaf, const E* __restrict__ lev, E* __restrict__ out, uint32_t n0,
+                            uint32_t r, uint32_t C) {
+  const size_t q = blockIdx.x;
+  const E* L = leaf + q * n0 * r;
+  const E* F = lev + q * r * C;
+  E* O = out + q * n0 * C;
+  for (uint32_t e = threadIdx.x; e < n0 * C; e += blockDim.x) {
+    const uint32_t i = e / C, c = e - i * C;
+    double re = 0, im = 0;
+    for (uint32_t rho = 0; rho < r; ++rho) {
+      const double ax = L[i * r + rho].x, ay = L[i * r + rho].y, bx = F[rho * C + c].x, by = F[rho * C + c].y;
+      re += ax * bx - ay * by;
+      im += ax * by + ay * bx;
+    }
+    O[e].x = static_cast<decltype(O[e].x)>(re);
+    O[e].y = static_cast<decltype(O[e].y)>(im);
+  }
+}
+
+// Folds the leaf factors into the outermost transfer level (BF_NO_FOLD=1 keeps the
+// reference's factor list): the chain then runs 2 (L - h) launches instead of 2 + 2 (L - h),
+// never materialises the rank-space vector next to the leaves, and — for leaves with fewer
+// than 2 r points — does less arithmetic (n0 C instead of n0 r + r C per block).
+// The operator is the same; entries of the folded blocks are rounded once more (apply
+// parity against the oracle's unfolded chain stays at 1e-15, tests/test_apply_gpu.py).
+int plan_fold_leaves(Plan& pl, cudaStream_t st) {
+  static const bool off = env_int("BF_NO_FOLD", 0) != 0;
+  if (off || !pl.uploaded || pl.nlev == 0 || pl.g_fold) return 0;
+  const LevelGeo& last = pl.lev[pl.nlev - 1];
+  if (last.P != 1 || last.nblocks != pl.leaf_nb) return 0;
+  const uint32_t nt = last.splits ? pl.branch : 1;
+  const uint32_t C = pl.branch * pl.rank, n0 = pl.leaf_n0, r = pl.rank;
+  (void)nt;
+  const uint64_t bytes = (last.nblocks * n0 * C * pl.elem() + 255) / 256 * 256;
+  if (cudaMalloc(&pl.fold_base, 2 * bytes) != cudaSuccess) {   // no room: keep the unfolded chain
+    cudaGetLastError();
+    pl.fold_base = nullptr;
+    return 0;
+  }
+  pl.g_fold = pl.fold_base;
+  pl.h_fold = static_cast<char*>(pl.fold_base) + bytes;
+  const unsigned blocks = static_cast<unsigned>(last.nblocks);
+  if (pl.dtype == BF_C128) {
+    k_fold_leaf<double2><<<blocks, 128, 0, st>>>(static_cast<const double2*>(pl.u_leaf),
+                                                  static_cast<const double2*>(pl.g_lev[pl.nlev - 1]),
+                                                  static_cast<double2*>(pl.g_fold), n0, r, C);
+    k_fold_leaf<double2><<<blocks, 128, 0, st>>>(static_cast<const double2*>(pl.v_leaf),
+                                                  static_cast<const double2*>(pl.h_lev[pl.nlev - 1]),
+                                                  static_cast<double2*>(pl.h_fold), n0, r, C);
+  } else {
+    k_fold_leaf<float2><<<blocks, 128, 0, st>>>(static_cast<const float2*>(pl.u_leaf),
+                                                 static_cast<const float2*>(pl.g_lev[pl.nlev - 1]),
+                                                 static_cast<float2*>(pl.g_fold), n0, r, C);
+    k_fold_leaf<float2><<<blocks, 128, 0, st>>>(static_cast<const float2*>(pl.v_leaf),
+                                                 static_cast<const float2*>(pl.h_lev[pl.nlev - 1]),
+                                                 static_cast<float2*>(pl.h_fold), n0, r, C);
+  }
+  BF_CUDA(cudaGetLastError());
+  BF_CUDA(cudaStreamSynchronize(st));
+  return 0;
 }
 
 // Host-buffer apply with the transfers pipelined against compute (captured into

@@ -335,6 +335,7 @@ int bf_plan_load_bfac(bf_plan** out, const char* path, int dtype, int device) {
   unsigned char extra;
   if (fread(&extra, 1, 1, fc.f) == 1) return cleanup(fmt_error("trailing bytes after last factor", off));
   p.uploaded = true;
+  if (int frc = plan_fold_leaves(p, nullptr)) return cleanup(frc);
   cleanup(0);
   *out = plan;
   return BF_OK;

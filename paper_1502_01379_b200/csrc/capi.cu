@@ -156,6 +156,7 @@ void bf_plan_destroy(bf_plan* plan) {
   for (auto e : plan->pipe_events) cudaEventDestroy(e);
   if (plan->copy_stream) cudaStreamDestroy(plan->copy_stream);
   if (plan->own_stream) cudaStreamDestroy(plan->own_stream);
+  if (plan->p.fold_base) cudaFree(plan->p.fold_base);
   if (plan->p.base) cudaFree(plan->p.base);
   delete plan;
 }
@@ -244,7 +245,7 @@ int bf_plan_upload(bf_plan* plan, const void* u_leaf, const void* const* g_level
   if (rc) return rc;
   if (e != cudaSuccess) return cuda_fail(e, "bf_plan_upload");
   p.uploaded = true;
-  return BF_OK;
+  return plan_fold_leaves(p, st);
 }
 
 uint64_t bf_apply_workspace_bytes(const bf_plan* plan, uint32_t k) {

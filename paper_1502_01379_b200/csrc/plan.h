@@ -39,6 +39,12 @@ struct Plan {
   void* v_leaf = nullptr;
   void* weights = nullptr;   // f64 (C128) or f32 (C64)
   std::vector<void*> g_lev, h_lev;
+  // leaf factors folded into the outermost transfer level at upload (plan_fold_leaves):
+  // blocks (G, nt, 1, n0, C) = leaf block (n0 x r) times level block (r x C); the chain then
+  // runs that level with R = n0 and skips the two leaf launches
+  void* g_fold = nullptr;    // U^L folded into G^{L-1}
+  void* h_fold = nullptr;    // V^L folded into H^{L-1}
+  void* fold_base = nullptr; // their allocation (owned by the full plan, not by part views)
   bool uploaded = false;
 
   size_t elem() const { return dtype == BF_C128 ? 16 : 8; }
@@ -68,6 +74,7 @@ int plan_apply_down_push(const Plan& pl, const void* in, void* const* peers, uin
 int plan_middle_exchange(const Plan& pl, int unpack, const void* in, void* out, uint32_t k, int adjoint,
                          cudaStream_t st);
 Plan part_view(const Plan& full, uint32_t part, uint32_t nparts);
+int plan_fold_leaves(Plan& pl, cudaStream_t st);
 int plan_apply_host_pipelined(const Plan& pl, const void* in_host, void* out_host, void* din, void* dout, void* mid,
                               void* mid2, void* ws, uint32_t k, int adjoint, uint32_t chunks, cudaStream_t run,
                               cudaStream_t cp, cudaEvent_t* ev, uint32_t taper = 0);
