@@ -254,8 +254,12 @@ bool wide_disabled() {
 constexpr int kWideNcw = 13;
 
 bool wide_applies(uint32_t R, uint32_t C, uint32_t nt, uint32_t k, int remap, size_t esz) {
+  // units wider than one stage (C > 64), and the branching-4 units of a rank-16 chain folded
+  // from pairs of binary levels (C = 64, nt = 4: 32.7 vs 53.9 ms at cfg2 size through the
+  // whole-unit stage); BF_WIDE_MIN_C lowers the threshold for any shape
+  static const uint32_t min_c = static_cast<uint32_t>(env_int("BF_WIDE_MIN_C", 65));
   return esz == 16 && !wide_disabled() && !dmma_disabled() && !gauss_disabled() && k >= kMrhsMinK && remap <= 2 &&
-         C > 64 && nt * R <= 8u * kWideNcw && C <= 8u * kWideNcw;
+         (C >= min_c || (C == 64 && nt == 4)) && nt * R <= 8u * kWideNcw && C <= 8u * kWideNcw;
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
@@ -1556,6 +1560,100 @@ __global__ void k_fold_leaf(const E* __restrict__ leaf, const E* __restrict__ le
     O[e].x = static_cast<decltype(O[e].x)>(re);
     O[e].y = static_cast<decltype(O[e].y)>(im);
   }
+}
+
+// ---------------------------------------------------------------- radix-4 folding
+// Two adjacent splitting levels A (index 2j, nearer the middle) and B (2j + 1) multiplied
+// into one level of branching 4: F4[g][2t + t'][q] (r x 4r) = [ B(t,t')[:, 0:r] A(t,0) |
+// B(t,t')[:, r:2r] A(t,1) ] with A(t,u) = A[(2g + t) P_A + 2q + u], B(t,t') =
+// B[((2g + t) 2 + t') P_B + q] (factors.py:120-139 applied twice). Unit (g, q) of the folded
+// level reads the 4r rows that A's units (g, 2q), (g, 2q + 1) read and writes the four
+// r-row blocks that B's units (2g, q), (2g + 1, q) write, so the result is an ordinary
+// level of a branching-4 plan (the quadtree plans' kernels) with exactly as many nonzeros
+// as the two levels it replaces: 16 r^2 per item either way.
+__global__ void k_fold_pair(const double2* __restrict__ fa, const double2* __restrict__ fb, double2* __restrict__ out,
+                            uint32_t r, uint32_t pa) {
+  const uint32_t pb = pa / 2, C = 2 * r;
+  const uint32_t item = blockIdx.x >> 2, t4 = blockIdx.x & 3, t = t4 >> 1, tp = t4 & 1;
+  const uint32_t g = item / pb, q = item - g * pb;
+  const double2* B = fb + static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q) * r * C;
+  double2* O = out + static_cast<size_t>((g * 4 + t4) * pb + q) * r * 2 * C;
+  for (uint32_t e = threadIdx.x; e < r * 2 * C; e += blockDim.x) {
+    const uint32_t row = e / (2 * C), col = e - row * 2 * C, u = col / C, c = col - u * C;
+    const double2* A = fa + static_cast<size_t>((g * 2 + t) * pa + 2 * q + u) * r * C;
+    double re = 0, im = 0;
+    for (uint32_t rho = 0; rho < r; ++rho) {
+      const double2 b = B[row * C + u * r + rho], a = A[rho * C + c];
+      re += b.x * a.x - b.y * a.y;
+      im += b.x * a.y + b.y * a.x;
+    }
+    O[e] = make_double2(re, im);
+  }
+}
+
+// The branching-4 twin of a binary complex128 plan for many right-hand sides (an even
+// number of splitting levels per side, 64 <= 4r <= 104 so its levels run as the K-pipelined
+// wide GEMM): half the launches, the chain's intermediate vectors read and written once
+// per TWO reference levels, 16 k-steps per unit instead of 8. Same operator; the folded
+// blocks are rounded once more. Leaves and middle weights are shared with `p`; returns
+// nullptr when the plan does not qualify or there is no memory for the copy (cfg2: 9.1 GB).
+Plan* plan_build_radix4(const Plan& p, cudaStream_t st) {
+  static const bool off = env_int("BF_NO_RADIX4", 0) != 0;
+  if (off || !p.uploaded || p.dtype != BF_C128 || p.branch != 2 || p.nlev < 2 || (p.nlev & 1)) return nullptr;
+  if (!wide_applies(p.rank, 4 * p.rank, 4, kMrhsMinK, 0, 16) && env_int("BF_RADIX4_ANY", 0) == 0) return nullptr;
+  for (uint32_t j = 0; j < p.nlev; j += 2) {
+    const LevelGeo& A = p.lev[j];
+    const LevelGeo& B = p.lev[j + 1];
+    if (!A.splits || !B.splits || A.P < 2 || B.G != 2 * A.G || 2 * B.P != A.P) return nullptr;
+    if (A.G * A.P / 2 * 4 >= (1ull << 31)) return nullptr;
+  }
+  Plan* q = new (std::nothrow) Plan(p);
+  if (!q) return nullptr;
+  q->branch = 4;
+  q->base = nullptr;
+  q->base_bytes = 0;
+  q->fold_base = q->g_fold = q->h_fold = nullptr;
+  q->nlev = p.nlev / 2;
+  q->lev.clear();
+  uint64_t bytes = 0;
+  const uint64_t blk = static_cast<uint64_t>(p.rank) * 4 * p.rank * sizeof(double2);
+  for (uint32_t j = 0; j < q->nlev; ++j) {
+    const LevelGeo& A = p.lev[2 * j];
+    LevelGeo g4{A.level, true, A.G, A.P / 2, A.G * 4 * (A.P / 2)};
+    q->lev.push_back(g4);
+    bytes += 2 * ((g4.nblocks * blk + 255) / 256 * 256);
+  }
+  if (cudaMalloc(&q->base, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    delete q;
+    return nullptr;
+  }
+  q->base_bytes = bytes;
+  q->g_lev.assign(q->nlev, nullptr);
+  q->h_lev.assign(q->nlev, nullptr);
+  char* cur = static_cast<char*>(q->base);
+  for (int side = 0; side < 2; ++side)
+    for (uint32_t j = 0; j < q->nlev; ++j) {
+      (side ? q->h_lev : q->g_lev)[j] = cur;
+      cur += (q->lev[j].nblocks * blk + 255) / 256 * 256;
+      const auto& src = side ? p.h_lev : p.g_lev;
+      k_fold_pair<<<static_cast<unsigned>(q->lev[j].nblocks), 128, 0, st>>>(
+          static_cast<const double2*>(src[2 * j]), static_cast<const double2*>(src[2 * j + 1]),
+          static_cast<double2*>((side ? q->h_lev : q->g_lev)[j]), p.rank, static_cast<uint32_t>(p.lev[2 * j].P));
+    }
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess || plan_fold_leaves(*q, st) != 0) {
+    cudaGetLastError();
+    plan_free_radix4(q);
+    return nullptr;
+  }
+  return q;
+}
+
+void plan_free_radix4(Plan* q) {
+  if (!q) return;
+  if (q->fold_base) cudaFree(q->fold_base);
+  if (q->base) cudaFree(q->base);
+  delete q;
 }
 
 // Folds the leaf factors into the outermost transfer level (BF_NO_FOLD=1 keeps the

@@ -156,6 +156,7 @@ void bf_plan_destroy(bf_plan* plan) {
   for (auto e : plan->pipe_events) cudaEventDestroy(e);
   if (plan->copy_stream) cudaStreamDestroy(plan->copy_stream);
   if (plan->own_stream) cudaStreamDestroy(plan->own_stream);
+  plan_free_radix4(plan->r4);
   if (plan->p.fold_base) cudaFree(plan->p.fold_base);
   if (plan->p.base) cudaFree(plan->p.base);
   delete plan;
@@ -260,13 +261,33 @@ static void drop_graphs_locked(const bf_plan* plan) {
   plan->graphs.clear();
 }
 
+// The plan a k-column apply runs on: the branching-4 twin (pairs of levels folded,
+// plan_build_radix4) for many right-hand sides once it exists, else the plan itself.
+// Built on first use (never inside a stream capture: callers resolve the plan first).
+static const Plan& chain_plan(const bf_plan* plan, uint32_t k, cudaStream_t st = nullptr) {
+  if (k < 8) return plan->p;
+  std::lock_guard<std::mutex> lock(plan->r4mu);
+  if (!plan->r4_tried && st) {   // a caller-side capture in progress: no allocation, no build
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return plan->p;
+    }
+  }
+  if (!plan->r4_tried) {
+    plan->r4_tried = true;
+    plan->r4 = plan_build_radix4(plan->p, nullptr);
+  }
+  return plan->r4 ? *plan->r4 : plan->p;
+}
+
 // The chain is a fixed sequence of 2 + 2(L-h) launches: replay it as one CUDA
 // graph per (buffers, k, direction, stream). A NULL stream is the legacy default
 // stream, which cannot be captured; the graph then runs on a plan-owned blocking
 // stream, which the legacy stream orders against implicitly. Caller holds gmu.
 static int apply_graph_locked(const bf_plan* plan, const void* in, void* out, uint32_t k, int adjoint,
                               void* workspace, cudaStream_t st) {
-  const Plan& p = plan->p;
+  const Plan& p = chain_plan(plan, k, st);
   cudaStream_t run = st;
   if (!run) {
     if (!plan->own_stream) BF_CUDA(cudaStreamCreate(&plan->own_stream));
@@ -315,7 +336,7 @@ int bf_apply(const bf_plan* plan, const void* in, void* out, uint32_t k, int adj
   if (p.nparts != 1) return fail(BF_EINVAL, "sharded plan: use bf_apply_down / bf_middle_pack / bf_apply_up");
   DeviceGuard dg(p.device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (!plan->graphs_enabled) return plan_apply(p, in, out, k, adjoint ? 1 : 0, workspace, st);
+  if (!plan->graphs_enabled) return plan_apply(chain_plan(plan, k, st), in, out, k, adjoint ? 1 : 0, workspace, st);
   std::lock_guard<std::mutex> lock(plan->gmu);
   return apply_graph_locked(plan, in, out, k, adjoint, workspace, st);
 }
@@ -329,7 +350,7 @@ int bf_apply_down(const bf_plan* plan, const void* in, void* mid, uint32_t k, in
   if (!workspace || workspace_bytes < bf_apply_workspace_bytes(plan, k))
     return fail(BF_EINVAL, "workspace too small (see bf_apply_workspace_bytes)");
   DeviceGuard dg(p.device);
-  return plan_apply_half(p, 0, in, mid, k, adjoint ? 1 : 0, workspace, static_cast<cudaStream_t>(stream));
+  return plan_apply_half(chain_plan(plan, k, static_cast<cudaStream_t>(stream)), 0, in, mid, k, adjoint ? 1 : 0, workspace, static_cast<cudaStream_t>(stream));
 }
 
 int bf_apply_up(const bf_plan* plan, const void* mid, void* out, uint32_t k, int adjoint, void* workspace,
@@ -341,7 +362,7 @@ int bf_apply_up(const bf_plan* plan, const void* mid, void* out, uint32_t k, int
   if (!workspace || workspace_bytes < bf_apply_workspace_bytes(plan, k))
     return fail(BF_EINVAL, "workspace too small (see bf_apply_workspace_bytes)");
   DeviceGuard dg(p.device);
-  return plan_apply_half(p, 1, mid, out, k, adjoint ? 1 : 0, workspace, static_cast<cudaStream_t>(stream));
+  return plan_apply_half(chain_plan(plan, k, static_cast<cudaStream_t>(stream)), 1, mid, out, k, adjoint ? 1 : 0, workspace, static_cast<cudaStream_t>(stream));
 }
 
 int bf_apply_down_push(const bf_plan* plan, const void* in, void* const* peers, uint32_t k, int adjoint,
@@ -418,7 +439,7 @@ int bf_apply_timed(const bf_plan* plan, const void* in, void* out, uint32_t k, i
   LaunchRecorder rec;
   rec.ev = timer->ev.data() + 2ull * timer->steps * timer->max_launches;
   rec.cap = timer->max_launches;
-  int rc = plan_apply(p, in, out, k, adjoint ? 1 : 0, workspace, static_cast<cudaStream_t>(stream), &rec);
+  int rc = plan_apply(chain_plan(plan, k), in, out, k, adjoint ? 1 : 0, workspace, static_cast<cudaStream_t>(stream), &rec);
   if (rc) return rc;
   if (timer->steps == 0) timer->launches = rec.used;
   if (rec.used != timer->launches) return fail(BF_EINVAL, "launch count changed between timed steps");
@@ -528,8 +549,10 @@ int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint
         return BF_OK;
       }
     char* w = static_cast<char*>(plan->host_ws);
+    (void)chain_plan(plan, k);   // build the many-RHS twin, if any, outside the capture
     BF_CUDA(cudaStreamBeginCapture(run, cudaStreamCaptureModeThreadLocal));
-    const int rc = plan_apply_host_pipelined(p, in_host, out_host, plan->host_in, plan->host_out, w, w + mid_bytes,
+    const Plan& cp = chain_plan(plan, k);   // (resolved above, before the capture began)
+    const int rc = plan_apply_host_pipelined(cp, in_host, out_host, plan->host_in, plan->host_out, w, w + mid_bytes,
                                              w + 2 * mid_bytes, k, adjoint ? 1 : 0, chunks, run, plan->copy_stream,
                                              plan->pipe_events.data(), taper);
     cudaGraph_t graph = nullptr;
@@ -555,7 +578,7 @@ int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint
   BF_CUDA(cudaMemcpyAsync(plan->host_in, in_host, io, cudaMemcpyHostToDevice, run));
   int rc = plan->graphs_enabled
                ? apply_graph_locked(plan, plan->host_in, plan->host_out, k, adjoint ? 1 : 0, plan->host_ws, run)
-               : plan_apply(p, plan->host_in, plan->host_out, k, adjoint ? 1 : 0, plan->host_ws, run);
+               : plan_apply(chain_plan(plan, k), plan->host_in, plan->host_out, k, adjoint ? 1 : 0, plan->host_ws, run);
   if (rc) return rc;
   BF_CUDA(cudaMemcpyAsync(out_host, plan->host_out, io, cudaMemcpyDeviceToHost, run));
   BF_CUDA(cudaStreamSynchronize(run));

@@ -75,6 +75,8 @@ int plan_middle_exchange(const Plan& pl, int unpack, const void* in, void* out, 
                          cudaStream_t st);
 Plan part_view(const Plan& full, uint32_t part, uint32_t nparts);
 int plan_fold_leaves(Plan& pl, cudaStream_t st);
+Plan* plan_build_radix4(const Plan& p, cudaStream_t st);
+void plan_free_radix4(Plan* q);
 int plan_apply_host_pipelined(const Plan& pl, const void* in_host, void* out_host, void* din, void* dout, void* mid,
                               void* mid2, void* ws, uint32_t k, int adjoint, uint32_t chunks, cudaStream_t run,
                               cudaStream_t cp, cudaEvent_t* ev, uint32_t taper = 0);
@@ -112,6 +114,10 @@ struct bf_plan {
   mutable void* host_ws = nullptr;
   mutable uint64_t host_io_bytes = 0, host_ws_bytes = 0;
   mutable cudaStream_t copy_stream = nullptr;      // host pipeline transfers
+  // branching-4 twin of the chain for many right-hand sides (plan_build_radix4), built on first use
+  mutable bfly::Plan* r4 = nullptr;
+  mutable bool r4_tried = false;
+  mutable std::mutex r4mu;
   mutable std::vector<cudaEvent_t> pipe_events;
 };
 

@@ -231,6 +231,33 @@ def test_rank16_pairs_opt_in(n, leaf, r, k):
     test_chunked_pairs_opt_in(n, leaf, r, k, env_flag="BF_PAIR16")
 
 
+@pytest.mark.parametrize("n,leaf,r,k", [
+    (1 << 14, 16, 16, 64),    # rank 16, 4 + 4 splitting levels: the branching-4 twin (plan_build_radix4), wide GEMM
+    (1 << 12, 16, 16, 256),
+    (1 << 12, 16, 20, 16),    # rank 20 (C4 = 80)
+    (1 << 10, 4, 16, 9),      # k not a multiple of 8
+])
+def test_radix4_twin(n, leaf, r, k):
+    """Many-RHS applies of rank-16..26 chains run on the branching-4 twin of the plan (pairs of
+    binary levels folded at first use); 1 RHS on the same plan runs the binary chain. Both
+    against the oracle, forward and adjoint; BF_NO_RADIX4=1 (child process) gives the same."""
+    p = bf.make_partition(n, leaf)
+    f = synthetic_chain(p, r, seed=n + k)
+    oc = oracle_of(f)
+    pl = f.plan()
+    for kk in (k, 1, k):
+        g = complex_gaussian(np.random.default_rng(kk), (n, kk))
+        gd = torch.from_numpy(g).cuda()
+        assert rel(pl.apply(gd), ochain.apply(oc, g)) <= TOL128
+        assert rel(pl.apply(gd, adjoint=True), ochain.apply(oc, g, adjoint=True)) <= TOL128
+    gh = complex_gaussian(np.random.default_rng(3), (n, k))
+    assert rel(torch.from_numpy(pl.apply(gh)), ochain.apply(oc, gh)) <= TOL128   # host-buffer path
+
+
+def test_radix4_switch():
+    test_chunked_pairs_opt_in(1 << 12, 16, 16, 64, env_flag="BF_NO_RADIX4")
+
+
 @pytest.mark.parametrize("flag", ["BF_NO_PAIR8_LEAF", "BF_NO_PAIR8"])
 def test_rank8_pairs_switches(flag):
     test_chunked_pairs_opt_in(1 << 12, 16, 8, 64, env_flag=flag)
