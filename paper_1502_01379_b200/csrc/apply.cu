@@ -304,7 +304,13 @@ int launch_wide(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_
   a.nt = nt;
   a.lgP = ilog2(P);
   a.k = k;
-  const uint32_t NT = k > 16 ? 4 : k > 8 ? 2 : 1;
+  // consumer warps: one per 8 output rows — 8 for the branching-4 units of a rank-16 chain
+  // (64 rows either way), 13 for the r = 25 quadtree (100 rows); with 8 warps the register
+  // budget allows 64 right-hand sides per item (NT = 8: each staged factor tile feeds twice
+  // the DMMAs; BF_WIDE_NT8=0 keeps 32)
+  const uint32_t ncw = std::max(nt * R, C) <= 64 ? 8 : kWideNcw;
+  static const bool nt8 = env_int("BF_WIDE_NT8", 1) != 0;
+  const uint32_t NT = (ncw == 8 && nt8 && k >= 64) ? 8 : k > 16 ? 4 : k > 8 ? 2 : 1;
   a.kc = std::min<uint32_t>(k, 8 * NT);
   a.nkc = (k + a.kc - 1) / a.kc;
   const uint64_t frows = units * nt * R, vrows = adjoint ? frows : units * C;
@@ -313,7 +319,8 @@ int launch_wide(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_
   a.items = static_cast<uint32_t>(units * a.nkc);
   // K tiles: forward BF_WIDE_KT block columns (multiple of 4, = 4 mod 8 for conflict-free A
   // fragment rows; default 20), adjoint one whole block (R rows)
-  static const int kt_env = env_int("BF_WIDE_KT", 20);
+  static const int kt_env0 = env_int("BF_WIDE_KT", 0);
+  const int kt_env = kt_env0 > 0 ? kt_env0 : (C == 64 ? 36 : 20);   // C = 64: tiles of 36 + 28 columns (31.8 vs 33.0 ms at 20)
   if (!adjoint) {
     a.KT = std::min<uint32_t>(static_cast<uint32_t>(std::max(4, kt_env / 4 * 4)), (C + 3) / 4 * 4);
     a.nks = (C + a.KT - 1) / a.KT;
@@ -352,7 +359,12 @@ int launch_wide(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_
   if (rc) return rc;
   const size_t smem = 128 + static_cast<size_t>(a.stages) * stage * sizeof(double2);
   void (*kern)(const WideArgs, const CUtensorMap, const CUtensorMap) = nullptr;
-  if (adjoint)
+  if (ncw == 8) {
+    if (adjoint)
+      kern = NT == 8 ? wide_kernel<8, 8, true> : NT == 4 ? wide_kernel<8, 4, true> : NT == 2 ? wide_kernel<8, 2, true> : wide_kernel<8, 1, true>;
+    else
+      kern = NT == 8 ? wide_kernel<8, 8, false> : NT == 4 ? wide_kernel<8, 4, false> : NT == 2 ? wide_kernel<8, 2, false> : wide_kernel<8, 1, false>;
+  } else if (adjoint)
     kern = NT == 4 ? wide_kernel<kWideNcw, 4, true> : NT == 2 ? wide_kernel<kWideNcw, 2, true> : wide_kernel<kWideNcw, 1, true>;
   else
     kern = NT == 4 ? wide_kernel<kWideNcw, 4, false> : NT == 2 ? wide_kernel<kWideNcw, 2, false> : wide_kernel<kWideNcw, 1, false>;
@@ -363,7 +375,7 @@ int launch_wide(const Plan& pl, const void* fac, uint32_t R, uint32_t C, uint32_
             C, nt, static_cast<unsigned long long>(units), k, a.kc, NT, a.KT, a.nks, a.stages, smem, adjoint);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(std::min<uint32_t>(a.items, static_cast<uint32_t>(pl.sms)));
-  cfg.blockDim = dim3((kWideNcw + 1) * 32);
+  cfg.blockDim = dim3((ncw + 1) * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
