@@ -282,7 +282,16 @@ def _rate(f, k, esz, ms):
     if k < 8:
         out.update(bound="hbm", frac=out["gbs"] / hbm, peak=hbm)
     elif esz == 16:
-        out.update(bound="fp64 tensor (DMMA)", frac=out["tflops"] / dmma, peak=dmma)
+        # flops the tensor pipe executes: 6 per complex multiply-add instead of 8 (3-multiplication
+        # form), and the leaf-folded outermost levels do n0 C instead of n0 r + r C per block
+        nb, n0, r = f.u_outer.blocks.shape
+        last = f.g_chain[-1].nnz if f.g_chain else 0
+        executed = 0.75 * (fl - 8 * k * (2 * nb * n0 * r + 2 * last - 2 * (last // r) * n0))
+        out.update(bound="fp64 tensor (DMMA)", frac=out["tflops"] / dmma, peak=dmma,
+                   executed_tflops=executed / (ms / 1e3) / 1e12, executed_frac=executed / (ms / 1e3) / 1e12 / dmma,
+                   note="tflops / frac count the reference factor list at 8 flops per complex multiply-add "
+                        "(SURVEY 8(d)) and can exceed the pipe's peak; executed_* count what the DMMA pipe runs "
+                        "(3 real products per complex one, leaf factors folded into the outermost levels)")
     else:
         out.update(bound="fp32 (FFMA)", frac=None, peak=None)
     return out
@@ -850,11 +859,16 @@ def main():
         lb = [("down half (node kernel)", alg_bytes // 2), ("up half (node kernel)", alg_bytes // 2)]
         lf_all = [("down half (node kernel)", alg_flops // 2), ("up half (node kernel)", alg_flops // 2)]
     else:
-        folded = nl.value == 2 * len(f.g_chain)    # leaf factors folded into the outermost levels
+        radix4 = nl.value == len(f.g_chain)         # many-RHS twin: pairs of levels folded (plan_build_radix4)
+        folded = radix4 or nl.value == 2 * len(f.g_chain)    # leaf factors folded into the outermost levels
         if folded:
             nlaunch = nl.value
         lb = launch_bytes(f, k, esz, folded)
         lf_all = launch_flops(f, k, folded)
+        if radix4:   # one launch per pair of reference levels; the vector between them is never moved
+            dim = f.g_chain[0].shape[0]
+            lb = [(f"{a[0]} + {b[0]}", a[1] + b[1] - 2 * esz * k * dim) for a, b in zip(lb[0::2], lb[1::2])]
+            lf_all = [(f"{a[0]} + {b[0]}", a[1] + b[1]) for a, b in zip(lf_all[0::2], lf_all[1::2])]
     moved_bytes = alg_bytes
     if not node and folded:
         nb_, n0_, r_ = f.u_outer.blocks.shape
@@ -971,7 +985,8 @@ def main():
             "rel_err": rel_err,
             "roofline": dict(roof, traffic=_ncu_traffic(args.config, args.dtype, k),
                              kernel="node_kernel (one launch per half)" if node else
-                             "level_kernel (transfer levels G/H)", kernel_share_of_step=share),
+                             ("wide_kernel (branching-4 twin: pairs of transfer levels)" if (not node and radix4)
+                              else "level_kernel (transfer levels G/H)"), kernel_share_of_step=share),
             "chain_roofline": {"algorithmic_bytes": alg_bytes, "algorithmic_flops": alg_flops,
                                "moved_bytes": moved_bytes,
                                "achieved_gbs": moved_bytes / (ms_step / 1e3) / 1e9,

@@ -1583,27 +1583,30 @@ __global__ void k_fold_leaf(const E* __restrict__ leaf, const E* __restrict__ le
 // r-row blocks that B's units (2g, q), (2g + 1, q) write, so the result is an ordinary
 // level of a branching-4 plan (the quadtree plans' kernels) with exactly as many nonzeros
 // as the two levels it replaces: 16 r^2 per item either way.
-__global__ void k_fold_pair(const double2* __restrict__ fa, const double2* __restrict__ fb, double2* __restrict__ out,
-                            uint32_t r, uint32_t pa) {
+template <typename E>
+__global__ void k_fold_pair(const E* __restrict__ fa, const E* __restrict__ fb, E* __restrict__ out, uint32_t r,
+                            uint32_t pa) {
   const uint32_t pb = pa / 2, C = 2 * r;
   const uint32_t item = blockIdx.x >> 2, t4 = blockIdx.x & 3, t = t4 >> 1, tp = t4 & 1;
   const uint32_t g = item / pb, q = item - g * pb;
-  const double2* B = fb + static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q) * r * C;
-  double2* O = out + static_cast<size_t>((g * 4 + t4) * pb + q) * r * 2 * C;
+  const E* B = fb + static_cast<size_t>(((2 * g + t) * 2 + tp) * pb + q) * r * C;
+  E* O = out + static_cast<size_t>((g * 4 + t4) * pb + q) * r * 2 * C;
   for (uint32_t e = threadIdx.x; e < r * 2 * C; e += blockDim.x) {
     const uint32_t row = e / (2 * C), col = e - row * 2 * C, u = col / C, c = col - u * C;
-    const double2* A = fa + static_cast<size_t>((g * 2 + t) * pa + 2 * q + u) * r * C;
+    const E* A = fa + static_cast<size_t>((g * 2 + t) * pa + 2 * q + u) * r * C;
     double re = 0, im = 0;
     for (uint32_t rho = 0; rho < r; ++rho) {
-      const double2 b = B[row * C + u * r + rho], a = A[rho * C + c];
-      re += b.x * a.x - b.y * a.y;
-      im += b.x * a.y + b.y * a.x;
+      const double bx = B[row * C + u * r + rho].x, by = B[row * C + u * r + rho].y;
+      const double ax = A[rho * C + c].x, ay = A[rho * C + c].y;
+      re += bx * ax - by * ay;
+      im += bx * ay + by * ax;
     }
-    O[e] = make_double2(re, im);
+    O[e].x = static_cast<decltype(O[e].x)>(re);
+    O[e].y = static_cast<decltype(O[e].y)>(im);
   }
 }
 
-// The branching-4 twin of a binary complex128 plan for many right-hand sides (an even
+// The branching-4 twin of a binary plan for many right-hand sides (an even
 // number of splitting levels per side, 64 <= 4r <= 104 so its levels run as the K-pipelined
 // wide GEMM): half the launches, the chain's intermediate vectors read and written once
 // per TWO reference levels, 16 k-steps per unit instead of 8. Same operator; the folded
@@ -1611,8 +1614,11 @@ __global__ void k_fold_pair(const double2* __restrict__ fa, const double2* __res
 // nullptr when the plan does not qualify or there is no memory for the copy (cfg2: 9.1 GB).
 Plan* plan_build_radix4(const Plan& p, cudaStream_t st) {
   static const bool off = env_int("BF_NO_RADIX4", 0) != 0;
-  if (off || !p.uploaded || p.dtype != BF_C128 || p.branch != 2 || p.nlev < 2 || (p.nlev & 1)) return nullptr;
+  if (off || !p.uploaded || p.branch != 2 || p.nlev < 2 || (p.nlev & 1)) return nullptr;
+  // complex128: ranks whose branching-4 levels run as the wide GEMM; complex64 (FFMA levels, 16 warps
+  // for wide blocks): the same ranks (cfg2 size, 256 RHS 26.8 -> 25.4 ms, 64 RHS 8.46 -> 7.11 ms)
   if (!wide_applies(p.rank, 4 * p.rank, 4, kMrhsMinK, 0, 16) && env_int("BF_RADIX4_ANY", 0) == 0) return nullptr;
+  if (p.dtype == BF_C64 && env_int("BF_NO_RADIX4_C64", 0) != 0) return nullptr;
   for (uint32_t j = 0; j < p.nlev; j += 2) {
     const LevelGeo& A = p.lev[j];
     const LevelGeo& B = p.lev[j + 1];
@@ -1628,7 +1634,7 @@ Plan* plan_build_radix4(const Plan& p, cudaStream_t st) {
   q->nlev = p.nlev / 2;
   q->lev.clear();
   uint64_t bytes = 0;
-  const uint64_t blk = static_cast<uint64_t>(p.rank) * 4 * p.rank * sizeof(double2);
+  const uint64_t blk = static_cast<uint64_t>(p.rank) * 4 * p.rank * p.elem();
   for (uint32_t j = 0; j < q->nlev; ++j) {
     const LevelGeo& A = p.lev[2 * j];
     LevelGeo g4{A.level, true, A.G, A.P / 2, A.G * 4 * (A.P / 2)};
@@ -1649,9 +1655,17 @@ Plan* plan_build_radix4(const Plan& p, cudaStream_t st) {
       (side ? q->h_lev : q->g_lev)[j] = cur;
       cur += (q->lev[j].nblocks * blk + 255) / 256 * 256;
       const auto& src = side ? p.h_lev : p.g_lev;
-      k_fold_pair<<<static_cast<unsigned>(q->lev[j].nblocks), 128, 0, st>>>(
-          static_cast<const double2*>(src[2 * j]), static_cast<const double2*>(src[2 * j + 1]),
-          static_cast<double2*>((side ? q->h_lev : q->g_lev)[j]), p.rank, static_cast<uint32_t>(p.lev[2 * j].P));
+      void* dst = (side ? q->h_lev : q->g_lev)[j];
+      const unsigned nb4 = static_cast<unsigned>(q->lev[j].nblocks);
+      const uint32_t pa = static_cast<uint32_t>(p.lev[2 * j].P);
+      if (p.dtype == BF_C128)
+        k_fold_pair<double2><<<nb4, 128, 0, st>>>(static_cast<const double2*>(src[2 * j]),
+                                                   static_cast<const double2*>(src[2 * j + 1]),
+                                                   static_cast<double2*>(dst), p.rank, pa);
+      else
+        k_fold_pair<float2><<<nb4, 128, 0, st>>>(static_cast<const float2*>(src[2 * j]),
+                                                  static_cast<const float2*>(src[2 * j + 1]),
+                                                  static_cast<float2*>(dst), p.rank, pa);
     }
   if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess || plan_fold_leaves(*q, st) != 0) {
     cudaGetLastError();

@@ -252,6 +252,10 @@ def test_radix4_twin(n, leaf, r, k):
         assert rel(pl.apply(gd, adjoint=True), ochain.apply(oc, g, adjoint=True)) <= TOL128
     gh = complex_gaussian(np.random.default_rng(3), (n, k))
     assert rel(torch.from_numpy(pl.apply(gh)), ochain.apply(oc, gh)) <= TOL128   # host-buffer path
+    p64 = f.plan("c64")                                                          # complex64 twin (FFMA levels)
+    gd = torch.from_numpy(gh).cuda()
+    assert rel(p64.apply(gd).to(torch.complex128), ochain.apply(oc, gh)) <= TOL64
+    assert rel(p64.apply(gd, adjoint=True).to(torch.complex128), ochain.apply(oc, gh, adjoint=True)) <= TOL64
 
 
 def test_radix4_switch():
