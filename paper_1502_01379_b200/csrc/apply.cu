@@ -1641,7 +1641,10 @@ Plan* plan_build_radix4(const Plan& p, cudaStream_t st) {
     q->lev.push_back(g4);
     bytes += 2 * ((g4.nblocks * blk + 255) / 256 * 256);
   }
-  if (cudaMalloc(&q->base, bytes) != cudaSuccess) {
+  // the twin doubles the plan's footprint: only when that leaves at least 15% of the device free
+  size_t mem_free = 0, mem_total = 0;
+  if (cudaMemGetInfo(&mem_free, &mem_total) != cudaSuccess || mem_free < bytes + mem_total * 15 / 100 ||
+      cudaMalloc(&q->base, bytes) != cudaSuccess) {
     cudaGetLastError();
     delete q;
     return nullptr;

@@ -33,6 +33,8 @@ def emulate(plans, g, adjoint):
     (1 << 12, 0.25, 4, 2, 8, "c128"),
     (1 << 16, 16, 8, 64, 8, "c128"),   # config-1 geometry, many-RHS kernel
     (1 << 14, 16, 16, 1, 4, "c64"),
+    (1 << 14, 16, 16, 16, 4, "c128"),  # rank 16, many RHS: every part runs on its branching-4 twin
+    (1 << 14, 16, 16, 64, 2, "c64"),
 ])
 def test_sharded_steps_match_full_apply(n, leaf, r, k, P, dtype):
     p = bf.make_partition(n, leaf)
@@ -74,7 +76,8 @@ def test_sharded_quadtree_steps():
         assert (torch.linalg.norm(got - want) / torch.linalg.norm(want)).item() <= 1e-13
 
 
-@pytest.mark.parametrize("n,leaf,r,k,P", [(1 << 12, 16, 8, 1, 2), (1 << 14, 16, 16, 3, 4), (1 << 16, 16, 8, 64, 8)])
+@pytest.mark.parametrize("n,leaf,r,k,P", [(1 << 12, 16, 8, 1, 2), (1 << 14, 16, 16, 3, 4), (1 << 16, 16, 8, 64, 8),
+                                         (1 << 14, 16, 16, 32, 4)])
 def test_fused_push_exchange_emulated(n, leaf, r, k, P):
     """bf_apply_down_push: the last down level stores (weights applied) straight into every
     part's receive buffer — emulated with P local buffers on one GPU (each part's push runs
