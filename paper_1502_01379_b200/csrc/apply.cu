@@ -1734,7 +1734,7 @@ int plan_fold_leaves(Plan& pl, cudaStream_t st) {
 // vector; chunk e's D2H overlaps the up half of chunk e+1.
 int plan_apply_host_pipelined(const Plan& pl, const void* in_host, void* out_host, void* din, void* dout, void* mid,
                               void* mid2, void* ws, uint32_t k, int adjoint, uint32_t chunks, cudaStream_t run,
-                              cudaStream_t cp, cudaEvent_t* ev, uint32_t taper) {
+                              cudaStream_t cp, cudaEvent_t* ev, uint32_t taper, cudaStream_t aux) {
   const uint64_t es = pl.elem();
   const uint64_t mid_rows = static_cast<uint64_t>(pl.m) * pl.m * pl.rank;
   // chunk c = part (first, second) of the middle nodes. Uniform: `chunks` equal parts.
@@ -1754,7 +1754,12 @@ int plan_apply_host_pipelined(const Plan& pl, const void* in_host, void* out_hos
     }
   }
   const uint32_t nc = static_cast<uint32_t>(down.size());
-  // ev[0]: fork; ev[1 .. nc]: inputs landed; ev[nc+1 .. 2 nc]: outputs ready; ev[2 nc+1]: join
+  // ev[0]: fork; ev[1 .. nc]: inputs landed; ev[nc+1 .. 2 nc]: outputs ready; ev[2 nc+1]: join;
+  // ev[2 nc+2 ..]: down halves finished on the second compute stream
+  // With a second compute stream (aux) the down halves of odd parts run there, each on its own
+  // slice of the workspace: a part's small launches fill the tails of its neighbour's (the up
+  // halves stay in order on `run`: the large part must finish first so that its download
+  // overlaps the rest).
   BF_CUDA(cudaEventRecord(ev[0], run));
   BF_CUDA(cudaStreamWaitEvent(cp, ev[0], 0));
   for (uint32_t c = 0; c < nc; ++c) {
@@ -1764,13 +1769,22 @@ int plan_apply_host_pipelined(const Plan& pl, const void* in_host, void* out_hos
                             cudaMemcpyHostToDevice, cp));
     BF_CUDA(cudaEventRecord(ev[1 + c], cp));
   }
+  uint64_t ws_off = 0;
   for (uint32_t c = 0; c < nc; ++c) {
-    BF_CUDA(cudaStreamWaitEvent(run, ev[1 + c], 0));
+    cudaStream_t sc = (aux && (c & 1)) ? aux : run;
+    BF_CUDA(cudaStreamWaitEvent(sc, ev[1 + c], 0));
     const Plan v = part_view(pl, down[c].first, down[c].second);
     const uint64_t rows_c = pl.n / down[c].second, mid_c = mid_rows / down[c].second;
+    // (with aux every part has its own workspace slice: 2 dim_max k / nparts elements)
+    void* wsc = aux ? static_cast<char*>(ws) + ws_off : ws;
+    if (aux) ws_off += 2 * (pl.dim_max / down[c].second) * k * es;
     int rc = plan_apply_half(v, 0, static_cast<char*>(din) + down[c].first * rows_c * k * es,
-                             static_cast<char*>(mid) + down[c].first * mid_c * k * es, k, adjoint, ws, run);
+                             static_cast<char*>(mid) + down[c].first * mid_c * k * es, k, adjoint, wsc, sc);
     if (rc) return rc;
+    if (sc == aux) {
+      BF_CUDA(cudaEventRecord(ev[2 + 2 * nc + c], aux));
+      BF_CUDA(cudaStreamWaitEvent(run, ev[2 + 2 * nc + c], 0));
+    }
   }
   int rc = pl.dtype == BF_C128 ? launch_middle<double2>(pl, mid, mid2, k, adjoint, run)
                                : launch_middle<float2>(pl, mid, mid2, k, adjoint, run);

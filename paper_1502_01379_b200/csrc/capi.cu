@@ -155,6 +155,7 @@ void bf_plan_destroy(bf_plan* plan) {
   if (plan->host_ws) cudaFree(plan->host_ws);
   for (auto e : plan->pipe_events) cudaEventDestroy(e);
   if (plan->copy_stream) cudaStreamDestroy(plan->copy_stream);
+  if (plan->aux_stream) cudaStreamDestroy(plan->aux_stream);
   if (plan->own_stream) cudaStreamDestroy(plan->own_stream);
   plan_free_radix4(plan->r4);
   if (plan->p.fold_base) cudaFree(plan->p.fold_base);
@@ -514,7 +515,13 @@ int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint
   const bool pipelined =
       plan->graphs_enabled && chunks > 1 && io >= (4ull << 20) && pinned(in_host) && pinned(out_host);
   const uint64_t mid_bytes = static_cast<uint64_t>(p.m) * p.m * p.rank * k * p.elem();
-  const uint64_t need_ws = pipelined ? 2 * mid_bytes + 2 * (p.dim_max / biggest) * k * p.elem() : wsb;
+  // BF_PIPE_STREAMS=2: the down halves of odd parts on a second compute stream (own workspace slices)
+  static const bool two_streams = [] {
+    const char* e = getenv("BF_PIPE_STREAMS");
+    return e && atoi(e) == 2;
+  }();
+  const uint64_t part_ws = two_streams ? 2 * p.dim_max * k * p.elem() * 2 : 2 * (p.dim_max / biggest) * k * p.elem();
+  const uint64_t need_ws = pipelined ? 2 * mid_bytes + part_ws : wsb;
   if (plan->host_io_bytes < io || plan->host_ws_bytes < need_ws) {
     BF_CUDA(cudaStreamSynchronize(run));
     // every cached graph that captured the old device buffers would replay against freed
@@ -533,11 +540,12 @@ int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint
   }
   if (pipelined) {
     if (!plan->copy_stream) BF_CUDA(cudaStreamCreateWithFlags(&plan->copy_stream, cudaStreamNonBlocking));
-    if (plan->pipe_events.size() < 2 * nchunk + 2) {  // BF_PIPE_CHUNKS is re-read on every call
+    if (two_streams && !plan->aux_stream) BF_CUDA(cudaStreamCreateWithFlags(&plan->aux_stream, cudaStreamNonBlocking));
+    if (plan->pipe_events.size() < 3 * nchunk + 3) {  // BF_PIPE_CHUNKS is re-read on every call
       BF_CUDA(cudaStreamSynchronize(run));
       drop_graphs_locked(plan);  // captured graphs reference the old events
       for (auto e : plan->pipe_events) cudaEventDestroy(e);
-      plan->pipe_events.assign(2 * nchunk + 2, nullptr);
+      plan->pipe_events.assign(3 * nchunk + 3, nullptr);
       for (auto& e : plan->pipe_events) BF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     void* const key_ws = reinterpret_cast<void*>(static_cast<uintptr_t>(1));  // marks the pipelined graph
@@ -554,7 +562,7 @@ int bf_apply_host(const bf_plan* plan, const void* in_host, void* out_host, uint
     const Plan& cp = chain_plan(plan, k);   // (resolved above, before the capture began)
     const int rc = plan_apply_host_pipelined(cp, in_host, out_host, plan->host_in, plan->host_out, w, w + mid_bytes,
                                              w + 2 * mid_bytes, k, adjoint ? 1 : 0, chunks, run, plan->copy_stream,
-                                             plan->pipe_events.data(), taper);
+                                             plan->pipe_events.data(), taper, two_streams ? plan->aux_stream : nullptr);
     cudaGraph_t graph = nullptr;
     const cudaError_t e = cudaStreamEndCapture(run, &graph);
     if (rc) {

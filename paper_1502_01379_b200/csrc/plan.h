@@ -79,7 +79,7 @@ Plan* plan_build_radix4(const Plan& p, cudaStream_t st);
 void plan_free_radix4(Plan* q);
 int plan_apply_host_pipelined(const Plan& pl, const void* in_host, void* out_host, void* din, void* dout, void* mid,
                               void* mid2, void* ws, uint32_t k, int adjoint, uint32_t chunks, cudaStream_t run,
-                              cudaStream_t cp, cudaEvent_t* ev, uint32_t taper = 0);
+                              cudaStream_t cp, cudaEvent_t* ev, uint32_t taper = 0, cudaStream_t aux = nullptr);
 int plan_apply_factor(const Plan& pl, int which, int lvl_idx, int adjoint, const void* in, void* out, uint32_t k,
                       cudaStream_t st);
 int entries(int kernel_id, uint64_t n, const int64_t* rows, uint32_t nr, const int64_t* cols, uint32_t nc, void* out,
@@ -114,6 +114,7 @@ struct bf_plan {
   mutable void* host_ws = nullptr;
   mutable uint64_t host_io_bytes = 0, host_ws_bytes = 0;
   mutable cudaStream_t copy_stream = nullptr;      // host pipeline transfers
+  mutable cudaStream_t aux_stream = nullptr;       // host pipeline: odd parts of the down half
   // branching-4 twin of the chain for many right-hand sides (plan_build_radix4), built on first use
   mutable bfly::Plan* r4 = nullptr;
   mutable bool r4_tried = false;
