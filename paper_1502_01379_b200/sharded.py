@@ -183,9 +183,7 @@ class ShardedPlan(ShardedApply):
                                         int(adjoint), ctypes.c_void_p(ws.data_ptr()), wsb, self._stream()))
         return out
 
-
-def _push_methods():
-    """Attach the fused down+exchange step to ShardedPlan (kept separate for readability)."""
+    # -- fused down + exchange step (peer stores over NVLink) --
 
     def down_push(self, x, adjoint, peers):
         """Down half whose last level stores (weights applied) straight into every part's
@@ -229,10 +227,3 @@ def _push_methods():
         recv = buf.view(torch.complex128) if self.tdt == torch.complex128 else buf
         recv = recv.view(self.nparts * self.chunk_rows, k)
         return self.up(self.unpack(recv, adjoint), adjoint)
-
-    ShardedPlan.down_push = down_push
-    ShardedPlan.push_buffer = push_buffer
-    ShardedPlan.apply_push = apply_push
-
-
-_push_methods()
