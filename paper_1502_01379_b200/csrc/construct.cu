@@ -1509,6 +1509,245 @@ __device__ void tsqr_reg(const F& src, int64_t part, int n, double2* smem, doubl
   __syncthreads();
 }
 
+// Register TSQR, second form: the row chunk lives in registers as well (lane j: column j
+// of 8 rows), reflector p's chunk column reaches every lane by shuffles and every lane
+// derives the reflector itself — no shared-memory traffic, no warp reductions and no
+// per-step barrier inside a fold; only the pairwise merge of the warps' R's goes through
+// shared memory.
+constexpr int kTsqrRows = 8;
+
+__device__ __forceinline__ void tsqr_fold_reg(double2 (&Rc)[32], double2 (&c)[kTsqrRows], int n) {
+  static_assert(kTsqrRows == 8, "the sums below are written out as trees over 8 rows");
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int p = 0; p < 32; ++p) {
+    if (p >= n) break;
+    double2 v[kTsqrRows];
+#pragma unroll
+    for (int i = 0; i < kTsqrRows; ++i) {
+      v[i].x = __shfl_sync(full, c[i].x, p);
+      v[i].y = __shfl_sync(full, c[i].y, p);
+    }
+    double2 al;
+    al.x = __shfl_sync(full, Rc[p].x, p);
+    al.y = __shfl_sync(full, Rc[p].y, p);
+    // |v|^2 and v^H c as balanced trees (the dependent-DFMA latency is the fold's critical
+    // path): every product is independent, three levels of adds
+    double q[kTsqrRows];
+    double2 e[kTsqrRows];
+#pragma unroll
+    for (int i = 0; i < kTsqrRows; ++i) {
+      q[i] = fma(v[i].x, v[i].x, v[i].y * v[i].y);
+      e[i].x = fma(v[i].x, c[i].x, v[i].y * c[i].y);    // conj(v) * c
+      e[i].y = fma(v[i].x, c[i].y, -(v[i].y * c[i].x));
+    }
+    const double s2 = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+    if (s2 == 0.0) continue;  // the chunk column is already zero: nothing to reflect (uniform)
+    double2 d;
+    d.x = ((e[0].x + e[1].x) + (e[2].x + e[3].x)) + ((e[4].x + e[5].x) + (e[6].x + e[7].x));
+    d.y = ((e[0].y + e[1].y) + (e[2].y + e[3].y)) + ((e[4].y + e[5].y) + (e[6].y + e[7].y));
+    // reflector: beta = -al / |al| * nx, v0 = al - beta, f = 2 / (|v0|^2 + s2) = 1 / (nx (nx + |al|))
+    const double aa2 = fma(al.x, al.x, al.y * al.y);
+    const double nx = sqrt(aa2 + s2);
+    const double ra = aa2 > 0 ? rsqrt(aa2) : 0.0;
+    const double aa = aa2 * ra;
+    const double f = 1.0 / (nx * (nx + aa));
+    const double sc = -nx * ra;
+    const double2 beta = aa2 > 0 ? make_double2(al.x * sc, al.y * sc) : make_double2(-nx, 0);
+    const double2 v0 = make_double2(al.x - beta.x, al.y - beta.y);
+    if (lane > p && lane < n) {
+      const double2 h = cmulc(v0, Rc[p]);
+      const double2 wj = make_double2((d.x + h.x) * f, (d.y + h.y) * f);
+      const double2 u = cmul(v0, wj);
+      Rc[p].x -= u.x;
+      Rc[p].y -= u.y;
+#pragma unroll
+      for (int i = 0; i < kTsqrRows; ++i) {
+        c[i].x = fma(-v[i].x, wj.x, fma(v[i].y, wj.y, c[i].x));
+        c[i].y = fma(-v[i].x, wj.y, fma(-v[i].y, wj.x, c[i].y));
+      }
+    }
+    if (lane == p) Rc[p] = beta;
+  }
+}
+
+// One reflector step of the register fold with R's row p in Rrow (see tsqr_fold_roll).
+template <int CH>
+__device__ __forceinline__ void tsqr_step_reg(double2& Rrow, double2 (&c)[CH], int p, int n) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  double2 v[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    v[i].x = __shfl_sync(full, c[i].x, p);
+    v[i].y = __shfl_sync(full, c[i].y, p);
+  }
+  double2 al;
+  al.x = __shfl_sync(full, Rrow.x, p);
+  al.y = __shfl_sync(full, Rrow.y, p);
+  // |v|^2 and v^H c on two accumulators each
+  double s2a = 0, s2b = 0;
+  double2 d0 = make_double2(0, 0), d1 = make_double2(0, 0);
+#pragma unroll
+  for (int i = 0; i < CH; i += 2) {
+    s2a = fma(v[i].x, v[i].x, fma(v[i].y, v[i].y, s2a));
+    s2b = fma(v[i + 1].x, v[i + 1].x, fma(v[i + 1].y, v[i + 1].y, s2b));
+    d0.x = fma(v[i].x, c[i].x, fma(v[i].y, c[i].y, d0.x));  // conj(v) * c
+    d0.y = fma(v[i].x, c[i].y, fma(-v[i].y, c[i].x, d0.y));
+    d1.x = fma(v[i + 1].x, c[i + 1].x, fma(v[i + 1].y, c[i + 1].y, d1.x));
+    d1.y = fma(v[i + 1].x, c[i + 1].y, fma(-v[i + 1].y, c[i + 1].x, d1.y));
+  }
+  const double s2 = s2a + s2b;
+  // reflector: beta = -al / |al| * nx, v0 = al - beta, f = 2 / (|v0|^2 + s2) = 1 / (nx (nx + |al|));
+  // a zero chunk column (s2 = 0) leaves everything as it is (f = 0, beta = al)
+  const bool live = s2 > 0.0;
+  const double aa2 = fma(al.x, al.x, al.y * al.y);
+  const double nx = sqrt(aa2 + s2);
+  const double ra = aa2 > 0 ? rsqrt(aa2) : 0.0;
+  const double aa = aa2 * ra;
+  const double f = live ? 1.0 / (nx * (nx + aa)) : 0.0;
+  const double sc = -nx * ra;
+  const double2 beta = !live ? al : aa2 > 0 ? make_double2(al.x * sc, al.y * sc) : make_double2(-nx, 0);
+  const double2 v0 = make_double2(al.x - beta.x, al.y - beta.y);
+  if (lane > p && lane < n) {
+    const double2 h = cmulc(v0, Rrow);
+    const double2 wj = make_double2(((d0.x + d1.x) + h.x) * f, ((d0.y + d1.y) + h.y) * f);
+    const double2 u = cmul(v0, wj);
+    Rrow.x -= u.x;
+    Rrow.y -= u.y;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      c[i].x = fma(-v[i].x, wj.x, fma(v[i].y, wj.y, c[i].x));
+      c[i].y = fma(-v[i].x, wj.y, fma(-v[i].y, wj.x, c[i].y));
+    }
+  }
+  if (lane == p) Rrow = beta;
+}
+
+// The fold as a rolled loop: four reflector steps on Rc[0..3], then the register R rotated
+// by four rows, eight times (back in place) — a loop body of ~1k instructions instead of
+// 32 unrolled steps (the unrolled fold overflows the instruction cache).
+__device__ __forceinline__ void tsqr_fold_roll(double2 (&Rc)[32], double2 (&c)[kTsqrRows], int n) {
+#pragma unroll 1
+  for (int p0 = 0; p0 < 32; p0 += 4) {
+    if (p0 < n) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+        if (p0 + s < n) tsqr_step_reg<kTsqrRows>(Rc[s], c, p0 + s, n);
+    }
+    const double2 t0 = Rc[0], t1 = Rc[1], t2 = Rc[2], t3 = Rc[3];
+#pragma unroll
+    for (int k = 0; k < 28; ++k) Rc[k] = Rc[k + 4];
+    Rc[28] = t0;
+    Rc[29] = t1;
+    Rc[30] = t2;
+    Rc[31] = t3;
+  }
+}
+
+// R of every tall stack (up to 32 wide) of the chunk -> a.rbuf, one warp (one 32-thread
+// CTA) per problem: no merges, no barriers, uniform control flow. The running R sits in
+// shared memory as a packed upper triangle (8.4 KB; lane j touches only column j, one
+// load and one store per reflector), the CH-row chunk in registers: ~100 registers, so
+// 16-20 problems share an SM and hide each other's sqrt / divide chains.
+__device__ __host__ __forceinline__ int tri_off(int p) { return p * 32 - (p * (p - 1)) / 2 - p; }
+constexpr int kTriElems = 528;
+
+template <int CH>
+__global__ void __launch_bounds__(32) k_recurse_tsqr1(RecArgs a) {
+  extern __shared__ double2 sm2[];
+  const int lane = threadIdx.x;
+  const int64_t idx = blockIdx.x;
+  const int64_t prob = a.p0 + idx;
+  const int b = a.b;
+  const int64_t pairs = a.pairs, part = a.rows / b;
+  const int n = b * a.r;
+  const int64_t gb = prob / (b * pairs), t = (prob / pairs) % b, p = prob % pairs;
+  const double2* base = a.cur + ((gb * a.rows + t * part) * pairs + p) * n + lane;
+  const int64_t rstride = pairs * n;
+  for (int x = lane; x < kTriElems; x += 32) sm2[x] = make_double2(0, 0);
+  __syncwarp();
+#pragma unroll 1
+  for (int64_t r0 = 0; r0 < part; r0 += CH) {
+    double2 c[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i)
+      c[i] = (lane < n && r0 + i < part) ? __ldcs(base + (r0 + i) * rstride) : make_double2(0, 0);
+#pragma unroll 1
+    for (int q = 0; q < n; ++q) {
+      double2* rp = sm2 + tri_off(q) + lane;
+      double2 Rrow = lane >= q ? *rp : make_double2(0, 0);
+      tsqr_step_reg<CH>(Rrow, c, q, n);
+      if (lane >= q) *rp = Rrow;
+    }
+  }
+  __syncwarp();
+  if (lane < n) {
+    double2* Rout = a.rbuf + idx * static_cast<int64_t>(n) * n;
+    for (int q = 0; q < n; ++q) Rout[q * n + lane] = q <= lane ? sm2[tri_off(q) + lane] : make_double2(0, 0);
+  }
+}
+
+// R of every tall stack (up to 32 wide) of the chunk -> a.rbuf, W warps per problem
+// (W = 1, 2, 4 or 8: 8 / W problems per CTA), each warp folding 8-row chunks into its
+// register R; the group's R's are merged pairwise through shared memory.
+__global__ void __launch_bounds__(256, 1) k_recurse_tsqr2(RecArgs a, int64_t cnt, int W) {
+  extern __shared__ double2 sm2[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wl = warp % W;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * (8 / W) + warp / W;
+  const bool active = idx < cnt;
+  const int64_t prob = a.p0 + (active ? idx : 0);
+  const int b = a.b;
+  const int64_t pairs = a.pairs, part = a.rows / b;
+  const int n = b * a.r;
+  const int64_t gb = prob / (b * pairs), t = (prob / pairs) % b, p = prob % pairs;
+  const double2* base = a.cur + ((gb * a.rows + t * part) * pairs + p) * n + lane;
+  const int64_t rstride = pairs * n;
+  const int ldc = 33;
+  double2 Rc[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) Rc[q] = make_double2(0, 0);
+  if (active) {
+    const int64_t nchunks = (part + kTsqrRows - 1) / kTsqrRows;
+    for (int64_t cidx = wl; cidx < nchunks; cidx += W) {
+      const int64_t r0 = cidx * kTsqrRows;
+      double2 c[kTsqrRows];
+#pragma unroll
+      for (int i = 0; i < kTsqrRows; ++i)
+        c[i] = (lane < n && r0 + i < part) ? __ldcs(base + (r0 + i) * rstride) : make_double2(0, 0);
+      tsqr_fold_roll(Rc, c, n);
+    }
+  }
+  double2* mine = sm2 + static_cast<int64_t>(warp) * ldc * 32;
+  for (int step = 1; step < W; step *= 2) {
+    __syncthreads();
+    if (wl % (2 * step) == step && lane < n) {
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (q < n) mine[lane * ldc + q] = Rc[q];
+    }
+    __syncthreads();
+    if (active && wl % (2 * step) == 0 && wl + step < W) {
+      const double2* other = sm2 + static_cast<int64_t>(warp + step) * ldc * 32;
+      for (int i0 = 0; i0 < n; i0 += kTsqrRows) {
+        double2 c[kTsqrRows];
+#pragma unroll
+        for (int i = 0; i < kTsqrRows; ++i)
+          c[i] = (lane < n && i0 + i < n) ? other[lane * ldc + i0 + i] : make_double2(0, 0);
+        tsqr_fold_roll(Rc, c, n);
+      }
+    }
+  }
+  if (active && wl == 0 && lane < n) {
+    double2* Rout = a.rbuf + idx * static_cast<int64_t>(n) * n;
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (q < n) Rout[q * n + lane] = q <= lane ? Rc[q] : make_double2(0, 0);
+  }
+}
+
 // R factor of a tall (part x n) stack by TSQR in shared memory: warps stream
 // row chunks into [R_acc; chunk] buffers (column-major, odd ld) and QR them (no
 // block barriers), then combine their R's pairwise. Leaves R (n x n, row-major)
@@ -1670,6 +1909,102 @@ __global__ void __launch_bounds__(TALL ? 256 : 512, 2) k_recurse_split(RecArgs a
   for (int x = threadIdx.x; x < r * w; x += blockDim.x) {
     const int rho = x / w, c = x % w;
     G[x] = rho < keep ? cconj(Vg[c * S + rho]) : make_double2(0, 0);
+  }
+}
+
+// Stacks up to 32 columns wide, one warp per problem: Jacobi on the columns of R^H (R from
+// k_recurse_tsqr, or the stack itself when it has at most 32 rows — zero rows below), held
+// one column per lane in registers. R^H J = V Sigma gives sigma and the right singular
+// vectors of the stack directly; no rotation matrix is accumulated and nothing lives in
+// shared memory, so 12 problems share an SM. Writes the transfer block G = vh[:keep]
+// (zero-padded rows); new_u = A conj(G)^T follows in k_recurse_av.
+template <int RR>
+__global__ void __launch_bounds__(128, RR > 16 ? 3 : 4) k_recurse_wsvd(RecArgs a, int64_t cnt, int from_r) {
+  const int lane = threadIdx.x & 31;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  if (idx >= cnt) return;
+  const int64_t prob = a.p0 + idx;
+  const int b = a.b, r = a.r, w = b * a.r;
+  const int64_t pairs = a.pairs, part = a.rows / b;
+  const int64_t gb = prob / (b * pairs), t = (prob / pairs) % b, p = prob % pairs;
+  const int keep = static_cast<int>(part < r ? part : r);
+  const int cc = from_r ? w : static_cast<int>(part);  // rows of R (or of the short stack) = columns of its adjoint
+  const double2* rowp = from_r ? a.rbuf + idx * static_cast<int64_t>(w) * w + static_cast<int64_t>(lane) * w
+                               : a.cur + ((gb * a.rows + t * part + lane) * pairs + p) * w;
+  double2 col[RR];
+#pragma unroll
+  for (int k = 0; k < RR; ++k) col[k] = (lane < cc && k < w) ? cconj(rowp[k]) : make_double2(0, 0);
+  warp_jacobi_reg<RR>(col, cc);
+  double nrm = 0;
+#pragma unroll
+  for (int k = 0; k < RR; ++k) nrm += col[k].x * col[k].x + col[k].y * col[k].y;
+  nrm = lane < cc ? sqrt(nrm) : -1.0;
+  int rank = 0;
+  for (int d = 0; d < cc; ++d) {
+    const double o = __shfl_sync(0xffffffffu, nrm, d);
+    rank += (o > nrm) || (o == nrm && d < lane);
+  }
+  // G[rho][c] = conj(V[c][rho]), V[:, rho] = column / sigma of the lane ranked rho
+  double2* G = a.g + prob * static_cast<int64_t>(r) * w;
+  if (lane < cc && rank < keep) {
+    double2* row = G + static_cast<int64_t>(rank) * w;
+    const double inv = nrm > 0 ? 1.0 / nrm : 0.0;
+#pragma unroll
+    for (int k = 0; k < RR; ++k)
+      if (k < w) row[k] = make_double2(col[k].x * inv, -col[k].y * inv);
+  }
+  for (int x = keep * w + lane; x < r * w; x += 32) G[x] = make_double2(0, 0);
+}
+
+// new_u = A V[:, :keep] = A conj(G)^T for the problems of a chunk: one CTA per (problem,
+// 128-row tile), each thread two rows by four ranks.
+__global__ void __launch_bounds__(256) k_recurse_av(RecArgs a, int tiles) {
+  extern __shared__ double2 sm2[];  // Vt[c][rho], w x R4
+  const int64_t idx = blockIdx.x / tiles;
+  const int tile = blockIdx.x % tiles;
+  const int64_t prob = a.p0 + idx;
+  const int b = a.b, r = a.r, w = b * a.r;
+  const int R4 = (r + 3) & ~3;
+  const int64_t pairs = a.pairs, part = a.rows / b;
+  const int64_t gb = prob / (b * pairs), t = (prob / pairs) % b, p = prob % pairs;
+  const double2* G = a.g + prob * static_cast<int64_t>(r) * w;
+  for (int x = threadIdx.x; x < R4 * w; x += blockDim.x) {
+    const int rho = x / w, c = x % w;
+    sm2[c * R4 + rho] = rho < r ? cconj(G[x]) : make_double2(0, 0);
+  }
+  __syncthreads();
+  const int rho0 = (threadIdx.x & 3) * 4;
+  const int64_t row0 = static_cast<int64_t>(tile) * 128 + (threadIdx.x >> 2) * 2;
+  if (rho0 >= r || row0 >= part) return;
+  const bool two = row0 + 1 < part;
+  const double2* a0 = a.cur + ((gb * a.rows + t * part + row0) * pairs + p) * w;
+  const double2* a1 = two ? a0 + pairs * w : a0;
+  double2 acc[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0, 0);
+#pragma unroll 4
+  for (int c = 0; c < w; ++c) {
+    const double2 x0 = a0[c], x1 = a1[c];
+    const double2* v = sm2 + c * R4 + rho0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double2 vj = v[j];
+      acc[0][j].x = fma(x0.x, vj.x, fma(-x0.y, vj.y, acc[0][j].x));
+      acc[0][j].y = fma(x0.x, vj.y, fma(x0.y, vj.x, acc[0][j].y));
+      acc[1][j].x = fma(x1.x, vj.x, fma(-x1.y, vj.y, acc[1][j].x));
+      acc[1][j].y = fma(x1.x, vj.y, fma(x1.y, vj.x, acc[1][j].y));
+    }
+  }
+  const int64_t out_base = ((gb * b + t) * part) * pairs + p;  // new_u.transpose(0,1,3,2,4): row (gb,t,row=0,p)
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    if (i == 1 && !two) break;
+    double2* o = a.nxt + (out_base + (row0 + i) * pairs) * r + rho0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (rho0 + j < r) o[j] = acc[i][j];
   }
 }
 
@@ -2040,8 +2375,13 @@ int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t ro
   const int64_t pairs = groups / branching;
   const int64_t part = rows / branching;
   const int64_t chunk = 2048;
-  const bool reg_tsqr = rows >= branching && S <= kSmemSet && w <= 32 && part > S;
-  const uint64_t scr_bytes = rows >= branching ? static_cast<uint64_t>(chunk) * rec_scratch_elems(part, w, S) * 16 : 0;
+  // stacks up to 32 wide: R by the register TSQR (stacks taller than 32 rows), warp-per-problem
+  // Jacobi on R^H, new_u = A V in its own kernel; BF_NO_WSVD=1 restores the CTA-per-problem SVD
+  static const bool wsvd_on = env_int_c("BF_NO_WSVD", 0) == 0;
+  const bool wsvd = wsvd_on && rows >= branching && w <= 32;
+  const bool reg_tsqr = rows >= branching && S <= kSmemSet && w <= 32 && part > (wsvd ? static_cast<int64_t>(w) : static_cast<int64_t>(S));
+  const uint64_t scr_bytes =
+      rows >= branching && !wsvd ? static_cast<uint64_t>(chunk) * rec_scratch_elems(part, w, S) * 16 : 0;
   const uint64_t need = scr_bytes + (reg_tsqr ? static_cast<uint64_t>(chunk) * w * w * 16 : 0);
   if (!workspace) {
     *ws_bytes = need;
@@ -2067,13 +2407,44 @@ int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t ro
     const size_t tsqr_smem = 8ull * (kTsqrCh + 1) * w * sizeof(double2);  // every warp streams its own chunk
     a.rbuf = reg_tsqr ? reinterpret_cast<double2*>(static_cast<char*>(workspace) + scr_bytes) : nullptr;
     if (reg_tsqr) BF_CUDA(allow_max_dyn_smem(k_recurse_tsqr));
+    if (reg_tsqr) BF_CUDA(allow_max_dyn_smem(k_recurse_tsqr2));
+    static const int tsqr_w_env = env_int_c("BF_TSQR_W", 0);
+    const int tsqr_w = (tsqr_w_env == 1 || tsqr_w_env == 2 || tsqr_w_env == 4 || tsqr_w_env == 8) ? tsqr_w_env : 0;
     const bool tall = part > S;
     void (*kern)(RecArgs) = tall ? k_recurse_split<true> : k_recurse_split<false>;
     BF_CUDA(allow_max_dyn_smem(kern));
+    const int av_tiles = static_cast<int>((part + 127) / 128);
+    const size_t av_smem = static_cast<size_t>((rank + 3) & ~3u) * w * sizeof(double2);
     for (int64_t p0 = 0; p0 < nprob; p0 += chunk) {
       a.p0 = p0;
       const int64_t cnt = std::min<int64_t>(chunk, nprob - p0);
-      if (reg_tsqr) k_recurse_tsqr<<<static_cast<unsigned>(cnt), 256, tsqr_smem, st>>>(a);
+      if (reg_tsqr && wsvd) {
+        // warps per problem: about four 8-row chunks each before the pairwise merge
+        const int64_t nch = (part + kTsqrRows - 1) / kTsqrRows;
+        // one warp per problem once the chunk fills the machine (8 warps per SM); fewer problems
+        // spread over W warps each (about four 8-row chunks per warp before the pairwise merge)
+        int W = nch >= 32 ? 8 : nch >= 16 ? 4 : nch >= 8 ? 2 : 1;
+        while (W > 1 && cnt * W > 2 * 148 * 8) W /= 2;
+        if (tsqr_w > 0) W = tsqr_w;
+        if (W == 1) {
+          static const int tsqr_ch = env_int_c("BF_TSQR_CH", 16);
+          const size_t tri = kTriElems * sizeof(double2);
+          if (tsqr_ch == 16) k_recurse_tsqr1<16><<<static_cast<unsigned>(cnt), 32, tri, st>>>(a);
+          else k_recurse_tsqr1<8><<<static_cast<unsigned>(cnt), 32, tri, st>>>(a);
+        } else {
+          const unsigned gt = static_cast<unsigned>((cnt * W + 7) / 8);
+          k_recurse_tsqr2<<<gt, 256, 8 * 33 * 32 * sizeof(double2), st>>>(a, cnt, W);
+        }
+      } else if (reg_tsqr) {
+        k_recurse_tsqr<<<static_cast<unsigned>(cnt), 256, tsqr_smem, st>>>(a);
+      }
+      if (wsvd) {
+        const unsigned g4 = static_cast<unsigned>((cnt + 3) / 4);
+        if (w <= 16) k_recurse_wsvd<16><<<g4, 128, 0, st>>>(a, cnt, reg_tsqr ? 1 : 0);
+        else k_recurse_wsvd<32><<<g4, 128, 0, st>>>(a, cnt, reg_tsqr ? 1 : 0);
+        k_recurse_av<<<static_cast<unsigned>(cnt * av_tiles), 256, av_smem, st>>>(a, av_tiles);
+        continue;
+      }
       kern<<<static_cast<unsigned>(cnt), tall ? 256 : 512, smem, st>>>(a);  // short stacks: 16 warps, one pass per Jacobi round
     }
   } else {

@@ -411,6 +411,86 @@ __device__ void warp_svd(const double2* src, int m, int n, int rs, int cs, doubl
   __syncwarp();
 }
 
+// One warp, columns only: one-sided Jacobi on the columns of a small matrix held one per
+// lane in registers (lane j: column j, RR rows, zero padded; cc active columns), with no
+// accumulated rotation matrix — the caller wants only the rotated columns W = M J (their
+// norms are the singular values, their directions the left singular vectors of M). Used
+// on M = R^H in the recursion, whose left singular vectors are the right singular vectors
+// of R. The pair's lower lane evaluates the three sums (fused multiply-adds, fixed order)
+// and hands them to the upper lane, so both lanes build the same rotation bit for bit.
+// A shuffle the compiler may not merge with an earlier identical one (the rotation pass
+// re-fetches the partner column rather than keeping 2 RR more registers live).
+__device__ __forceinline__ double shfl_again(double v, int src) {
+  int lo = __double2loint(v), hi = __double2hiint(v);
+  asm volatile("shfl.sync.idx.b32 %0, %0, %2, 31, 0xffffffff;\n\tshfl.sync.idx.b32 %1, %1, %2, 31, 0xffffffff;"
+               : "+r"(lo), "+r"(hi)
+               : "r"(src));
+  return __hiloint2double(hi, lo);
+}
+
+template <int RR>
+__device__ __forceinline__ void warp_jacobi_reg(double2 (&a)[RR], int cc) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int nn = cc + (cc & 1);
+  const double tol = (RR > 8 ? RR : 8) * 2.220446049250313e-16;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    bool rotated = false;
+    for (int round = 0; round < nn - 1; ++round) {
+      const int pj = rr_partner(lane, round, nn);
+      const bool valid = lane < cc && pj < cc && pj != lane;
+      const bool low = lane < pj;
+      int pjv = pj;
+      double no = 0, np = 0;
+      double2 d = make_double2(0, 0);
+#pragma unroll
+      for (int k = 0; k < RR; ++k) {
+        // every fourth fetch waits for the sums so far: keeps the partner column from
+        // being fetched (and held in registers) whole
+        if (k && k % 4 == 0) asm volatile("" : "+r"(pjv) : "d"(d.x), "d"(np));
+        double2 pk;
+        pk.x = __shfl_sync(full, a[k].x, pjv);
+        pk.y = __shfl_sync(full, a[k].y, pjv);
+        no = fma(a[k].x, a[k].x, fma(a[k].y, a[k].y, no));
+        np = fma(pk.x, pk.x, fma(pk.y, pk.y, np));
+        d.x = fma(a[k].x, pk.x, fma(a[k].y, pk.y, d.x));   // conj(own) * partner
+        d.y = fma(a[k].x, pk.y, fma(-a[k].y, pk.x, d.y));
+      }
+      const int from = low ? lane : pj;  // the pair's lower lane: own = x, partner = y
+      const double al = __shfl_sync(full, no, from), be = __shfl_sync(full, np, from);
+      double2 g;
+      g.x = __shfl_sync(full, d.x, from);
+      g.y = __shfl_sync(full, d.y, from);
+      const double g2 = g.x * g.x + g.y * g.y;
+      const bool rot = valid && !(g2 == 0.0 || g2 <= tol * tol * al * be);
+      if (!__any_sync(full, rot)) continue;
+      rotated = rotated || rot;
+      // [x', y'] = [x, y] [[c, s], [-s e^{-i phi}, c e^{-i phi}]]: own' = ca own + cb partner
+      double2 ca = make_double2(1, 0), cb = make_double2(0, 0);
+      if (rot) {
+        const double ig = rsqrt(g2);
+        const double zeta = (be - al) * 0.5 * ig;
+        const double az = fabs(zeta), sgn = zeta >= 0 ? 1.0 : -1.0;
+        const double t = az > 1e150 ? sgn * 0.5 / az : sgn / (az + sqrt(1.0 + zeta * zeta));
+        const double c = rsqrt(1.0 + t * t), s_ = c * t;
+        const double2 ph = make_double2(g.x * ig, -g.y * ig);  // e^{-i phi}
+        ca = low ? make_double2(c, 0) : make_double2(c * ph.x, c * ph.y);
+        cb = low ? make_double2(-s_ * ph.x, -s_ * ph.y) : make_double2(s_, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < RR; ++k) {
+        if (k && k % 4 == 0) asm volatile("" : "+r"(pjv) : "d"(a[k - 1].x), "d"(a[k - 1].y));
+        double2 pk;
+        pk.x = shfl_again(a[k].x, pjv);
+        pk.y = shfl_again(a[k].y, pjv);
+        const double2 u = cmul(ca, a[k]), w = cmul(cb, pk);
+        a[k] = make_double2(u.x + w.x, u.y + w.y);
+      }
+    }
+    if (!__any_sync(full, rotated)) break;
+  }
+}
+
 // floored_inverse (lowrank.py:79-87): 1/sigma where sigma > PINV_FLOOR * max, else 0.
 __device__ __forceinline__ double floored_inv(double s, double smax) {
   return s > kPinvFloor * smax ? 1.0 / s : 0.0;
