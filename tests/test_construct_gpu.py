@@ -392,3 +392,52 @@ np.savez(sys.argv[1], u=u.cpu().numpy(), v=v.cpu().numpy(), w=w.cpu().numpy())
         res[tag] = np.load(path)
     for key in ("u", "v", "w"):
         assert np.array_equal(res["cluster"][key], res["single"][key]), key
+
+
+@pytest.mark.parametrize("r,nb,rows,groups", [(16, 8, 128, 256), (12, 4, 160, 320), (5, 8, 96, 256), (16, 1, 4096, 16),
+                                               (8, 2, 32, 64), (16, 2, 16, 64)])
+def test_recurse_level_warp_paths(r, nb, rows, groups):
+    """One bf_recurse_level call per geometry of the stacks-up-to-32-wide path
+    (construct.py:127-163): enough problems for the one-warp TSQR (k_recurse_tsqr1), few tall
+    ones for the W-warp form (k_recurse_tsqr2), short stacks straight into the warp Jacobi.
+    Every stack's new_u G must equal numpy's rank-r truncated SVD of the stack, G's rows
+    orthonormal, and new_u's columns orthogonal with descending norms."""
+    import ctypes
+    from paper_1502_01379_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(100 * r + rows)
+    cur = complex_gaussian(rng, (nb, rows, groups, r))
+    cur *= (0.3 ** np.arange(r))[None, None, None, :]       # graded columns, like u0 * sigma0
+    pairs, part, w = groups // 2, rows // 2, 2 * r
+    keep = min(r, part)
+    cur_d = torch.from_numpy(cur).cuda()
+    blocks = torch.full((nb, 2, pairs, r, w), float("nan"), dtype=torch.complex128, device="cuda")
+    nxt = torch.full((2 * nb, part, pairs, r), float("nan"), dtype=torch.complex128, device="cuda")
+    need = ctypes.c_uint64(0)
+    _lib.check(lib.bf_recurse_level(r, 2, nb, rows, groups, None, None, None, None, ctypes.byref(need), None))
+    ws = torch.empty(max(int(need.value), 16), dtype=torch.uint8, device="cuda")
+    _lib.check(lib.bf_recurse_level(r, 2, nb, rows, groups, ctypes.c_void_p(cur_d.data_ptr()),
+                                    ctypes.c_void_p(blocks.data_ptr()), ctypes.c_void_p(nxt.data_ptr()),
+                                    ctypes.c_void_p(ws.data_ptr()), ctypes.byref(need), None))
+    torch.cuda.synchronize()
+    g = blocks.cpu().numpy()
+    nu = nxt.cpu().numpy().reshape(nb, 2, part, pairs, r)
+    assert not np.isnan(g.view(np.float64)).any() and not np.isnan(nu.view(np.float64)).any()
+    paired = cur.reshape(nb, rows, pairs, w)
+    worst = 0.0
+    for b_ in range(nb):
+        for t in range(2):
+            stack = paired[b_, t * part:(t + 1) * part].transpose(1, 0, 2)      # (pairs, part, w)
+            uu, ss, vh = np.linalg.svd(stack, full_matrices=False)
+            want = (uu[..., :keep] * ss[:, None, :keep]) @ vh[:, :keep]
+            got_u = nu[b_, t].transpose(1, 0, 2)                                # (pairs, part, r)
+            got = got_u @ g[b_, t]
+            scale = np.linalg.norm(stack, axis=(1, 2))
+            worst = max(worst, float((np.linalg.norm(got - want, axis=(1, 2)) / scale).max()))
+            gram = g[b_, t][:, :keep] @ g[b_, t][:, :keep].conj().swapaxes(-1, -2)
+            assert np.abs(gram - np.eye(keep)).max() <= 1e-12
+            assert not np.any(g[b_, t][:, keep:] != 0) and not np.any(got_u[..., keep:] != 0)
+            norms = np.linalg.norm(got_u[..., :keep], axis=1)
+            assert np.abs(norms - ss[:, :keep]).max() <= 1e-12 * ss[:, :1].max()
+    print("recurse level r=%d rows=%d: worst truncated-SVD deviation %.2e" % (r, rows, worst))
+    assert worst <= 1e-12
