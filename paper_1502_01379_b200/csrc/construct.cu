@@ -1189,6 +1189,86 @@ __global__ void k_assemble(MidArgs a) {
   }
 }
 
+// k_assemble with one thread per row of the block: the basis columns are read coalesced
+// (consecutive threads, consecutive rows of a column), the middle factors U_M, V_M sit in
+// shared memory (broadcast reads) and each thread keeps its row's R outputs in registers.
+// Same sums in the same order as k_assemble. Grid (blocks, ceil(side / 256)).
+template <int R>
+__global__ void __launch_bounds__(256, R <= 16 ? 2 : 1) k_assemble_rows(MidArgs a) {
+  extern __shared__ double2 sm2[];
+  const BlockState& s = a.st[blockIdx.x];
+  const int side = static_cast<int>(a.side), S = a.S;
+  const int r = a.r, t = s.t;
+  const bool dense = s.tc < 0;
+  const int tc = dense ? 0 : s.tc, tr = dense ? 0 : s.tr;
+  const int64_t SS = static_cast<int64_t>(S) * S;
+  const double2* scr = a.scr + static_cast<int64_t>(blockIdx.x) * 9 * SS;
+  const double2* UM = scr + 4 * SS;
+  const double2* VM = scr + 5 * SS;
+  const double* sig = a.sig + static_cast<int64_t>(blockIdx.x) * S;
+  double2* Us = sm2;
+  double2* Vs = sm2 + static_cast<int64_t>(tc) * R;
+  for (int x = threadIdx.x; x < tc * R; x += blockDim.x) {
+    const int l = x / R, rho = x % R;
+    Us[x] = rho < t ? UM[l * S + rho] : make_double2(0, 0);
+  }
+  for (int x = threadIdx.x; x < tr * R; x += blockDim.x) {
+    const int l = x / R, rho = x % R;
+    Vs[x] = rho < t ? VM[l * S + rho] : make_double2(0, 0);
+  }
+  __syncthreads();
+  if (blockIdx.y == 0 && threadIdx.x < r) {
+    double smax = 0;
+    for (int k = 0; k < t; ++k) smax = fmax(smax, sig[k]);
+    const int rho = threadIdx.x;
+    a.w_out[static_cast<int64_t>(blockIdx.x) * r + rho] = rho < t ? floored_inv(sig[rho], smax) : 0.0;
+  }
+  const int i = blockIdx.y * blockDim.x + threadIdx.x;
+  if (i >= side) return;
+#pragma unroll 1
+  for (int which = 0; which < 2; ++which) {
+    const double2* Q = (which == 0 ? a.qc : a.qr) + static_cast<int64_t>(blockIdx.x) * S * a.side + i;
+    const double2* Ms = which == 0 ? Us : Vs;
+    const double2* Md = which == 0 ? UM : VM;
+    const int tl = which == 0 ? tc : tr;
+    double2 acc[R];
+#pragma unroll
+    for (int rho = 0; rho < R; ++rho) acc[rho] = make_double2(0, 0);
+    if (dense) {
+#pragma unroll
+      for (int rho = 0; rho < R; ++rho)
+        if (rho < t) acc[rho] = Md[i * S + rho];
+    } else {
+      // eight basis values in flight per thread (the loop is bound by load latency otherwise)
+      constexpr int kAhead = R <= 16 ? 8 : 4;
+      for (int l0 = 0; l0 < tl; l0 += kAhead) {
+        double2 q[kAhead];
+#pragma unroll
+        for (int j = 0; j < kAhead; ++j)
+          q[j] = l0 + j < tl ? __ldcs(Q + static_cast<int64_t>(l0 + j) * side) : make_double2(0, 0);
+#pragma unroll
+        for (int j = 0; j < kAhead; ++j) {
+          if (l0 + j >= tl) break;
+          const double2* m = Ms + (l0 + j) * R;
+#pragma unroll
+          for (int rho = 0; rho < R; ++rho) {
+            const double2 g = cmul(q[j], m[rho]);
+            acc[rho].x += g.x;
+            acc[rho].y += g.y;
+          }
+        }
+      }
+    }
+    double2* o = (which == 0 ? a.u_out : a.v_out) + (static_cast<int64_t>(blockIdx.x) * a.side + i) * r;
+#pragma unroll
+    for (int rho = 0; rho < R; ++rho)
+      if (rho < r) {
+        const double sg = rho < t ? sig[rho] : 0.0;
+        o[rho] = rho < t ? make_double2(acc[rho].x * sg, acc[rho].y * sg) : make_double2(0, 0);
+      }
+  }
+}
+
 // ---------------------------------------------------------------- matvec mode
 // Probe product slices of block (i, j) into the tall buffer (side x width,
 // column-major): kCols y_col = k_cols[i side + row, j w + c], kRows y_row =
@@ -2124,6 +2204,29 @@ int env_int_c(const char* name, int dflt) {
   return e && *e ? atoi(e) : dflt;
 }
 
+// _assemble: one thread per block row with the middle factors in shared memory (ranks up
+// to 32); BF_ASSEMBLE_OLD=1 or a larger rank keeps the thread-per-output kernel.
+cudaError_t launch_assemble(const MidArgs& a, unsigned nblocks, cudaStream_t st) {
+  static const bool old = env_int_c("BF_ASSEMBLE_OLD", 0) != 0;
+  const int T = 256;
+  if (old || a.r > 32) {
+    const unsigned yas = static_cast<unsigned>(std::min<uint64_t>(32, (a.side * a.r + T - 1) / T));
+    k_assemble<<<dim3(nblocks, yas), T, 0, st>>>(a);
+    return cudaGetLastError();
+  }
+  const int R = a.r <= 4 ? 4 : a.r <= 8 ? 8 : a.r <= 16 ? 16 : 32;
+  const size_t smem = 2ull * a.S * R * sizeof(double2);
+  const dim3 grid(nblocks, static_cast<unsigned>((a.side + T - 1) / T));
+  cudaError_t e = cudaSuccess;
+  switch (R) {
+    case 4: e = allow_max_dyn_smem(k_assemble_rows<4>); k_assemble_rows<4><<<grid, T, smem, st>>>(a); break;
+    case 8: e = allow_max_dyn_smem(k_assemble_rows<8>); k_assemble_rows<8><<<grid, T, smem, st>>>(a); break;
+    case 16: e = allow_max_dyn_smem(k_assemble_rows<16>); k_assemble_rows<16><<<grid, T, smem, st>>>(a); break;
+    default: e = allow_max_dyn_smem(k_assemble_rows<32>); k_assemble_rows<32><<<grid, T, smem, st>>>(a); break;
+  }
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 // Greedy sweep pivots: the cluster kernel (k_pivot_wide_cl) for samples of >= 1024
 // columns, one CTA per SM (shared-memory request above half the SM) so that only
 // 148/CL blocks' samples are live in L2; BF_NO_PIVOT_CLUSTER=1 keeps one CTA per block.
@@ -2283,8 +2386,7 @@ static int middle_blocks(int kernel_id, uint64_t n, uint32_t levels, uint32_t br
     }
     k_mid<<<nblocks, 768, small_smem, st>>>(a);  // 24 warps: a 48-column Jacobi round in one pass
   }
-  const unsigned yas = static_cast<unsigned>(std::min<uint64_t>(32, (side * rank + T - 1) / T));
-  k_assemble<<<dim3(nblocks, yas), T, 0, st>>>(a);
+  BF_CUDA(launch_assemble(a, nblocks, st));
   BF_CUDA(cudaGetLastError());
   return BF_OK;
 }
@@ -2353,8 +2455,7 @@ int bf_middle_probes(uint64_t n, uint32_t levels, uint32_t branching, uint32_t r
   k_set_probe_counts<<<(nblocks + 127) / 128, 128, 0, st>>>(a);
   for (int which : {kCols, kRows}) launch_basis(a, nblocks, which, st);
   k_mid_probe<<<nblocks, T, small_smem, st>>>(a);
-  const unsigned yas = static_cast<unsigned>(std::min<uint64_t>(32, (side * rank + T - 1) / T));
-  k_assemble<<<dim3(nblocks, yas), T, 0, st>>>(a);
+  BF_CUDA(launch_assemble(a, nblocks, st));
   BF_CUDA(cudaGetLastError());
   return BF_OK;
 }
