@@ -454,10 +454,13 @@ def _place(chain, leaf, k0, cnt, leaf_k, pieces):
 
 
 def recursion_batch(m: int, side: int, r: int) -> int:
-    """Slabs per recursion launch: >= 2048 first-level problems (the level kernels
-    are latency-bound per problem, so the GPU needs many in flight), <= 4 GiB of slabs."""
+    """Slabs per recursion launch: >= BF_RECURSION_PROBLEMS (default 2048) first-level
+    problems (the level kernels are latency-bound per problem, so the GPU needs many in
+    flight — and several machine-fills of them, so that the last partial fill is a small
+    share), <= 4 GiB of slabs."""
+    target = max(1, int(os.environ.get("BF_RECURSION_PROBLEMS", "2048")))
     slab_bytes = 16 * side * m * r
-    return max(1, min(m, -(-2048 // m), (4 << 30) // max(1, slab_bytes)))
+    return max(1, min(m, -(-target // m), (4 << 30) // max(1, slab_bytes)))
 
 
 def factorize(oracle, p: DyadicPartition, r: int, params=DEFAULT_PARAMS, seed=0,

@@ -1998,8 +1998,8 @@ __global__ void __launch_bounds__(TALL ? 256 : 512, 2) k_recurse_split(RecArgs a
 // vectors of the stack directly; no rotation matrix is accumulated and nothing lives in
 // shared memory, so 12 problems share an SM. Writes the transfer block G = vh[:keep]
 // (zero-padded rows); new_u = A conj(G)^T follows in k_recurse_av.
-template <int RR>
-__global__ void __launch_bounds__(128, RR > 16 ? 3 : 4) k_recurse_wsvd(RecArgs a, int64_t cnt, int from_r) {
+template <int RR, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_recurse_wsvd(RecArgs a, int64_t cnt, int from_r) {
   const int lane = threadIdx.x & 31;
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * 4 + (threadIdx.x >> 5);
   if (idx >= cnt) return;
@@ -2014,7 +2014,7 @@ __global__ void __launch_bounds__(128, RR > 16 ? 3 : 4) k_recurse_wsvd(RecArgs a
   double2 col[RR];
 #pragma unroll
   for (int k = 0; k < RR; ++k) col[k] = (lane < cc && k < w) ? cconj(rowp[k]) : make_double2(0, 0);
-  warp_jacobi_reg<RR>(col, cc);
+  warp_jacobi_reg<RR>(col, cc, static_cast<int>(blockIdx.z));
   double nrm = 0;
 #pragma unroll
   for (int k = 0; k < RR; ++k) nrm += col[k].x * col[k].x + col[k].y * col[k].y;
@@ -2475,11 +2475,16 @@ int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t ro
   const int S = w <= static_cast<uint32_t>(kSmemSet) ? kSmemSet : kSetCap;
   const int64_t pairs = groups / branching;
   const int64_t part = rows / branching;
-  const int64_t chunk = 2048;
   // stacks up to 32 wide: R by the register TSQR (stacks taller than 32 rows), warp-per-problem
   // Jacobi on R^H, new_u = A V in its own kernel; BF_NO_WSVD=1 restores the CTA-per-problem SVD
   static const bool wsvd_on = env_int_c("BF_NO_WSVD", 0) == 0;
   const bool wsvd = wsvd_on && rows >= branching && w <= 32;
+  // problems per launch: the warp-per-problem kernels keep no per-problem scratch besides R,
+  // so one launch takes up to 8,192 (the block scheduler back-fills finished warps; 2,048
+  // problems are only 1.2 machine-fills of 12 warps per SM)
+  static const int64_t chunk_env = env_int_c("BF_RECURSE_CHUNK", 0);
+  const int64_t nprob_all = static_cast<int64_t>(nb) * (rows >= branching ? branching : 1) * pairs;
+  const int64_t chunk = std::min<int64_t>(chunk_env > 0 ? chunk_env : (wsvd ? 8192 : 2048), std::max<int64_t>(nprob_all, 1));
   const bool reg_tsqr = rows >= branching && S <= kSmemSet && w <= 32 && part > (wsvd ? static_cast<int64_t>(w) : static_cast<int64_t>(S));
   const uint64_t scr_bytes =
       rows >= branching && !wsvd ? static_cast<uint64_t>(chunk) * rec_scratch_elems(part, w, S) * 16 : 0;
@@ -2541,8 +2546,12 @@ int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t ro
       }
       if (wsvd) {
         const unsigned g4 = static_cast<unsigned>((cnt + 3) / 4);
-        if (w <= 16) k_recurse_wsvd<16><<<g4, 128, 0, st>>>(a, cnt, reg_tsqr ? 1 : 0);
-        else k_recurse_wsvd<32><<<g4, 128, 0, st>>>(a, cnt, reg_tsqr ? 1 : 0);
+        // 32-row columns: 255 registers and no spills at 8 warps per SM, or 168 registers with
+        // the column partly in local memory at 12 (BF_WSVD_OCC=3)
+        static const int occ = env_int_c("BF_WSVD_OCC", 2);
+        if (w <= 16) k_recurse_wsvd<16, 4><<<g4, 128, 0, st>>>(a, cnt, reg_tsqr ? 1 : 0);
+        else if (occ == 3) k_recurse_wsvd<32, 3><<<g4, 128, 0, st>>>(a, cnt, reg_tsqr ? 1 : 0);
+        else k_recurse_wsvd<32, 2><<<g4, 128, 0, st>>>(a, cnt, reg_tsqr ? 1 : 0);
         k_recurse_av<<<static_cast<unsigned>(cnt * av_tiles), 256, av_smem, st>>>(a, av_tiles);
         continue;
       }

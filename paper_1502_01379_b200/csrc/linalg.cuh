@@ -418,6 +418,10 @@ __device__ void warp_svd(const double2* src, int m, int n, int rs, int cs, doubl
 // on M = R^H in the recursion, whose left singular vectors are the right singular vectors
 // of R. The pair's lower lane evaluates the three sums (fused multiply-adds, fixed order)
 // and hands them to the upper lane, so both lanes build the same rotation bit for bit.
+// `zero` must be 0 at run time without the compiler knowing it (blockIdx.z of a launch
+// with gridDim.z = 1): every fourth partner fetch is made to depend on the arithmetic
+// before it through `& zero`, which keeps ptxas from hoisting all 2 RR fetches of a pass
+// ahead of the arithmetic and spilling the column.
 // A shuffle the compiler may not merge with an earlier identical one (the rotation pass
 // re-fetches the partner column rather than keeping 2 RR more registers live).
 __device__ __forceinline__ double shfl_again(double v, int src) {
@@ -429,7 +433,7 @@ __device__ __forceinline__ double shfl_again(double v, int src) {
 }
 
 template <int RR>
-__device__ __forceinline__ void warp_jacobi_reg(double2 (&a)[RR], int cc) {
+__device__ __forceinline__ void warp_jacobi_reg(double2 (&a)[RR], int cc, int zero) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int nn = cc + (cc & 1);
@@ -441,21 +445,33 @@ __device__ __forceinline__ void warp_jacobi_reg(double2 (&a)[RR], int cc) {
       const bool valid = lane < cc && pj < cc && pj != lane;
       const bool low = lane < pj;
       int pjv = pj;
-      double no = 0, np = 0;
-      double2 d = make_double2(0, 0);
+      // two accumulators per sum (even / odd rows): the dependent-DFMA chains are the pass's
+      // critical path
+      double no = 0, np = 0, no1 = 0, np1 = 0;
+      double2 d = make_double2(0, 0), d1 = make_double2(0, 0);
 #pragma unroll
-      for (int k = 0; k < RR; ++k) {
+      for (int k = 0; k < RR; k += 2) {
         // every fourth fetch waits for the sums so far: keeps the partner column from
         // being fetched (and held in registers) whole
-        if (k && k % 4 == 0) asm volatile("" : "+r"(pjv) : "d"(d.x), "d"(np));
-        double2 pk;
+        if (k && k % 4 == 0) pjv = pj + ((__double2hiint(d.x) ^ __double2hiint(np1)) & zero);
+        double2 pk, pk1;
         pk.x = __shfl_sync(full, a[k].x, pjv);
         pk.y = __shfl_sync(full, a[k].y, pjv);
+        pk1.x = __shfl_sync(full, a[k + 1].x, pjv);
+        pk1.y = __shfl_sync(full, a[k + 1].y, pjv);
         no = fma(a[k].x, a[k].x, fma(a[k].y, a[k].y, no));
         np = fma(pk.x, pk.x, fma(pk.y, pk.y, np));
         d.x = fma(a[k].x, pk.x, fma(a[k].y, pk.y, d.x));   // conj(own) * partner
         d.y = fma(a[k].x, pk.y, fma(-a[k].y, pk.x, d.y));
+        no1 = fma(a[k + 1].x, a[k + 1].x, fma(a[k + 1].y, a[k + 1].y, no1));
+        np1 = fma(pk1.x, pk1.x, fma(pk1.y, pk1.y, np1));
+        d1.x = fma(a[k + 1].x, pk1.x, fma(a[k + 1].y, pk1.y, d1.x));
+        d1.y = fma(a[k + 1].x, pk1.y, fma(-a[k + 1].y, pk1.x, d1.y));
       }
+      no += no1;
+      np += np1;
+      d.x += d1.x;
+      d.y += d1.y;
       const int from = low ? lane : pj;  // the pair's lower lane: own = x, partner = y
       const double al = __shfl_sync(full, no, from), be = __shfl_sync(full, np, from);
       double2 g;
@@ -479,7 +495,7 @@ __device__ __forceinline__ void warp_jacobi_reg(double2 (&a)[RR], int cc) {
       }
 #pragma unroll
       for (int k = 0; k < RR; ++k) {
-        if (k && k % 4 == 0) asm volatile("" : "+r"(pjv) : "d"(a[k - 1].x), "d"(a[k - 1].y));
+        if (k && k % 4 == 0) pjv = pj + ((__double2hiint(a[k - 1].x) ^ __double2hiint(a[k - 1].y)) & zero);
         double2 pk;
         pk.x = shfl_again(a[k].x, pjv);
         pk.y = shfl_again(a[k].y, pjv);
