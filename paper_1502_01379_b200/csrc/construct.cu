@@ -748,8 +748,8 @@ __global__ void k_cgs2(MidArgs a, int which) {
 // column is read 4 times per panel.
 constexpr int kPanelMax = 8;
 
-__global__ void __launch_bounds__(1024) k_bcgs2(MidArgs a, int which, int pw) {
-  extern __shared__ double2 pan[];  // pw columns of length side
+__global__ void __launch_bounds__(1024) k_bcgs2(MidArgs a, int which, int pw, int nseg) {
+  extern __shared__ double2 pan[];  // pw columns of length side, then S * nseg * pw partial coefficients
   __shared__ double2 coef[kSetCap][kPanelMax];
   __shared__ double red[2 * 32];
   const BlockState& s = a.st[blockIdx.x];
@@ -763,14 +763,20 @@ __global__ void __launch_bounds__(1024) k_bcgs2(MidArgs a, int which, int pw) {
     __syncthreads();
     for (int pass = 0; pass < 2; ++pass) {
       if (j0 > 0) {
-        // C = Q[:, :j0]^H pan, one warp per previous column
-        for (int l = warp; l < j0; l += nw) {
+        // C = Q[:, :j0]^H pan: one warp per (previous column, row segment) unit — with whole
+        // columns per warp only j0 of the 32 warps work (and 33..45 columns leave a second,
+        // mostly empty round); the segments' partial sums are added in segment order
+        double2* cpart = pan + static_cast<int64_t>(pw) * side;
+        const int seglen = (((side + nseg - 1) / nseg) + 31) & ~31;
+        for (int u = warp; u < j0 * nseg; u += nw) {
+          const int l = u % j0, sg = u / j0;
           const double2* ql = Q + static_cast<int64_t>(l) * side;
+          const int i1 = min(side, (sg + 1) * seglen);
           double2 acc[kPanelMax];
 #pragma unroll
           for (int b = 0; b < kPanelMax; ++b) acc[b] = make_double2(0, 0);
 #pragma unroll 4
-          for (int i = lane; i < side; i += 32) {
+          for (int i = sg * seglen + lane; i < i1; i += 32) {
             const double2 q = ql[i];
 #pragma unroll
             for (int b = 0; b < kPanelMax; ++b)
@@ -784,10 +790,26 @@ __global__ void __launch_bounds__(1024) k_bcgs2(MidArgs a, int which, int pw) {
           for (int b = 0; b < kPanelMax; ++b)
             if (b < nb) {
               const double2 v = warp_sum2(acc[b]);
-              if (lane == 0) coef[l][b] = v;
+              if (lane == 0) {
+                if (nseg == 1) coef[l][b] = v;
+                else cpart[(l * nseg + sg) * pw + b] = v;
+              }
             }
         }
         __syncthreads();
+        if (nseg > 1) {
+          for (int x = threadIdx.x; x < j0 * nb; x += blockDim.x) {
+            const int l = x / nb, b = x % nb;
+            double2 v = cpart[(l * nseg) * pw + b];
+            for (int sg = 1; sg < nseg; ++sg) {
+              const double2 w2 = cpart[(l * nseg + sg) * pw + b];
+              v.x += w2.x;
+              v.y += w2.y;
+            }
+            coef[l][b] = v;
+          }
+          __syncthreads();
+        }
         // pan -= Q[:, :j0] C, one thread per row
         for (int i = threadIdx.x; i < side; i += blockDim.x) {
           double2 v[kPanelMax];
@@ -2178,7 +2200,15 @@ void launch_basis(const MidArgs& a, uint32_t nblocks, int which, cudaStream_t st
   if (getenv("BF_CGS2")) pw = 0;
   if (pw >= 2) {
     allow_max_dyn_smem(k_bcgs2);
-    k_bcgs2<<<nblocks, 1024, static_cast<size_t>(pw) * col_bytes, st>>>(a, which, pw);
+    // coefficient sweeps split into row segments while the partial sums fit next to the panel
+    static const int seg_env = env_int_c("BF_BCGS2_SEG", 4);
+    int nseg = std::max(1, std::min(8, seg_env));
+    size_t smem = static_cast<size_t>(pw) * col_bytes + static_cast<size_t>(a.S) * nseg * pw * sizeof(double2);
+    if (nseg == 1 || smem > 207 * 1024) {
+      nseg = 1;
+      smem = static_cast<size_t>(pw) * col_bytes;
+    }
+    k_bcgs2<<<nblocks, 1024, smem, st>>>(a, which, pw, nseg);
   } else {
     k_cgs2<<<nblocks, 512, 0, st>>>(a, which);
   }
