@@ -2518,7 +2518,8 @@ int bf_recurse_level(uint32_t rank, uint32_t branching, uint64_t nb, uint64_t ro
   const bool reg_tsqr = rows >= branching && S <= kSmemSet && w <= 32 && part > (wsvd ? static_cast<int64_t>(w) : static_cast<int64_t>(S));
   const uint64_t scr_bytes =
       rows >= branching && !wsvd ? static_cast<uint64_t>(chunk) * rec_scratch_elems(part, w, S) * 16 : 0;
-  const uint64_t need = scr_bytes + (reg_tsqr ? static_cast<uint64_t>(chunk) * w * w * 16 : 0);
+  // never 0: a NULL workspace is the size query, so a caller must always have a buffer to pass
+  const uint64_t need = std::max<uint64_t>(16, scr_bytes + (reg_tsqr ? static_cast<uint64_t>(chunk) * w * w * 16 : 0));
   if (!workspace) {
     *ws_bytes = need;
     return BF_OK;
